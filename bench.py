@@ -1,0 +1,358 @@
+"""Benchmark: simulated 1-ms steps per second of the spiking hot loop.
+
+Default (N=1): BASELINE config 2 -- 1M LIF neurons x ~1k synapses (random, C=1,
+device-generated with the generate_synthetic distributions), single B200,
+update + delivery kernels, 1000 timed steps.  N>1 (torchrun): weak scaling,
+1M neurons per GPU, block partition, direct spike exchange.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints one JSON line (rank 0).  See DESIGN.md section 6 for every field.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "simulated steps/sec at 1/2/4/8 B200; p50/p99 spike-exchange µs/step"
+UNIT = "steps/s"
+
+
+def load_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.is_file():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "source": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, f[3:7]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# --------------------------------------------------------------------------- ours
+
+def run_ours(args) -> dict | None:
+    import torch
+    import torch.distributed as dist
+
+    from paper_2205_07125_b200 import sim as S
+    from paper_2205_07125_b200 import _native
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n_neurons = args.neurons * world
+    spec = S.GeneratorSpec.random(n_neurons, args.degree, seed=args.seed)
+    lay = S.ShardLayout.blocks(n_neurons, world)
+    t_build = time.time()
+    net = S.Network.generate(spec, lay, device=dev, shards=[rank])
+    torch.cuda.synchronize()
+    t_build = time.time() - t_build
+    lif = S.LifParams()
+    if world > 1:
+        from paper_2205_07125_b200 import distributed as D
+        sim = D.DistSimulator(net, lif, args.seed, None, transport=args.transport, delivery=args.delivery)
+    else:
+        sim = S.Simulator(net, lif, args.seed, None, delivery=args.delivery, graph_chunk=args.chunk)
+    sim.reset(1)
+    sim.advance(args.warmup)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    spikes0 = sum(int(s.spike_total.item()) for s in sim.states)
+    with ClockSampler(local) as clocks:
+        e0.record()
+        sim.advance(args.steps)
+        e1.record()
+        torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    spikes = sum(int(s.spike_total.item()) for s in sim.states) - spikes0
+    sim.check_status()
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        sp = torch.tensor([spikes], device=dev, dtype=torch.int64)
+        dist.all_reduce(sp)
+        spikes = int(sp.item())
+    value = args.steps / (ms * 1e-3)
+
+    # ---- dominant kernel, timed alone on its stream (CUDA events) ----
+    st = sim.states[0]
+    L = _native.lib()
+    stream = torch.cuda.current_stream()
+    k0 = torch.cuda.Event(enable_timing=True)
+    k1 = torch.cuda.Event(enable_timing=True)
+    reps = 50
+    import ctypes as C
+    k0.record(stream)
+    for _ in range(reps):
+        if args.delivery == "fused":
+            L.nc_sim_step_fused(C.byref(st.c), C.byref(sim.c_lif), stream.cuda_stream)
+        else:
+            L.nc_sim_deliver_push(C.byref(st.c), sim.c_lif.g_inh, stream.cuda_stream)
+    k1.record(stream)
+    torch.cuda.synchronize()
+    kernel_ms = k0.elapsed_time(k1) / reps
+    n_local = lay.n_local(rank)
+    csr = net.shards[rank]
+    syn_bytes = csr.n_synapses_padded * 4
+    neuron_bytes = n_local * (8 + 4 + 4 + 4 + 4 + 1 + 1 + 4) + lay.n_words * 4 + n_local // 8
+    alg_bytes = syn_bytes + neuron_bytes
+    peaks = load_peaks()
+    achieved = alg_bytes / (kernel_ms * 1e-3) / 1e9
+    traffic = None
+    prof = ROOT / "profiles" / "ncu_step_fused.json"
+    if prof.is_file():
+        traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+
+    result = None
+    if rank == 0:
+        cpu = cpu_baseline(net, lay, lif, args) if (world == 1 and not args.no_cpu) else None
+        e2e = e2e_measure(sim, net, args) if world == 1 else None
+        result = {
+            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 5), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "fp32 state / int32 synaptic sums",
+            "data": "synthetic (device SBM generator, generate_synthetic distributions)",
+            "config": {
+                "workload": ("config 2: 1M LIF neurons x 1k synapses, single B200, update + delivery kernels"
+                             if world == 1 else
+                             f"weak scaling: {args.neurons} neurons/GPU x {args.degree} synapses, block partition, "
+                             f"direct exchange ({args.transport})"),
+                "neurons": n_neurons, "mean_degree": args.degree, "synapses": int(net.n_synapses) * world,
+                "delivery": args.delivery, "exchange": "none" if world == 1 else "direct",
+                "firing_rate_hz": round(spikes / n_neurons / (args.steps * 1e-3), 3),
+                "l2": "inputs larger than L2 (CSR %.2f GB streamed every step)" % (syn_bytes / 1e9),
+                "graph_build_s": round(t_build, 2),
+            },
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": traffic,
+                         "kernel": "k_step_fused" if args.delivery == "fused" else "k_deliver_push",
+                         "kernel_ms": round(kernel_ms, 5), "algorithmic_bytes": int(alg_bytes),
+                         "peak_source": peaks["source"]},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps * sim.launches_per_step(),
+            "clocks": clocks.summary(),
+        }
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return result
+
+
+def gid_csr(net, lay, rank=0):
+    """Gid-space CSR of a single-shard network for the CPU oracle (unpacked on the GPU)."""
+    import torch
+    csr = net.shards[rank]
+    rp4 = csr.rowptr4
+    syn = csr.syn[: int(rp4[-1].item()) * 4].to(torch.int64) & 0xFFFFFFFF
+    keep = syn != lay.pad_entry
+    lens = torch.zeros(rp4.numel() - 1, dtype=torch.int64, device=syn.device)
+    rows = torch.repeat_interleave(torch.arange(rp4.numel() - 1, device=syn.device), (rp4[1:] - rp4[:-1]) * 4)
+    lens.index_add_(0, rows[keep], torch.ones_like(rows[keep]))
+    rowptr = torch.zeros(rp4.numel(), dtype=torch.int64, device=syn.device)
+    rowptr[1:] = torch.cumsum(lens, 0)
+    ent = syn[keep]
+    col = (ent >> 6).to(torch.int32)        # single block shard: internal id == gid
+    q = ((ent & 31) + 1).to(torch.uint8)
+    out = rowptr.cpu().numpy(), col.cpu().numpy(), q.cpu().numpy()
+    del rows, keep, syn
+    torch.cuda.empty_cache()
+    return out
+
+
+def cpu_baseline(net, lay, lif, args) -> dict:
+    """The CPU oracle (C, OpenMP on every host core) on a bounded sample of the same workload."""
+    from oracle import c_oracle
+    rowptr, col, q = gid_csr(net, lay)
+    threads = os.cpu_count() or 1
+    owner = np.zeros(lay.n_neurons, dtype=np.int32)
+    steps = args.cpu_steps
+    t = time.time()
+    c_oracle.simulate_csr(rowptr, col, q, owner, 1, [[-1]], lif.constants(args.seed), steps, threads=threads,
+                          raster=False, counts=False)
+    dt = time.time() - t
+    return {"value": round(steps / dt, 4), "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{steps} full steps of the same {lay.n_neurons}-neuron network (oracle/sim_oracle.c, "
+                      f"OpenMP {threads} threads), {dt:.1f} s"}
+
+
+def e2e_measure(sim, net, args) -> dict:
+    """Public API with host buffers: network uploaded from pinned host memory inside the
+    timed region (amortised per step), every step's spike bitmap read back to pinned host."""
+    import torch
+    st = sim.states[0]
+    csr = net.shards[0]
+    host_syn = torch.empty(csr.syn.shape, dtype=torch.int32, pin_memory=True)
+    host_syn.copy_(csr.syn)
+    host_rp = torch.empty(csr.rowptr4.shape, dtype=torch.int64, pin_memory=True)
+    host_rp.copy_(csr.rowptr4)
+    words = st.local_words
+    ring = torch.empty((2, words), dtype=torch.int32, pin_memory=True)
+    steps = args.steps
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    csr.syn.copy_(host_syn, non_blocking=True)
+    csr.rowptr4.copy_(host_rp, non_blocking=True)
+    sim.reset(1)
+    for t in range(steps):
+        sim.advance_eager(1)
+        cur = st.bitmaps[t & 1]
+        ring[t & 1].copy_(cur[: words], non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    h2d = host_syn.numel() * 4 + host_rp.numel() * 8
+    return {"value": round(steps / (ms * 1e-3), 2), "unit": UNIT, "h2d_bytes_per_step": int(h2d // steps),
+            "d2h_bytes_per_step": int(words * 4),
+            "note": "network H2D from pinned memory once per call (amortised), spike bitmap D2H every step"}
+
+
+# --------------------------------------------------------------------------- reference arm
+
+def run_reference(args) -> dict | None:
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return None
+    from oracle import c_oracle
+    from paper_2205_07125_b200.sim import LifParams
+    n = args.neurons
+    threads = os.cpu_count() or 1
+    t = time.time()
+    rowptr, col, q = c_oracle.generate_random_csr(n, args.degree, args.seed, threads=threads)
+    t_build = time.time() - t
+    owner = np.zeros(n, dtype=np.int32)
+    lif = LifParams()
+    steps = args.cpu_steps
+    t = time.time()
+    c_oracle.simulate_csr(rowptr, col, q, owner, 1, [[-1]], lif.constants(args.seed), args.warmup, threads=threads,
+                          raster=False, counts=False)
+    t = time.time()
+    c_oracle.simulate_csr(rowptr, col, q, owner, 1, [[-1]], lif.constants(args.seed), steps, threads=threads,
+                          raster=False, counts=False)
+    dt = time.time() - t
+    v = steps / dt
+    return {
+        "metric": METRIC, "value": round(v, 4), "unit": UNIT, "n_gpus": world, "steps": steps,
+        "warmup": args.warmup, "ms_per_step": round(dt * 1e3 / steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "fp32 state / int32 synaptic sums",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": "config 2: 1M LIF neurons x 1k synapses (CPU oracle port, all host threads)",
+                   "neurons": n, "mean_degree": args.degree, "synapses": int(rowptr[-1]),
+                   "graph_build_s": round(t_build, 2)},
+        "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{steps} full steps (oracle/sim_oracle.c, OpenMP)"},
+        "e2e": {"value": round(v, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main() -> int:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--neurons", type=int, default=1_000_000, help="neurons per GPU")
+    ap.add_argument("--degree", type=float, default=1000.0)
+    ap.add_argument("--delivery", default="fused", choices=["fused", "push"])
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"])
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--chunk", type=int, default=100)
+    ap.add_argument("--cpu-steps", type=int, default=3)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    res = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if res is not None:
+        print(json.dumps(res), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    raise SystemExit(main())

@@ -1,0 +1,237 @@
+/*
+ * neurocomm_b200.h -- C ABI of libneurocomm_b200.so, the B200 (sm_100a) engine
+ * behind the drop-in Python package paper_2205_07125_b200.
+ *
+ * Reference: arXiv 2205.07125 "neurocomm" (pkg/src/neurocomm).  The reference is
+ * pure Python + numpy and has no FFI; each entry point below names the
+ * reference function whose semantics it implements (file:line), or says
+ * "new" for the per-timestep loop the reference only models analytically
+ * (netsim.py:177-273).  The Python layer validates arguments and raises the
+ * reference's exception types before calling here; every entry point returns
+ * 0 on success and a non-zero NC_E* code otherwise, with a message available
+ * from nc_last_error().
+ *
+ * All pointers are plain device pointers unless marked [host].  `stream` is a
+ * cudaStream_t passed as void*.  No entry point allocates or frees memory it
+ * does not own; all device work is enqueued on `stream` and never synchronises
+ * the host unless stated.
+ */
+#ifndef NEUROCOMM_B200_H
+#define NEUROCOMM_B200_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NC_ABI_VERSION 1
+
+enum {
+  NC_OK = 0,
+  NC_E_ARG = 1,      /* invalid argument (Python maps to ValueError)        */
+  NC_E_CUDA = 2,     /* CUDA runtime error                                   */
+  NC_E_OVERFLOW = 3, /* a spike bucket exceeded its capacity                 */
+  NC_E_TIMEOUT = 4,  /* exchange watchdog expired waiting for a peer flag    */
+  NC_E_NCCL = 5      /* NCCL error                                           */
+};
+
+int nc_abi_version(void);
+const char* nc_last_error(void);
+
+/* ------------------------------------------------------------------ K6 --
+ * Capacity-bounded greedy bucket fill, bit-identical to
+ * neurocomm greedy.py:55-117 (called from partition.py:95-114 for
+ * neuron->GPU placement and routing.py:129-135 for GPU->group).
+ * [host] everything.  `capacity` is computed by the caller exactly as
+ * greedy.py:70 does ((fsum(w)/n_buckets)*(1+slack)); the C++ side uses an
+ * indexed max-heap keyed (score desc, weight desc, index asc) instead of the
+ * reference's lazy heapq, which selects the same item at every step. */
+int nc_greedy_fill(int64_t n_items, const double* weights, const int64_t* indptr,
+                   const int64_t* indices, const double* values, int32_t n_buckets,
+                   double capacity, int64_t* assignment_out);
+
+/* ------------------------------------------------------------------ K5 --
+ * Exact traffic histogram: device replacement for the summation in
+ * traffic.aggregate (traffic.py:66-84) and accum.keyed_sums (accum.py:21-41).
+ * contrib_e = (edge_p[e] * w[i]) * w[j]  (traffic.py:77, two RN multiplies);
+ * cell = lo*n_gpus + hi with lo/hi = min/max of the endpoints' GPUs.
+ * Each contribution is added EXACTLY into a fixed-point accumulator of
+ * `n_digits` 32-bit digits held in uint64 limbs whose least significant bit is
+ * 2^lsb_exponent; the caller rounds once (correctly, half-even) on the host,
+ * which reproduces math.fsum bit for bit.
+ *   nc_traffic_exponents: out_minmax[0] = min over edges of the binary
+ *     exponent of the contribution's lowest mantissa bit, out_minmax[1] = max
+ *     exponent of its leading bit (device int32[2], initialise to INT_MAX/INT_MIN).
+ *     Pass edge_i == NULL to scan `weights` (n_edges entries) instead.
+ *   nc_traffic_histogram: pg_limbs is uint64[n_gpus*n_gpus][n_digits] (only
+ *     lo<=hi cells are written), zero-initialised by the caller.
+ *   nc_weight_histogram: wg_limbs uint64[n_gpus][n_digits]: exact per-GPU
+ *     weight totals (partition.py:131-137 / traffic.py:83). */
+int nc_traffic_exponents(const int64_t* edge_i, const int64_t* edge_j, const double* edge_p,
+                         const double* weights, int64_t n_edges, int32_t* out_minmax,
+                         void* stream);
+int nc_traffic_histogram(const int64_t* edge_i, const int64_t* edge_j, const double* edge_p,
+                         const double* weights, const int64_t* assignment, int64_t n_edges,
+                         int32_t n_gpus, int32_t lsb_exponent, int32_t n_digits,
+                         unsigned long long* pg_limbs, void* stream);
+int nc_weight_histogram(const double* weights, const int64_t* assignment, int64_t n_neurons,
+                        int32_t n_gpus, int32_t lsb_exponent, int32_t n_digits,
+                        unsigned long long* wg_limbs, void* stream);
+
+/* ----------------------------------------------------- simulation state --
+ * New (the reference's only "step" is the analytic netsim.step_latency).
+ * One shard = the neurons one GPU owns under PartitionMap.assignment
+ * (partition.py:60-65).  Neurons are renumbered into an internal id space in
+ * which shard g owns the contiguous, 32-aligned range
+ * [local_base, local_base + n_local); bitmaps are indexed by internal id.
+ *
+ * Synapses: each undirected edge (i, j, p) of NeuronGraph is one synapse in
+ * each direction.  A pull-CSR entry of post-row r is a packed uint32
+ *     (pre_internal_id << 6) | (inhibitory(pre) << 5) | (q - 1),
+ * q = ceil(32 * p) in [1, 32]; its integer weight is q (excitatory pre) or
+ * -g_inh * q (inhibitory pre).  Rows are padded to a multiple of 4 entries
+ * with NC_PAD_ENTRY, whose pre id is the guard bit that never fires.
+ * rowptr4[r] is the row start in units of 4 entries. */
+
+#define NC_MAX_SHARDS 16
+#define NC_INTERNAL_ID_BITS 26
+
+typedef struct nc_lif_params {
+  float alpha_v;      /* exp(-dt/tau_m), computed in fp64 then rounded        */
+  float alpha_i;      /* exp(-dt/tau_syn)                                     */
+  float beta;         /* membrane gain applied to the synaptic current        */
+  float v_rest, v_reset, v_th;
+  float w_unit;       /* current per synaptic weight unit                     */
+  float w_ext;        /* current per external Poisson event                   */
+  float v_init_span;  /* v_th - v_reset (fp32): initial V is uniform in it    */
+  uint32_t ext_threshold; /* Philox lane k fires an external event if < this  */
+  int32_t ext_lanes;  /* number of Philox lanes (1..4) used as drive          */
+  int32_t t_ref;      /* refractory steps                                     */
+  int32_t g_inh;      /* inhibitory weight multiplier                         */
+  int32_t pad0;
+  uint64_t seed;
+} nc_lif_params_t;
+
+typedef struct nc_shard {
+  int32_t shard;          /* this shard's GPU index in the partition          */
+  int32_t n_shards;
+  int32_t n_local;        /* neurons owned                                     */
+  int32_t local_base;     /* first internal id owned (multiple of 32)          */
+  int32_t n_words;        /* bitmap words over all internal ids incl. guard   */
+  int32_t pad0;
+  /* neuron state, n_local each */
+  float* v;
+  float* i_syn;
+  uint8_t* refrac;
+  int32_t* acc;           /* synaptic input (push delivery / unfused path)    */
+  const uint32_t* gid;    /* global neuron id (Philox counter, raster ids)    */
+  const uint16_t* hop_mask; /* bit h: a spike of this neuron is sent to shard h */
+  /* pull CSR */
+  const int64_t* rowptr4; /* n_local+1                                         */
+  const uint32_t* syn;    /* packed entries                                    */
+  /* push CSR (optional): rows = internal pre ids, entries = (post_local<<6)|(inh<<5)|(q-1) */
+  const int64_t* push_rowptr;
+  const uint32_t* push_syn;
+  /* spikes */
+  uint32_t* bitmap0;      /* n_words; bitmap of step t lives in bitmap[t&1]   */
+  uint32_t* bitmap1;
+  uint32_t* fired_ids;    /* local fired internal ids of the current step      */
+  int32_t* fired_count;   /* [1]                                               */
+  /* per-destination send buckets: bucket h holds ids for shard h */
+  uint32_t* bucket_ids;   /* n_shards * bucket_cap                             */
+  int32_t* bucket_count;  /* n_shards                                          */
+  int64_t bucket_cap;
+  int32_t* status;        /* [0] overflow flag, [1] timeout flag               */
+  int32_t* step;          /* device step counter (read by every kernel)        */
+  /* records (NULL = off) */
+  uint32_t* raster;       /* [record_steps][local_words]: bitmap of local spikes */
+  int32_t record_steps;
+  int32_t local_words;
+  unsigned long long* spike_total; /* [1] running count of local spikes        */
+} nc_shard_t;
+
+/* Set kernel attributes (dynamic shared memory opt-in) once; call before any
+ * CUDA-graph capture of the step functions.  Implied by the first launch. */
+int nc_sim_prepare(void);
+
+/* Draw the initial state (V uniform in [v_reset, v_th), I = 0, refrac = 0),
+ * zero both bitmaps, counters and the step counter. */
+int nc_sim_init(const nc_shard_t* sh, const nc_lif_params_t* p, void* stream);
+
+/* One fused step on one shard (pull delivery K3 + LIF K1 + ballot/bucket K2):
+ * syn input = sum over the row's entries whose pre fired at step-1, integer;
+ * then the LIF update in the fixed fp32 operation order documented in
+ * DESIGN.md; fired ids are written to the current bitmap (local range), the
+ * fired list, and every bucket in the neuron's hop_mask (warp-aggregated).
+ * Also zeroes the remote part of the current bitmap for the exchange. */
+int nc_sim_step_fused(const nc_shard_t* sh, const nc_lif_params_t* p, void* stream);
+
+/* Unfused building blocks (same arithmetic):
+ *   deliver_pull: acc[r] = integer pull sum over the CSR row (K3 alone)
+ *   deliver_push: for every id set in the previous step's bitmap, add its
+ *                 push-CSR row into acc with integer atomics (event driven)
+ *   lif_update:   K1+K2 consuming and zeroing acc */
+int nc_sim_deliver_pull(const nc_shard_t* sh, int32_t g_inh, void* stream);
+int nc_sim_deliver_push(const nc_shard_t* sh, int32_t g_inh, void* stream);
+int nc_sim_lif_update(const nc_shard_t* sh, const nc_lif_params_t* p, void* stream);
+
+/* Advance the device step counter and reset the per-step bucket counts. */
+int nc_sim_end_step(const nc_shard_t* sh, void* stream);
+
+/* Single-process exchange over all shards of one device ("local" transport,
+ * used to run N partitions on one GPU and for the partition-invariance tests).
+ * Routing follows RoutingTable (routing.py:61-115, 184-231).  shards[] [host]
+ * are the n_shards shard descriptors; their next-hop buckets were filled by
+ * the step kernel.  fwd_table [host, n*n] holds, for relay b and source s, the
+ * destination shards d whose path is (s, b, d); dest_mask (device, per
+ * internal id) the shards hosting targets of each neuron.  fwd_ids/fwd_count
+ * are the relay buckets (n*n*fwd_cap ids, n*n counts; may be NULL when no path
+ * is bridged).  Counters (device int64, [n*n] or [steps][n*n] if per_step):
+ *   hop_ids[u*n+v]   ids carried on channel u->v (both phases)
+ *   deliv_ids[s*n+d] ids of source s delivered at d that have targets on d */
+int nc_exchange_local(const nc_shard_t* shards, int32_t n_shards, const uint16_t* dest_mask,
+                      const uint16_t* fwd_table, uint32_t* fwd_ids, int32_t* fwd_count,
+                      int64_t fwd_cap, long long* hop_ids, long long* deliv_ids, int32_t per_step,
+                      void* stream);
+
+/* ------------------------------------------------------- network build --
+ * Device SBM generator with the distributions of generate_synthetic
+ * (model.py:199-253): contiguous near-equal communities, intra pairs
+ * Bernoulli(p_in) with p ~ U(intra range), inter pairs Bernoulli(p_out) with
+ * p ~ U(inter range); counter-based (Philox) so every shard regenerates the
+ * same global graph and keeps the rows it owns.  Builds the pull CSR in the
+ * layout above.  Two passes: count (row lengths) then fill. */
+typedef struct nc_graphgen {
+  int64_t n_neurons;
+  int32_t n_communities;
+  int32_t shard;
+  double p_in, p_out;
+  double intra_lo, intra_hi, inter_lo, inter_hi;
+  uint64_t seed;
+  const int32_t* owner;       /* [n_neurons] shard of every gid               */
+  const int32_t* internal_id; /* [n_neurons] internal id of every gid         */
+  int32_t local_base;
+  int32_t inh_every;          /* gid % inh_every == inh_every-1 is inhibitory (0 = none) */
+} nc_graphgen_t;
+
+int nc_graphgen_count(const nc_graphgen_t* g, int32_t* lower_len, int32_t* upper_len,
+                      void* stream);
+int nc_graphgen_fill(const nc_graphgen_t* g, const int64_t* rowptr4, const int32_t* lower_len,
+                     int32_t* lower_fill, uint32_t* syn, void* stream);
+/* Write NC pad entries into [row length, 4*ceil(len/4)) of every local row. */
+int nc_graphgen_pad(const int64_t* rowptr4, const int32_t* lower_len, const int32_t* upper_len,
+                    int32_t n_local, uint32_t pad_entry, uint32_t* syn, void* stream);
+/* Destination masks from a built CSR (the adjacency is symmetric, so the
+ * pres of row r are exactly the posts r drives): dest_mask[r] = OR over the
+ * row's entries of (1 << owner shard of the pre id) without `self`, where shard
+ * h owns internal ids [shard_base[h], shard_base[h+1]) (device int32[n+1]). */
+int nc_dest_mask_from_csr(const int64_t* rowptr4, const uint32_t* syn, int32_t n_local,
+                          const int32_t* shard_base, int32_t n_shards, int32_t self,
+                          uint16_t* dest_mask, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NEUROCOMM_B200_H */

@@ -1,0 +1,143 @@
+"""ctypes binding of libneurocomm_b200.so (include/neurocomm_b200.h).
+
+The shared library is the only compute path: there is no Python or CPU
+fallback for any entry point.  If the library is missing or was built for a
+different ABI, every call raises ``RuntimeError`` naming the build command.
+Tensors are passed as raw pointers (``tensor.data_ptr()``) together with the
+current CUDA stream handle, so PyTorch only provides memory and streams.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+LIB_NAME = "libneurocomm_b200.so"
+LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
+ABI_VERSION = 1
+
+NC_OK, NC_E_ARG, NC_E_CUDA, NC_E_OVERFLOW, NC_E_TIMEOUT, NC_E_NCCL = range(6)
+MAX_SHARDS = 16
+INTERNAL_ID_BITS = 26
+
+c_void_p, c_int32, c_int64, c_uint32, c_uint64, c_double, c_float = (
+    C.c_void_p, C.c_int32, C.c_int64, C.c_uint32, C.c_uint64, C.c_double, C.c_float)
+
+
+class LifParamsC(C.Structure):
+    _fields_ = [
+        ("alpha_v", c_float), ("alpha_i", c_float), ("beta", c_float),
+        ("v_rest", c_float), ("v_reset", c_float), ("v_th", c_float),
+        ("w_unit", c_float), ("w_ext", c_float), ("v_init_span", c_float),
+        ("ext_threshold", c_uint32), ("ext_lanes", c_int32), ("t_ref", c_int32),
+        ("g_inh", c_int32), ("pad0", c_int32), ("seed", c_uint64),
+    ]
+
+
+class ShardC(C.Structure):
+    _fields_ = [
+        ("shard", c_int32), ("n_shards", c_int32), ("n_local", c_int32),
+        ("local_base", c_int32), ("n_words", c_int32), ("pad0", c_int32),
+        ("v", c_void_p), ("i_syn", c_void_p), ("refrac", c_void_p), ("acc", c_void_p),
+        ("gid", c_void_p), ("hop_mask", c_void_p),
+        ("rowptr4", c_void_p), ("syn", c_void_p),
+        ("push_rowptr", c_void_p), ("push_syn", c_void_p),
+        ("bitmap0", c_void_p), ("bitmap1", c_void_p),
+        ("fired_ids", c_void_p), ("fired_count", c_void_p),
+        ("bucket_ids", c_void_p), ("bucket_count", c_void_p), ("bucket_cap", c_int64),
+        ("status", c_void_p), ("step", c_void_p),
+        ("raster", c_void_p), ("record_steps", c_int32), ("local_words", c_int32),
+        ("spike_total", c_void_p),
+    ]
+
+
+class GraphGenC(C.Structure):
+    _fields_ = [
+        ("n_neurons", c_int64), ("n_communities", c_int32), ("shard", c_int32),
+        ("p_in", c_double), ("p_out", c_double),
+        ("intra_lo", c_double), ("intra_hi", c_double),
+        ("inter_lo", c_double), ("inter_hi", c_double),
+        ("seed", c_uint64),
+        ("owner", c_void_p), ("internal_id", c_void_p),
+        ("local_base", c_int32), ("inh_every", c_int32),
+    ]
+
+
+_SIGS = {
+    "nc_abi_version": (c_int32, []),
+    "nc_last_error": (C.c_char_p, []),
+    "nc_greedy_fill": (c_int32, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_double, c_void_p]),
+    "nc_traffic_exponents": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
+    "nc_traffic_histogram": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int32,
+                                       c_int32, c_int32, c_void_p, c_void_p]),
+    "nc_weight_histogram": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_int32, c_int32, c_void_p, c_void_p]),
+    "nc_sim_init": (c_int32, [C.POINTER(ShardC), C.POINTER(LifParamsC), c_void_p]),
+    "nc_sim_step_fused": (c_int32, [C.POINTER(ShardC), C.POINTER(LifParamsC), c_void_p]),
+    "nc_sim_deliver_pull": (c_int32, [C.POINTER(ShardC), c_int32, c_void_p]),
+    "nc_sim_deliver_push": (c_int32, [C.POINTER(ShardC), c_int32, c_void_p]),
+    "nc_sim_prepare": (c_int32, []),
+    "nc_sim_lif_update": (c_int32, [C.POINTER(ShardC), C.POINTER(LifParamsC), c_void_p]),
+    "nc_sim_end_step": (c_int32, [C.POINTER(ShardC), c_void_p]),
+    "nc_exchange_local": (c_int32, [C.POINTER(ShardC), c_int32, c_void_p, c_void_p, c_void_p, c_void_p,
+                                    c_int64, c_void_p, c_void_p, c_int32, c_void_p]),
+    "nc_graphgen_count": (c_int32, [C.POINTER(GraphGenC), c_void_p, c_void_p, c_void_p]),
+    "nc_graphgen_fill": (c_int32, [C.POINTER(GraphGenC), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "nc_graphgen_pad": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_uint32, c_void_p, c_void_p]),
+    "nc_dest_mask_from_csr": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p, c_int32, c_int32, c_void_p,
+                                        c_void_p]),
+}
+
+_lib = None
+
+
+def lib():
+    """Load the engine once; raise loudly if it is absent or stale."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = Path(os.environ.get("NEUROCOMM_B200_LIB", LIB_PATH))
+    if not path.is_file():
+        raise RuntimeError(
+            f"{path} not found: the CUDA engine is required (no CPU fallback). "
+            "Build it with `python -c 'import __graft_entry__ as g; g.build()'` or "
+            "`make -C paper_2205_07125_b200/csrc`."
+        )
+    handle = C.CDLL(str(path), mode=C.RTLD_GLOBAL)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(handle, name)
+        fn.restype = res
+        fn.argtypes = args
+    got = handle.nc_abi_version()
+    if got != ABI_VERSION:
+        raise RuntimeError(f"{path} has ABI {got}, expected {ABI_VERSION}; rebuild it")
+    _lib = handle
+    return _lib
+
+
+def exported_symbols() -> list[str]:
+    return sorted(_SIGS)
+
+
+def check(rc: int, what: str) -> None:
+    """Translate a non-zero NC_E* code into the reference's exception types."""
+    if rc == NC_OK:
+        return
+    msg = (lib().nc_last_error() or b"").decode(errors="replace")
+    if rc == NC_E_ARG:
+        raise ValueError(f"{what}: {msg}")
+    raise RuntimeError(f"{what} failed (code {rc}): {msg}")
+
+
+def ptr(t) -> int | None:
+    """Device/host pointer of a tensor or numpy array (None passes NULL)."""
+    if t is None:
+        return None
+    if hasattr(t, "data_ptr"):
+        return t.data_ptr()
+    return t.ctypes.data
+
+
+def stream_handle(device=None) -> int:
+    import torch
+    return torch.cuda.current_stream(device).cuda_stream

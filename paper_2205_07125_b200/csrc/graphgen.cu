@@ -1,0 +1,248 @@
+// Device network build: counter-based SBM generator -> pull CSR.
+//
+// Distributions follow neurocomm generate_synthetic (model.py:199-253):
+// contiguous near-equal communities (community_sizes, model.py:146-151), each
+// intra-community pair an edge with probability p_in and p ~ U(intra range),
+// each inter-community pair with p_out and p ~ U(inter range).  The reference
+// draws from one sequential PCG64 stream, which no GPU can replay; here every
+// (row i, block b) owns an independent Philox stream, so all shards generate
+// the identical global graph in parallel and keep only their own rows.
+//
+// Row i enumerates its upper neighbours j > i block by block with geometric
+// skipping (the same sampler as model.py:154-180, in fp64 log1p).  Each edge
+// (i, j) is one synapse in each direction: row i gets pre j, row j gets pre i.
+// Pass 1 counts per-row lengths (upper part directly, lower part with integer
+// atomics); the host scans the padded lengths into rowptr4; pass 2 regenerates
+// the same edges and writes them: row layout [lower part | upper part | pad].
+// The order inside the lower part depends on atomic arrival, which is harmless:
+// delivery sums integers, so any order gives the same input.
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <math.h>
+#include "nc_common.h"
+#include "philox.cuh"
+
+namespace {
+
+struct Comm {
+  int64_t q, r, big;  // sizes: first r communities have q+1, rest q; big = r*(q+1)
+  __device__ int64_t of(int64_t i) const { return i < big ? i / (q + 1) : r + (i - big) / q; }
+  __device__ int64_t start(int64_t c) const { return c < r ? c * (q + 1) : big + (c - r) * q; }
+  __device__ int64_t size(int64_t c) const { return c < r ? q + 1 : q; }
+};
+
+__device__ __forceinline__ Comm make_comm(const nc_graphgen_t& g) {
+  Comm c;
+  c.q = g.n_neurons / g.n_communities;
+  c.r = g.n_neurons % g.n_communities;
+  c.big = c.r * (c.q + 1);
+  return c;
+}
+
+// Uniform double in [0, 1) with 53 random bits.
+__device__ __forceinline__ double u53(uint32_t a, uint32_t b) {
+  return (double)(((uint64_t)a << 21) ^ (uint64_t)(b >> 11)) * 0x1.0p-53;
+}
+
+// Sequential geometric sampler over one block of n trials.
+struct GapStream {
+  uint32_t row, blk, k0, k1, ctr;
+  nc_u32x4 buf;
+  int avail;
+  double inv_log1m;
+  __device__ GapStream(uint32_t row_, uint32_t blk_, uint64_t seed, double p)
+      : row(row_), blk(blk_), k0((uint32_t)seed), k1((uint32_t)(seed >> 32)), ctr(0), avail(0) {
+    inv_log1m = 1.0 / log1p(-p);
+  }
+  __device__ double next_u() {
+    if (avail == 0) {
+      nc_u32x4 c = {row, blk, ctr++, NC_TAG_GAPS};
+      buf = nc_philox4x32_10(c, k0, k1);
+      avail = 2;
+    }
+    double u = (avail == 2) ? u53(buf.x, buf.y) : u53(buf.z, buf.w);
+    --avail;
+    return u;
+  }
+  // gap >= 1 between successes
+  __device__ int64_t gap() {
+    const double u = next_u();
+    const double gf = floor(log1p(-u) * inv_log1m);
+    return (gf >= 9.0e18) ? INT64_MAX / 4 : (int64_t)gf + 1;
+  }
+};
+
+__device__ __forceinline__ uint32_t edge_q(const nc_graphgen_t& g, int64_t i, int64_t j, bool intra) {
+  nc_u32x4 c = {(uint32_t)i, (uint32_t)j, NC_TAG_EDGEP, (uint32_t)((i >> 32) ^ ((j >> 32) << 16))};
+  nc_u32x4 x = nc_philox4x32_10(c, (uint32_t)g.seed, (uint32_t)(g.seed >> 32));
+  const double lo = intra ? g.intra_lo : g.inter_lo;
+  const double hi = intra ? g.intra_hi : g.inter_hi;
+  const double p = lo + (hi - lo) * u53(x.x, x.y);
+  double qf = ceil(p * 32.0);
+  qf = qf < 1.0 ? 1.0 : (qf > 32.0 ? 32.0 : qf);
+  return (uint32_t)qf;
+}
+
+__device__ __forceinline__ uint32_t is_inh(const nc_graphgen_t& g, int64_t gid) {
+  return (g.inh_every > 0 && (gid % g.inh_every) == g.inh_every - 1) ? 1u : 0u;
+}
+
+__device__ __forceinline__ uint32_t pack(uint32_t pre_internal, uint32_t inh, uint32_t q) {
+  return (pre_internal << 6) | (inh << 5) | (q - 1u);
+}
+
+// Visit every upper neighbour j of row i:  f(j, intra).
+template <typename F>
+__device__ void for_each_upper(const nc_graphgen_t& g, const Comm& cm, int64_t i, F&& f) {
+  const int64_t ci = cm.of(i);
+  const int64_t nc = g.n_communities;
+  for (int64_t b = ci; b < nc; ++b) {
+    const bool intra = (b == ci);
+    const double p = intra ? g.p_in : g.p_out;
+    if (p <= 0.0) continue;
+    const int64_t first = intra ? i + 1 : cm.start(b);
+    const int64_t n = intra ? cm.start(ci) + cm.size(ci) - i - 1 : cm.size(b);
+    if (n <= 0) continue;
+    if (p >= 1.0) {
+      for (int64_t t = 0; t < n; ++t) f(first + t, intra);
+      continue;
+    }
+    GapStream gs((uint32_t)i, (uint32_t)b, g.seed, p);
+    int64_t pos = -1;
+    for (;;) {
+      pos += gs.gap();
+      if (pos >= n) break;
+      f(first + pos, intra);
+    }
+  }
+}
+
+__global__ void k_count(const nc_graphgen_t g, int32_t* lower_len, int32_t* upper_len) {
+  const Comm cm = make_comm(g);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n_neurons;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const bool mine = g.owner[i] == g.shard;
+    int32_t up = 0;
+    for_each_upper(g, cm, i, [&](int64_t j, bool) {
+      ++up;
+      if (g.owner[j] == g.shard) atomicAdd(lower_len + (g.internal_id[j] - g.local_base), 1);
+    });
+    if (mine) upper_len[g.internal_id[i] - g.local_base] = up;
+  }
+}
+
+__global__ void k_fill(const nc_graphgen_t g, const int64_t* rowptr4, const int32_t* lower_len,
+                       int32_t* lower_fill, uint32_t* syn) {
+  const Comm cm = make_comm(g);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n_neurons;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const bool mine = g.owner[i] == g.shard;
+    const uint32_t iid = (uint32_t)g.internal_id[i];
+    const uint32_t inh_i = is_inh(g, i);
+    int64_t out = 0;
+    if (mine) {
+      const int64_t r = iid - g.local_base;
+      out = rowptr4[r] * 4 + lower_len[r];
+    }
+    for_each_upper(g, cm, i, [&](int64_t j, bool intra) {
+      const bool jm = g.owner[j] == g.shard;
+      if (!mine && !jm) return;
+      const uint32_t q = edge_q(g, i, j, intra);
+      if (mine) syn[out++] = pack((uint32_t)g.internal_id[j], is_inh(g, j), q);
+      if (jm) {
+        const int64_t rj = g.internal_id[j] - g.local_base;
+        const int32_t slot = atomicAdd(lower_fill + rj, 1);
+        syn[rowptr4[rj] * 4 + slot] = pack(iid, inh_i, q);
+      }
+    });
+  }
+}
+
+// Fill the pad entries [row length, 4*ceil(len/4)) of every local row.
+__global__ void k_pad(const int64_t* rowptr4, const int32_t* lower_len, const int32_t* upper_len,
+                      int32_t n_local, uint32_t pad_entry, uint32_t* syn) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_local;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t beg = rowptr4[r] * 4 + lower_len[r] + upper_len[r];
+    const int64_t end = rowptr4[r + 1] * 4;
+    for (int64_t k = beg; k < end; ++k) syn[k] = pad_entry;
+  }
+}
+
+__global__ void k_dest_mask(const int64_t* rowptr4, const uint32_t* syn, int32_t n_local,
+                            const int32_t* shard_base, int32_t n_shards, int32_t self,
+                            uint16_t* dest) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = wid; r < n_local; r += nw) {
+    uint32_t m = 0;
+    for (int64_t k = rowptr4[r] * 4 + lane; k < rowptr4[r + 1] * 4; k += 32) {
+      const uint32_t pre = syn[k] >> 6;
+      // owner: last shard whose base <= pre; the guard id is past every shard
+      int s = -1;
+      for (int h = 0; h < n_shards; ++h)
+        if ((int64_t)pre >= shard_base[h] && (int64_t)pre < shard_base[h + 1]) s = h;
+      if (s >= 0) m |= 1u << s;
+    }
+    m = __reduce_or_sync(0xffffffffu, m);
+    if (lane == 0) dest[r] = (uint16_t)(m & ~(1u << self));
+  }
+}
+
+int grid_for(int64_t n, int threads) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t b = (n + threads - 1) / threads;
+  if (b > (int64_t)sms * 16) b = (int64_t)sms * 16;
+  return b < 1 ? 1 : (int)b;
+}
+
+}  // namespace
+
+extern "C" int nc_graphgen_count(const nc_graphgen_t* g, int32_t* lower_len, int32_t* upper_len,
+                                 void* stream) {
+  if (!g || g->n_neurons < 1 || g->n_communities < 1 || g->n_communities > g->n_neurons) {
+    nc_set_error("nc_graphgen_count: invalid generator spec");
+    return NC_E_ARG;
+  }
+  k_count<<<grid_for(g->n_neurons, 128), 128, 0, (cudaStream_t)stream>>>(*g, lower_len, upper_len);
+  NC_LAUNCH_CHECK();
+  return NC_OK;
+}
+
+extern "C" int nc_graphgen_fill(const nc_graphgen_t* g, const int64_t* rowptr4, const int32_t* lower_len,
+                                int32_t* lower_fill, uint32_t* syn, void* stream) {
+  if (!g) {
+    nc_set_error("nc_graphgen_fill: null spec");
+    return NC_E_ARG;
+  }
+  k_fill<<<grid_for(g->n_neurons, 128), 128, 0, (cudaStream_t)stream>>>(*g, rowptr4, lower_len,
+                                                                          lower_fill, syn);
+  NC_LAUNCH_CHECK();
+  return NC_OK;
+}
+
+extern "C" int nc_graphgen_pad(const int64_t* rowptr4, const int32_t* lower_len, const int32_t* upper_len,
+                               int32_t n_local, uint32_t pad_entry, uint32_t* syn, void* stream) {
+  k_pad<<<grid_for(n_local, 256), 256, 0, (cudaStream_t)stream>>>(rowptr4, lower_len, upper_len, n_local,
+                                                                    pad_entry, syn);
+  NC_LAUNCH_CHECK();
+  return NC_OK;
+}
+
+extern "C" int nc_dest_mask_from_csr(const int64_t* rowptr4, const uint32_t* syn, int32_t n_local,
+                                     const int32_t* shard_base, int32_t n_shards, int32_t self,
+                                     uint16_t* dest_mask, void* stream) {
+  if (n_shards < 1 || n_shards > NC_MAX_SHARDS) {
+    nc_set_error("nc_dest_mask_from_csr: n_shards must be in [1, %d]", NC_MAX_SHARDS);
+    return NC_E_ARG;
+  }
+  if (n_local == 0) return NC_OK;
+  k_dest_mask<<<grid_for((int64_t)n_local * 32, 256), 256, 0, (cudaStream_t)stream>>>(
+      rowptr4, syn, n_local, shard_base, n_shards, self, dest_mask);
+  NC_LAUNCH_CHECK();
+  return NC_OK;
+}

@@ -1,0 +1,207 @@
+// K5: exact GPU traffic / edge-cut histogram.
+//
+// Device replacement for the summation in neurocomm traffic.aggregate
+// (traffic.py:66-84), whose per-cell sums go through accum.keyed_sums
+// (accum.py:21-41) = math.fsum, i.e. the correctly rounded exact sum.  fp64
+// atomics cannot reproduce that (the survey measured naive fp64 differing in
+// every cell), so each contribution is decomposed into its 53-bit integer
+// mantissa and exponent and added EXACTLY into a fixed-point accumulator of
+// 32-bit digits held in 64-bit limbs: integer adds are associative, the result
+// is order independent, and the host rounds the exact integer once.
+//
+// Per block the cells live in shared memory (N(N+1)/2 upper cells x n_digits
+// limbs); at the end each block carry-normalises its digits to < 2^32 and
+// adds them to the global limbs, which therefore stay below 2^64 for up to
+// 2^32 blocks.  When the cells do not fit in shared memory the kernel adds
+// straight into global limbs (each add < 2^32, safe for < 2^32 adds per limb).
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <climits>
+#include "nc_common.h"
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr size_t kSmemLimit = 96 * 1024;
+
+struct Decomposed {
+  unsigned long long mant;  // integer mantissa (0 => nothing to add)
+  int lsb;                  // exponent of the mantissa's bit 0
+};
+
+__device__ __forceinline__ Decomposed decompose(double x) {
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
+  const int e = (int)((bits >> 52) & 0x7ff);
+  Decomposed d;
+  d.mant = bits & 0xfffffffffffffull;
+  if (e == 0) {
+    d.lsb = -1074;
+  } else {
+    d.mant |= 1ull << 52;
+    d.lsb = e - 1075;
+  }
+  return d;
+}
+
+__device__ __forceinline__ double contrib(double p, double wi, double wj) {
+  return __dmul_rn(__dmul_rn(p, wi), wj);  // (p*W_i)*W_j, traffic.py:77
+}
+
+// Add mant * 2^(lsb - lsb0) into limbs[0..n_digits).
+__device__ __forceinline__ void add_fixed(unsigned long long* limbs, int n_digits, Decomposed d,
+                                          int lsb0) {
+  if (d.mant == 0) return;
+  const int s = d.lsb - lsb0;  // >= 0 by construction of lsb0
+  const int k = s >> 5, o = s & 31;
+  const unsigned long long lo = d.mant << o;                 // low 64 bits of mant << o
+  const unsigned long long hi = o ? (d.mant >> (64 - o)) : 0ull;  // bits 64.. (<= 21 bits)
+  const unsigned long long d0 = lo & 0xffffffffull, d1 = lo >> 32, d2 = hi;
+  if (d0 && k < n_digits) atomicAdd(limbs + k, d0);
+  if (d1 && k + 1 < n_digits) atomicAdd(limbs + k + 1, d1);
+  if (d2 && k + 2 < n_digits) atomicAdd(limbs + k + 2, d2);
+}
+
+__device__ __forceinline__ int cell_index(int64_t a, int64_t b, int n) {
+  const int lo = (int)(a < b ? a : b), hi = (int)(a < b ? b : a);
+  return lo * n + hi;
+}
+
+__global__ void k_exponents(const int64_t* __restrict__ ei, const int64_t* __restrict__ ej,
+                            const double* __restrict__ ep, const double* __restrict__ w, int64_t n,
+                            int* minmax) {
+  int lo = INT_MAX, hi = INT_MIN;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const double x = ei ? contrib(ep[k], w[ei[k]], w[ej[k]]) : w[k];
+    const Decomposed d = decompose(x);
+    if (d.mant == 0) continue;
+    lo = min(lo, d.lsb);
+    hi = max(hi, d.lsb + 63 - __clzll((long long)d.mant));
+  }
+  for (int off = 16; off; off >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, off));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, off));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (lo != INT_MAX) atomicMin(minmax, lo);
+    if (hi != INT_MIN) atomicMax(minmax + 1, hi);
+  }
+}
+
+// Carry-normalise a block's limbs for one cell and add into global.
+__device__ void flush_cell(unsigned long long* g, const unsigned long long* s, int n_digits) {
+  unsigned long long carry = 0;
+  for (int k = 0; k < n_digits; ++k) {
+    const unsigned long long v = s[k] + carry;  // s[k] < 2^63, carry < 2^32: no wrap
+    const unsigned long long digit = (k + 1 < n_digits) ? (v & 0xffffffffull) : v;
+    carry = (k + 1 < n_digits) ? (v >> 32) : 0;
+    if (digit) atomicAdd(g + k, digit);
+  }
+}
+
+template <bool kSmem>
+__global__ void __launch_bounds__(kThreads)
+k_histogram(const int64_t* __restrict__ ei, const int64_t* __restrict__ ej,
+            const double* __restrict__ ep, const double* __restrict__ w,
+            const int64_t* __restrict__ asg, int64_t n, int n_gpus, int lsb0, int n_digits,
+            unsigned long long* __restrict__ out) {
+  extern __shared__ unsigned long long sl[];
+  const int n_cells = ei ? n_gpus * n_gpus : n_gpus;
+  if (kSmem) {
+    for (int k = threadIdx.x; k < n_cells * n_digits; k += blockDim.x) sl[k] = 0ull;
+    __syncthreads();
+  }
+  unsigned long long* acc = kSmem ? sl : out;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    double x;
+    int cell;
+    if (ei) {
+      const int64_t i = ei[k], j = ej[k];
+      x = contrib(ep[k], w[i], w[j]);
+      cell = cell_index(asg[i], asg[j], n_gpus);
+    } else {  // per-GPU weight totals (binned_sums over assignment)
+      x = w[k];
+      cell = (int)asg[k];
+    }
+    add_fixed(acc + (int64_t)cell * n_digits, n_digits, decompose(x), lsb0);
+  }
+  if (kSmem) {
+    __syncthreads();
+    for (int c = threadIdx.x; c < n_cells; c += blockDim.x)
+      flush_cell(out + (int64_t)c * n_digits, sl + (int64_t)c * n_digits, n_digits);
+  }
+}
+
+int launch_hist(const int64_t* ei, const int64_t* ej, const double* ep, const double* w,
+                const int64_t* asg, int64_t n, int n_gpus, int lsb0, int n_digits,
+                unsigned long long* out, cudaStream_t st) {
+  if (n <= 0) return NC_OK;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t n_cells = ei ? (size_t)n_gpus * n_gpus : (size_t)n_gpus;
+  const size_t smem = n_cells * n_digits * sizeof(unsigned long long);
+  int64_t blocks = (n + kThreads - 1) / kThreads;
+  // each block handles >= 16 items per thread before flushing; cap the grid
+  const int64_t max_blocks = (int64_t)sms * 8;
+  if (blocks > max_blocks) blocks = max_blocks;
+  if (smem <= kSmemLimit) {
+    static bool attr = false;
+    if (!attr) {
+      NC_CUDA_TRY(cudaFuncSetAttribute(k_histogram<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)kSmemLimit));
+      attr = true;
+    }
+    k_histogram<true><<<(unsigned)blocks, kThreads, smem, st>>>(ei, ej, ep, w, asg, n, n_gpus, lsb0,
+                                                                 n_digits, out);
+  } else {
+    k_histogram<false><<<(unsigned)blocks, kThreads, 0, st>>>(ei, ej, ep, w, asg, n, n_gpus, lsb0,
+                                                               n_digits, out);
+  }
+  NC_LAUNCH_CHECK();
+  return NC_OK;
+}
+
+}  // namespace
+
+extern "C" int nc_traffic_exponents(const int64_t* edge_i, const int64_t* edge_j, const double* edge_p,
+                                    const double* weights, int64_t n_edges, int32_t* out_minmax,
+                                    void* stream) {
+  if (n_edges <= 0) return NC_OK;
+  if ((edge_i == nullptr) != (edge_j == nullptr)) {
+    nc_set_error("nc_traffic_exponents: edge_i/edge_j must both be set or both NULL");
+    return NC_E_ARG;
+  }
+  int64_t blocks = (n_edges + kThreads - 1) / kThreads;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_exponents<<<(unsigned)blocks, kThreads, 0, (cudaStream_t)stream>>>(edge_i, edge_j, edge_p, weights,
+                                                                        n_edges, out_minmax);
+  NC_LAUNCH_CHECK();
+  return NC_OK;
+}
+
+extern "C" int nc_traffic_histogram(const int64_t* edge_i, const int64_t* edge_j, const double* edge_p,
+                                    const double* weights, const int64_t* assignment, int64_t n_edges,
+                                    int32_t n_gpus, int32_t lsb_exponent, int32_t n_digits,
+                                    unsigned long long* pg_limbs, void* stream) {
+  if (n_gpus < 1 || n_digits < 3 || !edge_i || !edge_j) {
+    nc_set_error("nc_traffic_histogram: bad arguments (n_gpus=%d n_digits=%d)", n_gpus, n_digits);
+    return NC_E_ARG;
+  }
+  return launch_hist(edge_i, edge_j, edge_p, weights, assignment, n_edges, n_gpus, lsb_exponent,
+                     n_digits, pg_limbs, (cudaStream_t)stream);
+}
+
+extern "C" int nc_weight_histogram(const double* weights, const int64_t* assignment, int64_t n_neurons,
+                                   int32_t n_gpus, int32_t lsb_exponent, int32_t n_digits,
+                                   unsigned long long* wg_limbs, void* stream) {
+  if (n_gpus < 1 || n_digits < 3) {
+    nc_set_error("nc_weight_histogram: bad arguments");
+    return NC_E_ARG;
+  }
+  // same kernel with one cell per GPU (cell = assignment[k]), binned_sums semantics
+  return launch_hist(nullptr, nullptr, nullptr, weights, assignment, n_neurons, n_gpus, lsb_exponent,
+                     n_digits, wg_limbs, (cudaStream_t)stream);
+}

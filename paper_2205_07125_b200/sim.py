@@ -1,0 +1,719 @@
+"""simulate(steps): the per-timestep spiking hot loop on B200.
+
+New relative to the reference (neurocomm models one step only analytically,
+netsim.py:177-273); it consumes exactly what the reference pipeline produces:
+``NeuronGraph`` (model.py:53-92) -> ``PartitionMap`` (partition.py:60-65) ->
+``RoutingTable`` (routing.py:61-115).  Semantics are DESIGN.md section 3; the
+CPU oracle restating them is oracle/sim_oracle.c.
+
+Per step and shard (one shard per GPU, or several shards on one GPU with the
+"local" transport):
+
+  fused  : nc_sim_step_fused   K3 pull delivery + K1 LIF + K2 ballot/bucket
+  push   : nc_sim_deliver_push (event driven) then nc_sim_lif_update (K1+K2)
+  then the spike exchange (route-table next hops, two-level relay) and
+  nc_sim_end_step.  Everything stays on the device; the step counter lives in
+  device memory, so a chunk of steps is captured once in a CUDA graph and
+  replayed.
+
+PyTorch provides device memory, streams, CUDA graphs and torch.distributed;
+every kernel is in libneurocomm_b200.so.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from .model import INTER_P_RANGE, INTRA_P_RANGE, ModelSpec, NeuronGraph, community_sizes
+from .routing import RoutingTable
+
+__all__ = [
+    "LifParams", "ShardLayout", "ExchangePlan", "Network", "Simulator", "SimReport", "simulate",
+    "q_from_p", "inhibitory_mask", "PAD_Q_BITS",
+]
+
+PAD_Q_BITS = 6          # low bits of a packed entry: inhibitory flag + (q-1)
+Q_LEVELS = 32           # synaptic weight units: q = ceil(32 p) in [1, 32]
+
+
+# ---------------------------------------------------------------- parameters
+
+@dataclass(frozen=True)
+class LifParams:
+    """Current-based LIF neuron + Poisson drive.
+
+    Constants are computed in fp64 on the host and rounded once to fp32
+    (:meth:`constants`); the update then runs entirely in fp32 with explicit
+    round-to-nearest operations in a fixed order on both GPU and oracle.
+    """
+
+    dt_ms: float = 1.0
+    tau_m_ms: float = 20.0
+    tau_syn_ms: float = 5.0
+    v_rest: float = 0.0
+    v_reset: float = 0.0
+    v_th: float = 20.0
+    t_ref_steps: int = 2
+    w_syn: float = 0.32          # synaptic current of one q=32 (p=1) synapse event
+    g_inh: int = 4               # inhibitory synapses weigh -g_inh * q
+    inh_every: int = 5           # gid % inh_every == inh_every-1 is inhibitory (0 = none)
+    ext_rate_hz: float = 215.0   # Poisson rate of each of ext_lanes external inputs (~10 Hz firing)
+    ext_lanes: int = 4
+    w_ext: float = 4.0           # synaptic current of one external event
+
+    def constants(self, seed: int) -> dict:
+        f32 = lambda x: float(np.float32(x))  # noqa: E731
+        if not (self.dt_ms > 0 and self.tau_m_ms > 0 and self.tau_syn_ms > 0):
+            raise ValueError("dt_ms, tau_m_ms and tau_syn_ms must be > 0")
+        if not 0 <= self.t_ref_steps <= 255:
+            raise ValueError("t_ref_steps must be in [0, 255]")
+        if not 0 <= self.ext_lanes <= 4:
+            raise ValueError("ext_lanes must be in [0, 4]")
+        p_lane = self.ext_rate_hz * self.dt_ms * 1e-3
+        if not 0.0 <= p_lane < 1.0:
+            raise ValueError(f"ext_rate_hz * dt must be a probability < 1, got {p_lane}")
+        decay_v = math.exp(-self.dt_ms / self.tau_m_ms)
+        return {
+            "alpha_v": f32(decay_v),
+            "alpha_i": f32(math.exp(-self.dt_ms / self.tau_syn_ms)),
+            "beta": f32(1.0 - decay_v),
+            "v_rest": f32(self.v_rest), "v_reset": f32(self.v_reset), "v_th": f32(self.v_th),
+            "w_unit": f32(self.w_syn / Q_LEVELS),
+            "w_ext": f32(self.w_ext),
+            "v_init_span": float(np.float32(self.v_th) - np.float32(self.v_reset)),
+            "ext_threshold": min(int(round(p_lane * 2.0**32)), 2**32 - 1),
+            "ext_lanes": int(self.ext_lanes), "t_ref": int(self.t_ref_steps),
+            "g_inh": int(self.g_inh), "inh_every": int(self.inh_every),
+            "seed": int(seed) & (2**64 - 1),
+        }
+
+    def to_c(self, seed: int) -> _native.LifParamsC:
+        k = self.constants(seed)
+        return _native.LifParamsC(
+            alpha_v=k["alpha_v"], alpha_i=k["alpha_i"], beta=k["beta"], v_rest=k["v_rest"],
+            v_reset=k["v_reset"], v_th=k["v_th"], w_unit=k["w_unit"], w_ext=k["w_ext"],
+            v_init_span=k["v_init_span"], ext_threshold=k["ext_threshold"], ext_lanes=k["ext_lanes"],
+            t_ref=k["t_ref"], g_inh=k["g_inh"], pad0=0, seed=k["seed"])
+
+
+def q_from_p(p) -> np.ndarray:
+    """Synaptic weight units of connection probability p: ceil(32 p) clipped to [1, 32]."""
+    return np.clip(np.ceil(np.asarray(p, dtype=np.float64) * Q_LEVELS), 1, Q_LEVELS).astype(np.uint8)
+
+
+def inhibitory_mask(gid, every: int) -> np.ndarray:
+    g = np.asarray(gid, dtype=np.int64)
+    if every <= 0:
+        return np.zeros(g.shape, dtype=bool)
+    return (g % every) == every - 1
+
+
+# ---------------------------------------------------------------- layout
+
+@dataclass
+class ShardLayout:
+    """Internal renumbering: shard h owns the 32-aligned id range [base[h], base[h] + count[h])."""
+
+    n_neurons: int
+    n_shards: int
+    owner: np.ndarray          # int32 [M]
+    members: list              # per shard: ascending gids (int64)
+    base: np.ndarray           # int64 [n+1], base[n] = end of the last shard's padded range
+    internal_id: np.ndarray    # int32 [M]
+    n_words: int               # bitmap words incl. a guard word, multiple of 4
+
+    @classmethod
+    def from_assignment(cls, assignment, n_shards: int) -> "ShardLayout":
+        owner = np.ascontiguousarray(assignment, dtype=np.int64)
+        if owner.size and (owner.min() < 0 or owner.max() >= n_shards):
+            raise ValueError("assignment has GPU indices outside [0, n_gpus)")
+        if n_shards > _native.MAX_SHARDS:
+            raise ValueError(f"at most {_native.MAX_SHARDS} shards are supported, got {n_shards}")
+        members = [np.flatnonzero(owner == h) for h in range(n_shards)]
+        counts = np.array([m.size for m in members], dtype=np.int64)
+        padded = (counts + 31) // 32 * 32
+        base = np.zeros(n_shards + 1, dtype=np.int64)
+        base[1:] = np.cumsum(padded)
+        internal = np.empty(owner.size, dtype=np.int64)
+        for h, m in enumerate(members):
+            internal[m] = base[h] + np.arange(m.size)
+        n_words = (int(base[-1]) // 32 + 1 + 3) // 4 * 4
+        if n_words * 32 > (1 << _native.INTERNAL_ID_BITS):
+            raise ValueError(f"network too large for {_native.INTERNAL_ID_BITS}-bit neuron ids")
+        return cls(int(owner.size), n_shards, owner.astype(np.int32), members, base,
+                   internal.astype(np.int32), n_words)
+
+    @classmethod
+    def blocks(cls, n_neurons: int, n_shards: int) -> "ShardLayout":
+        """Contiguous near-equal blocks (the placement greedy recovers on C = N planted graphs)."""
+        sizes = community_sizes(n_neurons, n_shards)
+        return cls.from_assignment(np.repeat(np.arange(n_shards), sizes), n_shards)
+
+    @property
+    def guard_id(self) -> int:
+        return (self.n_words - 1) * 32
+
+    @property
+    def pad_entry(self) -> int:
+        return self.guard_id << PAD_Q_BITS
+
+    def n_local(self, h: int) -> int:
+        return int(self.members[h].size)
+
+
+# ---------------------------------------------------------------- network
+
+def _pack(pre_internal, inh, q):
+    return ((pre_internal.astype(np.uint32) << np.uint32(PAD_Q_BITS))
+            | (inh.astype(np.uint32) << np.uint32(5)) | (q.astype(np.uint32) - np.uint32(1)))
+
+
+def host_pull_csr(graph: NeuronGraph, layout: ShardLayout, shard: int, inh_every: int):
+    """Pull CSR of one shard from a host NeuronGraph (rows = local posts, padded to 4)."""
+    q = q_from_p(graph.edge_p)
+    post = np.concatenate([graph.edge_j, graph.edge_i]).astype(np.int64)
+    pre = np.concatenate([graph.edge_i, graph.edge_j]).astype(np.int64)
+    qq = np.concatenate([q, q])
+    keep = layout.owner[post] == shard
+    post, pre, qq = post[keep], pre[keep], qq[keep]
+    n_local = layout.n_local(shard)
+    row = layout.internal_id[post].astype(np.int64) - int(layout.base[shard])
+    entries = _pack(layout.internal_id[pre], inhibitory_mask(pre, inh_every), qq)
+    counts = np.bincount(row, minlength=n_local).astype(np.int64)
+    rowptr4 = np.zeros(n_local + 1, dtype=np.int64)
+    rowptr4[1:] = np.cumsum((counts + 3) // 4)
+    syn = np.full(int(rowptr4[-1]) * 4, layout.pad_entry, dtype=np.uint32)
+    order = np.argsort(row, kind="stable")
+    srow = row[order]
+    first = np.cumsum(counts) - counts
+    slot = np.arange(srow.size, dtype=np.int64) - first[srow]
+    syn[rowptr4[srow] * 4 + slot] = entries[order]
+    return rowptr4, syn
+
+
+@dataclass
+class GeneratorSpec:
+    """Device SBM generator spec with the distributions of ModelSpec/generate_synthetic."""
+
+    n_neurons: int
+    n_communities: int
+    p_in: float
+    p_out: float
+    seed: int = 0
+    intra_p_range: tuple = INTRA_P_RANGE
+    inter_p_range: tuple = INTER_P_RANGE
+
+    @classmethod
+    def from_model_spec(cls, spec: ModelSpec, **kw) -> "GeneratorSpec":
+        return cls(spec.n_neurons, spec.n_communities, spec.p_in, spec.p_out, spec.seed, **kw)
+
+    @classmethod
+    def random(cls, n_neurons: int, degree: float, seed: int = 0) -> "GeneratorSpec":
+        """C = 1 random network with mean degree `degree` (synapses per neuron)."""
+        return cls(n_neurons, 1, degree / max(n_neurons - 1, 1), 0.0, seed)
+
+
+@dataclass
+class ShardCSR:
+    rowptr4: object   # torch int64 [n_local+1] (device)
+    syn: object       # torch int32 [4*rowptr4[-1]] (device) -- packed uint32 entries
+    dest: object      # torch int32 [n_local] (device) -- shards hosting targets, self excluded
+
+    @property
+    def n_synapses_padded(self) -> int:
+        return int(self.syn.numel())
+
+
+class Network:
+    """Per-shard pull CSRs on the device plus the replicated destination masks."""
+
+    def __init__(self, layout: ShardLayout, shards: dict, device, inh_every: int, *, n_synapses: int,
+                 source: str):
+        self.layout = layout
+        self.shards = shards          # shard index -> ShardCSR (the shards this process owns)
+        self.device = device
+        self.inh_every = inh_every
+        self.n_synapses = n_synapses  # real (unpadded) synapses over the owned shards
+        self.source = source
+
+    # ------------------------------------------------------------ builders
+    @classmethod
+    def from_graph(cls, graph: NeuronGraph, layout: ShardLayout, *, device=None, inh_every: int = 5,
+                   shards=None) -> "Network":
+        import torch
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        own = range(layout.n_shards) if shards is None else shards
+        out = {}
+        nsyn = 0
+        for h in own:
+            rp, syn = host_pull_csr(graph, layout, h, inh_every)
+            csr = ShardCSR(torch.from_numpy(rp).to(dev), torch.from_numpy(syn.view(np.int32)).to(dev), None)
+            csr.dest = _dest_masks(csr, layout, h, dev)
+            out[h] = csr
+            nsyn += int(np.count_nonzero(syn != np.uint32(layout.pad_entry)))
+        return cls(layout, out, dev, inh_every, n_synapses=nsyn, source="host graph")
+
+    @classmethod
+    def generate(cls, spec: GeneratorSpec, layout: ShardLayout, *, device=None, inh_every: int = 5,
+                 shards=None) -> "Network":
+        """Counter-based device generator (csrc/graphgen.cu); every shard regenerates the same graph."""
+        import torch
+        if layout.n_neurons != spec.n_neurons:
+            raise ValueError("layout and generator disagree on the neuron count")
+        if not 1 <= spec.n_communities <= spec.n_neurons:
+            raise ValueError("n_communities must be in [1, n_neurons]")
+        if not 0.0 <= spec.p_out <= spec.p_in <= 1.0:
+            raise ValueError("edge probabilities must satisfy 0 <= p_out <= p_in <= 1")
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        L = _native.lib()
+        st = _native.stream_handle(dev)
+        owner_d = torch.from_numpy(layout.owner).to(dev)
+        internal_d = torch.from_numpy(layout.internal_id).to(dev)
+        own = range(layout.n_shards) if shards is None else shards
+        out = {}
+        nsyn = 0
+        for h in own:
+            n_local = layout.n_local(h)
+            g = _native.GraphGenC(
+                n_neurons=spec.n_neurons, n_communities=spec.n_communities, shard=h, p_in=spec.p_in,
+                p_out=spec.p_out, intra_lo=spec.intra_p_range[0], intra_hi=spec.intra_p_range[1],
+                inter_lo=spec.inter_p_range[0], inter_hi=spec.inter_p_range[1],
+                seed=int(spec.seed) & (2**64 - 1), owner=owner_d.data_ptr(), internal_id=internal_d.data_ptr(),
+                local_base=int(layout.base[h]), inh_every=inh_every)
+            lower = torch.zeros(max(n_local, 1), dtype=torch.int32, device=dev)
+            upper = torch.zeros(max(n_local, 1), dtype=torch.int32, device=dev)
+            _native.check(L.nc_graphgen_count(C.byref(g), lower.data_ptr(), upper.data_ptr(), st), "graphgen count")
+            lens = (lower[:n_local] + upper[:n_local]).to(torch.int64)
+            rowptr4 = torch.zeros(n_local + 1, dtype=torch.int64, device=dev)
+            rowptr4[1:] = torch.cumsum((lens + 3) // 4, 0)
+            total = int(rowptr4[-1].item()) * 4
+            syn = torch.empty(max(total, 4), dtype=torch.int32, device=dev)
+            fill = torch.zeros_like(lower)
+            _native.check(L.nc_graphgen_fill(C.byref(g), rowptr4.data_ptr(), lower.data_ptr(), fill.data_ptr(),
+                                             syn.data_ptr(), st), "graphgen fill")
+            _native.check(L.nc_graphgen_pad(rowptr4.data_ptr(), lower.data_ptr(), upper.data_ptr(), n_local,
+                                            layout.pad_entry, syn.data_ptr(), st), "graphgen pad")
+            csr = ShardCSR(rowptr4, syn, None)
+            csr.dest = _dest_masks(csr, layout, h, dev)
+            out[h] = csr
+            nsyn += int(lens.sum().item())
+        return cls(layout, out, dev, inh_every, n_synapses=nsyn, source="device generator")
+
+    # ------------------------------------------------------------ helpers
+    def global_dest(self):
+        """Destination mask of every internal id (int16 bit patterns), for relays."""
+        import torch
+        g = torch.zeros(self.layout.n_words * 32, dtype=torch.int32, device=self.device)
+        for h, csr in self.shards.items():
+            b = int(self.layout.base[h])
+            g[b:b + self.layout.n_local(h)] = csr.dest
+        return _as_u16(g)
+
+    def host_csr(self, shard: int):
+        """(rowptr, pre_gid, q) of one shard in gid space, for the oracle (test/bench only)."""
+        import torch
+        csr = self.shards[shard]
+        rp4 = csr.rowptr4.cpu().numpy()
+        syn = csr.syn.cpu().numpy().view(np.uint32)[: int(rp4[-1]) * 4]
+        keep = syn != np.uint32(self.layout.pad_entry)
+        rows = np.repeat(np.arange(rp4.size - 1), np.diff(rp4) * 4)[keep]
+        ent = syn[keep]
+        gid_of_internal = np.full(self.layout.n_words * 32, -1, dtype=np.int64)
+        for h, m in enumerate(self.layout.members):
+            gid_of_internal[int(self.layout.base[h]) + np.arange(m.size)] = m
+        pre = gid_of_internal[(ent >> PAD_Q_BITS).astype(np.int64)]
+        q = (ent & np.uint32(31)).astype(np.uint8) + 1
+        post = self.layout.members[shard][rows]
+        del torch
+        return post, pre, q
+
+
+def _as_u16(t32):
+    import torch
+    t = t32.to(torch.int32) & 0xFFFF
+    return torch.where(t >= 0x8000, t - 0x10000, t).to(torch.int16)
+
+
+def _dest_masks(csr: ShardCSR, layout: ShardLayout, h: int, dev):
+    import torch
+    n_local = layout.n_local(h)
+    bases = torch.from_numpy(layout.base.astype(np.int32)).to(dev)
+    out16 = torch.zeros(max(n_local, 1), dtype=torch.int16, device=dev)
+    L = _native.lib()
+    _native.check(L.nc_dest_mask_from_csr(csr.rowptr4.data_ptr(), csr.syn.data_ptr(), n_local, bases.data_ptr(),
+                                          layout.n_shards, h, out16.data_ptr(), _native.stream_handle(dev)),
+                  "dest mask")
+    return out16[:n_local].to(torch.int32) & 0xFFFF
+
+
+# ---------------------------------------------------------------- exchange plan
+
+class ExchangePlan:
+    """Next hops and relay sets from a RoutingTable (routing.py:61-115).
+
+    ``next_hop[s, d]``: first hop of demand (s, d), -1 if there is no demand.
+    ``fwd[b, s]``: bitmask of destinations d whose path is (s, b, d) -- the
+    shards relay b forwards spikes from s to (two-level routing).
+    """
+
+    def __init__(self, n_shards: int, rt: RoutingTable | None):
+        n = n_shards
+        if rt is None:
+            nh = np.full((n, n), -1, dtype=np.int64)
+            off = ~np.eye(n, dtype=bool)
+            nh[off] = np.tile(np.arange(n), (n, 1))[off]
+            via = np.full((n, n), -1, dtype=np.int64)
+        else:
+            if rt.n_gpus != n:
+                raise ValueError(f"routing table covers {rt.n_gpus} GPUs, partition has {n}")
+            nh = rt.next_hop_matrix()
+            via = np.full((n, n), -1, dtype=np.int64)
+            via[rt.src, rt.dst] = rt.via
+        fwd = np.zeros((n, n), dtype=np.int64)
+        for s in range(n):
+            for d in range(n):
+                if via[s, d] >= 0:
+                    fwd[via[s, d], s] |= 1 << d
+        self.n = n
+        self.next_hop = nh
+        self.fwd = fwd
+        self.two_level = bool((via >= 0).any())
+
+    def hop_masks(self, dest, shard: int):
+        """Per-neuron next-hop bitmask (int16) from its destination mask."""
+        import torch
+        hm = torch.zeros_like(dest)
+        for d in range(self.n):
+            if d == shard:
+                continue
+            bit = (dest >> d) & 1
+            h = int(self.next_hop[shard, d])
+            if h < 0:
+                if bool(bit.any()):
+                    raise ValueError(
+                        f"neurons on GPU {shard} target GPU {d} but the routing table has no demand ({shard}, {d})"
+                    )
+                continue
+            hm |= bit << h
+        return _as_u16(hm)
+
+    def fwd_table_u16(self) -> np.ndarray:
+        return np.ascontiguousarray(self.fwd.astype(np.uint16).reshape(-1))
+
+
+# ---------------------------------------------------------------- simulator
+
+@dataclass
+class SimReport:
+    """Outputs of :func:`simulate` (host numpy unless noted)."""
+
+    steps: int
+    n_gpus: int
+    raster: np.ndarray | None          # bool [recorded steps, M] in global neuron ids
+    deliv_ids: np.ndarray              # int64 [steps or 1, N, N]: ids of s delivered to d
+    hop_ids: np.ndarray                # int64 [steps or 1, N, N]: ids on channel u->v
+    spikes: int                        # total spikes
+    v: np.ndarray | None               # final membrane voltage per gid
+    i_syn: np.ndarray | None
+    elapsed_ms: float                  # device time of the step loop (CUDA events)
+    exchange: str = "none"
+    delivery: str = "fused"
+    extra: dict = field(default_factory=dict)
+
+    @property
+    def steps_per_s(self) -> float:
+        return self.steps / (self.elapsed_ms * 1e-3) if self.elapsed_ms > 0 else float("inf")
+
+    def spike_ids(self, t: int) -> np.ndarray:
+        return np.flatnonzero(self.raster[t])
+
+    def rate_hz(self, dt_ms: float = 1.0) -> float:
+        m = self.v.size if self.v is not None else 0
+        return self.spikes / max(m, 1) / (self.steps * dt_ms * 1e-3) if m else float("nan")
+
+
+class _ShardState:
+    """Device buffers and the C descriptor of one shard."""
+
+    def __init__(self, net: Network, h: int, plan: ExchangePlan, *, record_steps: int, push: bool,
+                 bucket_cap: int | None):
+        import torch
+        lay = net.layout
+        dev = net.device
+        n_local = lay.n_local(h)
+        nl = max(n_local, 1)
+        self.h = h
+        self.n_local = n_local
+        self.local_words = (n_local + 31) // 32
+        csr = net.shards[h]
+        self.csr = csr
+        self.v = torch.zeros(nl, dtype=torch.float32, device=dev)
+        self.i_syn = torch.zeros(nl, dtype=torch.float32, device=dev)
+        self.refrac = torch.zeros(nl, dtype=torch.uint8, device=dev)
+        self.acc = torch.zeros(nl, dtype=torch.int32, device=dev)
+        self.gid = torch.from_numpy(lay.members[h].astype(np.int32)).to(dev) if n_local else \
+            torch.zeros(1, dtype=torch.int32, device=dev)
+        self.hop_mask = plan.hop_masks(csr.dest, h) if (lay.n_shards > 1 and n_local) else \
+            torch.zeros(nl, dtype=torch.int16, device=dev)
+        self.bitmaps = torch.zeros((2, lay.n_words), dtype=torch.int32, device=dev)
+        n = lay.n_shards
+        if n > 1 and n_local:
+            hm = self.hop_mask.to(torch.int32) & 0xFFFF
+            per_hop = torch.stack([((hm >> k) & 1).sum() for k in range(n)]).cpu().numpy()
+            cap = int(per_hop.max()) if per_hop.size else 1
+        else:
+            cap = 1
+        if bucket_cap is not None:
+            cap = min(cap, int(bucket_cap))
+        self.bucket_cap = max(cap, 1)
+        self.bucket_ids = torch.zeros(n * self.bucket_cap, dtype=torch.int32, device=dev)
+        self.bucket_count = torch.zeros(n, dtype=torch.int32, device=dev)
+        self.status = torch.zeros(2, dtype=torch.int32, device=dev)
+        self.step = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.record_steps = int(record_steps)
+        self.raster = torch.zeros((max(self.record_steps, 1), max(self.local_words, 1)), dtype=torch.int32,
+                                  device=dev)
+        self.spike_total = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.push_rowptr = self.push_syn = None
+        if push:
+            self.push_rowptr, self.push_syn = _push_csr(csr, lay, h, dev)
+        self.c = _native.ShardC(
+            shard=h, n_shards=n, n_local=n_local, local_base=int(lay.base[h]), n_words=lay.n_words, pad0=0,
+            v=self.v.data_ptr(), i_syn=self.i_syn.data_ptr(), refrac=self.refrac.data_ptr(),
+            acc=self.acc.data_ptr(), gid=self.gid.data_ptr(), hop_mask=self.hop_mask.data_ptr(),
+            rowptr4=csr.rowptr4.data_ptr(), syn=csr.syn.data_ptr(),
+            push_rowptr=None if self.push_rowptr is None else self.push_rowptr.data_ptr(),
+            push_syn=None if self.push_syn is None else self.push_syn.data_ptr(),
+            bitmap0=self.bitmaps[0].data_ptr(), bitmap1=self.bitmaps[1].data_ptr(),
+            fired_ids=None, fired_count=None,
+            bucket_ids=self.bucket_ids.data_ptr(), bucket_count=self.bucket_count.data_ptr(),
+            bucket_cap=self.bucket_cap, status=self.status.data_ptr(), step=self.step.data_ptr(),
+            raster=self.raster.data_ptr() if self.record_steps > 0 else None,
+            record_steps=self.record_steps, local_words=self.local_words,
+            spike_total=self.spike_total.data_ptr())
+
+
+def _push_csr(csr: ShardCSR, lay: ShardLayout, h: int, dev):
+    """Transpose of the pull CSR: rows = internal pre ids, entries = (post_local << 6) | flags."""
+    import torch
+    n_local = lay.n_local(h)
+    rp4 = csr.rowptr4
+    total = int(rp4[-1].item()) * 4
+    syn = csr.syn[:total].to(torch.int64) & 0xFFFFFFFF
+    lens4 = (rp4[1:] - rp4[:-1]) * 4
+    post = torch.repeat_interleave(torch.arange(n_local, device=dev, dtype=torch.int64), lens4)
+    keep = syn != lay.pad_entry
+    syn, post = syn[keep], post[keep]
+    pre = syn >> PAD_Q_BITS
+    flags = syn & 63
+    order = torch.argsort(pre, stable=True)
+    pre, post, flags = pre[order], post[order], flags[order]
+    n_rows = lay.n_words * 32
+    rowptr = torch.zeros(n_rows + 1, dtype=torch.int64, device=dev)
+    rowptr[1:] = torch.cumsum(torch.bincount(pre, minlength=n_rows), 0)
+    ent = (post << PAD_Q_BITS) | flags
+    ent = torch.where(ent >= 2**31, ent - 2**32, ent).to(torch.int32)
+    return rowptr, ent
+
+
+class Simulator:
+    """Runs the step loop for the shards this process owns (all of them, on one device)."""
+
+    def __init__(self, net: Network, lif: LifParams = LifParams(), seed: int = 0, rt: RoutingTable | None = None,
+                 *, delivery: str = "fused", record_raster_steps: int = 0, per_step_counts: bool = False,
+                 bucket_cap: int | None = None, use_graph: bool = True, graph_chunk: int = 64):
+        import torch
+        if delivery not in ("fused", "push", "pull"):
+            raise ValueError(f"delivery must be 'fused', 'pull' or 'push', got {delivery!r}")
+        if set(net.shards) != set(range(net.layout.n_shards)):
+            raise ValueError("the single-process simulator needs every shard of the layout")
+        self.net = net
+        self.lif = lif
+        self.seed = seed
+        self.delivery = delivery
+        self.plan = ExchangePlan(net.layout.n_shards, rt)
+        self.c_lif = lif.to_c(seed)
+        self.lib = _native.lib()
+        self.n = net.layout.n_shards
+        self.per_step_counts = per_step_counts
+        self.use_graph = use_graph
+        self.graph_chunk = graph_chunk
+        self.record_steps = int(record_raster_steps)
+        self.states = [
+            _ShardState(net, h, self.plan, record_steps=self.record_steps, push=(delivery == "push"),
+                        bucket_cap=bucket_cap)
+            for h in range(self.n)
+        ]
+        dev = net.device
+        self.dest_global = net.global_dest() if self.n > 1 else torch.zeros(1, dtype=torch.int16, device=dev)
+        self.fwd_table = self.plan.fwd_table_u16()
+        self.fwd_cap = max(s.bucket_cap for s in self.states) * (self.n if self.plan.two_level else 1)
+        self.fwd_ids = torch.zeros(self.n * self.n * self.fwd_cap if self.plan.two_level else 1, dtype=torch.int32,
+                                   device=dev)
+        self.fwd_count = torch.zeros(self.n * self.n, dtype=torch.int32, device=dev)
+        self.shard_array = (_native.ShardC * self.n)(*[s.c for s in self.states])
+        self._counter_steps = 0
+        self.hop_ids = None
+        self.deliv_ids = None
+        self._graph = None
+        self._graph_len = 0
+        self._check(self.lib.nc_sim_prepare(), "prepare")
+
+    def _check(self, rc, what):
+        _native.check(rc, what)
+
+    def reset(self, counter_steps: int):
+        """Initial state and zeroed counters sized for `counter_steps` recorded steps."""
+        import torch
+        st = _native.stream_handle(self.net.device)
+        for s in self.states:
+            self._check(self.lib.nc_sim_init(C.byref(s.c), C.byref(self.c_lif), st), "sim init")
+            s.raster.zero_()
+        rows = counter_steps if self.per_step_counts else 1
+        self._counter_steps = rows
+        self.hop_ids = torch.zeros((rows, self.n, self.n), dtype=torch.int64, device=self.net.device)
+        self.deliv_ids = torch.zeros((rows, self.n, self.n), dtype=torch.int64, device=self.net.device)
+        self.fwd_count.zero_()
+        self._graph = None
+
+    def _one_step(self, st):
+        L = self.lib
+        lif = C.byref(self.c_lif)
+        if self.delivery == "fused":
+            for s in self.states:
+                self._check(L.nc_sim_step_fused(C.byref(s.c), lif, st), "step")
+        else:
+            for s in self.states:
+                if self.delivery == "push":
+                    self._check(L.nc_sim_deliver_push(C.byref(s.c), self.c_lif.g_inh, st), "deliver push")
+                else:
+                    self._check(L.nc_sim_deliver_pull(C.byref(s.c), self.c_lif.g_inh, st), "deliver pull")
+                self._check(L.nc_sim_lif_update(C.byref(s.c), lif, st), "lif update")
+        if self.n > 1:
+            self._check(L.nc_exchange_local(self.shard_array, self.n, self.dest_global.data_ptr(),
+                                            self.fwd_table.ctypes.data, self.fwd_ids.data_ptr(),
+                                            self.fwd_count.data_ptr(), self.fwd_cap, self.hop_ids.data_ptr(),
+                                            self.deliv_ids.data_ptr(), 1 if self.per_step_counts else 0, st),
+                        "exchange")
+        for s in self.states:
+            self._check(L.nc_sim_end_step(C.byref(s.c), st), "end step")
+
+    def launches_per_step(self) -> int:
+        per_shard = 2 if self.delivery == "fused" else 3
+        ex = 0
+        if self.n > 1:
+            ex = 3 if self.plan.two_level else 1
+        return per_shard * self.n + ex
+
+    def advance_eager(self, steps: int):
+        """Enqueue `steps` steps as plain launches on the current stream."""
+        st = _native.stream_handle(self.net.device)
+        for _ in range(steps):
+            self._one_step(st)
+
+    def advance(self, steps: int):
+        """Enqueue `steps` steps on the current stream (graph-replayed in chunks)."""
+        import torch
+        if not self.use_graph:
+            self.advance_eager(steps)
+            return
+        done = 0
+        while done < steps:
+            k = min(self.graph_chunk, steps - done)
+            if self._graph is None or self._graph_len != k:
+                g = torch.cuda.CUDAGraph()
+                side = torch.cuda.Stream(self.net.device)
+                side.wait_stream(torch.cuda.current_stream(self.net.device))
+                with torch.cuda.stream(side):
+                    g.capture_begin()
+                    cst = _native.stream_handle(self.net.device)
+                    for _ in range(k):
+                        self._one_step(cst)
+                    g.capture_end()
+                torch.cuda.current_stream(self.net.device).wait_stream(side)
+                self._graph, self._graph_len = g, k
+            self._graph.replay()
+            done += k
+
+    def check_status(self):
+        for s in self.states:
+            flags = s.status.cpu().tolist()
+            if flags[0]:
+                raise RuntimeError(f"spike bucket overflow on shard {s.h}: raise bucket_cap")
+            if flags[1]:
+                raise RuntimeError(f"exchange watchdog expired on shard {s.h}")
+
+    def run(self, steps: int, *, warmup_graph: bool = True) -> SimReport:
+        import torch
+        if steps < 0:
+            raise ValueError("steps must be >= 0")
+        self.reset(steps if self.per_step_counts else 1)
+        if self.record_steps and self.record_steps < steps:
+            raise ValueError("record_raster_steps is smaller than the number of steps")
+        torch.cuda.synchronize(self.net.device)
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        self.advance(steps)
+        t1.record()
+        torch.cuda.synchronize(self.net.device)
+        self.check_status()
+        return self.report(steps, t0.elapsed_time(t1))
+
+    def report(self, steps: int, elapsed_ms: float) -> SimReport:
+        lay = self.net.layout
+        raster = None
+        if self.record_steps:
+            raster = np.zeros((steps, lay.n_neurons), dtype=bool)
+            for s in self.states:
+                if not s.n_local:
+                    continue
+                words = s.raster[:steps, : s.local_words].cpu().numpy().view(np.uint32)
+                bits = (words[:, :, None] >> np.arange(32, dtype=np.uint32)) & np.uint32(1)
+                bits = bits.reshape(steps, -1)[:, : s.n_local]
+                raster[:, lay.members[s.h]] = bits.astype(bool)
+        v = np.zeros(lay.n_neurons, dtype=np.float32)
+        i = np.zeros(lay.n_neurons, dtype=np.float32)
+        spikes = 0
+        for s in self.states:
+            if s.n_local:
+                v[lay.members[s.h]] = s.v[: s.n_local].cpu().numpy()
+                i[lay.members[s.h]] = s.i_syn[: s.n_local].cpu().numpy()
+            spikes += int(s.spike_total.item())
+        hop = self.hop_ids.cpu().numpy()
+        deliv = self.deliv_ids.cpu().numpy()
+        if not self.per_step_counts:
+            hop, deliv = hop[:1], deliv[:1]
+        mode = "none" if self.n == 1 else ("two-level" if self.plan.two_level else "direct")
+        return SimReport(steps=steps, n_gpus=self.n, raster=raster, deliv_ids=deliv, hop_ids=hop, spikes=spikes,
+                         v=v, i_syn=i, elapsed_ms=elapsed_ms, exchange=mode, delivery=self.delivery)
+
+
+# ---------------------------------------------------------------- public API
+
+def simulate(graph: NeuronGraph, pm, rt: RoutingTable | None, steps: int, lif: LifParams = LifParams(),
+             seed: int = 0, *, delivery: str = "fused", record: tuple = ("raster", "counts"),
+             use_graph: bool = True, device=None) -> SimReport:
+    """Simulate `steps` 1-ms steps of the LIF network on the reference's partition and routes.
+
+    ``graph``/``pm``/``rt`` are the reference pipeline's outputs
+    (generate_synthetic -> partition_greedy -> build_routing_table or route_p2p).
+    ``rt=None`` means direct routing.  All partitions run on the current CUDA
+    device with the local exchange transport; use :mod:`.distributed` for one
+    process per GPU.
+    """
+    if steps < 0:
+        raise ValueError(f"steps must be >= 0, got {steps}")
+    if pm.assignment.size != graph.n_neurons:
+        raise ValueError(f"partition map covers {pm.assignment.size} neurons, graph has {graph.n_neurons}")
+    layout = ShardLayout.from_assignment(pm.assignment, pm.n_gpus)
+    net = Network.from_graph(graph, layout, device=device, inh_every=lif.inh_every)
+    sim = Simulator(net, lif, seed, rt, delivery=delivery,
+                    record_raster_steps=steps if "raster" in record else 0,
+                    per_step_counts="counts" in record, use_graph=use_graph)
+    return sim.run(steps)

@@ -1,0 +1,180 @@
+"""GPU-level traffic aggregation (the partitioner's edge-cut matrix) on the GPU.
+
+Drop-in for ``neurocomm/traffic.py``.  ``aggregate`` (traffic.py:66-84) runs
+the K5 histogram kernel (csrc/traffic_hist.cu): every contribution
+``(p*W_i)*W_j`` is added exactly into fixed-point limbs, and each cell is
+rounded once on the host (:func:`.accum.limbs_to_float`), which equals the
+reference's per-cell ``math.fsum`` bit for bit.  The N x N reports around it
+stay on the host; they touch at most a few hundred numbers.
+"""
+
+from __future__ import annotations
+
+import csv
+import json
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .accum import limbs_to_float
+
+__all__ = [
+    "GpuTrafficGraph", "TrafficReport", "report_from_vector", "aggregate", "per_gpu_send_traffic",
+    "peak_reduction", "write_traffic_csv", "read_traffic_csv", "write_traffic_summary",
+    "exact_bin_sums",
+]
+
+INT_MAX = 2**31 - 1
+INT_MIN = -(2**31)
+
+
+@dataclass(eq=False)
+class GpuTrafficGraph:
+    """Symmetric N x N traffic (diagonal = intra-GPU) plus per-GPU weight (traffic.py:27-42)."""
+
+    n_gpus: int
+    pg: np.ndarray
+    wg: np.ndarray
+
+    def __eq__(self, other) -> bool:
+        if not isinstance(other, GpuTrafficGraph):
+            return NotImplemented
+        return (self.n_gpus == other.n_gpus and np.array_equal(self.pg, other.pg)
+                and np.array_equal(self.wg, other.wg))
+
+
+@dataclass(eq=False)
+class TrafficReport:
+    """Per-GPU send traffic with max / mean / population std (traffic.py:45-56)."""
+
+    per_gpu_send: np.ndarray
+    peak: float
+    mean: float
+    stddev: float
+
+    @property
+    def n_gpus(self) -> int:
+        return int(self.per_gpu_send.size)
+
+
+def report_from_vector(values) -> TrafficReport:
+    v = np.asarray(values, dtype=np.float64)
+    if v.size == 0:
+        return TrafficReport(v, 0.0, 0.0, 0.0)
+    return TrafficReport(v, float(np.max(v)), float(np.mean(v)), float(np.std(v)))
+
+
+def _device():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("traffic aggregation runs on the GPU (K5 histogram); no CUDA device is visible")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _n_digits(lsb: int, msb: int, n_terms: int) -> int:
+    bits = (msb - lsb + 1) + max(1, int(n_terms).bit_length()) + 1
+    return (bits + 31) // 32 + 2
+
+
+def exact_bin_sums(values_dev, keys_dev, n_bins: int, *, pairs=None, stream=None):
+    """Correctly rounded per-bin sums on the device.
+
+    ``pairs=None``: bin ``keys[k]`` receives ``values[k]`` (binned_sums).
+    ``pairs=(ei, ej, ep)``: edge mode -- values are the neuron weights, keys
+    the assignment, and cell ``min*N+max`` receives ``(ep*w[ei])*w[ej]``.
+    Returns a float64 numpy array of ``n_bins`` (or ``n_bins**2``) cells.
+    """
+    import torch
+    L = _native.lib()
+    st = stream if stream is not None else _native.stream_handle()
+    dev = values_dev.device
+    mm = torch.tensor([INT_MAX, INT_MIN], dtype=torch.int32, device=dev)
+    if pairs is None:
+        n = int(values_dev.numel())
+        _native.check(L.nc_traffic_exponents(None, None, None, values_dev.data_ptr(), n, mm.data_ptr(), st),
+                      "weight exponents")
+    else:
+        ei, ej, ep = pairs
+        n = int(ei.numel())
+        _native.check(L.nc_traffic_exponents(ei.data_ptr(), ej.data_ptr(), ep.data_ptr(), values_dev.data_ptr(),
+                                             n, mm.data_ptr(), st), "traffic exponents")
+    n_cells = n_bins * n_bins if pairs is not None else n_bins
+    lo, hi = mm.cpu().tolist()
+    if n == 0 or lo == INT_MAX:
+        return np.zeros(n_cells, dtype=np.float64)
+    nd = _n_digits(lo, hi, n)
+    limbs = torch.zeros((n_cells, nd), dtype=torch.int64, device=dev)
+    if pairs is None:
+        rc = L.nc_weight_histogram(values_dev.data_ptr(), keys_dev.data_ptr(), n, n_bins, lo, nd,
+                                   limbs.data_ptr(), st)
+    else:
+        rc = L.nc_traffic_histogram(ei.data_ptr(), ej.data_ptr(), ep.data_ptr(), values_dev.data_ptr(),
+                                    keys_dev.data_ptr(), n, n_bins, lo, nd, limbs.data_ptr(), st)
+    _native.check(rc, "traffic histogram")
+    host = limbs.cpu().numpy().view(np.uint64)
+    out = np.zeros(n_cells, dtype=np.float64)
+    for c in np.flatnonzero(host.any(axis=1)).tolist():
+        out[c] = limbs_to_float(host[c].tolist(), lo)
+    return out
+
+
+def aggregate(graph, pm) -> GpuTrafficGraph:
+    """Collapse neuron traffic onto GPUs (traffic.py:66-84) with the K5 kernel."""
+    import torch
+    if pm.assignment.size != graph.n_neurons:
+        raise ValueError(
+            f"partition map covers {pm.assignment.size} neurons, graph has {graph.n_neurons}"
+        )
+    n = int(pm.n_gpus)
+    dev = _device()
+    w = torch.from_numpy(np.ascontiguousarray(graph.weights, dtype=np.float64)).to(dev)
+    asg = torch.from_numpy(np.ascontiguousarray(pm.assignment, dtype=np.int64)).to(dev)
+    ei = torch.from_numpy(np.ascontiguousarray(graph.edge_i, dtype=np.int64)).to(dev)
+    ej = torch.from_numpy(np.ascontiguousarray(graph.edge_j, dtype=np.int64)).to(dev)
+    ep = torch.from_numpy(np.ascontiguousarray(graph.edge_p, dtype=np.float64)).to(dev)
+    cells = exact_bin_sums(w, asg, n, pairs=(ei, ej, ep)).reshape(n, n)
+    upper = np.triu(cells)
+    pg = upper + np.triu(cells, 1).T
+    wg = exact_bin_sums(w, asg, n)
+    return GpuTrafficGraph(n, pg, wg)
+
+
+def per_gpu_send_traffic(gt: GpuTrafficGraph) -> TrafficReport:
+    """Off-diagonal row fsums (traffic.py:87-95)."""
+    send = np.array([math.fsum(np.delete(gt.pg[a], a)) for a in range(gt.n_gpus)], dtype=np.float64)
+    return report_from_vector(send)
+
+
+def peak_reduction(baseline: TrafficReport, candidate: TrafficReport) -> float:
+    """Percent drop of the candidate peak below the baseline peak (traffic.py:98-106)."""
+    if baseline.n_gpus != candidate.n_gpus:
+        raise ValueError(
+            f"reports cover different GPU counts: {baseline.n_gpus} vs {candidate.n_gpus}"
+        )
+    if baseline.peak == 0.0:
+        raise ValueError("baseline peak is zero; reduction is undefined")
+    return 100.0 * (baseline.peak - candidate.peak) / baseline.peak
+
+
+def write_traffic_csv(report: TrafficReport, destination, value_column: str = "send_traffic") -> None:
+    with open(destination, "w", newline="") as fh:
+        out = csv.writer(fh, lineterminator="\n")
+        out.writerow(["gpu", value_column])
+        out.writerows([g, repr(v)] for g, v in enumerate(report.per_gpu_send.tolist()))
+
+
+def read_traffic_csv(source) -> TrafficReport:
+    with open(source, newline="") as fh:
+        rows = list(csv.reader(fh))
+    if not rows or len(rows[0]) != 2 or rows[0][0] != "gpu":
+        raise ValueError(f"unexpected traffic CSV header in {source}")
+    return report_from_vector([float(r[1]) for r in rows[1:]])
+
+
+def write_traffic_summary(report: TrafficReport, destination) -> None:
+    doc = {"peak": report.peak, "mean": report.mean, "stddev": report.stddev, "n_gpus": report.n_gpus}
+    with open(destination, "w", newline="\n") as fh:
+        json.dump(doc, fh, indent=2, sort_keys=True)
+        fh.write("\n")

@@ -1,0 +1,227 @@
+"""GPU parity: the CUDA engine against the CPU oracle and the reference fixtures.
+
+* K5 aggregate: pg / wg bit-equal to the reference's fsum results.
+* simulate(): per-step rasters, per-pair delivered and per-hop id counts and
+  the final V / I bit-equal to oracle/sim_oracle.c, for 1, 2 and 4 partitions,
+  direct and two-level routing, fused / pull / push delivery.
+* the device graph generator: its CSR read back drives the oracle to the same
+  rasters, and its edge count matches the SBM expectation.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_2205_07125_b200 as nc
+from paper_2205_07125_b200 import sim as S
+from oracle import c_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+_graphs: dict = {}
+
+
+def graph(name, idx=None, **spec):
+    key = name
+    if key not in _graphs:
+        _graphs[key] = nc.generate_synthetic(nc.ModelSpec(**spec))
+    return _graphs[key]
+
+
+def cfg1(seed=1):
+    return graph(f"cfg1_{seed}", n_neurons=10_000, n_communities=1, p_in=100 / 9_999, p_out=0.0, seed=seed)
+
+
+# ------------------------------------------------------------------ K5
+
+def test_aggregate_bit_identical_to_reference(ref_fixtures):
+    idx, arr = ref_fixtures
+    for case in idx["cases"]:
+        g = graph(case["graph"], **idx["graphs"][case["graph"]]["spec"])
+        pm = nc.partition_greedy(g, case["n_gpus"], nc.PartitionConfig(balance_slack=case["slack"]))
+        gt = nc.aggregate(g, pm)
+        np.testing.assert_array_equal(gt.pg.view(np.uint64), arr[f"{case['key']}/pg"].view(np.uint64),
+                                      err_msg=case["key"])
+        np.testing.assert_array_equal(gt.wg.view(np.uint64), arr[f"{case['key']}/wg"].view(np.uint64))
+        rnd = nc.partition_random(g, case["n_gpus"], seed=case["random_seed"])
+        np.testing.assert_array_equal(nc.aggregate(g, rnd).pg, arr[f"{case['key']}/pg_random"])
+        assert nc.cross_traffic(g, pm).hex() == case["cross_traffic"]
+
+
+def test_aggregate_order_independent_and_wide_exponents():
+    rng = np.random.default_rng(3)
+    m, e = 300, 4000
+    i = rng.integers(0, m - 1, e)
+    j = np.minimum(i + 1 + rng.integers(0, 50, e), m - 1)
+    keep = i < j
+    key = np.unique(i[keep] * m + j[keep])
+    ei, ej = key // m, key % m
+    p = rng.uniform(1e-6, 1.0, ei.size)
+    w = np.exp(rng.uniform(-30, 30, m))  # ~2^87 dynamic range
+    g = nc.NeuronGraph(m, w, ei, ej, p)
+    pm = nc.PartitionMap(4, rng.integers(0, 4, m))
+    gt = nc.aggregate(g, pm)
+    perm = rng.permutation(ei.size)
+    gt2 = nc.aggregate(nc.NeuronGraph(m, w, ei[perm], ej[perm], p[perm]), pm)
+    np.testing.assert_array_equal(gt.pg, gt2.pg)
+    # correctly rounded: equal to fsum per cell
+    import math
+    a, b = pm.assignment[ei], pm.assignment[ej]
+    c = p * w[ei] * w[ej]
+    for x in range(4):
+        for y in range(x, 4):
+            sel = (np.minimum(a, b) == x) & (np.maximum(a, b) == y)
+            assert gt.pg[x, y] == math.fsum(c[sel])
+    assert all(gt.wg[x] == math.fsum(w[pm.assignment == x]) for x in range(4))
+
+
+# ------------------------------------------------------------------ simulate
+
+def oracle_run(g, pm, rt, lif, seed, steps):
+    q = S.q_from_p(g.edge_p)
+    rp, col, qq = c_oracle.symmetric_csr(g.n_neurons, g.edge_i, g.edge_j, q)
+    n = pm.n_gpus
+    nh = rt.next_hop_matrix() if rt is not None else S.ExchangePlan(n, None).next_hop
+    return c_oracle.simulate_csr(rp, col, qq, pm.assignment, n, nh, lif.constants(seed), steps, threads=8)
+
+
+def assert_same(rep, ref):
+    np.testing.assert_array_equal(rep.raster, ref["raster"])
+    np.testing.assert_array_equal(rep.v.view(np.uint32), ref["v"].view(np.uint32))
+    np.testing.assert_array_equal(rep.i_syn.view(np.uint32), ref["i"].view(np.uint32))
+    if rep.n_gpus > 1:
+        np.testing.assert_array_equal(rep.deliv_ids, ref["deliv"])
+        np.testing.assert_array_equal(rep.hop_ids, ref["hop"])
+
+
+def routes(g, pm, mode):
+    gt = nc.aggregate(g, pm)
+    if mode == "direct":
+        return nc.route_p2p(gt)
+    groups = nc.group_gpus(gt, 2)
+    return nc.build_routing_table(gt, groups, nc.select_bridges(gt, groups))
+
+
+@pytest.mark.parametrize("n_gpus,mode", [(1, "direct"), (2, "direct"), (4, "direct"), (4, "two-level")])
+def test_config1_simulate_matches_oracle(n_gpus, mode):
+    g = cfg1(1)
+    pm = nc.partition_greedy(g, n_gpus)
+    rt = routes(g, pm, mode) if n_gpus > 1 else None
+    lif = S.LifParams()
+    rep = nc.simulate(g, pm, rt, 100, lif, seed=1)
+    ref = oracle_run(g, pm, rt, lif, 1, 100)
+    assert ref["raster"].sum() > 1000
+    assert_same(rep, ref)
+    if mode == "two-level":
+        assert rep.exchange == "two-level" and rt.bridges == {(0, 1): 0, (1, 0): 2}
+
+
+@pytest.mark.parametrize("delivery", ["pull", "push"])
+def test_delivery_variants_identical(delivery):
+    g = cfg1(2)
+    pm = nc.partition_greedy(g, 4)
+    rt = routes(g, pm, "two-level")
+    lif = S.LifParams(ext_rate_hz=240.0)
+    a = nc.simulate(g, pm, rt, 60, lif, seed=2, delivery="fused")
+    b = nc.simulate(g, pm, rt, 60, lif, seed=2, delivery=delivery)
+    np.testing.assert_array_equal(a.raster, b.raster)
+    np.testing.assert_array_equal(a.v, b.v)
+    np.testing.assert_array_equal(a.hop_ids, b.hop_ids)
+
+
+def test_partition_invariance_and_route_independence():
+    """Rasters do not depend on how many GPUs or which routes carry the spikes."""
+    g = cfg1(3)
+    lif = S.LifParams()
+    base = nc.simulate(g, nc.partition_greedy(g, 1), None, 80, lif, seed=3)
+    for n in (2, 4):
+        pm = nc.partition_greedy(g, n)
+        for mode in ("direct", "two-level"):
+            rep = nc.simulate(g, pm, routes(g, pm, mode), 80, lif, seed=3)
+            np.testing.assert_array_equal(rep.raster, base.raster)
+            np.testing.assert_array_equal(rep.v, base.v)
+    # random placement too
+    pm = nc.partition_random(g, 4, seed=9)
+    rep = nc.simulate(g, pm, routes(g, pm, "direct"), 80, lif, seed=3)
+    np.testing.assert_array_equal(rep.raster, base.raster)
+
+
+def test_graph_replay_equals_eager():
+    g = cfg1(1)
+    pm = nc.partition_greedy(g, 2)
+    rt = routes(g, pm, "direct")
+    a = nc.simulate(g, pm, rt, 70, seed=5, use_graph=True)
+    b = nc.simulate(g, pm, rt, 70, seed=5, use_graph=False)
+    np.testing.assert_array_equal(a.raster, b.raster)
+    np.testing.assert_array_equal(a.deliv_ids, b.deliv_ids)
+
+
+def test_edge_cases_empty_and_tiny():
+    # no edges at all: only the drive acts
+    g = nc.generate_synthetic(nc.ModelSpec(40, 1, 0.0, 0.0, seed=1))
+    pm = nc.partition_greedy(g, 3)
+    rep = nc.simulate(g, pm, None, 30, S.LifParams(ext_rate_hz=300.0), seed=1)
+    ref = oracle_run(g, pm, None, S.LifParams(ext_rate_hz=300.0), 1, 30)
+    assert_same(rep, ref)
+    # a GPU with a single neuron, ragged shards
+    g = nc.generate_synthetic(nc.ModelSpec(33, 2, 0.5, 0.1, 0.5, 3.0, seed=4))
+    pm = nc.PartitionMap(3, np.array([0] * 31 + [1] + [2]))
+    rt = routes(g, pm, "direct")
+    rep = nc.simulate(g, pm, rt, 40, S.LifParams(ext_rate_hz=300.0), seed=2)
+    assert_same(rep, oracle_run(g, pm, rt, S.LifParams(ext_rate_hz=300.0), 2, 40))
+
+
+def test_missing_demand_rejected():
+    g = cfg1(1)
+    pm = nc.partition_greedy(g, 2)
+    gt = nc.GpuTrafficGraph(2, np.zeros((2, 2)), np.ones(2))
+    with pytest.raises(ValueError, match="no demand"):
+        nc.simulate(g, pm, nc.route_p2p(gt), 5)
+
+
+# ------------------------------------------------------------------ device generator
+
+def test_device_generator_matches_oracle_and_statistics():
+    import torch
+    spec = S.GeneratorSpec(12_000, 4, 0.02, 0.002, seed=7)
+    lay = S.ShardLayout.blocks(spec.n_neurons, 2)
+    net = S.Network.generate(spec, lay)
+    # expected undirected edges
+    sizes = nc.model.community_sizes(spec.n_neurons, spec.n_communities)
+    intra = sum(s * (s - 1) // 2 for s in sizes.tolist()) * spec.p_in
+    inter = (spec.n_neurons ** 2 - (sizes ** 2).sum()) / 2 * spec.p_out
+    mean = intra + inter
+    assert abs(net.n_synapses / 2 - mean) < 4 * np.sqrt(mean)
+    # symmetric: every synapse appears in both directions
+    posts, pres, qs = [], [], []
+    for h in range(2):
+        post, pre, q = net.host_csr(h)
+        posts.append(post), pres.append(pre), qs.append(q)
+    post, pre, q = np.concatenate(posts), np.concatenate(pres), np.concatenate(qs)
+    fw = np.stack([post, pre, q]).T
+    bw = np.stack([pre, post, q]).T
+    fw = fw[np.lexsort(fw.T[::-1])]
+    bw = bw[np.lexsort(bw.T[::-1])]
+    np.testing.assert_array_equal(fw, bw)
+    # the same network through the oracle
+    sel = pre > post
+    ei, ej, qq = post[sel], pre[sel], q[sel]
+    rp, col, qc = c_oracle.symmetric_csr(spec.n_neurons, ei, ej, qq)
+    lif = S.LifParams()
+    rt_nh = S.ExchangePlan(2, None).next_hop
+    ref = c_oracle.simulate_csr(rp, col, qc, lay.owner, 2, rt_nh, lif.constants(4), 50, threads=8)
+    sim = S.Simulator(net, lif, 4, None, record_raster_steps=50, per_step_counts=True)
+    rep = sim.run(50)
+    np.testing.assert_array_equal(rep.raster, ref["raster"])
+    np.testing.assert_array_equal(rep.deliv_ids, ref["deliv"])
+    np.testing.assert_array_equal(rep.v, ref["v"])
+    del torch
