@@ -343,7 +343,7 @@ def main() -> int:
     ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"])
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--chunk", type=int, default=100)
-    ap.add_argument("--cpu-steps", type=int, default=3)
+    ap.add_argument("--cpu-steps", type=int, default=10)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
