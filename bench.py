@@ -124,7 +124,9 @@ def run_ours(args) -> dict | None:
     lif = S.LifParams()
     if world > 1:
         from paper_2205_07125_b200 import distributed as D
-        sim = D.DistSimulator(net, lif, args.seed, None, transport=args.transport, delivery=args.delivery)
+        sim = D.DistSimulator(net, lif, args.seed, None, transport=args.transport, delivery=args.delivery,
+                              msg_cap=args.msg_cap, latency_steps=args.warmup + args.steps,
+                              graph_chunk=args.chunk)
     else:
         sim = S.Simulator(net, lif, args.seed, None, delivery=args.delivery, graph_chunk=args.chunk)
     sim.reset(1)
@@ -157,6 +159,9 @@ def run_ours(args) -> dict | None:
         dist.all_reduce(sp)
         spikes = int(sp.item())
     value = args.steps / (ms * 1e-3)
+    lat = None
+    if world > 1:
+        lat = sim.latencies_us(args.warmup + args.steps)[args.warmup:]
 
     # ---- dominant kernel, timed alone on its stream (CUDA events) ----
     st = sim.states[0]
@@ -177,8 +182,11 @@ def run_ours(args) -> dict | None:
     kernel_ms = k0.elapsed_time(k1) / reps
     n_local = lay.n_local(rank)
     csr = net.shards[rank]
-    syn_bytes = csr.n_synapses_padded * 4
-    neuron_bytes = n_local * (8 + 4 + 4 + 4 + 4 + 1 + 1 + 4) + lay.n_words * 4 + n_local // 8
+    # algorithmic bytes of one fused step: 4 B per synapse
+    # + per neuron rowptr 16 (E/I segment starts), V r/w 8, I r/w 8, refrac r/w 2,
+    # gid 4, + the previous spike bitmap read and the new one written
+    syn_bytes = int(net.n_synapses) * 4
+    neuron_bytes = n_local * (16 + 8 + 8 + 2 + 4) + 2 * (lay.n_words * 4)
     alg_bytes = syn_bytes + neuron_bytes
     peaks = load_peaks()
     achieved = alg_bytes / (kernel_ms * 1e-3) / 1e9
@@ -204,7 +212,7 @@ def run_ours(args) -> dict | None:
                 "neurons": n_neurons, "mean_degree": args.degree, "synapses": int(net.n_synapses) * world,
                 "delivery": args.delivery, "exchange": "none" if world == 1 else "direct",
                 "firing_rate_hz": round(spikes / n_neurons / (args.steps * 1e-3), 3),
-                "l2": "inputs larger than L2 (CSR %.2f GB streamed every step)" % (syn_bytes / 1e9),
+                "l2": "inputs larger than L2 (CSR %.2f GB streamed every step)" % (csr.n_synapses_padded * 4 / 1e9),
                 "graph_build_s": round(t_build, 2),
             },
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
@@ -212,12 +220,18 @@ def run_ours(args) -> dict | None:
                          "kernel": "k_step_fused" if args.delivery == "fused" else "k_deliver_push",
                          "kernel_ms": round(kernel_ms, 5), "algorithmic_bytes": int(alg_bytes),
                          "peak_source": peaks["source"]},
+            "exchange_us": None if lat is None else {
+                "p50": round(float(np.percentile(lat, 50)), 2), "p99": round(float(np.percentile(lat, 99)), 2),
+                "transport": args.transport,
+                "what": "device %globaltimer from buckets ready to all inbound spikes in the bitmap, "
+                        "per step max over ranks"},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": args.steps * sim.launches_per_step(),
             "clocks": clocks.summary(),
         }
     if world > 1:
+        sim.close()
         dist.barrier()
         dist.destroy_process_group()
     return result
@@ -226,20 +240,21 @@ def run_ours(args) -> dict | None:
 def gid_csr(net, lay, rank=0):
     """Gid-space CSR of a single-shard network for the CPU oracle (unpacked on the GPU)."""
     import torch
+    from paper_2205_07125_b200.sim import ID_BITS, ID_MASK
     csr = net.shards[rank]
     rp4 = csr.rowptr4
     syn = csr.syn[: int(rp4[-1].item()) * 4].to(torch.int64) & 0xFFFFFFFF
     keep = syn != lay.pad_entry
-    lens = torch.zeros(rp4.numel() - 1, dtype=torch.int64, device=syn.device)
-    rows = torch.repeat_interleave(torch.arange(rp4.numel() - 1, device=syn.device), (rp4[1:] - rp4[:-1]) * 4)
-    lens.index_add_(0, rows[keep], torch.ones_like(rows[keep]))
-    rowptr = torch.zeros(rp4.numel(), dtype=torch.int64, device=syn.device)
+    n_rows = (rp4.numel() - 1) // 2
+    seg = torch.repeat_interleave(torch.arange(2 * n_rows, device=syn.device), (rp4[1:] - rp4[:-1]) * 4)
+    lens = torch.bincount(seg[keep] // 2, minlength=n_rows)
+    rowptr = torch.zeros(n_rows + 1, dtype=torch.int64, device=syn.device)
     rowptr[1:] = torch.cumsum(lens, 0)
     ent = syn[keep]
-    col = (ent >> 6).to(torch.int32)        # single block shard: internal id == gid
-    q = ((ent & 31) + 1).to(torch.uint8)
+    col = (ent & ID_MASK).to(torch.int32)      # single block shard: internal id == gid
+    q = (ent >> ID_BITS).to(torch.uint8)
     out = rowptr.cpu().numpy(), col.cpu().numpy(), q.cpu().numpy()
-    del rows, keep, syn
+    del seg, keep, syn
     torch.cuda.empty_cache()
     return out
 
@@ -340,7 +355,8 @@ def main() -> int:
     ap.add_argument("--neurons", type=int, default=1_000_000, help="neurons per GPU")
     ap.add_argument("--degree", type=float, default=1000.0)
     ap.add_argument("--delivery", default="fused", choices=["fused", "push"])
-    ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"])
+    ap.add_argument("--transport", default="p2p", choices=["nccl", "p2p"])
+    ap.add_argument("--msg-cap", type=int, default=65536, help="ids per exchange message (NCCL sends all of it)")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--chunk", type=int, default=100)
     ap.add_argument("--cpu-steps", type=int, default=10)

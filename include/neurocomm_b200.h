@@ -88,12 +88,15 @@ int nc_weight_histogram(const double* weights, const int64_t* assignment, int64_
  * [local_base, local_base + n_local); bitmaps are indexed by internal id.
  *
  * Synapses: each undirected edge (i, j, p) of NeuronGraph is one synapse in
- * each direction.  A pull-CSR entry of post-row r is a packed uint32
- *     (pre_internal_id << 6) | (inhibitory(pre) << 5) | (q - 1),
- * q = ceil(32 * p) in [1, 32]; its integer weight is q (excitatory pre) or
- * -g_inh * q (inhibitory pre).  Rows are padded to a multiple of 4 entries
- * with NC_PAD_ENTRY, whose pre id is the guard bit that never fires.
- * rowptr4[r] is the row start in units of 4 entries. */
+ * each direction.  A pull-CSR entry is a packed uint32
+ *     (q << 26) | pre_internal_id,      q = ceil(32 * p) in [1, 32],
+ * and every post row r is split into two segments, 2r = excitatory pres
+ * (weight +q) and 2r+1 = inhibitory pres (weight -g_inh * q), so the inner
+ * loop never tests a sign.  Each segment is padded to a multiple of 4 entries
+ * with a pad entry whose pre id is the guard bit that never fires.
+ * rowptr4[s] (2*n_local+1 entries) is the start of segment s in units of
+ * 4 entries.  Push-CSR entries (rows = internal pre ids) are
+ *     (inhibitory(pre) << 31) | ((q - 1) << 26) | post_local. */
 
 #define NC_MAX_SHARDS 16
 #define NC_INTERNAL_ID_BITS 26
@@ -129,9 +132,9 @@ typedef struct nc_shard {
   const uint32_t* gid;    /* global neuron id (Philox counter, raster ids)    */
   const uint16_t* hop_mask; /* bit h: a spike of this neuron is sent to shard h */
   /* pull CSR */
-  const int64_t* rowptr4; /* n_local+1                                         */
+  const int64_t* rowptr4; /* 2*n_local+1 segment starts (E/I per row)          */
   const uint32_t* syn;    /* packed entries                                    */
-  /* push CSR (optional): rows = internal pre ids, entries = (post_local<<6)|(inh<<5)|(q-1) */
+  /* push CSR (optional): rows = internal pre ids, entries see above */
   const int64_t* push_rowptr;
   const uint32_t* push_syn;
   /* spikes */
@@ -196,6 +199,71 @@ int nc_exchange_local(const nc_shard_t* shards, int32_t n_shards, const uint16_t
                       int64_t fwd_cap, long long* hop_ids, long long* deliv_ids, int32_t per_step,
                       void* stream);
 
+/* ------------------------------------------------- multi-GPU exchange --
+ * One process per GPU; rank r owns shard r.  Route semantics as
+ * nc_exchange_local.  Channel masks (bit p = peer p) come from the global
+ * RoutingTable so every rank derives the same send/recv sets:
+ *   send1/recv1: first hops (s -> next_hop(s, d));  send2/recv2: relay hops.
+ * Messages carry at most `cap` ids; more sets status[0] (overflow). */
+typedef struct nc_xchg {
+  int32_t rank, n, cap, two_level;
+  int32_t per_step, lat_steps;
+  uint16_t send1_mask, recv1_mask, send2_mask, recv2_mask;
+  int64_t bucket_cap;              /* stride of the shard's bucket_ids rows     */
+  uint64_t timeout_ns;             /* P2P watchdog                              */
+  const int32_t* step;             /* shard step counter                        */
+  int32_t* status;                 /* shard status words                        */
+  uint32_t* bitmap0;
+  uint32_t* bitmap1;
+  const uint32_t* bucket_ids;      /* shard next-hop buckets                    */
+  const int32_t* bucket_count;
+  const uint16_t* dest_global;     /* dest mask of every internal id            */
+  int64_t shard_base[NC_MAX_SHARDS + 1];
+  uint16_t fwd_row[NC_MAX_SHARDS]; /* as relay: destinations forwarded for src s */
+  uint32_t* fwd_ids;               /* relay buckets [n][cap]                    */
+  int32_t* fwd_count;              /* [n]                                       */
+  long long* hop_ids;              /* [n*n] (or [steps][n*n])                   */
+  long long* deliv_ids;
+  /* NCCL transport buffers */
+  int32_t* send_hdr;
+  int32_t* send2_hdr;
+  int32_t* recv_hdr;
+  int32_t* recv2_hdr;
+  uint32_t* recv_ids;              /* [n][cap] */
+  uint32_t* recv2_ids;
+  /* P2P transport: IPC-mapped inboxes/flags */
+  uint32_t* my_inbox;
+  uint32_t* my_flags;              /* [2][NC_MAX_SHARDS]                        */
+  uint32_t* peer_inbox[NC_MAX_SHARDS];
+  uint32_t* peer_flags[NC_MAX_SHARDS];
+  uint32_t* done;                  /* monotonically counting block exits        */
+  uint32_t* barrier;               /* in-kernel grid barrier counter            */
+  unsigned long long* lat_start;
+  uint32_t* lat_ns;                /* per-step exchange latency (ns) or NULL    */
+} nc_xchg_t;
+
+/* Inbox words needed per rank for the P2P transport. */
+#define NC_P2P_INBOX_WORDS(n, cap) ((size_t)4 * (size_t)(n) * ((size_t)(cap) + 4))
+
+int nc_xchg_reset(const nc_xchg_t* X, void* stream);
+/* NCCL path: seal (headers + hop counters), grouped send/recv, scatter. */
+int nc_xchg_seal(const nc_xchg_t* X, int32_t phase, void* stream);
+int nc_xchg_scatter(const nc_xchg_t* X, int32_t phase, void* stream);
+int nc_nccl_get_unique_id(void* id_out /* 128 bytes */);
+int nc_nccl_comm_init(void** comm_out, int32_t nranks, const void* id /* 128 bytes */, int32_t rank);
+int nc_nccl_comm_destroy(void* comm);
+int nc_nccl_exchange(void* comm, const nc_xchg_t* X, int32_t phase, void* stream);
+/* P2P path: one device-initiated kernel per step (both phases). */
+int nc_xchg_p2p(const nc_xchg_t* X, void* stream);
+/* dst[*step] = %globaltimer (ns) if *step < max_steps: per-step exchange
+ * latency stamps, enqueued before and after the exchange. */
+int nc_stamp(unsigned long long* dst, const int32_t* step, int32_t max_steps, void* stream);
+/* CUDA IPC windows for the P2P inboxes. */
+int nc_ipc_alloc(size_t bytes, void** ptr_out, void* handle_out /* 64 bytes */);
+int nc_ipc_open(const void* handle /* 64 bytes */, void** ptr_out);
+int nc_ipc_close(void* ptr);
+int nc_free(void* ptr);
+
 /* ------------------------------------------------------- network build --
  * Device SBM generator with the distributions of generate_synthetic
  * (model.py:199-253): contiguous near-equal communities, intra pairs
@@ -216,11 +284,12 @@ typedef struct nc_graphgen {
   int32_t inh_every;          /* gid % inh_every == inh_every-1 is inhibitory (0 = none) */
 } nc_graphgen_t;
 
+/* lower_len/upper_len: [2*n_local] entries per segment (zero-initialised). */
 int nc_graphgen_count(const nc_graphgen_t* g, int32_t* lower_len, int32_t* upper_len,
                       void* stream);
 int nc_graphgen_fill(const nc_graphgen_t* g, const int64_t* rowptr4, const int32_t* lower_len,
                      int32_t* lower_fill, uint32_t* syn, void* stream);
-/* Write NC pad entries into [row length, 4*ceil(len/4)) of every local row. */
+/* Write pad entries into [segment length, 4*ceil(len/4)) of every segment. */
 int nc_graphgen_pad(const int64_t* rowptr4, const int32_t* lower_len, const int32_t* upper_len,
                     int32_t n_local, uint32_t pad_entry, uint32_t* syn, void* stream);
 /* Destination masks from a built CSR (the adjacency is symmetric, so the

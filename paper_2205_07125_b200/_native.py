@@ -64,6 +64,25 @@ class GraphGenC(C.Structure):
     ]
 
 
+class XchgC(C.Structure):
+    _fields_ = [
+        ("rank", c_int32), ("n", c_int32), ("cap", c_int32), ("two_level", c_int32),
+        ("per_step", c_int32), ("lat_steps", c_int32),
+        ("send1_mask", C.c_uint16), ("recv1_mask", C.c_uint16), ("send2_mask", C.c_uint16),
+        ("recv2_mask", C.c_uint16),
+        ("bucket_cap", c_int64), ("timeout_ns", c_uint64),
+        ("step", c_void_p), ("status", c_void_p), ("bitmap0", c_void_p), ("bitmap1", c_void_p),
+        ("bucket_ids", c_void_p), ("bucket_count", c_void_p), ("dest_global", c_void_p),
+        ("shard_base", c_int64 * (MAX_SHARDS + 1)), ("fwd_row", C.c_uint16 * MAX_SHARDS),
+        ("fwd_ids", c_void_p), ("fwd_count", c_void_p), ("hop_ids", c_void_p), ("deliv_ids", c_void_p),
+        ("send_hdr", c_void_p), ("send2_hdr", c_void_p), ("recv_hdr", c_void_p), ("recv2_hdr", c_void_p),
+        ("recv_ids", c_void_p), ("recv2_ids", c_void_p),
+        ("my_inbox", c_void_p), ("my_flags", c_void_p),
+        ("peer_inbox", c_void_p * MAX_SHARDS), ("peer_flags", c_void_p * MAX_SHARDS),
+        ("done", c_void_p), ("barrier", c_void_p), ("lat_start", c_void_p), ("lat_ns", c_void_p),
+    ]
+
+
 _SIGS = {
     "nc_abi_version": (c_int32, []),
     "nc_last_error": (C.c_char_p, []),
@@ -86,6 +105,19 @@ _SIGS = {
     "nc_graphgen_pad": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_uint32, c_void_p, c_void_p]),
     "nc_dest_mask_from_csr": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p, c_int32, c_int32, c_void_p,
                                         c_void_p]),
+    "nc_xchg_reset": (c_int32, [C.POINTER(XchgC), c_void_p]),
+    "nc_xchg_seal": (c_int32, [C.POINTER(XchgC), c_int32, c_void_p]),
+    "nc_xchg_scatter": (c_int32, [C.POINTER(XchgC), c_int32, c_void_p]),
+    "nc_xchg_p2p": (c_int32, [C.POINTER(XchgC), c_void_p]),
+    "nc_nccl_get_unique_id": (c_int32, [c_void_p]),
+    "nc_nccl_comm_init": (c_int32, [C.POINTER(c_void_p), c_int32, c_void_p, c_int32]),
+    "nc_nccl_comm_destroy": (c_int32, [c_void_p]),
+    "nc_nccl_exchange": (c_int32, [c_void_p, C.POINTER(XchgC), c_int32, c_void_p]),
+    "nc_ipc_alloc": (c_int32, [C.c_size_t, C.POINTER(c_void_p), c_void_p]),
+    "nc_ipc_open": (c_int32, [c_void_p, C.POINTER(c_void_p)]),
+    "nc_ipc_close": (c_int32, [c_void_p]),
+    "nc_free": (c_int32, [c_void_p]),
+    "nc_stamp": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p]),
 }
 
 _lib = None

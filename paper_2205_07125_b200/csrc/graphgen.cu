@@ -11,9 +11,10 @@
 // Row i enumerates its upper neighbours j > i block by block with geometric
 // skipping (the same sampler as model.py:154-180, in fp64 log1p).  Each edge
 // (i, j) is one synapse in each direction: row i gets pre j, row j gets pre i.
-// Pass 1 counts per-row lengths (upper part directly, lower part with integer
+// Pass 1 counts per-segment lengths (a post row has an excitatory-pre and an
+// inhibitory-pre segment; upper parts directly, lower parts with integer
 // atomics); the host scans the padded lengths into rowptr4; pass 2 regenerates
-// the same edges and writes them: row layout [lower part | upper part | pad].
+// the same edges and writes them: segment layout [lower part | upper part | pad].
 // The order inside the lower part depends on atomic arrival, which is harmless:
 // delivery sums integers, so any order gives the same input.
 
@@ -88,8 +89,8 @@ __device__ __forceinline__ uint32_t is_inh(const nc_graphgen_t& g, int64_t gid) 
   return (g.inh_every > 0 && (gid % g.inh_every) == g.inh_every - 1) ? 1u : 0u;
 }
 
-__device__ __forceinline__ uint32_t pack(uint32_t pre_internal, uint32_t inh, uint32_t q) {
-  return (pre_internal << 6) | (inh << 5) | (q - 1u);
+__device__ __forceinline__ uint32_t pack(uint32_t pre_internal, uint32_t q) {
+  return (q << 26) | pre_internal;
 }
 
 // Visit every upper neighbour j of row i:  f(j, intra).
@@ -123,12 +124,17 @@ __global__ void k_count(const nc_graphgen_t g, int32_t* lower_len, int32_t* uppe
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n_neurons;
        i += (int64_t)gridDim.x * blockDim.x) {
     const bool mine = g.owner[i] == g.shard;
-    int32_t up = 0;
+    const uint32_t inh_i = is_inh(g, i);
+    int32_t up[2] = {0, 0};
     for_each_upper(g, cm, i, [&](int64_t j, bool) {
-      ++up;
-      if (g.owner[j] == g.shard) atomicAdd(lower_len + (g.internal_id[j] - g.local_base), 1);
+      ++up[is_inh(g, j)];
+      if (g.owner[j] == g.shard) atomicAdd(lower_len + 2 * (g.internal_id[j] - g.local_base) + inh_i, 1);
     });
-    if (mine) upper_len[g.internal_id[i] - g.local_base] = up;
+    if (mine) {
+      const int64_t r = g.internal_id[i] - g.local_base;
+      upper_len[2 * r] = up[0];
+      upper_len[2 * r + 1] = up[1];
+    }
   }
 }
 
@@ -140,32 +146,33 @@ __global__ void k_fill(const nc_graphgen_t g, const int64_t* rowptr4, const int3
     const bool mine = g.owner[i] == g.shard;
     const uint32_t iid = (uint32_t)g.internal_id[i];
     const uint32_t inh_i = is_inh(g, i);
-    int64_t out = 0;
+    int64_t out[2] = {0, 0};
     if (mine) {
       const int64_t r = iid - g.local_base;
-      out = rowptr4[r] * 4 + lower_len[r];
+      out[0] = rowptr4[2 * r] * 4 + lower_len[2 * r];
+      out[1] = rowptr4[2 * r + 1] * 4 + lower_len[2 * r + 1];
     }
     for_each_upper(g, cm, i, [&](int64_t j, bool intra) {
       const bool jm = g.owner[j] == g.shard;
       if (!mine && !jm) return;
       const uint32_t q = edge_q(g, i, j, intra);
-      if (mine) syn[out++] = pack((uint32_t)g.internal_id[j], is_inh(g, j), q);
+      if (mine) syn[out[is_inh(g, j)]++] = pack((uint32_t)g.internal_id[j], q);
       if (jm) {
-        const int64_t rj = g.internal_id[j] - g.local_base;
-        const int32_t slot = atomicAdd(lower_fill + rj, 1);
-        syn[rowptr4[rj] * 4 + slot] = pack(iid, inh_i, q);
+        const int64_t seg = 2 * (g.internal_id[j] - g.local_base) + inh_i;
+        const int32_t slot = atomicAdd(lower_fill + seg, 1);
+        syn[rowptr4[seg] * 4 + slot] = pack(iid, q);
       }
     });
   }
 }
 
-// Fill the pad entries [row length, 4*ceil(len/4)) of every local row.
+// Fill the pad entries [segment length, 4*ceil(len/4)) of every segment.
 __global__ void k_pad(const int64_t* rowptr4, const int32_t* lower_len, const int32_t* upper_len,
-                      int32_t n_local, uint32_t pad_entry, uint32_t* syn) {
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_local;
-       r += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t beg = rowptr4[r] * 4 + lower_len[r] + upper_len[r];
-    const int64_t end = rowptr4[r + 1] * 4;
+                      int64_t n_seg, uint32_t pad_entry, uint32_t* syn) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n_seg;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t beg = rowptr4[s] * 4 + lower_len[s] + upper_len[s];
+    const int64_t end = rowptr4[s + 1] * 4;
     for (int64_t k = beg; k < end; ++k) syn[k] = pad_entry;
   }
 }
@@ -178,8 +185,8 @@ __global__ void k_dest_mask(const int64_t* rowptr4, const uint32_t* syn, int32_t
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t r = wid; r < n_local; r += nw) {
     uint32_t m = 0;
-    for (int64_t k = rowptr4[r] * 4 + lane; k < rowptr4[r + 1] * 4; k += 32) {
-      const uint32_t pre = syn[k] >> 6;
+    for (int64_t k = rowptr4[2 * r] * 4 + lane; k < rowptr4[2 * r + 2] * 4; k += 32) {
+      const uint32_t pre = syn[k] & 0x03FFFFFFu;
       // owner: last shard whose base <= pre; the guard id is past every shard
       int s = -1;
       for (int h = 0; h < n_shards; ++h)
@@ -227,8 +234,9 @@ extern "C" int nc_graphgen_fill(const nc_graphgen_t* g, const int64_t* rowptr4, 
 
 extern "C" int nc_graphgen_pad(const int64_t* rowptr4, const int32_t* lower_len, const int32_t* upper_len,
                                int32_t n_local, uint32_t pad_entry, uint32_t* syn, void* stream) {
-  k_pad<<<grid_for(n_local, 256), 256, 0, (cudaStream_t)stream>>>(rowptr4, lower_len, upper_len, n_local,
-                                                                    pad_entry, syn);
+  k_pad<<<grid_for(2 * (int64_t)n_local, 256), 256, 0, (cudaStream_t)stream>>>(rowptr4, lower_len, upper_len,
+                                                                                2 * (int64_t)n_local, pad_entry,
+                                                                                syn);
   NC_LAUNCH_CHECK();
   return NC_OK;
 }

@@ -22,7 +22,7 @@
 namespace {
 
 constexpr int kThreads = 1024;    // one CTA per SM in the smem-bitmap variant
-constexpr int kUnroll = 8;        // uint4 loads in flight per lane per row
+constexpr int kUnroll = 6;        // uint4 loads in flight per lane per row
 constexpr uint32_t kFull = 0xffffffffu;
 
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
@@ -39,26 +39,25 @@ __device__ __forceinline__ uint4 ld_keep(const uint4* p) {
   return r;
 }
 
-// Integer weight of one packed entry if its pre fired, else 0.
-__device__ __forceinline__ int32_t entry_term(uint32_t e, const uint32_t* __restrict__ bm,
-                                              int32_t negg) {
-  const uint32_t word = bm[e >> 11];
-  const uint32_t bit = (word >> ((e >> 6) & 31u)) & 1u;
-  const int32_t q = (int32_t)(e & 31u) + 1;
-  const int32_t w = (e & 32u) ? q * negg : q;
-  return bit ? w : 0;
+// Weight units of one packed entry (q << 26 | pre) if its pre fired, else 0.
+// The funnel shift rotates the bitmap word by the low 5 bits of the entry
+// (= pre & 31), so bit 0 is the pre's spike bit: 5 integer ops per synapse.
+__device__ __forceinline__ int32_t entry_term(uint32_t e, const uint32_t* __restrict__ bm) {
+  const uint32_t word = bm[(e & 0x03FFFFFFu) >> 5];
+  const uint32_t rot = __funnelshift_r(word, word, e);
+  return (rot & 1u) ? (int32_t)(e >> 26) : 0;
 }
 
-__device__ __forceinline__ int32_t quad_term(uint4 e, const uint32_t* __restrict__ bm, int32_t negg) {
-  return entry_term(e.x, bm, negg) + entry_term(e.y, bm, negg) + entry_term(e.z, bm, negg) +
-         entry_term(e.w, bm, negg);
+__device__ __forceinline__ int32_t quad_term(uint4 e, const uint32_t* __restrict__ bm) {
+  return entry_term(e.x, bm) + entry_term(e.y, bm) + entry_term(e.z, bm) + entry_term(e.w, bm);
 }
 
-// Pull sum of one CSR row [beg, end) (uint4 units) by the whole warp.
+// Pull sum of one row by the whole warp: excitatory segment [beg, mid),
+// inhibitory segment [mid, end) (uint4 units); returns sum_E - g * sum_I.
 template <bool kStream>
-__device__ __forceinline__ int32_t row_sum(const uint4* __restrict__ syn4, int64_t beg, int64_t end,
-                                           const uint32_t* __restrict__ bm, int32_t negg, int lane) {
-  int32_t s = 0;
+__device__ __forceinline__ int32_t row_sum(const uint4* __restrict__ syn4, int64_t beg, int64_t mid, int64_t end,
+                                           const uint32_t* __restrict__ bm, int32_t g_inh, int lane) {
+  int32_t se = 0, si = 0;
   for (int64_t k0 = beg + lane; k0 < end; k0 += 32 * kUnroll) {
     uint4 e[kUnroll];
 #pragma unroll
@@ -68,10 +67,16 @@ __device__ __forceinline__ int32_t row_sum(const uint4* __restrict__ syn4, int64
                        : make_uint4(0u, 0u, 0u, 0u);
     }
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u)
-      if (k0 + 32 * u < end) s += quad_term(e[u], bm, negg);
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t k = k0 + 32 * u;
+      if (k < end) {
+        const int32_t t = quad_term(e[u], bm);
+        if (k < mid) se += t;
+        else si += t;
+      }
+    }
   }
-  return __reduce_add_sync(kFull, s);
+  return __reduce_add_sync(kFull, se - g_inh * si);
 }
 
 // Exact LIF step; returns true if the neuron fired.  Operation order is the
@@ -188,22 +193,25 @@ k_step_fused(const nc_shard_t sh, const nc_lif_params_t p) {
   const int lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
   const int ntiles = (sh.n_local + 31) >> 5;
-  const int32_t negg = -p.g_inh;
+  const int32_t g_inh = p.g_inh;
   const uint4* syn4 = reinterpret_cast<const uint4*>(sh.syn);
   uint32_t my_spikes = 0;
 
   for (int tile = blockIdx.x * wpb + (threadIdx.x >> 5); tile < ntiles; tile += gridDim.x * wpb) {
     const int row0 = tile << 5;
     const int nrows = min(32, sh.n_local - row0);
-    const int64_t rp = sh.rowptr4[row0 + min(lane, nrows)];
+    // lane l holds the E and I segment starts of row row0+l; lane nrows the end
+    const int64_t rpe = sh.rowptr4[2 * (row0 + min(lane, nrows))];
+    const int64_t rpi = lane < nrows ? sh.rowptr4[2 * (row0 + lane) + 1] : rpe;
+    const int64_t rp_last = sh.rowptr4[2 * (row0 + nrows)];
     int32_t my_acc = 0;
-    int64_t beg = __shfl_sync(kFull, rp, 0);
     for (int r = 0; r < nrows; ++r) {
-      const int64_t end = __shfl_sync(kFull, rp, r + 1 < 32 ? r + 1 : 31);
-      const int64_t end_row = (r + 1 < 32) ? end : sh.rowptr4[row0 + 32];
-      const int32_t s = row_sum<true>(syn4, beg, end_row, bm, negg, lane);
+      const int64_t beg = __shfl_sync(kFull, rpe, r);
+      const int64_t mid = __shfl_sync(kFull, rpi, r);
+      const int64_t nxt = __shfl_sync(kFull, rpe, r + 1 < 32 ? r + 1 : 31);
+      const int64_t end = (r + 1 < nrows) ? nxt : rp_last;
+      const int32_t s = row_sum<true>(syn4, beg, mid, end, bm, g_inh, lane);
       if (lane == r) my_acc = s;
-      beg = end_row;
     }
     const int row = row0 + lane;
     bool fired = false;
@@ -224,7 +232,7 @@ k_step_fused(const nc_shard_t sh, const nc_lif_params_t p) {
 
 // K3 alone: acc[r] = pull sum.
 template <bool kSmemBitmap>
-__global__ void __launch_bounds__(kThreads, 1) k_deliver_pull(const nc_shard_t sh, int32_t negg) {
+__global__ void __launch_bounds__(kThreads, 1) k_deliver_pull(const nc_shard_t sh, int32_t g_inh) {
   extern __shared__ uint4 smem4[];
   const int step = *sh.step;
   const uint32_t* prev = ((step - 1) & 1) ? sh.bitmap1 : sh.bitmap0;
@@ -239,7 +247,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_deliver_pull(const nc_shard_t s
   const int wpb = blockDim.x >> 5;
   const uint4* syn4 = reinterpret_cast<const uint4*>(sh.syn);
   for (int row = blockIdx.x * wpb + (threadIdx.x >> 5); row < sh.n_local; row += gridDim.x * wpb) {
-    const int32_t s = row_sum<true>(syn4, sh.rowptr4[row], sh.rowptr4[row + 1], bm, negg, lane);
+    const int32_t s = row_sum<true>(syn4, sh.rowptr4[2 * row], sh.rowptr4[2 * row + 1], sh.rowptr4[2 * row + 2],
+                                    bm, g_inh, lane);
     if (lane == 0) sh.acc[row] = s;
   }
 }
@@ -293,8 +302,8 @@ __global__ void __launch_bounds__(256) k_deliver_push(const nc_shard_t sh, int32
       const int64_t beg = sh.push_rowptr[pre], end = sh.push_rowptr[pre + 1];
       for (int64_t e = beg + lane; e < end; e += 32) {
         const uint32_t x = sh.push_syn[e];
-        const int32_t q = (int32_t)(x & 31u) + 1;
-        atomicAdd(sh.acc + (x >> 6), (x & 32u) ? q * negg : q);
+        const int32_t q = (int32_t)((x >> 26) & 31u) + 1;
+        atomicAdd(sh.acc + (x & 0x03FFFFFFu), (x >> 31) ? q * negg : q);
       }
     }
   }
@@ -405,9 +414,9 @@ extern "C" int nc_sim_deliver_pull(const nc_shard_t* sh, int32_t g_inh, void* st
     if (!g_prepared) {
       if (int e = nc_sim_prepare()) return e;
     }
-    k_deliver_pull<true><<<grid, kThreads, smem, (cudaStream_t)stream>>>(*sh, -g_inh);
+    k_deliver_pull<true><<<grid, kThreads, smem, (cudaStream_t)stream>>>(*sh, g_inh);
   } else {
-    k_deliver_pull<false><<<grid, kThreads, 0, (cudaStream_t)stream>>>(*sh, -g_inh);
+    k_deliver_pull<false><<<grid, kThreads, 0, (cudaStream_t)stream>>>(*sh, g_inh);
   }
   NC_LAUNCH_CHECK();
   return NC_OK;

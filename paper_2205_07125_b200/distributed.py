@@ -1,0 +1,401 @@
+"""One process per GPU: the spike exchange over NVLink / NVSwitch.
+
+Rank r owns shard r of the reference's PartitionMap (partition.py:60-65) and
+runs the step kernel on its own neurons; spikes move between ranks along the
+RoutingTable (routing.py:61-115, 184-231):
+
+* ``transport="nccl"``: per phase one grouped ncclSend/ncclRecv (the engine's
+  own communicator, bootstrapped over torch.distributed) of fixed-capacity
+  [count | ids] messages, then a scatter kernel;
+* ``transport="p2p"``: one device-initiated kernel per step that stores ids
+  straight into the peers' IPC-mapped inboxes and signals with system-scope
+  release/acquire flags (csrc/exchange_dist.cu).
+
+Two-level routes (``rt.via >= 0``) add the relay phase: a bridge re-buckets the
+ids it received from its group by final destination and forwards them (phase
+2).  torch.distributed is used only for bootstrap (unique id, IPC handles,
+destination masks) and for gathering results; nothing on the step path goes
+through it.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _native
+from .routing import RoutingTable
+from .sim import ExchangePlan, LifParams, Network, SimReport, _ShardState, _as_u16
+
+__all__ = ["channel_masks", "gather_dest", "DistSimulator"]
+
+
+def channel_masks(plan: ExchangePlan) -> list[dict]:
+    """Per rank: send1/recv1 (first hops), send2/recv2 (relay hops) as peer bitmasks.
+
+    Derived from the global plan so both ends of every channel agree (NCCL
+    needs matched send/recv pairs).
+    """
+    n = plan.n
+    send1 = [0] * n
+    for s in range(n):
+        for d in range(n):
+            h = int(plan.next_hop[s, d])
+            if d != s and h >= 0 and h != s:
+                send1[s] |= 1 << h
+    send2 = [0] * n
+    for b in range(n):
+        for s in range(n):
+            send2[b] |= int(plan.fwd[b, s])
+    recv1 = [sum(1 << s for s in range(n) if (send1[s] >> r) & 1) for r in range(n)]
+    recv2 = [sum(1 << b for b in range(n) if (send2[b] >> r) & 1) for r in range(n)]
+    return [{"send1": send1[r], "recv1": recv1[r], "send2": send2[r], "recv2": recv2[r]} for r in range(n)]
+
+
+def gather_dest(net: Network, rank: int, world: int, device):
+    """Destination mask of every internal id on every rank (all_gather of the shard masks)."""
+    import torch
+    import torch.distributed as dist
+    lay = net.layout
+    width = max(lay.n_local(h) for h in range(lay.n_shards))
+    mine = torch.zeros(max(width, 1), dtype=torch.int32, device=device)
+    n_local = lay.n_local(rank)
+    if n_local:
+        mine[:n_local] = net.shards[rank].dest
+    parts = [torch.zeros_like(mine) for _ in range(world)]
+    dist.all_gather(parts, mine)
+    g = torch.zeros(lay.n_words * 32, dtype=torch.int32, device=device)
+    for h in range(world):
+        b = int(lay.base[h])
+        g[b:b + lay.n_local(h)] = parts[h][: lay.n_local(h)]
+    return _as_u16(g)
+
+
+class DistSimulator:
+    """Step loop of this rank's shard with a multi-GPU spike exchange."""
+
+    def __init__(self, net: Network, lif: LifParams = LifParams(), seed: int = 0, rt: RoutingTable | None = None,
+                 *, transport: str = "p2p", delivery: str = "fused", msg_cap: int | None = None,
+                 record_raster_steps: int = 0, per_step_counts: bool = False, latency_steps: int = 4096,
+                 use_graph: bool = True, graph_chunk: int = 64, timeout_s: float = 10.0):
+        import torch
+        import torch.distributed as dist
+        if transport not in ("p2p", "nccl"):
+            raise ValueError(f"transport must be 'p2p' or 'nccl', got {transport!r}")
+        if delivery not in ("fused", "push", "pull"):
+            raise ValueError(f"delivery must be 'fused', 'pull' or 'push', got {delivery!r}")
+        self.rank = dist.get_rank()
+        self.world = dist.get_world_size()
+        lay = net.layout
+        if lay.n_shards != self.world:
+            raise ValueError(f"partition has {lay.n_shards} GPUs but {self.world} ranks are running")
+        if self.rank not in net.shards:
+            raise ValueError(f"rank {self.rank} has no shard in this network")
+        self.net = net
+        self.lif = lif
+        self.c_lif = lif.to_c(seed)
+        self.lib = _native.lib()
+        self.transport = transport
+        self.delivery = delivery
+        self.plan = ExchangePlan(self.world, rt)
+        self.masks = channel_masks(self.plan)[self.rank]
+        self.n = self.world
+        self.use_graph = use_graph
+        self.graph_chunk = graph_chunk
+        self.per_step_counts = per_step_counts
+        self.latency_steps = latency_steps
+        dev = net.device
+        self.dev = dev
+
+        # global message capacity: the exact per-rank bucket bound, maxed over ranks
+        probe = _ShardState(net, self.rank, self.plan, record_steps=0, push=False, bucket_cap=None)
+        cap_t = torch.tensor([probe.exact_cap], dtype=torch.int64, device=dev)
+        dist.all_reduce(cap_t, op=dist.ReduceOp.MAX)
+        cap = int(cap_t.item())
+        if msg_cap is not None:
+            cap = min(cap, int(msg_cap))
+        self.cap = max(cap, 1)
+        del probe
+        self.state = _ShardState(net, self.rank, self.plan, record_steps=record_raster_steps,
+                                 push=(delivery == "push"), bucket_cap=None, bucket_stride=self.cap)
+        self.states = [self.state]
+        self.record_steps = int(record_raster_steps)
+        self.dest_global = gather_dest(net, self.rank, self.world, dev)
+
+        i32 = dict(dtype=torch.int32, device=dev)
+        n, cap = self.n, self.cap
+        self.fwd_ids = torch.zeros(n * cap if self.plan.two_level else 1, **i32)
+        self.fwd_count = torch.zeros(n, **i32)
+        self.hdr = torch.zeros(4, n, **i32)                    # send, send2, recv, recv2
+        self.recv_ids = torch.zeros(n * cap if transport == "nccl" else 1, **i32)
+        self.recv2_ids = torch.zeros(n * cap if (transport == "nccl" and self.plan.two_level) else 1, **i32)
+        self.lat_stamps = torch.zeros((2, max(latency_steps, 1)), dtype=torch.int64, device=dev)
+        self.sync_words = torch.zeros(8, **i32)
+        self.hop_ids = None
+        self.deliv_ids = None
+
+        X = _native.XchgC()
+        X.rank, X.n, X.cap, X.two_level = self.rank, n, cap, int(self.plan.two_level)
+        X.per_step, X.lat_steps = int(per_step_counts), 0
+        X.send1_mask, X.recv1_mask = self.masks["send1"], self.masks["recv1"]
+        X.send2_mask, X.recv2_mask = self.masks["send2"], self.masks["recv2"]
+        X.bucket_cap = self.state.bucket_cap
+        X.timeout_ns = int(timeout_s * 1e9)
+        st = self.state
+        X.step, X.status = st.step.data_ptr(), st.status.data_ptr()
+        X.bitmap0, X.bitmap1 = st.bitmaps[0].data_ptr(), st.bitmaps[1].data_ptr()
+        X.bucket_ids, X.bucket_count = st.bucket_ids.data_ptr(), st.bucket_count.data_ptr()
+        X.dest_global = self.dest_global.data_ptr()
+        for h in range(n + 1):
+            X.shard_base[h] = int(lay.base[h]) if h < n else int(lay.base[n])
+        for s in range(n):
+            X.fwd_row[s] = int(self.plan.fwd[self.rank, s])
+        X.fwd_ids, X.fwd_count = self.fwd_ids.data_ptr(), self.fwd_count.data_ptr()
+        X.send_hdr, X.send2_hdr = self.hdr[0].data_ptr(), self.hdr[1].data_ptr()
+        X.recv_hdr, X.recv2_hdr = self.hdr[2].data_ptr(), self.hdr[3].data_ptr()
+        X.recv_ids, X.recv2_ids = self.recv_ids.data_ptr(), self.recv2_ids.data_ptr()
+        self.X = X
+        self._comm = None
+        self._ipc_own: list[int] = []
+        self._ipc_peer: list[int] = []
+        if transport == "nccl":
+            self._setup_nccl()
+        else:
+            self._setup_p2p()
+        self._graph = None
+        self._graph_len = 0
+        _native.check(self.lib.nc_sim_prepare(), "prepare")
+
+    # ------------------------------------------------------------ bootstrap
+    def _setup_nccl(self):
+        import torch.distributed as dist
+        uid = C.create_string_buffer(128)
+        if self.rank == 0:
+            _native.check(self.lib.nc_nccl_get_unique_id(uid), "nccl unique id")
+        obj = [bytes(uid.raw) if self.rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        buf = C.create_string_buffer(obj[0], 128)
+        comm = C.c_void_p()
+        _native.check(self.lib.nc_nccl_comm_init(C.byref(comm), self.world, buf, self.rank), "nccl comm init")
+        self._comm = comm
+
+    def _setup_p2p(self):
+        import torch.distributed as dist
+        n, cap = self.n, self.cap
+        inbox_words = 4 * n * (cap + 4)
+        flag_words = 2 * _native.MAX_SHARDS + 16  # flags + done/barrier/lat_start
+        handles = []
+        ptrs = []
+        for words in (inbox_words, flag_words):
+            p = C.c_void_p()
+            h = C.create_string_buffer(64)
+            _native.check(self.lib.nc_ipc_alloc(words * 4, C.byref(p), h), "ipc alloc")
+            self._ipc_own.append(p.value)
+            handles.append(bytes(h.raw))
+            ptrs.append(p.value)
+        allh = [None] * self.world
+        dist.all_gather_object(allh, handles)
+        X = self.X
+        X.my_inbox, X.my_flags = ptrs[0], ptrs[1]
+        base = ptrs[1]
+        X.done = base + 4 * (2 * _native.MAX_SHARDS)
+        X.barrier = base + 4 * (2 * _native.MAX_SHARDS + 1)
+        X.lat_start = base + 4 * (2 * _native.MAX_SHARDS + 2)  # 8-byte aligned
+        for peer in range(self.world):
+            if peer == self.rank:
+                X.peer_inbox[peer], X.peer_flags[peer] = ptrs[0], ptrs[1]
+                continue
+            opened = []
+            for k in range(2):
+                p = C.c_void_p()
+                hb = C.create_string_buffer(allh[peer][k], 64)
+                _native.check(self.lib.nc_ipc_open(hb, C.byref(p)), "ipc open")
+                self._ipc_peer.append(p.value)
+                opened.append(p.value)
+            X.peer_inbox[peer], X.peer_flags[peer] = opened
+
+    def close(self):
+        """Release the communicator and IPC windows (collective: call on every rank)."""
+        import torch
+        import torch.distributed as dist
+        torch.cuda.synchronize(self.dev)
+        dist.barrier()
+        for p in self._ipc_peer:
+            self.lib.nc_ipc_close(C.c_void_p(p))
+        self._ipc_peer = []
+        dist.barrier()
+        for p in self._ipc_own:
+            self.lib.nc_free(C.c_void_p(p))
+        self._ipc_own = []
+        if self._comm is not None:
+            self.lib.nc_nccl_comm_destroy(self._comm)
+            self._comm = None
+
+    # ------------------------------------------------------------ stepping
+    def reset(self, counter_steps: int):
+        import torch
+        import torch.distributed as dist
+        st = _native.stream_handle(self.dev)
+        s = self.state
+        _native.check(self.lib.nc_sim_init(C.byref(s.c), C.byref(self.c_lif), st), "sim init")
+        s.raster.zero_()
+        rows = counter_steps if self.per_step_counts else 1
+        self.hop_ids = torch.zeros((rows, self.n, self.n), dtype=torch.int64, device=self.dev)
+        self.deliv_ids = torch.zeros((rows, self.n, self.n), dtype=torch.int64, device=self.dev)
+        self.X.hop_ids, self.X.deliv_ids = self.hop_ids.data_ptr(), self.deliv_ids.data_ptr()
+        self.lat_stamps.zero_()
+        _native.check(self.lib.nc_xchg_reset(C.byref(self.X), st), "xchg reset")
+        self._graph = None
+        torch.cuda.synchronize(self.dev)
+        dist.barrier()
+
+    def _exchange(self, st):
+        L, X = self.lib, C.byref(self.X)
+        if self.transport == "p2p":
+            _native.check(L.nc_xchg_p2p(X, st), "p2p exchange")
+            return
+        _native.check(L.nc_xchg_seal(X, 1, st), "seal")
+        _native.check(L.nc_nccl_exchange(self._comm, X, 1, st), "nccl exchange")
+        _native.check(L.nc_xchg_scatter(X, 1, st), "scatter")
+        if self.plan.two_level:
+            _native.check(L.nc_xchg_seal(X, 2, st), "seal 2")
+            _native.check(L.nc_nccl_exchange(self._comm, X, 2, st), "nccl exchange 2")
+            _native.check(L.nc_xchg_scatter(X, 2, st), "scatter 2")
+
+    def _one_step(self, st):
+        L = self.lib
+        s = self.state
+        lif = C.byref(self.c_lif)
+        if self.delivery == "fused":
+            _native.check(L.nc_sim_step_fused(C.byref(s.c), lif, st), "step")
+        else:
+            if self.delivery == "push":
+                _native.check(L.nc_sim_deliver_push(C.byref(s.c), self.c_lif.g_inh, st), "push")
+            else:
+                _native.check(L.nc_sim_deliver_pull(C.byref(s.c), self.c_lif.g_inh, st), "pull")
+            _native.check(L.nc_sim_lif_update(C.byref(s.c), lif, st), "lif")
+        _native.check(L.nc_stamp(self.lat_stamps[0].data_ptr(), s.step.data_ptr(), self.latency_steps, st), "stamp")
+        self._exchange(st)
+        _native.check(L.nc_stamp(self.lat_stamps[1].data_ptr(), s.step.data_ptr(), self.latency_steps, st), "stamp")
+        _native.check(L.nc_sim_end_step(C.byref(s.c), st), "end step")
+
+    def launches_per_step(self) -> int:
+        step = 2 if self.delivery == "fused" else 3
+        if self.transport == "p2p":
+            ex = 1 + (1 if self.plan.two_level else 0)
+        else:
+            ex = 2 * (2 if self.plan.two_level else 1) + (1 if self.plan.two_level else 0)
+        return step + ex + 2
+
+    def advance_eager(self, steps: int):
+        st = _native.stream_handle(self.dev)
+        for _ in range(steps):
+            self._one_step(st)
+
+    def advance(self, steps: int):
+        import torch
+        if not self.use_graph:
+            self.advance_eager(steps)
+            return
+        done = 0
+        while done < steps:
+            k = min(self.graph_chunk, steps - done)
+            if self._graph is None or self._graph_len != k:
+                g = torch.cuda.CUDAGraph()
+                side = torch.cuda.Stream(self.dev)
+                side.wait_stream(torch.cuda.current_stream(self.dev))
+                with torch.cuda.stream(side):
+                    g.capture_begin()
+                    cst = _native.stream_handle(self.dev)
+                    for _ in range(k):
+                        self._one_step(cst)
+                    g.capture_end()
+                torch.cuda.current_stream(self.dev).wait_stream(side)
+                self._graph, self._graph_len = g, k
+            self._graph.replay()
+            done += k
+
+    def check_status(self):
+        flags = self.state.status.cpu().tolist()
+        if flags[0]:
+            raise RuntimeError(f"rank {self.rank}: spike message overflow (capacity {self.cap}); raise msg_cap")
+        if flags[1]:
+            raise RuntimeError(f"rank {self.rank}: exchange watchdog expired waiting for a peer")
+
+    def latencies_us(self, steps: int) -> np.ndarray:
+        """Per-step exchange latency (us), max over ranks; first `steps` recorded steps."""
+        import torch
+        import torch.distributed as dist
+        k = min(steps, self.latency_steps)
+        d = (self.lat_stamps[1, :k] - self.lat_stamps[0, :k]).to(torch.float64)
+        dist.all_reduce(d, op=dist.ReduceOp.MAX)
+        return d.cpu().numpy() / 1e3
+
+    def run(self, steps: int) -> SimReport:
+        """Run `steps` steps; every rank gets the full report (rasters gathered)."""
+        import torch
+        import torch.distributed as dist
+        self.reset(steps if self.per_step_counts else 1)
+        if self.record_steps and self.record_steps < steps:
+            raise ValueError("record_raster_steps is smaller than the number of steps")
+        dist.barrier()
+        torch.cuda.synchronize(self.dev)
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        self.advance(steps)
+        t1.record()
+        torch.cuda.synchronize(self.dev)
+        ms = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device=self.dev)
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        self.check_status()
+        return self._report(steps, float(ms.item()))
+
+    def _report(self, steps: int, ms: float) -> SimReport:
+        import torch
+        import torch.distributed as dist
+        lay = self.net.layout
+        s = self.state
+        hop = self.hop_ids.clone()
+        deliv = self.deliv_ids.clone()
+        dist.all_reduce(hop)
+        dist.all_reduce(deliv)
+        width = max((lay.n_local(h) + 31) // 32 for h in range(lay.n_shards))
+        nmax = max(lay.n_local(h) for h in range(lay.n_shards))
+        raster = None
+        if self.record_steps:
+            mine = torch.zeros((steps, max(width, 1)), dtype=torch.int32, device=self.dev)
+            mine[:, : s.local_words] = s.raster[:steps, : s.local_words]
+            parts = [torch.zeros_like(mine) for _ in range(self.world)]
+            dist.all_gather(parts, mine)
+            raster = np.zeros((steps, lay.n_neurons), dtype=bool)
+            for h in range(self.world):
+                nl = lay.n_local(h)
+                if not nl:
+                    continue
+                words = parts[h].cpu().numpy().view(np.uint32)[:, : (nl + 31) // 32]
+                bits = ((words[:, :, None] >> np.arange(32, dtype=np.uint32)) & np.uint32(1)).reshape(steps, -1)
+                raster[:, lay.members[h]] = bits[:, :nl].astype(bool)
+        vt = torch.zeros((2, max(nmax, 1)), dtype=torch.float32, device=self.dev)
+        vt[0, : s.n_local] = s.v[: s.n_local]
+        vt[1, : s.n_local] = s.i_syn[: s.n_local]
+        parts = [torch.zeros_like(vt) for _ in range(self.world)]
+        dist.all_gather(parts, vt)
+        v = np.zeros(lay.n_neurons, dtype=np.float32)
+        i = np.zeros(lay.n_neurons, dtype=np.float32)
+        for h in range(self.world):
+            nl = lay.n_local(h)
+            p = parts[h].cpu().numpy()
+            v[lay.members[h]] = p[0, :nl]
+            i[lay.members[h]] = p[1, :nl]
+        sp = s.spike_total.clone()
+        dist.all_reduce(sp)
+        lat = self.latencies_us(steps)
+        mode = "two-level" if self.plan.two_level else "direct"
+        return SimReport(steps=steps, n_gpus=self.world, raster=raster, deliv_ids=deliv.cpu().numpy(),
+                         hop_ids=hop.cpu().numpy(), spikes=int(sp.item()), v=v, i_syn=i, elapsed_ms=ms,
+                         exchange=mode, delivery=self.delivery,
+                         extra={"transport": self.transport, "exchange_us": lat,
+                                "exchange_p50_us": float(np.percentile(lat, 50)) if lat.size else None,
+                                "exchange_p99_us": float(np.percentile(lat, 99)) if lat.size else None})

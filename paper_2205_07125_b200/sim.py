@@ -34,10 +34,11 @@ from .routing import RoutingTable
 
 __all__ = [
     "LifParams", "ShardLayout", "ExchangePlan", "Network", "Simulator", "SimReport", "simulate",
-    "q_from_p", "inhibitory_mask", "PAD_Q_BITS",
+    "q_from_p", "inhibitory_mask", "ID_BITS",
 ]
 
-PAD_Q_BITS = 6          # low bits of a packed entry: inhibitory flag + (q-1)
+ID_BITS = 26            # packed pull entry: (q << 26) | pre internal id
+ID_MASK = (1 << ID_BITS) - 1
 Q_LEVELS = 32           # synaptic weight units: q = ceil(32 p) in [1, 32]
 
 
@@ -160,7 +161,7 @@ class ShardLayout:
 
     @property
     def pad_entry(self) -> int:
-        return self.guard_id << PAD_Q_BITS
+        return (1 << ID_BITS) | self.guard_id
 
     def n_local(self, h: int) -> int:
         return int(self.members[h].size)
@@ -168,13 +169,16 @@ class ShardLayout:
 
 # ---------------------------------------------------------------- network
 
-def _pack(pre_internal, inh, q):
-    return ((pre_internal.astype(np.uint32) << np.uint32(PAD_Q_BITS))
-            | (inh.astype(np.uint32) << np.uint32(5)) | (q.astype(np.uint32) - np.uint32(1)))
+def _pack(pre_internal, q):
+    return (q.astype(np.uint32) << np.uint32(ID_BITS)) | pre_internal.astype(np.uint32)
 
 
 def host_pull_csr(graph: NeuronGraph, layout: ShardLayout, shard: int, inh_every: int):
-    """Pull CSR of one shard from a host NeuronGraph (rows = local posts, padded to 4)."""
+    """Pull CSR of one shard from a host NeuronGraph.
+
+    Segment 2r holds the excitatory pres of local post row r, 2r+1 the
+    inhibitory ones; every segment is padded to a multiple of 4 entries.
+    """
     q = q_from_p(graph.edge_p)
     post = np.concatenate([graph.edge_j, graph.edge_i]).astype(np.int64)
     pre = np.concatenate([graph.edge_i, graph.edge_j]).astype(np.int64)
@@ -183,16 +187,17 @@ def host_pull_csr(graph: NeuronGraph, layout: ShardLayout, shard: int, inh_every
     post, pre, qq = post[keep], pre[keep], qq[keep]
     n_local = layout.n_local(shard)
     row = layout.internal_id[post].astype(np.int64) - int(layout.base[shard])
-    entries = _pack(layout.internal_id[pre], inhibitory_mask(pre, inh_every), qq)
-    counts = np.bincount(row, minlength=n_local).astype(np.int64)
-    rowptr4 = np.zeros(n_local + 1, dtype=np.int64)
+    seg = 2 * row + inhibitory_mask(pre, inh_every)
+    entries = _pack(layout.internal_id[pre], qq)
+    counts = np.bincount(seg, minlength=2 * n_local).astype(np.int64)
+    rowptr4 = np.zeros(2 * n_local + 1, dtype=np.int64)
     rowptr4[1:] = np.cumsum((counts + 3) // 4)
     syn = np.full(int(rowptr4[-1]) * 4, layout.pad_entry, dtype=np.uint32)
-    order = np.argsort(row, kind="stable")
-    srow = row[order]
+    order = np.argsort(seg, kind="stable")
+    sseg = seg[order]
     first = np.cumsum(counts) - counts
-    slot = np.arange(srow.size, dtype=np.int64) - first[srow]
-    syn[rowptr4[srow] * 4 + slot] = entries[order]
+    slot = np.arange(sseg.size, dtype=np.int64) - first[sseg]
+    syn[rowptr4[sseg] * 4 + slot] = entries[order]
     return rowptr4, syn
 
 
@@ -285,11 +290,12 @@ class Network:
                 inter_lo=spec.inter_p_range[0], inter_hi=spec.inter_p_range[1],
                 seed=int(spec.seed) & (2**64 - 1), owner=owner_d.data_ptr(), internal_id=internal_d.data_ptr(),
                 local_base=int(layout.base[h]), inh_every=inh_every)
-            lower = torch.zeros(max(n_local, 1), dtype=torch.int32, device=dev)
-            upper = torch.zeros(max(n_local, 1), dtype=torch.int32, device=dev)
+            n_seg = 2 * n_local
+            lower = torch.zeros(max(n_seg, 1), dtype=torch.int32, device=dev)
+            upper = torch.zeros(max(n_seg, 1), dtype=torch.int32, device=dev)
             _native.check(L.nc_graphgen_count(C.byref(g), lower.data_ptr(), upper.data_ptr(), st), "graphgen count")
-            lens = (lower[:n_local] + upper[:n_local]).to(torch.int64)
-            rowptr4 = torch.zeros(n_local + 1, dtype=torch.int64, device=dev)
+            lens = (lower[:n_seg] + upper[:n_seg]).to(torch.int64)
+            rowptr4 = torch.zeros(n_seg + 1, dtype=torch.int64, device=dev)
             rowptr4[1:] = torch.cumsum((lens + 3) // 4, 0)
             total = int(rowptr4[-1].item()) * 4
             syn = torch.empty(max(total, 4), dtype=torch.int32, device=dev)
@@ -315,21 +321,21 @@ class Network:
         return _as_u16(g)
 
     def host_csr(self, shard: int):
-        """(rowptr, pre_gid, q) of one shard in gid space, for the oracle (test/bench only)."""
-        import torch
+        """(post_gid, pre_gid, q) of every synapse of one shard, for the oracle (test/bench only)."""
         csr = self.shards[shard]
         rp4 = csr.rowptr4.cpu().numpy()
         syn = csr.syn.cpu().numpy().view(np.uint32)[: int(rp4[-1]) * 4]
         keep = syn != np.uint32(self.layout.pad_entry)
-        rows = np.repeat(np.arange(rp4.size - 1), np.diff(rp4) * 4)[keep]
+        seg = np.repeat(np.arange(rp4.size - 1), np.diff(rp4) * 4)[keep]
         ent = syn[keep]
         gid_of_internal = np.full(self.layout.n_words * 32, -1, dtype=np.int64)
         for h, m in enumerate(self.layout.members):
             gid_of_internal[int(self.layout.base[h]) + np.arange(m.size)] = m
-        pre = gid_of_internal[(ent >> PAD_Q_BITS).astype(np.int64)]
-        q = (ent & np.uint32(31)).astype(np.uint8) + 1
-        post = self.layout.members[shard][rows]
-        del torch
+        pre = gid_of_internal[(ent & np.uint32(ID_MASK)).astype(np.int64)]
+        q = (ent >> np.uint32(ID_BITS)).astype(np.uint8)
+        post = self.layout.members[shard][seg // 2]
+        if (inhibitory_mask(pre, self.inh_every) != (seg % 2 == 1)).any():
+            raise AssertionError("segment / pre type mismatch in the pull CSR")
         return post, pre, q
 
 
@@ -441,7 +447,7 @@ class _ShardState:
     """Device buffers and the C descriptor of one shard."""
 
     def __init__(self, net: Network, h: int, plan: ExchangePlan, *, record_steps: int, push: bool,
-                 bucket_cap: int | None):
+                 bucket_cap: int | None, bucket_stride: int | None = None):
         import torch
         lay = net.layout
         dev = net.device
@@ -470,7 +476,8 @@ class _ShardState:
             cap = 1
         if bucket_cap is not None:
             cap = min(cap, int(bucket_cap))
-        self.bucket_cap = max(cap, 1)
+        self.exact_cap = cap
+        self.bucket_cap = max(cap, 1) if bucket_stride is None else int(bucket_stride)
         self.bucket_ids = torch.zeros(n * self.bucket_cap, dtype=torch.int32, device=dev)
         self.bucket_count = torch.zeros(n, dtype=torch.int32, device=dev)
         self.status = torch.zeros(2, dtype=torch.int32, device=dev)
@@ -499,24 +506,25 @@ class _ShardState:
 
 
 def _push_csr(csr: ShardCSR, lay: ShardLayout, h: int, dev):
-    """Transpose of the pull CSR: rows = internal pre ids, entries = (post_local << 6) | flags."""
+    """Transpose of the pull CSR: rows = internal pre ids,
+    entries = (inhibitory << 31) | ((q - 1) << 26) | post_local."""
     import torch
     n_local = lay.n_local(h)
     rp4 = csr.rowptr4
     total = int(rp4[-1].item()) * 4
     syn = csr.syn[:total].to(torch.int64) & 0xFFFFFFFF
     lens4 = (rp4[1:] - rp4[:-1]) * 4
-    post = torch.repeat_interleave(torch.arange(n_local, device=dev, dtype=torch.int64), lens4)
+    seg = torch.repeat_interleave(torch.arange(2 * n_local, device=dev, dtype=torch.int64), lens4)
     keep = syn != lay.pad_entry
-    syn, post = syn[keep], post[keep]
-    pre = syn >> PAD_Q_BITS
-    flags = syn & 63
+    syn, seg = syn[keep], seg[keep]
+    pre = syn & ID_MASK
+    q = syn >> ID_BITS
+    ent = ((seg & 1) << 31) | ((q - 1) << ID_BITS) | (seg >> 1)
     order = torch.argsort(pre, stable=True)
-    pre, post, flags = pre[order], post[order], flags[order]
+    pre, ent = pre[order], ent[order]
     n_rows = lay.n_words * 32
     rowptr = torch.zeros(n_rows + 1, dtype=torch.int64, device=dev)
     rowptr[1:] = torch.cumsum(torch.bincount(pre, minlength=n_rows), 0)
-    ent = (post << PAD_Q_BITS) | flags
     ent = torch.where(ent >= 2**31, ent - 2**32, ent).to(torch.int32)
     return rowptr, ent
 
