@@ -179,6 +179,14 @@ class DistSimulator:
         comm = C.c_void_p()
         _native.check(self.lib.nc_nccl_comm_init(C.byref(comm), self.world, buf, self.rank), "nccl comm init")
         self._comm = comm
+        # NCCL connects peers lazily on first use; do that eagerly (outside any
+        # CUDA-graph capture) with one exchange of empty messages per phase.
+        import torch
+        st = _native.stream_handle(self.dev)
+        for phase in ((1, 2) if self.plan.two_level else (1,)):
+            _native.check(self.lib.nc_nccl_exchange(self._comm, C.byref(self.X), phase, st), "nccl warm-up")
+        torch.cuda.synchronize(self.dev)
+        self.hdr.zero_()
 
     def _setup_p2p(self):
         import torch.distributed as dist
@@ -323,14 +331,19 @@ class DistSimulator:
         if flags[1]:
             raise RuntimeError(f"rank {self.rank}: exchange watchdog expired waiting for a peer")
 
-    def latencies_us(self, steps: int) -> np.ndarray:
-        """Per-step exchange latency (us), max over ranks; first `steps` recorded steps."""
+    def latencies_us(self, steps: int) -> tuple[np.ndarray, np.ndarray]:
+        """Per-step exchange time (us) from this rank's buckets-ready stamp to its last inbound
+        spike: (min over ranks, max over ranks).  The minimum is the rank that became
+        ready last, i.e. the pure transfer + signalling latency; the maximum adds the
+        wait for slower peers (step-time skew)."""
         import torch
         import torch.distributed as dist
         k = min(steps, self.latency_steps)
         d = (self.lat_stamps[1, :k] - self.lat_stamps[0, :k]).to(torch.float64)
-        dist.all_reduce(d, op=dist.ReduceOp.MAX)
-        return d.cpu().numpy() / 1e3
+        lo, hi = d.clone(), d.clone()
+        dist.all_reduce(lo, op=dist.ReduceOp.MIN)
+        dist.all_reduce(hi, op=dist.ReduceOp.MAX)
+        return lo.cpu().numpy() / 1e3, hi.cpu().numpy() / 1e3
 
     def run(self, steps: int) -> SimReport:
         """Run `steps` steps; every rank gets the full report (rasters gathered)."""
@@ -391,11 +404,11 @@ class DistSimulator:
             i[lay.members[h]] = p[1, :nl]
         sp = s.spike_total.clone()
         dist.all_reduce(sp)
-        lat = self.latencies_us(steps)
+        lat, lat_max = self.latencies_us(steps)
         mode = "two-level" if self.plan.two_level else "direct"
         return SimReport(steps=steps, n_gpus=self.world, raster=raster, deliv_ids=deliv.cpu().numpy(),
                          hop_ids=hop.cpu().numpy(), spikes=int(sp.item()), v=v, i_syn=i, elapsed_ms=ms,
                          exchange=mode, delivery=self.delivery,
-                         extra={"transport": self.transport, "exchange_us": lat,
+                         extra={"transport": self.transport, "exchange_us": lat, "exchange_wait_us": lat_max,
                                 "exchange_p50_us": float(np.percentile(lat, 50)) if lat.size else None,
                                 "exchange_p99_us": float(np.percentile(lat, 99)) if lat.size else None})

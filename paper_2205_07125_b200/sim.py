@@ -67,6 +67,18 @@ class LifParams:
     ext_lanes: int = 4
     w_ext: float = 4.0           # synaptic current of one external event
 
+    @classmethod
+    def for_rate(cls, hz: float, **kw) -> "LifParams":
+        """Parameters whose drive gives about `hz` Hz mean firing (degree 100-1000 nets).
+
+        Interpolates RATE_CALIBRATION, measured with the C oracle on a 20k-neuron,
+        degree-1000 random network (steps 100-400, default parameters).
+        """
+        ext, rate = RATE_CALIBRATION[:, 0], RATE_CALIBRATION[:, 1]
+        if not rate[0] <= hz <= rate[-1]:
+            raise ValueError(f"calibrated for {rate[0]}..{rate[-1]} Hz, got {hz}")
+        return cls(ext_rate_hz=float(np.interp(hz, rate, ext)), **kw)
+
     def constants(self, seed: int) -> dict:
         f32 = lambda x: float(np.float32(x))  # noqa: E731
         if not (self.dt_ms > 0 and self.tau_m_ms > 0 and self.tau_syn_ms > 0):
@@ -100,6 +112,13 @@ class LifParams:
             v_reset=k["v_reset"], v_th=k["v_th"], w_unit=k["w_unit"], w_ext=k["w_ext"],
             v_init_span=k["v_init_span"], ext_threshold=k["ext_threshold"], ext_lanes=k["ext_lanes"],
             t_ref=k["t_ref"], g_inh=k["g_inh"], pad0=0, seed=k["seed"])
+
+
+# (ext_rate_hz per lane, measured firing rate Hz) -- see LifParams.for_rate
+RATE_CALIBRATION = np.array([
+    (140, 0.068), (160, 0.676), (180, 2.994), (190, 4.91), (200, 7.314), (210, 9.727), (215, 10.968),
+    (220, 12.248), (230, 14.867), (240, 17.438), (260, 22.468), (280, 27.036), (300, 31.523),
+    (330, 37.63), (360, 43.524), (400, 50.916)])
 
 
 def q_from_p(p) -> np.ndarray:

@@ -52,7 +52,7 @@ def main() -> int:
             rp, col, q = c_oracle.symmetric_csr(g.n_neurons, g.edge_i, g.edge_j, S.q_from_p(g.edge_p))
             ref = c_oracle.simulate_csr(rp, col, q, pm.assignment, world, rt.next_hop_matrix(), lif.constants(1),
                                         steps, threads=8)
-        for transport in ("p2p", "nccl"):
+        for transport in os.environ.get("NC_TRANSPORTS", "p2p,nccl").split(","):
             sim = DistSimulator(net, lif, 1, rt, transport=transport, record_raster_steps=steps,
                                 per_step_counts=True)
             rep = sim.run(steps)
