@@ -184,10 +184,10 @@ def run_ours(args) -> dict | None:
     n_local = lay.n_local(rank)
     csr = net.shards[rank]
     # algorithmic bytes of one fused step: 4 B per synapse
-    # + per neuron rowptr 16 (E/I segment starts), V r/w 8, I r/w 8, refrac r/w 2,
-    # gid 4, + the previous spike bitmap read and the new one written
+    # + per neuron emid 2/tile, V r/w 8, I r/w 8, refrac r/w 2, gid 4, the slice
+    # pointers, + the previous spike bitmap read and the new one written
     syn_bytes = int(net.n_synapses) * 4
-    neuron_bytes = n_local * (16 + 8 + 8 + 2 + 4) + 2 * (lay.n_words * 4)
+    neuron_bytes = n_local * (2 * csr.n_tiles + 8 + 8 + 2 + 4) + csr.slice_ptr.numel() * 8 + 2 * (lay.n_words * 4)
     alg_bytes = syn_bytes + neuron_bytes
     peaks = load_peaks()
     achieved = alg_bytes / (kernel_ms * 1e-3) / 1e9
@@ -213,7 +213,9 @@ def run_ours(args) -> dict | None:
                 "neurons": n_neurons, "mean_degree": args.degree, "synapses": int(net.n_synapses) * world,
                 "delivery": args.delivery, "exchange": "none" if world == 1 else "direct",
                 "firing_rate_hz": round(spikes / n_neurons / (args.steps * 1e-3), 3),
-                "l2": "inputs larger than L2 (CSR %.2f GB streamed every step)" % (csr.n_synapses_padded * 4 / 1e9),
+                "l2": "inputs larger than L2 (synapse array %.2f GB streamed every step)" % (csr.n_entries * 4 / 1e9),
+                "sell_padding": round(csr.n_entries / max(csr.n_real, 1) - 1.0, 4),
+                "bitmap_tiles": csr.n_tiles,
                 "graph_build_s": round(t_build, 2),
             },
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
@@ -242,25 +244,19 @@ def run_ours(args) -> dict | None:
 
 
 def gid_csr(net, lay, rank=0):
-    """Gid-space CSR of a single-shard network for the CPU oracle (unpacked on the GPU)."""
+    """Gid-space CSR of a single-shard network for the CPU oracle (decoded on the GPU)."""
     import torch
-    from paper_2205_07125_b200.sim import ID_BITS, ID_MASK
-    csr = net.shards[rank]
-    rp4 = csr.rowptr4
-    syn = csr.syn[: int(rp4[-1].item()) * 4].to(torch.int64) & 0xFFFFFFFF
-    keep = syn != lay.pad_entry
-    n_rows = (rp4.numel() - 1) // 2
-    seg = torch.repeat_interleave(torch.arange(2 * n_rows, device=syn.device), (rp4[1:] - rp4[:-1]) * 4)
-    lens = torch.bincount(seg[keep] // 2, minlength=n_rows)
-    rowptr = torch.zeros(n_rows + 1, dtype=torch.int64, device=syn.device)
-    rowptr[1:] = torch.cumsum(lens, 0)
-    ent = syn[keep]
-    col = (ent & ID_MASK).to(torch.int32)      # single block shard: internal id == gid
-    q = (ent >> ID_BITS).to(torch.uint8)
-    out = rowptr.cpu().numpy(), col.cpu().numpy(), q.cpu().numpy()
-    del seg, keep, syn
+    from paper_2205_07125_b200 import sell
+    row, pre, q, _ = sell.decode(net.shards[rank])
+    order = torch.argsort(row, stable=True)
+    row, pre, q = row[order], pre[order], q[order]
+    n = lay.n_local(rank)
+    rowptr = torch.zeros(n + 1, dtype=torch.int64, device=row.device)
+    rowptr[1:] = torch.cumsum(torch.bincount(row, minlength=n), 0)
+    out = rowptr.cpu().numpy(), pre.to(torch.int32).cpu().numpy(), q.to(torch.uint8).cpu().numpy()
+    del row, pre, q, order
     torch.cuda.empty_cache()
-    return out
+    return out                                # single block shard: internal id == gid
 
 
 def cpu_baseline(net, lay, lif, args) -> dict:
@@ -287,8 +283,10 @@ def e2e_measure(sim, net, args) -> dict:
     csr = net.shards[0]
     host_syn = torch.empty(csr.syn.shape, dtype=torch.int32, pin_memory=True)
     host_syn.copy_(csr.syn)
-    host_rp = torch.empty(csr.rowptr4.shape, dtype=torch.int64, pin_memory=True)
-    host_rp.copy_(csr.rowptr4)
+    host_rp = torch.empty(csr.slice_ptr.shape, dtype=torch.int64, pin_memory=True)
+    host_rp.copy_(csr.slice_ptr)
+    host_em = torch.empty(csr.row_emid.shape, dtype=torch.int16, pin_memory=True)
+    host_em.copy_(csr.row_emid)
     words = st.local_words
     ring = torch.empty((2, words), dtype=torch.int32, pin_memory=True)
     steps = args.steps
@@ -297,7 +295,8 @@ def e2e_measure(sim, net, args) -> dict:
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
     csr.syn.copy_(host_syn, non_blocking=True)
-    csr.rowptr4.copy_(host_rp, non_blocking=True)
+    csr.slice_ptr.copy_(host_rp, non_blocking=True)
+    csr.row_emid.copy_(host_em, non_blocking=True)
     sim.reset(1)
     for t in range(steps):
         sim.advance_eager(1)
@@ -306,7 +305,7 @@ def e2e_measure(sim, net, args) -> dict:
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
-    h2d = host_syn.numel() * 4 + host_rp.numel() * 8
+    h2d = host_syn.numel() * 4 + host_rp.numel() * 8 + host_em.numel() * 2
     return {"value": round(steps / (ms * 1e-3), 2), "unit": UNIT, "h2d_bytes_per_step": int(h2d // steps),
             "d2h_bytes_per_step": int(words * 4),
             "note": "network H2D from pinned memory once per call (amortised), spike bitmap D2H every step"}

@@ -88,14 +88,18 @@ int nc_weight_histogram(const double* weights, const int64_t* assignment, int64_
  * [local_base, local_base + n_local); bitmaps are indexed by internal id.
  *
  * Synapses: each undirected edge (i, j, p) of NeuronGraph is one synapse in
- * each direction.  A pull-CSR entry is a packed uint32
- *     (q << 26) | pre_internal_id,      q = ceil(32 * p) in [1, 32],
- * and every post row r is split into two segments, 2r = excitatory pres
- * (weight +q) and 2r+1 = inhibitory pres (weight -g_inh * q), so the inner
- * loop never tests a sign.  Each segment is padded to a multiple of 4 entries
- * with a pad entry whose pre id is the guard bit that never fires.
- * rowptr4[s] (2*n_local+1 entries) is the start of segment s in units of
- * 4 entries.  Push-CSR entries (rows = internal pre ids) are
+ * each direction.  A pull entry is a packed uint32
+ *     (q << 26) | pre_internal_id,      q = ceil(32 * p) in [1, 32].
+ * Layout: sliced ELL with slice = one warp = 32 consecutive local rows
+ * ("SELL-32"), further split by bitmap tile t (the spike bitmap is staged in
+ * shared memory tile by tile when it exceeds one tile).  Block (slice s,
+ * tile t) starts at slice_ptr[s*n_tiles + t] (uint4 units) and holds `len`
+ * slots of 32 uint4: slot u of lane l is entries 4u..4u+3 of row 32s+l.  A
+ * row's slots [0, emid) hold its excitatory pres (weight +q), the next slots
+ * its inhibitory pres (weight -g_inh*q); emid = row_emid[row*n_tiles + t].
+ * Unused entries hold the pad entry (guard id, never fires).  Lanes read
+ * consecutive 16-byte words, each lane owns one row: no cross-lane reduction.
+ * Push entries (rows = internal pre ids):
  *     (inhibitory(pre) << 31) | ((q - 1) << 26) | post_local. */
 
 #define NC_MAX_SHARDS 16
@@ -123,6 +127,8 @@ typedef struct nc_shard {
   int32_t n_local;        /* neurons owned                                     */
   int32_t local_base;     /* first internal id owned (multiple of 32)          */
   int32_t n_words;        /* bitmap words over all internal ids incl. guard   */
+  int32_t n_tiles;        /* bitmap tiles (1 = whole bitmap in shared memory)  */
+  int32_t tile_words;     /* words per bitmap tile (multiple of 4)             */
   int32_t pad0;
   /* neuron state, n_local each */
   float* v;
@@ -131,9 +137,10 @@ typedef struct nc_shard {
   int32_t* acc;           /* synaptic input (push delivery / unfused path)    */
   const uint32_t* gid;    /* global neuron id (Philox counter, raster ids)    */
   const uint16_t* hop_mask; /* bit h: a spike of this neuron is sent to shard h */
-  /* pull CSR */
-  const int64_t* rowptr4; /* 2*n_local+1 segment starts (E/I per row)          */
-  const uint32_t* syn;    /* packed entries                                    */
+  /* pull SELL-32 */
+  const int64_t* slice_ptr; /* n_slices*n_tiles+1 block starts (uint4 units)   */
+  const uint16_t* row_emid; /* n_local*n_tiles excitatory slots per row/tile   */
+  const uint32_t* syn;      /* packed entries                                  */
   /* push CSR (optional): rows = internal pre ids, entries see above */
   const int64_t* push_rowptr;
   const uint32_t* push_syn;
@@ -284,19 +291,26 @@ typedef struct nc_graphgen {
   int32_t inh_every;          /* gid % inh_every == inh_every-1 is inhibitory (0 = none) */
 } nc_graphgen_t;
 
-/* lower_len/upper_len: [2*n_local] entries per segment (zero-initialised). */
-int nc_graphgen_count(const nc_graphgen_t* g, int32_t* lower_len, int32_t* upper_len,
-                      void* stream);
-int nc_graphgen_fill(const nc_graphgen_t* g, const int64_t* rowptr4, const int32_t* lower_len,
-                     int32_t* lower_fill, uint32_t* syn, void* stream);
-/* Write pad entries into [segment length, 4*ceil(len/4)) of every segment. */
-int nc_graphgen_pad(const int64_t* rowptr4, const int32_t* lower_len, const int32_t* upper_len,
-                    int32_t n_local, uint32_t pad_entry, uint32_t* syn, void* stream);
+/* Pass 1.  lower_len/upper_len: [n_local * n_tiles * 2] entries per
+ * (row, tile, sign) (zero-initialised); tile_words as in nc_shard_t. */
+int nc_graphgen_count(const nc_graphgen_t* g, int32_t n_tiles, int32_t tile_words, int32_t* lower_len,
+                      int32_t* upper_len, void* stream);
+/* Pass 2 into the SELL-32 layout (slice_ptr/row_emid computed by the host
+ * from the pass-1 counts); lower_fill [n_local*n_tiles*2] zero-initialised
+ * (slot claims; lower_len is unused and may be NULL).  syn must be pre-filled
+ * with nc_sell_fill_pads. */
+int nc_graphgen_fill(const nc_graphgen_t* g, int32_t n_tiles, int32_t tile_words, const int64_t* slice_ptr,
+                     const uint16_t* row_emid, const int32_t* lower_len, int32_t* lower_fill, uint32_t* syn,
+                     void* stream);
+/* Pad pre-fill of a SELL-32 array: block b = (slice, tile b % n_tiles) gets
+ * (first id of its tile) with q = 0 in every entry. */
+int nc_sell_fill_pads(const int64_t* slice_ptr, int64_t n_blocks, int32_t n_tiles, int32_t tile_words,
+                      uint32_t* syn, void* stream);
 /* Destination masks from a built CSR (the adjacency is symmetric, so the
  * pres of row r are exactly the posts r drives): dest_mask[r] = OR over the
  * row's entries of (1 << owner shard of the pre id) without `self`, where shard
  * h owns internal ids [shard_base[h], shard_base[h+1]) (device int32[n+1]). */
-int nc_dest_mask_from_csr(const int64_t* rowptr4, const uint32_t* syn, int32_t n_local,
+int nc_dest_mask_from_csr(const int64_t* slice_ptr, int32_t n_tiles, const uint32_t* syn, int32_t n_local,
                           const int32_t* shard_base, int32_t n_shards, int32_t self,
                           uint16_t* dest_mask, void* stream);
 

@@ -38,10 +38,11 @@ class LifParamsC(C.Structure):
 class ShardC(C.Structure):
     _fields_ = [
         ("shard", c_int32), ("n_shards", c_int32), ("n_local", c_int32),
-        ("local_base", c_int32), ("n_words", c_int32), ("pad0", c_int32),
+        ("local_base", c_int32), ("n_words", c_int32), ("n_tiles", c_int32), ("tile_words", c_int32),
+        ("pad0", c_int32),
         ("v", c_void_p), ("i_syn", c_void_p), ("refrac", c_void_p), ("acc", c_void_p),
         ("gid", c_void_p), ("hop_mask", c_void_p),
-        ("rowptr4", c_void_p), ("syn", c_void_p),
+        ("slice_ptr", c_void_p), ("row_emid", c_void_p), ("syn", c_void_p),
         ("push_rowptr", c_void_p), ("push_syn", c_void_p),
         ("bitmap0", c_void_p), ("bitmap1", c_void_p),
         ("fired_ids", c_void_p), ("fired_count", c_void_p),
@@ -100,10 +101,11 @@ _SIGS = {
     "nc_sim_end_step": (c_int32, [C.POINTER(ShardC), c_void_p]),
     "nc_exchange_local": (c_int32, [C.POINTER(ShardC), c_int32, c_void_p, c_void_p, c_void_p, c_void_p,
                                     c_int64, c_void_p, c_void_p, c_int32, c_void_p]),
-    "nc_graphgen_count": (c_int32, [C.POINTER(GraphGenC), c_void_p, c_void_p, c_void_p]),
-    "nc_graphgen_fill": (c_int32, [C.POINTER(GraphGenC), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
-    "nc_graphgen_pad": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_uint32, c_void_p, c_void_p]),
-    "nc_dest_mask_from_csr": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p, c_int32, c_int32, c_void_p,
+    "nc_graphgen_count": (c_int32, [C.POINTER(GraphGenC), c_int32, c_int32, c_void_p, c_void_p, c_void_p]),
+    "nc_graphgen_fill": (c_int32, [C.POINTER(GraphGenC), c_int32, c_int32, c_void_p, c_void_p, c_void_p, c_void_p,
+                                   c_void_p, c_void_p]),
+    "nc_sell_fill_pads": (c_int32, [c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p]),
+    "nc_dest_mask_from_csr": (c_int32, [c_void_p, c_int32, c_void_p, c_int32, c_void_p, c_int32, c_int32, c_void_p,
                                         c_void_p]),
     "nc_xchg_reset": (c_int32, [C.POINTER(XchgC), c_void_p]),
     "nc_xchg_seal": (c_int32, [C.POINTER(XchgC), c_int32, c_void_p]),

@@ -119,79 +119,98 @@ __device__ void for_each_upper(const nc_graphgen_t& g, const Comm& cm, int64_t i
   }
 }
 
-__global__ void k_count(const nc_graphgen_t g, int32_t* lower_len, int32_t* upper_len) {
-  const Comm cm = make_comm(g);
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n_neurons;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const bool mine = g.owner[i] == g.shard;
-    const uint32_t inh_i = is_inh(g, i);
-    int32_t up[2] = {0, 0};
-    for_each_upper(g, cm, i, [&](int64_t j, bool) {
-      ++up[is_inh(g, j)];
-      if (g.owner[j] == g.shard) atomicAdd(lower_len + 2 * (g.internal_id[j] - g.local_base) + inh_i, 1);
-    });
-    if (mine) {
-      const int64_t r = g.internal_id[i] - g.local_base;
-      upper_len[2 * r] = up[0];
-      upper_len[2 * r + 1] = up[1];
-    }
-  }
+__device__ __forceinline__ int64_t seg_index(int64_t row, int32_t T, int32_t TW, uint32_t pre_internal,
+                                             uint32_t inh) {
+  return (row * T + (int64_t)((pre_internal >> 5) / (uint32_t)TW)) * 2 + inh;
 }
 
-__global__ void k_fill(const nc_graphgen_t g, const int64_t* rowptr4, const int32_t* lower_len,
-                       int32_t* lower_fill, uint32_t* syn) {
+// Pass 1: entries per (row, tile, sign).  Upper entries of row i are only
+// produced by row i's thread (plain increments); lower ones use atomics.
+__global__ void k_count(const nc_graphgen_t g, int32_t T, int32_t TW, int32_t* lower_len, int32_t* upper_len) {
   const Comm cm = make_comm(g);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n_neurons;
        i += (int64_t)gridDim.x * blockDim.x) {
     const bool mine = g.owner[i] == g.shard;
     const uint32_t iid = (uint32_t)g.internal_id[i];
     const uint32_t inh_i = is_inh(g, i);
-    int64_t out[2] = {0, 0};
-    if (mine) {
-      const int64_t r = iid - g.local_base;
-      out[0] = rowptr4[2 * r] * 4 + lower_len[2 * r];
-      out[1] = rowptr4[2 * r + 1] * 4 + lower_len[2 * r + 1];
-    }
+    const int64_t ri = (int64_t)iid - g.local_base;
+    for_each_upper(g, cm, i, [&](int64_t j, bool) {
+      const uint32_t jid = (uint32_t)g.internal_id[j];
+      if (mine) upper_len[seg_index(ri, T, TW, jid, is_inh(g, j))] += 1;
+      if (g.owner[j] == g.shard) atomicAdd(lower_len + seg_index((int64_t)jid - g.local_base, T, TW, iid, inh_i), 1);
+    });
+  }
+}
+
+// Position of the k-th entry of (row, tile, sign) in the SELL-32 layout (uint32 units).
+__device__ __forceinline__ int64_t sell_pos(const int64_t* slice_ptr, const uint16_t* row_emid, int32_t T,
+                                            int64_t row, int64_t seg, int32_t k) {
+  const int64_t t = (seg >> 1) - row * T;
+  const int64_t blk = slice_ptr[(row >> 5) * T + t];
+  const int64_t slot = ((seg & 1) ? (int64_t)row_emid[row * T + t] : 0) + (k >> 2);
+  return (blk + slot * 32 + (row & 31)) * 4 + (k & 3);
+}
+
+// Pass 2: regenerate the same edges and place them; slots inside a
+// (row, tile, sign) segment are claimed with atomics (any order is fine:
+// delivery sums integers).
+__global__ void k_fill(const nc_graphgen_t g, int32_t T, int32_t TW, const int64_t* slice_ptr,
+                       const uint16_t* row_emid, int32_t* fill, uint32_t* syn) {
+  const Comm cm = make_comm(g);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n_neurons;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const bool mine = g.owner[i] == g.shard;
+    const uint32_t iid = (uint32_t)g.internal_id[i];
+    const uint32_t inh_i = is_inh(g, i);
+    const int64_t ri = (int64_t)iid - g.local_base;
     for_each_upper(g, cm, i, [&](int64_t j, bool intra) {
       const bool jm = g.owner[j] == g.shard;
       if (!mine && !jm) return;
       const uint32_t q = edge_q(g, i, j, intra);
-      if (mine) syn[out[is_inh(g, j)]++] = pack((uint32_t)g.internal_id[j], q);
+      const uint32_t jid = (uint32_t)g.internal_id[j];
+      if (mine) {
+        const int64_t seg = seg_index(ri, T, TW, jid, is_inh(g, j));
+        const int32_t k = atomicAdd(fill + seg, 1);
+        syn[sell_pos(slice_ptr, row_emid, T, ri, seg, k)] = pack(jid, q);
+      }
       if (jm) {
-        const int64_t seg = 2 * (g.internal_id[j] - g.local_base) + inh_i;
-        const int32_t slot = atomicAdd(lower_fill + seg, 1);
-        syn[rowptr4[seg] * 4 + slot] = pack(iid, q);
+        const int64_t rj = (int64_t)jid - g.local_base;
+        const int64_t seg = seg_index(rj, T, TW, iid, inh_i);
+        const int32_t k = atomicAdd(fill + seg, 1);
+        syn[sell_pos(slice_ptr, row_emid, T, rj, seg, k)] = pack(iid, q);
       }
     });
   }
 }
 
-// Fill the pad entries [segment length, 4*ceil(len/4)) of every segment.
-__global__ void k_pad(const int64_t* rowptr4, const int32_t* lower_len, const int32_t* upper_len,
-                      int64_t n_seg, uint32_t pad_entry, uint32_t* syn) {
-  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n_seg;
-       s += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t beg = rowptr4[s] * 4 + lower_len[s] + upper_len[s];
-    const int64_t end = rowptr4[s + 1] * 4;
-    for (int64_t k = beg; k < end; ++k) syn[k] = pad_entry;
+// Pad pre-fill: every entry of block (slice, tile t) = first id of tile t with
+// q = 0, so an unused slot looks up a staged word and adds nothing.
+__global__ void k_fill_pads(const int64_t* slice_ptr, int64_t n_blocks, int32_t T, int32_t TW, uint32_t* syn) {
+  for (int64_t b = blockIdx.x; b < n_blocks; b += gridDim.x) {
+    const uint32_t pad = (uint32_t)((b % T) * (int64_t)TW * 32);
+    const uint4 v = make_uint4(pad, pad, pad, pad);
+    uint4* s4 = reinterpret_cast<uint4*>(syn);
+    for (int64_t k = slice_ptr[b] + threadIdx.x; k < slice_ptr[b + 1]; k += blockDim.x) s4[k] = v;
   }
 }
 
-__global__ void k_dest_mask(const int64_t* rowptr4, const uint32_t* syn, int32_t n_local,
-                            const int32_t* shard_base, int32_t n_shards, int32_t self,
-                            uint16_t* dest) {
+__global__ void k_dest_mask(const int64_t* slice_ptr, int32_t T, const uint32_t* syn, int32_t n_local,
+                            const int32_t* shard_base, int32_t n_shards, int32_t self, uint16_t* dest) {
   const int lane = threadIdx.x & 31;
   const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t r = wid; r < n_local; r += nw) {
     uint32_t m = 0;
-    for (int64_t k = rowptr4[2 * r] * 4 + lane; k < rowptr4[2 * r + 2] * 4; k += 32) {
-      const uint32_t pre = syn[k] & 0x03FFFFFFu;
-      // owner: last shard whose base <= pre; the guard id is past every shard
-      int s = -1;
-      for (int h = 0; h < n_shards; ++h)
-        if ((int64_t)pre >= shard_base[h] && (int64_t)pre < shard_base[h + 1]) s = h;
-      if (s >= 0) m |= 1u << s;
+    for (int32_t t = 0; t < T; ++t) {
+      const int64_t b0 = slice_ptr[(r >> 5) * T + t], b1 = slice_ptr[(r >> 5) * T + t + 1];
+      const int64_t len = (b1 - b0) >> 5;
+      for (int64_t k = lane; k < len * 4; k += 32) {
+        const uint32_t e = syn[(b0 + (k >> 2) * 32 + (r & 31)) * 4 + (k & 3)];
+        if ((e >> 26) == 0) continue;  // pad
+        const int64_t pre = e & 0x03FFFFFFu;
+        for (int h = 0; h < n_shards; ++h)
+          if (pre >= shard_base[h] && pre < shard_base[h + 1]) m |= 1u << h;
+      }
     }
     m = __reduce_or_sync(0xffffffffu, m);
     if (lane == 0) dest[r] = (uint16_t)(m & ~(1u << self));
@@ -209,39 +228,43 @@ int grid_for(int64_t n, int threads) {
 
 }  // namespace
 
-extern "C" int nc_graphgen_count(const nc_graphgen_t* g, int32_t* lower_len, int32_t* upper_len,
-                                 void* stream) {
-  if (!g || g->n_neurons < 1 || g->n_communities < 1 || g->n_communities > g->n_neurons) {
+extern "C" int nc_graphgen_count(const nc_graphgen_t* g, int32_t n_tiles, int32_t tile_words, int32_t* lower_len,
+                                 int32_t* upper_len, void* stream) {
+  if (!g || g->n_neurons < 1 || g->n_communities < 1 || g->n_communities > g->n_neurons || n_tiles < 1 ||
+      tile_words < 1) {
     nc_set_error("nc_graphgen_count: invalid generator spec");
     return NC_E_ARG;
   }
-  k_count<<<grid_for(g->n_neurons, 128), 128, 0, (cudaStream_t)stream>>>(*g, lower_len, upper_len);
+  k_count<<<grid_for(g->n_neurons, 128), 128, 0, (cudaStream_t)stream>>>(*g, n_tiles, tile_words, lower_len,
+                                                                           upper_len);
   NC_LAUNCH_CHECK();
   return NC_OK;
 }
 
-extern "C" int nc_graphgen_fill(const nc_graphgen_t* g, const int64_t* rowptr4, const int32_t* lower_len,
-                                int32_t* lower_fill, uint32_t* syn, void* stream) {
-  if (!g) {
-    nc_set_error("nc_graphgen_fill: null spec");
+extern "C" int nc_graphgen_fill(const nc_graphgen_t* g, int32_t n_tiles, int32_t tile_words, const int64_t* slice_ptr,
+                                const uint16_t* row_emid, const int32_t* lower_len, int32_t* lower_fill, uint32_t* syn,
+                                void* stream) {
+  (void)lower_len;
+  if (!g || n_tiles < 1 || tile_words < 1) {
+    nc_set_error("nc_graphgen_fill: bad arguments");
     return NC_E_ARG;
   }
-  k_fill<<<grid_for(g->n_neurons, 128), 128, 0, (cudaStream_t)stream>>>(*g, rowptr4, lower_len,
-                                                                          lower_fill, syn);
+  k_fill<<<grid_for(g->n_neurons, 128), 128, 0, (cudaStream_t)stream>>>(*g, n_tiles, tile_words, slice_ptr,
+                                                                          row_emid, lower_fill, syn);
   NC_LAUNCH_CHECK();
   return NC_OK;
 }
 
-extern "C" int nc_graphgen_pad(const int64_t* rowptr4, const int32_t* lower_len, const int32_t* upper_len,
-                               int32_t n_local, uint32_t pad_entry, uint32_t* syn, void* stream) {
-  k_pad<<<grid_for(2 * (int64_t)n_local, 256), 256, 0, (cudaStream_t)stream>>>(rowptr4, lower_len, upper_len,
-                                                                                2 * (int64_t)n_local, pad_entry,
-                                                                                syn);
+extern "C" int nc_sell_fill_pads(const int64_t* slice_ptr, int64_t n_blocks, int32_t n_tiles, int32_t tile_words,
+                                 uint32_t* syn, void* stream) {
+  if (n_blocks <= 0) return NC_OK;
+  int64_t grid = n_blocks < 65535 ? n_blocks : 65535;
+  k_fill_pads<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(slice_ptr, n_blocks, n_tiles, tile_words, syn);
   NC_LAUNCH_CHECK();
   return NC_OK;
 }
 
-extern "C" int nc_dest_mask_from_csr(const int64_t* rowptr4, const uint32_t* syn, int32_t n_local,
+extern "C" int nc_dest_mask_from_csr(const int64_t* slice_ptr, int32_t n_tiles, const uint32_t* syn, int32_t n_local,
                                      const int32_t* shard_base, int32_t n_shards, int32_t self,
                                      uint16_t* dest_mask, void* stream) {
   if (n_shards < 1 || n_shards > NC_MAX_SHARDS) {
@@ -250,7 +273,7 @@ extern "C" int nc_dest_mask_from_csr(const int64_t* rowptr4, const uint32_t* syn
   }
   if (n_local == 0) return NC_OK;
   k_dest_mask<<<grid_for((int64_t)n_local * 32, 256), 256, 0, (cudaStream_t)stream>>>(
-      rowptr4, syn, n_local, shard_base, n_shards, self, dest_mask);
+      slice_ptr, n_tiles, syn, n_local, shard_base, n_shards, self, dest_mask);
   NC_LAUNCH_CHECK();
   return NC_OK;
 }

@@ -1,18 +1,20 @@
 // Per-timestep hot loop of the spiking simulator on sm_100a.
 //
-//   K3 deliver (pull): integer segmented reduction over the post-sorted CSR,
-//      one warp per row, 16-byte streaming loads, pre-spike bitmap staged in
-//      shared memory; no float atomics -- the integer sum is order free, so
-//      every reduction order gives the same int and hence the same fp32 input.
+//   K3 deliver (pull): integer reduction over the pull synapse matrix in the
+//      SELL-32 layout (include/neurocomm_b200.h): a warp owns 32 consecutive
+//      post rows, every lane streams its own row with 16-byte coalesced loads
+//      (512 contiguous bytes per warp per slot) and looks each pre up in the
+//      previous step's spike bitmap staged in shared memory (tile by tile when
+//      it exceeds one tile).  No float atomics and no cross-lane reduction: the
+//      row sum is an int32 in the lane that owns the neuron, exact and order
+//      free.
 //   K1 LIF update: fp32 with explicit _rn intrinsics in the fixed order of
 //      DESIGN.md section 3 (no FMA contraction), Philox drive.
 //   K2 spike detect/bucket: __ballot_sync/__popc warp-aggregated appends of
 //      fired internal ids into per-destination buckets (hop_mask from the
 //      reference's RoutingTable, routing.py:184-231).
-// nc_sim_step_fused runs K3+K1+K2 in one pass: a warp owns a tile of 32
-// consecutive rows, reduces each row into the lane that owns that neuron and
-// then updates the 32 neurons together, so the synaptic input never touches
-// HBM.  The unfused entry points exist for the event-driven delivery variant.
+// nc_sim_step_fused runs K3+K1+K2 in one pass, so the synaptic input never
+// touches HBM.  The unfused entry points exist for the event-driven variant.
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -22,7 +24,7 @@
 namespace {
 
 constexpr int kThreads = 1024;    // one CTA per SM in the smem-bitmap variant
-constexpr int kUnroll = 6;        // uint4 loads in flight per lane per row
+constexpr int kUnroll = 8;        // 16-byte slots in flight per lane
 constexpr uint32_t kFull = 0xffffffffu;
 
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
@@ -52,31 +54,37 @@ __device__ __forceinline__ int32_t quad_term(uint4 e, const uint32_t* __restrict
   return entry_term(e.x, bm) + entry_term(e.y, bm) + entry_term(e.z, bm) + entry_term(e.w, bm);
 }
 
-// Pull sum of one row by the whole warp: excitatory segment [beg, mid),
-// inhibitory segment [mid, end) (uint4 units); returns sum_E - g * sum_I.
-template <bool kStream>
-__device__ __forceinline__ int32_t row_sum(const uint4* __restrict__ syn4, int64_t beg, int64_t mid, int64_t end,
-                                           const uint32_t* __restrict__ bm, int32_t g_inh, int lane) {
+// One lane's row in one SELL-32 block: slots [0, len) at blk + u*32 + lane;
+// slots below emid are excitatory.  Returns sum_E - g * sum_I (weight units).
+__device__ __forceinline__ int32_t sell_row_sum(const uint4* __restrict__ blk, int len, int emid,
+                                                const uint32_t* __restrict__ bm, int32_t g_inh, int lane) {
   int32_t se = 0, si = 0;
-  for (int64_t k0 = beg + lane; k0 < end; k0 += 32 * kUnroll) {
+  const uint4* p = blk + lane;
+  int u0 = 0;
+  for (; u0 + kUnroll <= len; u0 += kUnroll) {
     uint4 e[kUnroll];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const int64_t k = k0 + 32 * u;
-      e[u] = (k < end) ? (kStream ? ld_stream(syn4 + k) : ld_keep(syn4 + k))
-                       : make_uint4(0u, 0u, 0u, 0u);
-    }
+    for (int u = 0; u < kUnroll; ++u) e[u] = ld_stream(p + (u0 + u) * 32);
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      const int64_t k = k0 + 32 * u;
-      if (k < end) {
-        const int32_t t = quad_term(e[u], bm);
-        if (k < mid) se += t;
-        else si += t;
-      }
+      const int32_t t = quad_term(e[u], bm);
+      if (u0 + u < emid) se += t;
+      else si += t;
     }
   }
-  return __reduce_add_sync(kFull, se - g_inh * si);
+  if (u0 < len) {  // uniform tail: < kUnroll slots
+    uint4 e[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+      e[u] = (u0 + u < len) ? ld_stream(p + (u0 + u) * 32) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int32_t t = quad_term(e[u], bm);   // zero entries have q = 0
+      if (u0 + u < emid) se += t;
+      else si += t;
+    }
+  }
+  return se - g_inh * si;
 }
 
 // Exact LIF step; returns true if the neuron fired.  Operation order is the
@@ -172,7 +180,27 @@ __device__ __forceinline__ void add_spike_total(const nc_shard_t& sh, uint32_t l
     atomicAdd(sh.spike_total, (unsigned long long)*block_count);
 }
 
-template <bool kSmemBitmap>
+// LIF + spike emission for the 32 rows of one slice (lane = row).
+__device__ __forceinline__ uint32_t update_slice(const nc_shard_t& sh, const nc_lif_params_t& p, uint32_t* cur,
+                                                 int slice, int lane, int32_t acc, int step) {
+  const int row = (slice << 5) + lane;
+  bool fired = false;
+  if (row < sh.n_local) {
+    float v = sh.v[row];
+    float isyn = sh.i_syn[row];
+    uint8_t ref = sh.refrac[row];
+    fired = lif_step(v, isyn, ref, acc, sh.gid[row], (uint32_t)step, p);
+    sh.v[row] = v;
+    sh.i_syn[row] = isyn;
+    sh.refrac[row] = ref;
+  }
+  return emit_spikes(sh, cur, slice, row, fired, lane, step);
+}
+
+// K3 (+K1+K2 when kLif).  kTiled: the bitmap does not fit in shared memory;
+// every CTA owns a fixed range of slices, loops over the bitmap tiles and
+// keeps the per-row partial sums in shared memory behind the tile.
+template <bool kTiled, bool kLif>
 __global__ void __launch_bounds__(kThreads, 1)
 k_step_fused(const nc_shard_t sh, const nc_lif_params_t p) {
   extern __shared__ uint4 smem4[];
@@ -180,77 +208,73 @@ k_step_fused(const nc_shard_t sh, const nc_lif_params_t p) {
   const int step = *sh.step;
   const uint32_t* prev = ((step - 1) & 1) ? sh.bitmap1 : sh.bitmap0;
   uint32_t* cur = (step & 1) ? sh.bitmap1 : sh.bitmap0;
+  uint32_t* sbm = reinterpret_cast<uint32_t*>(smem4);
   if (threadIdx.x == 0) block_count = 0;
-  if (kSmemBitmap) {
-    const uint4* src = reinterpret_cast<const uint4*>(prev);
-    const int n4 = (sh.n_words + 3) >> 2;
-    for (int k = threadIdx.x; k < n4; k += blockDim.x) smem4[k] = ld_keep(src + k);
-  }
-  __syncthreads();
-  const uint32_t* bm = kSmemBitmap ? reinterpret_cast<const uint32_t*>(smem4) : prev;
-  clear_remote(sh, cur);
-
+  if (kLif) clear_remote(sh, cur);
   const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
   const int wpb = blockDim.x >> 5;
-  const int ntiles = (sh.n_local + 31) >> 5;
+  const int n_slices = (sh.n_local + 31) >> 5;
   const int32_t g_inh = p.g_inh;
   const uint4* syn4 = reinterpret_cast<const uint4*>(sh.syn);
   uint32_t my_spikes = 0;
 
-  for (int tile = blockIdx.x * wpb + (threadIdx.x >> 5); tile < ntiles; tile += gridDim.x * wpb) {
-    const int row0 = tile << 5;
-    const int nrows = min(32, sh.n_local - row0);
-    // lane l holds the E and I segment starts of row row0+l; lane nrows the end
-    const int64_t rpe = sh.rowptr4[2 * (row0 + min(lane, nrows))];
-    const int64_t rpi = lane < nrows ? sh.rowptr4[2 * (row0 + lane) + 1] : rpe;
-    const int64_t rp_last = sh.rowptr4[2 * (row0 + nrows)];
-    int32_t my_acc = 0;
-    for (int r = 0; r < nrows; ++r) {
-      const int64_t beg = __shfl_sync(kFull, rpe, r);
-      const int64_t mid = __shfl_sync(kFull, rpi, r);
-      const int64_t nxt = __shfl_sync(kFull, rpe, r + 1 < 32 ? r + 1 : 31);
-      const int64_t end = (r + 1 < nrows) ? nxt : rp_last;
-      const int32_t s = row_sum<true>(syn4, beg, mid, end, bm, g_inh, lane);
-      if (lane == r) my_acc = s;
-    }
-    const int row = row0 + lane;
-    bool fired = false;
-    if (lane < nrows) {
-      float v = sh.v[row];
-      float isyn = sh.i_syn[row];
-      uint8_t ref = sh.refrac[row];
-      fired = lif_step(v, isyn, ref, my_acc, sh.gid[row], (uint32_t)step, p);
-      sh.v[row] = v;
-      sh.i_syn[row] = isyn;
-      sh.refrac[row] = ref;
-    }
-    const uint32_t fm = emit_spikes(sh, cur, tile, row, fired, lane, step);
-    if (lane == 0) my_spikes += __popc(fm);
-  }
-  add_spike_total(sh, my_spikes, &block_count);
-}
-
-// K3 alone: acc[r] = pull sum.
-template <bool kSmemBitmap>
-__global__ void __launch_bounds__(kThreads, 1) k_deliver_pull(const nc_shard_t sh, int32_t g_inh) {
-  extern __shared__ uint4 smem4[];
-  const int step = *sh.step;
-  const uint32_t* prev = ((step - 1) & 1) ? sh.bitmap1 : sh.bitmap0;
-  if (kSmemBitmap) {
+  if (!kTiled) {
     const uint4* src = reinterpret_cast<const uint4*>(prev);
     const int n4 = (sh.n_words + 3) >> 2;
     for (int k = threadIdx.x; k < n4; k += blockDim.x) smem4[k] = ld_keep(src + k);
     __syncthreads();
+    for (int slice = blockIdx.x * wpb + warp; slice < n_slices; slice += gridDim.x * wpb) {
+      const int row = (slice << 5) + lane;
+      const int64_t b0 = sh.slice_ptr[slice];
+      const int len = (int)((sh.slice_ptr[slice + 1] - b0) >> 5);
+      const int emid = row < sh.n_local ? (int)sh.row_emid[row] : 0;
+      const int32_t acc = sell_row_sum(syn4 + b0, len, emid, sbm, g_inh, lane);
+      if (kLif) {
+        const uint32_t fm = update_slice(sh, p, cur, slice, lane, acc, step);
+        if (lane == 0) my_spikes += __popc(fm);
+      } else if (row < sh.n_local) {
+        sh.acc[row] = acc;
+      }
+    }
+  } else {
+    const int T = sh.n_tiles, TW = sh.tile_words;
+    const int per = (n_slices + gridDim.x - 1) / gridDim.x;
+    const int s0 = blockIdx.x * per;
+    const int s1 = min(n_slices, s0 + per);
+    int32_t* part = reinterpret_cast<int32_t*>(sbm + TW);
+    for (int k = threadIdx.x; k < per * 32; k += blockDim.x) part[k] = 0;
+    for (int t = 0; t < T; ++t) {
+      __syncthreads();
+      const int w0 = t * TW;
+      const int nw = min(TW, sh.n_words - w0);
+      const uint4* src = reinterpret_cast<const uint4*>(prev + w0);
+      for (int k = threadIdx.x; k < (nw + 3) >> 2; k += blockDim.x) smem4[k] = ld_keep(src + k);
+      __syncthreads();
+      // tile-relative view: bm[global word] hits the staged copy
+      const uint32_t* bm = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(sbm) -
+                                                             (uintptr_t)w0 * 4u);
+      for (int slice = s0 + warp; slice < s1; slice += wpb) {
+        const int row = (slice << 5) + lane;
+        const int64_t b0 = sh.slice_ptr[(int64_t)slice * T + t];
+        const int len = (int)((sh.slice_ptr[(int64_t)slice * T + t + 1] - b0) >> 5);
+        const int emid = row < sh.n_local ? (int)sh.row_emid[(int64_t)row * T + t] : 0;
+        part[(slice - s0) * 32 + lane] += sell_row_sum(syn4 + b0, len, emid, bm, g_inh, lane);
+      }
+    }
+    __syncthreads();
+    for (int slice = s0 + warp; slice < s1; slice += wpb) {
+      const int row = (slice << 5) + lane;
+      const int32_t acc = part[(slice - s0) * 32 + lane];
+      if (kLif) {
+        const uint32_t fm = update_slice(sh, p, cur, slice, lane, acc, step);
+        if (lane == 0) my_spikes += __popc(fm);
+      } else if (row < sh.n_local) {
+        sh.acc[row] = acc;
+      }
+    }
   }
-  const uint32_t* bm = kSmemBitmap ? reinterpret_cast<const uint32_t*>(smem4) : prev;
-  const int lane = threadIdx.x & 31;
-  const int wpb = blockDim.x >> 5;
-  const uint4* syn4 = reinterpret_cast<const uint4*>(sh.syn);
-  for (int row = blockIdx.x * wpb + (threadIdx.x >> 5); row < sh.n_local; row += gridDim.x * wpb) {
-    const int32_t s = row_sum<true>(syn4, sh.rowptr4[2 * row], sh.rowptr4[2 * row + 1], sh.rowptr4[2 * row + 2],
-                                    bm, g_inh, lane);
-    if (lane == 0) sh.acc[row] = s;
-  }
+  if (kLif) add_spike_total(sh, my_spikes, &block_count);
 }
 
 // K1+K2 alone: consumes and zeroes acc.
@@ -357,13 +381,39 @@ int num_sms() {
   return g_num_sms;
 }
 
-constexpr size_t kMaxSmemBitmapBytes = 200 * 1024;
+constexpr int kMaxDynSmem = 227 * 1024;
 
-size_t bitmap_smem_bytes(const nc_shard_t& sh) { return (size_t)((sh.n_words + 3) >> 2) * 16; }
+// dynamic shared memory of the step kernel: whole bitmap, or one tile plus
+// the per-row partial sums of the CTA's slice range
+size_t step_smem_bytes(const nc_shard_t& sh, int grid) {
+  if (sh.n_tiles <= 1) return (size_t)((sh.n_words + 3) >> 2) * 16;
+  const int n_slices = (sh.n_local + 31) >> 5;
+  const int per = (n_slices + grid - 1) / grid;
+  return (size_t)sh.tile_words * 4 + (size_t)per * 32 * 4;
+}
+
+template <bool kLif>
+int launch_step(const nc_shard_t& sh, const nc_lif_params_t& p, cudaStream_t st) {
+  const int grid = num_sms();
+  const size_t smem = step_smem_bytes(sh, grid);
+  if (smem > (size_t)kMaxDynSmem) {
+    nc_set_error("step kernel needs %zu B of shared memory (tile_words=%d): re-tile the network", smem,
+                 sh.tile_words);
+    return NC_E_ARG;
+  }
+  if (sh.n_tiles <= 1)
+    k_step_fused<false, kLif><<<grid, kThreads, smem, st>>>(sh, p);
+  else
+    k_step_fused<true, kLif><<<grid, kThreads, smem, st>>>(sh, p);
+  NC_LAUNCH_CHECK();
+  return NC_OK;
+}
 
 int check_shard(const nc_shard_t* sh) {
   if (!sh || sh->n_local < 0 || sh->n_words < 1 || (sh->local_base & 31) || !sh->step ||
-      !sh->status || !sh->bitmap0 || !sh->bitmap1) {
+      !sh->status || !sh->bitmap0 || !sh->bitmap1 || sh->n_tiles < 1 ||
+      (sh->n_tiles > 1 && (sh->tile_words < 4 || (sh->tile_words & 3) ||
+                           (int64_t)sh->tile_words * sh->n_tiles < sh->n_words))) {
     nc_set_error("invalid nc_shard_t");
     return NC_E_ARG;
   }
@@ -375,10 +425,14 @@ int check_shard(const nc_shard_t* sh) {
 // Set kernel attributes once, outside any stream capture.
 extern "C" int nc_sim_prepare(void) {
   (void)num_sms();
-  NC_CUDA_TRY(cudaFuncSetAttribute(k_step_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)kMaxSmemBitmapBytes));
-  NC_CUDA_TRY(cudaFuncSetAttribute(k_deliver_pull<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)kMaxSmemBitmapBytes));
+  NC_CUDA_TRY(cudaFuncSetAttribute(k_step_fused<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kMaxDynSmem));
+  NC_CUDA_TRY(cudaFuncSetAttribute(k_step_fused<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kMaxDynSmem));
+  NC_CUDA_TRY(cudaFuncSetAttribute(k_step_fused<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kMaxDynSmem));
+  NC_CUDA_TRY(cudaFuncSetAttribute(k_step_fused<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kMaxDynSmem));
   g_prepared = true;
   return NC_OK;
 }
@@ -392,34 +446,22 @@ extern "C" int nc_sim_init(const nc_shard_t* sh, const nc_lif_params_t* p, void*
 
 extern "C" int nc_sim_step_fused(const nc_shard_t* sh, const nc_lif_params_t* p, void* stream) {
   if (int e = check_shard(sh)) return e;
-  const size_t smem = bitmap_smem_bytes(*sh);
-  const int grid = num_sms();
-  if (smem <= kMaxSmemBitmapBytes) {
-    if (!g_prepared) {
-      if (int e = nc_sim_prepare()) return e;
-    }
-    k_step_fused<true><<<grid, kThreads, smem, (cudaStream_t)stream>>>(*sh, *p);
-  } else {
-    k_step_fused<false><<<grid, kThreads, 0, (cudaStream_t)stream>>>(*sh, *p);
-  }
-  NC_LAUNCH_CHECK();
-  return NC_OK;
+  if (!g_prepared)
+    if (int e = nc_sim_prepare()) return e;
+  return launch_step<true>(*sh, *p, (cudaStream_t)stream);
 }
 
 extern "C" int nc_sim_deliver_pull(const nc_shard_t* sh, int32_t g_inh, void* stream) {
   if (int e = check_shard(sh)) return e;
-  const size_t smem = bitmap_smem_bytes(*sh);
-  const int grid = num_sms();
-  if (smem <= kMaxSmemBitmapBytes) {
-    if (!g_prepared) {
-      if (int e = nc_sim_prepare()) return e;
-    }
-    k_deliver_pull<true><<<grid, kThreads, smem, (cudaStream_t)stream>>>(*sh, g_inh);
-  } else {
-    k_deliver_pull<false><<<grid, kThreads, 0, (cudaStream_t)stream>>>(*sh, g_inh);
+  if (!sh->acc) {
+    nc_set_error("nc_sim_deliver_pull: shard has no acc buffer");
+    return NC_E_ARG;
   }
-  NC_LAUNCH_CHECK();
-  return NC_OK;
+  if (!g_prepared)
+    if (int e = nc_sim_prepare()) return e;
+  nc_lif_params_t p{};
+  p.g_inh = g_inh;
+  return launch_step<false>(*sh, p, (cudaStream_t)stream);
 }
 
 extern "C" int nc_sim_deliver_push(const nc_shard_t* sh, int32_t g_inh, void* stream) {

@@ -29,6 +29,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native
+from . import sell
 from .model import INTER_P_RANGE, INTRA_P_RANGE, ModelSpec, NeuronGraph, community_sizes
 from .routing import RoutingTable
 
@@ -37,8 +38,8 @@ __all__ = [
     "q_from_p", "inhibitory_mask", "ID_BITS",
 ]
 
-ID_BITS = 26            # packed pull entry: (q << 26) | pre internal id
-ID_MASK = (1 << ID_BITS) - 1
+ID_BITS = sell.ID_BITS  # packed pull entry: (q << 26) | pre internal id
+ID_MASK = sell.ID_MASK
 Q_LEVELS = 32           # synaptic weight units: q = ceil(32 p) in [1, 32]
 
 
@@ -178,46 +179,24 @@ class ShardLayout:
     def guard_id(self) -> int:
         return (self.n_words - 1) * 32
 
-    @property
-    def pad_entry(self) -> int:
-        return (1 << ID_BITS) | self.guard_id
-
     def n_local(self, h: int) -> int:
         return int(self.members[h].size)
 
 
 # ---------------------------------------------------------------- network
 
-def _pack(pre_internal, q):
-    return (q.astype(np.uint32) << np.uint32(ID_BITS)) | pre_internal.astype(np.uint32)
-
-
-def host_pull_csr(graph: NeuronGraph, layout: ShardLayout, shard: int, inh_every: int):
-    """Pull CSR of one shard from a host NeuronGraph.
-
-    Segment 2r holds the excitatory pres of local post row r, 2r+1 the
-    inhibitory ones; every segment is padded to a multiple of 4 entries.
-    """
+def host_sell(graph: NeuronGraph, layout: ShardLayout, shard: int, inh_every: int, n_tiles: int,
+              tile_words: int):
+    """SELL-32 arrays of one shard from a host NeuronGraph (numpy; see sell.py)."""
     q = q_from_p(graph.edge_p)
     post = np.concatenate([graph.edge_j, graph.edge_i]).astype(np.int64)
     pre = np.concatenate([graph.edge_i, graph.edge_j]).astype(np.int64)
     qq = np.concatenate([q, q])
     keep = layout.owner[post] == shard
     post, pre, qq = post[keep], pre[keep], qq[keep]
-    n_local = layout.n_local(shard)
     row = layout.internal_id[post].astype(np.int64) - int(layout.base[shard])
-    seg = 2 * row + inhibitory_mask(pre, inh_every)
-    entries = _pack(layout.internal_id[pre], qq)
-    counts = np.bincount(seg, minlength=2 * n_local).astype(np.int64)
-    rowptr4 = np.zeros(2 * n_local + 1, dtype=np.int64)
-    rowptr4[1:] = np.cumsum((counts + 3) // 4)
-    syn = np.full(int(rowptr4[-1]) * 4, layout.pad_entry, dtype=np.uint32)
-    order = np.argsort(seg, kind="stable")
-    sseg = seg[order]
-    first = np.cumsum(counts) - counts
-    slot = np.arange(sseg.size, dtype=np.int64) - first[sseg]
-    syn[rowptr4[sseg] * 4 + slot] = entries[order]
-    return rowptr4, syn
+    return sell.host_build(row, layout.internal_id[pre], qq, inhibitory_mask(pre, inh_every),
+                           layout.n_local(shard), n_tiles, tile_words)
 
 
 @dataclass
@@ -242,15 +221,7 @@ class GeneratorSpec:
         return cls(n_neurons, 1, degree / max(n_neurons - 1, 1), 0.0, seed)
 
 
-@dataclass
-class ShardCSR:
-    rowptr4: object   # torch int64 [n_local+1] (device)
-    syn: object       # torch int32 [4*rowptr4[-1]] (device) -- packed uint32 entries
-    dest: object      # torch int32 [n_local] (device) -- shards hosting targets, self excluded
-
-    @property
-    def n_synapses_padded(self) -> int:
-        return int(self.syn.numel())
+ShardCSR = sell.SellCSR
 
 
 class Network:
@@ -268,23 +239,28 @@ class Network:
     # ------------------------------------------------------------ builders
     @classmethod
     def from_graph(cls, graph: NeuronGraph, layout: ShardLayout, *, device=None, inh_every: int = 5,
-                   shards=None) -> "Network":
+                   shards=None, tile_words: int | None = None) -> "Network":
         import torch
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         own = range(layout.n_shards) if shards is None else shards
         out = {}
         nsyn = 0
+        sms = sell.device_sms(dev)
         for h in own:
-            rp, syn = host_pull_csr(graph, layout, h, inh_every)
-            csr = ShardCSR(torch.from_numpy(rp).to(dev), torch.from_numpy(syn.view(np.int32)).to(dev), None)
+            n_local = layout.n_local(h)
+            T, TW = _tiles(layout, n_local, sms, tile_words)
+            ptr, emid, syn = host_sell(graph, layout, h, inh_every, T, TW)
+            n_real = int(np.count_nonzero((syn >> np.uint32(ID_BITS)) > 0))
+            csr = ShardCSR(torch.from_numpy(ptr).to(dev), torch.from_numpy(emid.view(np.int16)).to(dev),
+                           torch.from_numpy(syn.view(np.int32)).to(dev), T, TW, n_local, n_real)
             csr.dest = _dest_masks(csr, layout, h, dev)
             out[h] = csr
-            nsyn += int(np.count_nonzero(syn != np.uint32(layout.pad_entry)))
+            nsyn += n_real
         return cls(layout, out, dev, inh_every, n_synapses=nsyn, source="host graph")
 
     @classmethod
     def generate(cls, spec: GeneratorSpec, layout: ShardLayout, *, device=None, inh_every: int = 5,
-                 shards=None) -> "Network":
+                 shards=None, tile_words: int | None = None) -> "Network":
         """Counter-based device generator (csrc/graphgen.cu); every shard regenerates the same graph."""
         import torch
         if layout.n_neurons != spec.n_neurons:
@@ -301,32 +277,36 @@ class Network:
         own = range(layout.n_shards) if shards is None else shards
         out = {}
         nsyn = 0
+        sms = sell.device_sms(dev)
         for h in own:
             n_local = layout.n_local(h)
+            T, TW = _tiles(layout, n_local, sms, tile_words)
             g = _native.GraphGenC(
                 n_neurons=spec.n_neurons, n_communities=spec.n_communities, shard=h, p_in=spec.p_in,
                 p_out=spec.p_out, intra_lo=spec.intra_p_range[0], intra_hi=spec.intra_p_range[1],
                 inter_lo=spec.inter_p_range[0], inter_hi=spec.inter_p_range[1],
                 seed=int(spec.seed) & (2**64 - 1), owner=owner_d.data_ptr(), internal_id=internal_d.data_ptr(),
                 local_base=int(layout.base[h]), inh_every=inh_every)
-            n_seg = 2 * n_local
-            lower = torch.zeros(max(n_seg, 1), dtype=torch.int32, device=dev)
-            upper = torch.zeros(max(n_seg, 1), dtype=torch.int32, device=dev)
-            _native.check(L.nc_graphgen_count(C.byref(g), lower.data_ptr(), upper.data_ptr(), st), "graphgen count")
-            lens = (lower[:n_seg] + upper[:n_seg]).to(torch.int64)
-            rowptr4 = torch.zeros(n_seg + 1, dtype=torch.int64, device=dev)
-            rowptr4[1:] = torch.cumsum((lens + 3) // 4, 0)
-            total = int(rowptr4[-1].item()) * 4
-            syn = torch.empty(max(total, 4), dtype=torch.int32, device=dev)
-            fill = torch.zeros_like(lower)
-            _native.check(L.nc_graphgen_fill(C.byref(g), rowptr4.data_ptr(), lower.data_ptr(), fill.data_ptr(),
-                                             syn.data_ptr(), st), "graphgen fill")
-            _native.check(L.nc_graphgen_pad(rowptr4.data_ptr(), lower.data_ptr(), upper.data_ptr(), n_local,
-                                            layout.pad_entry, syn.data_ptr(), st), "graphgen pad")
-            csr = ShardCSR(rowptr4, syn, None)
+            n_seg = max(n_local * T * 2, 1)
+            lower = torch.zeros(n_seg, dtype=torch.int32, device=dev)
+            upper = torch.zeros(n_seg, dtype=torch.int32, device=dev)
+            _native.check(L.nc_graphgen_count(C.byref(g), T, TW, lower.data_ptr(), upper.data_ptr(), st),
+                          "graphgen count")
+            counts = (lower + upper)[: n_local * T * 2].to(torch.int64)
+            ptr, emid = sell.layout_from_counts(counts, n_local, T)
+            total = int(ptr[-1].item())
+            syn = torch.zeros(max(total * 4, 4), dtype=torch.int32, device=dev)
+            _native.check(L.nc_sell_fill_pads(ptr.data_ptr(), ptr.numel() - 1, T, TW, syn.data_ptr(), st),
+                          "sell pads")
+            lower.zero_()
+            _native.check(L.nc_graphgen_fill(C.byref(g), T, TW, ptr.data_ptr(), emid.data_ptr(), None,
+                                             lower.data_ptr(), syn.data_ptr(), st), "graphgen fill")
+            n_real = int(counts.sum().item())
+            del upper, counts
+            csr = ShardCSR(ptr, emid, syn, T, TW, n_local, n_real)
             csr.dest = _dest_masks(csr, layout, h, dev)
             out[h] = csr
-            nsyn += int(lens.sum().item())
+            nsyn += n_real
         return cls(layout, out, dev, inh_every, n_synapses=nsyn, source="device generator")
 
     # ------------------------------------------------------------ helpers
@@ -341,21 +321,22 @@ class Network:
 
     def host_csr(self, shard: int):
         """(post_gid, pre_gid, q) of every synapse of one shard, for the oracle (test/bench only)."""
-        csr = self.shards[shard]
-        rp4 = csr.rowptr4.cpu().numpy()
-        syn = csr.syn.cpu().numpy().view(np.uint32)[: int(rp4[-1]) * 4]
-        keep = syn != np.uint32(self.layout.pad_entry)
-        seg = np.repeat(np.arange(rp4.size - 1), np.diff(rp4) * 4)[keep]
-        ent = syn[keep]
+        row, pre_int, q, inh = (x.cpu().numpy() for x in sell.decode(self.shards[shard]))
         gid_of_internal = np.full(self.layout.n_words * 32, -1, dtype=np.int64)
         for h, m in enumerate(self.layout.members):
             gid_of_internal[int(self.layout.base[h]) + np.arange(m.size)] = m
-        pre = gid_of_internal[(ent & np.uint32(ID_MASK)).astype(np.int64)]
-        q = (ent >> np.uint32(ID_BITS)).astype(np.uint8)
-        post = self.layout.members[shard][seg // 2]
-        if (inhibitory_mask(pre, self.inh_every) != (seg % 2 == 1)).any():
-            raise AssertionError("segment / pre type mismatch in the pull CSR")
-        return post, pre, q
+        pre = gid_of_internal[pre_int]
+        if (inhibitory_mask(pre, self.inh_every) != inh).any():
+            raise AssertionError("E/I slot split disagrees with the pre neuron types")
+        return self.layout.members[shard][row], pre, q.astype(np.uint8)
+
+
+def _tiles(layout: ShardLayout, n_local: int, sms: int, tile_words: int | None):
+    """Bitmap tiling: planned from shared memory, or forced (tests) with `tile_words`."""
+    if tile_words is None:
+        return sell.plan_tiles(layout.n_words, n_local, sms)
+    tw = max(4, int(tile_words) // 4 * 4)
+    return (layout.n_words + tw - 1) // tw, tw
 
 
 def _as_u16(t32):
@@ -370,7 +351,8 @@ def _dest_masks(csr: ShardCSR, layout: ShardLayout, h: int, dev):
     bases = torch.from_numpy(layout.base.astype(np.int32)).to(dev)
     out16 = torch.zeros(max(n_local, 1), dtype=torch.int16, device=dev)
     L = _native.lib()
-    _native.check(L.nc_dest_mask_from_csr(csr.rowptr4.data_ptr(), csr.syn.data_ptr(), n_local, bases.data_ptr(),
+    _native.check(L.nc_dest_mask_from_csr(csr.slice_ptr.data_ptr(), csr.n_tiles, csr.syn.data_ptr(), n_local,
+                                          bases.data_ptr(),
                                           layout.n_shards, h, out16.data_ptr(), _native.stream_handle(dev)),
                   "dest mask")
     return out16[:n_local].to(torch.int32) & 0xFFFF
@@ -509,10 +491,11 @@ class _ShardState:
         if push:
             self.push_rowptr, self.push_syn = _push_csr(csr, lay, h, dev)
         self.c = _native.ShardC(
-            shard=h, n_shards=n, n_local=n_local, local_base=int(lay.base[h]), n_words=lay.n_words, pad0=0,
+            shard=h, n_shards=n, n_local=n_local, local_base=int(lay.base[h]), n_words=lay.n_words,
+            n_tiles=csr.n_tiles, tile_words=csr.tile_words, pad0=0,
             v=self.v.data_ptr(), i_syn=self.i_syn.data_ptr(), refrac=self.refrac.data_ptr(),
             acc=self.acc.data_ptr(), gid=self.gid.data_ptr(), hop_mask=self.hop_mask.data_ptr(),
-            rowptr4=csr.rowptr4.data_ptr(), syn=csr.syn.data_ptr(),
+            slice_ptr=csr.slice_ptr.data_ptr(), row_emid=csr.row_emid.data_ptr(), syn=csr.syn.data_ptr(),
             push_rowptr=None if self.push_rowptr is None else self.push_rowptr.data_ptr(),
             push_syn=None if self.push_syn is None else self.push_syn.data_ptr(),
             bitmap0=self.bitmaps[0].data_ptr(), bitmap1=self.bitmaps[1].data_ptr(),
@@ -525,20 +508,11 @@ class _ShardState:
 
 
 def _push_csr(csr: ShardCSR, lay: ShardLayout, h: int, dev):
-    """Transpose of the pull CSR: rows = internal pre ids,
+    """Transpose of the pull synapses: rows = internal pre ids,
     entries = (inhibitory << 31) | ((q - 1) << 26) | post_local."""
     import torch
-    n_local = lay.n_local(h)
-    rp4 = csr.rowptr4
-    total = int(rp4[-1].item()) * 4
-    syn = csr.syn[:total].to(torch.int64) & 0xFFFFFFFF
-    lens4 = (rp4[1:] - rp4[:-1]) * 4
-    seg = torch.repeat_interleave(torch.arange(2 * n_local, device=dev, dtype=torch.int64), lens4)
-    keep = syn != lay.pad_entry
-    syn, seg = syn[keep], seg[keep]
-    pre = syn & ID_MASK
-    q = syn >> ID_BITS
-    ent = ((seg & 1) << 31) | ((q - 1) << ID_BITS) | (seg >> 1)
+    row, pre, q, inh = sell.decode(csr)
+    ent = (inh.to(torch.int64) << 31) | ((q - 1) << ID_BITS) | row
     order = torch.argsort(pre, stable=True)
     pre, ent = pre[order], ent[order]
     n_rows = lay.n_words * 32

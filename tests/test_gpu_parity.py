@@ -155,6 +155,21 @@ def test_partition_invariance_and_route_independence():
     np.testing.assert_array_equal(rep.raster, base.raster)
 
 
+@pytest.mark.parametrize("tile_words", [64, 100])
+def test_tiled_bitmap_matches_oracle(tile_words):
+    """Force the shared-memory tiling of the spike bitmap (used above ~1.8 M neurons)."""
+    g = cfg1(2)
+    pm = nc.partition_greedy(g, 2)
+    rt = routes(g, pm, "direct")
+    lif = S.LifParams()
+    lay = S.ShardLayout.from_assignment(pm.assignment, 2)
+    net = S.Network.from_graph(g, lay, tile_words=tile_words)
+    assert all(c.n_tiles > 1 for c in net.shards.values())
+    for delivery in ("fused", "pull"):
+        rep = S.Simulator(net, lif, 2, rt, delivery=delivery, record_raster_steps=60, per_step_counts=True).run(60)
+        assert_same(rep, oracle_run(g, pm, rt, lif, 2, 60))
+
+
 def test_graph_replay_equals_eager():
     g = cfg1(1)
     pm = nc.partition_greedy(g, 2)
@@ -195,6 +210,7 @@ def test_device_generator_matches_oracle_and_statistics():
     spec = S.GeneratorSpec(12_000, 4, 0.02, 0.002, seed=7)
     lay = S.ShardLayout.blocks(spec.n_neurons, 2)
     net = S.Network.generate(spec, lay)
+    tiled = S.Network.generate(spec, lay, tile_words=40)
     # expected undirected edges
     sizes = nc.model.community_sizes(spec.n_neurons, spec.n_communities)
     intra = sum(s * (s - 1) // 2 for s in sizes.tolist()) * spec.p_in
@@ -219,9 +235,10 @@ def test_device_generator_matches_oracle_and_statistics():
     lif = S.LifParams()
     rt_nh = S.ExchangePlan(2, None).next_hop
     ref = c_oracle.simulate_csr(rp, col, qc, lay.owner, 2, rt_nh, lif.constants(4), 50, threads=8)
-    sim = S.Simulator(net, lif, 4, None, record_raster_steps=50, per_step_counts=True)
-    rep = sim.run(50)
-    np.testing.assert_array_equal(rep.raster, ref["raster"])
-    np.testing.assert_array_equal(rep.deliv_ids, ref["deliv"])
-    np.testing.assert_array_equal(rep.v, ref["v"])
+    for nw in (net, tiled):
+        sim = S.Simulator(nw, lif, 4, None, record_raster_steps=50, per_step_counts=True)
+        rep = sim.run(50)
+        np.testing.assert_array_equal(rep.raster, ref["raster"])
+        np.testing.assert_array_equal(rep.deliv_ids, ref["deliv"])
+        np.testing.assert_array_equal(rep.v, ref["v"])
     del torch
