@@ -381,7 +381,7 @@ int num_sms() {
   return g_num_sms;
 }
 
-constexpr int kMaxDynSmem = 227 * 1024;
+int g_max_dyn_smem = 0;   // opt-in limit minus the kernels' static shared memory
 
 // dynamic shared memory of the step kernel: whole bitmap, or one tile plus
 // the per-row partial sums of the CTA's slice range
@@ -396,7 +396,7 @@ template <bool kLif>
 int launch_step(const nc_shard_t& sh, const nc_lif_params_t& p, cudaStream_t st) {
   const int grid = num_sms();
   const size_t smem = step_smem_bytes(sh, grid);
-  if (smem > (size_t)kMaxDynSmem) {
+  if (smem > (size_t)g_max_dyn_smem) {
     nc_set_error("step kernel needs %zu B of shared memory (tile_words=%d): re-tile the network", smem,
                  sh.tile_words);
     return NC_E_ARG;
@@ -422,17 +422,27 @@ int check_shard(const nc_shard_t* sh) {
 
 }  // namespace
 
+template <typename K>
+int opt_in_smem(K kernel, int optin) {
+  cudaFuncAttributes fa;
+  NC_CUDA_TRY(cudaFuncGetAttributes(&fa, kernel));
+  const int dyn = optin - (int)fa.sharedSizeBytes;
+  NC_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+  if (g_max_dyn_smem == 0 || dyn < g_max_dyn_smem) g_max_dyn_smem = dyn;
+  return NC_OK;
+}
+
 // Set kernel attributes once, outside any stream capture.
 extern "C" int nc_sim_prepare(void) {
   (void)num_sms();
-  NC_CUDA_TRY(cudaFuncSetAttribute(k_step_fused<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   kMaxDynSmem));
-  NC_CUDA_TRY(cudaFuncSetAttribute(k_step_fused<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   kMaxDynSmem));
-  NC_CUDA_TRY(cudaFuncSetAttribute(k_step_fused<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   kMaxDynSmem));
-  NC_CUDA_TRY(cudaFuncSetAttribute(k_step_fused<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   kMaxDynSmem));
+  int dev = 0, optin = 0;
+  NC_CUDA_TRY(cudaGetDevice(&dev));
+  NC_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  g_max_dyn_smem = 0;
+  if (int e = opt_in_smem(k_step_fused<false, true>, optin)) return e;
+  if (int e = opt_in_smem(k_step_fused<true, true>, optin)) return e;
+  if (int e = opt_in_smem(k_step_fused<false, false>, optin)) return e;
+  if (int e = opt_in_smem(k_step_fused<true, false>, optin)) return e;
   g_prepared = true;
   return NC_OK;
 }
