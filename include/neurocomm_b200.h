@@ -291,6 +291,10 @@ typedef struct nc_graphgen {
   int32_t inh_every;          /* gid % inh_every == inh_every-1 is inhibitory (0 = none) */
 } nc_graphgen_t;
 
+/* Pass 0: deg[gid] += number of edges of every neuron (zero-initialised
+ * int32[n_neurons]); owner/internal_id are not read.  The host orders each
+ * shard's rows by degree so the 32 rows of a slice have similar lengths. */
+int nc_graphgen_degrees(const nc_graphgen_t* g, int32_t* deg, void* stream);
 /* Pass 1.  lower_len/upper_len: [n_local * n_tiles * 2] entries per
  * (row, tile, sign) (zero-initialised); tile_words as in nc_shard_t. */
 int nc_graphgen_count(const nc_graphgen_t* g, int32_t n_tiles, int32_t tile_words, int32_t* lower_len,

@@ -142,6 +142,20 @@ __global__ void k_count(const nc_graphgen_t g, int32_t T, int32_t TW, int32_t* l
   }
 }
 
+// Degree of every neuron (both endpoints of every edge), for the SELL row order.
+__global__ void k_degrees(const nc_graphgen_t g, int32_t* deg) {
+  const Comm cm = make_comm(g);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n_neurons;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t up = 0;
+    for_each_upper(g, cm, i, [&](int64_t j, bool) {
+      ++up;
+      atomicAdd(deg + j, 1);
+    });
+    if (up) atomicAdd(deg + i, up);
+  }
+}
+
 // Position of the k-th entry of (row, tile, sign) in the SELL-32 layout (uint32 units).
 __device__ __forceinline__ int64_t sell_pos(const int64_t* slice_ptr, const uint16_t* row_emid, int32_t T,
                                             int64_t row, int64_t seg, int32_t k) {
@@ -237,6 +251,16 @@ extern "C" int nc_graphgen_count(const nc_graphgen_t* g, int32_t n_tiles, int32_
   }
   k_count<<<grid_for(g->n_neurons, 128), 128, 0, (cudaStream_t)stream>>>(*g, n_tiles, tile_words, lower_len,
                                                                            upper_len);
+  NC_LAUNCH_CHECK();
+  return NC_OK;
+}
+
+extern "C" int nc_graphgen_degrees(const nc_graphgen_t* g, int32_t* deg, void* stream) {
+  if (!g || g->n_neurons < 1 || g->n_communities < 1 || g->n_communities > g->n_neurons) {
+    nc_set_error("nc_graphgen_degrees: invalid generator spec");
+    return NC_E_ARG;
+  }
+  k_degrees<<<grid_for(g->n_neurons, 128), 128, 0, (cudaStream_t)stream>>>(*g, deg);
   NC_LAUNCH_CHECK();
   return NC_OK;
 }

@@ -32,8 +32,11 @@ extern "C" int nc_nccl_comm_init(void** comm_out, int32_t nranks, const void* id
   return NC_OK;
 }
 
+// Callers synchronise their streams first; abort then frees the communicator
+// without the collective finalisation handshake (which can block when another
+// communicator of the process is mid-teardown).
 extern "C" int nc_nccl_comm_destroy(void* comm) {
-  if (comm) NC_NCCL_TRY(ncclCommDestroy((ncclComm_t)comm));
+  if (comm) NC_NCCL_TRY(ncclCommAbort((ncclComm_t)comm));
   return NC_OK;
 }
 

@@ -56,8 +56,11 @@ __device__ __forceinline__ int32_t quad_term(uint4 e, const uint32_t* __restrict
 
 // One lane's row in one SELL-32 block: slots [0, len) at blk + u*32 + lane;
 // slots below emid are excitatory.  Returns sum_E - g * sum_I (weight units).
+// `pad` (the block's pad entry: first id of its tile, q = 0) fills the tail
+// registers so that their lookups stay inside the staged tile.
 __device__ __forceinline__ int32_t sell_row_sum(const uint4* __restrict__ blk, int len, int emid,
-                                                const uint32_t* __restrict__ bm, int32_t g_inh, int lane) {
+                                                const uint32_t* __restrict__ bm, int32_t g_inh, int lane,
+                                                uint32_t pad) {
   int32_t se = 0, si = 0;
   const uint4* p = blk + lane;
   int u0 = 0;
@@ -76,7 +79,7 @@ __device__ __forceinline__ int32_t sell_row_sum(const uint4* __restrict__ blk, i
     uint4 e[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u)
-      e[u] = (u0 + u < len) ? ld_stream(p + (u0 + u) * 32) : make_uint4(0u, 0u, 0u, 0u);
+      e[u] = (u0 + u < len) ? ld_stream(p + (u0 + u) * 32) : make_uint4(pad, pad, pad, pad);
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       const int32_t t = quad_term(e[u], bm);   // zero entries have q = 0
@@ -229,7 +232,7 @@ k_step_fused(const nc_shard_t sh, const nc_lif_params_t p) {
       const int64_t b0 = sh.slice_ptr[slice];
       const int len = (int)((sh.slice_ptr[slice + 1] - b0) >> 5);
       const int emid = row < sh.n_local ? (int)sh.row_emid[row] : 0;
-      const int32_t acc = sell_row_sum(syn4 + b0, len, emid, sbm, g_inh, lane);
+      const int32_t acc = sell_row_sum(syn4 + b0, len, emid, sbm, g_inh, lane, 0u);
       if (kLif) {
         const uint32_t fm = update_slice(sh, p, cur, slice, lane, acc, step);
         if (lane == 0) my_spikes += __popc(fm);
@@ -259,7 +262,7 @@ k_step_fused(const nc_shard_t sh, const nc_lif_params_t p) {
         const int64_t b0 = sh.slice_ptr[(int64_t)slice * T + t];
         const int len = (int)((sh.slice_ptr[(int64_t)slice * T + t + 1] - b0) >> 5);
         const int emid = row < sh.n_local ? (int)sh.row_emid[(int64_t)row * T + t] : 0;
-        part[(slice - s0) * 32 + lane] += sell_row_sum(syn4 + b0, len, emid, bm, g_inh, lane);
+        part[(slice - s0) * 32 + lane] += sell_row_sum(syn4 + b0, len, emid, bm, g_inh, lane, (uint32_t)w0 * 32u);
       }
     }
     __syncthreads();

@@ -228,6 +228,9 @@ class DistSimulator:
         import torch
         import torch.distributed as dist
         torch.cuda.synchronize(self.dev)
+        # captured graphs reference the communicator and the IPC windows
+        self._graph = None
+        torch.cuda.synchronize(self.dev)
         dist.barrier()
         for p in self._ipc_peer:
             self.lib.nc_ipc_close(C.c_void_p(p))
