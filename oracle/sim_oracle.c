@@ -135,6 +135,7 @@ int oracle_simulate(int64_t M, const int64_t* rowptr, const int32_t* col, const 
   uint8_t* cur = (uint8_t*)calloc(M, 1);
   uint32_t* dests = (uint32_t*)calloc(M, sizeof(uint32_t));
   int rc = 0;
+#pragma omp parallel for schedule(dynamic, 1024) reduction(min : rc)
   for (int64_t i = 0; i < M; ++i) {
     v[i] = v_initial((uint32_t)i, p);
     isyn[i] = 0.0f;

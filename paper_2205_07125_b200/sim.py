@@ -149,13 +149,20 @@ class ShardLayout:
     n_words: int               # bitmap words incl. a guard word, multiple of 4
 
     @classmethod
-    def from_assignment(cls, assignment, n_shards: int) -> "ShardLayout":
+    def from_assignment(cls, assignment, n_shards: int, order_key=None) -> "ShardLayout":
+        """Shards from a PartitionMap assignment.  Inside a shard, neurons are in
+        ascending gid, or by descending `order_key` (ties: gid) when given --
+        the engine passes the degree so the 32 rows of a SELL slice have
+        similar lengths (less padding)."""
         owner = np.ascontiguousarray(assignment, dtype=np.int64)
         if owner.size and (owner.min() < 0 or owner.max() >= n_shards):
             raise ValueError("assignment has GPU indices outside [0, n_gpus)")
         if n_shards > _native.MAX_SHARDS:
             raise ValueError(f"at most {_native.MAX_SHARDS} shards are supported, got {n_shards}")
         members = [np.flatnonzero(owner == h) for h in range(n_shards)]
+        if order_key is not None:
+            key = np.asarray(order_key)
+            members = [m[np.lexsort((m, -key[m]))] for m in members]
         counts = np.array([m.size for m in members], dtype=np.int64)
         padded = (counts + 31) // 32 * 32
         base = np.zeros(n_shards + 1, dtype=np.int64)
@@ -174,6 +181,10 @@ class ShardLayout:
         """Contiguous near-equal blocks (the placement greedy recovers on C = N planted graphs)."""
         sizes = community_sizes(n_neurons, n_shards)
         return cls.from_assignment(np.repeat(np.arange(n_shards), sizes), n_shards)
+
+    def reordered(self, order_key) -> "ShardLayout":
+        """Same shards, rows ordered by descending `order_key` inside each shard."""
+        return ShardLayout.from_assignment(self.owner, self.n_shards, order_key)
 
     @property
     def guard_id(self) -> int:
@@ -242,6 +253,9 @@ class Network:
                    shards=None, tile_words: int | None = None) -> "Network":
         import torch
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        deg = np.bincount(graph.edge_i, minlength=graph.n_neurons) + np.bincount(graph.edge_j,
+                                                                               minlength=graph.n_neurons)
+        layout = layout.reordered(deg)
         own = range(layout.n_shards) if shards is None else shards
         out = {}
         nsyn = 0
@@ -272,6 +286,16 @@ class Network:
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         L = _native.lib()
         st = _native.stream_handle(dev)
+        # pass 0: degrees -> rows of each shard ordered by degree (SELL padding)
+        g0 = _native.GraphGenC(
+            n_neurons=spec.n_neurons, n_communities=spec.n_communities, shard=0, p_in=spec.p_in, p_out=spec.p_out,
+            intra_lo=spec.intra_p_range[0], intra_hi=spec.intra_p_range[1], inter_lo=spec.inter_p_range[0],
+            inter_hi=spec.inter_p_range[1], seed=int(spec.seed) & (2**64 - 1), owner=None, internal_id=None,
+            local_base=0, inh_every=inh_every)
+        deg = torch.zeros(spec.n_neurons, dtype=torch.int32, device=dev)
+        _native.check(L.nc_graphgen_degrees(C.byref(g0), deg.data_ptr(), st), "graphgen degrees")
+        layout = layout.reordered(deg.cpu().numpy())
+        del deg
         owner_d = torch.from_numpy(layout.owner).to(dev)
         internal_d = torch.from_numpy(layout.internal_id).to(dev)
         own = range(layout.n_shards) if shards is None else shards
