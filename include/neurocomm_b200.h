@@ -244,6 +244,9 @@ typedef struct nc_xchg {
   uint32_t* peer_inbox[NC_MAX_SHARDS];
   uint32_t* peer_flags[NC_MAX_SHARDS];
   uint32_t* done;                  /* monotonically counting block exits        */
+  uint32_t* send_done;             /* [2][NC_MAX_SHARDS] chunk-publish counters */
+  int32_t blocks_per_peer;         /* P2P kernel blocks per peer (chunks)       */
+  int32_t pad1;
   uint32_t* barrier;               /* in-kernel grid barrier counter            */
   unsigned long long* lat_start;
   uint32_t* lat_ns;                /* per-step exchange latency (ns) or NULL    */

@@ -80,7 +80,8 @@ class XchgC(C.Structure):
         ("recv_ids", c_void_p), ("recv2_ids", c_void_p),
         ("my_inbox", c_void_p), ("my_flags", c_void_p),
         ("peer_inbox", c_void_p * MAX_SHARDS), ("peer_flags", c_void_p * MAX_SHARDS),
-        ("done", c_void_p), ("barrier", c_void_p), ("lat_start", c_void_p), ("lat_ns", c_void_p),
+        ("done", c_void_p), ("send_done", c_void_p), ("blocks_per_peer", c_int32), ("pad1", c_int32),
+        ("barrier", c_void_p), ("lat_start", c_void_p), ("lat_ns", c_void_p),
     ]
 
 

@@ -150,17 +150,41 @@ __device__ __forceinline__ int64_t slot_off(const nc_xchg_t& X, int phase, int p
   return ((int64_t)((phase * 2 + parity) * X.n + src)) * (X.cap + 4);
 }
 
-// Copy cnt ids to a (possibly remote) slot with 16-byte stores where aligned.
-__device__ void push_ids(uint32_t* dst, const uint32_t* src, int64_t cnt) {
-  const int64_t n4 = cnt >> 2;
+// Copy ids [lo, hi) to a (possibly remote) slot, 16-byte stores where aligned.
+__device__ void push_ids(uint32_t* dst, const uint32_t* src, int64_t lo, int64_t hi) {
+  const int64_t a4 = (lo + 3) >> 2, b4 = hi >> 2;
+  for (int64_t k = lo + threadIdx.x; k < min(hi, a4 << 2); k += blockDim.x) dst[k] = src[k];
   const uint4* s4 = reinterpret_cast<const uint4*>(src);
   uint4* d4 = reinterpret_cast<uint4*>(dst);
-  for (int64_t k = threadIdx.x; k < n4; k += blockDim.x) d4[k] = s4[k];
-  for (int64_t k = (n4 << 2) + threadIdx.x; k < cnt; k += blockDim.x) dst[k] = src[k];
+  for (int64_t k = a4 + threadIdx.x; k < b4; k += blockDim.x) d4[k] = s4[k];
+  for (int64_t k = max(lo, b4 << 2) + threadIdx.x; k < hi; k += blockDim.x) dst[k] = src[k];
 }
 
-__global__ void __launch_bounds__(512) k_p2p(const nc_xchg_t X) {
-  const int b = blockIdx.x;  // peer handled by this block
+__device__ __forceinline__ void chunk(int64_t cnt, int k, int B, int64_t* lo, int64_t* hi) {
+  const int64_t per = (((cnt + B - 1) / B) + 3) & ~int64_t(3);  // 16-byte aligned chunks
+  *lo = min(cnt, per * k);
+  *hi = min(cnt, per * (k + 1));
+}
+
+// Publish one phase's message to peer b once all B blocks of it have stored
+// their chunk: every block fences (system scope) and counts itself in; the
+// last one releases the flag.
+__device__ void publish(const nc_xchg_t& X, int phase, int b, uint32_t want, int B) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    const uint32_t arrived = atomicAdd(X.send_done + phase * NC_MAX_SHARDS + b, 1u) + 1u;
+    if (arrived == want * (uint32_t)B) {
+      __threadfence_system();
+      st_release_sys(X.peer_flags[b] + phase * NC_MAX_SHARDS + X.rank, want);
+    }
+  }
+}
+
+// grid = n peers x B blocks; block (b, k) moves chunk k of the traffic with peer b.
+__global__ void __launch_bounds__(512) k_p2p(const nc_xchg_t X, int B) {
+  const int b = blockIdx.x / B;   // peer handled by this block
+  const int kb = blockIdx.x % B;  // chunk
   const int step = *X.step;
   const int par = step & 1;
   const uint32_t want = (uint32_t)step + 1u;
@@ -168,39 +192,41 @@ __global__ void __launch_bounds__(512) k_p2p(const nc_xchg_t X) {
   long long* hop = step_row(X.hop_ids, X, step);
   long long* deliv = step_row(X.deliv_ids, X, step);
   __shared__ uint64_t t_start;
+  __shared__ bool ok;
   if (threadIdx.x == 0) t_start = globaltimer();
   const bool peer = (b < X.n && b != X.rank);
 
-  // ---- phase 1 push (data on route channels, heartbeat to everyone)
+  // ---- phase 1 push (data on route channels, heartbeat flag to everyone)
   if (peer) {
     int64_t cnt = 0;
     if ((X.send1_mask >> b) & 1u) {
       cnt = X.bucket_count[b];
       if (cnt > X.cap) {
-        if (threadIdx.x == 0) atomicExch(X.status, 1);
+        if (threadIdx.x == 0 && kb == 0) atomicExch(X.status, 1);
         cnt = X.cap;
       }
       uint32_t* slot = X.peer_inbox[b] + slot_off(X, 0, par, X.rank);
-      push_ids(slot + 4, X.bucket_ids + (int64_t)b * X.bucket_cap, cnt);
-      if (threadIdx.x == 0) slot[0] = (uint32_t)cnt;
+      int64_t lo, hi;
+      chunk(cnt, kb, B, &lo, &hi);
+      push_ids(slot + 4, X.bucket_ids + (int64_t)b * X.bucket_cap, lo, hi);
+      if (threadIdx.x == 0 && kb == 0) {
+        slot[0] = (uint32_t)cnt;
+        if (cnt) add64(hop + X.rank * X.n + b, cnt);
+      }
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence_system();
-      st_release_sys(X.peer_flags[b] + 0 * NC_MAX_SHARDS + X.rank, want);
-      if (cnt) add64(hop + X.rank * X.n + b, cnt);
-    }
+    publish(X, 0, b, want, B);
   }
-  // ---- phase 1 receive from peer b
+  // ---- phase 1 receive from peer b, chunk kb
   if (peer) {
-    __shared__ bool ok;
     if (threadIdx.x == 0) ok = wait_flag(X.my_flags + 0 * NC_MAX_SHARDS + b, want, X.timeout_ns, X.status);
     __syncthreads();
     if (ok && ((X.recv1_mask >> b) & 1u)) {
       const uint32_t* slot = X.my_inbox + slot_off(X, 0, par, b);
       int64_t cnt = *(volatile const uint32_t*)slot;
       if (cnt > X.cap) cnt = X.cap;
-      scatter_ids(X, slot + 4, cnt, b, false, cur, deliv, X.status);
+      int64_t lo, hi;
+      chunk(cnt, kb, B, &lo, &hi);
+      scatter_ids(X, slot + 4 + lo, hi - lo, b, false, cur, deliv, X.status);
     }
   }
   if (X.two_level) {
@@ -224,42 +250,43 @@ __global__ void __launch_bounds__(512) k_p2p(const nc_xchg_t X) {
     if (peer && ((X.send2_mask >> b) & 1u)) {
       int64_t cnt = X.fwd_count[b];
       if (cnt > X.cap) {
-        if (threadIdx.x == 0) atomicExch(X.status, 1);
+        if (threadIdx.x == 0 && kb == 0) atomicExch(X.status, 1);
         cnt = X.cap;
       }
       uint32_t* slot = X.peer_inbox[b] + slot_off(X, 1, par, X.rank);
-      push_ids(slot + 4, X.fwd_ids + (int64_t)b * X.cap, cnt);
-      if (threadIdx.x == 0) slot[0] = (uint32_t)cnt;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        __threadfence_system();
-        st_release_sys(X.peer_flags[b] + 1 * NC_MAX_SHARDS + X.rank, want);
+      int64_t lo, hi;
+      chunk(cnt, kb, B, &lo, &hi);
+      push_ids(slot + 4, X.fwd_ids + (int64_t)b * X.cap, lo, hi);
+      if (threadIdx.x == 0 && kb == 0) {
+        slot[0] = (uint32_t)cnt;
         if (cnt) add64(hop + X.rank * X.n + b, cnt);
       }
+      publish(X, 1, b, want, B);
     }
     // ---- phase 2 receive from relay b
     if (peer && ((X.recv2_mask >> b) & 1u)) {
-      __shared__ bool ok2;
-      if (threadIdx.x == 0) ok2 = wait_flag(X.my_flags + 1 * NC_MAX_SHARDS + b, want, X.timeout_ns, X.status);
+      if (threadIdx.x == 0) ok = wait_flag(X.my_flags + 1 * NC_MAX_SHARDS + b, want, X.timeout_ns, X.status);
       __syncthreads();
-      if (ok2) {
+      if (ok) {
         const uint32_t* slot = X.my_inbox + slot_off(X, 1, par, b);
         int64_t cnt = *(volatile const uint32_t*)slot;
         if (cnt > X.cap) cnt = X.cap;
-        scatter_ids(X, slot + 4, cnt, b, true, cur, deliv, X.status);
+        int64_t lo, hi;
+        chunk(cnt, kb, B, &lo, &hi);
+        scatter_ids(X, slot + 4 + lo, hi - lo, b, true, cur, deliv, X.status);
       }
     }
   }
   // ---- latency record: last block out stamps (end - start of block 0)
   __syncthreads();
   if (threadIdx.x == 0) {
-    if (b == 0) X.lat_start[0] = t_start;
+    if (blockIdx.x == 0) *X.lat_start = t_start;
     __threadfence();
     const uint32_t done = atomicAdd(X.done, 1u) + 1u;
     if (done == (uint32_t)(step + 1) * gridDim.x) {
       __threadfence();
       const uint64_t t_end = globaltimer();
-      const uint64_t t0 = *(volatile uint64_t*)X.lat_start;
+      const uint64_t t0 = *(volatile unsigned long long*)X.lat_start;
       if (X.lat_ns && step < X.lat_steps) X.lat_ns[step] = (t_end > t0) ? (uint32_t)(t_end - t0) : 0u;
     }
   }
@@ -283,6 +310,7 @@ int check_x(const nc_xchg_t* X) {
 __global__ void k_reset(const nc_xchg_t X) {
   const int t = threadIdx.x;
   if (t < 2 * NC_MAX_SHARDS && X.my_flags) X.my_flags[t] = 0u;
+  if (t < 2 * NC_MAX_SHARDS && X.send_done) X.send_done[t] = 0u;
   if (t == 0) {
     if (X.done) *X.done = 0u;
     if (X.barrier) *X.barrier = 0u;
@@ -321,7 +349,8 @@ extern "C" int nc_xchg_p2p(const nc_xchg_t* X, void* stream) {
     nc_set_error("nc_xchg_p2p: inbox / flags not set up");
     return NC_E_ARG;
   }
-  k_p2p<<<X->n, 512, 0, (cudaStream_t)stream>>>(*X);
+  const int B = X->blocks_per_peer > 0 ? X->blocks_per_peer : 1;
+  k_p2p<<<X->n * B, 512, 0, (cudaStream_t)stream>>>(*X, B);
   NC_LAUNCH_CHECK();
   if (X->two_level) {
     k_p2p_tail<<<1, 32, 0, (cudaStream_t)stream>>>(*X);

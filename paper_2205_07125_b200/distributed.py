@@ -78,7 +78,8 @@ class DistSimulator:
     def __init__(self, net: Network, lif: LifParams = LifParams(), seed: int = 0, rt: RoutingTable | None = None,
                  *, transport: str = "p2p", delivery: str = "fused", msg_cap: int | None = None,
                  record_raster_steps: int = 0, per_step_counts: bool = False, latency_steps: int = 4096,
-                 use_graph: bool = True, graph_chunk: int = 64, timeout_s: float = 10.0):
+                 use_graph: bool = True, graph_chunk: int = 64, timeout_s: float = 10.0,
+                 blocks_per_peer: int = 8):
         import torch
         import torch.distributed as dist
         if transport not in ("p2p", "nccl"):
@@ -105,6 +106,7 @@ class DistSimulator:
         self.graph_chunk = graph_chunk
         self.per_step_counts = per_step_counts
         self.latency_steps = latency_steps
+        self.blocks_per_peer = max(1, int(blocks_per_peer))
         dev = net.device
         self.dev = dev
 
@@ -192,7 +194,7 @@ class DistSimulator:
         import torch.distributed as dist
         n, cap = self.n, self.cap
         inbox_words = 4 * n * (cap + 4)
-        flag_words = 2 * _native.MAX_SHARDS + 16  # flags + done/barrier/lat_start
+        flag_words = 2 * _native.MAX_SHARDS + 16 + 2 * _native.MAX_SHARDS  # flags, done/barrier/lat, send_done
         handles = []
         ptrs = []
         for words in (inbox_words, flag_words):
@@ -210,6 +212,8 @@ class DistSimulator:
         X.done = base + 4 * (2 * _native.MAX_SHARDS)
         X.barrier = base + 4 * (2 * _native.MAX_SHARDS + 1)
         X.lat_start = base + 4 * (2 * _native.MAX_SHARDS + 2)  # 8-byte aligned
+        X.send_done = base + 4 * (2 * _native.MAX_SHARDS + 16)
+        X.blocks_per_peer = self.blocks_per_peer
         for peer in range(self.world):
             if peer == self.rank:
                 X.peer_inbox[peer], X.peer_flags[peer] = ptrs[0], ptrs[1]
