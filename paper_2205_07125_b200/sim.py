@@ -533,8 +533,12 @@ class _ShardState:
 
 def _push_csr(csr: ShardCSR, lay: ShardLayout, h: int, dev):
     """Transpose of the pull synapses: rows = internal pre ids,
-    entries = (inhibitory << 31) | ((q - 1) << 26) | post_local."""
+    entries = (inhibitory << 31) | ((q - 1) << 26) | post_local.  Built once per
+    shard and cached on the SellCSR."""
     import torch
+    cached = getattr(csr, "_push_cache", None)
+    if cached is not None:
+        return cached
     row, pre, q, inh = sell.decode(csr)
     ent = (inh.to(torch.int64) << 31) | ((q - 1) << ID_BITS) | row
     order = torch.argsort(pre, stable=True)
@@ -543,6 +547,7 @@ def _push_csr(csr: ShardCSR, lay: ShardLayout, h: int, dev):
     rowptr = torch.zeros(n_rows + 1, dtype=torch.int64, device=dev)
     rowptr[1:] = torch.cumsum(torch.bincount(pre, minlength=n_rows), 0)
     ent = torch.where(ent >= 2**31, ent - 2**32, ent).to(torch.int32)
+    csr._push_cache = (rowptr, ent)
     return rowptr, ent
 
 
