@@ -184,10 +184,10 @@ def run_ours(args) -> dict | None:
     n_local = lay.n_local(rank)
     csr = net.shards[rank]
     # algorithmic bytes of one fused step: 4 B per synapse
-    # + per neuron emid 2/tile, V r/w 8, I r/w 8, refrac r/w 2, gid 4, the slice
+    # + per neuron row_meta 4/tile, V r/w 8, I r/w 8, refrac r/w 2, gid 4, the slice
     # pointers, + the previous spike bitmap read and the new one written
     syn_bytes = int(net.n_synapses) * 4
-    neuron_bytes = n_local * (2 * csr.n_tiles + 8 + 8 + 2 + 4) + csr.slice_ptr.numel() * 8 + 2 * (lay.n_words * 4)
+    neuron_bytes = n_local * (4 * csr.n_tiles + 8 + 8 + 2 + 4) + csr.slice_ptr.numel() * 8 + 2 * (lay.n_words * 4)
     alg_bytes = syn_bytes + neuron_bytes
     peaks = load_peaks()
     achieved = alg_bytes / (kernel_ms * 1e-3) / 1e9
@@ -296,8 +296,8 @@ def e2e_measure(sim, net, args) -> dict:
     host_syn.copy_(csr.syn)
     host_rp = torch.empty(csr.slice_ptr.shape, dtype=torch.int64, pin_memory=True)
     host_rp.copy_(csr.slice_ptr)
-    host_em = torch.empty(csr.row_emid.shape, dtype=torch.int16, pin_memory=True)
-    host_em.copy_(csr.row_emid)
+    host_em = torch.empty(csr.row_meta.shape, dtype=torch.int32, pin_memory=True)
+    host_em.copy_(csr.row_meta)
     words = st.local_words
     ring = torch.empty((2, words), dtype=torch.int32, pin_memory=True)
     steps = args.steps
@@ -307,7 +307,7 @@ def e2e_measure(sim, net, args) -> dict:
     e0.record()
     csr.syn.copy_(host_syn, non_blocking=True)
     csr.slice_ptr.copy_(host_rp, non_blocking=True)
-    csr.row_emid.copy_(host_em, non_blocking=True)
+    csr.row_meta.copy_(host_em, non_blocking=True)
     sim.reset(1)
     for t in range(steps):
         sim.advance_eager(1)
@@ -316,7 +316,7 @@ def e2e_measure(sim, net, args) -> dict:
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
-    h2d = host_syn.numel() * 4 + host_rp.numel() * 8 + host_em.numel() * 2
+    h2d = host_syn.numel() * 4 + host_rp.numel() * 8 + host_em.numel() * 4
     return {"value": round(steps / (ms * 1e-3), 2), "unit": UNIT, "h2d_bytes_per_step": int(h2d // steps),
             "d2h_bytes_per_step": int(words * 4),
             "note": "network H2D from pinned memory once per call (amortised), spike bitmap D2H every step"}

@@ -96,7 +96,9 @@ int nc_weight_histogram(const double* weights, const int64_t* assignment, int64_
  * tile t) starts at slice_ptr[s*n_tiles + t] (uint4 units) and holds `len`
  * slots of 32 uint4: slot u of lane l is entries 4u..4u+3 of row 32s+l.  A
  * row's slots [0, emid) hold its excitatory pres (weight +q), the next slots
- * its inhibitory pres (weight -g_inh*q); emid = row_emid[row*n_tiles + t].
+ * its inhibitory pres (weight -g_inh*q), its last used slot is len_r - 1:
+ * row_meta[row*n_tiles + t] = emid | (len_r << 16).  Lanes only load their own
+ * len_r slots, so the padding of a block to its longest row costs no traffic.
  * Unused entries hold the pad entry (guard id, never fires).  Lanes read
  * consecutive 16-byte words, each lane owns one row: no cross-lane reduction.
  * Push entries (rows = internal pre ids):
@@ -139,7 +141,7 @@ typedef struct nc_shard {
   const uint16_t* hop_mask; /* bit h: a spike of this neuron is sent to shard h */
   /* pull SELL-32 */
   const int64_t* slice_ptr; /* n_slices*n_tiles+1 block starts (uint4 units)   */
-  const uint16_t* row_emid; /* n_local*n_tiles excitatory slots per row/tile   */
+  const uint32_t* row_meta; /* n_local*n_tiles: emid | (row slots << 16)        */
   const uint32_t* syn;      /* packed entries                                  */
   /* push CSR (optional): rows = internal pre ids, entries see above */
   const int64_t* push_rowptr;
@@ -302,12 +304,12 @@ int nc_graphgen_degrees(const nc_graphgen_t* g, int32_t* deg, void* stream);
  * (row, tile, sign) (zero-initialised); tile_words as in nc_shard_t. */
 int nc_graphgen_count(const nc_graphgen_t* g, int32_t n_tiles, int32_t tile_words, int32_t* lower_len,
                       int32_t* upper_len, void* stream);
-/* Pass 2 into the SELL-32 layout (slice_ptr/row_emid computed by the host
+/* Pass 2 into the SELL-32 layout (slice_ptr/row_meta computed by the host
  * from the pass-1 counts); lower_fill [n_local*n_tiles*2] zero-initialised
  * (slot claims; lower_len is unused and may be NULL).  syn must be pre-filled
  * with nc_sell_fill_pads. */
 int nc_graphgen_fill(const nc_graphgen_t* g, int32_t n_tiles, int32_t tile_words, const int64_t* slice_ptr,
-                     const uint16_t* row_emid, const int32_t* lower_len, int32_t* lower_fill, uint32_t* syn,
+                     const uint32_t* row_meta, const int32_t* lower_len, int32_t* lower_fill, uint32_t* syn,
                      void* stream);
 /* Pad pre-fill of a SELL-32 array: block b = (slice, tile b % n_tiles) gets
  * (first id of its tile) with q = 0 in every entry. */

@@ -42,7 +42,7 @@ class ShardC(C.Structure):
         ("pad0", c_int32),
         ("v", c_void_p), ("i_syn", c_void_p), ("refrac", c_void_p), ("acc", c_void_p),
         ("gid", c_void_p), ("hop_mask", c_void_p),
-        ("slice_ptr", c_void_p), ("row_emid", c_void_p), ("syn", c_void_p),
+        ("slice_ptr", c_void_p), ("row_meta", c_void_p), ("syn", c_void_p),
         ("push_rowptr", c_void_p), ("push_syn", c_void_p),
         ("bitmap0", c_void_p), ("bitmap1", c_void_p),
         ("fired_ids", c_void_p), ("fired_count", c_void_p),

@@ -157,11 +157,11 @@ __global__ void k_degrees(const nc_graphgen_t g, int32_t* deg) {
 }
 
 // Position of the k-th entry of (row, tile, sign) in the SELL-32 layout (uint32 units).
-__device__ __forceinline__ int64_t sell_pos(const int64_t* slice_ptr, const uint16_t* row_emid, int32_t T,
+__device__ __forceinline__ int64_t sell_pos(const int64_t* slice_ptr, const uint32_t* row_meta, int32_t T,
                                             int64_t row, int64_t seg, int32_t k) {
   const int64_t t = (seg >> 1) - row * T;
   const int64_t blk = slice_ptr[(row >> 5) * T + t];
-  const int64_t slot = ((seg & 1) ? (int64_t)row_emid[row * T + t] : 0) + (k >> 2);
+  const int64_t slot = ((seg & 1) ? (int64_t)(row_meta[row * T + t] & 0xFFFFu) : 0) + (k >> 2);
   return (blk + slot * 32 + (row & 31)) * 4 + (k & 3);
 }
 
@@ -169,7 +169,7 @@ __device__ __forceinline__ int64_t sell_pos(const int64_t* slice_ptr, const uint
 // (row, tile, sign) segment are claimed with atomics (any order is fine:
 // delivery sums integers).
 __global__ void k_fill(const nc_graphgen_t g, int32_t T, int32_t TW, const int64_t* slice_ptr,
-                       const uint16_t* row_emid, int32_t* fill, uint32_t* syn) {
+                       const uint32_t* row_meta, int32_t* fill, uint32_t* syn) {
   const Comm cm = make_comm(g);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n_neurons;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -185,13 +185,13 @@ __global__ void k_fill(const nc_graphgen_t g, int32_t T, int32_t TW, const int64
       if (mine) {
         const int64_t seg = seg_index(ri, T, TW, jid, is_inh(g, j));
         const int32_t k = atomicAdd(fill + seg, 1);
-        syn[sell_pos(slice_ptr, row_emid, T, ri, seg, k)] = pack(jid, q);
+        syn[sell_pos(slice_ptr, row_meta, T, ri, seg, k)] = pack(jid, q);
       }
       if (jm) {
         const int64_t rj = (int64_t)jid - g.local_base;
         const int64_t seg = seg_index(rj, T, TW, iid, inh_i);
         const int32_t k = atomicAdd(fill + seg, 1);
-        syn[sell_pos(slice_ptr, row_emid, T, rj, seg, k)] = pack(iid, q);
+        syn[sell_pos(slice_ptr, row_meta, T, rj, seg, k)] = pack(iid, q);
       }
     });
   }
@@ -266,7 +266,7 @@ extern "C" int nc_graphgen_degrees(const nc_graphgen_t* g, int32_t* deg, void* s
 }
 
 extern "C" int nc_graphgen_fill(const nc_graphgen_t* g, int32_t n_tiles, int32_t tile_words, const int64_t* slice_ptr,
-                                const uint16_t* row_emid, const int32_t* lower_len, int32_t* lower_fill, uint32_t* syn,
+                                const uint32_t* row_meta, const int32_t* lower_len, int32_t* lower_fill, uint32_t* syn,
                                 void* stream) {
   (void)lower_len;
   if (!g || n_tiles < 1 || tile_words < 1) {
@@ -274,7 +274,7 @@ extern "C" int nc_graphgen_fill(const nc_graphgen_t* g, int32_t n_tiles, int32_t
     return NC_E_ARG;
   }
   k_fill<<<grid_for(g->n_neurons, 128), 128, 0, (cudaStream_t)stream>>>(*g, n_tiles, tile_words, slice_ptr,
-                                                                          row_emid, lower_fill, syn);
+                                                                          row_meta, lower_fill, syn);
   NC_LAUNCH_CHECK();
   return NC_OK;
 }

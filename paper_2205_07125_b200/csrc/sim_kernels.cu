@@ -54,35 +54,26 @@ __device__ __forceinline__ int32_t quad_term(uint4 e, const uint32_t* __restrict
   return entry_term(e.x, bm) + entry_term(e.y, bm) + entry_term(e.z, bm) + entry_term(e.w, bm);
 }
 
-// One lane's row in one SELL-32 block: slots [0, len) at blk + u*32 + lane;
-// slots below emid are excitatory.  Returns sum_E - g * sum_I (weight units).
-// `pad` (the block's pad entry: first id of its tile, q = 0) fills the tail
-// registers so that their lookups stay inside the staged tile.
-__device__ __forceinline__ int32_t sell_row_sum(const uint4* __restrict__ blk, int len, int emid,
+// One lane's row in one SELL-32 block: block slots [0, len) at blk + u*32 + lane;
+// this row uses meta >> 16 of them, the first (meta & 0xFFFF) excitatory.
+// Slots past the row's own length are not loaded (`pad` stands in: the block's
+// pad entry, first id of its tile with q = 0, so its lookup stays in the
+// staged tile and adds nothing).  Returns sum_E - g * sum_I (weight units).
+__device__ __forceinline__ int32_t sell_row_sum(const uint4* __restrict__ blk, int len, uint32_t meta,
                                                 const uint32_t* __restrict__ bm, int32_t g_inh, int lane,
                                                 uint32_t pad) {
+  const int emid = (int)(meta & 0xFFFFu);
+  const int mine = (int)(meta >> 16);
   int32_t se = 0, si = 0;
   const uint4* p = blk + lane;
-  int u0 = 0;
-  for (; u0 + kUnroll <= len; u0 += kUnroll) {
+  const uint4 padv = make_uint4(pad, pad, pad, pad);
+  for (int u0 = 0; u0 < len; u0 += kUnroll) {
     uint4 e[kUnroll];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) e[u] = ld_stream(p + (u0 + u) * 32);
+    for (int u = 0; u < kUnroll; ++u) e[u] = (u0 + u < mine) ? ld_stream(p + (u0 + u) * 32) : padv;
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       const int32_t t = quad_term(e[u], bm);
-      if (u0 + u < emid) se += t;
-      else si += t;
-    }
-  }
-  if (u0 < len) {  // uniform tail: < kUnroll slots
-    uint4 e[kUnroll];
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u)
-      e[u] = (u0 + u < len) ? ld_stream(p + (u0 + u) * 32) : make_uint4(pad, pad, pad, pad);
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const int32_t t = quad_term(e[u], bm);   // zero entries have q = 0
       if (u0 + u < emid) se += t;
       else si += t;
     }
@@ -231,8 +222,8 @@ k_step_fused(const nc_shard_t sh, const nc_lif_params_t p) {
       const int row = (slice << 5) + lane;
       const int64_t b0 = sh.slice_ptr[slice];
       const int len = (int)((sh.slice_ptr[slice + 1] - b0) >> 5);
-      const int emid = row < sh.n_local ? (int)sh.row_emid[row] : 0;
-      const int32_t acc = sell_row_sum(syn4 + b0, len, emid, sbm, g_inh, lane, 0u);
+      const uint32_t meta = row < sh.n_local ? sh.row_meta[row] : 0u;
+      const int32_t acc = sell_row_sum(syn4 + b0, len, meta, sbm, g_inh, lane, 0u);
       if (kLif) {
         const uint32_t fm = update_slice(sh, p, cur, slice, lane, acc, step);
         if (lane == 0) my_spikes += __popc(fm);
@@ -261,8 +252,8 @@ k_step_fused(const nc_shard_t sh, const nc_lif_params_t p) {
         const int row = (slice << 5) + lane;
         const int64_t b0 = sh.slice_ptr[(int64_t)slice * T + t];
         const int len = (int)((sh.slice_ptr[(int64_t)slice * T + t + 1] - b0) >> 5);
-        const int emid = row < sh.n_local ? (int)sh.row_emid[(int64_t)row * T + t] : 0;
-        part[(slice - s0) * 32 + lane] += sell_row_sum(syn4 + b0, len, emid, bm, g_inh, lane, (uint32_t)w0 * 32u);
+        const uint32_t meta = row < sh.n_local ? sh.row_meta[(int64_t)row * T + t] : 0u;
+        part[(slice - s0) * 32 + lane] += sell_row_sum(syn4 + b0, len, meta, bm, g_inh, lane, (uint32_t)w0 * 32u);
       }
     }
     __syncthreads();

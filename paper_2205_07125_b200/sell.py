@@ -4,8 +4,9 @@ A slice is one warp's 32 consecutive local post rows.  For every (slice,
 bitmap tile) block, lane l owns row 32*slice + l and reads slot u at
 ``slice_ptr[block] + 32*u + l`` (16-byte words of 4 entries).  Within a row's
 part of a block, the excitatory pres fill slots [0, emid), the inhibitory
-ones the next ceil(n_I/4) slots; everything else is a pad entry (q = 0 and
-the tile's first id, so it looks up a staged word and adds nothing).
+ones the next ceil(n_I/4) slots (row length len_r); row_meta = emid |
+(len_r << 16).  Lanes never load past their own len_r; storage past it (up
+to the block's longest row) holds pad entries (q = 0 and the tile's first id).
 
 Tiles: when the spike bitmap is larger than shared memory, it is staged in
 tiles of ``tile_words`` words and every block only references pres of its
@@ -48,7 +49,7 @@ class SellCSR:
     """One shard's pull synapses on the device."""
 
     slice_ptr: object      # torch int64 [n_slices*n_tiles + 1], uint4 units
-    row_emid: object       # torch int16 [n_local*n_tiles] (uint16 bit patterns)
+    row_meta: object       # torch int32 [n_local*n_tiles]: emid | (row slots << 16)
     syn: object            # torch int32 [4*slice_ptr[-1]] packed entries
     n_tiles: int
     tile_words: int
@@ -62,7 +63,7 @@ class SellCSR:
 
 
 def layout_from_counts(counts, n_local: int, n_tiles: int):
-    """slice_ptr, row_emid from per-(row, tile, sign) entry counts (torch or numpy int arrays)."""
+    """slice_ptr, row_meta from per-(row, tile, sign) entry counts (torch or numpy int arrays)."""
     xp = _xp(counts)
     c = counts.reshape(n_local, n_tiles, 2)
     e_slots = (c[:, :, 0] + 3) // 4
@@ -76,17 +77,17 @@ def layout_from_counts(counts, n_local: int, n_tiles: int):
     flat = blk.reshape(-1).astype("int64") if xp == "np" else blk.reshape(-1).to(_torch().int64)
     ptr = _zeros(xp, (n_slices * n_tiles + 1,), like=flat)
     if xp == "torch":
-        ptr[1:] = _torch().cumsum(flat * 32, 0)
-        emid = e_slots.reshape(-1).to(_torch().int32)
-        if int(emid.max().item() if emid.numel() else 0) > 0xFFFF:
+        torch = _torch()
+        ptr[1:] = torch.cumsum(flat * 32, 0)
+        if row_slots.numel() and int(row_slots.max().item()) > 0x7FFF:
             raise ValueError("row too long for 16-bit slot counts")
-        emid = _torch().where(emid >= 0x8000, emid - 0x10000, emid).to(_torch().int16)
+        meta = (e_slots.reshape(-1).to(torch.int64) | (row_slots.reshape(-1).to(torch.int64) << 16)).to(torch.int32)
     else:
         ptr[1:] = np.cumsum(flat * 32)
-        if e_slots.size and e_slots.max() > 0xFFFF:
+        if row_slots.size and row_slots.max() > 0x7FFF:
             raise ValueError("row too long for 16-bit slot counts")
-        emid = e_slots.reshape(-1).astype(np.uint16)
-    return ptr, emid
+        meta = (e_slots.reshape(-1).astype(np.uint32) | (row_slots.reshape(-1).astype(np.uint32) << 16))
+    return ptr, meta
 
 
 def host_build(row, pre_internal, q, inh, n_local: int, n_tiles: int, tile_words: int):
@@ -96,7 +97,8 @@ def host_build(row, pre_internal, q, inh, n_local: int, n_tiles: int, tile_words
     tile = (pre >> 5) // tile_words
     seg = (row * n_tiles + tile) * 2 + np.asarray(inh, dtype=np.int64)
     counts = np.bincount(seg, minlength=n_local * n_tiles * 2).astype(np.int64)
-    ptr, emid = layout_from_counts(counts, n_local, n_tiles)
+    ptr, meta = layout_from_counts(counts, n_local, n_tiles)
+    emid = meta & np.uint32(0xFFFF)
     syn = np.zeros(int(ptr[-1]) * 4, dtype=np.uint32)
     n_blocks = ptr.size - 1
     for b in range(n_tiles if n_tiles > 1 else 0):  # pad = first id of the block's tile
@@ -112,7 +114,7 @@ def host_build(row, pre_internal, q, inh, n_local: int, n_tiles: int, tile_words
     slot = np.where(sseg % 2 == 1, emid.astype(np.int64)[r * n_tiles + t], 0) + k // 4
     pos = (ptr[(r // 32) * n_tiles + t] + slot * 32 + (r % 32)) * 4 + (k % 4)
     syn[pos] = (np.asarray(q, dtype=np.uint32)[order] << np.uint32(ID_BITS)) | pre[order].astype(np.uint32)
-    return ptr, emid, syn
+    return ptr, meta, syn
 
 
 def decode(csr: SellCSR):
@@ -133,7 +135,7 @@ def decode(csr: SellCSR):
     ent = csr.syn[: total * 4].view(-1, 4).to(torch.int64) & 0xFFFFFFFF      # [total, 4]
     valid_row = row < csr.n_local
     emid = torch.zeros_like(row)
-    emid[valid_row] = (csr.row_emid.to(torch.int64) & 0xFFFF)[row[valid_row] * T + t[valid_row]]
+    emid[valid_row] = (csr.row_meta.to(torch.int64) & 0xFFFF)[row[valid_row] * T + t[valid_row]]
     inh = (u >= emid)
     q = ent >> ID_BITS
     keep = (q > 0) & valid_row[:, None]

@@ -263,9 +263,9 @@ class Network:
         for h in own:
             n_local = layout.n_local(h)
             T, TW = _tiles(layout, n_local, sms, tile_words)
-            ptr, emid, syn = host_sell(graph, layout, h, inh_every, T, TW)
+            ptr, meta, syn = host_sell(graph, layout, h, inh_every, T, TW)
             n_real = int(np.count_nonzero((syn >> np.uint32(ID_BITS)) > 0))
-            csr = ShardCSR(torch.from_numpy(ptr).to(dev), torch.from_numpy(emid.view(np.int16)).to(dev),
+            csr = ShardCSR(torch.from_numpy(ptr).to(dev), torch.from_numpy(meta.view(np.int32)).to(dev),
                            torch.from_numpy(syn.view(np.int32)).to(dev), T, TW, n_local, n_real)
             csr.dest = _dest_masks(csr, layout, h, dev)
             out[h] = csr
@@ -317,17 +317,17 @@ class Network:
             _native.check(L.nc_graphgen_count(C.byref(g), T, TW, lower.data_ptr(), upper.data_ptr(), st),
                           "graphgen count")
             counts = (lower + upper)[: n_local * T * 2].to(torch.int64)
-            ptr, emid = sell.layout_from_counts(counts, n_local, T)
+            ptr, meta = sell.layout_from_counts(counts, n_local, T)
             total = int(ptr[-1].item())
             syn = torch.zeros(max(total * 4, 4), dtype=torch.int32, device=dev)
             _native.check(L.nc_sell_fill_pads(ptr.data_ptr(), ptr.numel() - 1, T, TW, syn.data_ptr(), st),
                           "sell pads")
             lower.zero_()
-            _native.check(L.nc_graphgen_fill(C.byref(g), T, TW, ptr.data_ptr(), emid.data_ptr(), None,
+            _native.check(L.nc_graphgen_fill(C.byref(g), T, TW, ptr.data_ptr(), meta.data_ptr(), None,
                                              lower.data_ptr(), syn.data_ptr(), st), "graphgen fill")
             n_real = int(counts.sum().item())
             del upper, counts
-            csr = ShardCSR(ptr, emid, syn, T, TW, n_local, n_real)
+            csr = ShardCSR(ptr, meta, syn, T, TW, n_local, n_real)
             csr.dest = _dest_masks(csr, layout, h, dev)
             out[h] = csr
             nsyn += n_real
@@ -519,7 +519,7 @@ class _ShardState:
             n_tiles=csr.n_tiles, tile_words=csr.tile_words, pad0=0,
             v=self.v.data_ptr(), i_syn=self.i_syn.data_ptr(), refrac=self.refrac.data_ptr(),
             acc=self.acc.data_ptr(), gid=self.gid.data_ptr(), hop_mask=self.hop_mask.data_ptr(),
-            slice_ptr=csr.slice_ptr.data_ptr(), row_emid=csr.row_emid.data_ptr(), syn=csr.syn.data_ptr(),
+            slice_ptr=csr.slice_ptr.data_ptr(), row_meta=csr.row_meta.data_ptr(), syn=csr.syn.data_ptr(),
             push_rowptr=None if self.push_rowptr is None else self.push_rowptr.data_ptr(),
             push_syn=None if self.push_syn is None else self.push_syn.data_ptr(),
             bitmap0=self.bitmaps[0].data_ptr(), bitmap1=self.bitmaps[1].data_ptr(),

@@ -19,9 +19,9 @@ def test_host_build_round_trip(n_local, n_tiles, tile_words):
     pre = rng.integers(0, n_ids, m)
     q = rng.integers(1, 33, m)
     inh = rng.random(m) < 0.2
-    ptr, emid, syn = sell.host_build(row, pre, q, inh, n_local, n_tiles, tile_words)
+    ptr, meta, syn = sell.host_build(row, pre, q, inh, n_local, n_tiles, tile_words)
     assert ptr[-1] * 4 == syn.size and (np.diff(ptr) % 32 == 0).all()
-    csr = sell.SellCSR(torch.from_numpy(ptr), torch.from_numpy(emid.view(np.int16)),
+    csr = sell.SellCSR(torch.from_numpy(ptr), torch.from_numpy(meta.view(np.int32)),
                        torch.from_numpy(syn.view(np.int32)), n_tiles, tile_words, n_local, m)
     r2, p2, q2, i2 = (x.numpy() for x in sell.decode(csr))
     a = np.stack([row, pre, q, inh]).T
@@ -29,6 +29,11 @@ def test_host_build_round_trip(n_local, n_tiles, tile_words):
     a = a[np.lexsort(a.T[::-1])]
     b = b[np.lexsort(b.T[::-1])]
     np.testing.assert_array_equal(a, b)
+    # row lengths bound the real entries, blocks are as long as their longest row
+    lens = (meta >> np.uint32(16)).astype(np.int64).reshape(n_local, n_tiles)
+    pad_rows = np.zeros(((n_local + 31) // 32 * 32, n_tiles), dtype=np.int64)
+    pad_rows[:n_local] = lens
+    np.testing.assert_array_equal(pad_rows.reshape(-1, 32, n_tiles).max(axis=1).reshape(-1) * 32, np.diff(ptr))
     # every entry of block (slice, t) references tile t
     for blk in range(ptr.size - 1):
         t = blk % n_tiles
@@ -51,4 +56,4 @@ def test_layout_from_counts_torch_matches_numpy():
     p1, e1 = sell.layout_from_counts(counts, 77, 3)
     p2, e2 = sell.layout_from_counts(torch.from_numpy(counts), 77, 3)
     np.testing.assert_array_equal(p1, p2.numpy())
-    np.testing.assert_array_equal(e1.view(np.int16), e2.numpy())
+    np.testing.assert_array_equal(e1.view(np.int32), e2.numpy())
