@@ -318,10 +318,18 @@ __global__ void __launch_bounds__(256) k_deliver_push(const nc_shard_t sh, int32
       bits &= bits - 1;
       const int64_t pre = (w << 5) + b;
       const int64_t beg = sh.push_rowptr[pre], end = sh.push_rowptr[pre + 1];
-      for (int64_t e = beg + lane; e < end; e += 32) {
-        const uint32_t x = sh.push_syn[e];
-        const int32_t q = (int32_t)((x >> 26) & 31u) + 1;
-        atomicAdd(sh.acc + (x & 0x03FFFFFFu), (x >> 31) ? q * negg : q);
+      // 4 independent loads in flight per lane, then 4 fire-and-forget reductions
+      for (int64_t e0 = beg + lane; e0 < end; e0 += 128) {
+        uint32_t x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) x[u] = (e0 + 32 * u < end) ? __ldg(sh.push_syn + e0 + 32 * u) : 0u;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (e0 + 32 * u < end) {
+            const int32_t q = (int32_t)((x[u] >> 26) & 31u) + 1;
+            atomicAdd(sh.acc + (x[u] & 0x03FFFFFFu), (x[u] >> 31) ? q * negg : q);
+          }
+        }
       }
     }
   }
