@@ -238,17 +238,25 @@ k_step_fused(const nc_shard_t sh, const nc_lif_params_t p) {
     const int s1 = min(n_slices, s0 + per);
     int32_t* part = reinterpret_cast<int32_t*>(sbm + TW);
     for (int k = threadIdx.x; k < per * 32; k += blockDim.x) part[k] = 0;
+    __shared__ int next_slice[2];
+    if (threadIdx.x == 0) next_slice[0] = next_slice[1] = s0;
     for (int t = 0; t < T; ++t) {
       __syncthreads();
       const int w0 = t * TW;
       const int nw = min(TW, sh.n_words - w0);
       const uint4* src = reinterpret_cast<const uint4*>(prev + w0);
       for (int k = threadIdx.x; k < (nw + 3) >> 2; k += blockDim.x) smem4[k] = ld_keep(src + k);
+      if (threadIdx.x == 0) next_slice[(t + 1) & 1] = s0;  // counter of the next tile
       __syncthreads();
       // tile-relative view: bm[global word] hits the staged copy
       const uint32_t* bm = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(sbm) -
                                                              (uintptr_t)w0 * 4u);
-      for (int slice = s0 + warp; slice < s1; slice += wpb) {
+      // warps claim slices dynamically so the per-tile barrier waits for at most one slice
+      for (;;) {
+        int slice = 0;
+        if (lane == 0) slice = atomicAdd(&next_slice[t & 1], 1);
+        slice = __shfl_sync(kFull, slice, 0);
+        if (slice >= s1) break;
         const int row = (slice << 5) + lane;
         const int64_t b0 = sh.slice_ptr[(int64_t)slice * T + t];
         const int len = (int)((sh.slice_ptr[(int64_t)slice * T + t + 1] - b0) >> 5);
@@ -496,9 +504,11 @@ extern "C" int nc_sim_lif_update(const nc_shard_t* sh, const nc_lif_params_t* p,
     nc_set_error("nc_sim_lif_update: shard has no acc buffer");
     return NC_E_ARG;
   }
+  // grid-stride over 32-neuron tiles with ~2 CTAs per SM: one global spike-count
+  // atomic per CTA (thousands of same-address atomics cost more than the update)
   const int tiles = (sh->n_local + 31) / 32;
   int grid = (tiles + 7) / 8;
-  grid = grid < 1 ? 1 : (grid > 16 * num_sms() ? 16 * num_sms() : grid);
+  grid = grid < 1 ? 1 : (grid > 2 * num_sms() ? 2 * num_sms() : grid);
   k_lif_update<<<grid, 256, 0, (cudaStream_t)stream>>>(*sh, *p);
   NC_LAUNCH_CHECK();
   return NC_OK;
