@@ -102,12 +102,103 @@ def dist_env():
 
 # --------------------------------------------------------------------------- ours
 
+def make_sim(net, lif, args, delivery, world):
+    from paper_2205_07125_b200 import sim as S
+    if world > 1:
+        from paper_2205_07125_b200 import distributed as D
+        return D.DistSimulator(net, lif, args.seed, None, transport=args.transport, delivery=delivery,
+                               msg_cap=args.msg_cap, latency_steps=args.warmup + args.steps, graph_chunk=args.chunk)
+    return S.Simulator(net, lif, args.seed, None, delivery=delivery, graph_chunk=args.chunk)
+
+
+def time_steps(sim, args, world, dev, clocks=None):
+    """W warm-up steps, then exactly K timed steps between barrier + synchronize;
+    CUDA events on the launching stream, max over ranks.  Returns (ms, spikes, lat, lat_max)."""
+    import torch
+    import torch.distributed as dist
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    sim.reset(1)
+    sim.advance(args.warmup)
+    barrier()
+    spikes0 = sum(int(s.spike_total.item()) for s in sim.states)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    ctx = clocks if clocks is not None else _Null()
+    with ctx:
+        e0.record()
+        sim.advance(args.steps)
+        e1.record()
+        torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    spikes = sum(int(s.spike_total.item()) for s in sim.states) - spikes0
+    sim.check_status()
+    lat = lat_max = None
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        sp = torch.tensor([spikes], device=dev, dtype=torch.int64)
+        dist.all_reduce(sp)
+        spikes = int(sp.item())
+        lat, lat_max = sim.latencies_us(args.warmup + args.steps)
+        lat, lat_max = lat[args.warmup:], lat_max[args.warmup:]
+    return ms, spikes, lat, lat_max
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def kernel_ms(sim, which: str, reps: int = 50) -> float:
+    """Average duration of one kernel, timed alone with CUDA events on its stream."""
+    import ctypes as C
+    import torch
+    from paper_2205_07125_b200 import _native
+    st = sim.states[0]
+    L = _native.lib()
+    stream = torch.cuda.current_stream()
+    k0 = torch.cuda.Event(enable_timing=True)
+    k1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    k0.record(stream)
+    for _ in range(reps):
+        if which == "fused":
+            L.nc_sim_step_fused(C.byref(st.c), C.byref(sim.c_lif), stream.cuda_stream)
+        elif which == "push":
+            L.nc_sim_deliver_push(C.byref(st.c), sim.c_lif.g_inh, stream.cuda_stream)
+        else:
+            L.nc_sim_lif_update(C.byref(st.c), C.byref(sim.c_lif), stream.cuda_stream)
+    k1.record(stream)
+    torch.cuda.synchronize()
+    return k0.elapsed_time(k1) / reps
+
+
+def lat_summary(lat, lat_max, transport):
+    if lat is None:
+        return None
+    return {"p50": round(float(np.percentile(lat, 50)), 2), "p99": round(float(np.percentile(lat, 99)), 2),
+            "p50_incl_skew": round(float(np.percentile(lat_max, 50)), 2),
+            "p99_incl_skew": round(float(np.percentile(lat_max, 99)), 2), "transport": transport,
+            "what": "device %globaltimer from a rank's buckets-ready to its last inbound spike in the bitmap; "
+                    "p50/p99 over steps of the min over ranks (the last-ready rank: transfer + signalling), "
+                    "*_incl_skew: max over ranks (adds waiting for slower peers)"}
+
+
 def run_ours(args) -> dict | None:
     import torch
     import torch.distributed as dist
 
     from paper_2205_07125_b200 import sim as S
-    from paper_2205_07125_b200 import _native
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -122,65 +213,14 @@ def run_ours(args) -> dict | None:
     torch.cuda.synchronize()
     t_build = time.time() - t_build
     lif = S.LifParams()
-    if world > 1:
-        from paper_2205_07125_b200 import distributed as D
-        sim = D.DistSimulator(net, lif, args.seed, None, transport=args.transport, delivery=args.delivery,
-                              msg_cap=args.msg_cap, latency_steps=args.warmup + args.steps,
-                              graph_chunk=args.chunk)
-    else:
-        sim = S.Simulator(net, lif, args.seed, None, delivery=args.delivery, graph_chunk=args.chunk)
-    sim.reset(1)
-    sim.advance(args.warmup)
-    torch.cuda.synchronize()
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    barrier()
-    spikes0 = sum(int(s.spike_total.item()) for s in sim.states)
-    with ClockSampler(local) as clocks:
-        e0.record()
-        sim.advance(args.steps)
-        e1.record()
-        torch.cuda.synchronize()
-    barrier()
-    ms = e0.elapsed_time(e1)
-    spikes = sum(int(s.spike_total.item()) for s in sim.states) - spikes0
-    sim.check_status()
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        sp = torch.tensor([spikes], device=dev, dtype=torch.int64)
-        dist.all_reduce(sp)
-        spikes = int(sp.item())
+    # ---- headline: the delivery asked for (default: fused pull, the north-star K3 path)
+    sim = make_sim(net, lif, args, args.delivery, world)
+    clocks = ClockSampler(local)
+    ms, spikes, lat, lat_max = time_steps(sim, args, world, dev, clocks)
     value = args.steps / (ms * 1e-3)
-    lat = lat_max = None
-    if world > 1:
-        lat, lat_max = sim.latencies_us(args.warmup + args.steps)
-        lat, lat_max = lat[args.warmup:], lat_max[args.warmup:]
-
-    # ---- dominant kernel, timed alone on its stream (CUDA events) ----
-    st = sim.states[0]
-    L = _native.lib()
-    stream = torch.cuda.current_stream()
-    k0 = torch.cuda.Event(enable_timing=True)
-    k1 = torch.cuda.Event(enable_timing=True)
-    reps = 50
-    import ctypes as C
-    k0.record(stream)
-    for _ in range(reps):
-        if args.delivery == "fused":
-            L.nc_sim_step_fused(C.byref(st.c), C.byref(sim.c_lif), stream.cuda_stream)
-        else:
-            L.nc_sim_deliver_push(C.byref(st.c), sim.c_lif.g_inh, stream.cuda_stream)
-    k1.record(stream)
-    torch.cuda.synchronize()
-    kernel_ms = k0.elapsed_time(k1) / reps
+    main_kernel = "fused" if args.delivery == "fused" else "push"
+    kms = kernel_ms(sim, main_kernel)
     n_local = lay.n_local(rank)
     csr = net.shards[rank]
     # algorithmic bytes of one fused step: 4 B per synapse
@@ -190,16 +230,39 @@ def run_ours(args) -> dict | None:
     neuron_bytes = n_local * (4 * csr.n_tiles + 8 + 8 + 2 + 4) + csr.slice_ptr.numel() * 8 + 2 * (lay.n_words * 4)
     alg_bytes = syn_bytes + neuron_bytes
     peaks = load_peaks()
-    achieved = alg_bytes / (kernel_ms * 1e-3) / 1e9
+    achieved = alg_bytes / (kms * 1e-3) / 1e9
     traffic = None
     prof = ROOT / "profiles" / "ncu_step_fused.json"
-    if prof.is_file():
+    if prof.is_file() and main_kernel == "fused" and world == 1:
         traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+    e2e = e2e_measure(sim, net, args) if (world == 1 and rank == 0) else None
+    launches = args.steps * sim.launches_per_step()
+    if world > 1:
+        sim.close()
+    del sim
+
+    # ---- the event-driven alternative on the same network (bit-identical results)
+    event = None
+    if args.with_push and args.delivery == "fused":
+        psim = make_sim(net, lif, args, "push", world)
+        pms, pspikes, plat, plat_max = time_steps(psim, args, world, dev)
+        push_ms = kernel_ms(psim, "push")
+        lif_ms = kernel_ms(psim, "lif")
+        fired_syn = pspikes / max(args.steps, 1) * args.degree / max(world, 1)
+        push_bytes = fired_syn * 12          # 4 B entry read + 4 B read + 4 B write per reduction
+        event = {"value": round(args.steps / (pms * 1e-3), 2), "ms_per_step": round(pms / args.steps, 5),
+                 "push_kernel_ms": round(push_ms, 5), "lif_kernel_ms": round(lif_ms, 5),
+                 "push_bound": "L2 atomics: %.3g reductions/s" % (fired_syn / (push_ms * 1e-3)),
+                 "push_achieved_gbs": round(push_bytes / (push_ms * 1e-3) / 1e9, 1),
+                 "exchange_us": lat_summary(plat, plat_max, args.transport),
+                 "gpu_launches": args.steps * psim.launches_per_step()}
+        if world > 1:
+            psim.close()
+        del psim
 
     result = None
     if rank == 0:
         cpu = cpu_baseline(net, lay, lif, args) if (world == 1 and not args.no_cpu) else None
-        e2e = e2e_measure(sim, net, args) if world == 1 else None
         result = {
             "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 5), "higher_is_better": True,
@@ -221,23 +284,16 @@ def run_ours(args) -> dict | None:
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": traffic,
                          "kernel": "k_step_fused" if args.delivery == "fused" else "k_deliver_push",
-                         "kernel_ms": round(kernel_ms, 5), "algorithmic_bytes": int(alg_bytes),
+                         "kernel_ms": round(kms, 5), "algorithmic_bytes": int(alg_bytes),
                          "peak_source": peaks["source"]},
-            "exchange_us": None if lat is None else {
-                "p50": round(float(np.percentile(lat, 50)), 2), "p99": round(float(np.percentile(lat, 99)), 2),
-                "p50_incl_skew": round(float(np.percentile(lat_max, 50)), 2),
-                "p99_incl_skew": round(float(np.percentile(lat_max, 99)), 2),
-                "transport": args.transport,
-                "what": "device %globaltimer from a rank's buckets-ready to its last inbound spike in the "
-                        "bitmap; p50/p99 over steps of the min over ranks (the last-ready rank: transfer + "
-                        "signalling), *_incl_skew: max over ranks (adds waiting for slower peers)"},
+            "event_driven": event,
+            "exchange_us": lat_summary(lat, lat_max, args.transport),
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": args.steps * sim.launches_per_step(),
+            "gpu_launches": launches,
             "clocks": clocks.summary(),
         }
     if world > 1:
-        sim.close()
         dist.barrier()
         dist.destroy_process_group()
     return result
@@ -389,6 +445,8 @@ def main() -> int:
     ap.add_argument("--chunk", type=int, default=100)
     ap.add_argument("--cpu-steps", type=int, default=10)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-push", dest="with_push", action="store_false",
+                    help="skip the event-driven (push) measurement reported beside the headline")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
