@@ -189,6 +189,15 @@ int nc_sim_deliver_pull(const nc_shard_t* sh, int32_t g_inh, void* stream);
 int nc_sim_deliver_push(const nc_shard_t* sh, int32_t g_inh, void* stream);
 int nc_sim_lif_update(const nc_shard_t* sh, const nc_lif_params_t* p, void* stream);
 
+/* Event-driven delivery needs the transpose of the pull synapses (push CSR,
+ * rows = internal pre ids over n_words*32 rows).  Built on the device by a
+ * counting sort: phase 0 adds every real entry's count into push_rowptr[pre+1]
+ * (zero-initialised int64[n_words*32+1]); the caller prefix-sums push_rowptr;
+ * phase 1 writes the entries (push_fill int32[n_words*32] zero-initialised).
+ * The shard's slice_ptr/row_meta/syn must be set; push fields are ignored. */
+int nc_build_push_csr(const nc_shard_t* sh, int32_t phase, int64_t* push_rowptr, int32_t* push_fill,
+                      uint32_t* push_syn, void* stream);
+
 /* Advance the device step counter and reset the per-step bucket counts. */
 int nc_sim_end_step(const nc_shard_t* sh, void* stream);
 

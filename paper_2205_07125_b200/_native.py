@@ -100,6 +100,7 @@ _SIGS = {
     "nc_sim_prepare": (c_int32, []),
     "nc_sim_lif_update": (c_int32, [C.POINTER(ShardC), C.POINTER(LifParamsC), c_void_p]),
     "nc_sim_end_step": (c_int32, [C.POINTER(ShardC), c_void_p]),
+    "nc_build_push_csr": (c_int32, [C.POINTER(ShardC), c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
     "nc_exchange_local": (c_int32, [C.POINTER(ShardC), c_int32, c_void_p, c_void_p, c_void_p, c_void_p,
                                     c_int64, c_void_p, c_void_p, c_int32, c_void_p]),
     "nc_graphgen_count": (c_int32, [C.POINTER(GraphGenC), c_int32, c_int32, c_void_p, c_void_p, c_void_p]),

@@ -280,21 +280,35 @@ k_step_fused(const nc_shard_t sh, const nc_lif_params_t p) {
 }
 
 // K1+K2 alone: consumes and zeroes acc.
-__global__ void __launch_bounds__(256) k_lif_update(const nc_shard_t sh, const nc_lif_params_t p) {
+// K1+K2 alone (consumes and zeroes acc).  Bucket appends are aggregated per
+// CTA: warps reserve offsets in shared memory, one thread per bucket claims the
+// CTA's range with a single global atomic, then warps write their ids -- a
+// few hundred global atomics per step instead of one per warp per bucket
+// (same-address atomics serialise in L2).
+constexpr int kLifThreads = 256;
+constexpr int kLifWarps = kLifThreads / 32;
+
+__global__ void __launch_bounds__(kLifThreads) k_lif_update(const nc_shard_t sh, const nc_lif_params_t p) {
   __shared__ unsigned int block_count;
+  __shared__ int cta_cnt[NC_MAX_SHARDS + 1];
+  __shared__ int cta_base[NC_MAX_SHARDS + 1];
+  __shared__ int warp_off[kLifWarps][NC_MAX_SHARDS + 1];
   if (threadIdx.x == 0) block_count = 0;
   __syncthreads();
   const int step = *sh.step;
   uint32_t* cur = (step & 1) ? sh.bitmap1 : sh.bitmap0;
   clear_remote(sh, cur);
   const int lane = threadIdx.x & 31;
-  const int wpb = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5;
   const int ntiles = (sh.n_local + 31) >> 5;
+  const int nq = sh.n_shards > 1 ? sh.n_shards : 0;      // buckets in use
+  const int nlist = sh.fired_ids ? 1 : 0;                // + the fired list (slot nq)
   uint32_t my_spikes = 0;
-  for (int tile = blockIdx.x * wpb + (threadIdx.x >> 5); tile < ntiles; tile += gridDim.x * wpb) {
+  for (int base = blockIdx.x * kLifWarps; base < ntiles; base += gridDim.x * kLifWarps) {
+    const int tile = base + warp;                         // uniform trip count per CTA
     const int row = (tile << 5) + lane;
     bool fired = false;
-    if (row < sh.n_local) {
+    if (tile < ntiles && row < sh.n_local) {
       float v = sh.v[row];
       float isyn = sh.i_syn[row];
       uint8_t ref = sh.refrac[row];
@@ -305,8 +319,43 @@ __global__ void __launch_bounds__(256) k_lif_update(const nc_shard_t sh, const n
       sh.i_syn[row] = isyn;
       sh.refrac[row] = ref;
     }
-    const uint32_t fm = emit_spikes(sh, cur, tile, row, fired, lane, step);
-    if (lane == 0) my_spikes += __popc(fm);
+    const uint32_t fmask = __ballot_sync(kFull, fired);
+    if (tile < ntiles && lane == 0) {
+      cur[(sh.local_base >> 5) + tile] = fmask;
+      if (sh.raster != nullptr && step < sh.record_steps)
+        sh.raster[(int64_t)step * sh.local_words + tile] = fmask;
+      my_spikes += __popc(fmask);
+    }
+    if (nq + nlist == 0) continue;
+    __syncthreads();
+    if ((int)threadIdx.x <= NC_MAX_SHARDS) cta_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const uint32_t hm = fired ? (uint32_t)sh.hop_mask[row] : 0u;
+    // pass 1: reserve CTA-local offsets
+    for (int h = 0; h < nq + nlist; ++h) {
+      const uint32_t m = (h < nq) ? __ballot_sync(kFull, (hm >> h) & 1u) : fmask;
+      int off = 0;
+      if (lane == 0 && m) off = atomicAdd(&cta_cnt[h], __popc(m));
+      if (lane == 0) warp_off[warp][h] = off;
+    }
+    __syncthreads();
+    if ((int)threadIdx.x < nq + nlist) {
+      const int h = threadIdx.x;
+      int32_t* cnt = h < nq ? sh.bucket_count + h : sh.fired_count;
+      cta_base[h] = cta_cnt[h] ? atomicAdd(cnt, cta_cnt[h]) : 0;
+    }
+    __syncthreads();
+    // pass 2: write ids
+    const uint32_t my_id = (uint32_t)(sh.local_base + row);
+    for (int h = 0; h < nq + nlist; ++h) {
+      const uint32_t m = (h < nq) ? __ballot_sync(kFull, (hm >> h) & 1u) : fmask;
+      if ((m >> lane) & 1u) {
+        const int64_t pos = (int64_t)cta_base[h] + warp_off[warp][h] + __popc(m & ((1u << lane) - 1u));
+        const int64_t cap = h < nq ? sh.bucket_cap : sh.n_local;
+        if (pos < cap) (h < nq ? sh.bucket_ids + (int64_t)h * sh.bucket_cap : sh.fired_ids)[pos] = my_id;
+        else atomicExch(sh.status, 1);
+      }
+    }
   }
   add_spike_total(sh, my_spikes, &block_count);
 }
@@ -507,9 +556,9 @@ extern "C" int nc_sim_lif_update(const nc_shard_t* sh, const nc_lif_params_t* p,
   // grid-stride over 32-neuron tiles with ~2 CTAs per SM: one global spike-count
   // atomic per CTA (thousands of same-address atomics cost more than the update)
   const int tiles = (sh->n_local + 31) / 32;
-  int grid = (tiles + 7) / 8;
+  int grid = (tiles + kLifWarps - 1) / kLifWarps;
   grid = grid < 1 ? 1 : (grid > 2 * num_sms() ? 2 * num_sms() : grid);
-  k_lif_update<<<grid, 256, 0, (cudaStream_t)stream>>>(*sh, *p);
+  k_lif_update<<<grid, kLifThreads, 0, (cudaStream_t)stream>>>(*sh, *p);
   NC_LAUNCH_CHECK();
   return NC_OK;
 }
@@ -517,6 +566,58 @@ extern "C" int nc_sim_lif_update(const nc_shard_t* sh, const nc_lif_params_t* p,
 extern "C" int nc_sim_end_step(const nc_shard_t* sh, void* stream) {
   if (int e = check_shard(sh)) return e;
   k_end_step<<<1, 32, 0, (cudaStream_t)stream>>>(*sh);
+  NC_LAUNCH_CHECK();
+  return NC_OK;
+}
+
+// ---------------------------------------------------------------- push CSR
+// Transpose of the SELL-32 pull synapses (rows = internal pre ids) built on
+// the device by counting sort: phase 0 counts entries per pre into
+// push_rowptr[pre + 1]; the host scans; phase 1 claims slots with atomics.
+// Entry = (inhibitory << 31) | ((q - 1) << 26) | post_local.
+namespace {
+__global__ void k_push_build(const nc_shard_t sh, int phase, int64_t* rowptr, int32_t* fill, uint32_t* out) {
+  const int lane = threadIdx.x & 31;
+  const int T = sh.n_tiles;
+  const int n_slices = (sh.n_local + 31) >> 5;
+  const int64_t n_blocks = (int64_t)n_slices * T;
+  const uint4* syn4 = reinterpret_cast<const uint4*>(sh.syn);
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t blk = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; blk < n_blocks; blk += nw) {
+    const int slice = (int)(blk / T), t = (int)(blk % T);
+    const int row = (slice << 5) + lane;
+    const int64_t b0 = sh.slice_ptr[blk];
+    const uint32_t meta = row < sh.n_local ? sh.row_meta[(int64_t)row * T + t] : 0u;
+    const int emid = (int)(meta & 0xFFFFu), mine = (int)(meta >> 16);
+    for (int u = 0; u < mine; ++u) {
+      const uint4 e4 = syn4[b0 + (int64_t)u * 32 + lane];
+      const uint32_t es[4] = {e4.x, e4.y, e4.z, e4.w};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint32_t e = es[c];
+        const uint32_t q = e >> 26;
+        if (q == 0) continue;
+        const uint32_t pre = e & 0x03FFFFFFu;
+        if (phase == 0) {
+          atomicAdd(reinterpret_cast<unsigned long long*>(rowptr + pre + 1), 1ull);
+        } else {
+          const int32_t slot = atomicAdd(fill + pre, 1);
+          out[rowptr[pre] + slot] = ((u >= emid ? 1u : 0u) << 31) | ((q - 1u) << 26) | (uint32_t)row;
+        }
+      }
+    }
+  }
+}
+}  // namespace
+
+extern "C" int nc_build_push_csr(const nc_shard_t* sh, int32_t phase, int64_t* push_rowptr, int32_t* push_fill,
+                                 uint32_t* push_syn, void* stream) {
+  if (int e = check_shard(sh)) return e;
+  if (phase != 0 && phase != 1) {
+    nc_set_error("nc_build_push_csr: phase must be 0 or 1");
+    return NC_E_ARG;
+  }
+  k_push_build<<<16 * num_sms(), 256, 0, (cudaStream_t)stream>>>(*sh, phase, push_rowptr, push_fill, push_syn);
   NC_LAUNCH_CHECK();
   return NC_OK;
 }

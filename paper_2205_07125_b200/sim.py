@@ -532,21 +532,31 @@ class _ShardState:
 
 
 def _push_csr(csr: ShardCSR, lay: ShardLayout, h: int, dev):
-    """Transpose of the pull synapses: rows = internal pre ids,
-    entries = (inhibitory << 31) | ((q - 1) << 26) | post_local.  Built once per
-    shard and cached on the SellCSR."""
+    """Transpose of the pull synapses (rows = internal pre ids), entries
+    (inhibitory << 31) | ((q - 1) << 26) | post_local, built on the device by
+    the counting-sort kernel nc_build_push_csr.  Cached on the SellCSR."""
     import torch
     cached = getattr(csr, "_push_cache", None)
     if cached is not None:
         return cached
-    row, pre, q, inh = sell.decode(csr)
-    ent = (inh.to(torch.int64) << 31) | ((q - 1) << ID_BITS) | row
-    order = torch.argsort(pre, stable=True)
-    pre, ent = pre[order], ent[order]
+    L = _native.lib()
+    st = _native.stream_handle(dev)
     n_rows = lay.n_words * 32
+    scratch = torch.zeros(8, dtype=torch.int32, device=dev)
+    c = _native.ShardC(shard=h, n_shards=lay.n_shards, n_local=lay.n_local(h), local_base=int(lay.base[h]),
+                       n_words=lay.n_words, n_tiles=csr.n_tiles, tile_words=csr.tile_words, pad0=0,
+                       slice_ptr=csr.slice_ptr.data_ptr(), row_meta=csr.row_meta.data_ptr(), syn=csr.syn.data_ptr(),
+                       bitmap0=scratch.data_ptr(), bitmap1=scratch.data_ptr(), status=scratch.data_ptr(),
+                       step=scratch.data_ptr())
     rowptr = torch.zeros(n_rows + 1, dtype=torch.int64, device=dev)
-    rowptr[1:] = torch.cumsum(torch.bincount(pre, minlength=n_rows), 0)
-    ent = torch.where(ent >= 2**31, ent - 2**32, ent).to(torch.int32)
+    _native.check(L.nc_build_push_csr(C.byref(c), 0, rowptr.data_ptr(), None, None, st), "push csr count")
+    torch.cumsum(rowptr, 0, out=rowptr)
+    total = int(rowptr[-1].item())
+    ent = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+    fill = torch.zeros(n_rows, dtype=torch.int32, device=dev)
+    _native.check(L.nc_build_push_csr(C.byref(c), 1, rowptr.data_ptr(), fill.data_ptr(), ent.data_ptr(), st),
+                  "push csr fill")
+    del fill, scratch
     csr._push_cache = (rowptr, ent)
     return rowptr, ent
 
