@@ -93,6 +93,16 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def workload_name(args, world: int) -> str:
+    if args.communities > 1:
+        return (f"regional (config 5 family): {args.neurons * world} neurons in {args.communities} regions, "
+                f"{args.intra_frac:.0%} of ~{args.degree:.0f} synapses intra-region, {world} GPU(s), block partition")
+    if world == 1 and args.neurons == 1_000_000:
+        return "config 2: 1M LIF neurons x 1k synapses, single B200, update + delivery kernels"
+    return (f"weak scaling: {args.neurons} neurons/GPU x {args.degree:.0f} synapses, {world} GPU(s), "
+            f"block partition, direct exchange ({args.transport})")
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -206,7 +216,15 @@ def run_ours(args) -> dict | None:
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     n_neurons = args.neurons * world
-    spec = S.GeneratorSpec.random(n_neurons, args.degree, seed=args.seed)
+    if args.communities > 1:
+        # regional model (config 5): `intra_frac` of each neuron's ~degree synapses inside its region
+        c = args.communities
+        size = n_neurons / c
+        p_in = args.intra_frac * args.degree / max(size - 1, 1)
+        p_out = (1 - args.intra_frac) * args.degree / max(n_neurons - size, 1)
+        spec = S.GeneratorSpec(n_neurons, c, min(p_in, 1.0), min(p_out, p_in), seed=args.seed)
+    else:
+        spec = S.GeneratorSpec.random(n_neurons, args.degree, seed=args.seed)
     lay = S.ShardLayout.blocks(n_neurons, world)
     t_build = time.time()
     net = S.Network.generate(spec, lay, device=dev, shards=[rank])
@@ -269,10 +287,7 @@ def run_ours(args) -> dict | None:
             "scaling": "weak", "vs_baseline": None, "dtype": "fp32 state / int32 synaptic sums",
             "data": "synthetic (device SBM generator, generate_synthetic distributions)",
             "config": {
-                "workload": ("config 2: 1M LIF neurons x 1k synapses, single B200, update + delivery kernels"
-                             if world == 1 else
-                             f"weak scaling: {args.neurons} neurons/GPU x {args.degree} synapses, block partition, "
-                             f"direct exchange ({args.transport})"),
+                "workload": workload_name(args, world),
                 "neurons": n_neurons, "mean_degree": args.degree, "synapses": int(net.n_synapses) * world,
                 "delivery": args.delivery, "exchange": "none" if world == 1 else "direct",
                 "firing_rate_hz": round(spikes / n_neurons / (args.steps * 1e-3), 3),
@@ -438,6 +453,8 @@ def main() -> int:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--neurons", type=int, default=1_000_000, help="neurons per GPU")
     ap.add_argument("--degree", type=float, default=1000.0)
+    ap.add_argument("--communities", type=int, default=1, help=">1: regional SBM (config 5 family)")
+    ap.add_argument("--intra-frac", type=float, default=0.9, help="regional: fraction of synapses inside a region")
     ap.add_argument("--delivery", default="fused", choices=["fused", "push"])
     ap.add_argument("--transport", default="p2p", choices=["nccl", "p2p"])
     ap.add_argument("--msg-cap", type=int, default=65536, help="ids per exchange message (NCCL sends all of it)")
