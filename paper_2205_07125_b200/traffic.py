@@ -120,6 +120,36 @@ def exact_bin_sums(values_dev, keys_dev, n_bins: int, *, pairs=None, stream=None
     return out
 
 
+_DEVICE_GRAPHS: "weakref.WeakKeyDictionary" = None
+
+
+def _device_graph(graph, dev):
+    """Edge columns and weights of `graph` on the device, uploaded once per graph object.
+
+    Graphs are treated as immutable (SPEC concurrency model); the cache is keyed
+    by the object and the identity of its arrays, so replacing an array re-uploads.
+    Repeated aggregation (cross_traffic, the GA fitness, sweep_noise) then only
+    moves the assignment.
+    """
+    import torch
+    import weakref
+    global _DEVICE_GRAPHS
+    if _DEVICE_GRAPHS is None:
+        _DEVICE_GRAPHS = weakref.WeakKeyDictionary()
+    key = (str(dev), id(graph.weights), id(graph.edge_i), id(graph.edge_j), id(graph.edge_p))
+    hit = _DEVICE_GRAPHS.get(graph)
+    if hit is not None and hit[0] == key:
+        return hit[1]
+    up = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev)  # noqa: E731
+    val = (up(graph.weights, np.float64), up(graph.edge_i, np.int64), up(graph.edge_j, np.int64),
+           up(graph.edge_p, np.float64))
+    try:
+        _DEVICE_GRAPHS[graph] = (key, val)
+    except TypeError:  # not weak-referenceable: no caching
+        pass
+    return val
+
+
 def aggregate(graph, pm) -> GpuTrafficGraph:
     """Collapse neuron traffic onto GPUs (traffic.py:66-84) with the K5 kernel."""
     import torch
@@ -129,11 +159,8 @@ def aggregate(graph, pm) -> GpuTrafficGraph:
         )
     n = int(pm.n_gpus)
     dev = _device()
-    w = torch.from_numpy(np.ascontiguousarray(graph.weights, dtype=np.float64)).to(dev)
+    w, ei, ej, ep = _device_graph(graph, dev)
     asg = torch.from_numpy(np.ascontiguousarray(pm.assignment, dtype=np.int64)).to(dev)
-    ei = torch.from_numpy(np.ascontiguousarray(graph.edge_i, dtype=np.int64)).to(dev)
-    ej = torch.from_numpy(np.ascontiguousarray(graph.edge_j, dtype=np.int64)).to(dev)
-    ep = torch.from_numpy(np.ascontiguousarray(graph.edge_p, dtype=np.float64)).to(dev)
     cells = exact_bin_sums(w, asg, n, pairs=(ei, ej, ep)).reshape(n, n)
     upper = np.triu(cells)
     pg = upper + np.triu(cells, 1).T

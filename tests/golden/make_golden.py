@@ -107,6 +107,15 @@ def main() -> int:
                 "bottleneck": rep.bottleneck_link,
                 "topology": {"gpus_per_node": 2, "nodes_per_switch": 2}, "noise": 0.3,
             })
+    # GA baseline (partition.py:187-267): small populations, fitness through aggregate
+    index["ga"] = []
+    for name, n_gpus, pop, gens, seed in (("tiny_c3", 3, 8, 6, 1), ("sbm_c4", 4, 6, 4, 2)):
+        g = nc.generate_synthetic(nc.ModelSpec(**specs[name]))
+        ga = nc.partition_genetic(g, n_gpus, nc.GaConfig(population_size=pop, generations=gens, seed=seed))
+        key = f"ga/{name}/{n_gpus}"
+        arrays[key] = ga.assignment
+        index["ga"].append({"key": key, "graph": name, "n_gpus": n_gpus, "population_size": pop,
+                            "generations": gens, "seed": seed})
     np.savez_compressed(OUT / "reference_fixtures.npz", **arrays)
     (OUT / "reference_fixtures.json").write_text(json.dumps(index, indent=1, sort_keys=True) + "\n")
     print(f"wrote {len(arrays)} arrays, {len(index['cases'])} cases")

@@ -57,6 +57,17 @@ def test_aggregate_bit_identical_to_reference(ref_fixtures):
         assert nc.cross_traffic(g, pm).hex() == case["cross_traffic"]
 
 
+def test_genetic_partition_matches_reference(ref_fixtures):
+    """GA baseline: same numpy stream, fitness through the exact GPU aggregate."""
+    idx, arr = ref_fixtures
+    for case in idx["ga"]:
+        g = graph(case["graph"], **idx["graphs"][case["graph"]]["spec"])
+        cfg = nc.GaConfig(population_size=case["population_size"], generations=case["generations"],
+                          seed=case["seed"])
+        pm = nc.partition_genetic(g, case["n_gpus"], cfg)
+        np.testing.assert_array_equal(pm.assignment, arr[case["key"]], err_msg=case["key"])
+
+
 def test_aggregate_order_independent_and_wide_exponents():
     rng = np.random.default_rng(3)
     m, e = 300, 4000

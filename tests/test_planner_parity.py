@@ -177,6 +177,23 @@ def test_io_round_trips(tmp_path):
     assert e.value.line == 4
 
 
+def test_binary_sidecar_round_trip(tmp_path):
+    from paper_2205_07125_b200.model import load_graph_binary, save_graph_binary
+    g = nc.generate_synthetic(nc.ModelSpec(500, 4, 0.05, 0.005, 0.5, 2.0, seed=3))
+    save_graph_binary(g, tmp_path / "g.nngb")
+    h = load_graph_binary(tmp_path / "g.nngb")
+    assert h == g and h.n_edges == g.n_edges
+    np.testing.assert_array_equal(h.edge_i, g.edge_i)          # ascending order preserved
+    raw = bytearray((tmp_path / "g.nngb").read_bytes())
+    raw[0:8] = b"XXXXXXXX"
+    (tmp_path / "bad.nngb").write_bytes(bytes(raw))
+    with pytest.raises(nc.ParseError):
+        load_graph_binary(tmp_path / "bad.nngb")
+    (tmp_path / "short.nngb").write_bytes((tmp_path / "g.nngb").read_bytes()[:-8])
+    with pytest.raises(nc.ParseError):
+        load_graph_binary(tmp_path / "short.nngb")
+
+
 def test_validate_and_spec_errors():
     with pytest.raises(nc.SpecificationError):
         nc.generate_synthetic(nc.ModelSpec(0, 1, 0.1, 0.0))
