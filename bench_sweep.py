@@ -129,7 +129,16 @@ def main() -> int:
                 })
                 print(json.dumps(rows[-1]), flush=True)
     if rank == 0:
-        doc = {"config": {"neurons": n, "gpus": world, "groups": args.groups, "degree": args.degree,
+        # calibrate the reference's analytic model on the measured exchange latency
+        samples = [(tables[r["route"]], r["rate_hz"] * 1e-3, r["exchange_us_p50"]) for r in rows]
+        spec, fit = nc.netsim.calibrate_topology(samples, gt, world)
+        for r, (_, _, meas, model) in zip(rows, fit):
+            r["netsim_calibrated_us"] = round(model, 2)
+        calib = {k: getattr(spec, k) for k in ("gpus_per_node", "nodes_per_switch", "intra_node_bandwidth",
+                                               "inter_node_bandwidth", "per_hop_latency",
+                                               "connection_setup_cost")}
+        doc = {"calibrated_topology_spec_us": calib, "pg": pg.tolist(),
+               "config": {"neurons": n, "gpus": world, "groups": args.groups, "degree": args.degree,
                           "delivery": args.delivery, "steps": args.steps, "warmup": args.warmup,
                           "groups_membership": groups.membership.tolist(),
                           "bridges": [[a, b, v] for (a, b), v in sorted(tables["two-level"].bridges.items())],

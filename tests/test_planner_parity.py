@@ -217,3 +217,20 @@ def test_netsim_linearity_and_checks():
         netsim.map_flows(rt, gt, topo, 0.0)
     with pytest.raises(nc.SpecificationError):
         nc.build_topology(nc.TopologySpec(gpus_per_node=0), 4)
+
+
+def test_calibrate_topology_recovers_parameters():
+    """Synthetic measurements from a known spec are fitted back (NVSwitch one-box model)."""
+    n = 4
+    pg = np.ones((n, n)) - np.eye(n)
+    gt = nc.GpuTrafficGraph(n, pg * 1000.0, np.ones(n))
+    groups = nc.group_gpus(gt, 2)
+    tables = [nc.route_p2p(gt), nc.build_routing_table(gt, groups, nc.select_bridges(gt, groups))]
+    true = nc.TopologySpec(gpus_per_node=1, nodes_per_switch=n, intra_node_bandwidth=50.0,
+                           inter_node_bandwidth=20.0, per_hop_latency=1.5, connection_setup_cost=0.5)
+    topo = nc.build_topology(true, n)
+    samples = [(rt, nu, nc.step_latency(nc.map_flows(rt, gt, topo, nu), rt, topo, nu).step_time)
+               for rt in tables for nu in (0.001, 0.005, 0.01, 0.02, 0.05)]
+    spec, rows = netsim.calibrate_topology(samples, gt, n)
+    for _, _, meas, model in rows:
+        assert abs(model - meas) <= 1e-6 * max(1.0, meas)
