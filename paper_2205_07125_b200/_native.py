@@ -39,7 +39,7 @@ class ShardC(C.Structure):
     _fields_ = [
         ("shard", c_int32), ("n_shards", c_int32), ("n_local", c_int32),
         ("local_base", c_int32), ("n_words", c_int32), ("n_tiles", c_int32), ("tile_words", c_int32),
-        ("pad0", c_int32),
+        ("flags", c_int32),
         ("v", c_void_p), ("i_syn", c_void_p), ("refrac", c_void_p), ("acc", c_void_p),
         ("gid", c_void_p), ("hop_mask", c_void_p),
         ("slice_ptr", c_void_p), ("row_meta", c_void_p), ("syn", c_void_p),

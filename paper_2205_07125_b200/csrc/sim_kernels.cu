@@ -236,8 +236,11 @@ k_step_fused(const nc_shard_t sh, const nc_lif_params_t p) {
     const int per = (n_slices + gridDim.x - 1) / gridDim.x;
     const int s0 = blockIdx.x * per;
     const int s1 = min(n_slices, s0 + per);
-    int32_t* part = reinterpret_cast<int32_t*>(sbm + TW);
-    for (int k = threadIdx.x; k < per * 32; k += blockDim.x) part[k] = 0;
+    // partial sums per row: shared memory behind the tile, or the acc array when
+    // the CTA's rows do not fit next to a useful tile (flags bit 0)
+    int32_t* part = (sh.flags & 1) ? sh.acc + (int64_t)s0 * 32 : reinterpret_cast<int32_t*>(sbm + TW);
+    const int n_part = (sh.flags & 1) ? min(per * 32, sh.n_local - s0 * 32) : per * 32;
+    for (int k = threadIdx.x; k < n_part; k += blockDim.x) part[k] = 0;
     __shared__ int next_slice[2];
     if (threadIdx.x == 0) next_slice[0] = next_slice[1] = s0;
     for (int t = 0; t < T; ++t) {
@@ -280,35 +283,42 @@ k_step_fused(const nc_shard_t sh, const nc_lif_params_t p) {
 }
 
 // K1+K2 alone: consumes and zeroes acc.
-// K1+K2 alone (consumes and zeroes acc).  Bucket appends are aggregated per
-// CTA: warps reserve offsets in shared memory, one thread per bucket claims the
-// CTA's range with a single global atomic, then warps write their ids -- a
-// few hundred global atomics per step instead of one per warp per bucket
-// (same-address atomics serialise in L2).
+// K1+K2 alone (consumes and zeroes acc).  Every CTA owns a contiguous range of
+// 32-neuron tiles and appends to the buckets with ONE global atomic per bucket
+// for the whole step: pass A runs the LIF update, stores each tile's spike mask
+// in shared memory and counts per warp and bucket; the CTA then claims its
+// ranges; pass B recomputes the per-bucket ballots from the stored masks and the
+// static hop masks and writes the ids.  (Same-address atomics serialise in L2:
+// one per warp per bucket cost more than the update itself.)
 constexpr int kLifThreads = 256;
 constexpr int kLifWarps = kLifThreads / 32;
+constexpr int kLifMaxTiles = 2048;   // tiles per CTA (fmask storage: 8 KB)
 
 __global__ void __launch_bounds__(kLifThreads) k_lif_update(const nc_shard_t sh, const nc_lif_params_t p) {
   __shared__ unsigned int block_count;
-  __shared__ int cta_cnt[NC_MAX_SHARDS + 1];
+  __shared__ uint32_t fmask_s[kLifMaxTiles];
+  __shared__ int warp_cnt[kLifWarps][NC_MAX_SHARDS + 1];
   __shared__ int cta_base[NC_MAX_SHARDS + 1];
-  __shared__ int warp_off[kLifWarps][NC_MAX_SHARDS + 1];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int nq = sh.n_shards > 1 ? sh.n_shards : 0;      // buckets in use
+  const int nb = nq + (sh.fired_ids ? 1 : 0);            // + the fired list (slot nq)
   if (threadIdx.x == 0) block_count = 0;
+  for (int k = threadIdx.x; k < kLifWarps * (NC_MAX_SHARDS + 1); k += blockDim.x)
+    (&warp_cnt[0][0])[k] = 0;
   __syncthreads();
   const int step = *sh.step;
   uint32_t* cur = (step & 1) ? sh.bitmap1 : sh.bitmap0;
   clear_remote(sh, cur);
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
   const int ntiles = (sh.n_local + 31) >> 5;
-  const int nq = sh.n_shards > 1 ? sh.n_shards : 0;      // buckets in use
-  const int nlist = sh.fired_ids ? 1 : 0;                // + the fired list (slot nq)
+  const int per = (ntiles + gridDim.x - 1) / gridDim.x;
+  const int t0 = blockIdx.x * per, t1 = min(ntiles, t0 + per);
   uint32_t my_spikes = 0;
-  for (int base = blockIdx.x * kLifWarps; base < ntiles; base += gridDim.x * kLifWarps) {
-    const int tile = base + warp;                         // uniform trip count per CTA
+  // ---- pass A: update, spike masks, per-warp bucket counts
+  for (int tile = t0 + warp; tile < t1; tile += kLifWarps) {
     const int row = (tile << 5) + lane;
     bool fired = false;
-    if (tile < ntiles && row < sh.n_local) {
+    if (row < sh.n_local) {
       float v = sh.v[row];
       float isyn = sh.i_syn[row];
       uint8_t ref = sh.refrac[row];
@@ -320,40 +330,54 @@ __global__ void __launch_bounds__(kLifThreads) k_lif_update(const nc_shard_t sh,
       sh.refrac[row] = ref;
     }
     const uint32_t fmask = __ballot_sync(kFull, fired);
-    if (tile < ntiles && lane == 0) {
+    if (lane == 0) {
       cur[(sh.local_base >> 5) + tile] = fmask;
-      if (sh.raster != nullptr && step < sh.record_steps)
-        sh.raster[(int64_t)step * sh.local_words + tile] = fmask;
+      if (sh.raster != nullptr && step < sh.record_steps) sh.raster[(int64_t)step * sh.local_words + tile] = fmask;
+      fmask_s[tile - t0] = fmask;
       my_spikes += __popc(fmask);
     }
-    if (nq + nlist == 0) continue;
-    __syncthreads();
-    if ((int)threadIdx.x <= NC_MAX_SHARDS) cta_cnt[threadIdx.x] = 0;
-    __syncthreads();
-    const uint32_t hm = fired ? (uint32_t)sh.hop_mask[row] : 0u;
-    // pass 1: reserve CTA-local offsets
-    for (int h = 0; h < nq + nlist; ++h) {
-      const uint32_t m = (h < nq) ? __ballot_sync(kFull, (hm >> h) & 1u) : fmask;
-      int off = 0;
-      if (lane == 0 && m) off = atomicAdd(&cta_cnt[h], __popc(m));
-      if (lane == 0) warp_off[warp][h] = off;
+    if (nb && fmask) {
+      const uint32_t hm = fired ? (uint32_t)sh.hop_mask[row] : 0u;
+      for (int h = 0; h < nb; ++h) {
+        const uint32_t m = (h < nq) ? __ballot_sync(kFull, (hm >> h) & 1u) : fmask;
+        if (lane == 0) warp_cnt[warp][h] += __popc(m);
+      }
     }
-    __syncthreads();
-    if ((int)threadIdx.x < nq + nlist) {
-      const int h = threadIdx.x;
-      int32_t* cnt = h < nq ? sh.bucket_count + h : sh.fired_count;
-      cta_base[h] = cta_cnt[h] ? atomicAdd(cnt, cta_cnt[h]) : 0;
+  }
+  __syncthreads();
+  // ---- one global atomic per bucket per CTA; warp prefix inside the CTA
+  if ((int)threadIdx.x < nb) {
+    const int h = threadIdx.x;
+    int total = 0;
+    for (int w = 0; w < kLifWarps; ++w) {
+      const int c = warp_cnt[w][h];
+      warp_cnt[w][h] = total;  // exclusive prefix = the warp's base
+      total += c;
     }
-    __syncthreads();
-    // pass 2: write ids
-    const uint32_t my_id = (uint32_t)(sh.local_base + row);
-    for (int h = 0; h < nq + nlist; ++h) {
-      const uint32_t m = (h < nq) ? __ballot_sync(kFull, (hm >> h) & 1u) : fmask;
-      if ((m >> lane) & 1u) {
-        const int64_t pos = (int64_t)cta_base[h] + warp_off[warp][h] + __popc(m & ((1u << lane) - 1u));
-        const int64_t cap = h < nq ? sh.bucket_cap : sh.n_local;
-        if (pos < cap) (h < nq ? sh.bucket_ids + (int64_t)h * sh.bucket_cap : sh.fired_ids)[pos] = my_id;
-        else atomicExch(sh.status, 1);
+    int32_t* cnt = h < nq ? sh.bucket_count + h : sh.fired_count;
+    cta_base[h] = total ? atomicAdd(cnt, total) : 0;
+  }
+  __syncthreads();
+  // ---- pass B: write ids
+  if (nb) {
+    for (int tile = t0 + warp; tile < t1; tile += kLifWarps) {
+      const uint32_t fmask = fmask_s[tile - t0];
+      if (!fmask) continue;
+      const int row = (tile << 5) + lane;
+      const bool fired = (fmask >> lane) & 1u;
+      const uint32_t hm = fired ? (uint32_t)sh.hop_mask[row] : 0u;
+      const uint32_t my_id = (uint32_t)(sh.local_base + row);
+      for (int h = 0; h < nb; ++h) {
+        const uint32_t m = (h < nq) ? __ballot_sync(kFull, (hm >> h) & 1u) : fmask;
+        if ((m >> lane) & 1u) {
+          const int64_t pos = (int64_t)cta_base[h] + warp_cnt[warp][h] + __popc(m & ((1u << lane) - 1u));
+          const int64_t cap = h < nq ? sh.bucket_cap : sh.n_local;
+          if (pos < cap) (h < nq ? sh.bucket_ids + (int64_t)h * sh.bucket_cap : sh.fired_ids)[pos] = my_id;
+          else atomicExch(sh.status, 1);
+        }
+        __syncwarp();
+        if (lane == 0) warp_cnt[warp][h] += __popc(m);
+        __syncwarp();
       }
     }
   }
@@ -446,6 +470,7 @@ int g_max_dyn_smem = 0;   // opt-in limit minus the kernels' static shared memor
 // the per-row partial sums of the CTA's slice range
 size_t step_smem_bytes(const nc_shard_t& sh, int grid) {
   if (sh.n_tiles <= 1) return (size_t)((sh.n_words + 3) >> 2) * 16;
+  if (sh.flags & 1) return (size_t)sh.tile_words * 4;
   const int n_slices = (sh.n_local + 31) >> 5;
   const int per = (n_slices + grid - 1) / grid;
   return (size_t)sh.tile_words * 4 + (size_t)per * 32 * 4;
@@ -472,7 +497,8 @@ int check_shard(const nc_shard_t* sh) {
   if (!sh || sh->n_local < 0 || sh->n_words < 1 || (sh->local_base & 31) || !sh->step ||
       !sh->status || !sh->bitmap0 || !sh->bitmap1 || sh->n_tiles < 1 ||
       (sh->n_tiles > 1 && (sh->tile_words < 4 || (sh->tile_words & 3) ||
-                           (int64_t)sh->tile_words * sh->n_tiles < sh->n_words))) {
+                           (int64_t)sh->tile_words * sh->n_tiles < sh->n_words)) ||
+      ((sh->flags & 1) && !sh->acc)) {
     nc_set_error("invalid nc_shard_t");
     return NC_E_ARG;
   }
@@ -553,11 +579,12 @@ extern "C" int nc_sim_lif_update(const nc_shard_t* sh, const nc_lif_params_t* p,
     nc_set_error("nc_sim_lif_update: shard has no acc buffer");
     return NC_E_ARG;
   }
-  // grid-stride over 32-neuron tiles with ~2 CTAs per SM: one global spike-count
-  // atomic per CTA (thousands of same-address atomics cost more than the update)
+  // contiguous tile ranges, ~2 CTAs per SM (more if a range would exceed the
+  // shared spike-mask storage): one global atomic per bucket per CTA
   const int tiles = (sh->n_local + 31) / 32;
-  int grid = (tiles + kLifWarps - 1) / kLifWarps;
-  grid = grid < 1 ? 1 : (grid > 2 * num_sms() ? 2 * num_sms() : grid);
+  int grid = 2 * num_sms();
+  if ((tiles + grid - 1) / grid > kLifMaxTiles) grid = (tiles + kLifMaxTiles - 1) / kLifMaxTiles;
+  if (grid > tiles) grid = tiles > 0 ? tiles : 1;
   k_lif_update<<<grid, kLifThreads, 0, (cudaStream_t)stream>>>(*sh, *p);
   NC_LAUNCH_CHECK();
   return NC_OK;

@@ -25,18 +25,26 @@ SMEM_BYTES = 227 * 1024            # opt-in dynamic shared memory per CTA on sm_
 SMEM_RESERVE = 1024                # static shared memory + slack
 
 
-def plan_tiles(n_words: int, n_local: int, n_sms: int) -> tuple[int, int]:
-    """(n_tiles, tile_words) for a shard: one tile if the whole bitmap fits."""
+def plan_tiles(n_words: int, n_local: int, n_sms: int) -> tuple[int, int, bool]:
+    """(n_tiles, tile_words, partials_in_global) for a shard.
+
+    One tile if the whole bitmap fits in shared memory.  Otherwise the per-row
+    partial sums of a CTA's rows share the shared memory with the tile; when
+    they would take more than a quarter of it (very large shards) they move to
+    the global `acc` array instead (one extra 8-byte read-modify-write per row
+    and tile).
+    """
+    budget_all = SMEM_BYTES - SMEM_RESERVE
     whole = (n_words + 3) // 4 * 4
-    if whole * 4 <= SMEM_BYTES - SMEM_RESERVE:
-        return 1, whole
+    if whole * 4 <= budget_all:
+        return 1, whole, False
     n_slices = (n_local + 31) // 32
     per = (n_slices + n_sms - 1) // n_sms
-    budget = SMEM_BYTES - SMEM_RESERVE - per * 32 * 4
-    if budget < 16 * 1024:
-        raise ValueError(f"shard of {n_local} neurons leaves no shared memory for the bitmap tile")
+    part = per * 32 * 4
+    global_part = part > budget_all // 4
+    budget = budget_all - (0 if global_part else part)
     tw = budget // 4 // 4 * 4
-    return (n_words + tw - 1) // tw, tw
+    return (n_words + tw - 1) // tw, tw, global_part
 
 
 def device_sms(device=None) -> int:
@@ -56,6 +64,7 @@ class SellCSR:
     n_local: int
     n_real: int            # real (non-pad) synapses
     dest: object = None    # torch int32 [n_local]: shards hosting targets of each row
+    partials_global: bool = False
 
     @property
     def n_entries(self) -> int:

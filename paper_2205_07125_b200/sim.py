@@ -250,7 +250,7 @@ class Network:
     # ------------------------------------------------------------ builders
     @classmethod
     def from_graph(cls, graph: NeuronGraph, layout: ShardLayout, *, device=None, inh_every: int = 5,
-                   shards=None, tile_words: int | None = None) -> "Network":
+                   shards=None, tile_words: int | None = None, partials_global: bool = False) -> "Network":
         import torch
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         deg = np.bincount(graph.edge_i, minlength=graph.n_neurons) + np.bincount(graph.edge_j,
@@ -262,11 +262,12 @@ class Network:
         sms = sell.device_sms(dev)
         for h in own:
             n_local = layout.n_local(h)
-            T, TW = _tiles(layout, n_local, sms, tile_words)
+            T, TW, pglob = _tiles(layout, n_local, sms, tile_words, partials_global)
             ptr, meta, syn = host_sell(graph, layout, h, inh_every, T, TW)
             n_real = int(np.count_nonzero((syn >> np.uint32(ID_BITS)) > 0))
             csr = ShardCSR(torch.from_numpy(ptr).to(dev), torch.from_numpy(meta.view(np.int32)).to(dev),
-                           torch.from_numpy(syn.view(np.int32)).to(dev), T, TW, n_local, n_real)
+                           torch.from_numpy(syn.view(np.int32)).to(dev), T, TW, n_local, n_real,
+                           partials_global=pglob)
             csr.dest = _dest_masks(csr, layout, h, dev)
             out[h] = csr
             nsyn += n_real
@@ -304,7 +305,7 @@ class Network:
         sms = sell.device_sms(dev)
         for h in own:
             n_local = layout.n_local(h)
-            T, TW = _tiles(layout, n_local, sms, tile_words)
+            T, TW, pglob = _tiles(layout, n_local, sms, tile_words)
             g = _native.GraphGenC(
                 n_neurons=spec.n_neurons, n_communities=spec.n_communities, shard=h, p_in=spec.p_in,
                 p_out=spec.p_out, intra_lo=spec.intra_p_range[0], intra_hi=spec.intra_p_range[1],
@@ -327,7 +328,7 @@ class Network:
                                              lower.data_ptr(), syn.data_ptr(), st), "graphgen fill")
             n_real = int(counts.sum().item())
             del upper, counts
-            csr = ShardCSR(ptr, meta, syn, T, TW, n_local, n_real)
+            csr = ShardCSR(ptr, meta, syn, T, TW, n_local, n_real, partials_global=pglob)
             csr.dest = _dest_masks(csr, layout, h, dev)
             out[h] = csr
             nsyn += n_real
@@ -355,12 +356,13 @@ class Network:
         return self.layout.members[shard][row], pre, q.astype(np.uint8)
 
 
-def _tiles(layout: ShardLayout, n_local: int, sms: int, tile_words: int | None):
-    """Bitmap tiling: planned from shared memory, or forced (tests) with `tile_words`."""
+def _tiles(layout: ShardLayout, n_local: int, sms: int, tile_words: int | None, partials_global: bool = False):
+    """Bitmap tiling (n_tiles, tile_words, partials_in_global): planned from shared
+    memory, or forced (tests) with `tile_words` / `partials_global`."""
     if tile_words is None:
         return sell.plan_tiles(layout.n_words, n_local, sms)
     tw = max(4, int(tile_words) // 4 * 4)
-    return (layout.n_words + tw - 1) // tw, tw
+    return (layout.n_words + tw - 1) // tw, tw, bool(partials_global)
 
 
 def _as_u16(t32):
@@ -516,7 +518,7 @@ class _ShardState:
             self.push_rowptr, self.push_syn = _push_csr(csr, lay, h, dev)
         self.c = _native.ShardC(
             shard=h, n_shards=n, n_local=n_local, local_base=int(lay.base[h]), n_words=lay.n_words,
-            n_tiles=csr.n_tiles, tile_words=csr.tile_words, pad0=0,
+            n_tiles=csr.n_tiles, tile_words=csr.tile_words, flags=1 if csr.partials_global else 0,
             v=self.v.data_ptr(), i_syn=self.i_syn.data_ptr(), refrac=self.refrac.data_ptr(),
             acc=self.acc.data_ptr(), gid=self.gid.data_ptr(), hop_mask=self.hop_mask.data_ptr(),
             slice_ptr=csr.slice_ptr.data_ptr(), row_meta=csr.row_meta.data_ptr(), syn=csr.syn.data_ptr(),
@@ -544,7 +546,7 @@ def _push_csr(csr: ShardCSR, lay: ShardLayout, h: int, dev):
     n_rows = lay.n_words * 32
     scratch = torch.zeros(8, dtype=torch.int32, device=dev)
     c = _native.ShardC(shard=h, n_shards=lay.n_shards, n_local=lay.n_local(h), local_base=int(lay.base[h]),
-                       n_words=lay.n_words, n_tiles=csr.n_tiles, tile_words=csr.tile_words, pad0=0,
+                       n_words=lay.n_words, n_tiles=csr.n_tiles, tile_words=csr.tile_words, flags=0,
                        slice_ptr=csr.slice_ptr.data_ptr(), row_meta=csr.row_meta.data_ptr(), syn=csr.syn.data_ptr(),
                        bitmap0=scratch.data_ptr(), bitmap1=scratch.data_ptr(), status=scratch.data_ptr(),
                        step=scratch.data_ptr())

@@ -166,15 +166,16 @@ def test_partition_invariance_and_route_independence():
     np.testing.assert_array_equal(rep.raster, base.raster)
 
 
-@pytest.mark.parametrize("tile_words", [64, 100])
-def test_tiled_bitmap_matches_oracle(tile_words):
-    """Force the shared-memory tiling of the spike bitmap (used above ~1.8 M neurons)."""
+@pytest.mark.parametrize("tile_words,glob", [(64, False), (100, False), (96, True)])
+def test_tiled_bitmap_matches_oracle(tile_words, glob):
+    """Force the shared-memory tiling of the spike bitmap (used above ~1.8 M neurons),
+    with the per-row partial sums in shared memory or (huge shards) in global memory."""
     g = cfg1(2)
     pm = nc.partition_greedy(g, 2)
     rt = routes(g, pm, "direct")
     lif = S.LifParams()
     lay = S.ShardLayout.from_assignment(pm.assignment, 2)
-    net = S.Network.from_graph(g, lay, tile_words=tile_words)
+    net = S.Network.from_graph(g, lay, tile_words=tile_words, partials_global=glob)
     assert all(c.n_tiles > 1 for c in net.shards.values())
     for delivery in ("fused", "pull"):
         rep = S.Simulator(net, lif, 2, rt, delivery=delivery, record_raster_steps=60, per_step_counts=True).run(60)

@@ -43,11 +43,13 @@ def test_host_build_round_trip(n_local, n_tiles, tile_words):
 
 
 def test_plan_tiles():
-    assert sell.plan_tiles(1000, 10_000, 148) == (1, 1000)
-    T, tw = sell.plan_tiles(312_500 + 1, 1_250_000, 148)    # 10 M neurons, 1.25 M local
-    assert T > 1 and tw % 4 == 0 and T * tw >= 312_501
+    assert sell.plan_tiles(1000, 10_000, 148) == (1, 1000, False)
+    T, tw, glob = sell.plan_tiles(312_500 + 1, 1_250_000, 148)    # 10 M neurons, 1.25 M local
+    assert T > 1 and tw % 4 == 0 and T * tw >= 312_501 and not glob
     per = (1_250_000 // 32 + 147) // 148
     assert tw * 4 + per * 128 <= sell.SMEM_BYTES - sell.SMEM_RESERVE
+    T, tw, glob = sell.plan_tiles(1_562_500 + 1, 12_500_000, 148)  # 50 M neurons, 12.5 M local
+    assert glob and T * tw >= 1_562_501 and tw * 4 <= sell.SMEM_BYTES - sell.SMEM_RESERVE
 
 
 def test_layout_from_counts_torch_matches_numpy():
