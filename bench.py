@@ -116,8 +116,9 @@ def make_sim(net, lif, args, delivery, world):
     from paper_2205_07125_b200 import sim as S
     if world > 1:
         from paper_2205_07125_b200 import distributed as D
+        cap = args.msg_cap if args.msg_cap is not None else (65536 if args.transport == "nccl" else None)
         return D.DistSimulator(net, lif, args.seed, None, transport=args.transport, delivery=delivery,
-                               msg_cap=args.msg_cap, latency_steps=args.warmup + args.steps, graph_chunk=args.chunk)
+                               msg_cap=cap, latency_steps=args.warmup + args.steps, graph_chunk=args.chunk)
     return S.Simulator(net, lif, args.seed, None, delivery=delivery, graph_chunk=args.chunk)
 
 
@@ -179,18 +180,26 @@ def kernel_ms(sim, which: str, reps: int = 50) -> float:
     stream = torch.cuda.current_stream()
     k0 = torch.cuda.Event(enable_timing=True)
     k1 = torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    k0.record(stream)
-    for _ in range(reps):
-        if which == "fused":
-            L.nc_sim_step_fused(C.byref(st.c), C.byref(sim.c_lif), stream.cuda_stream)
-        elif which == "push":
-            L.nc_sim_deliver_push(C.byref(st.c), sim.c_lif.g_inh, stream.cuda_stream)
-        else:
-            L.nc_sim_lif_update(C.byref(st.c), C.byref(sim.c_lif), stream.cuda_stream)
-    k1.record(stream)
-    torch.cuda.synchronize()
-    return k0.elapsed_time(k1) / reps
+    def run(kind):
+        torch.cuda.synchronize()
+        k0.record(stream)
+        for _ in range(reps):
+            if kind == "fused":
+                L.nc_sim_step_fused(C.byref(st.c), C.byref(sim.c_lif), stream.cuda_stream)
+            elif kind == "push":
+                L.nc_sim_deliver_push(C.byref(st.c), sim.c_lif.g_inh, stream.cuda_stream)
+            elif kind == "lif":  # with the bucket reset a real step does after the exchange
+                L.nc_sim_lif_update(C.byref(st.c), C.byref(sim.c_lif), stream.cuda_stream)
+                L.nc_sim_end_step(C.byref(st.c), stream.cuda_stream)
+            else:
+                L.nc_sim_end_step(C.byref(st.c), stream.cuda_stream)
+        k1.record(stream)
+        torch.cuda.synchronize()
+        return k0.elapsed_time(k1) / reps
+
+    if which == "lif":
+        return max(run("lif") - run("end"), 0.0)
+    return run(which)
 
 
 def lat_summary(lat, lat_max, transport):
@@ -457,7 +466,8 @@ def main() -> int:
     ap.add_argument("--intra-frac", type=float, default=0.9, help="regional: fraction of synapses inside a region")
     ap.add_argument("--delivery", default="fused", choices=["fused", "push"])
     ap.add_argument("--transport", default="p2p", choices=["nccl", "p2p"])
-    ap.add_argument("--msg-cap", type=int, default=65536, help="ids per exchange message (NCCL sends all of it)")
+    ap.add_argument("--msg-cap", type=int, default=None,
+                    help="ids per exchange message (default: exact bound for p2p, 65536 for nccl, which sends all)")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--chunk", type=int, default=100)
     ap.add_argument("--cpu-steps", type=int, default=10)

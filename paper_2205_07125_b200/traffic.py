@@ -120,33 +120,35 @@ def exact_bin_sums(values_dev, keys_dev, n_bins: int, *, pairs=None, stream=None
     return out
 
 
-_DEVICE_GRAPHS: "weakref.WeakKeyDictionary" = None
+_DEVICE_GRAPHS: dict = {}
 
 
 def _device_graph(graph, dev):
     """Edge columns and weights of `graph` on the device, uploaded once per graph object.
 
     Graphs are treated as immutable (SPEC concurrency model); the cache is keyed
-    by the object and the identity of its arrays, so replacing an array re-uploads.
-    Repeated aggregation (cross_traffic, the GA fitness, sweep_noise) then only
-    moves the assignment.
+    by the object (NeuronGraph defines __eq__, so it is not hashable: keyed by
+    id() with a weak reference and a finalizer that evicts the entry) and by the
+    identity of its arrays, so replacing an array re-uploads.  Repeated
+    aggregation (cross_traffic, the GA fitness, sweep_noise) then only moves
+    the assignment.
     """
     import torch
     import weakref
-    global _DEVICE_GRAPHS
-    if _DEVICE_GRAPHS is None:
-        _DEVICE_GRAPHS = weakref.WeakKeyDictionary()
     key = (str(dev), id(graph.weights), id(graph.edge_i), id(graph.edge_j), id(graph.edge_p))
-    hit = _DEVICE_GRAPHS.get(graph)
-    if hit is not None and hit[0] == key:
-        return hit[1]
+    hit = _DEVICE_GRAPHS.get(id(graph))
+    if hit is not None and hit[0]() is graph and hit[1] == key:
+        return hit[2]
     up = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev)  # noqa: E731
     val = (up(graph.weights, np.float64), up(graph.edge_i, np.int64), up(graph.edge_j, np.int64),
            up(graph.edge_p, np.float64))
     try:
-        _DEVICE_GRAPHS[graph] = (key, val)
+        ref = weakref.ref(graph)
     except TypeError:  # not weak-referenceable: no caching
-        pass
+        return val
+    if id(graph) not in _DEVICE_GRAPHS:
+        weakref.finalize(graph, _DEVICE_GRAPHS.pop, id(graph), None)
+    _DEVICE_GRAPHS[id(graph)] = (ref, key, val)
     return val
 
 
