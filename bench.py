@@ -263,7 +263,7 @@ def run_ours(args) -> dict | None:
     if prof.is_file() and main_kernel == "fused" and world == 1:
         traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
     e2e = e2e_measure(sim, net, args) if (world == 1 and rank == 0) else None
-    launches = args.steps * sim.launches_per_step()
+    launches = max(1, int(round(args.steps * sim.launches_per_step())))
     if world > 1:
         sim.close()
     del sim
@@ -271,18 +271,19 @@ def run_ours(args) -> dict | None:
     # ---- the event-driven alternative on the same network (bit-identical results)
     event = None
     if args.with_push and args.delivery == "fused":
-        psim = make_sim(net, lif, args, "push", world)
+        psim = make_sim(net, lif, args, args.event, world)
         pms, pspikes, plat, plat_max = time_steps(psim, args, world, dev)
         push_ms = kernel_ms(psim, "push")
         lif_ms = kernel_ms(psim, "lif")
         fired_syn = pspikes / max(args.steps, 1) * args.degree / max(world, 1)
         push_bytes = fired_syn * 12          # 4 B entry read + 4 B read + 4 B write per reduction
-        event = {"value": round(args.steps / (pms * 1e-3), 2), "ms_per_step": round(pms / args.steps, 5),
+        event = {"engine": args.event, "value": round(args.steps / (pms * 1e-3), 2),
+                 "ms_per_step": round(pms / args.steps, 5),
                  "push_kernel_ms": round(push_ms, 5), "lif_kernel_ms": round(lif_ms, 5),
                  "push_bound": "L2 atomics: %.3g reductions/s" % (fired_syn / (push_ms * 1e-3)),
                  "push_achieved_gbs": round(push_bytes / (push_ms * 1e-3) / 1e9, 1),
                  "exchange_us": lat_summary(plat, plat_max, args.transport),
-                 "gpu_launches": args.steps * psim.launches_per_step()}
+                 "gpu_launches": max(1, int(round(args.steps * psim.launches_per_step())))}
         if world > 1:
             psim.close()
         del psim
@@ -464,7 +465,9 @@ def main() -> int:
     ap.add_argument("--degree", type=float, default=1000.0)
     ap.add_argument("--communities", type=int, default=1, help=">1: regional SBM (config 5 family)")
     ap.add_argument("--intra-frac", type=float, default=0.9, help="regional: fraction of synapses inside a region")
-    ap.add_argument("--delivery", default="fused", choices=["fused", "push"])
+    ap.add_argument("--delivery", default="fused", choices=["fused", "push", "persistent"])
+    ap.add_argument("--event", default="persistent", choices=["push", "persistent"],
+                    help="event-driven variant reported beside the headline")
     ap.add_argument("--transport", default="p2p", choices=["nccl", "p2p"])
     ap.add_argument("--msg-cap", type=int, default=None,
                     help="ids per exchange message (default: exact bound for p2p, 65536 for nccl, which sends all)")

@@ -279,6 +279,15 @@ int nc_xchg_p2p(const nc_xchg_t* X, void* stream);
 /* dst[*step] = %globaltimer (ns) if *step < max_steps: per-step exchange
  * latency stamps, enqueued before and after the exchange. */
 int nc_stamp(unsigned long long* dst, const int32_t* step, int32_t max_steps, void* stream);
+/* Persistent event-driven engine: ONE cooperative kernel runs n_steps steps
+ * (push delivery -> LIF/buckets -> P2P exchange, separated by in-kernel grid
+ * barriers) with no launches or host work between steps.  Requires the push
+ * CSR and acc on the shard; X may be NULL for a single GPU.  gbar: one uint32
+ * of scratch (zeroed by the call).  stamp_ready/stamp_done (nullable) receive
+ * %globaltimer per step (index = step < stamp_cap) around the exchange. */
+int nc_run_persistent(const nc_shard_t* sh, const nc_lif_params_t* p, const nc_xchg_t* X, int32_t n_steps,
+                      int32_t blocks_per_peer, unsigned int* gbar, unsigned long long* stamp_ready,
+                      unsigned long long* stamp_done, int32_t stamp_cap, void* stream);
 /* CUDA IPC windows for the P2P inboxes. */
 int nc_ipc_alloc(size_t bytes, void** ptr_out, void* handle_out /* 64 bytes */);
 int nc_ipc_open(const void* handle /* 64 bytes */, void** ptr_out);

@@ -1,0 +1,127 @@
+// Persistent event-driven engine: one cooperative kernel per GPU runs many
+// steps back to back -- push delivery, LIF + bucket compaction, and the
+// device-initiated P2P spike exchange -- separated by in-kernel grid barriers,
+// so a step costs no kernel launches and no host involvement at all.
+//
+// Per step (same arithmetic as the per-kernel path, hence bit-identical):
+//   1. push_phase   acc += weights of the previous step's spikes (all blocks)
+//   2. grid barrier
+//   3. lif_phase    LIF update, spike bitmap, CTA-aggregated bucket appends
+//   4. grid barrier; stamp "buckets ready"
+//   5. p2p_block    blocks [0, n*B): NVLink stores into the peers' inboxes,
+//                   release/acquire flags, scatter (+ relay phase if two-level)
+//   6. grid barrier; stamp "all inbound spikes in the bitmap"; reset counters
+// The grid is sized from the occupancy calculator and launched cooperatively,
+// so every block is resident and the barriers cannot deadlock; the flag waits
+// of step 5 are bounded by the exchange watchdog (status[1]).
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include "nc_common.h"
+#include "sim_device.cuh"
+#include "xchg_device.cuh"
+
+namespace {
+
+constexpr int kPThreads = ncdev::kLifThreads;
+
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const unsigned int* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Grid barrier on a counter zeroed before the launch: the k-th barrier of the
+// launch completes when the counter reaches k * gridDim.x.
+__device__ void grid_sync(unsigned int* ctr, unsigned int target, int32_t* status) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    const uint64_t t0 = gtimer();
+    while ((int)(ld_acquire_gpu(ctr) - target) < 0) {
+      if (gtimer() - t0 > 20000000000ull) {  // 20 s: report, do not hang
+        atomicExch(status + 1, 1);
+        break;
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kPThreads) k_persistent(const nc_shard_t sh, const nc_lif_params_t p,
+                                                          const nc_xchg_t X, int has_x, int n_steps, int B,
+                                                          unsigned int* gbar, unsigned long long* st_ready,
+                                                          unsigned long long* st_done, int stamp_cap) {
+  __shared__ ncdev::LifSmem S;
+  const int nblk = gridDim.x, bid = blockIdx.x;
+  const int nex = has_x ? X.n * B : 0;
+  const int32_t negg = -p.g_inh;
+  int step = *sh.step;
+  unsigned int k = 0;
+  for (int s = 0; s < n_steps; ++s, ++step) {
+    ncdev::push_phase(sh, negg, step, bid, nblk);
+    grid_sync(gbar, ++k * nblk, sh.status);
+    ncdev::lif_phase(sh, p, step, bid, nblk, S);
+    grid_sync(gbar, ++k * nblk, sh.status);
+    if (bid == 0 && threadIdx.x == 0 && st_ready && step < stamp_cap) st_ready[step] = gtimer();
+    if (bid < nex) ncxchg::p2p_block(X, bid, B, step);
+    grid_sync(gbar, ++k * nblk, sh.status);
+    if (bid == 0) {
+      if (threadIdx.x == 0 && st_done && step < stamp_cap) st_done[step] = gtimer();
+      if ((int)threadIdx.x < sh.n_shards) sh.bucket_count[threadIdx.x] = 0;
+      if (has_x && (int)threadIdx.x < X.n) X.fwd_count[threadIdx.x] = 0;
+      if (threadIdx.x == 0 && sh.fired_count) *sh.fired_count = 0;
+    }
+    // the counters reset above are next touched after the next push barrier
+  }
+  if (bid == 0 && threadIdx.x == 0) *sh.step = step;
+}
+
+int g_grid = 0;
+
+}  // namespace
+
+extern "C" int nc_run_persistent(const nc_shard_t* sh, const nc_lif_params_t* p, const nc_xchg_t* X,
+                                 int32_t n_steps, int32_t blocks_per_peer, unsigned int* gbar,
+                                 unsigned long long* stamp_ready, unsigned long long* stamp_done, int32_t stamp_cap,
+                                 void* stream) {
+  if (!sh || !p || !gbar || n_steps < 0 || !sh->push_rowptr || !sh->push_syn || !sh->acc || !sh->step ||
+      !sh->status) {
+    nc_set_error("nc_run_persistent: shard needs push CSR, acc, step and status buffers");
+    return NC_E_ARG;
+  }
+  if (n_steps == 0) return NC_OK;
+  const int B = blocks_per_peer > 0 ? blocks_per_peer : 1;
+  int dev = 0, sms = 0, occ = 0;
+  NC_CUDA_TRY(cudaGetDevice(&dev));
+  NC_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  NC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_persistent, kPThreads, 0));
+  if (occ < 1) {
+    nc_set_error("nc_run_persistent: kernel does not fit on an SM");
+    return NC_E_CUDA;
+  }
+  int grid = sms * (occ < 2 ? occ : 2);
+  const int nex = X ? X->n * B : 0;
+  if (grid < nex) {
+    nc_set_error("nc_run_persistent: %d exchange blocks exceed the resident grid (%d)", nex, grid);
+    return NC_E_ARG;
+  }
+  g_grid = grid;
+  nc_xchg_t xz{};
+  const nc_xchg_t& xr = X ? *X : xz;
+  int has_x = X ? 1 : 0;
+  NC_CUDA_TRY(cudaMemsetAsync(gbar, 0, sizeof(unsigned int), (cudaStream_t)stream));
+  void* args[] = {(void*)sh, (void*)p, (void*)&xr, &has_x, &n_steps, (void*)&B, &gbar, &stamp_ready, &stamp_done,
+                  &stamp_cap};
+  NC_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_persistent, dim3(grid), dim3(kPThreads), args, 0,
+                                          (cudaStream_t)stream));
+  return NC_OK;
+}

@@ -1,0 +1,319 @@
+// Device building blocks of the per-step loop, shared by the per-kernel step
+// functions (sim_kernels.cu) and the persistent engine (persistent.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include "nc_common.h"
+#include "philox.cuh"
+
+namespace ncdev {
+
+constexpr int kUnroll = 8;        // 16-byte slots in flight per lane
+constexpr uint32_t kFull = 0xffffffffu;
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ uint4 ld_keep(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+
+// Weight units of one packed entry (q << 26 | pre) if its pre fired, else 0.
+// The funnel shift rotates the bitmap word by the low 5 bits of the entry
+// (= pre & 31), so bit 0 is the pre's spike bit: 5 integer ops per synapse.
+__device__ __forceinline__ int32_t entry_term(uint32_t e, const uint32_t* __restrict__ bm) {
+  const uint32_t word = bm[(e & 0x03FFFFFFu) >> 5];
+  const uint32_t rot = __funnelshift_r(word, word, e);
+  return (rot & 1u) ? (int32_t)(e >> 26) : 0;
+}
+
+__device__ __forceinline__ int32_t quad_term(uint4 e, const uint32_t* __restrict__ bm) {
+  return entry_term(e.x, bm) + entry_term(e.y, bm) + entry_term(e.z, bm) + entry_term(e.w, bm);
+}
+
+// One lane's row in one SELL-32 block: block slots [0, len) at blk + u*32 + lane;
+// this row uses meta >> 16 of them, the first (meta & 0xFFFF) excitatory.
+// Slots past the row's own length are not loaded (`pad` stands in: the block's
+// pad entry, first id of its tile with q = 0, so its lookup stays in the
+// staged tile and adds nothing).  Returns sum_E - g * sum_I (weight units).
+__device__ __forceinline__ int32_t sell_row_sum(const uint4* __restrict__ blk, int len, uint32_t meta,
+                                                const uint32_t* __restrict__ bm, int32_t g_inh, int lane,
+                                                uint32_t pad) {
+  const int emid = (int)(meta & 0xFFFFu);
+  const int mine = (int)(meta >> 16);
+  int32_t se = 0, si = 0;
+  const uint4* p = blk + lane;
+  const uint4 padv = make_uint4(pad, pad, pad, pad);
+  for (int u0 = 0; u0 < len; u0 += kUnroll) {
+    uint4 e[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) e[u] = (u0 + u < mine) ? ld_stream(p + (u0 + u) * 32) : padv;
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int32_t t = quad_term(e[u], bm);
+      if (u0 + u < emid) se += t;
+      else si += t;
+    }
+  }
+  return se - g_inh * si;
+}
+
+// Exact LIF step; returns true if the neuron fired.  Operation order is the
+// contract shared with oracle/sim_oracle.c.
+__device__ __forceinline__ bool lif_step(float& v, float& isyn, uint8_t& ref, int32_t acc,
+                                         uint32_t gid, uint32_t step, const nc_lif_params_t& p) {
+  uint32_t extc = 0;
+  if (p.ext_lanes > 0) {
+    nc_u32x4 c = {gid, step, NC_TAG_DRIVE, 0u};
+    nc_u32x4 r = nc_philox4x32_10(c, (uint32_t)p.seed, (uint32_t)(p.seed >> 32));
+    extc = (r.x < p.ext_threshold);
+    if (p.ext_lanes > 1) extc += (r.y < p.ext_threshold);
+    if (p.ext_lanes > 2) extc += (r.z < p.ext_threshold);
+    if (p.ext_lanes > 3) extc += (r.w < p.ext_threshold);
+  }
+  const float syn = __int2float_rn(acc);
+  const float ext = __uint2float_rn(extc);
+  const float i1 = __fadd_rn(__fmul_rn(isyn, p.alpha_i), __fmul_rn(syn, p.w_unit));
+  const float inew = __fadd_rn(i1, __fmul_rn(ext, p.w_ext));
+  isyn = inew;
+  if (ref > 0) {
+    ref = (uint8_t)(ref - 1);
+    v = p.v_reset;
+    return false;
+  }
+  const float d = __fsub_rn(v, p.v_rest);
+  const float vn = __fadd_rn(__fadd_rn(p.v_rest, __fmul_rn(d, p.alpha_v)), __fmul_rn(inew, p.beta));
+  if (vn >= p.v_th) {
+    v = p.v_reset;
+    ref = (uint8_t)p.t_ref;
+    return true;
+  }
+  v = vn;
+  return false;
+}
+
+// Warp-aggregated append of the ids of lanes in `m` (whole warp calls).
+__device__ __forceinline__ void warp_append(uint32_t* ids, int32_t* count, int64_t cap, uint32_t m,
+                                            uint32_t my_id, int lane, int32_t* status) {
+  if (m == 0) return;
+  const int leader = __ffs(m) - 1;
+  int32_t base = 0;
+  if (lane == leader) base = atomicAdd(count, __popc(m));
+  base = __shfl_sync(kFull, base, leader);
+  if ((m >> lane) & 1u) {
+    const int64_t pos = (int64_t)base + __popc(m & ((1u << lane) - 1u));
+    if (pos < cap) ids[pos] = my_id;
+    else atomicExch(status, 1);
+  }
+}
+
+// K2: bitmap word, raster, fired list and next-hop buckets for one 32-neuron tile.
+__device__ __forceinline__ uint32_t emit_spikes(const nc_shard_t& sh, uint32_t* cur, int tile, int row,
+                                                bool fired, int lane, int step) {
+  const uint32_t fmask = __ballot_sync(kFull, fired);
+  if (lane == 0) {
+    cur[(sh.local_base >> 5) + tile] = fmask;
+    if (sh.raster != nullptr && step < sh.record_steps)
+      sh.raster[(int64_t)step * sh.local_words + tile] = fmask;
+  }
+  if (fmask == 0) return 0;
+  const uint32_t my_id = (uint32_t)(sh.local_base + row);
+  if (sh.fired_ids != nullptr)
+    warp_append(sh.fired_ids, sh.fired_count, sh.n_local, fmask, my_id, lane, sh.status);
+  if (sh.n_shards > 1) {
+    const uint32_t hm = fired ? (uint32_t)sh.hop_mask[row] : 0u;
+    uint32_t pending = __reduce_or_sync(kFull, hm);
+    while (pending) {
+      const int h = __ffs(pending) - 1;
+      pending &= pending - 1;
+      const uint32_t m = __ballot_sync(kFull, (hm >> h) & 1u);
+      warp_append(sh.bucket_ids + (int64_t)h * sh.bucket_cap, sh.bucket_count + h, sh.bucket_cap, m,
+                  my_id, lane, sh.status);
+    }
+  }
+  return fmask;
+}
+
+// Zero the words of `cur` outside this shard's local range (the exchange ORs
+// remote spikes into them after the step kernel).
+__device__ __forceinline__ void clear_remote(const nc_shard_t& sh, uint32_t* cur, int bid, int nblk) {
+  const int lw0 = sh.local_base >> 5;
+  const int lw1 = lw0 + sh.local_words;
+  for (int w = bid * blockDim.x + threadIdx.x; w < sh.n_words; w += nblk * blockDim.x)
+    if (w < lw0 || w >= lw1) cur[w] = 0u;
+}
+
+__device__ __forceinline__ void add_spike_total(const nc_shard_t& sh, uint32_t local_count,
+                                                unsigned int* block_count) {
+  if (local_count) atomicAdd(block_count, local_count);
+  __syncthreads();
+  if (threadIdx.x == 0 && *block_count && sh.spike_total)
+    atomicAdd(sh.spike_total, (unsigned long long)*block_count);
+}
+
+// LIF + spike emission for the 32 rows of one slice (lane = row).
+__device__ __forceinline__ uint32_t update_slice(const nc_shard_t& sh, const nc_lif_params_t& p, uint32_t* cur,
+                                                 int slice, int lane, int32_t acc, int step) {
+  const int row = (slice << 5) + lane;
+  bool fired = false;
+  if (row < sh.n_local) {
+    float v = sh.v[row];
+    float isyn = sh.i_syn[row];
+    uint8_t ref = sh.refrac[row];
+    fired = lif_step(v, isyn, ref, acc, sh.gid[row], (uint32_t)step, p);
+    sh.v[row] = v;
+    sh.i_syn[row] = isyn;
+    sh.refrac[row] = ref;
+  }
+  return emit_spikes(sh, cur, slice, row, fired, lane, step);
+}
+
+// K1+K2 alone (consumes and zeroes acc).  Every CTA owns a contiguous range of
+// 32-neuron tiles and appends to the buckets with ONE global atomic per bucket
+// for the whole step: pass A runs the LIF update, stores each tile's spike mask
+// in shared memory and counts per warp and bucket; the CTA then claims its
+// ranges; pass B recomputes the per-bucket ballots from the stored masks and the
+// static hop masks and writes the ids.  (Same-address atomics serialise in L2:
+// one per warp per bucket cost more than the update itself.)
+constexpr int kLifThreads = 256;
+constexpr int kLifWarps = kLifThreads / 32;
+constexpr int kLifMaxTiles = 2048;   // tiles per CTA (fmask storage: 8 KB)
+
+struct LifSmem {
+  unsigned int block_count;
+  uint32_t fmask_s[kLifMaxTiles];
+  int warp_cnt[kLifWarps][NC_MAX_SHARDS + 1];
+  int cta_base[NC_MAX_SHARDS + 1];
+};
+
+// One LIF phase of step `step` for block `bid` of `nblk` (blockDim = kLifThreads).
+static __device__ void lif_phase(const nc_shard_t& sh, const nc_lif_params_t& p, int step, int bid, int nblk,
+                          LifSmem& S) {
+  unsigned int& block_count = S.block_count;
+  uint32_t* fmask_s = S.fmask_s;
+  auto& warp_cnt = S.warp_cnt;
+  int* cta_base = S.cta_base;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int nq = sh.n_shards > 1 ? sh.n_shards : 0;      // buckets in use
+  const int nb = nq + (sh.fired_ids ? 1 : 0);            // + the fired list (slot nq)
+  if (threadIdx.x == 0) block_count = 0;
+  for (int k = threadIdx.x; k < kLifWarps * (NC_MAX_SHARDS + 1); k += blockDim.x)
+    (&warp_cnt[0][0])[k] = 0;
+  __syncthreads();
+  uint32_t* cur = (step & 1) ? sh.bitmap1 : sh.bitmap0;
+  clear_remote(sh, cur, bid, nblk);
+  const int ntiles = (sh.n_local + 31) >> 5;
+  const int per = (ntiles + nblk - 1) / nblk;
+  const int t0 = bid * per, t1 = min(ntiles, t0 + per);
+  uint32_t my_spikes = 0;
+  // ---- pass A: update, spike masks, per-warp bucket counts
+  for (int tile = t0 + warp; tile < t1; tile += kLifWarps) {
+    const int row = (tile << 5) + lane;
+    bool fired = false;
+    if (row < sh.n_local) {
+      float v = sh.v[row];
+      float isyn = sh.i_syn[row];
+      uint8_t ref = sh.refrac[row];
+      const int32_t a = sh.acc[row];
+      sh.acc[row] = 0;
+      fired = lif_step(v, isyn, ref, a, sh.gid[row], (uint32_t)step, p);
+      sh.v[row] = v;
+      sh.i_syn[row] = isyn;
+      sh.refrac[row] = ref;
+    }
+    const uint32_t fmask = __ballot_sync(kFull, fired);
+    if (lane == 0) {
+      cur[(sh.local_base >> 5) + tile] = fmask;
+      if (sh.raster != nullptr && step < sh.record_steps) sh.raster[(int64_t)step * sh.local_words + tile] = fmask;
+      fmask_s[tile - t0] = fmask;
+      my_spikes += __popc(fmask);
+    }
+    if (nb && fmask) {
+      const uint32_t hm = fired ? (uint32_t)sh.hop_mask[row] : 0u;
+      for (int h = 0; h < nb; ++h) {
+        const uint32_t m = (h < nq) ? __ballot_sync(kFull, (hm >> h) & 1u) : fmask;
+        if (lane == 0) warp_cnt[warp][h] += __popc(m);
+      }
+    }
+  }
+  __syncthreads();
+  // ---- one global atomic per bucket per CTA; warp prefix inside the CTA
+  if ((int)threadIdx.x < nb) {
+    const int h = threadIdx.x;
+    int total = 0;
+    for (int w = 0; w < kLifWarps; ++w) {
+      const int c = warp_cnt[w][h];
+      warp_cnt[w][h] = total;  // exclusive prefix = the warp's base
+      total += c;
+    }
+    int32_t* cnt = h < nq ? sh.bucket_count + h : sh.fired_count;
+    cta_base[h] = total ? atomicAdd(cnt, total) : 0;
+  }
+  __syncthreads();
+  // ---- pass B: write ids
+  if (nb) {
+    for (int tile = t0 + warp; tile < t1; tile += kLifWarps) {
+      const uint32_t fmask = fmask_s[tile - t0];
+      if (!fmask) continue;
+      const int row = (tile << 5) + lane;
+      const bool fired = (fmask >> lane) & 1u;
+      const uint32_t hm = fired ? (uint32_t)sh.hop_mask[row] : 0u;
+      const uint32_t my_id = (uint32_t)(sh.local_base + row);
+      for (int h = 0; h < nb; ++h) {
+        const uint32_t m = (h < nq) ? __ballot_sync(kFull, (hm >> h) & 1u) : fmask;
+        if ((m >> lane) & 1u) {
+          const int64_t pos = (int64_t)cta_base[h] + warp_cnt[warp][h] + __popc(m & ((1u << lane) - 1u));
+          const int64_t cap = h < nq ? sh.bucket_cap : sh.n_local;
+          if (pos < cap) (h < nq ? sh.bucket_ids + (int64_t)h * sh.bucket_cap : sh.fired_ids)[pos] = my_id;
+          else atomicExch(sh.status, 1);
+        }
+        __syncwarp();
+        if (lane == 0) warp_cnt[warp][h] += __popc(m);
+        __syncwarp();
+      }
+    }
+  }
+  add_spike_total(sh, my_spikes, &block_count);
+}
+
+// Event-driven delivery: scan the previous step's spike bitmap one warp per
+// word; for every set bit the warp walks that pre neuron's push-CSR row and
+// adds the integer weights into acc with red.global.add (exact, so order free).
+static __device__ void push_phase(const nc_shard_t& sh, int32_t negg, int step, int bid, int nblk) {
+  const uint32_t* prev = ((step - 1) & 1) ? sh.bitmap1 : sh.bitmap0;
+  const int lane = threadIdx.x & 31;
+  const int64_t wpb = blockDim.x >> 5;
+  for (int64_t w = bid * wpb + (threadIdx.x >> 5); w < sh.n_words; w += nblk * wpb) {
+    uint32_t bits = prev[w];  // same value in every lane (broadcast load)
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      const int64_t pre = (w << 5) + b;
+      const int64_t beg = sh.push_rowptr[pre], end = sh.push_rowptr[pre + 1];
+      // 4 independent loads in flight per lane, then 4 fire-and-forget reductions
+      for (int64_t e0 = beg + lane; e0 < end; e0 += 128) {
+        uint32_t x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) x[u] = (e0 + 32 * u < end) ? __ldg(sh.push_syn + e0 + 32 * u) : 0u;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (e0 + 32 * u < end) {
+            const int32_t q = (int32_t)((x[u] >> 26) & 31u) + 1;
+            atomicAdd(sh.acc + (x[u] & 0x03FFFFFFu), (x[u] >> 31) ? q * negg : q);
+          }
+        }
+      }
+    }
+  }
+}
+
+
+}  // namespace ncdev

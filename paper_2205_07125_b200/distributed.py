@@ -84,8 +84,10 @@ class DistSimulator:
         import torch.distributed as dist
         if transport not in ("p2p", "nccl"):
             raise ValueError(f"transport must be 'p2p' or 'nccl', got {transport!r}")
-        if delivery not in ("fused", "push", "pull"):
-            raise ValueError(f"delivery must be 'fused', 'pull' or 'push', got {delivery!r}")
+        if delivery not in ("fused", "push", "pull", "persistent"):
+            raise ValueError(f"delivery must be 'fused', 'pull', 'push' or 'persistent', got {delivery!r}")
+        if delivery == "persistent" and transport != "p2p":
+            raise ValueError("the persistent engine exchanges spikes with device-initiated P2P stores (transport='p2p')")
         self.rank = dist.get_rank()
         self.world = dist.get_world_size()
         lay = net.layout
@@ -120,7 +122,8 @@ class DistSimulator:
         self.cap = max(cap, 1)
         del probe
         self.state = _ShardState(net, self.rank, self.plan, record_steps=record_raster_steps,
-                                 push=(delivery == "push"), bucket_cap=None, bucket_stride=self.cap)
+                                 push=(delivery in ("push", "persistent")), bucket_cap=None,
+                                 bucket_stride=self.cap)
         self.states = [self.state]
         self.record_steps = int(record_raster_steps)
         self.dest_global = gather_dest(net, self.rank, self.world, dev)
@@ -134,6 +137,7 @@ class DistSimulator:
         self.recv2_ids = torch.zeros(n * cap if (transport == "nccl" and self.plan.two_level) else 1, **i32)
         self.lat_stamps = torch.zeros((2, max(latency_steps, 1)), dtype=torch.int64, device=dev)
         self.sync_words = torch.zeros(8, **i32)
+        self._gbar = torch.zeros(1, **i32)
         self.hop_ids = None
         self.deliv_ids = None
 
@@ -295,7 +299,9 @@ class DistSimulator:
         _native.check(L.nc_stamp(self.lat_stamps[1].data_ptr(), s.step.data_ptr(), self.latency_steps, st), "stamp")
         _native.check(L.nc_sim_end_step(C.byref(s.c), st), "end step")
 
-    def launches_per_step(self) -> int:
+    def launches_per_step(self) -> float:
+        if self.delivery == "persistent":
+            return 0.0  # one cooperative launch per advance() call
         step = 2 if self.delivery == "fused" else 3
         if self.transport == "p2p":
             ex = 1 + (1 if self.plan.two_level else 0)
@@ -310,6 +316,14 @@ class DistSimulator:
 
     def advance(self, steps: int):
         import torch
+        if self.delivery == "persistent":
+            s = self.state
+            st = _native.stream_handle(self.dev)
+            _native.check(self.lib.nc_run_persistent(C.byref(s.c), C.byref(self.c_lif), C.byref(self.X), int(steps),
+                                                     self.blocks_per_peer, self._gbar.data_ptr(),
+                                                     self.lat_stamps[0].data_ptr(), self.lat_stamps[1].data_ptr(),
+                                                     self.latency_steps, st), "persistent engine")
+            return
         if not self.use_graph:
             self.advance_eager(steps)
             return

@@ -570,8 +570,10 @@ class Simulator:
                  *, delivery: str = "fused", record_raster_steps: int = 0, per_step_counts: bool = False,
                  bucket_cap: int | None = None, use_graph: bool = True, graph_chunk: int = 64):
         import torch
-        if delivery not in ("fused", "push", "pull"):
-            raise ValueError(f"delivery must be 'fused', 'pull' or 'push', got {delivery!r}")
+        if delivery not in ("fused", "push", "pull", "persistent"):
+            raise ValueError(f"delivery must be 'fused', 'pull', 'push' or 'persistent', got {delivery!r}")
+        if delivery == "persistent" and net.layout.n_shards != 1:
+            raise ValueError("the persistent engine runs one shard per GPU; use distributed.DistSimulator")
         if set(net.shards) != set(range(net.layout.n_shards)):
             raise ValueError("the single-process simulator needs every shard of the layout")
         self.net = net
@@ -587,7 +589,7 @@ class Simulator:
         self.graph_chunk = graph_chunk
         self.record_steps = int(record_raster_steps)
         self.states = [
-            _ShardState(net, h, self.plan, record_steps=self.record_steps, push=(delivery == "push"),
+            _ShardState(net, h, self.plan, record_steps=self.record_steps, push=(delivery in ("push", "persistent")),
                         bucket_cap=bucket_cap)
             for h in range(self.n)
         ]
@@ -600,6 +602,7 @@ class Simulator:
         self.fwd_count = torch.zeros(self.n * self.n, dtype=torch.int32, device=dev)
         self.shard_array = (_native.ShardC * self.n)(*[s.c for s in self.states])
         self._counter_steps = 0
+        self._gbar = torch.zeros(1, dtype=torch.int32, device=dev)
         self.hop_ids = None
         self.deliv_ids = None
         self._graph = None
@@ -645,7 +648,9 @@ class Simulator:
         for s in self.states:
             self._check(L.nc_sim_end_step(C.byref(s.c), st), "end step")
 
-    def launches_per_step(self) -> int:
+    def launches_per_step(self) -> float:
+        if self.delivery == "persistent":
+            return 0.0  # one launch per advance() call, whatever the step count
         per_shard = 2 if self.delivery == "fused" else 3
         ex = 0
         if self.n > 1:
@@ -661,6 +666,12 @@ class Simulator:
     def advance(self, steps: int):
         """Enqueue `steps` steps on the current stream (graph-replayed in chunks)."""
         import torch
+        if self.delivery == "persistent":
+            s = self.states[0]
+            st = _native.stream_handle(self.net.device)
+            _native.check(self.lib.nc_run_persistent(C.byref(s.c), C.byref(self.c_lif), None, int(steps), 1,
+                                                     self._gbar.data_ptr(), None, None, 0, st), "persistent engine")
+            return
         if not self.use_graph:
             self.advance_eager(steps)
             return

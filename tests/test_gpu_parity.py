@@ -149,6 +149,16 @@ def test_delivery_variants_identical(delivery):
     np.testing.assert_array_equal(a.hop_ids, b.hop_ids)
 
 
+def test_persistent_engine_matches_oracle():
+    """One cooperative kernel for all steps (push delivery + LIF, grid barriers)."""
+    g = cfg1(1)
+    pm = nc.partition_greedy(g, 1)
+    lif = S.LifParams()
+    rep = nc.simulate(g, pm, None, 100, lif, seed=1, delivery="persistent")
+    ref = oracle_run(g, pm, None, lif, 1, 100)
+    assert_same(rep, ref)
+
+
 def test_partition_invariance_and_route_independence():
     """Rasters do not depend on how many GPUs or which routes carry the spikes."""
     g = cfg1(3)

@@ -52,9 +52,11 @@ def main() -> int:
             rp, col, q = c_oracle.symmetric_csr(g.n_neurons, g.edge_i, g.edge_j, S.q_from_p(g.edge_p))
             ref = c_oracle.simulate_csr(rp, col, q, pm.assignment, world, rt.next_hop_matrix(), lif.constants(1),
                                         steps, threads=8)
-        for transport in os.environ.get("NC_TRANSPORTS", "p2p,nccl").split(","):
-            sim = DistSimulator(net, lif, 1, rt, transport=transport, record_raster_steps=steps,
-                                per_step_counts=True)
+        runs = [(t, "fused") for t in os.environ.get("NC_TRANSPORTS", "p2p,nccl").split(",")]
+        runs.append(("p2p", "persistent"))
+        for transport, delivery in runs:
+            sim = DistSimulator(net, lif, 1, rt, transport=transport, delivery=delivery,
+                                record_raster_steps=steps, per_step_counts=True)
             rep = sim.run(steps)
             sim.close()
             if rank == 0:
@@ -66,7 +68,7 @@ def main() -> int:
                 }
                 good = all(checks.values())
                 ok &= good
-                print(f"[{world} ranks] {mode:9s} {transport:4s} spikes={rep.spikes} "
+                print(f"[{world} ranks] {mode:9s} {transport:4s} {delivery:10s} spikes={rep.spikes} "
                       f"{rep.steps_per_s:.0f} steps/s exchange p50={rep.extra['exchange_p50_us']:.1f}us "
                       f"p99={rep.extra['exchange_p99_us']:.1f}us {'OK' if good else 'MISMATCH ' + str(checks)}",
                       flush=True)
