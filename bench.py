@@ -257,6 +257,10 @@ def run_ours(args) -> dict | None:
     neuron_bytes = n_local * (4 * csr.n_tiles + 8 + 8 + 2 + 4) + csr.slice_ptr.numel() * 8 + 2 * (lay.n_words * 4)
     alg_bytes = syn_bytes + neuron_bytes
     peaks = load_peaks()
+    if main_kernel != "fused":
+        # event-driven headline: the push kernel moves 12 B per delivered synapse
+        fired_syn = spikes / max(args.steps, 1) * args.degree / max(world, 1)
+        alg_bytes = fired_syn * 12
     achieved = alg_bytes / (kms * 1e-3) / 1e9
     traffic = None
     prof = ROOT / "profiles" / "ncu_step_fused.json"

@@ -108,7 +108,9 @@ extern "C" int nc_run_persistent(const nc_shard_t* sh, const nc_lif_params_t* p,
     nc_set_error("nc_run_persistent: kernel does not fit on an SM");
     return NC_E_CUDA;
   }
-  int grid = sms * (occ < 2 ? occ : 2);
+  // every resident slot: the push and LIF phases are latency bound and want
+  // as many warps in flight as the SM holds
+  int grid = sms * (occ < 8 ? occ : 8);
   const int nex = X ? X->n * B : 0;
   if (grid < nex) {
     nc_set_error("nc_run_persistent: %d exchange blocks exceed the resident grid (%d)", nex, grid);
