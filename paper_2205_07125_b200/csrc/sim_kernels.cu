@@ -68,44 +68,53 @@ k_step_fused(const nc_shard_t sh, const nc_lif_params_t p) {
     }
   } else {
     const int T = sh.n_tiles, TW = sh.tile_words;
-    const int per = (n_slices + gridDim.x - 1) / gridDim.x;
-    const int s0 = blockIdx.x * per;
-    const int s1 = min(n_slices, s0 + per);
-    // partial sums per row: shared memory behind the tile, or the acc array when
-    // the CTA's rows do not fit next to a useful tile (flags bit 0)
-    int32_t* part = (sh.flags & 1) ? sh.acc + (int64_t)s0 * 32 : reinterpret_cast<int32_t*>(sbm + TW);
-    const int n_part = (sh.flags & 1) ? min(per * 32, sh.n_local - s0 * 32) : per * 32;
-    for (int k = threadIdx.x; k < n_part; k += blockDim.x) part[k] = 0;
+    // CTA c owns slices c, c+G, c+2G, ...: rows are ordered by degree inside the
+    // shard, so interleaving gives every CTA the same mix of long and short rows
+    const int G = gridDim.x, c = blockIdx.x;
+    const int cnt = c < n_slices ? (n_slices - c + G - 1) / G : 0;
+    // partial sums per owned row: shared memory behind the tile, or the acc array
+    // (indexed by row) when the CTA's rows do not fit next to a useful tile (flags bit 0)
+    const bool pglob = (sh.flags & 1) != 0;
+    int32_t* part = pglob ? sh.acc : reinterpret_cast<int32_t*>(sbm + TW);
+    for (int k = threadIdx.x; k < cnt * 32; k += blockDim.x) {
+      const int row = ((c + (k >> 5) * G) << 5) + (k & 31);
+      if (!pglob) part[k] = 0;
+      else if (row < sh.n_local) part[row] = 0;
+    }
     __shared__ int next_slice[2];
-    if (threadIdx.x == 0) next_slice[0] = next_slice[1] = s0;
+    if (threadIdx.x == 0) next_slice[0] = next_slice[1] = 0;
     for (int t = 0; t < T; ++t) {
       __syncthreads();
       const int w0 = t * TW;
       const int nw = min(TW, sh.n_words - w0);
       const uint4* src = reinterpret_cast<const uint4*>(prev + w0);
       for (int k = threadIdx.x; k < (nw + 3) >> 2; k += blockDim.x) smem4[k] = ld_keep(src + k);
-      if (threadIdx.x == 0) next_slice[(t + 1) & 1] = s0;  // counter of the next tile
+      if (threadIdx.x == 0) next_slice[(t + 1) & 1] = 0;  // counter of the next tile
       __syncthreads();
       // tile-relative view: bm[global word] hits the staged copy
       const uint32_t* bm = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(sbm) -
                                                              (uintptr_t)w0 * 4u);
       // warps claim slices dynamically so the per-tile barrier waits for at most one slice
       for (;;) {
-        int slice = 0;
-        if (lane == 0) slice = atomicAdd(&next_slice[t & 1], 1);
-        slice = __shfl_sync(kFull, slice, 0);
-        if (slice >= s1) break;
+        int j = 0;
+        if (lane == 0) j = atomicAdd(&next_slice[t & 1], 1);
+        j = __shfl_sync(kFull, j, 0);
+        if (j >= cnt) break;
+        const int slice = c + j * G;
         const int row = (slice << 5) + lane;
         const int64_t b0 = sh.slice_ptr[(int64_t)slice * T + t];
         const int len = (int)((sh.slice_ptr[(int64_t)slice * T + t + 1] - b0) >> 5);
         const uint32_t meta = row < sh.n_local ? sh.row_meta[(int64_t)row * T + t] : 0u;
-        part[(slice - s0) * 32 + lane] += sell_row_sum(syn4 + b0, len, meta, bm, g_inh, lane, (uint32_t)w0 * 32u);
+        const int32_t sum = sell_row_sum(syn4 + b0, len, meta, bm, g_inh, lane, (uint32_t)w0 * 32u);
+        if (!pglob) part[j * 32 + lane] += sum;
+        else if (row < sh.n_local) part[row] += sum;
       }
     }
     __syncthreads();
-    for (int slice = s0 + warp; slice < s1; slice += wpb) {
+    for (int j = warp; j < cnt; j += wpb) {
+      const int slice = c + j * G;
       const int row = (slice << 5) + lane;
-      const int32_t acc = part[(slice - s0) * 32 + lane];
+      const int32_t acc = pglob ? (row < sh.n_local ? part[row] : 0) : part[j * 32 + lane];
       if (kLif) {
         const uint32_t fm = update_slice(sh, p, cur, slice, lane, acc, step);
         if (lane == 0) my_spikes += __popc(fm);
