@@ -288,6 +288,10 @@ int nc_stamp(unsigned long long* dst, const int32_t* step, int32_t max_steps, vo
 int nc_run_persistent(const nc_shard_t* sh, const nc_lif_params_t* p, const nc_xchg_t* X, int32_t n_steps,
                       int32_t blocks_per_peer, unsigned int* gbar, unsigned long long* stamp_ready,
                       unsigned long long* stamp_done, int32_t stamp_cap, void* stream);
+/* Diagnostics for nc_run_persistent: when dst (device uint64[64][4]) is set,
+ * the next launches record (start, after push, after LIF, after exchange)
+ * %globaltimer stamps of their first 64 steps.  NULL switches it off. */
+int nc_persistent_phase_stamps(unsigned long long* dst);
 /* CUDA IPC windows for the P2P inboxes. */
 int nc_ipc_alloc(size_t bytes, void** ptr_out, void* handle_out /* 64 bytes */);
 int nc_ipc_open(const void* handle /* 64 bytes */, void** ptr_out);

@@ -123,6 +123,7 @@ _SIGS = {
     "nc_ipc_close": (c_int32, [c_void_p]),
     "nc_free": (c_int32, [c_void_p]),
     "nc_stamp": (c_int32, [c_void_p, c_void_p, c_int32, c_void_p]),
+    "nc_persistent_phase_stamps": (c_int32, [c_void_p]),
     "nc_run_persistent": (c_int32, [C.POINTER(ShardC), C.POINTER(LifParamsC), C.POINTER(XchgC), c_int32, c_int32,
                                     c_void_p, c_void_p, c_void_p, c_int32, c_void_p]),
 }

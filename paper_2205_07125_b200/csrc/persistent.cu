@@ -49,21 +49,27 @@ __device__ __forceinline__ void grid_sync(unsigned int*, unsigned int, int32_t*)
 __global__ void __launch_bounds__(kPThreads) k_persistent(const nc_shard_t sh, const nc_lif_params_t p,
                                                           const nc_xchg_t X, int has_x, int n_steps, int B,
                                                           unsigned int* gbar, unsigned long long* st_ready,
-                                                          unsigned long long* st_done, int stamp_cap) {
+                                                          unsigned long long* st_done, int stamp_cap,
+                                                          unsigned long long* phase_st) {
   __shared__ ncdev::LifSmem S;
   const int nblk = gridDim.x, bid = blockIdx.x;
   const int nex = has_x ? X.n * B : 0;
   const int32_t negg = -p.g_inh;
   int step = *sh.step;
   unsigned int k = 0;
+  const bool ph = phase_st && bid == 0 && threadIdx.x == 0;
   for (int s = 0; s < n_steps; ++s, ++step) {
+    if (ph && s < 64) phase_st[s * 4 + 0] = gtimer();
     ncdev::push_phase(sh, negg, step, bid, nblk);
     grid_sync(gbar, ++k * nblk, sh.status);
+    if (ph && s < 64) phase_st[s * 4 + 1] = gtimer();
     ncdev::lif_phase(sh, p, step, bid, nblk, S);
     grid_sync(gbar, ++k * nblk, sh.status);
+    if (ph && s < 64) phase_st[s * 4 + 2] = gtimer();
     if (bid == 0 && threadIdx.x == 0 && st_ready && step < stamp_cap) st_ready[step] = gtimer();
     if (bid < nex) ncxchg::p2p_block(X, bid, B, step);
     grid_sync(gbar, ++k * nblk, sh.status);
+    if (ph && s < 64) phase_st[s * 4 + 3] = gtimer();
     if (bid == 0) {
       if (threadIdx.x == 0 && st_done && step < stamp_cap) st_done[step] = gtimer();
       if ((int)threadIdx.x < sh.n_shards) sh.bucket_count[threadIdx.x] = 0;
@@ -78,6 +84,15 @@ __global__ void __launch_bounds__(kPThreads) k_persistent(const nc_shard_t sh, c
 int g_grid = 0;
 
 }  // namespace
+
+static unsigned long long* g_phase_stamps = nullptr;
+
+// Diagnostics: record (start, after push, after LIF, after exchange) globaltimer
+// stamps of the first 64 steps of the next persistent launches into dst[64][4].
+extern "C" int nc_persistent_phase_stamps(unsigned long long* dst) {
+  g_phase_stamps = dst;
+  return NC_OK;
+}
 
 extern "C" int nc_run_persistent(const nc_shard_t* sh, const nc_lif_params_t* p, const nc_xchg_t* X,
                                  int32_t n_steps, int32_t blocks_per_peer, unsigned int* gbar,
@@ -107,12 +122,14 @@ extern "C" int nc_run_persistent(const nc_shard_t* sh, const nc_lif_params_t* p,
     return NC_E_ARG;
   }
   g_grid = grid;
+  (void)g_grid;
   nc_xchg_t xz{};
   const nc_xchg_t& xr = X ? *X : xz;
   int has_x = X ? 1 : 0;
   NC_CUDA_TRY(cudaMemsetAsync(gbar, 0, sizeof(unsigned int), (cudaStream_t)stream));
+  unsigned long long* phase = g_phase_stamps;
   void* args[] = {(void*)sh, (void*)p, (void*)&xr, &has_x, &n_steps, (void*)&B, &gbar, &stamp_ready, &stamp_done,
-                  &stamp_cap};
+                  &stamp_cap, &phase};
   NC_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_persistent, dim3(grid), dim3(kPThreads), args, 0,
                                           (cudaStream_t)stream));
   return NC_OK;
