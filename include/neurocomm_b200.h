@@ -162,6 +162,8 @@ typedef struct nc_shard {
   int32_t record_steps;
   int32_t local_words;
   unsigned long long* spike_total; /* [1] running count of local spikes        */
+  uint32_t* work;         /* [4] scratch counters (push work claims), zeroed by
+                             nc_sim_init / nc_sim_end_step                      */
 } nc_shard_t;
 
 /* Set kernel attributes (dynamic shared memory opt-in) once; call before any

@@ -49,7 +49,7 @@ class ShardC(C.Structure):
         ("bucket_ids", c_void_p), ("bucket_count", c_void_p), ("bucket_cap", c_int64),
         ("status", c_void_p), ("step", c_void_p),
         ("raster", c_void_p), ("record_steps", c_int32), ("local_words", c_int32),
-        ("spike_total", c_void_p),
+        ("spike_total", c_void_p), ("work", c_void_p),
     ]
 
 

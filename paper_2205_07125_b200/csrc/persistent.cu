@@ -18,6 +18,7 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include "nc_common.h"
 #include "sim_device.cuh"
 #include "xchg_device.cuh"
@@ -52,6 +53,7 @@ __global__ void __launch_bounds__(kPThreads) k_persistent(const nc_shard_t sh, c
                                                           unsigned long long* st_done, int stamp_cap,
                                                           unsigned long long* phase_st) {
   __shared__ ncdev::LifSmem S;
+  __shared__ ncdev::PushSmem P;
   const int nblk = gridDim.x, bid = blockIdx.x;
   const int nex = has_x ? X.n * B : 0;
   const int32_t negg = -p.g_inh;
@@ -60,7 +62,7 @@ __global__ void __launch_bounds__(kPThreads) k_persistent(const nc_shard_t sh, c
   const bool ph = phase_st && bid == 0 && threadIdx.x == 0;
   for (int s = 0; s < n_steps; ++s, ++step) {
     if (ph && s < 64) phase_st[s * 4 + 0] = gtimer();
-    ncdev::push_phase(sh, negg, step, bid, nblk);
+    ncdev::push_phase(sh, negg, step, P);
     grid_sync(gbar, ++k * nblk, sh.status);
     if (ph && s < 64) phase_st[s * 4 + 1] = gtimer();
     ncdev::lif_phase(sh, p, step, bid, nblk, S);
@@ -73,6 +75,7 @@ __global__ void __launch_bounds__(kPThreads) k_persistent(const nc_shard_t sh, c
     if (bid == 0) {
       if (threadIdx.x == 0 && st_done && step < stamp_cap) st_done[step] = gtimer();
       if ((int)threadIdx.x < sh.n_shards) sh.bucket_count[threadIdx.x] = 0;
+      if (threadIdx.x == 0) sh.work[0] = 0u;   // push chunk claims of the next step
       if (has_x && (int)threadIdx.x < X.n) X.fwd_count[threadIdx.x] = 0;
       if (threadIdx.x == 0 && sh.fired_count) *sh.fired_count = 0;
     }
@@ -99,7 +102,7 @@ extern "C" int nc_run_persistent(const nc_shard_t* sh, const nc_lif_params_t* p,
                                  unsigned long long* stamp_ready, unsigned long long* stamp_done, int32_t stamp_cap,
                                  void* stream) {
   if (!sh || !p || !gbar || n_steps < 0 || !sh->push_rowptr || !sh->push_syn || !sh->acc || !sh->step ||
-      !sh->status) {
+      !sh->status || !sh->work) {
     nc_set_error("nc_run_persistent: shard needs push CSR, acc, step and status buffers");
     return NC_E_ARG;
   }
@@ -115,7 +118,12 @@ extern "C" int nc_run_persistent(const nc_shard_t* sh, const nc_lif_params_t* p,
   }
   // every resident slot: the push and LIF phases are latency bound and want
   // as many warps in flight as the SM holds
-  int grid = sms * (occ < 8 ? occ : 8);
+  int per_sm = occ < 8 ? occ : 8;
+  if (const char* e = getenv("NC_PERSIST_BLOCKS_PER_SM")) {   // tuning knob
+    const int v = atoi(e);
+    if (v >= 1 && v < per_sm) per_sm = v;
+  }
+  int grid = sms * per_sm;
   const int nex = X ? X->n * B : 0;
   if (grid < nex) {
     nc_set_error("nc_run_persistent: %d exchange blocks exceed the resident grid (%d)", nex, grid);

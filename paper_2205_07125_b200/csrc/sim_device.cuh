@@ -284,36 +284,73 @@ static __device__ void lif_phase(const nc_shard_t& sh, const nc_lif_params_t& p,
   add_spike_total(sh, my_spikes, &block_count);
 }
 
-// Event-driven delivery: scan the previous step's spike bitmap one warp per
-// word; for every set bit the warp walks that pre neuron's push-CSR row and
-// adds the integer weights into acc with red.global.add (exact, so order free).
-static __device__ void push_phase(const nc_shard_t& sh, int32_t negg, int step, int bid, int nblk) {
+// Event-driven delivery.  Blocks claim chunks of 32 bitmap words from a
+// per-step counter (dynamic: the number of spikes per chunk varies); warp 0
+// compacts the chunk's spikes into a shared list, then the warps take spikes
+// round-robin and walk each pre neuron's push row with 8 loads in flight per
+// lane, adding integer weights with red.global.add (exact, so order free).
+constexpr int kPushIds = 1024;
+
+// Fire-and-forget add.  Written out because inside the persistent kernel nvcc
+// otherwise emits ATOMG (returns a value) for the same atomicAdd.
+__device__ __forceinline__ void red_add(int32_t* p, int32_t v) {
+  asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+struct PushSmem {
+  int chunk;
+  int n;
+  uint32_t ids[kPushIds];
+};
+
+static __device__ void push_phase(const nc_shard_t& sh, int32_t negg, int step, PushSmem& P) {
   const uint32_t* prev = ((step - 1) & 1) ? sh.bitmap1 : sh.bitmap0;
   const int lane = threadIdx.x & 31;
-  const int64_t wpb = blockDim.x >> 5;
-  for (int64_t w = bid * wpb + (threadIdx.x >> 5); w < sh.n_words; w += nblk * wpb) {
-    uint32_t bits = prev[w];  // same value in every lane (broadcast load)
-    while (bits) {
-      const int b = __ffs(bits) - 1;
-      bits &= bits - 1;
-      const int64_t pre = (w << 5) + b;
+  const int warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  const int n_chunks = (sh.n_words + 31) >> 5;
+  for (;;) {
+    if (threadIdx.x == 0) P.chunk = (int)atomicAdd(sh.work, 1u);
+    __syncthreads();
+    const int c = P.chunk;
+    if (c >= n_chunks) break;
+    if (warp == 0) {
+      const int w = (c << 5) + lane;
+      uint32_t bits = w < sh.n_words ? prev[w] : 0u;
+      const int cnt = __popc(bits);
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int pos = incl - cnt;
+      if (lane == 31) P.n = incl;
+      while (bits) {
+        const int b = __ffs(bits) - 1;
+        bits &= bits - 1;
+        P.ids[pos++] = ((uint32_t)w << 5) + (uint32_t)b;
+      }
+    }
+    __syncthreads();
+    for (int i = warp; i < P.n; i += nwarps) {
+      const uint32_t pre = P.ids[i];
       const int64_t beg = sh.push_rowptr[pre], end = sh.push_rowptr[pre + 1];
-      // 4 independent loads in flight per lane, then 4 fire-and-forget reductions
-      for (int64_t e0 = beg + lane; e0 < end; e0 += 128) {
-        uint32_t x[4];
+      for (int64_t e0 = beg + lane; e0 < end; e0 += 256) {
+        uint32_t x[8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) x[u] = (e0 + 32 * u < end) ? __ldg(sh.push_syn + e0 + 32 * u) : 0u;
+        for (int u = 0; u < 8; ++u) x[u] = (e0 + 32 * u < end) ? __ldg(sh.push_syn + e0 + 32 * u) : 0u;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 8; ++u) {
           if (e0 + 32 * u < end) {
             const int32_t q = (int32_t)((x[u] >> 26) & 31u) + 1;
-            atomicAdd(sh.acc + (x[u] & 0x03FFFFFFu), (x[u] >> 31) ? q * negg : q);
+            red_add(sh.acc + (x[u] & 0x03FFFFFFu), (x[u] >> 31) ? q * negg : q);
           }
         }
       }
     }
+    __syncthreads();
   }
 }
-
 
 }  // namespace ncdev

@@ -133,12 +133,14 @@ __global__ void __launch_bounds__(kLifThreads) k_lif_update(const nc_shard_t sh,
 }
 
 __global__ void __launch_bounds__(256) k_deliver_push(const nc_shard_t sh, int32_t negg) {
-  push_phase(sh, negg, *sh.step, blockIdx.x, gridDim.x);
+  __shared__ PushSmem P;
+  push_phase(sh, negg, *sh.step, P);
 }
 
 __global__ void k_end_step(const nc_shard_t sh) {
   const int t = threadIdx.x;
   if (t < sh.n_shards) sh.bucket_count[t] = 0;
+  if (t < 4 && sh.work) sh.work[t] = 0u;
   if (t == 0) {
     if (sh.fired_count) *sh.fired_count = 0;
     *sh.step += 1;
@@ -162,6 +164,7 @@ __global__ void k_init(const nc_shard_t sh, const nc_lif_params_t p) {
     sh.bitmap1[w] = 0u;
   }
   if (t0 < sh.n_shards) sh.bucket_count[t0] = 0;
+  if (t0 < 4 && sh.work) sh.work[t0] = 0u;
   if (t0 == 0) {
     *sh.step = 0;
     sh.status[0] = 0;
@@ -281,12 +284,12 @@ extern "C" int nc_sim_deliver_pull(const nc_shard_t* sh, int32_t g_inh, void* st
 
 extern "C" int nc_sim_deliver_push(const nc_shard_t* sh, int32_t g_inh, void* stream) {
   if (int e = check_shard(sh)) return e;
-  if (!sh->push_rowptr || !sh->push_syn || !sh->acc) {
-    nc_set_error("nc_sim_deliver_push: shard has no push CSR / acc");
+  if (!sh->push_rowptr || !sh->push_syn || !sh->acc || !sh->work) {
+    nc_set_error("nc_sim_deliver_push: shard has no push CSR / acc / work counters");
     return NC_E_ARG;
   }
-  int64_t grid = (sh->n_words + 7) / 8;
-  if (grid > 16 * num_sms()) grid = 16 * num_sms();
+  int64_t grid = ((sh->n_words + 31) / 32 + 1) / 2;   // blocks claim 32-word chunks dynamically
+  if (grid > 8 * num_sms()) grid = 8 * num_sms();
   if (grid < 1) grid = 1;
   k_deliver_push<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(*sh, -g_inh);
   NC_LAUNCH_CHECK();

@@ -513,6 +513,7 @@ class _ShardState:
         self.raster = torch.zeros((max(self.record_steps, 1), max(self.local_words, 1)), dtype=torch.int32,
                                   device=dev)
         self.spike_total = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.work = torch.zeros(4, dtype=torch.int32, device=dev)
         self.push_rowptr = self.push_syn = None
         if push:
             self.push_rowptr, self.push_syn = _push_csr(csr, lay, h, dev)
@@ -530,7 +531,7 @@ class _ShardState:
             bucket_cap=self.bucket_cap, status=self.status.data_ptr(), step=self.step.data_ptr(),
             raster=self.raster.data_ptr() if self.record_steps > 0 else None,
             record_steps=self.record_steps, local_words=self.local_words,
-            spike_total=self.spike_total.data_ptr())
+            spike_total=self.spike_total.data_ptr(), work=self.work.data_ptr())
 
 
 def _push_csr(csr: ShardCSR, lay: ShardLayout, h: int, dev):
