@@ -90,17 +90,20 @@ int nc_weight_histogram(const double* weights, const int64_t* assignment, int64_
  * Synapses: each undirected edge (i, j, p) of NeuronGraph is one synapse in
  * each direction.  A pull entry is a packed uint32
  *     (q << 26) | pre_internal_id,      q = ceil(32 * p) in [1, 32].
- * Layout: sliced ELL with slice = one warp = 32 consecutive local rows
- * ("SELL-32"), further split by bitmap tile t (the spike bitmap is staged in
- * shared memory tile by tile when it exceeds one tile).  Block (slice s,
- * tile t) starts at slice_ptr[s*n_tiles + t] (uint4 units) and holds `len`
- * slots of 32 uint4: slot u of lane l is entries 4u..4u+3 of row 32s+l.  A
- * row's slots [0, emid) hold its excitatory pres (weight +q), the next slots
- * its inhibitory pres (weight -g_inh*q), its last used slot is len_r - 1:
- * row_meta[row*n_tiles + t] = emid | (len_r << 16).  Lanes only load their own
- * len_r slots, so the padding of a block to its longest row costs no traffic.
- * Unused entries hold the pad entry (guard id, never fires).  Lanes read
- * consecutive 16-byte words, each lane owns one row: no cross-lane reduction.
+ * Layout "J-SELL-32": jagged sliced ELL with slice = one warp = 32
+ * consecutive local rows, further split by bitmap tile t (the spike bitmap is
+ * staged in shared memory tile by tile when it exceeds one tile).  Row r of
+ * slice s has len_r 16-byte slots (4 entries each) in block (s, t); its slots
+ * [0, emid) hold its excitatory pres (weight +q), the next ones its inhibitory
+ * pres (weight -g_inh*q): row_meta[row*n_tiles + t] = emid | (len_r << 16).
+ * Block (s, t) starts at slice_ptr[s*n_tiles + t] (uint4 units) and stores
+ * slot u of every lane with len > u contiguously, in lane order:
+ *     position(u, l) = sum_{v<u} cnt_v + #{l' < l : len_l' > u},
+ *     cnt_v = #{l : len_l > v},
+ * so for u below the block's shortest row it is plain u*32 + l (coalesced
+ * 512-byte warp loads) and the block holds no padding beyond each E/I
+ * segment rounded up to 4 entries (those hold the pad entry 0: tile-relative
+ * id 0 with q = 0).  Each lane owns one row: no cross-lane reduction.
  * Push entries (rows = internal pre ids):
  *     (inhibitory(pre) << 31) | ((q - 1) << 26) | post_local. */
 
@@ -328,24 +331,32 @@ int nc_graphgen_degrees(const nc_graphgen_t* g, int32_t* deg, void* stream);
  * (row, tile, sign) (zero-initialised); tile_words as in nc_shard_t. */
 int nc_graphgen_count(const nc_graphgen_t* g, int32_t n_tiles, int32_t tile_words, int32_t* lower_len,
                       int32_t* upper_len, void* stream);
-/* Pass 2 into the SELL-32 layout (slice_ptr/row_meta computed by the host
- * from the pass-1 counts); lower_fill [n_local*n_tiles*2] zero-initialised
- * (slot claims; lower_len is unused and may be NULL).  syn must be pre-filled
- * with nc_sell_fill_pads. */
+/* Pass 2 into the PADDED SELL-32 layout (every block = its longest row x 32
+ * lanes, slot u of lane l at padded_ptr[block] + u*32 + l; padded_ptr and
+ * row_meta computed by the host from the pass-1 counts); lower_fill
+ * [n_local*n_tiles*2] zero-initialised (slot claims; lower_len is unused and
+ * may be NULL).  syn must be pre-filled with nc_sell_fill_pads; convert the
+ * result with nc_sell_repack. */
 int nc_graphgen_fill(const nc_graphgen_t* g, int32_t n_tiles, int32_t tile_words, const int64_t* slice_ptr,
                      const uint32_t* row_meta, const int32_t* lower_len, int32_t* lower_fill, uint32_t* syn,
                      void* stream);
-/* Pad pre-fill of a SELL-32 array: block b = (slice, tile b % n_tiles) gets
- * (first id of its tile) with q = 0 in every entry. */
+/* Pad pre-fill of a padded SELL-32 array: every entry = 0 (tile-relative id
+ * 0, q = 0).  n_tiles / tile_words are accepted for ABI stability. */
 int nc_sell_fill_pads(const int64_t* slice_ptr, int64_t n_blocks, int32_t n_tiles, int32_t tile_words,
                       uint32_t* syn, void* stream);
 /* Destination masks from a built CSR (the adjacency is symmetric, so the
  * pres of row r are exactly the posts r drives): dest_mask[r] = OR over the
  * row's entries of (1 << owner shard of the pre id) without `self`, where shard
  * h owns internal ids [shard_base[h], shard_base[h+1]) (device int32[n+1]). */
-int nc_dest_mask_from_csr(const int64_t* slice_ptr, int32_t n_tiles, const uint32_t* syn, int32_t n_local,
-                          const int32_t* shard_base, int32_t n_shards, int32_t self,
-                          uint16_t* dest_mask, void* stream);
+int nc_dest_mask_from_csr(const int64_t* slice_ptr, const uint32_t* row_meta, int32_t n_tiles, int32_t tile_words,
+                          const uint32_t* syn, int32_t n_local, const int32_t* shard_base, int32_t n_shards,
+                          int32_t self, uint16_t* dest_mask, void* stream);
+/* Padded SELL-32 (padded_ptr, as filled by nc_graphgen_fill) <-> J-SELL-32
+ * (slice_ptr): to_jagged != 0 copies src (padded) into dst (jagged), else
+ * the reverse (dst must be pre-filled; slots past a row's length are left
+ * untouched).  Pointers in uint4 units, n_slices * n_tiles + 1 entries. */
+int nc_sell_repack(const int64_t* padded_ptr, const int64_t* slice_ptr, const uint32_t* row_meta, int32_t n_tiles,
+                   int32_t n_local, const uint32_t* src, uint32_t* dst, int32_t to_jagged, void* stream);
 
 #ifdef __cplusplus
 }

@@ -108,8 +108,10 @@ _SIGS = {
                                    c_void_p, c_void_p]),
     "nc_graphgen_degrees": (c_int32, [C.POINTER(GraphGenC), c_void_p, c_void_p]),
     "nc_sell_fill_pads": (c_int32, [c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p]),
-    "nc_dest_mask_from_csr": (c_int32, [c_void_p, c_int32, c_void_p, c_int32, c_void_p, c_int32, c_int32, c_void_p,
-                                        c_void_p]),
+    "nc_dest_mask_from_csr": (c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_int32, c_void_p, c_int32,
+                                        c_int32, c_void_p, c_void_p]),
+    "nc_sell_repack": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_int32,
+                                 c_void_p]),
     "nc_xchg_reset": (c_int32, [C.POINTER(XchgC), c_void_p]),
     "nc_xchg_seal": (c_int32, [C.POINTER(XchgC), c_int32, c_void_p]),
     "nc_xchg_scatter": (c_int32, [C.POINTER(XchgC), c_int32, c_void_p]),

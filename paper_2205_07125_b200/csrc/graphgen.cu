@@ -22,6 +22,7 @@
 #include <stdint.h>
 #include <math.h>
 #include "nc_common.h"
+#include "jsell.cuh"
 #include "philox.cuh"
 
 namespace {
@@ -87,6 +88,11 @@ __device__ __forceinline__ uint32_t edge_q(const nc_graphgen_t& g, int64_t i, in
 
 __device__ __forceinline__ uint32_t is_inh(const nc_graphgen_t& g, int64_t gid) {
   return (g.inh_every > 0 && (gid % g.inh_every) == g.inh_every - 1) ? 1u : 0u;
+}
+
+// First internal id of the bitmap tile holding `id` (entries store ids relative to it).
+__device__ __forceinline__ uint32_t tile_base(uint32_t id, int32_t TW) {
+  return (id >> 5) / (uint32_t)TW * (uint32_t)TW * 32u;
 }
 
 __device__ __forceinline__ uint32_t pack(uint32_t pre_internal, uint32_t q) {
@@ -185,49 +191,81 @@ __global__ void k_fill(const nc_graphgen_t g, int32_t T, int32_t TW, const int64
       if (mine) {
         const int64_t seg = seg_index(ri, T, TW, jid, is_inh(g, j));
         const int32_t k = atomicAdd(fill + seg, 1);
-        syn[sell_pos(slice_ptr, row_meta, T, ri, seg, k)] = pack(jid, q);
+        syn[sell_pos(slice_ptr, row_meta, T, ri, seg, k)] = pack(jid - tile_base(jid, TW), q);
       }
       if (jm) {
         const int64_t rj = (int64_t)jid - g.local_base;
         const int64_t seg = seg_index(rj, T, TW, iid, inh_i);
         const int32_t k = atomicAdd(fill + seg, 1);
-        syn[sell_pos(slice_ptr, row_meta, T, rj, seg, k)] = pack(iid, q);
+        syn[sell_pos(slice_ptr, row_meta, T, rj, seg, k)] = pack(iid - tile_base(iid, TW), q);
       }
     });
   }
 }
 
-// Pad pre-fill: every entry of block (slice, tile t) = first id of tile t with
-// q = 0, so an unused slot looks up a staged word and adds nothing.
-__global__ void k_fill_pads(const int64_t* slice_ptr, int64_t n_blocks, int32_t T, int32_t TW, uint32_t* syn) {
-  for (int64_t b = blockIdx.x; b < n_blocks; b += gridDim.x) {
-    const uint32_t pad = (uint32_t)((b % T) * (int64_t)TW * 32);
-    const uint4 v = make_uint4(pad, pad, pad, pad);
-    uint4* s4 = reinterpret_cast<uint4*>(syn);
-    for (int64_t k = slice_ptr[b] + threadIdx.x; k < slice_ptr[b + 1]; k += blockDim.x) s4[k] = v;
-  }
+// Pad pre-fill: entries hold tile-relative ids, so the pad entry (id 0 of
+// the block's tile with q = 0: a staged word, adds nothing) is all zeros.
+__global__ void k_fill_pads(const int64_t* slice_ptr, int64_t n_blocks, uint32_t* syn) {
+  uint4* s4 = reinterpret_cast<uint4*>(syn);
+  for (int64_t b = blockIdx.x; b < n_blocks; b += gridDim.x)
+    for (int64_t k = slice_ptr[b] + threadIdx.x; k < slice_ptr[b + 1]; k += blockDim.x) s4[k] = make_uint4(0, 0, 0, 0);
 }
 
-__global__ void k_dest_mask(const int64_t* slice_ptr, int32_t T, const uint32_t* syn, int32_t n_local,
-                            const int32_t* shard_base, int32_t n_shards, int32_t self, uint16_t* dest) {
+// Destination shards of every local row: warp per slice, lane = row, over the
+// row's entries in every tile block (J-SELL order, pads have q = 0).
+__global__ void k_dest_mask(const int64_t* slice_ptr, const uint32_t* row_meta, int32_t T, int32_t tile_words,
+                            const uint32_t* syn, int32_t n_local, const int32_t* shard_base, int32_t n_shards, int32_t self,
+                            uint16_t* dest) {
   const int lane = threadIdx.x & 31;
   const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r = wid; r < n_local; r += nw) {
+  const int64_t n_slices = (n_local + 31) >> 5;
+  for (int64_t s = wid; s < n_slices; s += nw) {
+    const int64_t r = (s << 5) + lane;
     uint32_t m = 0;
     for (int32_t t = 0; t < T; ++t) {
-      const int64_t b0 = slice_ptr[(r >> 5) * T + t], b1 = slice_ptr[(r >> 5) * T + t + 1];
-      const int64_t len = (b1 - b0) >> 5;
-      for (int64_t k = lane; k < len * 4; k += 32) {
-        const uint32_t e = syn[(b0 + (k >> 2) * 32 + (r & 31)) * 4 + (k & 3)];
-        if ((e >> 26) == 0) continue;  // pad
-        const int64_t pre = e & 0x03FFFFFFu;
-        for (int h = 0; h < n_shards; ++h)
-          if (pre >= shard_base[h] && pre < shard_base[h + 1]) m |= 1u << h;
+      const int64_t b0 = slice_ptr[s * T + t];
+      const int64_t tbase = (int64_t)t * tile_words * 32;
+      const int mine = r < n_local ? (int)(row_meta[r * T + t] >> 16) : 0;
+      const int hi = (int)__reduce_max_sync(0xffffffffu, (unsigned)mine);
+      int off = 0;
+      for (int u = 0; u < hi; ++u) {
+        const int pos = ncdev::jsell_pos(u, mine, lane, off);
+        if (u >= mine) continue;
+        for (int c = 0; c < 4; ++c) {
+          const uint32_t e = syn[(b0 + pos) * 4 + c];
+          if ((e >> 26) == 0) continue;  // pad
+          const int64_t pre = (e & 0x03FFFFFFu) + tbase;
+          for (int h = 0; h < n_shards; ++h)
+            if (pre >= shard_base[h] && pre < shard_base[h + 1]) m |= 1u << h;
+        }
       }
     }
-    m = __reduce_or_sync(0xffffffffu, m);
-    if (lane == 0) dest[r] = (uint16_t)(m & ~(1u << self));
+    if (r < n_local) dest[r] = (uint16_t)(m & ~(1u << self));
+  }
+}
+
+// Padded SELL-32 (block = longest row x 32 lanes, slot u of lane l at u*32 + l:
+// what the generator fills) <-> J-SELL (jsell.cuh).  Warp per block.
+__global__ void k_sell_repack(const int64_t* pptr, const int64_t* cptr, const uint32_t* row_meta, int32_t T,
+                              int32_t n_local, const uint4* src, uint4* dst, int to_compact) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t n_blocks = ((int64_t)(n_local + 31) >> 5) * T;
+  for (int64_t b = wid; b < n_blocks; b += nw) {
+    const int64_t r = ((b / T) << 5) + lane;
+    const int64_t t = b % T;
+    const int mine = r < n_local ? (int)(row_meta[r * T + t] >> 16) : 0;
+    const int hi = (int)__reduce_max_sync(0xffffffffu, (unsigned)mine);
+    int off = 0;
+    for (int u = 0; u < hi; ++u) {
+      const int pos = ncdev::jsell_pos(u, mine, lane, off);
+      if (u >= mine) continue;
+      const int64_t pp = pptr[b] + (int64_t)u * 32 + lane, cp = cptr[b] + pos;
+      if (to_compact) dst[cp] = src[pp];
+      else dst[pp] = src[cp];
+    }
   }
 }
 
@@ -283,21 +321,39 @@ extern "C" int nc_sell_fill_pads(const int64_t* slice_ptr, int64_t n_blocks, int
                                  uint32_t* syn, void* stream) {
   if (n_blocks <= 0) return NC_OK;
   int64_t grid = n_blocks < 65535 ? n_blocks : 65535;
-  k_fill_pads<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(slice_ptr, n_blocks, n_tiles, tile_words, syn);
+  (void)n_tiles;
+  (void)tile_words;
+  k_fill_pads<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(slice_ptr, n_blocks, syn);
   NC_LAUNCH_CHECK();
   return NC_OK;
 }
 
-extern "C" int nc_dest_mask_from_csr(const int64_t* slice_ptr, int32_t n_tiles, const uint32_t* syn, int32_t n_local,
-                                     const int32_t* shard_base, int32_t n_shards, int32_t self,
-                                     uint16_t* dest_mask, void* stream) {
+extern "C" int nc_sell_repack(const int64_t* padded_ptr, const int64_t* slice_ptr, const uint32_t* row_meta,
+                              int32_t n_tiles, int32_t n_local, const uint32_t* src, uint32_t* dst, int32_t to_jagged,
+                              void* stream) {
+  if (n_tiles < 1 || n_local < 0 || !padded_ptr || !slice_ptr || !row_meta) {
+    nc_set_error("nc_sell_repack: bad arguments");
+    return NC_E_ARG;
+  }
+  if (n_local == 0) return NC_OK;
+  const int64_t n_blocks = ((int64_t)(n_local + 31) / 32) * n_tiles;
+  k_sell_repack<<<grid_for(n_blocks * 32, 256), 256, 0, (cudaStream_t)stream>>>(
+      padded_ptr, slice_ptr, row_meta, n_tiles, n_local, reinterpret_cast<const uint4*>(src),
+      reinterpret_cast<uint4*>(dst), to_jagged ? 1 : 0);
+  NC_LAUNCH_CHECK();
+  return NC_OK;
+}
+
+extern "C" int nc_dest_mask_from_csr(const int64_t* slice_ptr, const uint32_t* row_meta, int32_t n_tiles,
+                                     int32_t tile_words, const uint32_t* syn, int32_t n_local, const int32_t* shard_base,
+                                     int32_t n_shards, int32_t self, uint16_t* dest_mask, void* stream) {
   if (n_shards < 1 || n_shards > NC_MAX_SHARDS) {
     nc_set_error("nc_dest_mask_from_csr: n_shards must be in [1, %d]", NC_MAX_SHARDS);
     return NC_E_ARG;
   }
   if (n_local == 0) return NC_OK;
   k_dest_mask<<<grid_for((int64_t)n_local * 32, 256), 256, 0, (cudaStream_t)stream>>>(
-      slice_ptr, n_tiles, syn, n_local, shard_base, n_shards, self, dest_mask);
+      slice_ptr, row_meta, n_tiles, tile_words, syn, n_local, shard_base, n_shards, self, dest_mask);
   NC_LAUNCH_CHECK();
   return NC_OK;
 }

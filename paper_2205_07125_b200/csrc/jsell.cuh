@@ -1,0 +1,23 @@
+// Jagged SELL-32 (J-SELL) addressing, shared by the delivery kernels and the
+// builders (include/neurocomm_b200.h documents the layout).
+#pragma once
+#include <cuda_runtime.h>
+
+namespace ncdev {
+
+// Jagged SELL-32 (J-SELL) block: lane l's row has len_l = meta >> 16 slots,
+// the first (meta & 0xFFFF) excitatory.  Slot u of the lanes with len > u is
+// stored contiguously, in lane order: position = sum_{v<u} cnt_v + rank of the
+// lane among them, cnt_v = #lanes with len > v.  So the regular part
+// u < min_l len_l is plain SELL (u*32 + lane) and only the ragged tail needs a
+// ballot per slot -- and the block stores no padding beyond each row's E/I
+// segments rounded up to 4 entries.  A warp steps u in lockstep; jsell_pos
+// returns this lane's position of slot u and advances `off` to slot u + 1.
+__device__ __forceinline__ int jsell_pos(int u, int mine, int lane, int& off) {
+  const uint32_t act = __ballot_sync(0xffffffffu, u < mine);
+  const int pos = off + __popc(act & ((1u << lane) - 1u));
+  off += __popc(act);
+  return pos;
+}
+
+}  // namespace ncdev

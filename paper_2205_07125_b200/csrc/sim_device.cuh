@@ -5,6 +5,7 @@
 #include <stdint.h>
 #include "nc_common.h"
 #include "philox.cuh"
+#include "jsell.cuh"
 
 namespace ncdev {
 
@@ -25,44 +26,121 @@ __device__ __forceinline__ uint4 ld_keep(const uint4* p) {
   return r;
 }
 
-// Weight units of one packed entry (q << 26 | pre) if its pre fired, else 0.
-// The funnel shift rotates the bitmap word by the low 5 bits of the entry
-// (= pre & 31), so bit 0 is the pre's spike bit: 5 integer ops per synapse.
-__device__ __forceinline__ int32_t entry_term(uint32_t e, const uint32_t* __restrict__ bm) {
+// Weight units of one packed entry (q << 26 | pre, pre relative to the staged
+// tile) if its pre fired, else 0.  The funnel shift rotates the bitmap word by
+// the low 5 bits of the entry (= pre & 31), so bit 0 is the pre's spike bit;
+// the product folds into an IMAD with the running sum.
+__device__ __forceinline__ uint32_t entry_bit(uint32_t e, const uint32_t* __restrict__ bm) {
   const uint32_t word = bm[(e & 0x03FFFFFFu) >> 5];
-  const uint32_t rot = __funnelshift_r(word, word, e);
-  return (rot & 1u) ? (int32_t)(e >> 26) : 0;
+  return __funnelshift_r(word, word, e) & 1u;
 }
 
 __device__ __forceinline__ int32_t quad_term(uint4 e, const uint32_t* __restrict__ bm) {
-  return entry_term(e.x, bm) + entry_term(e.y, bm) + entry_term(e.z, bm) + entry_term(e.w, bm);
+  uint32_t s = entry_bit(e.x, bm) * (e.x >> 26);
+  s += entry_bit(e.y, bm) * (e.y >> 26);
+  s += entry_bit(e.z, bm) * (e.z >> 26);
+  s += entry_bit(e.w, bm) * (e.w >> 26);
+  return (int32_t)s;
 }
 
-// One lane's row in one SELL-32 block: block slots [0, len) at blk + u*32 + lane;
-// this row uses meta >> 16 of them, the first (meta & 0xFFFF) excitatory.
-// Slots past the row's own length are not loaded (`pad` stands in: the block's
-// pad entry, first id of its tile with q = 0, so its lookup stays in the
-// staged tile and adds nothing).  Returns sum_E - g * sum_I (weight units).
-__device__ __forceinline__ int32_t sell_row_sum(const uint4* __restrict__ blk, int len, uint32_t meta,
+// ---- 1-D TMA bulk copies into shared memory, completed on an mbarrier
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+// arrive (count 1) + expect `bytes` of transactions on the current phase
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+// global -> shared bulk copy (16-byte aligned, size a multiple of 16) by the TMA engine
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// order this thread's earlier generic-proxy shared accesses before later async-proxy (TMA) ones
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// TMA-engine prefetch of a contiguous range into L2 (no registers held).
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// Slots ahead of the loads for the tiled kernel's L2 prefetch: with the
+// bitmap tile filling shared memory, registers cap the loads in flight and the
+// prefetch keeps HBM busy (measured +7% at 2 tiles; at 1 tile it costs ~1%).
+#ifndef NC_PF_DIST
+#define NC_PF_DIST 8
+#endif
+constexpr int kPfTiled = NC_PF_DIST;
+
+// Sum over one lane's row of a J-SELL block: returns sum_E - g * sum_I
+// (weight units).  Slots past the lane's own length are not loaded (`pad`
+// stands in: id 0 with q = 0, so its lookup stays in the staged tile and adds
+// nothing).
+template <int kPfDist>
+__device__ __forceinline__ int32_t sell_row_sum(const uint4* __restrict__ blk, uint32_t meta,
                                                 const uint32_t* __restrict__ bm, int32_t g_inh, int lane,
                                                 uint32_t pad) {
   const int emid = (int)(meta & 0xFFFFu);
   const int mine = (int)(meta >> 16);
-  int32_t se = 0, si = 0;
+  const int lo = __reduce_min_sync(kFull, (unsigned)mine);
+  const int hi = __reduce_max_sync(kFull, (unsigned)mine);
+  const int32_t wi = -g_inh;   // weight of an inhibitory slot
+  int32_t acc = 0;
   const uint4* p = blk + lane;
   const uint4 padv = make_uint4(pad, pad, pad, pad);
-  for (int u0 = 0; u0 < len; u0 += kUnroll) {
+  // regular part: every lane has slots [0, lo)
+  for (int u0 = 0; u0 < lo; u0 += kUnroll) {
+    if (kPfDist > 0 && lane == 0 && u0 + kPfDist < lo) {
+      const int a = u0 + kPfDist;
+      prefetch_l2(blk + a * 32, (uint32_t)min(kUnroll, lo - a) * 512u);
+    }
     uint4 e[kUnroll];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) e[u] = (u0 + u < mine) ? ld_stream(p + (u0 + u) * 32) : padv;
+    for (int u = 0; u < kUnroll; ++u) e[u] = (u0 + u < lo) ? ld_stream(p + (u0 + u) * 32) : padv;
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      const int32_t t = quad_term(e[u], bm);
-      if (u0 + u < emid) se += t;
-      else si += t;
+      if (u0 + u >= lo) break;   // warp-uniform: no lookups for the pad of a partial group
+      acc += quad_term(e[u], bm) * (u0 + u < emid ? 1 : wi);
     }
   }
-  return se - g_inh * si;
+  // ragged tail
+  int off = lo * 32;
+  for (int u0 = lo; u0 < hi; u0 += kUnroll) {
+    uint4 e[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int pos = jsell_pos(u0 + u, mine, lane, off);
+      e[u] = (u0 + u < mine) ? ld_stream(blk + pos) : padv;
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      if (u0 + u >= hi) break;   // warp-uniform
+      acc += quad_term(e[u], bm) * (u0 + u < emid ? 1 : wi);
+    }
+  }
+  return acc;
 }
 
 // Exact LIF step; returns true if the neuron fired.  Operation order is the

@@ -26,6 +26,7 @@ namespace {
 using namespace ncdev;
 
 constexpr int kThreads = 1024;    // one CTA per SM in the smem-bitmap variant
+constexpr int kMaxTiles = 256;    // bitmap tiles per shard (sell.py plan_tiles)
 // K3 (+K1+K2 when kLif).  kTiled: the bitmap does not fit in shared memory;
 // every CTA owns a fixed range of slices, loops over the bitmap tiles and
 // keeps the per-row partial sums in shared memory behind the tile.
@@ -53,12 +54,27 @@ k_step_fused(const nc_shard_t sh, const nc_lif_params_t p) {
     const int n4 = (sh.n_words + 3) >> 2;
     for (int k = threadIdx.x; k < n4; k += blockDim.x) smem4[k] = ld_keep(src + k);
     __syncthreads();
-    for (int slice = blockIdx.x * wpb + warp; slice < n_slices; slice += gridDim.x * wpb) {
+    // the next slice's block start and row_meta load while this one streams
+    const int stride = gridDim.x * wpb;
+    int slice = blockIdx.x * wpb + warp;
+    int64_t b0 = 0;
+    uint32_t meta = 0u;
+    if (slice < n_slices) {
+      b0 = sh.slice_ptr[slice];
+      meta = (slice << 5) + lane < sh.n_local ? sh.row_meta[(slice << 5) + lane] : 0u;
+    }
+    for (; slice < n_slices; slice += stride) {
       const int row = (slice << 5) + lane;
-      const int64_t b0 = sh.slice_ptr[slice];
-      const int len = (int)((sh.slice_ptr[slice + 1] - b0) >> 5);
-      const uint32_t meta = row < sh.n_local ? sh.row_meta[row] : 0u;
-      const int32_t acc = sell_row_sum(syn4 + b0, len, meta, sbm, g_inh, lane, 0u);
+      const int nxt = slice + stride;
+      int64_t b0n = 0;
+      uint32_t metan = 0u;
+      if (nxt < n_slices) {
+        b0n = sh.slice_ptr[nxt];
+        metan = (nxt << 5) + lane < sh.n_local ? sh.row_meta[(nxt << 5) + lane] : 0u;
+      }
+      const int32_t acc = sell_row_sum<0>(syn4 + b0, meta, sbm, g_inh, lane, 0u);
+      b0 = b0n;
+      meta = metan;
       if (kLif) {
         const uint32_t fm = update_slice(sh, p, cur, slice, lane, acc, step);
         if (lane == 0) my_spikes += __popc(fm);
@@ -67,54 +83,97 @@ k_step_fused(const nc_shard_t sh, const nc_lif_params_t p) {
       }
     }
   } else {
+    // Tiled: two tile buffers in shared memory, filled by TMA bulk copies that
+    // complete on mbarriers.  Warps claim (slice, tile) blocks dynamically and
+    // move on to the next tile as soon as they run out of work -- no CTA-wide
+    // barrier between tiles: the last warp to leave tile t refills t's buffer
+    // with tile t + 2.  Warps span at most two consecutive tiles, so partial
+    // sums are combined with shared (or, flags bit 0, global) integer atomics.
     const int T = sh.n_tiles, TW = sh.tile_words;
     // CTA c owns slices c, c+G, c+2G, ...: rows are ordered by degree inside the
     // shard, so interleaving gives every CTA the same mix of long and short rows
     const int G = gridDim.x, c = blockIdx.x;
     const int cnt = c < n_slices ? (n_slices - c + G - 1) / G : 0;
-    // partial sums per owned row: shared memory behind the tile, or the acc array
-    // (indexed by row) when the CTA's rows do not fit next to a useful tile (flags bit 0)
     const bool pglob = (sh.flags & 1) != 0;
-    int32_t* part = pglob ? sh.acc : reinterpret_cast<int32_t*>(sbm + TW);
+    int32_t* spart = reinterpret_cast<int32_t*>(sbm + 2 * TW);   // shared partials (!pglob)
+    __shared__ uint64_t full[2];
+    __shared__ int done[2];
+    __shared__ int next_slice[kMaxTiles];
     for (int k = threadIdx.x; k < cnt * 32; k += blockDim.x) {
       const int row = ((c + (k >> 5) * G) << 5) + (k & 31);
-      if (!pglob) part[k] = 0;
-      else if (row < sh.n_local) part[row] = 0;
+      if (!pglob) spart[k] = 0;
+      else if (row < sh.n_local) sh.acc[row] = 0;
     }
-    __shared__ int next_slice[2];
-    if (threadIdx.x == 0) next_slice[0] = next_slice[1] = 0;
-    for (int t = 0; t < T; ++t) {
-      __syncthreads();
-      const int w0 = t * TW;
-      const int nw = min(TW, sh.n_words - w0);
-      const uint4* src = reinterpret_cast<const uint4*>(prev + w0);
-      for (int k = threadIdx.x; k < (nw + 3) >> 2; k += blockDim.x) smem4[k] = ld_keep(src + k);
-      if (threadIdx.x == 0) next_slice[(t + 1) & 1] = 0;  // counter of the next tile
-      __syncthreads();
-      // tile-relative view: bm[global word] hits the staged copy
-      const uint32_t* bm = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(sbm) -
-                                                             (uintptr_t)w0 * 4u);
-      // warps claim slices dynamically so the per-tile barrier waits for at most one slice
-      for (;;) {
-        int j = 0;
-        if (lane == 0) j = atomicAdd(&next_slice[t & 1], 1);
-        j = __shfl_sync(kFull, j, 0);
-        if (j >= cnt) break;
-        const int slice = c + j * G;
-        const int row = (slice << 5) + lane;
-        const int64_t b0 = sh.slice_ptr[(int64_t)slice * T + t];
-        const int len = (int)((sh.slice_ptr[(int64_t)slice * T + t + 1] - b0) >> 5);
-        const uint32_t meta = row < sh.n_local ? sh.row_meta[(int64_t)row * T + t] : 0u;
-        const int32_t sum = sell_row_sum(syn4 + b0, len, meta, bm, g_inh, lane, (uint32_t)w0 * 32u);
-        if (!pglob) part[j * 32 + lane] += sum;
-        else if (row < sh.n_local) part[row] += sum;
+    for (int k = threadIdx.x; k < T; k += blockDim.x) next_slice[k] = 0;
+    auto tile_bytes = [&](int t) {
+      return (uint32_t)((min(TW, sh.n_words - t * TW) + 3) >> 2) * 16u;
+    };
+    if (threadIdx.x == 0) {
+      done[0] = done[1] = 0;
+      mbar_init(&full[0], 1);
+      mbar_init(&full[1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      for (int t = 0; t < 2 && t < T; ++t) {
+        mbar_arrive_expect_tx(&full[t], tile_bytes(t));
+        bulk_g2s(sbm + t * TW, prev + t * TW, tile_bytes(t), &full[t]);
       }
     }
     __syncthreads();
+    for (int t = 0; t < T; ++t) {
+      const int b = t & 1;
+      const int w0 = t * TW;
+      mbar_wait(&full[b], (uint32_t)(t >> 1) & 1u);
+      // entries hold tile-relative pre ids: look them up in the staged copy directly
+      const uint32_t* bm = sbm + b * TW;
+      // the next claim's block start and row_meta load (and its first slots are
+      // prefetched into L2) while the current block streams
+      auto claim = [&](int64_t& b0, uint32_t& m) {
+        int j = 0;
+        if (lane == 0) j = atomicAdd(&next_slice[t], 1);
+        j = __shfl_sync(kFull, j, 0);
+        if (j < cnt) {
+          const int r = ((c + j * G) << 5) + lane;
+          b0 = sh.slice_ptr[(int64_t)(c + j * G) * T + t];
+          m = r < sh.n_local ? sh.row_meta[(int64_t)r * T + t] : 0u;
+          if (kPfTiled > 0 && lane == 0) prefetch_l2(syn4 + b0, kPfTiled * 512u);
+        }
+        return j;
+      };
+      int64_t b0 = 0;
+      uint32_t meta = 0u;
+      int j = claim(b0, meta);
+      while (j < cnt) {
+        int64_t b0n = 0;
+        uint32_t metan = 0u;
+        const int jn = claim(b0n, metan);
+        const int row = ((c + j * G) << 5) + lane;
+        const int32_t sum = sell_row_sum<kPfTiled>(syn4 + b0, meta, bm, g_inh, lane, 0u);
+        if (!pglob) atomicAdd(&spart[j * 32 + lane], sum);
+        else if (row < sh.n_local) red_add(&sh.acc[row], sum);
+        j = jn;
+        b0 = b0n;
+        meta = metan;
+      }
+      // leave tile t; the last warp out refills its buffer with tile t + 2
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();
+        if (atomicAdd(&done[b], 1) == wpb - 1) {
+          done[b] = 0;
+          if (t + 2 < T) {
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(&full[b], tile_bytes(t + 2));
+            bulk_g2s(sbm + b * TW, prev + (t + 2) * TW, tile_bytes(t + 2), &full[b]);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (pglob) __threadfence();
     for (int j = warp; j < cnt; j += wpb) {
       const int slice = c + j * G;
       const int row = (slice << 5) + lane;
-      const int32_t acc = pglob ? (row < sh.n_local ? part[row] : 0) : part[j * 32 + lane];
+      const int32_t acc = pglob ? (row < sh.n_local ? sh.acc[row] : 0) : spart[j * 32 + lane];
       if (kLif) {
         const uint32_t fm = update_slice(sh, p, cur, slice, lane, acc, step);
         if (lane == 0) my_spikes += __popc(fm);
@@ -193,10 +252,11 @@ int g_max_dyn_smem = 0;   // opt-in limit minus the kernels' static shared memor
 // the per-row partial sums of the CTA's slice range
 size_t step_smem_bytes(const nc_shard_t& sh, int grid) {
   if (sh.n_tiles <= 1) return (size_t)((sh.n_words + 3) >> 2) * 16;
-  if (sh.flags & 1) return (size_t)sh.tile_words * 4;
+  // two tile buffers (+ the CTA's partial sums unless they live in acc)
+  if (sh.flags & 1) return (size_t)sh.tile_words * 8;
   const int n_slices = (sh.n_local + 31) >> 5;
   const int per = (n_slices + grid - 1) / grid;
-  return (size_t)sh.tile_words * 4 + (size_t)per * 32 * 4;
+  return (size_t)sh.tile_words * 8 + (size_t)per * 32 * 4;
 }
 
 template <bool kLif>
@@ -219,7 +279,7 @@ int launch_step(const nc_shard_t& sh, const nc_lif_params_t& p, cudaStream_t st)
 int check_shard(const nc_shard_t* sh) {
   if (!sh || sh->n_local < 0 || sh->n_words < 1 || (sh->local_base & 31) || !sh->step ||
       !sh->status || !sh->bitmap0 || !sh->bitmap1 || sh->n_tiles < 1 ||
-      (sh->n_tiles > 1 && (sh->tile_words < 4 || (sh->tile_words & 3) ||
+      (sh->n_tiles > 1 && (sh->tile_words < 4 || (sh->tile_words & 3) || sh->n_tiles > kMaxTiles ||
                            (int64_t)sh->tile_words * sh->n_tiles < sh->n_words)) ||
       ((sh->flags & 1) && !sh->acc)) {
     nc_set_error("invalid nc_shard_t");
@@ -339,15 +399,19 @@ __global__ void k_push_build(const nc_shard_t sh, int phase, int64_t* rowptr, in
     const int64_t b0 = sh.slice_ptr[blk];
     const uint32_t meta = row < sh.n_local ? sh.row_meta[(int64_t)row * T + t] : 0u;
     const int emid = (int)(meta & 0xFFFFu), mine = (int)(meta >> 16);
-    for (int u = 0; u < mine; ++u) {
-      const uint4 e4 = syn4[b0 + (int64_t)u * 32 + lane];
+    const int hi = (int)__reduce_max_sync(0xffffffffu, (unsigned)mine);
+    int off = 0;
+    for (int u = 0; u < hi; ++u) {
+      const int pos = jsell_pos(u, mine, lane, off);
+      if (u >= mine) continue;
+      const uint4 e4 = syn4[b0 + pos];
       const uint32_t es[4] = {e4.x, e4.y, e4.z, e4.w};
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const uint32_t e = es[c];
         const uint32_t q = e >> 26;
         if (q == 0) continue;
-        const uint32_t pre = e & 0x03FFFFFFu;
+        const uint32_t pre = (e & 0x03FFFFFFu) + (uint32_t)t * (uint32_t)sh.tile_words * 32u;
         if (phase == 0) {
           atomicAdd(reinterpret_cast<unsigned long long*>(rowptr + pre + 1), 1ull);
         } else {

@@ -1,12 +1,18 @@
-"""SELL-32 pull-synapse layout (include/neurocomm_b200.h) -- host-side planning.
+"""J-SELL-32 pull-synapse layout (include/neurocomm_b200.h) -- host-side planning.
 
 A slice is one warp's 32 consecutive local post rows.  For every (slice,
-bitmap tile) block, lane l owns row 32*slice + l and reads slot u at
-``slice_ptr[block] + 32*u + l`` (16-byte words of 4 entries).  Within a row's
-part of a block, the excitatory pres fill slots [0, emid), the inhibitory
-ones the next ceil(n_I/4) slots (row length len_r); row_meta = emid |
-(len_r << 16).  Lanes never load past their own len_r; storage past it (up
-to the block's longest row) holds pad entries (q = 0 and the tile's first id).
+bitmap tile) block, lane l owns row 32*slice + l, which has len_l 16-byte
+slots of 4 entries there: the excitatory pres fill slots [0, emid), the
+inhibitory ones the next ceil(n_I/4) slots; row_meta = emid | (len_l << 16).
+The block stores slot u of every lane with len > u contiguously, in lane
+order (jagged: no padding to the longest row), so below the shortest row of
+the block slot u of lane l sits at u*32 + l.  Entries are (q << 26) | id
+with the pre id relative to the first id of the block's tile; unused entries
+of a row's E/I segments hold the pad entry 0 (id 0, q = 0).
+
+Builders fill the *padded* SELL-32 form first (block = longest row x 32 lanes,
+slot u of lane l at padded_ptr + u*32 + l) and convert it (nc_sell_repack on
+the device, :func:`jagged_gather` on the host).
 
 Tiles: when the spike bitmap is larger than shared memory, it is staged in
 tiles of ``tile_words`` words and every block only references pres of its
@@ -22,17 +28,20 @@ import numpy as np
 ID_BITS = 26
 ID_MASK = (1 << ID_BITS) - 1
 SMEM_BYTES = 227 * 1024            # opt-in dynamic shared memory per CTA on sm_100
-SMEM_RESERVE = 1024                # static shared memory + slack
+SMEM_RESERVE = 2048                # static shared memory (tile claim counters, mbarriers) + slack
+
+
+MAX_TILES = 256                    # csrc/sim_kernels.cu kMaxTiles
 
 
 def plan_tiles(n_words: int, n_local: int, n_sms: int) -> tuple[int, int, bool]:
     """(n_tiles, tile_words, partials_in_global) for a shard.
 
-    One tile if the whole bitmap fits in shared memory.  Otherwise the per-row
-    partial sums of a CTA's rows share the shared memory with the tile; when
-    they would take more than a quarter of it (very large shards) they move to
-    the global `acc` array instead (one extra 8-byte read-modify-write per row
-    and tile).
+    One tile if the whole bitmap fits in shared memory.  Otherwise the tiled
+    kernel double-buffers tiles (two buffers of ``tile_words``), next to the
+    per-row partial sums of a CTA's rows; when those would take more than a
+    quarter of shared memory (very large shards) they move to the global `acc`
+    array instead (one extra integer reduction per row and tile).
     """
     budget_all = SMEM_BYTES - SMEM_RESERVE
     whole = (n_words + 3) // 4 * 4
@@ -43,8 +52,11 @@ def plan_tiles(n_words: int, n_local: int, n_sms: int) -> tuple[int, int, bool]:
     part = per * 32 * 4
     global_part = part > budget_all // 4
     budget = budget_all - (0 if global_part else part)
-    tw = budget // 4 // 4 * 4
-    return (n_words + tw - 1) // tw, tw, global_part
+    tw = budget // 8 // 4 * 4
+    T = (n_words + tw - 1) // tw
+    if T > MAX_TILES:
+        raise ValueError(f"spike bitmap of {n_words} words needs {T} tiles (max {MAX_TILES})")
+    return T, tw, global_part
 
 
 def device_sms(device=None) -> int:
@@ -56,7 +68,7 @@ def device_sms(device=None) -> int:
 class SellCSR:
     """One shard's pull synapses on the device."""
 
-    slice_ptr: object      # torch int64 [n_slices*n_tiles + 1], uint4 units
+    slice_ptr: object      # torch int64 [n_slices*n_tiles + 1], J-SELL block starts, uint4 units
     row_meta: object       # torch int32 [n_local*n_tiles]: emid | (row slots << 16)
     syn: object            # torch int32 [4*slice_ptr[-1]] packed entries
     n_tiles: int
@@ -72,7 +84,8 @@ class SellCSR:
 
 
 def layout_from_counts(counts, n_local: int, n_tiles: int):
-    """slice_ptr, row_meta from per-(row, tile, sign) entry counts (torch or numpy int arrays)."""
+    """Padded SELL-32 block starts and row_meta from per-(row, tile, sign) entry
+    counts (torch or numpy int arrays); jagged_ptr(meta) gives the J-SELL starts."""
     xp = _xp(counts)
     c = counts.reshape(n_local, n_tiles, 2)
     e_slots = (c[:, :, 0] + 3) // 4
@@ -99,8 +112,61 @@ def layout_from_counts(counts, n_local: int, n_tiles: int):
     return ptr, meta
 
 
+def _block_lens(meta, n_local: int, n_tiles: int):
+    """Row slot counts as [n_blocks, 32] (block = slice * n_tiles + tile), numpy or torch."""
+    xp = _xp(meta)
+    n_slices = (n_local + 31) // 32
+    if xp == "np":
+        lens = np.zeros((n_slices * 32, n_tiles), dtype=np.int64)
+        lens[:n_local] = (np.asarray(meta).view(np.uint32) >> np.uint32(16)).astype(np.int64).reshape(n_local, n_tiles)
+        return lens.reshape(n_slices, 32, n_tiles).transpose(0, 2, 1).reshape(-1, 32)
+    torch = _torch()
+    lens = torch.zeros((n_slices * 32, n_tiles), dtype=torch.int64, device=meta.device)
+    lens[:n_local] = ((meta.to(torch.int64) & 0xFFFFFFFF) >> 16).reshape(n_local, n_tiles)
+    return lens.reshape(n_slices, 32, n_tiles).permute(0, 2, 1).reshape(-1, 32)
+
+
+def jagged_ptr(meta, n_local: int, n_tiles: int):
+    """J-SELL block starts (uint4 units, n_blocks + 1) from row_meta."""
+    lens = _block_lens(meta, n_local, n_tiles)
+    if _xp(meta) == "np":
+        out = np.zeros(lens.shape[0] + 1, dtype=np.int64)
+        out[1:] = np.cumsum(lens.sum(axis=1))
+        return out
+    torch = _torch()
+    out = torch.zeros(lens.shape[0] + 1, dtype=torch.int64, device=meta.device)
+    out[1:] = torch.cumsum(lens.sum(1), 0)
+    return out
+
+
+def padded_ptr(meta, n_local: int, n_tiles: int):
+    """Padded SELL-32 block starts (uint4 units): every block = longest row x 32."""
+    lens = _block_lens(meta, n_local, n_tiles)
+    if _xp(meta) == "np":
+        out = np.zeros(lens.shape[0] + 1, dtype=np.int64)
+        out[1:] = np.cumsum(lens.max(axis=1) * 32)
+        return out
+    torch = _torch()
+    out = torch.zeros(lens.shape[0] + 1, dtype=torch.int64, device=meta.device)
+    out[1:] = torch.cumsum(lens.max(1)[0] * 32, 0)
+    return out
+
+
+def jagged_gather(pptr: np.ndarray, meta: np.ndarray, n_local: int, n_tiles: int) -> np.ndarray:
+    """For every J-SELL slot (in storage order), its position in the padded form (uint4 units)."""
+    lens = _block_lens(meta, n_local, n_tiles)
+    hi = lens.max(axis=1)
+    n_pairs = int(hi.sum())
+    b_idx = np.repeat(np.arange(lens.shape[0], dtype=np.int64), hi)
+    u = np.arange(n_pairs, dtype=np.int64) - np.repeat(np.cumsum(hi) - hi, hi)
+    act = lens[b_idx] > u[:, None]                                     # [pairs, 32]
+    padded = np.asarray(pptr, dtype=np.int64)[b_idx][:, None] + u[:, None] * 32 + np.arange(32, dtype=np.int64)
+    return padded[act]                                                 # row-major = storage order
+
+
 def host_build(row, pre_internal, q, inh, n_local: int, n_tiles: int, tile_words: int):
-    """numpy SELL-32 arrays from a synapse list (row = local post, pre internal id, q, inhibitory)."""
+    """numpy J-SELL-32 arrays (slice_ptr, row_meta, syn) from a synapse list
+    (row = local post, pre internal id, q, inhibitory)."""
     row = np.asarray(row, dtype=np.int64)
     pre = np.asarray(pre_internal, dtype=np.int64)
     tile = (pre >> 5) // tile_words
@@ -108,12 +174,7 @@ def host_build(row, pre_internal, q, inh, n_local: int, n_tiles: int, tile_words
     counts = np.bincount(seg, minlength=n_local * n_tiles * 2).astype(np.int64)
     ptr, meta = layout_from_counts(counts, n_local, n_tiles)
     emid = meta & np.uint32(0xFFFF)
-    syn = np.zeros(int(ptr[-1]) * 4, dtype=np.uint32)
-    n_blocks = ptr.size - 1
-    for b in range(n_tiles if n_tiles > 1 else 0):  # pad = first id of the block's tile
-        pad = np.uint32(b * tile_words * 32)
-        for blk in range(b, n_blocks, n_tiles):
-            syn[ptr[blk] * 4: ptr[blk + 1] * 4] = pad
+    syn = np.zeros(int(ptr[-1]) * 4, dtype=np.uint32)   # pad entry 0: tile-relative id 0, q = 0
     order = np.argsort(seg, kind="stable")
     sseg = seg[order]
     first = np.cumsum(counts) - counts
@@ -122,16 +183,37 @@ def host_build(row, pre_internal, q, inh, n_local: int, n_tiles: int, tile_words
     t = (sseg // 2) % n_tiles
     slot = np.where(sseg % 2 == 1, emid.astype(np.int64)[r * n_tiles + t], 0) + k // 4
     pos = (ptr[(r // 32) * n_tiles + t] + slot * 32 + (r % 32)) * 4 + (k % 4)
-    syn[pos] = (np.asarray(q, dtype=np.uint32)[order] << np.uint32(ID_BITS)) | pre[order].astype(np.uint32)
-    return ptr, meta, syn
+    rel = pre[order] - (pre[order] >> 5) // tile_words * tile_words * 32     # tile-relative id
+    syn[pos] = (np.asarray(q, dtype=np.uint32)[order] << np.uint32(ID_BITS)) | rel.astype(np.uint32)
+    gather = jagged_gather(ptr, meta, n_local, n_tiles)
+    jsyn = syn.reshape(-1, 4)[gather].reshape(-1)
+    return jagged_ptr(meta, n_local, n_tiles), meta, jsyn
+
+
+def to_padded(csr: SellCSR):
+    """(padded_ptr, padded syn) of a SellCSR; slots past a row's length hold 0 (q = 0)."""
+    torch = _torch()
+    T, n_local = csr.n_tiles, csr.n_local
+    pptr = padded_ptr(csr.row_meta, n_local, T)
+    out = torch.zeros(max(int(pptr[-1].item()) * 4, 4), dtype=torch.int32, device=csr.syn.device)
+    if csr.syn.is_cuda:
+        from . import _native
+        _native.check(_native.lib().nc_sell_repack(pptr.data_ptr(), csr.slice_ptr.data_ptr(),
+                                                   csr.row_meta.data_ptr(), T, n_local, csr.syn.data_ptr(),
+                                                   out.data_ptr(), 0, _native.stream_handle(csr.syn.device)),
+                      "sell repack")
+    else:
+        g = jagged_gather(pptr.numpy(), csr.row_meta.numpy(), n_local, T)
+        out.view(-1, 4)[torch.from_numpy(g)] = csr.syn[: g.size * 4].view(-1, 4)
+    return pptr, out
 
 
 def decode(csr: SellCSR):
-    """Every real synapse of a device SellCSR as torch tensors (row_local, pre_internal, q, inh)."""
+    """Every real synapse of a SellCSR as torch tensors (row_local, pre_internal, q, inh)."""
     import torch
-    dev = csr.syn.device
+    ptr, syn = to_padded(csr)
+    dev = syn.device
     T = csr.n_tiles
-    ptr = csr.slice_ptr
     n_blocks = ptr.numel() - 1
     blen = (ptr[1:] - ptr[:-1]) // 32                                        # slots per block
     total = int(ptr[-1].item())
@@ -141,7 +223,7 @@ def decode(csr: SellCSR):
     u, lane = off // 32, off % 32
     s, t = blk_of // T, blk_of % T
     row = s * 32 + lane
-    ent = csr.syn[: total * 4].view(-1, 4).to(torch.int64) & 0xFFFFFFFF      # [total, 4]
+    ent = syn[: total * 4].view(-1, 4).to(torch.int64) & 0xFFFFFFFF          # [total, 4]
     valid_row = row < csr.n_local
     emid = torch.zeros_like(row)
     emid[valid_row] = (csr.row_meta.to(torch.int64) & 0xFFFF)[row[valid_row] * T + t[valid_row]]
@@ -150,7 +232,8 @@ def decode(csr: SellCSR):
     keep = (q > 0) & valid_row[:, None]
     rows4 = row[:, None].expand(-1, 4)[keep]
     inh4 = inh[:, None].expand(-1, 4)[keep]
-    return rows4, (ent & ID_MASK)[keep], q[keep], inh4
+    pre = (ent & ID_MASK) + (t * (csr.tile_words * 32))[:, None]             # back to internal ids
+    return rows4, pre[keep], q[keep], inh4
 
 
 def _xp(a):

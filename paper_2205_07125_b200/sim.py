@@ -327,8 +327,15 @@ class Network:
             _native.check(L.nc_graphgen_fill(C.byref(g), T, TW, ptr.data_ptr(), meta.data_ptr(), None,
                                              lower.data_ptr(), syn.data_ptr(), st), "graphgen fill")
             n_real = int(counts.sum().item())
-            del upper, counts
-            csr = ShardCSR(ptr, meta, syn, T, TW, n_local, n_real, partials_global=pglob)
+            del upper, counts, lower
+            # padded SELL-32 -> J-SELL-32 (drops the padding of every block to its longest row)
+            jptr = sell.jagged_ptr(meta, n_local, T)
+            jsyn = torch.empty(max(int(jptr[-1].item()) * 4, 4), dtype=torch.int32, device=dev)
+            _native.check(L.nc_sell_repack(ptr.data_ptr(), jptr.data_ptr(), meta.data_ptr(), T, n_local,
+                                           syn.data_ptr(), jsyn.data_ptr(), 1, st), "sell repack")
+            torch.cuda.synchronize(dev)
+            del syn, ptr
+            csr = ShardCSR(jptr, meta, jsyn, T, TW, n_local, n_real, partials_global=pglob)
             csr.dest = _dest_masks(csr, layout, h, dev)
             out[h] = csr
             nsyn += n_real
@@ -377,7 +384,8 @@ def _dest_masks(csr: ShardCSR, layout: ShardLayout, h: int, dev):
     bases = torch.from_numpy(layout.base.astype(np.int32)).to(dev)
     out16 = torch.zeros(max(n_local, 1), dtype=torch.int16, device=dev)
     L = _native.lib()
-    _native.check(L.nc_dest_mask_from_csr(csr.slice_ptr.data_ptr(), csr.n_tiles, csr.syn.data_ptr(), n_local,
+    _native.check(L.nc_dest_mask_from_csr(csr.slice_ptr.data_ptr(), csr.row_meta.data_ptr(), csr.n_tiles,
+                                          csr.tile_words, csr.syn.data_ptr(), n_local,
                                           bases.data_ptr(),
                                           layout.n_shards, h, out16.data_ptr(), _native.stream_handle(dev)),
                   "dest mask")

@@ -20,7 +20,7 @@ def test_host_build_round_trip(n_local, n_tiles, tile_words):
     q = rng.integers(1, 33, m)
     inh = rng.random(m) < 0.2
     ptr, meta, syn = sell.host_build(row, pre, q, inh, n_local, n_tiles, tile_words)
-    assert ptr[-1] * 4 == syn.size and (np.diff(ptr) % 32 == 0).all()
+    assert ptr[-1] * 4 == syn.size
     csr = sell.SellCSR(torch.from_numpy(ptr), torch.from_numpy(meta.view(np.int32)),
                        torch.from_numpy(syn.view(np.int32)), n_tiles, tile_words, n_local, m)
     r2, p2, q2, i2 = (x.numpy() for x in sell.decode(csr))
@@ -29,17 +29,41 @@ def test_host_build_round_trip(n_local, n_tiles, tile_words):
     a = a[np.lexsort(a.T[::-1])]
     b = b[np.lexsort(b.T[::-1])]
     np.testing.assert_array_equal(a, b)
-    # row lengths bound the real entries, blocks are as long as their longest row
+    # jagged blocks hold exactly their rows' slots; every row's slots hold its
+    # E entries, then its I entries, each segment padded to a multiple of 4
     lens = (meta >> np.uint32(16)).astype(np.int64).reshape(n_local, n_tiles)
+    emid = (meta & np.uint32(0xFFFF)).astype(np.int64).reshape(n_local, n_tiles)
     pad_rows = np.zeros(((n_local + 31) // 32 * 32, n_tiles), dtype=np.int64)
     pad_rows[:n_local] = lens
-    np.testing.assert_array_equal(pad_rows.reshape(-1, 32, n_tiles).max(axis=1).reshape(-1) * 32, np.diff(ptr))
-    # every entry of block (slice, t) references tile t
-    for blk in range(ptr.size - 1):
-        t = blk % n_tiles
-        ent = syn[ptr[blk] * 4: ptr[blk + 1] * 4]
-        ids = ent & np.uint32(sell.ID_MASK)
-        assert ((ids >> 5) // tile_words == t).all()
+    np.testing.assert_array_equal(pad_rows.reshape(-1, 32, n_tiles).sum(axis=1).reshape(-1), np.diff(ptr))
+    seg = (row * n_tiles + (pre >> 5) // tile_words) * 2 + inh
+    cnt = np.bincount(seg, minlength=n_local * n_tiles * 2).reshape(n_local, n_tiles, 2)
+    np.testing.assert_array_equal(emid, (cnt[:, :, 0] + 3) // 4)
+    np.testing.assert_array_equal(lens - emid, (cnt[:, :, 1] + 3) // 4)
+    # entries of a tile block hold ids relative to the tile (they index the staged copy)
+    ids = syn & np.uint32(sell.ID_MASK)
+    assert (ids < tile_words * 32).all()
+
+
+def test_jagged_positions_match_the_formula():
+    """position(u, l) = sum_{v<u} cnt_v + #{l' < l: len_l' > u} (include/neurocomm_b200.h)."""
+    rng = np.random.default_rng(3)
+    n_local, T = 70, 2
+    lens = rng.integers(0, 9, (n_local, T))
+    meta = (lens.astype(np.uint32) << np.uint32(16)).reshape(-1)
+    pptr = sell.padded_ptr(meta, n_local, T)
+    jptr = sell.jagged_ptr(meta, n_local, T)
+    g = sell.jagged_gather(pptr, meta, n_local, T)
+    assert g.size == jptr[-1] == lens.sum()
+    for b in range(jptr.size - 1):
+        s, t = divmod(b, T)
+        L = np.zeros(32, dtype=np.int64)
+        rows = np.arange(s * 32, min(s * 32 + 32, n_local))
+        L[: rows.size] = lens[rows, t]
+        for u in range(L.max(initial=0)):
+            for l in np.nonzero(L > u)[0]:
+                pos = sum(int((L > v).sum()) for v in range(u)) + int((L[:l] > u).sum())
+                assert g[jptr[b] + pos] == pptr[b] + u * 32 + l
 
 
 def test_plan_tiles():
@@ -47,9 +71,9 @@ def test_plan_tiles():
     T, tw, glob = sell.plan_tiles(312_500 + 1, 1_250_000, 148)    # 10 M neurons, 1.25 M local
     assert T > 1 and tw % 4 == 0 and T * tw >= 312_501 and not glob
     per = (1_250_000 // 32 + 147) // 148
-    assert tw * 4 + per * 128 <= sell.SMEM_BYTES - sell.SMEM_RESERVE
+    assert 2 * tw * 4 + per * 128 <= sell.SMEM_BYTES - sell.SMEM_RESERVE
     T, tw, glob = sell.plan_tiles(1_562_500 + 1, 12_500_000, 148)  # 50 M neurons, 12.5 M local
-    assert glob and T * tw >= 1_562_501 and tw * 4 <= sell.SMEM_BYTES - sell.SMEM_RESERVE
+    assert glob and T * tw >= 1_562_501 and 2 * tw * 4 <= sell.SMEM_BYTES - sell.SMEM_RESERVE
 
 
 def test_layout_from_counts_torch_matches_numpy():
