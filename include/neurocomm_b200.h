@@ -104,6 +104,13 @@ int nc_weight_histogram(const double* weights, const int64_t* assignment, int64_
  * 512-byte warp loads) and the block holds no padding beyond each E/I
  * segment rounded up to 4 entries (those hold the pad entry 0: tile-relative
  * id 0 with q = 0).  Each lane owns one row: no cross-lane reduction.
+ * Tiled placement: with n_tiles > 1, lane l of block (s, t) works on
+ * position p = 32s + l, which holds local row row_perm[t*n_local + p]
+ * (positions >= n_local hold no row).  Within the slices a CTA owns
+ * (s = c mod cta_groups) the rows are placed in descending order of their
+ * tile-t length, so the 32 rows of every block have near-equal lengths in
+ * every tile (the jagged tail stays short); row_meta is indexed by position:
+ * row_meta[p*n_tiles + t].  With one tile positions are rows.
  * Push entries (rows = internal pre ids):
  *     (inhibitory(pre) << 31) | ((q - 1) << 26) | post_local. */
 
@@ -167,6 +174,12 @@ typedef struct nc_shard {
   unsigned long long* spike_total; /* [1] running count of local spikes        */
   uint32_t* work;         /* [4] scratch counters (push work claims), zeroed by
                              nc_sim_init / nc_sim_end_step                      */
+  /* tiled layouts (n_tiles > 1): per-tile row placement, see the layout notes */
+  const int32_t* row_perm; /* [n_tiles][n_local]: local row at position p of
+                              tile t (NULL = identity)                          */
+  int32_t cta_groups;     /* G the placement was built for (CTA c owns slices
+                             c, c+G, ...); the tiled step launches G CTAs       */
+  int32_t pad2;
 } nc_shard_t;
 
 /* Set kernel attributes (dynamic shared memory opt-in) once; call before any
@@ -334,11 +347,11 @@ int nc_graphgen_count(const nc_graphgen_t* g, int32_t n_tiles, int32_t tile_word
 /* Pass 2 into the PADDED SELL-32 layout (every block = its longest row x 32
  * lanes, slot u of lane l at padded_ptr[block] + u*32 + l; padded_ptr and
  * row_meta computed by the host from the pass-1 counts); lower_fill
- * [n_local*n_tiles*2] zero-initialised (slot claims; lower_len is unused and
- * may be NULL).  syn must be pre-filled with nc_sell_fill_pads; convert the
+ * [n_local*n_tiles*2] zero-initialised (slot claims); pos_of[row*n_tiles + t]
+ * = position of the row in tile t (inverse of row_perm; NULL = identity).  syn must be pre-filled with nc_sell_fill_pads; convert the
  * result with nc_sell_repack. */
 int nc_graphgen_fill(const nc_graphgen_t* g, int32_t n_tiles, int32_t tile_words, const int64_t* slice_ptr,
-                     const uint32_t* row_meta, const int32_t* lower_len, int32_t* lower_fill, uint32_t* syn,
+                     const uint32_t* row_meta, const int32_t* pos_of, int32_t* lower_fill, uint32_t* syn,
                      void* stream);
 /* Pad pre-fill of a padded SELL-32 array: every entry = 0 (tile-relative id
  * 0, q = 0).  n_tiles / tile_words are accepted for ABI stability. */
@@ -347,10 +360,12 @@ int nc_sell_fill_pads(const int64_t* slice_ptr, int64_t n_blocks, int32_t n_tile
 /* Destination masks from a built CSR (the adjacency is symmetric, so the
  * pres of row r are exactly the posts r drives): dest_mask[r] = OR over the
  * row's entries of (1 << owner shard of the pre id) without `self`, where shard
- * h owns internal ids [shard_base[h], shard_base[h+1]) (device int32[n+1]). */
-int nc_dest_mask_from_csr(const int64_t* slice_ptr, const uint32_t* row_meta, int32_t n_tiles, int32_t tile_words,
-                          const uint32_t* syn, int32_t n_local, const int32_t* shard_base, int32_t n_shards,
-                          int32_t self, uint16_t* dest_mask, void* stream);
+ * h owns internal ids [shard_base[h], shard_base[h+1]) (device int32[n+1]).
+ * dest_mask must be zeroed and 4-byte aligned (rows are OR-ed in per tile). */
+int nc_dest_mask_from_csr(const int64_t* slice_ptr, const uint32_t* row_meta, const int32_t* row_perm,
+                          int32_t n_tiles, int32_t tile_words, const uint32_t* syn, int32_t n_local,
+                          const int32_t* shard_base, int32_t n_shards, int32_t self, uint16_t* dest_mask,
+                          void* stream);
 /* Padded SELL-32 (padded_ptr, as filled by nc_graphgen_fill) <-> J-SELL-32
  * (slice_ptr): to_jagged != 0 copies src (padded) into dst (jagged), else
  * the reverse (dst must be pre-filled; slots past a row's length are left

@@ -50,6 +50,7 @@ class ShardC(C.Structure):
         ("status", c_void_p), ("step", c_void_p),
         ("raster", c_void_p), ("record_steps", c_int32), ("local_words", c_int32),
         ("spike_total", c_void_p), ("work", c_void_p),
+        ("row_perm", c_void_p), ("cta_groups", c_int32), ("pad2", c_int32),
     ]
 
 
@@ -108,8 +109,8 @@ _SIGS = {
                                    c_void_p, c_void_p]),
     "nc_graphgen_degrees": (c_int32, [C.POINTER(GraphGenC), c_void_p, c_void_p]),
     "nc_sell_fill_pads": (c_int32, [c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p]),
-    "nc_dest_mask_from_csr": (c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_int32, c_void_p, c_int32,
-                                        c_int32, c_void_p, c_void_p]),
+    "nc_dest_mask_from_csr": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_int32, c_void_p,
+                                        c_int32, c_int32, c_void_p, c_void_p]),
     "nc_sell_repack": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_int32,
                                  c_void_p]),
     "nc_xchg_reset": (c_int32, [C.POINTER(XchgC), c_void_p]),

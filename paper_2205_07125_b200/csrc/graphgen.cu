@@ -163,19 +163,20 @@ __global__ void k_degrees(const nc_graphgen_t g, int32_t* deg) {
 }
 
 // Position of the k-th entry of (row, tile, sign) in the SELL-32 layout (uint32 units).
-__device__ __forceinline__ int64_t sell_pos(const int64_t* slice_ptr, const uint32_t* row_meta, int32_t T,
-                                            int64_t row, int64_t seg, int32_t k) {
+__device__ __forceinline__ int64_t sell_pos(const int64_t* slice_ptr, const uint32_t* row_meta,
+                                            const int32_t* pos_of, int32_t T, int64_t row, int64_t seg, int32_t k) {
   const int64_t t = (seg >> 1) - row * T;
-  const int64_t blk = slice_ptr[(row >> 5) * T + t];
-  const int64_t slot = ((seg & 1) ? (int64_t)(row_meta[row * T + t] & 0xFFFFu) : 0) + (k >> 2);
-  return (blk + slot * 32 + (row & 31)) * 4 + (k & 3);
+  const int64_t p = pos_of ? (int64_t)pos_of[row * T + t] : row;   // position of the row in tile t
+  const int64_t blk = slice_ptr[(p >> 5) * T + t];
+  const int64_t slot = ((seg & 1) ? (int64_t)(row_meta[p * T + t] & 0xFFFFu) : 0) + (k >> 2);
+  return (blk + slot * 32 + (p & 31)) * 4 + (k & 3);
 }
 
 // Pass 2: regenerate the same edges and place them; slots inside a
 // (row, tile, sign) segment are claimed with atomics (any order is fine:
 // delivery sums integers).
 __global__ void k_fill(const nc_graphgen_t g, int32_t T, int32_t TW, const int64_t* slice_ptr,
-                       const uint32_t* row_meta, int32_t* fill, uint32_t* syn) {
+                       const uint32_t* row_meta, const int32_t* pos_of, int32_t* fill, uint32_t* syn) {
   const Comm cm = make_comm(g);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n_neurons;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -191,13 +192,13 @@ __global__ void k_fill(const nc_graphgen_t g, int32_t T, int32_t TW, const int64
       if (mine) {
         const int64_t seg = seg_index(ri, T, TW, jid, is_inh(g, j));
         const int32_t k = atomicAdd(fill + seg, 1);
-        syn[sell_pos(slice_ptr, row_meta, T, ri, seg, k)] = pack(jid - tile_base(jid, TW), q);
+        syn[sell_pos(slice_ptr, row_meta, pos_of, T, ri, seg, k)] = pack(jid - tile_base(jid, TW), q);
       }
       if (jm) {
         const int64_t rj = (int64_t)jid - g.local_base;
         const int64_t seg = seg_index(rj, T, TW, iid, inh_i);
         const int32_t k = atomicAdd(fill + seg, 1);
-        syn[sell_pos(slice_ptr, row_meta, T, rj, seg, k)] = pack(iid - tile_base(iid, TW), q);
+        syn[sell_pos(slice_ptr, row_meta, pos_of, T, rj, seg, k)] = pack(iid - tile_base(iid, TW), q);
       }
     });
   }
@@ -211,37 +212,42 @@ __global__ void k_fill_pads(const int64_t* slice_ptr, int64_t n_blocks, uint32_t
     for (int64_t k = slice_ptr[b] + threadIdx.x; k < slice_ptr[b + 1]; k += blockDim.x) s4[k] = make_uint4(0, 0, 0, 0);
 }
 
-// Destination shards of every local row: warp per slice, lane = row, over the
-// row's entries in every tile block (J-SELL order, pads have q = 0).
-__global__ void k_dest_mask(const int64_t* slice_ptr, const uint32_t* row_meta, int32_t T, int32_t tile_words,
-                            const uint32_t* syn, int32_t n_local, const int32_t* shard_base, int32_t n_shards, int32_t self,
-                            uint16_t* dest) {
+// Destination shards of every local row: warp per (slice, tile) block, lane =
+// position (row_perm places rows per tile), OR-ed into the row's 16-bit mask
+// through the aligned 32-bit word holding it.  Pads have q = 0.
+__global__ void k_dest_mask(const int64_t* slice_ptr, const uint32_t* row_meta, const int32_t* row_perm, int32_t T,
+                            int32_t tile_words, const uint32_t* syn, int32_t n_local, const int32_t* shard_base,
+                            int32_t n_shards, int32_t self, uint16_t* dest) {
   const int lane = threadIdx.x & 31;
   const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t n_slices = (n_local + 31) >> 5;
-  for (int64_t s = wid; s < n_slices; s += nw) {
-    const int64_t r = (s << 5) + lane;
+  const int64_t n_blocks = ((int64_t)(n_local + 31) >> 5) * T;
+  for (int64_t b = wid; b < n_blocks; b += nw) {
+    const int64_t s = b / T, t = b % T;
+    const int64_t p = (s << 5) + lane;
+    const int64_t b0 = slice_ptr[b];
+    const int64_t tbase = t * tile_words * 32;
+    const int mine = p < n_local ? (int)(row_meta[p * T + t] >> 16) : 0;
+    const int hi = (int)__reduce_max_sync(0xffffffffu, (unsigned)mine);
     uint32_t m = 0;
-    for (int32_t t = 0; t < T; ++t) {
-      const int64_t b0 = slice_ptr[s * T + t];
-      const int64_t tbase = (int64_t)t * tile_words * 32;
-      const int mine = r < n_local ? (int)(row_meta[r * T + t] >> 16) : 0;
-      const int hi = (int)__reduce_max_sync(0xffffffffu, (unsigned)mine);
-      int off = 0;
-      for (int u = 0; u < hi; ++u) {
-        const int pos = ncdev::jsell_pos(u, mine, lane, off);
-        if (u >= mine) continue;
-        for (int c = 0; c < 4; ++c) {
-          const uint32_t e = syn[(b0 + pos) * 4 + c];
-          if ((e >> 26) == 0) continue;  // pad
-          const int64_t pre = (e & 0x03FFFFFFu) + tbase;
-          for (int h = 0; h < n_shards; ++h)
-            if (pre >= shard_base[h] && pre < shard_base[h + 1]) m |= 1u << h;
-        }
+    int off = 0;
+    for (int u = 0; u < hi; ++u) {
+      const int pos = ncdev::jsell_pos(u, mine, lane, off);
+      if (u >= mine) continue;
+      for (int c = 0; c < 4; ++c) {
+        const uint32_t e = syn[(b0 + pos) * 4 + c];
+        if ((e >> 26) == 0) continue;  // pad
+        const int64_t pre = (e & 0x03FFFFFFu) + tbase;
+        for (int h = 0; h < n_shards; ++h)
+          if (pre >= shard_base[h] && pre < shard_base[h + 1]) m |= 1u << h;
       }
     }
-    if (r < n_local) dest[r] = (uint16_t)(m & ~(1u << self));
+    m &= ~(1u << self);
+    if (p < n_local && m) {
+      const int64_t r = row_perm ? row_perm[t * n_local + p] : p;
+      unsigned int* w = reinterpret_cast<unsigned int*>(dest + (r & ~1ll));
+      atomicOr(w, m << (16 * (r & 1)));
+    }
   }
 }
 
@@ -304,15 +310,14 @@ extern "C" int nc_graphgen_degrees(const nc_graphgen_t* g, int32_t* deg, void* s
 }
 
 extern "C" int nc_graphgen_fill(const nc_graphgen_t* g, int32_t n_tiles, int32_t tile_words, const int64_t* slice_ptr,
-                                const uint32_t* row_meta, const int32_t* lower_len, int32_t* lower_fill, uint32_t* syn,
+                                const uint32_t* row_meta, const int32_t* pos_of, int32_t* lower_fill, uint32_t* syn,
                                 void* stream) {
-  (void)lower_len;
   if (!g || n_tiles < 1 || tile_words < 1) {
     nc_set_error("nc_graphgen_fill: bad arguments");
     return NC_E_ARG;
   }
   k_fill<<<grid_for(g->n_neurons, 128), 128, 0, (cudaStream_t)stream>>>(*g, n_tiles, tile_words, slice_ptr,
-                                                                          row_meta, lower_fill, syn);
+                                                                          row_meta, pos_of, lower_fill, syn);
   NC_LAUNCH_CHECK();
   return NC_OK;
 }
@@ -344,8 +349,8 @@ extern "C" int nc_sell_repack(const int64_t* padded_ptr, const int64_t* slice_pt
   return NC_OK;
 }
 
-extern "C" int nc_dest_mask_from_csr(const int64_t* slice_ptr, const uint32_t* row_meta, int32_t n_tiles,
-                                     int32_t tile_words, const uint32_t* syn, int32_t n_local, const int32_t* shard_base,
+extern "C" int nc_dest_mask_from_csr(const int64_t* slice_ptr, const uint32_t* row_meta, const int32_t* row_perm,
+                                     int32_t n_tiles, int32_t tile_words, const uint32_t* syn, int32_t n_local, const int32_t* shard_base,
                                      int32_t n_shards, int32_t self, uint16_t* dest_mask, void* stream) {
   if (n_shards < 1 || n_shards > NC_MAX_SHARDS) {
     nc_set_error("nc_dest_mask_from_csr: n_shards must be in [1, %d]", NC_MAX_SHARDS);
@@ -353,7 +358,7 @@ extern "C" int nc_dest_mask_from_csr(const int64_t* slice_ptr, const uint32_t* r
   }
   if (n_local == 0) return NC_OK;
   k_dest_mask<<<grid_for((int64_t)n_local * 32, 256), 256, 0, (cudaStream_t)stream>>>(
-      slice_ptr, row_meta, n_tiles, tile_words, syn, n_local, shard_base, n_shards, self, dest_mask);
+      slice_ptr, row_meta, row_perm, n_tiles, tile_words, syn, n_local, shard_base, n_shards, self, dest_mask);
   NC_LAUNCH_CHECK();
   return NC_OK;
 }

@@ -132,9 +132,9 @@ k_step_fused(const nc_shard_t sh, const nc_lif_params_t p) {
         if (lane == 0) j = atomicAdd(&next_slice[t], 1);
         j = __shfl_sync(kFull, j, 0);
         if (j < cnt) {
-          const int r = ((c + j * G) << 5) + lane;
+          const int pos = ((c + j * G) << 5) + lane;
           b0 = sh.slice_ptr[(int64_t)(c + j * G) * T + t];
-          m = r < sh.n_local ? sh.row_meta[(int64_t)r * T + t] : 0u;
+          m = pos < sh.n_local ? sh.row_meta[(int64_t)pos * T + t] : 0u;
           if (kPfTiled > 0 && lane == 0) prefetch_l2(syn4 + b0, kPfTiled * 512u);
         }
         return j;
@@ -146,10 +146,14 @@ k_step_fused(const nc_shard_t sh, const nc_lif_params_t p) {
         int64_t b0n = 0;
         uint32_t metan = 0u;
         const int jn = claim(b0n, metan);
-        const int row = ((c + j * G) << 5) + lane;
+        const int pos = ((c + j * G) << 5) + lane;
+        // the row at this position in tile t (rows stay inside the CTA's slices)
+        const int row = (pos < sh.n_local && sh.row_perm) ? sh.row_perm[(int64_t)t * sh.n_local + pos] : pos;
         const int32_t sum = sell_row_sum<kPfTiled>(syn4 + b0, meta, bm, g_inh, lane, 0u);
-        if (!pglob) atomicAdd(&spart[j * 32 + lane], sum);
-        else if (row < sh.n_local) red_add(&sh.acc[row], sum);
+        if (row < sh.n_local) {
+          if (!pglob) atomicAdd(&spart[(((row >> 5) - c) / G) * 32 + (row & 31)], sum);
+          else red_add(&sh.acc[row], sum);
+        }
         j = jn;
         b0 = b0n;
         meta = metan;
@@ -261,7 +265,8 @@ size_t step_smem_bytes(const nc_shard_t& sh, int grid) {
 
 template <bool kLif>
 int launch_step(const nc_shard_t& sh, const nc_lif_params_t& p, cudaStream_t st) {
-  const int grid = num_sms();
+  // tiled: the row placement was built for cta_groups CTAs (sh.row_perm)
+  const int grid = sh.n_tiles > 1 ? sh.cta_groups : num_sms();
   const size_t smem = step_smem_bytes(sh, grid);
   if (smem > (size_t)g_max_dyn_smem) {
     nc_set_error("step kernel needs %zu B of shared memory (tile_words=%d): re-tile the network", smem,
@@ -280,6 +285,7 @@ int check_shard(const nc_shard_t* sh) {
   if (!sh || sh->n_local < 0 || sh->n_words < 1 || (sh->local_base & 31) || !sh->step ||
       !sh->status || !sh->bitmap0 || !sh->bitmap1 || sh->n_tiles < 1 ||
       (sh->n_tiles > 1 && (sh->tile_words < 4 || (sh->tile_words & 3) || sh->n_tiles > kMaxTiles ||
+                           sh->cta_groups < 1 ||
                            (int64_t)sh->tile_words * sh->n_tiles < sh->n_words)) ||
       ((sh->flags & 1) && !sh->acc)) {
     nc_set_error("invalid nc_shard_t");
@@ -395,9 +401,10 @@ __global__ void k_push_build(const nc_shard_t sh, int phase, int64_t* rowptr, in
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t blk = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; blk < n_blocks; blk += nw) {
     const int slice = (int)(blk / T), t = (int)(blk % T);
-    const int row = (slice << 5) + lane;
+    const int pos = (slice << 5) + lane;
+    const int row = (pos < sh.n_local && sh.row_perm) ? sh.row_perm[(int64_t)t * sh.n_local + pos] : pos;
     const int64_t b0 = sh.slice_ptr[blk];
-    const uint32_t meta = row < sh.n_local ? sh.row_meta[(int64_t)row * T + t] : 0u;
+    const uint32_t meta = pos < sh.n_local ? sh.row_meta[(int64_t)pos * T + t] : 0u;
     const int emid = (int)(meta & 0xFFFFu), mine = (int)(meta >> 16);
     const int hi = (int)__reduce_max_sync(0xffffffffu, (unsigned)mine);
     int off = 0;

@@ -77,17 +77,73 @@ class SellCSR:
     n_real: int            # real (non-pad) synapses
     dest: object = None    # torch int32 [n_local]: shards hosting targets of each row
     partials_global: bool = False
+    row_perm: object = None  # torch int32 [n_tiles*n_local]: row at position p of tile t (None = identity)
+    cta_groups: int = 1      # CTAs the tiled placement was built for
 
     @property
     def n_entries(self) -> int:
         return int(self.syn.numel())
 
 
-def layout_from_counts(counts, n_local: int, n_tiles: int):
-    """Padded SELL-32 block starts and row_meta from per-(row, tile, sign) entry
-    counts (torch or numpy int arrays); jagged_ptr(meta) gives the J-SELL starts."""
+def tile_placement(lens, n_local: int, n_tiles: int, cta_groups: int):
+    """Per-tile row placement for tiled layouts (include/neurocomm_b200.h).
+
+    ``lens``: [n_local, n_tiles] slots of every row in every tile (numpy or
+    torch).  Within the positions CTA c owns (slices s = c mod cta_groups, in
+    slice then lane order) the rows of those same slices are placed in
+    descending order of their tile-t length.  Returns (perm [n_tiles, n_local]
+    position -> row, pos_of [n_local, n_tiles] row -> position), or
+    (None, None) for one tile."""
+    if n_tiles == 1:
+        return None, None
+    G = int(cta_groups)
+    if _xp(lens) == "np":
+        rows = np.arange(n_local, dtype=np.int64)
+        cta = (rows >> 5) % G
+        perm = np.empty((n_tiles, n_local), dtype=np.int32)
+        pos_of = np.empty((n_local, n_tiles), dtype=np.int32)
+        order_pos = np.lexsort((rows, cta))
+        for t in range(n_tiles):
+            order_rows = np.lexsort((rows, -np.asarray(lens[:, t], dtype=np.int64), cta))
+            perm[t, order_pos] = order_rows
+            pos_of[order_rows, t] = order_pos
+        return perm, pos_of
+    torch = _torch()
+    dev = lens.device
+    rows = torch.arange(n_local, dtype=torch.int64, device=dev)
+    cta = (rows >> 5) % G
+    lens = lens.to(torch.int64)
+    span = int(lens.max().item()) + 1 if lens.numel() else 1
+    perm = torch.empty((n_tiles, n_local), dtype=torch.int32, device=dev)
+    pos_of = torch.empty((n_local, n_tiles), dtype=torch.int32, device=dev)
+    order_pos = torch.argsort(cta * n_local + rows)
+    for t in range(n_tiles):
+        key = (cta * span + (span - 1 - lens[:, t])) * n_local + rows
+        order_rows = torch.argsort(key)
+        perm[t, order_pos] = order_rows.to(torch.int32)
+        pos_of[order_rows, t] = order_pos.to(torch.int32)
+    return perm, pos_of
+
+
+def row_slots(counts, n_local: int, n_tiles: int):
+    """[n_local, n_tiles] slots per row and tile from per-(row, tile, sign) entry counts."""
+    c = counts.reshape(n_local, n_tiles, 2)
+    return (c[:, :, 0] + 3) // 4 + (c[:, :, 1] + 3) // 4
+
+
+def layout_from_counts(counts, n_local: int, n_tiles: int, perm=None):
+    """Padded SELL-32 block starts and (position-indexed) row_meta from
+    per-(row, tile, sign) entry counts (torch or numpy int arrays) and the
+    tile placement `perm` (None = identity); jagged_ptr(meta) gives the J-SELL
+    starts."""
     xp = _xp(counts)
     c = counts.reshape(n_local, n_tiles, 2)
+    if perm is not None:   # to position order: c[p, t] = counts of the row placed at p in tile t
+        if xp == "np":
+            c = c[np.asarray(perm, dtype=np.int64).T, np.arange(n_tiles)[None, :]]
+        else:
+            torch = _torch()
+            c = c[perm.to(torch.int64).T, torch.arange(n_tiles, device=c.device)[None, :]]
     e_slots = (c[:, :, 0] + 3) // 4
     i_slots = (c[:, :, 1] + 3) // 4
     row_slots = e_slots + i_slots
@@ -164,15 +220,17 @@ def jagged_gather(pptr: np.ndarray, meta: np.ndarray, n_local: int, n_tiles: int
     return padded[act]                                                 # row-major = storage order
 
 
-def host_build(row, pre_internal, q, inh, n_local: int, n_tiles: int, tile_words: int):
-    """numpy J-SELL-32 arrays (slice_ptr, row_meta, syn) from a synapse list
-    (row = local post, pre internal id, q, inhibitory)."""
+def host_build(row, pre_internal, q, inh, n_local: int, n_tiles: int, tile_words: int, cta_groups: int = 148):
+    """numpy J-SELL-32 arrays (slice_ptr, row_meta, syn, row_perm) from a synapse
+    list (row = local post, pre internal id, q, inhibitory).  row_perm is the
+    flattened [n_tiles, n_local] tile placement, None for one tile."""
     row = np.asarray(row, dtype=np.int64)
     pre = np.asarray(pre_internal, dtype=np.int64)
     tile = (pre >> 5) // tile_words
     seg = (row * n_tiles + tile) * 2 + np.asarray(inh, dtype=np.int64)
     counts = np.bincount(seg, minlength=n_local * n_tiles * 2).astype(np.int64)
-    ptr, meta = layout_from_counts(counts, n_local, n_tiles)
+    perm, pos_of = tile_placement(row_slots(counts, n_local, n_tiles), n_local, n_tiles, cta_groups)
+    ptr, meta = layout_from_counts(counts, n_local, n_tiles, perm)
     emid = meta & np.uint32(0xFFFF)
     syn = np.zeros(int(ptr[-1]) * 4, dtype=np.uint32)   # pad entry 0: tile-relative id 0, q = 0
     order = np.argsort(seg, kind="stable")
@@ -181,13 +239,14 @@ def host_build(row, pre_internal, q, inh, n_local: int, n_tiles: int, tile_words
     k = np.arange(sseg.size, dtype=np.int64) - first[sseg]
     r = sseg // 2 // n_tiles
     t = (sseg // 2) % n_tiles
-    slot = np.where(sseg % 2 == 1, emid.astype(np.int64)[r * n_tiles + t], 0) + k // 4
-    pos = (ptr[(r // 32) * n_tiles + t] + slot * 32 + (r % 32)) * 4 + (k % 4)
+    p = r if pos_of is None else pos_of[r, t].astype(np.int64)           # position of the row in tile t
+    slot = np.where(sseg % 2 == 1, emid.astype(np.int64)[p * n_tiles + t], 0) + k // 4
+    pos = (ptr[(p // 32) * n_tiles + t] + slot * 32 + (p % 32)) * 4 + (k % 4)
     rel = pre[order] - (pre[order] >> 5) // tile_words * tile_words * 32     # tile-relative id
     syn[pos] = (np.asarray(q, dtype=np.uint32)[order] << np.uint32(ID_BITS)) | rel.astype(np.uint32)
     gather = jagged_gather(ptr, meta, n_local, n_tiles)
     jsyn = syn.reshape(-1, 4)[gather].reshape(-1)
-    return jagged_ptr(meta, n_local, n_tiles), meta, jsyn
+    return jagged_ptr(meta, n_local, n_tiles), meta, jsyn, (None if perm is None else perm.reshape(-1))
 
 
 def to_padded(csr: SellCSR):
@@ -222,11 +281,14 @@ def decode(csr: SellCSR):
     off = torch.arange(total, device=dev, dtype=torch.int64) - ptr[:-1][blk_of]
     u, lane = off // 32, off % 32
     s, t = blk_of // T, blk_of % T
-    row = s * 32 + lane
+    pos = s * 32 + lane                                                     # position in its tile
     ent = syn[: total * 4].view(-1, 4).to(torch.int64) & 0xFFFFFFFF          # [total, 4]
-    valid_row = row < csr.n_local
-    emid = torch.zeros_like(row)
-    emid[valid_row] = (csr.row_meta.to(torch.int64) & 0xFFFF)[row[valid_row] * T + t[valid_row]]
+    valid_row = pos < csr.n_local
+    emid = torch.zeros_like(pos)
+    emid[valid_row] = (csr.row_meta.to(torch.int64) & 0xFFFF)[pos[valid_row] * T + t[valid_row]]
+    row = pos.clone()
+    if csr.row_perm is not None:
+        row[valid_row] = csr.row_perm.to(torch.int64)[t[valid_row] * csr.n_local + pos[valid_row]]
     inh = (u >= emid)
     q = ent >> ID_BITS
     keep = (q > 0) & valid_row[:, None]

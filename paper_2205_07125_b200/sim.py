@@ -197,8 +197,8 @@ class ShardLayout:
 # ---------------------------------------------------------------- network
 
 def host_sell(graph: NeuronGraph, layout: ShardLayout, shard: int, inh_every: int, n_tiles: int,
-              tile_words: int):
-    """SELL-32 arrays of one shard from a host NeuronGraph (numpy; see sell.py)."""
+              tile_words: int, cta_groups: int = 148):
+    """J-SELL-32 arrays (ptr, meta, syn, row_perm) of one shard from a host NeuronGraph (numpy; see sell.py)."""
     q = q_from_p(graph.edge_p)
     post = np.concatenate([graph.edge_j, graph.edge_i]).astype(np.int64)
     pre = np.concatenate([graph.edge_i, graph.edge_j]).astype(np.int64)
@@ -207,7 +207,7 @@ def host_sell(graph: NeuronGraph, layout: ShardLayout, shard: int, inh_every: in
     post, pre, qq = post[keep], pre[keep], qq[keep]
     row = layout.internal_id[post].astype(np.int64) - int(layout.base[shard])
     return sell.host_build(row, layout.internal_id[pre], qq, inhibitory_mask(pre, inh_every),
-                           layout.n_local(shard), n_tiles, tile_words)
+                           layout.n_local(shard), n_tiles, tile_words, cta_groups)
 
 
 @dataclass
@@ -263,11 +263,12 @@ class Network:
         for h in own:
             n_local = layout.n_local(h)
             T, TW, pglob = _tiles(layout, n_local, sms, tile_words, partials_global)
-            ptr, meta, syn = host_sell(graph, layout, h, inh_every, T, TW)
+            ptr, meta, syn, perm = host_sell(graph, layout, h, inh_every, T, TW, sms)
             n_real = int(np.count_nonzero((syn >> np.uint32(ID_BITS)) > 0))
             csr = ShardCSR(torch.from_numpy(ptr).to(dev), torch.from_numpy(meta.view(np.int32)).to(dev),
                            torch.from_numpy(syn.view(np.int32)).to(dev), T, TW, n_local, n_real,
-                           partials_global=pglob)
+                           partials_global=pglob,
+                           row_perm=None if perm is None else torch.from_numpy(perm).to(dev), cta_groups=sms)
             csr.dest = _dest_masks(csr, layout, h, dev)
             out[h] = csr
             nsyn += n_real
@@ -318,13 +319,16 @@ class Network:
             _native.check(L.nc_graphgen_count(C.byref(g), T, TW, lower.data_ptr(), upper.data_ptr(), st),
                           "graphgen count")
             counts = (lower + upper)[: n_local * T * 2].to(torch.int64)
-            ptr, meta = sell.layout_from_counts(counts, n_local, T)
+            perm, pos_of = sell.tile_placement(sell.row_slots(counts, n_local, T), n_local, T, sms)
+            ptr, meta = sell.layout_from_counts(counts, n_local, T, perm)
             total = int(ptr[-1].item())
             syn = torch.zeros(max(total * 4, 4), dtype=torch.int32, device=dev)
             _native.check(L.nc_sell_fill_pads(ptr.data_ptr(), ptr.numel() - 1, T, TW, syn.data_ptr(), st),
                           "sell pads")
             lower.zero_()
-            _native.check(L.nc_graphgen_fill(C.byref(g), T, TW, ptr.data_ptr(), meta.data_ptr(), None,
+            pos_of = None if pos_of is None else pos_of.contiguous()
+            _native.check(L.nc_graphgen_fill(C.byref(g), T, TW, ptr.data_ptr(), meta.data_ptr(),
+                                             None if pos_of is None else pos_of.data_ptr(),
                                              lower.data_ptr(), syn.data_ptr(), st), "graphgen fill")
             n_real = int(counts.sum().item())
             del upper, counts, lower
@@ -334,8 +338,9 @@ class Network:
             _native.check(L.nc_sell_repack(ptr.data_ptr(), jptr.data_ptr(), meta.data_ptr(), T, n_local,
                                            syn.data_ptr(), jsyn.data_ptr(), 1, st), "sell repack")
             torch.cuda.synchronize(dev)
-            del syn, ptr
-            csr = ShardCSR(jptr, meta, jsyn, T, TW, n_local, n_real, partials_global=pglob)
+            del syn, ptr, pos_of
+            csr = ShardCSR(jptr, meta, jsyn, T, TW, n_local, n_real, partials_global=pglob,
+                           row_perm=None if perm is None else perm.reshape(-1).contiguous(), cta_groups=sms)
             csr.dest = _dest_masks(csr, layout, h, dev)
             out[h] = csr
             nsyn += n_real
@@ -382,9 +387,10 @@ def _dest_masks(csr: ShardCSR, layout: ShardLayout, h: int, dev):
     import torch
     n_local = layout.n_local(h)
     bases = torch.from_numpy(layout.base.astype(np.int32)).to(dev)
-    out16 = torch.zeros(max(n_local, 1), dtype=torch.int16, device=dev)
+    out16 = torch.zeros(n_local + 2, dtype=torch.int16, device=dev)   # OR-ed through aligned 32-bit words
     L = _native.lib()
-    _native.check(L.nc_dest_mask_from_csr(csr.slice_ptr.data_ptr(), csr.row_meta.data_ptr(), csr.n_tiles,
+    _native.check(L.nc_dest_mask_from_csr(csr.slice_ptr.data_ptr(), csr.row_meta.data_ptr(),
+                                          None if csr.row_perm is None else csr.row_perm.data_ptr(), csr.n_tiles,
                                           csr.tile_words, csr.syn.data_ptr(), n_local,
                                           bases.data_ptr(),
                                           layout.n_shards, h, out16.data_ptr(), _native.stream_handle(dev)),
@@ -539,7 +545,8 @@ class _ShardState:
             bucket_cap=self.bucket_cap, status=self.status.data_ptr(), step=self.step.data_ptr(),
             raster=self.raster.data_ptr() if self.record_steps > 0 else None,
             record_steps=self.record_steps, local_words=self.local_words,
-            spike_total=self.spike_total.data_ptr(), work=self.work.data_ptr())
+            spike_total=self.spike_total.data_ptr(), work=self.work.data_ptr(),
+            row_perm=None if csr.row_perm is None else csr.row_perm.data_ptr(), cta_groups=csr.cta_groups)
 
 
 def _push_csr(csr: ShardCSR, lay: ShardLayout, h: int, dev):
@@ -558,7 +565,9 @@ def _push_csr(csr: ShardCSR, lay: ShardLayout, h: int, dev):
                        n_words=lay.n_words, n_tiles=csr.n_tiles, tile_words=csr.tile_words, flags=0,
                        slice_ptr=csr.slice_ptr.data_ptr(), row_meta=csr.row_meta.data_ptr(), syn=csr.syn.data_ptr(),
                        bitmap0=scratch.data_ptr(), bitmap1=scratch.data_ptr(), status=scratch.data_ptr(),
-                       step=scratch.data_ptr())
+                       step=scratch.data_ptr(),
+                       row_perm=None if csr.row_perm is None else csr.row_perm.data_ptr(),
+                       cta_groups=csr.cta_groups)
     rowptr = torch.zeros(n_rows + 1, dtype=torch.int64, device=dev)
     _native.check(L.nc_build_push_csr(C.byref(c), 0, rowptr.data_ptr(), None, None, st), "push csr count")
     torch.cumsum(rowptr, 0, out=rowptr)

@@ -19,27 +19,38 @@ def test_host_build_round_trip(n_local, n_tiles, tile_words):
     pre = rng.integers(0, n_ids, m)
     q = rng.integers(1, 33, m)
     inh = rng.random(m) < 0.2
-    ptr, meta, syn = sell.host_build(row, pre, q, inh, n_local, n_tiles, tile_words)
+    ptr, meta, syn, perm = sell.host_build(row, pre, q, inh, n_local, n_tiles, tile_words, cta_groups=2)
     assert ptr[-1] * 4 == syn.size
     csr = sell.SellCSR(torch.from_numpy(ptr), torch.from_numpy(meta.view(np.int32)),
-                       torch.from_numpy(syn.view(np.int32)), n_tiles, tile_words, n_local, m)
+                       torch.from_numpy(syn.view(np.int32)), n_tiles, tile_words, n_local, m,
+                       row_perm=None if perm is None else torch.from_numpy(perm), cta_groups=2)
     r2, p2, q2, i2 = (x.numpy() for x in sell.decode(csr))
     a = np.stack([row, pre, q, inh]).T
     b = np.stack([r2, p2, q2, i2]).T
     a = a[np.lexsort(a.T[::-1])]
     b = b[np.lexsort(b.T[::-1])]
     np.testing.assert_array_equal(a, b)
-    # jagged blocks hold exactly their rows' slots; every row's slots hold its
+    # jagged blocks hold exactly their positions' slots; every row's slots hold its
     # E entries, then its I entries, each segment padded to a multiple of 4
-    lens = (meta >> np.uint32(16)).astype(np.int64).reshape(n_local, n_tiles)
+    perm2 = np.tile(np.arange(n_local), (n_tiles, 1)) if perm is None else perm.reshape(n_tiles, n_local)
+    lens = (meta >> np.uint32(16)).astype(np.int64).reshape(n_local, n_tiles)       # by position
     emid = (meta & np.uint32(0xFFFF)).astype(np.int64).reshape(n_local, n_tiles)
     pad_rows = np.zeros(((n_local + 31) // 32 * 32, n_tiles), dtype=np.int64)
     pad_rows[:n_local] = lens
     np.testing.assert_array_equal(pad_rows.reshape(-1, 32, n_tiles).sum(axis=1).reshape(-1), np.diff(ptr))
     seg = (row * n_tiles + (pre >> 5) // tile_words) * 2 + inh
     cnt = np.bincount(seg, minlength=n_local * n_tiles * 2).reshape(n_local, n_tiles, 2)
-    np.testing.assert_array_equal(emid, (cnt[:, :, 0] + 3) // 4)
-    np.testing.assert_array_equal(lens - emid, (cnt[:, :, 1] + 3) // 4)
+    for t in range(n_tiles):
+        r = perm2[t]
+        np.testing.assert_array_equal(emid[:, t], (cnt[r, t, 0] + 3) // 4)
+        np.testing.assert_array_equal(lens[:, t] - emid[:, t], (cnt[r, t, 1] + 3) // 4)
+        # placement: a permutation that keeps every row inside its CTA's slices,
+        # in descending tile-t length within each CTA
+        assert sorted(r.tolist()) == list(range(n_local))
+        np.testing.assert_array_equal((r >> 5) % 2, (np.arange(n_local) >> 5) % 2)
+        for c in range(2):
+            own = np.nonzero((np.arange(n_local) >> 5) % 2 == c)[0]
+            assert (np.diff(lens[own, t]) <= 0).all() or n_tiles == 1
     # entries of a tile block hold ids relative to the tile (they index the staged copy)
     ids = syn & np.uint32(sell.ID_MASK)
     assert (ids < tile_words * 32).all()
@@ -83,3 +94,14 @@ def test_layout_from_counts_torch_matches_numpy():
     p2, e2 = sell.layout_from_counts(torch.from_numpy(counts), 77, 3)
     np.testing.assert_array_equal(p1, p2.numpy())
     np.testing.assert_array_equal(e1.view(np.int32), e2.numpy())
+
+
+def test_tile_placement_torch_matches_numpy():
+    rng = np.random.default_rng(5)
+    lens = rng.integers(0, 40, (301, 3))
+    p1, q1 = sell.tile_placement(lens, 301, 3, 4)
+    p2, q2 = sell.tile_placement(torch.from_numpy(lens), 301, 3, 4)
+    np.testing.assert_array_equal(p1, p2.numpy())
+    np.testing.assert_array_equal(q1, q2.numpy())
+    for t in range(3):
+        np.testing.assert_array_equal(p1[t][q1[:, t]], np.arange(301))   # inverse
