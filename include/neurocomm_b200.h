@@ -105,12 +105,15 @@ int nc_weight_histogram(const double* weights, const int64_t* assignment, int64_
  * segment rounded up to 4 entries (those hold the pad entry 0: tile-relative
  * id 0 with q = 0).  Each lane owns one row: no cross-lane reduction.
  * Tiled placement: with n_tiles > 1, lane l of block (s, t) works on
- * position p = 32s + l, which holds local row row_perm[t*n_local + p]
- * (positions >= n_local hold no row).  Within the slices a CTA owns
- * (s = c mod cta_groups) the rows are placed in descending order of their
- * tile-t length, so the 32 rows of every block have near-equal lengths in
- * every tile (the jagged tail stays short); row_meta is indexed by position:
- * row_meta[p*n_tiles + t].  With one tile positions are rows.
+ * position p = 32s + l (positions >= n_local hold no row).  CTA c of the
+ * tiled step owns slices s = c mod G (G = cta_groups); its rows are numbered
+ * k = 32*(s div G) + (row mod 32) and the row at position p of tile t is
+ * k = row_perm[t*n_local + p], i.e. row = 32*(c + (k div 32)*G) + k mod 32
+ * with c = (p div 32) mod G.  Rows are placed in descending order of their
+ * tile-t length within their CTA, so the 32 rows of every block have
+ * near-equal lengths in every tile (the jagged tail stays short).  row_meta
+ * is tile-major by position: row_meta[t*n_local + p].  With one tile
+ * positions are rows.
  * Push entries (rows = internal pre ids):
  *     (inhibitory(pre) << 31) | ((q - 1) << 26) | post_local. */
 
@@ -151,7 +154,7 @@ typedef struct nc_shard {
   const uint16_t* hop_mask; /* bit h: a spike of this neuron is sent to shard h */
   /* pull SELL-32 */
   const int64_t* slice_ptr; /* n_slices*n_tiles+1 block starts (uint4 units)   */
-  const uint32_t* row_meta; /* n_local*n_tiles: emid | (row slots << 16)        */
+  const uint32_t* row_meta; /* [n_tiles][n_local] by position: emid | (slots << 16) */
   const uint32_t* syn;      /* packed entries                                  */
   /* push CSR (optional): rows = internal pre ids, entries see above */
   const int64_t* push_rowptr;
@@ -175,8 +178,8 @@ typedef struct nc_shard {
   uint32_t* work;         /* [4] scratch counters (push work claims), zeroed by
                              nc_sim_init / nc_sim_end_step                      */
   /* tiled layouts (n_tiles > 1): per-tile row placement, see the layout notes */
-  const int32_t* row_perm; /* [n_tiles][n_local]: local row at position p of
-                              tile t (NULL = identity)                          */
+  const int32_t* row_perm; /* [n_tiles][n_local]: CTA-local index of the row
+                              at position p of tile t (NULL = identity)         */
   int32_t cta_groups;     /* G the placement was built for (CTA c owns slices
                              c, c+G, ...); the tiled step launches G CTAs       */
   int32_t pad2;
@@ -334,6 +337,8 @@ typedef struct nc_graphgen {
   const int32_t* internal_id; /* [n_neurons] internal id of every gid         */
   int32_t local_base;
   int32_t inh_every;          /* gid % inh_every == inh_every-1 is inhibitory (0 = none) */
+  int32_t n_local;            /* rows of this shard (nc_graphgen_fill)        */
+  int32_t pad0;
 } nc_graphgen_t;
 
 /* Pass 0: deg[gid] += number of edges of every neuron (zero-initialised
@@ -348,7 +353,7 @@ int nc_graphgen_count(const nc_graphgen_t* g, int32_t n_tiles, int32_t tile_word
  * lanes, slot u of lane l at padded_ptr[block] + u*32 + l; padded_ptr and
  * row_meta computed by the host from the pass-1 counts); lower_fill
  * [n_local*n_tiles*2] zero-initialised (slot claims); pos_of[row*n_tiles + t]
- * = position of the row in tile t (inverse of row_perm; NULL = identity).  syn must be pre-filled with nc_sell_fill_pads; convert the
+ * = position of the row in tile t (inverse of the placement; NULL = identity).  syn must be pre-filled with nc_sell_fill_pads; convert the
  * result with nc_sell_repack. */
 int nc_graphgen_fill(const nc_graphgen_t* g, int32_t n_tiles, int32_t tile_words, const int64_t* slice_ptr,
                      const uint32_t* row_meta, const int32_t* pos_of, int32_t* lower_fill, uint32_t* syn,
@@ -363,7 +368,8 @@ int nc_sell_fill_pads(const int64_t* slice_ptr, int64_t n_blocks, int32_t n_tile
  * h owns internal ids [shard_base[h], shard_base[h+1]) (device int32[n+1]).
  * dest_mask must be zeroed and 4-byte aligned (rows are OR-ed in per tile). */
 int nc_dest_mask_from_csr(const int64_t* slice_ptr, const uint32_t* row_meta, const int32_t* row_perm,
-                          int32_t n_tiles, int32_t tile_words, const uint32_t* syn, int32_t n_local,
+                          int32_t cta_groups, int32_t n_tiles, int32_t tile_words, const uint32_t* syn,
+                          int32_t n_local,
                           const int32_t* shard_base, int32_t n_shards, int32_t self, uint16_t* dest_mask,
                           void* stream);
 /* Padded SELL-32 (padded_ptr, as filled by nc_graphgen_fill) <-> J-SELL-32

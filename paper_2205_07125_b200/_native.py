@@ -63,6 +63,7 @@ class GraphGenC(C.Structure):
         ("seed", c_uint64),
         ("owner", c_void_p), ("internal_id", c_void_p),
         ("local_base", c_int32), ("inh_every", c_int32),
+        ("n_local", c_int32), ("pad0", c_int32),
     ]
 
 
@@ -109,8 +110,8 @@ _SIGS = {
                                    c_void_p, c_void_p]),
     "nc_graphgen_degrees": (c_int32, [C.POINTER(GraphGenC), c_void_p, c_void_p]),
     "nc_sell_fill_pads": (c_int32, [c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p]),
-    "nc_dest_mask_from_csr": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_int32, c_void_p,
-                                        c_int32, c_int32, c_void_p, c_void_p]),
+    "nc_dest_mask_from_csr": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_int32, c_void_p, c_int32,
+                                        c_void_p, c_int32, c_int32, c_void_p, c_void_p]),
     "nc_sell_repack": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_int32,
                                  c_void_p]),
     "nc_xchg_reset": (c_int32, [C.POINTER(XchgC), c_void_p]),

@@ -164,11 +164,12 @@ __global__ void k_degrees(const nc_graphgen_t g, int32_t* deg) {
 
 // Position of the k-th entry of (row, tile, sign) in the SELL-32 layout (uint32 units).
 __device__ __forceinline__ int64_t sell_pos(const int64_t* slice_ptr, const uint32_t* row_meta,
-                                            const int32_t* pos_of, int32_t T, int64_t row, int64_t seg, int32_t k) {
+                                            const int32_t* pos_of, int32_t T, int64_t n_local, int64_t row,
+                                            int64_t seg, int32_t k) {
   const int64_t t = (seg >> 1) - row * T;
   const int64_t p = pos_of ? (int64_t)pos_of[row * T + t] : row;   // position of the row in tile t
   const int64_t blk = slice_ptr[(p >> 5) * T + t];
-  const int64_t slot = ((seg & 1) ? (int64_t)(row_meta[p * T + t] & 0xFFFFu) : 0) + (k >> 2);
+  const int64_t slot = ((seg & 1) ? (int64_t)(row_meta[t * n_local + p] & 0xFFFFu) : 0) + (k >> 2);
   return (blk + slot * 32 + (p & 31)) * 4 + (k & 3);
 }
 
@@ -192,13 +193,13 @@ __global__ void k_fill(const nc_graphgen_t g, int32_t T, int32_t TW, const int64
       if (mine) {
         const int64_t seg = seg_index(ri, T, TW, jid, is_inh(g, j));
         const int32_t k = atomicAdd(fill + seg, 1);
-        syn[sell_pos(slice_ptr, row_meta, pos_of, T, ri, seg, k)] = pack(jid - tile_base(jid, TW), q);
+        syn[sell_pos(slice_ptr, row_meta, pos_of, T, g.n_local, ri, seg, k)] = pack(jid - tile_base(jid, TW), q);
       }
       if (jm) {
         const int64_t rj = (int64_t)jid - g.local_base;
         const int64_t seg = seg_index(rj, T, TW, iid, inh_i);
         const int32_t k = atomicAdd(fill + seg, 1);
-        syn[sell_pos(slice_ptr, row_meta, pos_of, T, rj, seg, k)] = pack(iid - tile_base(iid, TW), q);
+        syn[sell_pos(slice_ptr, row_meta, pos_of, T, g.n_local, rj, seg, k)] = pack(iid - tile_base(iid, TW), q);
       }
     });
   }
@@ -215,8 +216,8 @@ __global__ void k_fill_pads(const int64_t* slice_ptr, int64_t n_blocks, uint32_t
 // Destination shards of every local row: warp per (slice, tile) block, lane =
 // position (row_perm places rows per tile), OR-ed into the row's 16-bit mask
 // through the aligned 32-bit word holding it.  Pads have q = 0.
-__global__ void k_dest_mask(const int64_t* slice_ptr, const uint32_t* row_meta, const int32_t* row_perm, int32_t T,
-                            int32_t tile_words, const uint32_t* syn, int32_t n_local, const int32_t* shard_base,
+__global__ void k_dest_mask(const int64_t* slice_ptr, const uint32_t* row_meta, const int32_t* row_perm, int32_t G,
+                            int32_t T, int32_t tile_words, const uint32_t* syn, int32_t n_local, const int32_t* shard_base,
                             int32_t n_shards, int32_t self, uint16_t* dest) {
   const int lane = threadIdx.x & 31;
   const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -227,7 +228,7 @@ __global__ void k_dest_mask(const int64_t* slice_ptr, const uint32_t* row_meta, 
     const int64_t p = (s << 5) + lane;
     const int64_t b0 = slice_ptr[b];
     const int64_t tbase = t * tile_words * 32;
-    const int mine = p < n_local ? (int)(row_meta[p * T + t] >> 16) : 0;
+    const int mine = p < n_local ? (int)(row_meta[t * n_local + p] >> 16) : 0;
     const int hi = (int)__reduce_max_sync(0xffffffffu, (unsigned)mine);
     uint32_t m = 0;
     int off = 0;
@@ -244,7 +245,7 @@ __global__ void k_dest_mask(const int64_t* slice_ptr, const uint32_t* row_meta, 
     }
     m &= ~(1u << self);
     if (p < n_local && m) {
-      const int64_t r = row_perm ? row_perm[t * n_local + p] : p;
+      const int64_t r = ncdev::placed_row(row_perm, n_local, G, t, p);
       unsigned int* w = reinterpret_cast<unsigned int*>(dest + (r & ~1ll));
       atomicOr(w, m << (16 * (r & 1)));
     }
@@ -262,7 +263,7 @@ __global__ void k_sell_repack(const int64_t* pptr, const int64_t* cptr, const ui
   for (int64_t b = wid; b < n_blocks; b += nw) {
     const int64_t r = ((b / T) << 5) + lane;
     const int64_t t = b % T;
-    const int mine = r < n_local ? (int)(row_meta[r * T + t] >> 16) : 0;
+    const int mine = r < n_local ? (int)(row_meta[t * n_local + r] >> 16) : 0;
     const int hi = (int)__reduce_max_sync(0xffffffffu, (unsigned)mine);
     int off = 0;
     for (int u = 0; u < hi; ++u) {
@@ -350,7 +351,7 @@ extern "C" int nc_sell_repack(const int64_t* padded_ptr, const int64_t* slice_pt
 }
 
 extern "C" int nc_dest_mask_from_csr(const int64_t* slice_ptr, const uint32_t* row_meta, const int32_t* row_perm,
-                                     int32_t n_tiles, int32_t tile_words, const uint32_t* syn, int32_t n_local, const int32_t* shard_base,
+                                     int32_t cta_groups, int32_t n_tiles, int32_t tile_words, const uint32_t* syn, int32_t n_local, const int32_t* shard_base,
                                      int32_t n_shards, int32_t self, uint16_t* dest_mask, void* stream) {
   if (n_shards < 1 || n_shards > NC_MAX_SHARDS) {
     nc_set_error("nc_dest_mask_from_csr: n_shards must be in [1, %d]", NC_MAX_SHARDS);
@@ -358,7 +359,8 @@ extern "C" int nc_dest_mask_from_csr(const int64_t* slice_ptr, const uint32_t* r
   }
   if (n_local == 0) return NC_OK;
   k_dest_mask<<<grid_for((int64_t)n_local * 32, 256), 256, 0, (cudaStream_t)stream>>>(
-      slice_ptr, row_meta, row_perm, n_tiles, tile_words, syn, n_local, shard_base, n_shards, self, dest_mask);
+      slice_ptr, row_meta, row_perm, cta_groups < 1 ? 1 : cta_groups, n_tiles, tile_words, syn, n_local, shard_base,
+      n_shards, self, dest_mask);
   NC_LAUNCH_CHECK();
   return NC_OK;
 }

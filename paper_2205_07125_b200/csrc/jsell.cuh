@@ -2,6 +2,7 @@
 // builders (include/neurocomm_b200.h documents the layout).
 #pragma once
 #include <cuda_runtime.h>
+#include <stdint.h>
 
 namespace ncdev {
 
@@ -18,6 +19,17 @@ __device__ __forceinline__ int jsell_pos(int u, int mine, int lane, int& off) {
   const int pos = off + __popc(act & ((1u << lane) - 1u));
   off += __popc(act);
   return pos;
+}
+
+// Local row at position p of tile t (tiled placement; identity without one):
+// row_perm holds the CTA-local index k, row = 32*(c + (k/32)*G) + k%32 with
+// c = (p/32) mod G.
+__device__ __forceinline__ int64_t placed_row(const int32_t* row_perm, int64_t n_local, int32_t G, int64_t t,
+                                              int64_t p) {
+  if (!row_perm) return p;
+  const int64_t k = row_perm[t * n_local + p];
+  const int64_t c = (p >> 5) % G;
+  return ((c + (k >> 5) * G) << 5) + (k & 31);
 }
 
 }  // namespace ncdev

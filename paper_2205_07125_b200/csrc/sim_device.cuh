@@ -10,6 +10,10 @@
 namespace ncdev {
 
 constexpr int kUnroll = 8;        // 16-byte slots in flight per lane
+#ifndef NC_TAIL_UNROLL
+#define NC_TAIL_UNROLL 4
+#endif
+constexpr int kTailUnroll = NC_TAIL_UNROLL;   // ... in the ragged tail of a J-SELL block
 constexpr uint32_t kFull = 0xffffffffu;
 
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
@@ -86,9 +90,8 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
-// Slots ahead of the loads for the tiled kernel's L2 prefetch: with the
-// bitmap tile filling shared memory, registers cap the loads in flight and the
-// prefetch keeps HBM busy (measured +7% at 2 tiles; at 1 tile it costs ~1%).
+// Slots ahead of the loads for the L2 prefetch of the tiled kernel when its
+// partial sums live in global memory (flags bit 0).
 #ifndef NC_PF_DIST
 #define NC_PF_DIST 8
 #endif
@@ -125,17 +128,17 @@ __device__ __forceinline__ int32_t sell_row_sum(const uint4* __restrict__ blk, u
       acc += quad_term(e[u], bm) * (u0 + u < emid ? 1 : wi);
     }
   }
-  // ragged tail
+  // ragged tail (short: rows of a block have near-equal lengths)
   int off = lo * 32;
-  for (int u0 = lo; u0 < hi; u0 += kUnroll) {
-    uint4 e[kUnroll];
+  for (int u0 = lo; u0 < hi; u0 += kTailUnroll) {
+    uint4 e[kTailUnroll];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
+    for (int u = 0; u < kTailUnroll; ++u) {
       const int pos = jsell_pos(u0 + u, mine, lane, off);
       e[u] = (u0 + u < mine) ? ld_stream(blk + pos) : padv;
     }
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
+    for (int u = 0; u < kTailUnroll; ++u) {
       if (u0 + u >= hi) break;   // warp-uniform
       acc += quad_term(e[u], bm) * (u0 + u < emid ? 1 : wi);
     }

@@ -312,7 +312,7 @@ class Network:
                 p_out=spec.p_out, intra_lo=spec.intra_p_range[0], intra_hi=spec.intra_p_range[1],
                 inter_lo=spec.inter_p_range[0], inter_hi=spec.inter_p_range[1],
                 seed=int(spec.seed) & (2**64 - 1), owner=owner_d.data_ptr(), internal_id=internal_d.data_ptr(),
-                local_base=int(layout.base[h]), inh_every=inh_every)
+                local_base=int(layout.base[h]), inh_every=inh_every, n_local=n_local)
             n_seg = max(n_local * T * 2, 1)
             lower = torch.zeros(n_seg, dtype=torch.int32, device=dev)
             upper = torch.zeros(n_seg, dtype=torch.int32, device=dev)
@@ -340,7 +340,8 @@ class Network:
             torch.cuda.synchronize(dev)
             del syn, ptr, pos_of
             csr = ShardCSR(jptr, meta, jsyn, T, TW, n_local, n_real, partials_global=pglob,
-                           row_perm=None if perm is None else perm.reshape(-1).contiguous(), cta_groups=sms)
+                           row_perm=None if perm is None else sell.local_index(perm, sms).reshape(-1).contiguous(),
+                           cta_groups=sms)
             csr.dest = _dest_masks(csr, layout, h, dev)
             out[h] = csr
             nsyn += n_real
@@ -390,7 +391,8 @@ def _dest_masks(csr: ShardCSR, layout: ShardLayout, h: int, dev):
     out16 = torch.zeros(n_local + 2, dtype=torch.int16, device=dev)   # OR-ed through aligned 32-bit words
     L = _native.lib()
     _native.check(L.nc_dest_mask_from_csr(csr.slice_ptr.data_ptr(), csr.row_meta.data_ptr(),
-                                          None if csr.row_perm is None else csr.row_perm.data_ptr(), csr.n_tiles,
+                                          None if csr.row_perm is None else csr.row_perm.data_ptr(),
+                                          csr.cta_groups, csr.n_tiles,
                                           csr.tile_words, csr.syn.data_ptr(), n_local,
                                           bases.data_ptr(),
                                           layout.n_shards, h, out16.data_ptr(), _native.stream_handle(dev)),

@@ -32,9 +32,14 @@ def test_host_build_round_trip(n_local, n_tiles, tile_words):
     np.testing.assert_array_equal(a, b)
     # jagged blocks hold exactly their positions' slots; every row's slots hold its
     # E entries, then its I entries, each segment padded to a multiple of 4
-    perm2 = np.tile(np.arange(n_local), (n_tiles, 1)) if perm is None else perm.reshape(n_tiles, n_local)
-    lens = (meta >> np.uint32(16)).astype(np.int64).reshape(n_local, n_tiles)       # by position
-    emid = (meta & np.uint32(0xFFFF)).astype(np.int64).reshape(n_local, n_tiles)
+    if perm is None:
+        perm2 = np.tile(np.arange(n_local), (n_tiles, 1))
+    else:   # CTA-local index -> row
+        k = perm.reshape(n_tiles, n_local).astype(np.int64)
+        c = (np.arange(n_local) >> 5) % 2
+        perm2 = ((c + (k >> 5) * 2) << 5) + (k & 31)
+    lens = (meta >> np.uint32(16)).astype(np.int64).reshape(n_tiles, n_local).T     # by position
+    emid = (meta & np.uint32(0xFFFF)).astype(np.int64).reshape(n_tiles, n_local).T
     pad_rows = np.zeros(((n_local + 31) // 32 * 32, n_tiles), dtype=np.int64)
     pad_rows[:n_local] = lens
     np.testing.assert_array_equal(pad_rows.reshape(-1, 32, n_tiles).sum(axis=1).reshape(-1), np.diff(ptr))
@@ -61,7 +66,7 @@ def test_jagged_positions_match_the_formula():
     rng = np.random.default_rng(3)
     n_local, T = 70, 2
     lens = rng.integers(0, 9, (n_local, T))
-    meta = (lens.astype(np.uint32) << np.uint32(16)).reshape(-1)
+    meta = (lens.T.astype(np.uint32) << np.uint32(16)).reshape(-1)   # tile-major
     pptr = sell.padded_ptr(meta, n_local, T)
     jptr = sell.jagged_ptr(meta, n_local, T)
     g = sell.jagged_gather(pptr, meta, n_local, T)
@@ -82,7 +87,7 @@ def test_plan_tiles():
     T, tw, glob = sell.plan_tiles(312_500 + 1, 1_250_000, 148)    # 10 M neurons, 1.25 M local
     assert T > 1 and tw % 4 == 0 and T * tw >= 312_501 and not glob
     per = (1_250_000 // 32 + 147) // 148
-    assert 2 * tw * 4 + per * 128 <= sell.SMEM_BYTES - sell.SMEM_RESERVE
+    assert 2 * tw * 4 + per * 128 <= sell.SMEM_TILED
     T, tw, glob = sell.plan_tiles(1_562_500 + 1, 12_500_000, 148)  # 50 M neurons, 12.5 M local
     assert glob and T * tw >= 1_562_501 and 2 * tw * 4 <= sell.SMEM_BYTES - sell.SMEM_RESERVE
 
