@@ -282,6 +282,9 @@ typedef struct nc_xchg {
   uint32_t* barrier;               /* in-kernel grid barrier counter            */
   unsigned long long* lat_start;
   uint32_t* lat_ns;                /* per-step exchange latency (ns) or NULL    */
+  unsigned long long* dbg;         /* diagnostics or NULL: [64 steps][n*B blocks][4]
+                                      globaltimer at block start, message published,
+                                      peer flag seen, inbound ids scattered      */
 } nc_xchg_t;
 
 /* Inbox words needed per rank for the P2P transport. */

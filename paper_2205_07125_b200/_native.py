@@ -83,7 +83,7 @@ class XchgC(C.Structure):
         ("my_inbox", c_void_p), ("my_flags", c_void_p),
         ("peer_inbox", c_void_p * MAX_SHARDS), ("peer_flags", c_void_p * MAX_SHARDS),
         ("done", c_void_p), ("send_done", c_void_p), ("blocks_per_peer", c_int32), ("pad1", c_int32),
-        ("barrier", c_void_p), ("lat_start", c_void_p), ("lat_ns", c_void_p),
+        ("barrier", c_void_p), ("lat_start", c_void_p), ("lat_ns", c_void_p), ("dbg", c_void_p),
     ]
 
 

@@ -9,16 +9,19 @@
 //    capturable), followed by a scatter kernel that ORs the ids into the spike
 //    bitmap and, on relays, re-buckets them for phase 2.
 //  * P2P (nc_xchg_p2p): one device-initiated kernel per step.  Inboxes are
-//    cudaMalloc'd regions opened by every peer through CUDA IPC; block b pushes
-//    this rank's bucket for peer b straight into b's inbox with NVLink stores,
-//    publishes it with a system-scope release store of the step number into b's
-//    flag word, then acquires the flag of source b and scatters what arrived.
-//    Phase-1 flags go to every peer every step (a heartbeat that bounds the
-//    step lag between any two ranks to one), so inbox slots double-buffered by
-//    step parity are never overwritten before they are read.  Two-level routes
-//    add an in-kernel grid barrier (every phase-1 inbox drained) and a phase-2
-//    push from relays.  Every spin is bounded by a %globaltimer watchdog that
-//    sets status[1] and returns instead of hanging the GPU.
+//    cudaMalloc'd regions opened by every peer through CUDA IPC; the B blocks
+//    of peer b store this rank's bucket for b straight into b's inbox with
+//    NVLink stores, in a low-latency protocol: every 8-byte word carries the
+//    step tag next to its payload (header word: tag | count), so no fence or
+//    flag is needed -- the receiving blocks poll the header and their chunk's
+//    words until the tag matches, then OR the ids into the spike bitmap.
+//    Phase-1 messages go to every peer every step (possibly empty: a
+//    heartbeat that bounds the step lag between any two ranks to one), so
+//    inbox slots double-buffered by step parity are never overwritten before
+//    they are read.  Two-level routes add an in-kernel grid barrier (every
+//    phase-1 inbox drained) and a phase-2 push from relays.  Every spin is
+//    bounded by a %globaltimer watchdog that sets status[1] and returns
+//    instead of hanging the GPU.
 //
 // Counters: hop_ids[u*n+v] (ids this rank sent on u->v, u = this rank) and
 // deliv_ids[s*n+d] (d = this rank); per-step rows when per_step is set.

@@ -35,22 +35,6 @@ __device__ __forceinline__ int owner_of(const nc_xchg_t& X, uint32_t id) {
   return -1;
 }
 
-// Spin until *flag >= want; false on watchdog expiry.
-static __device__ bool wait_flag(const uint32_t* flag, uint32_t want, uint64_t timeout_ns, int32_t* status) {
-  const uint64_t t0 = globaltimer();
-  uint32_t spins = 0;
-  while ((int32_t)(ld_acquire_sys(flag) - want) < 0) {
-    if ((++spins & 255u) == 0) {
-      if (globaltimer() - t0 > timeout_ns) {
-        atomicExch(status + 1, 1);
-        return false;
-      }
-      if (*(volatile int32_t*)(status + 1)) return false;  // another block timed out
-    }
-  }
-  return true;
-}
-
 // OR `cnt` ids into the bitmap, count deliveries, relay-bucket if asked.
 // Called by a whole block.
 static __device__ void scatter_ids(const nc_xchg_t& X, const uint32_t* ids, int64_t cnt, int src, bool phase2,
@@ -83,42 +67,113 @@ __device__ __forceinline__ long long* step_row(long long* base, const nc_xchg_t&
 }
 
 // ---------------------------------------------------------------- P2P path
-// Inbox layout (uint32 words) on every rank, per (phase, parity, source):
-//   slot = ((phase * 2 + parity) * n + src) * (cap + 4): [count, pad, pad, pad, ids...]
-// Flags (separate region): flags[phase * NC_MAX_SHARDS + src].
+// Low-latency protocol: every 8-byte word of a message carries its own step
+// tag -- (tag << 32) | payload -- so the receiver polls the words themselves
+// and the sender needs no system-scope fence or separate flag (8-byte aligned
+// stores are single-copy atomic).  Inbox layout (uint64 words) on every rank,
+// per (phase, parity, source):
+//   slot = ((phase * 2 + parity) * n + src) * (cap + 1): [tag|count, tag|id ...]
+// The tag is step + 1: a slot is reused every second step, so a stale word
+// never matches.
 
 __device__ __forceinline__ int64_t slot_off(const nc_xchg_t& X, int phase, int parity, int src) {
-  return ((int64_t)((phase * 2 + parity) * X.n + src)) * (X.cap + 4);
+  return ((int64_t)((phase * 2 + parity) * X.n + src)) * (X.cap + 1);
 }
 
-// Copy ids [lo, hi) to a (possibly remote) slot, 16-byte stores where aligned.
-static __device__ void push_ids(uint32_t* dst, const uint32_t* src, int64_t lo, int64_t hi) {
-  const int64_t a4 = (lo + 3) >> 2, b4 = hi >> 2;
-  for (int64_t k = lo + threadIdx.x; k < min(hi, a4 << 2); k += blockDim.x) dst[k] = src[k];
-  const uint4* s4 = reinterpret_cast<const uint4*>(src);
-  uint4* d4 = reinterpret_cast<uint4*>(dst);
-  for (int64_t k = a4 + threadIdx.x; k < b4; k += blockDim.x) d4[k] = s4[k];
-  for (int64_t k = max(lo, b4 << 2) + threadIdx.x; k < hi; k += blockDim.x) dst[k] = src[k];
+__device__ __forceinline__ void st_relaxed_sys_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ uint64_t ld_relaxed_sys_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 
 __device__ __forceinline__ void chunk(int64_t cnt, int k, int B, int64_t* lo, int64_t* hi) {
-  const int64_t per = (((cnt + B - 1) / B) + 3) & ~int64_t(3);  // 16-byte aligned chunks
+  const int64_t per = (cnt + B - 1) / B;
   *lo = min(cnt, per * k);
   *hi = min(cnt, per * (k + 1));
 }
 
-// Publish one phase's message to peer b once all B blocks of it have stored
-// their chunk: every block fences (system scope) and counts itself in; the
-// last one releases the flag.
-static __device__ void publish(const nc_xchg_t& X, int phase, int b, uint32_t want, int B) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    const uint32_t arrived = atomicAdd(X.send_done + phase * NC_MAX_SHARDS + b, 1u) + 1u;
-    if (arrived == want * (uint32_t)B) {
-      __threadfence_system();
-      st_release_sys(X.peer_flags[b] + phase * NC_MAX_SHARDS + X.rank, want);
+// Chunk kb of B of a message of `cnt` ids to a (possibly remote) slot; block kb
+// 0 also writes the header.  Called by a whole block.
+static __device__ void ll_send(uint64_t* slot, const uint32_t* ids, int64_t cnt, int kb, int B, uint32_t tag) {
+  int64_t lo, hi;
+  chunk(cnt, kb, B, &lo, &hi);
+  const uint64_t t = (uint64_t)tag << 32;
+  for (int64_t k = lo + threadIdx.x; k < hi; k += blockDim.x) st_relaxed_sys_u64(slot + 1 + k, t | ids[k]);
+  if (kb == 0 && threadIdx.x == 0) st_relaxed_sys_u64(slot, t | (uint32_t)cnt);
+}
+
+// Spin until the word carries `tag` (into *out); false on watchdog expiry.
+__device__ __forceinline__ bool ll_wait(const uint64_t* w, uint32_t tag, uint64_t timeout_ns, int32_t* status,
+                                        uint64_t* out) {
+  uint64_t v = ld_relaxed_sys_u64(w);
+  if ((uint32_t)(v >> 32) == tag) {
+    *out = v;
+    return true;
+  }
+  const uint64_t t0 = globaltimer();
+  uint32_t spins = 0;
+  for (;;) {
+    v = ld_relaxed_sys_u64(w);
+    if ((uint32_t)(v >> 32) == tag) {
+      *out = v;
+      return true;
     }
+    if ((++spins & 255u) == 0) {
+      if (globaltimer() - t0 > timeout_ns) {
+        atomicExch(status + 1, 1);
+        return false;
+      }
+      if (*(volatile int32_t*)(status + 1)) return false;  // another block timed out
+    }
+  }
+}
+
+// Receive chunk kb of the message in `slot` and OR its ids into the bitmap,
+// count deliveries, relay-bucket if asked (two-level phase 1).  Whole block.
+static __device__ void ll_recv_scatter(const nc_xchg_t& X, const uint64_t* slot, int kb, int B, uint32_t tag,
+                                       int src, bool phase2, uint32_t* cur, long long* deliv) {
+  __shared__ long long s_cnt;
+  __shared__ unsigned int per_src[NC_MAX_SHARDS];
+  if (threadIdx.x < NC_MAX_SHARDS) per_src[threadIdx.x] = 0;
+  if (threadIdx.x == 0) {
+    uint64_t h = 0;
+    s_cnt = ll_wait(slot, tag, X.timeout_ns, X.status, &h) ? (long long)(uint32_t)h : -1;
+  }
+  __syncthreads();
+  int64_t cnt = s_cnt;
+  if (cnt < 0) return;
+  if (cnt > X.cap) cnt = X.cap;
+  int64_t lo, hi;
+  chunk(cnt, kb, B, &lo, &hi);
+  const uint32_t fwd = phase2 ? 0u : (uint32_t)X.fwd_row[src];
+  // direct delivery (not relaying for src): every id received is for this rank
+  const bool plain = !phase2 && fwd == 0u;
+  for (int64_t k = lo + threadIdx.x; k < hi; k += blockDim.x) {
+    uint64_t v = 0;
+    if (!ll_wait(slot + 1 + k, tag, X.timeout_ns, X.status, &v)) break;
+    const uint32_t id = (uint32_t)v;
+    atomicOr(cur + (id >> 5), 1u << (id & 31));
+    if (plain) continue;
+    const uint32_t dm = (uint16_t)X.dest_global[id];
+    if ((dm >> X.rank) & 1u) atomicAdd(&per_src[phase2 ? max(owner_of(X, id), 0) : src], 1u);
+    uint32_t f = dm & fwd;
+    while (f) {
+      const int d = __ffs(f) - 1;
+      f &= f - 1;
+      const int32_t pos = atomicAdd(X.fwd_count + d, 1);
+      if (pos < X.cap) X.fwd_ids[(int64_t)d * X.cap + pos] = id;
+      else atomicExch(X.status, 1);
+    }
+  }
+  __syncthreads();
+  if (plain) {
+    if (threadIdx.x == 0 && hi > lo) add64(deliv + (int64_t)src * X.n + X.rank, (long long)(hi - lo));
+  } else if (threadIdx.x < X.n && per_src[threadIdx.x]) {
+    add64(deliv + (int64_t)threadIdx.x * X.n + X.rank, (long long)per_src[threadIdx.x]);
   }
 }
 
@@ -130,16 +185,18 @@ static __device__ void p2p_block(const nc_xchg_t& X, int ex, int B, int step) {
   const int b = ex / B;   // peer handled by this block
   const int kb = ex % B;  // chunk
   const int par = step & 1;
-  const uint32_t want = (uint32_t)step + 1u;
+  const uint32_t tag = (uint32_t)step + 1u;
   uint32_t* cur = (step & 1) ? X.bitmap1 : X.bitmap0;
   long long* hop = step_row(X.hop_ids, X, step);
   long long* deliv = step_row(X.deliv_ids, X, step);
+  uint64_t* my_inbox = reinterpret_cast<uint64_t*>(X.my_inbox);
   __shared__ uint64_t t_start;
-  __shared__ bool ok;
   if (threadIdx.x == 0) t_start = globaltimer();
   const bool peer = (b < X.n && b != X.rank);
+  unsigned long long* dbg = (X.dbg && step < 64 && threadIdx.x == 0) ? X.dbg + ((int64_t)step * nex + ex) * 4 : nullptr;
+  if (dbg) dbg[0] = t_start;
 
-  // ---- phase 1 push (data on route channels, heartbeat flag to everyone)
+  // ---- phase 1 push: every peer gets a message (possibly empty: the heartbeat)
   if (peer) {
     int64_t cnt = 0;
     if ((X.send1_mask >> b) & 1u) {
@@ -148,29 +205,16 @@ static __device__ void p2p_block(const nc_xchg_t& X, int ex, int B, int step) {
         if (threadIdx.x == 0 && kb == 0) atomicExch(X.status, 1);
         cnt = X.cap;
       }
-      uint32_t* slot = X.peer_inbox[b] + slot_off(X, 0, par, X.rank);
-      int64_t lo, hi;
-      chunk(cnt, kb, B, &lo, &hi);
-      push_ids(slot + 4, X.bucket_ids + (int64_t)b * X.bucket_cap, lo, hi);
-      if (threadIdx.x == 0 && kb == 0) {
-        slot[0] = (uint32_t)cnt;
-        if (cnt) add64(hop + X.rank * X.n + b, cnt);
-      }
+      if (threadIdx.x == 0 && kb == 0 && cnt) add64(hop + X.rank * X.n + b, cnt);
     }
-    publish(X, 0, b, want, B);
+    ll_send(reinterpret_cast<uint64_t*>(X.peer_inbox[b]) + slot_off(X, 0, par, X.rank),
+            X.bucket_ids + (int64_t)b * X.bucket_cap, cnt, kb, B, tag);
+    if (dbg) dbg[1] = globaltimer();
   }
   // ---- phase 1 receive from peer b, chunk kb
   if (peer) {
-    if (threadIdx.x == 0) ok = wait_flag(X.my_flags + 0 * NC_MAX_SHARDS + b, want, X.timeout_ns, X.status);
-    __syncthreads();
-    if (ok && ((X.recv1_mask >> b) & 1u)) {
-      const uint32_t* slot = X.my_inbox + slot_off(X, 0, par, b);
-      int64_t cnt = *(volatile const uint32_t*)slot;
-      if (cnt > X.cap) cnt = X.cap;
-      int64_t lo, hi;
-      chunk(cnt, kb, B, &lo, &hi);
-      scatter_ids(X, slot + 4 + lo, hi - lo, b, false, cur, deliv, X.status);
-    }
+    if (dbg) dbg[2] = globaltimer();
+    ll_recv_scatter(X, my_inbox + slot_off(X, 0, par, b), kb, B, tag, b, false, cur, deliv);
   }
   if (X.two_level) {
     // ---- grid barrier: every phase-1 inbox drained, forward buckets complete
@@ -196,32 +240,17 @@ static __device__ void p2p_block(const nc_xchg_t& X, int ex, int B, int step) {
         if (threadIdx.x == 0 && kb == 0) atomicExch(X.status, 1);
         cnt = X.cap;
       }
-      uint32_t* slot = X.peer_inbox[b] + slot_off(X, 1, par, X.rank);
-      int64_t lo, hi;
-      chunk(cnt, kb, B, &lo, &hi);
-      push_ids(slot + 4, X.fwd_ids + (int64_t)b * X.cap, lo, hi);
-      if (threadIdx.x == 0 && kb == 0) {
-        slot[0] = (uint32_t)cnt;
-        if (cnt) add64(hop + X.rank * X.n + b, cnt);
-      }
-      publish(X, 1, b, want, B);
+      if (threadIdx.x == 0 && kb == 0 && cnt) add64(hop + X.rank * X.n + b, cnt);
+      ll_send(reinterpret_cast<uint64_t*>(X.peer_inbox[b]) + slot_off(X, 1, par, X.rank),
+              X.fwd_ids + (int64_t)b * X.cap, cnt, kb, B, tag);
     }
     // ---- phase 2 receive from relay b
-    if (peer && ((X.recv2_mask >> b) & 1u)) {
-      if (threadIdx.x == 0) ok = wait_flag(X.my_flags + 1 * NC_MAX_SHARDS + b, want, X.timeout_ns, X.status);
-      __syncthreads();
-      if (ok) {
-        const uint32_t* slot = X.my_inbox + slot_off(X, 1, par, b);
-        int64_t cnt = *(volatile const uint32_t*)slot;
-        if (cnt > X.cap) cnt = X.cap;
-        int64_t lo, hi;
-        chunk(cnt, kb, B, &lo, &hi);
-        scatter_ids(X, slot + 4 + lo, hi - lo, b, true, cur, deliv, X.status);
-      }
-    }
+    if (peer && ((X.recv2_mask >> b) & 1u))
+      ll_recv_scatter(X, my_inbox + slot_off(X, 1, par, b), kb, B, tag, b, true, cur, deliv);
   }
   // ---- latency record: last block out stamps (end - start of block 0)
   __syncthreads();
+  if (dbg) dbg[3] = globaltimer();
   if (threadIdx.x == 0) {
     if (ex == 0) *X.lat_start = t_start;
     __threadfence();

@@ -20,6 +20,8 @@ through it.
 
 from __future__ import annotations
 
+import os
+
 import ctypes as C
 
 import numpy as np
@@ -161,6 +163,10 @@ class DistSimulator:
         X.send_hdr, X.send2_hdr = self.hdr[0].data_ptr(), self.hdr[1].data_ptr()
         X.recv_hdr, X.recv2_hdr = self.hdr[2].data_ptr(), self.hdr[3].data_ptr()
         X.recv_ids, X.recv2_ids = self.recv_ids.data_ptr(), self.recv2_ids.data_ptr()
+        self.dbg = None
+        if os.environ.get("NC_XCHG_DBG"):   # diagnostics (tools/xchg_stamps.py)
+            self.dbg = torch.zeros((64, n * self.blocks_per_peer, 4), dtype=torch.int64, device=dev)
+            X.dbg = self.dbg.data_ptr()
         self.X = X
         self._comm = None
         self._ipc_own: list[int] = []
@@ -197,7 +203,7 @@ class DistSimulator:
     def _setup_p2p(self):
         import torch.distributed as dist
         n, cap = self.n, self.cap
-        inbox_words = 4 * n * (cap + 4)
+        inbox_words = 4 * n * (cap + 1) * 2    # (phase, parity, src) slots of (cap + 1) tagged 8-byte words
         flag_words = 2 * _native.MAX_SHARDS + 16 + 2 * _native.MAX_SHARDS  # flags, done/barrier/lat, send_done
         handles = []
         ptrs = []
