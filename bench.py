@@ -209,7 +209,8 @@ def lat_summary(lat, lat_max, transport):
     return {"p50": round(float(np.percentile(lat, 50)), 2), "p99": round(float(np.percentile(lat, 99)), 2),
             "p50_incl_skew": round(float(np.percentile(lat_max, 50)), 2),
             "p99_incl_skew": round(float(np.percentile(lat_max, 99)), 2), "transport": transport,
-            "what": "device %globaltimer from a rank's buckets-ready to its last inbound spike in the bitmap; "
+            "what": "device %globaltimer per step and rank from buckets ready (p2p: the exchange kernel's "
+                    "first block starts after the step kernel) to the last inbound spike ORed into the bitmap; "
                     "p50/p99 over steps of the min over ranks (the last-ready rank: transfer + signalling), "
                     "*_incl_skew: max over ranks (adds waiting for slower peers)"}
 

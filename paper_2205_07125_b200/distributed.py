@@ -138,6 +138,8 @@ class DistSimulator:
         self.recv_ids = torch.zeros(n * cap if transport == "nccl" else 1, **i32)
         self.recv2_ids = torch.zeros(n * cap if (transport == "nccl" and self.plan.two_level) else 1, **i32)
         self.lat_stamps = torch.zeros((2, max(latency_steps, 1)), dtype=torch.int64, device=dev)
+        # P2P: the exchange kernel records its own duration per step (no stamp kernels)
+        self.lat_ns = torch.zeros(max(latency_steps, 1), **i32)
         self.sync_words = torch.zeros(8, **i32)
         self._gbar = torch.zeros(1, **i32)
         self.hop_ids = None
@@ -146,6 +148,8 @@ class DistSimulator:
         X = _native.XchgC()
         X.rank, X.n, X.cap, X.two_level = self.rank, n, cap, int(self.plan.two_level)
         X.per_step, X.lat_steps = int(per_step_counts), 0
+        if transport == "p2p":
+            X.lat_ns, X.lat_steps = self.lat_ns.data_ptr(), int(latency_steps)
         X.send1_mask, X.recv1_mask = self.masks["send1"], self.masks["recv1"]
         X.send2_mask, X.recv2_mask = self.masks["send2"], self.masks["recv2"]
         X.bucket_cap = self.state.bucket_cap
@@ -270,6 +274,7 @@ class DistSimulator:
         self.deliv_ids = torch.zeros((rows, self.n, self.n), dtype=torch.int64, device=self.dev)
         self.X.hop_ids, self.X.deliv_ids = self.hop_ids.data_ptr(), self.deliv_ids.data_ptr()
         self.lat_stamps.zero_()
+        self.lat_ns.zero_()
         _native.check(self.lib.nc_xchg_reset(C.byref(self.X), st), "xchg reset")
         self._graph = None
         torch.cuda.synchronize(self.dev)
@@ -300,9 +305,14 @@ class DistSimulator:
             else:
                 _native.check(L.nc_sim_deliver_pull(C.byref(s.c), self.c_lif.g_inh, st), "pull")
             _native.check(L.nc_sim_lif_update(C.byref(s.c), lif, st), "lif")
-        _native.check(L.nc_stamp(self.lat_stamps[0].data_ptr(), s.step.data_ptr(), self.latency_steps, st), "stamp")
-        self._exchange(st)
-        _native.check(L.nc_stamp(self.lat_stamps[1].data_ptr(), s.step.data_ptr(), self.latency_steps, st), "stamp")
+        if self.transport == "p2p":
+            self._exchange(st)          # stamps its own start (buckets ready) and end
+        else:
+            _native.check(L.nc_stamp(self.lat_stamps[0].data_ptr(), s.step.data_ptr(), self.latency_steps, st),
+                          "stamp")
+            self._exchange(st)
+            _native.check(L.nc_stamp(self.lat_stamps[1].data_ptr(), s.step.data_ptr(), self.latency_steps, st),
+                          "stamp")
         _native.check(L.nc_sim_end_step(C.byref(s.c), st), "end step")
 
     def launches_per_step(self) -> float:
@@ -310,9 +320,8 @@ class DistSimulator:
             return 0.0  # one cooperative launch per advance() call
         step = 2 if self.delivery == "fused" else 3
         if self.transport == "p2p":
-            ex = 1 + (1 if self.plan.two_level else 0)
-        else:
-            ex = 2 * (2 if self.plan.two_level else 1) + (1 if self.plan.two_level else 0)
+            return step + 1 + (1 if self.plan.two_level else 0)
+        ex = 2 * (2 if self.plan.two_level else 1) + (1 if self.plan.two_level else 0)
         return step + ex + 2
 
     def advance_eager(self, steps: int):
@@ -366,7 +375,10 @@ class DistSimulator:
         import torch
         import torch.distributed as dist
         k = min(steps, self.latency_steps)
-        d = (self.lat_stamps[1, :k] - self.lat_stamps[0, :k]).to(torch.float64)
+        if self.transport == "p2p" and self.delivery != "persistent":
+            d = self.lat_ns[:k].to(torch.float64)
+        else:
+            d = (self.lat_stamps[1, :k] - self.lat_stamps[0, :k]).to(torch.float64)
         lo, hi = d.clone(), d.clone()
         dist.all_reduce(lo, op=dist.ReduceOp.MIN)
         dist.all_reduce(hi, op=dist.ReduceOp.MAX)
