@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <utility>
 #include "nc_common.h"
 #include "philox.cuh"
 #include "jsell.cuh"
@@ -23,6 +24,24 @@ __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
   return r;
 }
 
+// Same with an immediate byte offset ([reg + imm] addressing: one instruction
+// per load in an unrolled group instead of a 64-bit address computation each).
+template <int kOff>
+__device__ __forceinline__ uint4 ld_stream_at(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4+%5];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "n"(kOff));
+  return r;
+}
+
+// Slots [0, n) of a group of kUnroll: slot u of this lane at q + 32u (512 B apart).
+template <int... U>
+__device__ __forceinline__ void load_group(uint4 (&e)[sizeof...(U)], const uint4* q, int n, uint4 padv,
+                                           std::integer_sequence<int, U...>) {
+  ((e[U] = (U < n) ? ld_stream_at<U * 512>(q) : padv), ...);
+}
+
 __device__ __forceinline__ uint4 ld_keep(const uint4* p) {
   uint4 r;
   asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -39,11 +58,18 @@ __device__ __forceinline__ uint32_t entry_bit(uint32_t e, const uint32_t* __rest
   return __funnelshift_r(word, word, e) & 1u;
 }
 
+// bit * q + acc as one IMAD (left to itself the compiler emits ISETP + SEL + IADD)
+__device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+
 __device__ __forceinline__ int32_t quad_term(uint4 e, const uint32_t* __restrict__ bm) {
-  uint32_t s = entry_bit(e.x, bm) * (e.x >> 26);
-  s += entry_bit(e.y, bm) * (e.y >> 26);
-  s += entry_bit(e.z, bm) * (e.z >> 26);
-  s += entry_bit(e.w, bm) * (e.w >> 26);
+  uint32_t s = mad_u32(entry_bit(e.x, bm), e.x >> 26, 0u);
+  s = mad_u32(entry_bit(e.y, bm), e.y >> 26, s);
+  s = mad_u32(entry_bit(e.z, bm), e.z >> 26, s);
+  s = mad_u32(entry_bit(e.w, bm), e.w >> 26, s);
   return (int32_t)s;
 }
 
@@ -120,8 +146,7 @@ __device__ __forceinline__ int32_t sell_row_sum(const uint4* __restrict__ blk, u
       prefetch_l2(blk + a * 32, (uint32_t)min(kUnroll, lo - a) * 512u);
     }
     uint4 e[kUnroll];
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) e[u] = (u0 + u < lo) ? ld_stream(p + (u0 + u) * 32) : padv;
+    load_group(e, p + u0 * 32, lo - u0, padv, std::make_integer_sequence<int, kUnroll>{});
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       if (u0 + u >= lo) break;   // warp-uniform: no lookups for the pad of a partial group
