@@ -121,8 +121,10 @@ def main() -> int:
                     "exchange_us_p50": round(float(np.percentile(lat, 50)), 2),
                     "exchange_us_p99": round(float(np.percentile(lat, 99)), 2),
                     "exchange_us_p50_incl_skew": round(float(np.percentile(lat_max, 50)), 2),
-                    "ids_per_step": round(float(h.sum()), 1), "bytes_per_step": round(float(h.sum()) * 4, 1),
-                    "max_channel_bytes_per_step": round(float(h.max()) * 4, 1),
+                    "ids_per_step": round(float(h.sum()), 1), "payload_bytes_per_step": round(float(h.sum()) * 4, 1),
+                    # P2P low-latency protocol: 8 bytes per id on the wire (tag + id) + an 8-byte header per message
+                    "wire_bytes_per_step": round(float(h.sum()) * 8 + 8 * int((h > 0).sum()), 1),
+                    "max_channel_payload_bytes_per_step": round(float(h.max()) * 4, 1),
                     "channels": int((h > 0).sum()),
                     "connections_out_degree": nc.connection_stats(rt).out_degree.tolist(),
                     "netsim_step_time_model_units": model.step_time,

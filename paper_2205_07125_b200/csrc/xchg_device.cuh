@@ -152,21 +152,32 @@ static __device__ void ll_recv_scatter(const nc_xchg_t& X, const uint64_t* slot,
   const uint32_t fwd = phase2 ? 0u : (uint32_t)X.fwd_row[src];
   // direct delivery (not relaying for src): every id received is for this rank
   const bool plain = !phase2 && fwd == 0u;
-  for (int64_t k = lo + threadIdx.x; k < hi; k += blockDim.x) {
+  // warp-uniform loop (relay appends are warp-aggregated: one atomic per warp and destination)
+  const int lane = threadIdx.x & 31;
+  for (int64_t k0 = lo + (threadIdx.x & ~31); k0 < hi; k0 += blockDim.x) {
+    const int64_t k = k0 + lane;
     uint64_t v = 0;
-    if (!ll_wait(slot + 1 + k, tag, X.timeout_ns, X.status, &v)) break;
+    const bool good = k < hi && ll_wait(slot + 1 + k, tag, X.timeout_ns, X.status, &v);
     const uint32_t id = (uint32_t)v;
-    atomicOr(cur + (id >> 5), 1u << (id & 31));
+    if (good) atomicOr(cur + (id >> 5), 1u << (id & 31));
     if (plain) continue;
-    const uint32_t dm = (uint16_t)X.dest_global[id];
+    const uint32_t dm = good ? (uint32_t)(uint16_t)X.dest_global[id] : 0u;
     if ((dm >> X.rank) & 1u) atomicAdd(&per_src[phase2 ? max(owner_of(X, id), 0) : src], 1u);
-    uint32_t f = dm & fwd;
-    while (f) {
-      const int d = __ffs(f) - 1;
-      f &= f - 1;
-      const int32_t pos = atomicAdd(X.fwd_count + d, 1);
-      if (pos < X.cap) X.fwd_ids[(int64_t)d * X.cap + pos] = id;
-      else atomicExch(X.status, 1);
+    const uint32_t f = dm & fwd;
+    uint32_t pending = __reduce_or_sync(kFull, f);
+    while (pending) {
+      const int d = __ffs(pending) - 1;
+      pending &= pending - 1;
+      const uint32_t m = __ballot_sync(kFull, (f >> d) & 1u);
+      const int leader = __ffs(m) - 1;
+      int32_t base = 0;
+      if (lane == leader) base = atomicAdd(X.fwd_count + d, __popc(m));
+      base = __shfl_sync(kFull, base, leader);
+      if ((f >> d) & 1u) {
+        const int32_t pos = base + __popc(m & ((1u << lane) - 1u));
+        if (pos < X.cap) X.fwd_ids[(int64_t)d * X.cap + pos] = id;
+        else atomicExch(X.status, 1);
+      }
     }
   }
   __syncthreads();
