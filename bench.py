@@ -238,7 +238,8 @@ def run_ours(args) -> dict | None:
         spec = S.GeneratorSpec.random(n_neurons, args.degree, seed=args.seed)
     lay = S.ShardLayout.blocks(n_neurons, world)
     t_build = time.time()
-    net = S.Network.generate(spec, lay, device=dev, shards=[rank], tile_words=args.tile_words)
+    net = S.Network.generate(spec, lay, device=dev, shards=[rank], tile_words=args.tile_words,
+                             bank_order=args.bank_order)
     torch.cuda.synchronize()
     t_build = time.time() - t_build
     lif = S.LifParams()
@@ -479,6 +480,8 @@ def main() -> int:
                     help="ids per exchange message (default: exact bound for p2p, 65536 for nccl, which sends all)")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--tile-words", type=int, default=None, help="force a bitmap tile size (words; tuning)")
+    ap.add_argument("--bank-order", action="store_true",
+                    help="shared-memory bank placement of the synapse entries (tuning; off: measured slower)")
     ap.add_argument("--chunk", type=int, default=100)
     ap.add_argument("--cpu-steps", type=int, default=10)
     ap.add_argument("--no-cpu", action="store_true")

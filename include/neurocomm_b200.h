@@ -375,6 +375,12 @@ int nc_dest_mask_from_csr(const int64_t* slice_ptr, const uint32_t* row_meta, co
                           int32_t n_local,
                           const int32_t* shard_base, int32_t n_shards, int32_t self, uint16_t* dest_mask,
                           void* stream);
+/* Shared-memory bank placement inside each row's E / I segments of a padded
+ * SELL-32 array (src: a copy of it, dst: the array): entry 4u+k of lane l gets a
+ * pre whose bitmap word is in bank (l + 4u + k) mod 32 where the row has one, so
+ * the 32 lookups of one step-kernel instruction hit distinct banks. */
+int nc_sell_bank_order(const int64_t* padded_ptr, const uint32_t* row_meta, int32_t n_tiles, int32_t n_local,
+                       const uint32_t* src, uint32_t* dst, void* stream);
 /* Padded SELL-32 (padded_ptr, as filled by nc_graphgen_fill) <-> J-SELL-32
  * (slice_ptr): to_jagged != 0 copies src (padded) into dst (jagged), else
  * the reverse (dst must be pre-filled; slots past a row's length are left

@@ -252,6 +252,59 @@ __global__ void k_dest_mask(const int64_t* slice_ptr, const uint32_t* row_meta, 
   }
 }
 
+// Shared-memory bank placement (padded SELL-32, before nc_sell_repack).  The
+// step kernel looks entry k of slot u up for all 32 lanes in one shared-memory
+// instruction; its bank is the bitmap word's low 5 bits, (entry >> 5) & 31.
+// Within each E / I segment of a row, entry j = 4u + k of lane l is given a pre
+// in bank (l + j) & 31 where the row has one left (so the 32 lanes of one
+// lookup hit 32 different banks), the rest fill the remaining positions.
+// Thread per (position, tile); src = a copy of the padded array, dst = it.
+__global__ void k_bank_order(const int64_t* pptr, const uint32_t* row_meta, int32_t T, int32_t n_local,
+                             const uint32_t* src, uint32_t* dst) {
+  const int64_t total = (int64_t)n_local * T;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < total;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = x / n_local, p = x % n_local;
+    const int lane = (int)(p & 31);
+    const int64_t base = pptr[(p >> 5) * T + t];
+    const uint32_t meta = row_meta[t * n_local + p];
+    const int emid = (int)(meta & 0xFFFFu), len = (int)(meta >> 16);
+    auto at = [&](int j) { return (base + (int64_t)(j >> 2) * 32 + lane) * 4 + (j & 3); };
+    for (int seg = 0; seg < 2; ++seg) {
+      const int j0 = seg ? 4 * emid : 0, j1 = seg ? 4 * len : 4 * emid;
+      if (j1 <= j0) continue;
+      int cnt[32], seen[32];
+      for (int b = 0; b < 32; ++b) cnt[b] = seen[b] = 0;
+      for (int j = j0; j < j1; ++j) ++cnt[(src[at(j)] >> 5) & 31];
+      auto first = [&](int b) { return j0 + ((b - lane - j0) & 31); };   // first j >= j0 wanting bank b
+      auto cap = [&](int b) { const int f = first(b); return f < j1 ? (j1 - 1 - f) / 32 + 1 : 0; };
+      int ov = 0;
+      for (int j = j0; j < j1; ++j) {
+        const uint32_t e = src[at(j)];
+        const int b = (int)((e >> 5) & 31);
+        const int i = seen[b]++;
+        int target;
+        if (i < cap(b)) {
+          target = first(b) + 32 * i;
+        } else {   // the ov-th free position: the unfilled tails of the banks in short supply
+          int k = ov++;
+          target = j0;
+          for (int c = 0; c < 32; ++c) {
+            const int d = cap(c) - cnt[c];
+            if (d <= 0) continue;
+            if (k < d) {
+              target = first(c) + 32 * (cnt[c] + k);
+              break;
+            }
+            k -= d;
+          }
+        }
+        dst[at(target)] = e;
+      }
+    }
+  }
+}
+
 // Padded SELL-32 (block = longest row x 32 lanes, slot u of lane l at u*32 + l:
 // what the generator fills) <-> J-SELL (jsell.cuh).  Warp per block.
 __global__ void k_sell_repack(const int64_t* pptr, const int64_t* cptr, const uint32_t* row_meta, int32_t T,
@@ -330,6 +383,19 @@ extern "C" int nc_sell_fill_pads(const int64_t* slice_ptr, int64_t n_blocks, int
   (void)n_tiles;
   (void)tile_words;
   k_fill_pads<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(slice_ptr, n_blocks, syn);
+  NC_LAUNCH_CHECK();
+  return NC_OK;
+}
+
+extern "C" int nc_sell_bank_order(const int64_t* padded_ptr, const uint32_t* row_meta, int32_t n_tiles,
+                                  int32_t n_local, const uint32_t* src, uint32_t* dst, void* stream) {
+  if (n_tiles < 1 || n_local < 0 || !padded_ptr || !row_meta || !src || !dst || src == dst) {
+    nc_set_error("nc_sell_bank_order: bad arguments");
+    return NC_E_ARG;
+  }
+  if (n_local == 0) return NC_OK;
+  k_bank_order<<<grid_for((int64_t)n_local * n_tiles, 128), 128, 0, (cudaStream_t)stream>>>(
+      padded_ptr, row_meta, n_tiles, n_local, src, dst);
   NC_LAUNCH_CHECK();
   return NC_OK;
 }

@@ -59,11 +59,11 @@ def plan_tiles(n_words: int, n_local: int, n_sms: int) -> tuple[int, int, bool]:
     part = per * 32 * 4
     global_part = part > budget_all // 4
     budget = min(budget_all, SMEM_TILED) - (0 if global_part else part)
-    tw_max = max(4, budget // 8 // 4 * 4)
+    tw_max = max(32, budget // 8 // 32 * 32)
     T = (n_words + tw_max - 1) // tw_max
     if T > MAX_TILES:
         raise ValueError(f"spike bitmap of {n_words} words needs {T} tiles (max {MAX_TILES})")
-    tw = ((n_words + T - 1) // T + 3) // 4 * 4
+    tw = ((n_words + T - 1) // T + 31) // 32 * 32   # multiple of 32: both buffers start in bank 0
     return T, tw, global_part
 
 

@@ -276,7 +276,7 @@ class Network:
 
     @classmethod
     def generate(cls, spec: GeneratorSpec, layout: ShardLayout, *, device=None, inh_every: int = 5,
-                 shards=None, tile_words: int | None = None) -> "Network":
+                 shards=None, tile_words: int | None = None, bank_order: bool = False) -> "Network":
         """Counter-based device generator (csrc/graphgen.cu); every shard regenerates the same graph."""
         import torch
         if layout.n_neurons != spec.n_neurons:
@@ -332,6 +332,13 @@ class Network:
                                              lower.data_ptr(), syn.data_ptr(), st), "graphgen fill")
             n_real = int(counts.sum().item())
             del upper, counts, lower
+            if bank_order:   # spread each lookup instruction's 32 lanes over the 32 banks (measured on
+                # config 2: shared wavefronts 110 M -> 52 M but the kernel 2.5 % slower: off by default)
+                src = syn.clone()
+                _native.check(L.nc_sell_bank_order(ptr.data_ptr(), meta.data_ptr(), T, n_local, src.data_ptr(),
+                                                   syn.data_ptr(), st), "bank order")
+                torch.cuda.synchronize(dev)
+                del src
             # padded SELL-32 -> J-SELL-32 (drops the padding of every block to its longest row)
             jptr = sell.jagged_ptr(meta, n_local, T)
             jsyn = torch.empty(max(int(jptr[-1].item()) * 4, 4), dtype=torch.int32, device=dev)

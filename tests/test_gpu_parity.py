@@ -233,6 +233,7 @@ def test_device_generator_matches_oracle_and_statistics():
     lay = S.ShardLayout.blocks(spec.n_neurons, 2)
     net = S.Network.generate(spec, lay)
     tiled = S.Network.generate(spec, lay, tile_words=40)
+    banked = S.Network.generate(spec, lay, tile_words=64, bank_order=True)
     # expected undirected edges
     sizes = nc.model.community_sizes(spec.n_neurons, spec.n_communities)
     intra = sum(s * (s - 1) // 2 for s in sizes.tolist()) * spec.p_in
@@ -257,7 +258,7 @@ def test_device_generator_matches_oracle_and_statistics():
     lif = S.LifParams()
     rt_nh = S.ExchangePlan(2, None).next_hop
     ref = c_oracle.simulate_csr(rp, col, qc, lay.owner, 2, rt_nh, lif.constants(4), 50, threads=8)
-    for nw in (net, tiled):
+    for nw in (net, tiled, banked):
         sim = S.Simulator(nw, lif, 4, None, record_raster_steps=50, per_step_counts=True)
         rep = sim.run(50)
         np.testing.assert_array_equal(rep.raster, ref["raster"])
