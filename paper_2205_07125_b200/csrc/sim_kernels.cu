@@ -57,33 +57,45 @@ k_step_fused(const nc_shard_t sh, const nc_lif_params_t p) {
     const int n4 = (sh.n_words + 3) >> 2;
     for (int k = threadIdx.x; k < n4; k += blockDim.x) smem4[k] = ld_keep(src + k);
     __syncthreads();
-    // the next slice's block start and row_meta load while this one streams
-    const int stride = gridDim.x * wpb;
-    int slice = blockIdx.x * wpb + warp;
+    // CTA c owns slices c, c+G, ... (rows are degree ordered, so interleaving
+    // balances the CTAs); its warps claim them dynamically (no tail of warps
+    // with one slice more than others), and the next claim's block start and
+    // row_meta load while the current slice streams
+    const int G = gridDim.x, c = blockIdx.x;
+    const int cnt = c < n_slices ? (n_slices - c + G - 1) / G : 0;
+    __shared__ int next1;
+    if (threadIdx.x == 0) next1 = 0;
+    __syncthreads();
+    auto claim = [&](int64_t& b0, uint32_t& m) {
+      int j = 0;
+      if (lane == 0) j = atomicAdd(&next1, 1);
+      j = __shfl_sync(kFull, j, 0);
+      if (j < cnt) {
+        const int row = ((c + j * G) << 5) + lane;
+        b0 = sh.slice_ptr[c + j * G];
+        m = row < sh.n_local ? sh.row_meta[row] : 0u;
+      }
+      return j;
+    };
     int64_t b0 = 0;
     uint32_t meta = 0u;
-    if (slice < n_slices) {
-      b0 = sh.slice_ptr[slice];
-      meta = (slice << 5) + lane < sh.n_local ? sh.row_meta[(slice << 5) + lane] : 0u;
-    }
-    for (; slice < n_slices; slice += stride) {
-      const int row = (slice << 5) + lane;
-      const int nxt = slice + stride;
+    int j = claim(b0, meta);
+    while (j < cnt) {
       int64_t b0n = 0;
       uint32_t metan = 0u;
-      if (nxt < n_slices) {
-        b0n = sh.slice_ptr[nxt];
-        metan = (nxt << 5) + lane < sh.n_local ? sh.row_meta[(nxt << 5) + lane] : 0u;
-      }
+      const int jn = claim(b0n, metan);
+      const int slice = c + j * G;
+      const int row = (slice << 5) + lane;
       const int32_t acc = sell_row_sum<0>(syn4 + b0, meta, sbm, g_inh, lane, 0u);
-      b0 = b0n;
-      meta = metan;
       if (kLif) {
         const uint32_t fm = update_slice(sh, p, cur, slice, lane, acc, step);
         if (lane == 0) my_spikes += __popc(fm);
       } else if (row < sh.n_local) {
         sh.acc[row] = acc;
       }
+      j = jn;
+      b0 = b0n;
+      meta = metan;
     }
   } else {
     // Tiled: two tile buffers in shared memory, filled by TMA bulk copies that

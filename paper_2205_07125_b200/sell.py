@@ -34,7 +34,7 @@ SMEM_RESERVE = 2048                # static shared memory (tile claim counters, 
 MAX_TILES = 256                    # csrc/sim_kernels.cu kMaxTiles
 
 
-SMEM_TILED = 196 * 1024            # tiled step: shared memory left to L1 for the loads in flight
+SMEM_TILED = 160 * 1024            # tiled step: shared memory left to L1 for the loads in flight
 
 
 def plan_tiles(n_words: int, n_local: int, n_sms: int) -> tuple[int, int, bool]:
@@ -48,7 +48,8 @@ def plan_tiles(n_words: int, n_local: int, n_sms: int) -> tuple[int, int, bool]:
     kernel keeps its shared memory under SMEM_TILED: the rest of the SM's
     256 KB stays L1, which stages the synapse loads in flight (measured on
     B200 at 2/4 GPUs: 0.92/0.85 of HBM peak at 194 KB against 0.78/0.75 at
-    227 KB).  Tiles are equal-sized.
+    227 KB; with the v5 kernel 152 KB beats 196 KB by 1.4 % at 2 GPUs and ties
+    at 4, while every extra tile costs ~1 %).  Tiles are equal-sized.
     """
     budget_all = SMEM_BYTES - SMEM_RESERVE
     whole = (n_words + 3) // 4 * 4
