@@ -253,10 +253,10 @@ def run_ours(args) -> dict | None:
     kms = kernel_ms(sim, main_kernel)
     n_local = lay.n_local(rank)
     csr = net.shards[rank]
-    # algorithmic bytes of one fused step: 4 B per synapse
+    # algorithmic bytes of one fused step: 3.2 B per synapse (16-byte slots of 5)
     # + per neuron row_meta 4/tile, V r/w 8, I r/w 8, refrac r/w 2, gid 4, the slice
     # pointers, + the previous spike bitmap read and the new one written
-    syn_bytes = int(net.n_synapses) * 4
+    syn_bytes = int(net.n_synapses) * 16 // 5
     neuron_bytes = n_local * (4 * csr.n_tiles + 8 + 8 + 2 + 4) + csr.slice_ptr.numel() * 8 + 2 * (lay.n_words * 4)
     alg_bytes = syn_bytes + neuron_bytes
     peaks = load_peaks()
@@ -309,7 +309,7 @@ def run_ours(args) -> dict | None:
                 "delivery": args.delivery, "exchange": "none" if world == 1 else "direct",
                 "firing_rate_hz": round(spikes / n_neurons / (args.steps * 1e-3), 3),
                 "l2": "inputs larger than L2 (synapse array %.2f GB streamed every step)" % (csr.n_entries * 4 / 1e9),
-                "sell_padding": round(csr.n_entries / max(csr.n_real, 1) - 1.0, 4),
+                "sell_padding": round(csr.n_entries * 4 / max(csr.n_real * 3.2, 1) - 1.0, 4),
                 "bitmap_tiles": csr.n_tiles,
                 "graph_build_s": round(t_build, 2),
             },
@@ -480,8 +480,8 @@ def main() -> int:
                     help="ids per exchange message (default: exact bound for p2p, 65536 for nccl, which sends all)")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--tile-words", type=int, default=None, help="force a bitmap tile size (words; tuning)")
-    ap.add_argument("--bank-order", action="store_true",
-                    help="shared-memory bank placement of the synapse entries (tuning; off: measured slower)")
+    ap.add_argument("--no-bank-order", dest="bank_order", action="store_false",
+                    help="skip the shared-memory bank placement of the synapse entries (tuning)")
     ap.add_argument("--chunk", type=int, default=100)
     ap.add_argument("--cpu-steps", type=int, default=10)
     ap.add_argument("--no-cpu", action="store_true")

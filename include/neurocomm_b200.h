@@ -88,22 +88,26 @@ int nc_weight_histogram(const double* weights, const int64_t* assignment, int64_
  * [local_base, local_base + n_local); bitmaps are indexed by internal id.
  *
  * Synapses: each undirected edge (i, j, p) of NeuronGraph is one synapse in
- * each direction.  A pull entry is a packed uint32
- *     (q << 26) | pre_internal_id,      q = ceil(32 * p) in [1, 32].
+ * each direction.  A pull synapse is a 25-bit field
+ *     (q << 19) | (pre_internal_id - first id of its bitmap tile),
+ * q = ceil(32 * p) in [1, 32]; q = 0 is the pad.  Tiles are at most 16384
+ * words, so the tile-relative id fits 19 bits (with one tile it is the
+ * internal id).  A 16-byte slot holds 5 fields, field i at bit 25 i of
+ * (x | y << 32 | z << 64 | w << 96): 3.2 bytes per synapse.
  * Layout "J-SELL-32": jagged sliced ELL with slice = one warp = 32
  * consecutive local rows, further split by bitmap tile t (the spike bitmap is
- * staged in shared memory tile by tile when it exceeds one tile).  Row r of
- * slice s has len_r 16-byte slots (4 entries each) in block (s, t); its slots
- * [0, emid) hold its excitatory pres (weight +q), the next ones its inhibitory
- * pres (weight -g_inh*q): row_meta[row*n_tiles + t] = emid | (len_r << 16).
+ * staged in shared memory tile by tile).  Row r of slice s has len_r slots in
+ * block (s, t); its slots [0, emid) hold its excitatory pres (weight +q), the
+ * next ones its inhibitory pres (weight -g_inh*q), each segment padded to
+ * whole slots with pad fields: row_meta[t*n_local + p] = emid | (len_r << 16)
+ * (p = the row's position, see the placement below).
  * Block (s, t) starts at slice_ptr[s*n_tiles + t] (uint4 units) and stores
  * slot u of every lane with len > u contiguously, in lane order:
  *     position(u, l) = sum_{v<u} cnt_v + #{l' < l : len_l' > u},
  *     cnt_v = #{l : len_l > v},
  * so for u below the block's shortest row it is plain u*32 + l (coalesced
- * 512-byte warp loads) and the block holds no padding beyond each E/I
- * segment rounded up to 4 entries (those hold the pad entry 0: tile-relative
- * id 0 with q = 0).  Each lane owns one row: no cross-lane reduction.
+ * 512-byte warp loads) and the block holds no padding to its longest row.
+ * Each lane owns one row: no cross-lane reduction.
  * Tiled placement: with n_tiles > 1, lane l of block (s, t) works on
  * position p = 32s + l (positions >= n_local hold no row).  CTA c of the
  * tiled step owns slices s = c mod G (G = cta_groups); its rows are numbered
@@ -288,7 +292,7 @@ typedef struct nc_xchg {
 } nc_xchg_t;
 
 /* Inbox words needed per rank for the P2P transport. */
-#define NC_P2P_INBOX_WORDS(n, cap) ((size_t)4 * (size_t)(n) * ((size_t)(cap) + 4))
+#define NC_P2P_INBOX_WORDS(n, cap) ((size_t)8 * (size_t)(n) * ((size_t)(cap) + 1))
 
 int nc_xchg_reset(const nc_xchg_t* X, void* stream);
 /* NCCL path: seal (headers + hop counters), grouped send/recv, scatter. */
@@ -352,8 +356,9 @@ int nc_graphgen_degrees(const nc_graphgen_t* g, int32_t* deg, void* stream);
  * (row, tile, sign) (zero-initialised); tile_words as in nc_shard_t. */
 int nc_graphgen_count(const nc_graphgen_t* g, int32_t n_tiles, int32_t tile_words, int32_t* lower_len,
                       int32_t* upper_len, void* stream);
-/* Pass 2 into the PADDED SELL-32 layout (every block = its longest row x 32
- * lanes, slot u of lane l at padded_ptr[block] + u*32 + l; padded_ptr and
+/* Pass 2 into the UNPACKED PADDED SELL-32 layout (every block = its longest
+ * row x 32 lanes, slot u of lane l = 5 uint32 entries (q << 26 | tile-relative
+ * id) at 5 * (padded_ptr[block] + u*32 + l); padded_ptr and
  * row_meta computed by the host from the pass-1 counts); lower_fill
  * [n_local*n_tiles*2] zero-initialised (slot claims); pos_of[row*n_tiles + t]
  * = position of the row in tile t (inverse of the placement; NULL = identity).  syn must be pre-filled with nc_sell_fill_pads; convert the
@@ -361,8 +366,8 @@ int nc_graphgen_count(const nc_graphgen_t* g, int32_t n_tiles, int32_t tile_word
 int nc_graphgen_fill(const nc_graphgen_t* g, int32_t n_tiles, int32_t tile_words, const int64_t* slice_ptr,
                      const uint32_t* row_meta, const int32_t* pos_of, int32_t* lower_fill, uint32_t* syn,
                      void* stream);
-/* Pad pre-fill of a padded SELL-32 array: every entry = 0 (tile-relative id
- * 0, q = 0).  n_tiles / tile_words are accepted for ABI stability. */
+/* Pad pre-fill of an unpacked padded SELL-32 array: every entry = 0 (q = 0).
+ * n_tiles / tile_words are accepted for ABI stability. */
 int nc_sell_fill_pads(const int64_t* slice_ptr, int64_t n_blocks, int32_t n_tiles, int32_t tile_words,
                       uint32_t* syn, void* stream);
 /* Destination masks from a built CSR (the adjacency is symmetric, so the
@@ -375,9 +380,11 @@ int nc_dest_mask_from_csr(const int64_t* slice_ptr, const uint32_t* row_meta, co
                           int32_t n_local,
                           const int32_t* shard_base, int32_t n_shards, int32_t self, uint16_t* dest_mask,
                           void* stream);
+/* Unpacked padded entries (5 uint32 per slot) -> packed 16-byte slots. */
+int nc_sell_pack(const uint32_t* unpacked, int64_t n_slots, uint32_t* packed, void* stream);
 /* Shared-memory bank placement inside each row's E / I segments of a padded
- * SELL-32 array (src: a copy of it, dst: the array): entry 4u+k of lane l gets a
- * pre whose bitmap word is in bank (l + 4u + k) mod 32 where the row has one, so
+ * SELL-32 array, unpacked (src: a copy of it, dst: the array): entry 5u+k of
+ * lane l gets a pre whose bitmap word is in bank (l + 5u + k) mod 32 where the row has one, so
  * the 32 lookups of one step-kernel instruction hit distinct banks. */
 int nc_sell_bank_order(const int64_t* padded_ptr, const uint32_t* row_meta, int32_t n_tiles, int32_t n_local,
                        const uint32_t* src, uint32_t* dst, void* stream);

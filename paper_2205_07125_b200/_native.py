@@ -112,6 +112,7 @@ _SIGS = {
     "nc_sell_fill_pads": (c_int32, [c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p]),
     "nc_dest_mask_from_csr": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_int32, c_void_p, c_int32,
                                         c_void_p, c_int32, c_int32, c_void_p, c_void_p]),
+    "nc_sell_pack": (c_int32, [c_void_p, c_int64, c_void_p, c_void_p]),
     "nc_sell_bank_order": (c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_void_p]),
     "nc_sell_repack": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_int32,
                                  c_void_p]),

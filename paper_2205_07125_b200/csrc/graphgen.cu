@@ -162,15 +162,16 @@ __global__ void k_degrees(const nc_graphgen_t g, int32_t* deg) {
   }
 }
 
-// Position of the k-th entry of (row, tile, sign) in the SELL-32 layout (uint32 units).
+// Position of the k-th entry of (row, tile, sign) in the unpacked padded SELL-32
+// layout (uint32 units, ncdev::kSlotEntries words per slot; nc_sell_pack packs them).
 __device__ __forceinline__ int64_t sell_pos(const int64_t* slice_ptr, const uint32_t* row_meta,
                                             const int32_t* pos_of, int32_t T, int64_t n_local, int64_t row,
                                             int64_t seg, int32_t k) {
   const int64_t t = (seg >> 1) - row * T;
   const int64_t p = pos_of ? (int64_t)pos_of[row * T + t] : row;   // position of the row in tile t
   const int64_t blk = slice_ptr[(p >> 5) * T + t];
-  const int64_t slot = ((seg & 1) ? (int64_t)(row_meta[t * n_local + p] & 0xFFFFu) : 0) + (k >> 2);
-  return (blk + slot * 32 + (p & 31)) * 4 + (k & 3);
+  const int64_t slot = ((seg & 1) ? (int64_t)(row_meta[t * n_local + p] & 0xFFFFu) : 0) + k / ncdev::kSlotEntries;
+  return (blk + slot * 32 + (p & 31)) * ncdev::kSlotEntries + k % ncdev::kSlotEntries;
 }
 
 // Pass 2: regenerate the same edges and place them; slots inside a
@@ -205,12 +206,27 @@ __global__ void k_fill(const nc_graphgen_t g, int32_t T, int32_t TW, const int64
   }
 }
 
-// Pad pre-fill: entries hold tile-relative ids, so the pad entry (id 0 of
-// the block's tile with q = 0: a staged word, adds nothing) is all zeros.
+// Pad pre-fill of the unpacked padded layout: the pad entry (q = 0) is 0.
 __global__ void k_fill_pads(const int64_t* slice_ptr, int64_t n_blocks, uint32_t* syn) {
-  uint4* s4 = reinterpret_cast<uint4*>(syn);
   for (int64_t b = blockIdx.x; b < n_blocks; b += gridDim.x)
-    for (int64_t k = slice_ptr[b] + threadIdx.x; k < slice_ptr[b + 1]; k += blockDim.x) s4[k] = make_uint4(0, 0, 0, 0);
+    for (int64_t k = slice_ptr[b] * ncdev::kSlotEntries + threadIdx.x; k < slice_ptr[b + 1] * ncdev::kSlotEntries;
+         k += blockDim.x)
+      syn[k] = 0u;
+}
+
+// Unpacked entries (q << 26 | tile-relative id, ncdev::kSlotEntries per slot)
+// -> packed 16-byte slots of 25-bit fields (q << 19 | id).
+__global__ void k_sell_pack(const uint32_t* src, int64_t n_slots, uint4* dst) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n_slots;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t f[ncdev::kSlotEntries];
+#pragma unroll
+    for (int i = 0; i < ncdev::kSlotEntries; ++i) {
+      const uint32_t e = src[s * ncdev::kSlotEntries + i];
+      f[i] = ((e >> 26) << 19) | (e & ncdev::kFieldIdMask);
+    }
+    dst[s] = ncdev::pack_slot(f);
+  }
 }
 
 // Destination shards of every local row: warp per (slice, tile) block, lane =
@@ -235,10 +251,11 @@ __global__ void k_dest_mask(const int64_t* slice_ptr, const uint32_t* row_meta, 
     for (int u = 0; u < hi; ++u) {
       const int pos = ncdev::jsell_pos(u, mine, lane, off);
       if (u >= mine) continue;
-      for (int c = 0; c < 4; ++c) {
-        const uint32_t e = syn[(b0 + pos) * 4 + c];
-        if ((e >> 26) == 0) continue;  // pad
-        const int64_t pre = (e & 0x03FFFFFFu) + tbase;
+      const ncdev::Fields x = ncdev::unpack_slot(reinterpret_cast<const uint4*>(syn)[b0 + pos]);
+      for (int c = 0; c < ncdev::kSlotEntries; ++c) {
+        const uint32_t f = x.f[c] & ncdev::kFieldMask;
+        if ((f >> 19) == 0) continue;  // pad
+        const int64_t pre = (f & ncdev::kFieldIdMask) + tbase;
         for (int h = 0; h < n_shards; ++h)
           if (pre >= shard_base[h] && pre < shard_base[h + 1]) m |= 1u << h;
       }
@@ -255,7 +272,7 @@ __global__ void k_dest_mask(const int64_t* slice_ptr, const uint32_t* row_meta, 
 // Shared-memory bank placement (padded SELL-32, before nc_sell_repack).  The
 // step kernel looks entry k of slot u up for all 32 lanes in one shared-memory
 // instruction; its bank is the bitmap word's low 5 bits, (entry >> 5) & 31.
-// Within each E / I segment of a row, entry j = 4u + k of lane l is given a pre
+// Within each E / I segment of a row, entry j = 5u + k of lane l is given a pre
 // in bank (l + j) & 31 where the row has one left (so the 32 lanes of one
 // lookup hit 32 different banks), the rest fill the remaining positions.
 // Thread per (position, tile); src = a copy of the padded array, dst = it.
@@ -269,9 +286,10 @@ __global__ void k_bank_order(const int64_t* pptr, const uint32_t* row_meta, int3
     const int64_t base = pptr[(p >> 5) * T + t];
     const uint32_t meta = row_meta[t * n_local + p];
     const int emid = (int)(meta & 0xFFFFu), len = (int)(meta >> 16);
-    auto at = [&](int j) { return (base + (int64_t)(j >> 2) * 32 + lane) * 4 + (j & 3); };
+    constexpr int E = ncdev::kSlotEntries;
+    auto at = [&](int j) { return (base + (int64_t)(j / E) * 32 + lane) * E + j % E; };
     for (int seg = 0; seg < 2; ++seg) {
-      const int j0 = seg ? 4 * emid : 0, j1 = seg ? 4 * len : 4 * emid;
+      const int j0 = seg ? E * emid : 0, j1 = seg ? E * len : E * emid;
       if (j1 <= j0) continue;
       int cnt[32], seen[32];
       for (int b = 0; b < 32; ++b) cnt[b] = seen[b] = 0;
@@ -383,6 +401,18 @@ extern "C" int nc_sell_fill_pads(const int64_t* slice_ptr, int64_t n_blocks, int
   (void)n_tiles;
   (void)tile_words;
   k_fill_pads<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(slice_ptr, n_blocks, syn);
+  NC_LAUNCH_CHECK();
+  return NC_OK;
+}
+
+extern "C" int nc_sell_pack(const uint32_t* unpacked, int64_t n_slots, uint32_t* packed, void* stream) {
+  if (n_slots < 0 || (n_slots > 0 && (!unpacked || !packed))) {
+    nc_set_error("nc_sell_pack: bad arguments");
+    return NC_E_ARG;
+  }
+  if (n_slots == 0) return NC_OK;
+  k_sell_pack<<<grid_for(n_slots, 256), 256, 0, (cudaStream_t)stream>>>(unpacked, n_slots,
+                                                                         reinterpret_cast<uint4*>(packed));
   NC_LAUNCH_CHECK();
   return NC_OK;
 }

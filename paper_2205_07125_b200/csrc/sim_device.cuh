@@ -49,15 +49,10 @@ __device__ __forceinline__ uint4 ld_keep(const uint4* p) {
   return r;
 }
 
-// Weight units of one packed entry (q << 26 | pre, pre relative to the staged
+// Weight units of one synapse field (q << 19 | id, id relative to the staged
 // tile) if its pre fired, else 0.  The funnel shift rotates the bitmap word by
-// the low 5 bits of the entry (= pre & 31), so bit 0 is the pre's spike bit;
-// the product folds into an IMAD with the running sum.
-__device__ __forceinline__ uint32_t entry_bit(uint32_t e, const uint32_t* __restrict__ bm) {
-  const uint32_t word = bm[(e & 0x03FFFFFFu) >> 5];
-  return __funnelshift_r(word, word, e) & 1u;
-}
-
+// the low 5 bits of the field (= id & 31), so bit 0 is the pre's spike bit; the
+// product folds into an IMAD with the running sum.
 // bit * q + acc as one IMAD (left to itself the compiler emits ISETP + SEL + IADD)
 __device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t r;
@@ -65,11 +60,18 @@ __device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) 
   return r;
 }
 
-__device__ __forceinline__ int32_t quad_term(uint4 e, const uint32_t* __restrict__ bm) {
-  uint32_t s = mad_u32(entry_bit(e.x, bm), e.x >> 26, 0u);
-  s = mad_u32(entry_bit(e.y, bm), e.y >> 26, s);
-  s = mad_u32(entry_bit(e.z, bm), e.z >> 26, s);
-  s = mad_u32(entry_bit(e.w, bm), e.w >> 26, s);
+__device__ __forceinline__ uint32_t field_term(uint32_t f, const uint32_t* __restrict__ bm, uint32_t acc) {
+  const uint32_t word = bm[(f >> 5) & (kFieldIdMask >> 5)];
+  const uint32_t bit = __funnelshift_r(word, word, f) & 1u;
+  return mad_u32(bit, (f >> 19) & 63u, acc);
+}
+
+// Weight units of the fired pres of one 16-byte slot (5 synapses).
+__device__ __forceinline__ int32_t slot_term(uint4 e, const uint32_t* __restrict__ bm) {
+  const Fields x = unpack_slot(e);
+  uint32_t s = field_term(x.f[0], bm, 0u);
+#pragma unroll
+  for (int i = 1; i < kSlotEntries; ++i) s = field_term(x.f[i], bm, s);
   return (int32_t)s;
 }
 
@@ -124,9 +126,9 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
 constexpr int kPfTiled = NC_PF_DIST;
 
 // Sum over one lane's row of a J-SELL block: returns sum_E - g * sum_I
-// (weight units).  Slots past the lane's own length are not loaded (`pad`
-// stands in: id 0 with q = 0, so its lookup stays in the staged tile and adds
-// nothing).
+// (weight units).  Slots past the lane's own length are not loaded (`pad`, the
+// all-pad slot 0 -- id 0, q = 0 -- stands in: its lookups stay in the staged
+// tile and add nothing).
 template <int kPfDist>
 __device__ __forceinline__ int32_t sell_row_sum(const uint4* __restrict__ blk, uint32_t meta,
                                                 const uint32_t* __restrict__ bm, int32_t g_inh, int lane,
@@ -150,7 +152,7 @@ __device__ __forceinline__ int32_t sell_row_sum(const uint4* __restrict__ blk, u
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       if (u0 + u >= lo) break;   // warp-uniform: no lookups for the pad of a partial group
-      acc += quad_term(e[u], bm) * (u0 + u < emid ? 1 : wi);
+      acc += slot_term(e[u], bm) * (u0 + u < emid ? 1 : wi);
     }
   }
   // ragged tail (short: rows of a block have near-equal lengths)
@@ -165,7 +167,7 @@ __device__ __forceinline__ int32_t sell_row_sum(const uint4* __restrict__ blk, u
 #pragma unroll
     for (int u = 0; u < kTailUnroll; ++u) {
       if (u0 + u >= hi) break;   // warp-uniform
-      acc += quad_term(e[u], bm) * (u0 + u < emid ? 1 : wi);
+      acc += slot_term(e[u], bm) * (u0 + u < emid ? 1 : wi);
     }
   }
   return acc;

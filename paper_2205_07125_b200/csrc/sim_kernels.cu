@@ -432,14 +432,13 @@ __global__ void k_push_build(const nc_shard_t sh, int phase, int64_t* rowptr, in
     for (int u = 0; u < hi; ++u) {
       const int pos = jsell_pos(u, mine, lane, off);
       if (u >= mine) continue;
-      const uint4 e4 = syn4[b0 + pos];
-      const uint32_t es[4] = {e4.x, e4.y, e4.z, e4.w};
+      const Fields x = unpack_slot(syn4[b0 + pos]);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const uint32_t e = es[c];
-        const uint32_t q = e >> 26;
+      for (int c = 0; c < kSlotEntries; ++c) {
+        const uint32_t f = x.f[c] & kFieldMask;
+        const uint32_t q = f >> 19;
         if (q == 0) continue;
-        const uint32_t pre = (e & 0x03FFFFFFu) + (uint32_t)t * (uint32_t)sh.tile_words * 32u;
+        const uint32_t pre = (f & kFieldIdMask) + (uint32_t)t * (uint32_t)sh.tile_words * 32u;
         if (phase == 0) {
           atomicAdd(reinterpret_cast<unsigned long long*>(rowptr + pre + 1), 1ull);
         } else {

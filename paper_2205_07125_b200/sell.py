@@ -25,8 +25,12 @@ from dataclasses import dataclass
 
 import numpy as np
 
-ID_BITS = 26
+ID_BITS = 26                       # unpacked builder entry: (q << 26) | tile-relative id
 ID_MASK = (1 << ID_BITS) - 1
+SLOT_ENTRIES = 5                   # packed slot: 5 fields of 25 bits, (q << 19) | tile-relative id
+FIELD_ID_BITS = 19
+FIELD_MASK = (1 << 25) - 1
+MAX_TILE_WORDS = 1 << (FIELD_ID_BITS - 5)   # 16384 words: tile-relative ids fit 19 bits
 SMEM_BYTES = 227 * 1024            # opt-in dynamic shared memory per CTA on sm_100
 SMEM_RESERVE = 2048                # static shared memory (tile claim counters, mbarriers) + slack
 
@@ -53,14 +57,14 @@ def plan_tiles(n_words: int, n_local: int, n_sms: int) -> tuple[int, int, bool]:
     """
     budget_all = SMEM_BYTES - SMEM_RESERVE
     whole = (n_words + 3) // 4 * 4
-    if whole * 4 <= budget_all:
+    if whole <= MAX_TILE_WORDS and whole * 4 <= min(budget_all, SMEM_TILED):
         return 1, whole, False
     n_slices = (n_local + 31) // 32
     per = (n_slices + n_sms - 1) // n_sms
     part = per * 32 * 4
     global_part = part > budget_all // 4
     budget = min(budget_all, SMEM_TILED) - (0 if global_part else part)
-    tw_max = max(32, budget // 8 // 32 * 32)
+    tw_max = min(MAX_TILE_WORDS, max(32, budget // 8 // 32 * 32))
     T = (n_words + tw_max - 1) // tw_max
     if T > MAX_TILES:
         raise ValueError(f"spike bitmap of {n_words} words needs {T} tiles (max {MAX_TILES})")
@@ -143,7 +147,8 @@ def local_index(perm, cta_groups: int):
 def row_slots(counts, n_local: int, n_tiles: int):
     """[n_local, n_tiles] slots per row and tile from per-(row, tile, sign) entry counts."""
     c = counts.reshape(n_local, n_tiles, 2)
-    return (c[:, :, 0] + 3) // 4 + (c[:, :, 1] + 3) // 4
+    E = SLOT_ENTRIES
+    return (c[:, :, 0] + E - 1) // E + (c[:, :, 1] + E - 1) // E
 
 
 def layout_from_counts(counts, n_local: int, n_tiles: int, perm=None):
@@ -159,8 +164,8 @@ def layout_from_counts(counts, n_local: int, n_tiles: int, perm=None):
         else:
             torch = _torch()
             c = c[perm.to(torch.int64).T, torch.arange(n_tiles, device=c.device)[None, :]]
-    e_slots = (c[:, :, 0] + 3) // 4
-    i_slots = (c[:, :, 1] + 3) // 4
+    e_slots = (c[:, :, 0] + SLOT_ENTRIES - 1) // SLOT_ENTRIES
+    i_slots = (c[:, :, 1] + SLOT_ENTRIES - 1) // SLOT_ENTRIES
     row_slots = e_slots + i_slots
     n_slices = (n_local + 31) // 32
     padded = _zeros(xp, (n_slices * 32, n_tiles), like=row_slots)
@@ -248,7 +253,8 @@ def host_build(row, pre_internal, q, inh, n_local: int, n_tiles: int, tile_words
     perm, pos_of = tile_placement(row_slots(counts, n_local, n_tiles), n_local, n_tiles, cta_groups)
     ptr, meta = layout_from_counts(counts, n_local, n_tiles, perm)
     emid = meta & np.uint32(0xFFFF)
-    syn = np.zeros(int(ptr[-1]) * 4, dtype=np.uint32)   # pad entry 0: tile-relative id 0, q = 0
+    E = SLOT_ENTRIES
+    syn = np.zeros(int(ptr[-1]) * E, dtype=np.uint32)   # unpacked, pad entry 0 (q = 0)
     order = np.argsort(seg, kind="stable")
     sseg = seg[order]
     first = np.cumsum(counts) - counts
@@ -256,14 +262,37 @@ def host_build(row, pre_internal, q, inh, n_local: int, n_tiles: int, tile_words
     r = sseg // 2 // n_tiles
     t = (sseg // 2) % n_tiles
     p = r if pos_of is None else pos_of[r, t].astype(np.int64)           # position of the row in tile t
-    slot = np.where(sseg % 2 == 1, emid.astype(np.int64)[t * n_local + p], 0) + k // 4
-    pos = (ptr[(p // 32) * n_tiles + t] + slot * 32 + (p % 32)) * 4 + (k % 4)
+    slot = np.where(sseg % 2 == 1, emid.astype(np.int64)[t * n_local + p], 0) + k // E
+    pos = (ptr[(p // 32) * n_tiles + t] + slot * 32 + (p % 32)) * E + (k % E)
     rel = pre[order] - (pre[order] >> 5) // tile_words * tile_words * 32     # tile-relative id
     syn[pos] = (np.asarray(q, dtype=np.uint32)[order] << np.uint32(ID_BITS)) | rel.astype(np.uint32)
+    packed = pack_slots(syn)
     gather = jagged_gather(ptr, meta, n_local, n_tiles)
-    jsyn = syn.reshape(-1, 4)[gather].reshape(-1)
+    jsyn = packed.reshape(-1, 4)[gather].reshape(-1)
     return (jagged_ptr(meta, n_local, n_tiles), meta, jsyn,
             None if perm is None else local_index(perm, cta_groups).reshape(-1))
+
+
+def pack_slots(unpacked: np.ndarray) -> np.ndarray:
+    """numpy twin of nc_sell_pack: 5 unpacked entries (q << 26 | id) per slot -> 4 uint32 words."""
+    e = np.asarray(unpacked, dtype=np.uint64).reshape(-1, SLOT_ENTRIES)
+    f = ((e >> np.uint64(ID_BITS)) << np.uint64(FIELD_ID_BITS)) | (e & np.uint64((1 << FIELD_ID_BITS) - 1))
+    lo = f[:, 0] | (f[:, 1] << np.uint64(25)) | ((f[:, 2] & np.uint64((1 << 14) - 1)) << np.uint64(50))
+    hi = (f[:, 2] >> np.uint64(14)) | (f[:, 3] << np.uint64(11)) | (f[:, 4] << np.uint64(36))
+    out = np.empty((e.shape[0], 4), dtype=np.uint32)
+    out[:, 0] = (lo & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+    out[:, 1] = (lo >> np.uint64(32)).astype(np.uint32)
+    out[:, 2] = (hi & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+    out[:, 3] = (hi >> np.uint64(32)).astype(np.uint32)
+    return out.reshape(-1)
+
+
+def unpack_slots(words):
+    """Packed slots ([n, 4] int64 tensor of uint32 words) -> [n, 5] fields (torch)."""
+    x, y, z, w = (words[:, i] for i in range(4))
+    f = [x, (x >> 25) | (y << 7), (y >> 18) | (z << 14), (z >> 11) | (w << 21), w >> 4]
+    import torch
+    return torch.stack(f, 1) & FIELD_MASK
 
 
 def to_padded(csr: SellCSR):
@@ -299,7 +328,7 @@ def decode(csr: SellCSR):
     u, lane = off // 32, off % 32
     s, t = blk_of // T, blk_of % T
     pos = s * 32 + lane                                                     # position in its tile
-    ent = syn[: total * 4].view(-1, 4).to(torch.int64) & 0xFFFFFFFF          # [total, 4]
+    ent = unpack_slots(syn[: total * 4].view(-1, 4).to(torch.int64) & 0xFFFFFFFF)   # [total, 5] fields
     valid_row = pos < csr.n_local
     emid = torch.zeros_like(pos)
     emid[valid_row] = (csr.row_meta.to(torch.int64) & 0xFFFF)[t[valid_row] * csr.n_local + pos[valid_row]]
@@ -310,12 +339,12 @@ def decode(csr: SellCSR):
         c = (pos[valid_row] >> 5) % G
         row[valid_row] = ((c + (k >> 5) * G) << 5) + (k & 31)
     inh = (u >= emid)
-    q = ent >> ID_BITS
+    q = ent >> FIELD_ID_BITS
     keep = (q > 0) & valid_row[:, None]
-    rows4 = row[:, None].expand(-1, 4)[keep]
-    inh4 = inh[:, None].expand(-1, 4)[keep]
-    pre = (ent & ID_MASK) + (t * (csr.tile_words * 32))[:, None]             # back to internal ids
-    return rows4, pre[keep], q[keep], inh4
+    rows5 = row[:, None].expand(-1, SLOT_ENTRIES)[keep]
+    inh5 = inh[:, None].expand(-1, SLOT_ENTRIES)[keep]
+    pre = (ent & ((1 << FIELD_ID_BITS) - 1)) + (t * (csr.tile_words * 32))[:, None]   # back to internal ids
+    return rows5, pre[keep], q[keep], inh5
 
 
 def _xp(a):

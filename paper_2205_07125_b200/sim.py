@@ -38,7 +38,7 @@ __all__ = [
     "q_from_p", "inhibitory_mask", "ID_BITS",
 ]
 
-ID_BITS = sell.ID_BITS  # packed pull entry: (q << 26) | pre internal id
+ID_BITS = sell.ID_BITS  # unpacked builder entry: (q << 26) | tile-relative pre id
 ID_MASK = sell.ID_MASK
 Q_LEVELS = 32           # synaptic weight units: q = ceil(32 p) in [1, 32]
 
@@ -264,7 +264,8 @@ class Network:
             n_local = layout.n_local(h)
             T, TW, pglob = _tiles(layout, n_local, sms, tile_words, partials_global)
             ptr, meta, syn, perm = host_sell(graph, layout, h, inh_every, T, TW, sms)
-            n_real = int(np.count_nonzero((syn >> np.uint32(ID_BITS)) > 0))
+            counts_real = int(np.count_nonzero(layout.owner[np.concatenate([graph.edge_i, graph.edge_j])] == h))
+            n_real = int(counts_real)
             csr = ShardCSR(torch.from_numpy(ptr).to(dev), torch.from_numpy(meta.view(np.int32)).to(dev),
                            torch.from_numpy(syn.view(np.int32)).to(dev), T, TW, n_local, n_real,
                            partials_global=pglob,
@@ -276,7 +277,7 @@ class Network:
 
     @classmethod
     def generate(cls, spec: GeneratorSpec, layout: ShardLayout, *, device=None, inh_every: int = 5,
-                 shards=None, tile_words: int | None = None, bank_order: bool = False) -> "Network":
+                 shards=None, tile_words: int | None = None, bank_order: bool = True) -> "Network":
         """Counter-based device generator (csrc/graphgen.cu); every shard regenerates the same graph."""
         import torch
         if layout.n_neurons != spec.n_neurons:
@@ -322,7 +323,7 @@ class Network:
             perm, pos_of = sell.tile_placement(sell.row_slots(counts, n_local, T), n_local, T, sms)
             ptr, meta = sell.layout_from_counts(counts, n_local, T, perm)
             total = int(ptr[-1].item())
-            syn = torch.zeros(max(total * 4, 4), dtype=torch.int32, device=dev)
+            syn = torch.zeros(max(total * sell.SLOT_ENTRIES, 4), dtype=torch.int32, device=dev)   # unpacked
             _native.check(L.nc_sell_fill_pads(ptr.data_ptr(), ptr.numel() - 1, T, TW, syn.data_ptr(), st),
                           "sell pads")
             lower.zero_()
@@ -332,13 +333,19 @@ class Network:
                                              lower.data_ptr(), syn.data_ptr(), st), "graphgen fill")
             n_real = int(counts.sum().item())
             del upper, counts, lower
-            if bank_order:   # spread each lookup instruction's 32 lanes over the 32 banks (measured on
-                # config 2: shared wavefronts 110 M -> 52 M but the kernel 2.5 % slower: off by default)
+            if bank_order:   # spread each lookup instruction's 32 lanes over the 32 banks (config 2,
+                # packed slots: shared wavefronts 110 M -> 60 M, kernel 1.3 % faster)
                 src = syn.clone()
                 _native.check(L.nc_sell_bank_order(ptr.data_ptr(), meta.data_ptr(), T, n_local, src.data_ptr(),
                                                    syn.data_ptr(), st), "bank order")
                 torch.cuda.synchronize(dev)
                 del src
+            # 5 entries per slot -> 16-byte slots of 25-bit fields
+            packed = torch.empty(max(total * 4, 4), dtype=torch.int32, device=dev)
+            _native.check(L.nc_sell_pack(syn.data_ptr(), total, packed.data_ptr(), st), "sell pack")
+            torch.cuda.synchronize(dev)
+            del syn
+            syn = packed
             # padded SELL-32 -> J-SELL-32 (drops the padding of every block to its longest row)
             jptr = sell.jagged_ptr(meta, n_local, T)
             jsyn = torch.empty(max(int(jptr[-1].item()) * 4, 4), dtype=torch.int32, device=dev)

@@ -31,7 +31,7 @@ def test_host_build_round_trip(n_local, n_tiles, tile_words):
     b = b[np.lexsort(b.T[::-1])]
     np.testing.assert_array_equal(a, b)
     # jagged blocks hold exactly their positions' slots; every row's slots hold its
-    # E entries, then its I entries, each segment padded to a multiple of 4
+    # E entries, then its I entries, each segment padded to a multiple of 5
     if perm is None:
         perm2 = np.tile(np.arange(n_local), (n_tiles, 1))
     else:   # CTA-local index -> row
@@ -47,8 +47,8 @@ def test_host_build_round_trip(n_local, n_tiles, tile_words):
     cnt = np.bincount(seg, minlength=n_local * n_tiles * 2).reshape(n_local, n_tiles, 2)
     for t in range(n_tiles):
         r = perm2[t]
-        np.testing.assert_array_equal(emid[:, t], (cnt[r, t, 0] + 3) // 4)
-        np.testing.assert_array_equal(lens[:, t] - emid[:, t], (cnt[r, t, 1] + 3) // 4)
+        np.testing.assert_array_equal(emid[:, t], (cnt[r, t, 0] + 4) // 5)
+        np.testing.assert_array_equal(lens[:, t] - emid[:, t], (cnt[r, t, 1] + 4) // 5)
         # placement: a permutation that keeps every row inside its CTA's slices,
         # in descending tile-t length within each CTA
         assert sorted(r.tolist()) == list(range(n_local))
@@ -56,9 +56,25 @@ def test_host_build_round_trip(n_local, n_tiles, tile_words):
         for c in range(2):
             own = np.nonzero((np.arange(n_local) >> 5) % 2 == c)[0]
             assert (np.diff(lens[own, t]) <= 0).all() or n_tiles == 1
-    # entries of a tile block hold ids relative to the tile (they index the staged copy)
-    ids = syn & np.uint32(sell.ID_MASK)
-    assert (ids < tile_words * 32).all()
+    # fields of a tile block hold ids relative to the tile (they index the staged copy)
+    f = sell.unpack_slots(torch.from_numpy(syn.astype(np.int64)).view(-1, 4))
+    assert (f & ((1 << sell.FIELD_ID_BITS) - 1) < tile_words * 32).all()
+    assert int((f >> sell.FIELD_ID_BITS > 0).sum()) == m
+
+
+def test_pack_slots_bit_layout():
+    """Field i of a slot sits at bit 25 i of x | y<<32 | z<<64 | w<<96 (include/neurocomm_b200.h)."""
+    rng = np.random.default_rng(2)
+    q = rng.integers(0, 33, (50, 5))
+    ids = rng.integers(0, 1 << 19, (50, 5))
+    unpacked = ((q << 26) | ids).astype(np.uint32)
+    words = sell.pack_slots(unpacked.reshape(-1)).reshape(-1, 4).astype(object)
+    for s_ in range(50):
+        v = sum(int(words[s_, i]) << (32 * i) for i in range(4))
+        for i in range(5):
+            assert (v >> (25 * i)) & ((1 << 25) - 1) == (int(q[s_, i]) << 19) | int(ids[s_, i])
+    f = sell.unpack_slots(torch.from_numpy(sell.pack_slots(unpacked.reshape(-1)).astype(np.int64)).view(-1, 4))
+    np.testing.assert_array_equal(f.numpy(), (q << 19) | ids)
 
 
 def test_jagged_positions_match_the_formula():
@@ -84,6 +100,8 @@ def test_jagged_positions_match_the_formula():
 
 def test_plan_tiles():
     assert sell.plan_tiles(1000, 10_000, 148) == (1, 1000, False)
+    T, tw, _ = sell.plan_tiles(31_252, 1_000_000, 148)   # config 2: two tiles (ids fit 19 bits)
+    assert T == 2 and tw <= sell.MAX_TILE_WORDS
     T, tw, glob = sell.plan_tiles(312_500 + 1, 1_250_000, 148)    # 10 M neurons, 1.25 M local
     assert T > 1 and tw % 4 == 0 and T * tw >= 312_501 and not glob
     per = (1_250_000 // 32 + 147) // 148
