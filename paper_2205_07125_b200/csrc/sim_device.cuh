@@ -61,7 +61,10 @@ __device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) 
 }
 
 __device__ __forceinline__ uint32_t field_term(uint32_t f, const uint32_t* __restrict__ bm, uint32_t acc) {
-  const uint32_t word = bm[(f >> 5) & (kFieldIdMask >> 5)];
+  // byte offset of the bitmap word, added to the (warp-uniform) buffer base by
+  // the load itself: LDS [R + UR], 2 ALU ops per lookup
+  const uint32_t word = *reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(bm) +
+                                                           ((f >> 3) & ((kFieldIdMask >> 5) << 2)));
   const uint32_t bit = __funnelshift_r(word, word, f) & 1u;
   return mad_u32(bit, (f >> 19) & 63u, acc);
 }
