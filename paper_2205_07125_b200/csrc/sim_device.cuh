@@ -51,9 +51,10 @@ __device__ __forceinline__ uint4 ld_keep(const uint4* p) {
 
 // Weight units of one synapse field (q << 19 | id, id relative to the staged
 // tile) if its pre fired, else 0.  The funnel shift rotates the bitmap word by
-// the low 5 bits of the field (= id & 31), so bit 0 is the pre's spike bit; the
-// product folds into an IMAD with the running sum.
-// bit * q + acc as one IMAD (left to itself the compiler emits ISETP + SEL + IADD)
+// the low 5 bits of the field (= id & 31), so bit 0 is the pre's spike bit;
+// bit * q + acc is one IMAD (left to itself the compiler emits ISETP + SEL +
+// IADD).  Moving the bit and q extraction to the FMA pipe (mul.hi tricks)
+// balanced the pipes but measured 2-3 % slower, so this stays on the ALU pipe.
 __device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t r;
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
