@@ -34,7 +34,9 @@ enum {
   NC_E_CUDA = 2,     /* CUDA runtime error                                   */
   NC_E_OVERFLOW = 3, /* a spike bucket exceeded its capacity                 */
   NC_E_TIMEOUT = 4,  /* exchange watchdog expired waiting for a peer flag    */
-  NC_E_NCCL = 5      /* NCCL error                                           */
+  NC_E_NCCL = 5,     /* NCCL error                                           */
+  NC_E_PARSE = 6,    /* malformed NNG / PMAP text (Python: ParseError)       */
+  NC_E_IO = 7        /* file cannot be opened / read / written (OSError)     */
 };
 
 int nc_abi_version(void);
@@ -394,6 +396,26 @@ int nc_sell_bank_order(const int64_t* padded_ptr, const uint32_t* row_meta, int3
  * untouched).  Pointers in uint4 units, n_slices * n_tiles + 1 entries. */
 int nc_sell_repack(const int64_t* padded_ptr, const int64_t* slice_ptr, const uint32_t* row_meta, int32_t n_tiles,
                    int32_t n_local, const uint32_t* src, uint32_t* dst, int32_t to_jagged, void* stream);
+
+/* ---------------------------------------------------------------- text I/O
+ * Native readers / writers of the reference's text artefacts with its exact
+ * acceptance rules and error texts (str.splitlines lines, float()/int()
+ * tokens, repr() in messages); writers emit repr() floats, byte-identical to
+ * the reference.  On NC_E_PARSE, nc_last_error() is the ParseError message and
+ * *err_line its 1-based line.  Read = scan (header counts) + read (arrays of
+ * those sizes, allocated by the caller). */
+/* replaces load_graph model.py:307-364 (with nc_nng_read) */
+int nc_nng_scan(const char* path, int64_t* n_neurons, int64_t* n_edges, int64_t* err_line);
+int nc_nng_read(const char* path, int64_t n_neurons, int64_t n_edges, double* weights, int64_t* edge_i,
+                int64_t* edge_j, double* edge_p, int64_t* err_line);
+/* replaces save_graph model.py:293-304; edges in ascending (i, j) order */
+int nc_nng_write(const char* path, int64_t n_neurons, int64_t n_edges, const double* weights, const int64_t* edge_i,
+                 const int64_t* edge_j, const double* edge_p);
+/* replaces load_partition_map partition.py:278-306 (with nc_pmap_read) */
+int nc_pmap_scan(const char* path, int64_t* n_neurons, int64_t* n_gpus, int64_t* err_line);
+int nc_pmap_read(const char* path, int64_t n_neurons, int64_t n_gpus, int64_t* assignment, int64_t* err_line);
+/* replaces save_partition_map partition.py:270-275 */
+int nc_pmap_write(const char* path, int64_t n_neurons, int64_t n_gpus, const int64_t* assignment);
 
 #ifdef __cplusplus
 }

@@ -17,7 +17,7 @@ LIB_NAME = "libneurocomm_b200.so"
 LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
 ABI_VERSION = 1
 
-NC_OK, NC_E_ARG, NC_E_CUDA, NC_E_OVERFLOW, NC_E_TIMEOUT, NC_E_NCCL = range(6)
+NC_OK, NC_E_ARG, NC_E_CUDA, NC_E_OVERFLOW, NC_E_TIMEOUT, NC_E_NCCL, NC_E_PARSE, NC_E_IO = range(8)
 MAX_SHARDS = 16
 INTERNAL_ID_BITS = 26
 
@@ -112,6 +112,12 @@ _SIGS = {
     "nc_sell_fill_pads": (c_int32, [c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p]),
     "nc_dest_mask_from_csr": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_int32, c_void_p, c_int32,
                                         c_void_p, c_int32, c_int32, c_void_p, c_void_p]),
+    "nc_nng_scan": (c_int32, [C.c_char_p, c_void_p, c_void_p, c_void_p]),
+    "nc_nng_read": (c_int32, [C.c_char_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "nc_nng_write": (c_int32, [C.c_char_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "nc_pmap_scan": (c_int32, [C.c_char_p, c_void_p, c_void_p, c_void_p]),
+    "nc_pmap_read": (c_int32, [C.c_char_p, c_int64, c_int64, c_void_p, c_void_p]),
+    "nc_pmap_write": (c_int32, [C.c_char_p, c_int64, c_int64, c_void_p]),
     "nc_sell_pack": (c_int32, [c_void_p, c_int64, c_void_p, c_void_p]),
     "nc_sell_bank_order": (c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_void_p]),
     "nc_sell_repack": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_int32,
@@ -165,11 +171,17 @@ def exported_symbols() -> list[str]:
     return sorted(_SIGS)
 
 
-def check(rc: int, what: str) -> None:
-    """Translate a non-zero NC_E* code into the reference's exception types."""
+def check(rc: int, what: str, err_line=None) -> None:
+    """Translate a non-zero NC_E* code into the reference's exception types
+    (NC_E_PARSE -> ParseError(message, line) with the reference's message)."""
     if rc == NC_OK:
         return
     msg = (lib().nc_last_error() or b"").decode(errors="replace")
+    if rc == NC_E_PARSE:
+        from .errors import ParseError
+        raise ParseError(msg, int(err_line.value) if err_line is not None else 0)
+    if rc == NC_E_IO:
+        raise OSError(msg)
     if rc == NC_E_ARG:
         raise ValueError(f"{what}: {msg}")
     raise RuntimeError(f"{what} failed (code {rc}): {msg}")

@@ -10,6 +10,8 @@ connection stats, level-2 traffic and the analytic netsim step.  The GPU
 from __future__ import annotations
 
 import hashlib
+import json
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -234,3 +236,48 @@ def test_calibrate_topology_recovers_parameters():
     spec, rows = netsim.calibrate_topology(samples, gt, n)
     for _, _, meas, model in rows:
         assert abs(model - meas) <= 1e-6 * max(1.0, meas)
+
+
+# ------------------------------------------------------------------ native text I/O
+IO = json.loads((Path(__file__).resolve().parent / "golden" / "reference_io.json").read_text())
+
+
+@pytest.mark.parametrize("name", sorted(IO["nng"]))
+def test_nng_reader_matches_reference(tmp_path, name):
+    case = IO["nng"][name]
+    p = tmp_path / "g.nng"
+    p.write_bytes(case["text"].encode())
+    if case["ok"]:
+        g = nc.load_graph(p)
+        assert [float(x).hex() for x in g.weights] == case["weights"]
+        assert [[int(i), int(j), float(q).hex()] for i, j, q in zip(g.edge_i, g.edge_j, g.edge_p)] == case["edges"]
+    else:
+        with pytest.raises(nc.ParseError) as e:
+            nc.load_graph(p)
+        assert str(e.value) == case["message"] and e.value.line == case["line"]
+
+
+@pytest.mark.parametrize("name", sorted(IO["pmap"]))
+def test_pmap_reader_matches_reference(tmp_path, name):
+    from paper_2205_07125_b200.partition import load_partition_map
+    case = IO["pmap"][name]
+    p = tmp_path / "p.pmap"
+    p.write_bytes(case["text"].encode())
+    if case["ok"]:
+        pm = load_partition_map(p)
+        assert pm.n_gpus == case["n_gpus"] and pm.assignment.tolist() == case["assignment"]
+    else:
+        with pytest.raises(nc.ParseError) as e:
+            load_partition_map(p)
+        assert str(e.value) == case["message"] and e.value.line == case["line"]
+
+
+@pytest.mark.parametrize("name", sorted(IO["nng_write"]))
+def test_writers_byte_identical_to_reference(tmp_path, name):
+    from paper_2205_07125_b200.partition import save_partition_map
+    spec = IO["nng_write"][name]["spec"]
+    g = nc.generate_synthetic(nc.ModelSpec(**spec))
+    nc.save_graph(g, tmp_path / "g.nng")
+    assert (tmp_path / "g.nng").read_text() == IO["nng_write"][name]["text"]
+    save_partition_map(nc.partition_greedy(g, 3), tmp_path / "p.pmap")
+    assert (tmp_path / "p.pmap").read_text() == IO["pmap_write"][name]["text"]
