@@ -67,6 +67,14 @@ inline size_t line_break(const char* p, const char* end) {
 
 // Line cursor over the buffer (str.splitlines semantics: no empty last line
 // after a final break).
+struct BreakTable {
+  bool t[256] = {};
+  BreakTable() {
+    for (unsigned char c : {'\n', '\r', '\x0b', '\x0c', '\x1c', '\x1d', '\x1e', '\xc2', '\xe2'}) t[c] = true;
+  }
+};
+const BreakTable kBreaks;
+
 struct Lines {
   const char* p;
   const char* end;
@@ -74,6 +82,10 @@ struct Lines {
     if (p >= end) return false;
     const char* s = p;
     while (p < end) {
+      if (!kBreaks.t[(unsigned char)*p]) {
+        ++p;
+        continue;
+      }
       const size_t k = line_break(p, end);
       if (k) {
         line = std::string_view(s, (size_t)(p - s));
@@ -148,8 +160,12 @@ bool ieq(std::string_view a, const char* b) {
 bool py_float(std::string_view text, double& v) {
   std::string_view s = strip(text);
   std::string tmp;
-  if (!drop_underscores(s, tmp) || tmp.empty()) return false;
-  std::string_view t(tmp);
+  std::string_view t = s;
+  if (s.find('_') != std::string_view::npos) {
+    if (!drop_underscores(s, tmp)) return false;
+    t = tmp;
+  }
+  if (t.empty()) return false;
   bool neg = false;
   if (t[0] == '+' || t[0] == '-') {
     neg = t[0] == '-';
@@ -185,8 +201,12 @@ bool py_float(std::string_view text, double& v) {
 bool py_int(std::string_view text, int64_t& v) {
   std::string_view s = strip(text);
   std::string tmp;
-  if (!drop_underscores(s, tmp) || tmp.empty()) return false;
-  std::string_view t(tmp);
+  std::string_view t = s;
+  if (s.find('_') != std::string_view::npos) {
+    if (!drop_underscores(s, tmp)) return false;
+    t = tmp;
+  }
+  if (t.empty()) return false;
   bool neg = false;
   if (t[0] == '+' || t[0] == '-') {
     neg = t[0] == '-';
@@ -228,6 +248,67 @@ std::string py_repr(std::string_view s) {
 }
 
 // repr() of a float: shortest round-trip digits, fixed for -4 < decpt <= 16, else exponent.
+std::string py_float_repr(double v);
+
+// The same into buf (>= 40 bytes), returns the end; the writers' hot path.
+char* py_float_repr_to(char* buf, double v) {
+  if (!std::isfinite(v) || v == 0.0) {
+    const std::string r = py_float_repr(v);
+    std::memcpy(buf, r.data(), r.size());
+    return buf + r.size();
+  }
+  char sci[40];
+  const auto r = std::to_chars(sci, sci + sizeof(sci), v, std::chars_format::scientific);
+  const char* q = sci;
+  char* o = buf;
+  if (*q == '-') {
+    *o++ = '-';
+    ++q;
+  }
+  char digits[24];
+  int nd = 0;
+  const char* e = q;
+  while (*e != 'e') {
+    if (*e != '.') digits[nd++] = *e;
+    ++e;
+  }
+  int exp10 = 0;
+  std::from_chars(e + 1 + (e[1] == '+' ? 1 : 0), r.ptr, exp10);
+  const int decpt = exp10 + 1;
+  if (decpt <= -4 || decpt > 16) {
+    *o++ = digits[0];
+    if (nd > 1) {
+      *o++ = '.';
+      std::memcpy(o, digits + 1, (size_t)(nd - 1));
+      o += nd - 1;
+    }
+    *o++ = 'e';
+    *o++ = exp10 < 0 ? '-' : '+';
+    const int a = exp10 < 0 ? -exp10 : exp10;
+    if (a < 10) *o++ = '0';
+    o = std::to_chars(o, o + 8, a).ptr;
+  } else if (decpt <= 0) {
+    *o++ = '0';
+    *o++ = '.';
+    for (int i = 0; i < -decpt; ++i) *o++ = '0';
+    std::memcpy(o, digits, (size_t)nd);
+    o += nd;
+  } else if (decpt >= nd) {
+    std::memcpy(o, digits, (size_t)nd);
+    o += nd;
+    for (int i = nd; i < decpt; ++i) *o++ = '0';
+    *o++ = '.';
+    *o++ = '0';
+  } else {
+    std::memcpy(o, digits, (size_t)decpt);
+    o += decpt;
+    *o++ = '.';
+    std::memcpy(o, digits + decpt, (size_t)(nd - decpt));
+    o += nd - decpt;
+  }
+  return o;
+}
+
 std::string py_float_repr(double v) {
   if (std::isnan(v)) return "nan";
   if (std::isinf(v)) return v < 0 ? "-inf" : "inf";
@@ -293,8 +374,8 @@ int parse_header(std::string_view line, const char* tag, bool separate_version, 
 class Writer {
  public:
   explicit Writer(FILE* f) : f_(f) { buf_.reserve(1 << 20); }
-  void put(const std::string& s) {
-    buf_ += s;
+  void put(const std::string& s) { buf_ += s; }
+  void maybe_flush() {
     if (buf_.size() >= (1u << 20)) flush();
   }
   void put_int(int64_t v) {
@@ -302,6 +383,11 @@ class Writer {
     const auto r = std::to_chars(b, b + sizeof(b), v);
     buf_.append(b, r.ptr);
   }
+  void put_float(double v) {
+    char b[48];
+    buf_.append(b, py_float_repr_to(b, v));
+  }
+  void put_char(char c) { buf_.push_back(c); }
   bool flush() {
     const bool ok = std::fwrite(buf_.data(), 1, buf_.size(), f_) == buf_.size();
     buf_.clear();
@@ -398,12 +484,19 @@ extern "C" int nc_nng_write(const char* path, int64_t m, int64_t e, const double
   w.put(" ");
   w.put_int(e);
   w.put("\n");
-  for (int64_t k = 0; k < m; ++k) w.put(py_float_repr(weights[k]) + "\n");
+  for (int64_t k = 0; k < m; ++k) {
+    w.put_float(weights[k]);
+    w.put_char('\n');
+    w.maybe_flush();
+  }
   for (int64_t k = 0; k < e; ++k) {
     w.put_int(edge_i[k]);
-    w.put(" ");
+    w.put_char(' ');
     w.put_int(edge_j[k]);
-    w.put(" " + py_float_repr(edge_p[k]) + "\n");
+    w.put_char(' ');
+    w.put_float(edge_p[k]);
+    w.put_char('\n');
+    w.maybe_flush();
   }
   const bool ok = w.flush();
   if (std::fclose(f) != 0 || !ok) {
@@ -464,7 +557,8 @@ extern "C" int nc_pmap_write(const char* path, int64_t m, int64_t n, const int64
   w.put("\n");
   for (int64_t k = 0; k < m; ++k) {
     w.put_int(assignment[k]);
-    w.put("\n");
+    w.put_char('\n');
+    w.maybe_flush();
   }
   const bool ok = w.flush();
   if (std::fclose(f) != 0 || !ok) {

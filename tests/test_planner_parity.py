@@ -281,3 +281,16 @@ def test_writers_byte_identical_to_reference(tmp_path, name):
     assert (tmp_path / "g.nng").read_text() == IO["nng_write"][name]["text"]
     save_partition_map(nc.partition_greedy(g, 3), tmp_path / "p.pmap")
     assert (tmp_path / "p.pmap").read_text() == IO["pmap_write"][name]["text"]
+
+
+def test_writer_float_repr_fuzz(tmp_path):
+    """The native writer's float text equals Python repr() (shortest round trip, fixed/exponent switch)."""
+    rng = np.random.default_rng(0)
+    vals = np.concatenate([rng.random(3000), rng.random(500) * 1e-6, rng.random(500) * 1e20,
+                           10.0 ** rng.integers(-30, 30, 500).astype(np.float64),
+                           [1.0, 0.5, 1e16, 1e15, 123456789012345678.0, 1e-4, 1e-5, 0.1, 2.0 ** -1074,
+                            1.7976931348623157e308, 9999999999999998.0]])
+    g = nc.NeuronGraph(vals.size, vals, np.zeros(0, np.int64), np.zeros(0, np.int64), np.zeros(0))
+    nc.save_graph(g, tmp_path / "f.nng")
+    lines = (tmp_path / "f.nng").read_text().splitlines()[1:]
+    assert lines == [repr(float(x)) for x in vals]
