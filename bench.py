@@ -219,6 +219,7 @@ def run_ours(args) -> dict | None:
     import torch
     import torch.distributed as dist
 
+    from paper_2205_07125_b200 import sell
     from paper_2205_07125_b200 import sim as S
 
     rank, world, local = dist_env()
@@ -249,8 +250,9 @@ def run_ours(args) -> dict | None:
     clocks = ClockSampler(local)
     ms, spikes, lat, lat_max = time_steps(sim, args, world, dev, clocks)
     value = args.steps / (ms * 1e-3)
-    main_kernel = "fused" if args.delivery == "fused" else "push"
-    kms = kernel_ms(sim, main_kernel)
+    main_kernel = {"fused": "fused", "push": "push"}.get(args.delivery, "step")
+    # binned / persistent engines: one kernel (or one launch) per step, timed as the step
+    kms = kernel_ms(sim, main_kernel) if main_kernel != "step" else ms / args.steps
     n_local = lay.n_local(rank)
     csr = net.shards[rank]
     # algorithmic bytes of one fused step: 3.2 B per synapse (16-byte slots of 5)
@@ -261,9 +263,14 @@ def run_ours(args) -> dict | None:
     alg_bytes = syn_bytes + neuron_bytes
     peaks = load_peaks()
     if main_kernel != "fused":
-        # event-driven headline: the push kernel moves 12 B per delivered synapse
         fired_syn = spikes / max(args.steps, 1) * args.degree / max(world, 1)
-        alg_bytes = fired_syn * 12
+        if args.delivery == "binned":
+            # per spike and bin a 32-byte sector of bin offsets, 4 B per delivered synapse,
+            # + LIF state r/w 22 B per neuron
+            alg_bytes = spikes / max(args.steps, 1) * sell.device_sms(dev) * 32 + fired_syn * 4 + n_local * 22
+        else:
+            # the push kernel moves 12 B per delivered synapse
+            alg_bytes = fired_syn * 12
     achieved = alg_bytes / (kms * 1e-3) / 1e9
     traffic = None
     prof = ROOT / "profiles" / "ncu_step_fused.json"
@@ -280,17 +287,19 @@ def run_ours(args) -> dict | None:
     if args.with_push and args.delivery == "fused":
         psim = make_sim(net, lif, args, args.event, world)
         pms, pspikes, plat, plat_max = time_steps(psim, args, world, dev)
-        push_ms = kernel_ms(psim, "push")
-        lif_ms = kernel_ms(psim, "lif")
         fired_syn = pspikes / max(args.steps, 1) * args.degree / max(world, 1)
-        push_bytes = fired_syn * 12          # 4 B entry read + 4 B read + 4 B write per reduction
         event = {"engine": args.event, "value": round(args.steps / (pms * 1e-3), 2),
                  "ms_per_step": round(pms / args.steps, 5),
-                 "push_kernel_ms": round(push_ms, 5), "lif_kernel_ms": round(lif_ms, 5),
-                 "push_bound": "L2 atomics: %.3g reductions/s" % (fired_syn / (push_ms * 1e-3)),
-                 "push_achieved_gbs": round(push_bytes / (push_ms * 1e-3) / 1e9, 1),
+                 "delivered_synapses_per_step": round(fired_syn, 1),
                  "exchange_us": lat_summary(plat, plat_max, args.transport),
                  "gpu_launches": max(1, int(round(args.steps * psim.launches_per_step())))}
+        if args.event in ("push", "persistent"):
+            push_ms = kernel_ms(psim, "push")
+            lif_ms = kernel_ms(psim, "lif")
+            push_bytes = fired_syn * 12          # 4 B entry read + 4 B read + 4 B write per reduction
+            event.update({"push_kernel_ms": round(push_ms, 5), "lif_kernel_ms": round(lif_ms, 5),
+                          "push_bound": "L2 atomics: %.3g reductions/s" % (fired_syn / (push_ms * 1e-3)),
+                          "push_achieved_gbs": round(push_bytes / (push_ms * 1e-3) / 1e9, 1)})
         if world > 1:
             psim.close()
         del psim
@@ -315,7 +324,7 @@ def run_ours(args) -> dict | None:
             },
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": traffic,
-                         "kernel": "k_step_fused" if args.delivery == "fused" else "k_deliver_push",
+                         "kernel": {"fused": "k_step_fused", "push": "k_deliver_push", "binned": "k_step_binned (whole step)"}.get(args.delivery, "k_persistent (whole step)"),
                          "kernel_ms": round(kms, 5), "algorithmic_bytes": int(alg_bytes),
                          "peak_source": peaks["source"]},
             "event_driven": event,
@@ -472,8 +481,8 @@ def main() -> int:
     ap.add_argument("--degree", type=float, default=1000.0)
     ap.add_argument("--communities", type=int, default=1, help=">1: regional SBM (config 5 family)")
     ap.add_argument("--intra-frac", type=float, default=0.9, help="regional: fraction of synapses inside a region")
-    ap.add_argument("--delivery", default="fused", choices=["fused", "push", "persistent"])
-    ap.add_argument("--event", default="persistent", choices=["push", "persistent"],
+    ap.add_argument("--delivery", default="fused", choices=["fused", "push", "persistent", "binned"])
+    ap.add_argument("--engine", dest="event", default="persistent", choices=["push", "persistent", "binned"],
                     help="event-driven variant reported beside the headline")
     ap.add_argument("--transport", default="p2p", choices=["nccl", "p2p"])
     ap.add_argument("--msg-cap", type=int, default=None,

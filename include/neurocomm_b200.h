@@ -188,7 +188,23 @@ typedef struct nc_shard {
                               at position p of tile t (NULL = identity)         */
   int32_t cta_groups;     /* G the placement was built for (CTA c owns slices
                              c, c+G, ...); the tiled step launches G CTAs       */
-  int32_t pad2;
+  int32_t pb_bins;        /* binned push (optional): B target bins = CTAs      */
+  /* binned push synapses: rows = internal pre ids, each row's entries grouped
+   * by the bin of their post row (bin c = local rows [c*pb_rows, (c+1)*pb_rows)),
+   * entry = (inh << 31) | ((q - 1) << 26) | (post_local - c*pb_rows);
+   * bin c of pre i = pb_syn[pb_rowptr[i] + pb_binoff[i*(B+1) + c] ...
+   * pb_rowptr[i] + pb_binoff[i*(B+1) + c + 1]) */
+  const int64_t* pb_rowptr;
+  const uint16_t* pb_binoff;
+  const uint32_t* pb_syn;
+  int32_t pb_rows;        /* local rows per bin (multiple of 32)               */
+  int32_t pad3;
+  /* spike lists by step parity (binned delivery): the local spikes of step t
+   * (LIF) and the remote ones (exchange) are appended to list t&1, which the
+   * step t+1 kernel reads; nc_sim_end_step empties list (t+1)&1 */
+  uint32_t* spk_ids;      /* [2][spk_cap] */
+  int32_t* spk_count;     /* [2] */
+  int64_t spk_cap;
 } nc_shard_t;
 
 /* Set kernel attributes (dynamic shared memory opt-in) once; call before any
@@ -222,6 +238,19 @@ int nc_sim_lif_update(const nc_shard_t* sh, const nc_lif_params_t* p, void* stre
  * (zero-initialised int64[n_words*32+1]); the caller prefix-sums push_rowptr;
  * phase 1 writes the entries (push_fill int32[n_words*32] zero-initialised).
  * The shard's slice_ptr/row_meta/syn must be set; push fields are ignored. */
+/* Binned push synapses (see nc_shard_t) from the pull arrays of the shard.
+ * phase 0: counts[pre*B + bin] += 1 (uint32, zeroed, n_pre*B); the host turns
+ * them into pb_rowptr / pb_binoff (per-row prefix, < 65536 entries per row);
+ * phase 1: places the entries, claiming slots with atomics on `fill`
+ * (uint32 [n_pre*B], zeroed).  Uses sh->pb_bins / pb_rows for the bins. */
+int nc_build_push_binned(const nc_shard_t* sh, int32_t phase, uint32_t* counts, const int64_t* pb_rowptr,
+                         const uint16_t* pb_binoff, uint32_t* fill, uint32_t* pb_syn, void* stream);
+/* Event-driven step with binned push (replaces push + LIF + end-of-step
+ * bucketing): CTA c owns the rows of bin c, reads the spike list of step t-1,
+ * sums the weights of its bin of every spiking pre in shared memory (integer,
+ * order free), then runs K1 + K2 on its rows and appends its spikes to list
+ * t&1.  Launches pb_bins CTAs; needs pb_* and spk_*. */
+int nc_sim_step_binned(const nc_shard_t* sh, const nc_lif_params_t* p, void* stream);
 int nc_build_push_csr(const nc_shard_t* sh, int32_t phase, int64_t* push_rowptr, int32_t* push_fill,
                       uint32_t* push_syn, void* stream);
 
@@ -288,6 +317,9 @@ typedef struct nc_xchg {
   uint32_t* barrier;               /* in-kernel grid barrier counter            */
   unsigned long long* lat_start;
   uint32_t* lat_ns;                /* per-step exchange latency (ns) or NULL    */
+  uint32_t* spk_ids;               /* binned delivery: append received ids to the  */
+  int32_t* spk_count;              /* step's spike list ([2][spk_cap], [2]) or NULL */
+  int64_t spk_cap;
   unsigned long long* dbg;         /* diagnostics or NULL: [64 steps][n*B blocks][4]
                                       globaltimer at block start, message published,
                                       peer flag seen, inbound ids scattered      */

@@ -50,7 +50,9 @@ class ShardC(C.Structure):
         ("status", c_void_p), ("step", c_void_p),
         ("raster", c_void_p), ("record_steps", c_int32), ("local_words", c_int32),
         ("spike_total", c_void_p), ("work", c_void_p),
-        ("row_perm", c_void_p), ("cta_groups", c_int32), ("pad2", c_int32),
+        ("row_perm", c_void_p), ("cta_groups", c_int32), ("pb_bins", c_int32),
+        ("pb_rowptr", c_void_p), ("pb_binoff", c_void_p), ("pb_syn", c_void_p), ("pb_rows", c_int32),
+        ("pad3", c_int32), ("spk_ids", c_void_p), ("spk_count", c_void_p), ("spk_cap", c_int64),
     ]
 
 
@@ -83,7 +85,8 @@ class XchgC(C.Structure):
         ("my_inbox", c_void_p), ("my_flags", c_void_p),
         ("peer_inbox", c_void_p * MAX_SHARDS), ("peer_flags", c_void_p * MAX_SHARDS),
         ("done", c_void_p), ("send_done", c_void_p), ("blocks_per_peer", c_int32), ("pad1", c_int32),
-        ("barrier", c_void_p), ("lat_start", c_void_p), ("lat_ns", c_void_p), ("dbg", c_void_p),
+        ("barrier", c_void_p), ("lat_start", c_void_p), ("lat_ns", c_void_p),
+        ("spk_ids", c_void_p), ("spk_count", c_void_p), ("spk_cap", c_int64), ("dbg", c_void_p),
     ]
 
 
@@ -118,6 +121,9 @@ _SIGS = {
     "nc_pmap_scan": (c_int32, [C.c_char_p, c_void_p, c_void_p, c_void_p]),
     "nc_pmap_read": (c_int32, [C.c_char_p, c_int64, c_int64, c_void_p, c_void_p]),
     "nc_pmap_write": (c_int32, [C.c_char_p, c_int64, c_int64, c_void_p]),
+    "nc_build_push_binned": (c_int32, [C.POINTER(ShardC), c_int32, c_void_p, c_void_p, c_void_p, c_void_p,
+                                       c_void_p, c_void_p]),
+    "nc_sim_step_binned": (c_int32, [C.POINTER(ShardC), C.POINTER(LifParamsC), c_void_p]),
     "nc_sell_pack": (c_int32, [c_void_p, c_int64, c_void_p, c_void_p]),
     "nc_sell_bank_order": (c_int32, [c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_void_p]),
     "nc_sell_repack": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_int32,

@@ -64,7 +64,7 @@ __global__ void k_scatter(const nc_xchg_t X, int phase) {
   if (cnt > X.cap) cnt = X.cap;
   const uint32_t* ids = (phase == 1 ? X.recv_ids : X.recv2_ids) + (int64_t)src * X.cap;
   uint32_t* cur = (step & 1) ? X.bitmap1 : X.bitmap0;
-  scatter_ids(X, ids, cnt, src, phase == 2, cur, step_row(X.deliv_ids, X, step), X.status);
+  scatter_ids(X, ids, cnt, src, phase == 2, cur, step_row(X.deliv_ids, X, step), X.status, step);
 }
 
 __global__ void k_reset_fwd(const nc_xchg_t X) {

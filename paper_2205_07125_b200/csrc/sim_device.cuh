@@ -298,16 +298,23 @@ constexpr int kLifThreads = 256;
 constexpr int kLifWarps = kLifThreads / 32;
 constexpr int kLifMaxTiles = 2048;   // tiles per CTA (fmask storage: 8 KB)
 
-struct LifSmem {
+template <int kWarps>
+struct LifSmemT {
   unsigned int block_count;
   uint32_t fmask_s[kLifMaxTiles];
-  int warp_cnt[kLifWarps][NC_MAX_SHARDS + 1];
+  int warp_cnt[kWarps][NC_MAX_SHARDS + 1];
   int cta_base[NC_MAX_SHARDS + 1];
 };
+using LifSmem = LifSmemT<kLifWarps>;
 
-// One LIF phase of step `step` for block `bid` of `nblk` (blockDim = kLifThreads).
+// One LIF phase of step `step` for block `bid` of `nblk` (blockDim = 32 *
+// kWarps).  Block bid owns the 32-row tiles [bid*per, (bid+1)*per).  The
+// synaptic input comes from acc (consumed and zeroed) or, when sacc is given,
+// from shared memory indexed by the row's offset in the block's range.  The
+// fired list is sh.fired_ids, or the step's spike list when sh.spk_ids is set.
+template <int kWarps>
 static __device__ void lif_phase(const nc_shard_t& sh, const nc_lif_params_t& p, int step, int bid, int nblk,
-                          LifSmem& S) {
+                                 LifSmemT<kWarps>& S, const int32_t* sacc = nullptr) {
   unsigned int& block_count = S.block_count;
   uint32_t* fmask_s = S.fmask_s;
   auto& warp_cnt = S.warp_cnt;
@@ -315,9 +322,12 @@ static __device__ void lif_phase(const nc_shard_t& sh, const nc_lif_params_t& p,
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int nq = sh.n_shards > 1 ? sh.n_shards : 0;      // buckets in use
-  const int nb = nq + (sh.fired_ids ? 1 : 0);            // + the fired list (slot nq)
+  uint32_t* fired_ids = sh.spk_ids ? sh.spk_ids + (int64_t)(step & 1) * sh.spk_cap : sh.fired_ids;
+  int32_t* fired_count = sh.spk_ids ? sh.spk_count + (step & 1) : sh.fired_count;
+  const int64_t fired_cap = sh.spk_ids ? sh.spk_cap : sh.n_local;
+  const int nb = nq + (fired_ids ? 1 : 0);               // + the fired list (slot nq)
   if (threadIdx.x == 0) block_count = 0;
-  for (int k = threadIdx.x; k < kLifWarps * (NC_MAX_SHARDS + 1); k += blockDim.x)
+  for (int k = threadIdx.x; k < kWarps * (NC_MAX_SHARDS + 1); k += blockDim.x)
     (&warp_cnt[0][0])[k] = 0;
   __syncthreads();
   uint32_t* cur = (step & 1) ? sh.bitmap1 : sh.bitmap0;
@@ -327,15 +337,20 @@ static __device__ void lif_phase(const nc_shard_t& sh, const nc_lif_params_t& p,
   const int t0 = bid * per, t1 = min(ntiles, t0 + per);
   uint32_t my_spikes = 0;
   // ---- pass A: update, spike masks, per-warp bucket counts
-  for (int tile = t0 + warp; tile < t1; tile += kLifWarps) {
+  for (int tile = t0 + warp; tile < t1; tile += kWarps) {
     const int row = (tile << 5) + lane;
     bool fired = false;
     if (row < sh.n_local) {
       float v = sh.v[row];
       float isyn = sh.i_syn[row];
       uint8_t ref = sh.refrac[row];
-      const int32_t a = sh.acc[row];
-      sh.acc[row] = 0;
+      int32_t a;
+      if (sacc) {
+        a = sacc[row - (t0 << 5)];
+      } else {
+        a = sh.acc[row];
+        sh.acc[row] = 0;
+      }
       fired = lif_step(v, isyn, ref, a, sh.gid[row], (uint32_t)step, p);
       sh.v[row] = v;
       sh.i_syn[row] = isyn;
@@ -361,18 +376,18 @@ static __device__ void lif_phase(const nc_shard_t& sh, const nc_lif_params_t& p,
   if ((int)threadIdx.x < nb) {
     const int h = threadIdx.x;
     int total = 0;
-    for (int w = 0; w < kLifWarps; ++w) {
+    for (int w = 0; w < kWarps; ++w) {
       const int c = warp_cnt[w][h];
       warp_cnt[w][h] = total;  // exclusive prefix = the warp's base
       total += c;
     }
-    int32_t* cnt = h < nq ? sh.bucket_count + h : sh.fired_count;
+    int32_t* cnt = h < nq ? sh.bucket_count + h : fired_count;
     cta_base[h] = total ? atomicAdd(cnt, total) : 0;
   }
   __syncthreads();
   // ---- pass B: write ids
   if (nb) {
-    for (int tile = t0 + warp; tile < t1; tile += kLifWarps) {
+    for (int tile = t0 + warp; tile < t1; tile += kWarps) {
       const uint32_t fmask = fmask_s[tile - t0];
       if (!fmask) continue;
       const int row = (tile << 5) + lane;
@@ -383,8 +398,8 @@ static __device__ void lif_phase(const nc_shard_t& sh, const nc_lif_params_t& p,
         const uint32_t m = (h < nq) ? __ballot_sync(kFull, (hm >> h) & 1u) : fmask;
         if ((m >> lane) & 1u) {
           const int64_t pos = (int64_t)cta_base[h] + warp_cnt[warp][h] + __popc(m & ((1u << lane) - 1u));
-          const int64_t cap = h < nq ? sh.bucket_cap : sh.n_local;
-          if (pos < cap) (h < nq ? sh.bucket_ids + (int64_t)h * sh.bucket_cap : sh.fired_ids)[pos] = my_id;
+          const int64_t cap = h < nq ? sh.bucket_cap : fired_cap;
+          if (pos < cap) (h < nq ? sh.bucket_ids + (int64_t)h * sh.bucket_cap : fired_ids)[pos] = my_id;
           else atomicExch(sh.status, 1);
         }
         __syncwarp();

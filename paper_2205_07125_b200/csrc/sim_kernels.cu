@@ -28,6 +28,7 @@ using namespace ncdev;
 
 constexpr int kThreads = 1024;    // one CTA per SM in the smem-bitmap variant
 constexpr int kMaxTiles = 256;    // bitmap tiles per shard (sell.py plan_tiles)
+__global__ void __launch_bounds__(1024, 1) k_step_binned(const nc_shard_t sh, const nc_lif_params_t p);
 // K3 (+K1+K2 when kLif).  kTiled: the bitmap does not fit in shared memory;
 // every CTA owns a fixed range of slices, loops over the bitmap tiles and
 // keeps the per-row partial sums in shared memory behind the tile.
@@ -221,6 +222,7 @@ __global__ void k_end_step(const nc_shard_t sh) {
   if (t < 4 && sh.work) sh.work[t] = 0u;
   if (t == 0) {
     if (sh.fired_count) *sh.fired_count = 0;
+    if (sh.spk_count) sh.spk_count[(*sh.step + 1) & 1] = 0;   // the list step + 1 appends to
     *sh.step += 1;
   }
 }
@@ -243,6 +245,7 @@ __global__ void k_init(const nc_shard_t sh, const nc_lif_params_t p) {
   }
   if (t0 < sh.n_shards) sh.bucket_count[t0] = 0;
   if (t0 < 4 && sh.work) sh.work[t0] = 0u;
+  if (t0 < 2 && sh.spk_count) sh.spk_count[t0] = 0;
   if (t0 == 0) {
     *sh.step = 0;
     sh.status[0] = 0;
@@ -338,6 +341,7 @@ extern "C" int nc_sim_prepare(void) {
   if (int e = opt_in_smem(k_step_fused<true, false>, optin)) return e;
   if (int e = opt_in_smem(k_step_fused<true, true, true>, optin)) return e;
   if (int e = opt_in_smem(k_step_fused<true, false, true>, optin)) return e;
+  if (int e = opt_in_smem(k_step_binned, optin)) return e;
   g_prepared = true;
   return NC_OK;
 }
@@ -449,6 +453,107 @@ __global__ void k_push_build(const nc_shard_t sh, int phase, int64_t* rowptr, in
     }
   }
 }
+
+// Binned push: same walk over the pull synapses as k_push_build; the bin of a
+// synapse is the CTA that owns its post row in k_step_binned.
+__global__ void k_push_binned(const nc_shard_t sh, int phase, uint32_t* counts, const int64_t* rowptr,
+                              const uint16_t* binoff, uint32_t* fill, uint32_t* out) {
+  const int lane = threadIdx.x & 31;
+  const int T = sh.n_tiles;
+  const int B = sh.pb_bins, R = sh.pb_rows;
+  const int n_slices = (sh.n_local + 31) >> 5;
+  const int64_t n_blocks = (int64_t)n_slices * T;
+  const uint4* syn4 = reinterpret_cast<const uint4*>(sh.syn);
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t blk = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; blk < n_blocks; blk += nw) {
+    const int slice = (int)(blk / T), t = (int)(blk % T);
+    const int pos = (slice << 5) + lane;
+    const int row = pos < sh.n_local ? (int)placed_row(sh.row_perm, sh.n_local, sh.cta_groups, t, pos) : pos;
+    const int64_t b0 = sh.slice_ptr[blk];
+    const uint32_t meta = pos < sh.n_local ? sh.row_meta[(int64_t)t * sh.n_local + pos] : 0u;
+    const int emid = (int)(meta & 0xFFFFu), mine = (int)(meta >> 16);
+    const int hi = (int)__reduce_max_sync(0xffffffffu, (unsigned)mine);
+    const int bin = row / R;
+    const uint32_t rel = (uint32_t)(row - bin * R);
+    int off = 0;
+    for (int u = 0; u < hi; ++u) {
+      const int p = jsell_pos(u, mine, lane, off);
+      if (u >= mine) continue;
+      const Fields x = unpack_slot(syn4[b0 + p]);
+#pragma unroll
+      for (int c = 0; c < kSlotEntries; ++c) {
+        const uint32_t f = x.f[c] & kFieldMask;
+        const uint32_t q = f >> 19;
+        if (q == 0) continue;
+        const uint32_t pre = (f & kFieldIdMask) + (uint32_t)t * (uint32_t)sh.tile_words * 32u;
+        const int64_t key = (int64_t)pre * B + bin;
+        if (phase == 0) {
+          atomicAdd(counts + key, 1u);
+        } else {
+          const uint32_t k = atomicAdd(fill + key, 1u);
+          out[rowptr[pre] + binoff[(int64_t)pre * (B + 1) + bin] + k] =
+              ((u >= emid ? 1u : 0u) << 31) | ((q - 1u) << 26) | rel;
+        }
+      }
+    }
+  }
+}
+
+// One event-driven step with binned push (see nc_sim_step_binned).
+constexpr int kBinThreads = 1024;
+constexpr int kBinWarps = kBinThreads / 32;
+
+__global__ void __launch_bounds__(kBinThreads, 1) k_step_binned(const nc_shard_t sh, const nc_lif_params_t p) {
+  extern __shared__ int32_t sacc[];
+  __shared__ LifSmemT<kBinWarps> S;
+  const int step = *sh.step;
+  const int c = blockIdx.x, B = sh.pb_bins, R = sh.pb_rows;
+  const int32_t negg = -p.g_inh;
+  for (int k = threadIdx.x; k < R; k += blockDim.x) sacc[k] = 0;
+  __syncthreads();
+  // the spikes of step - 1 (local from that step's LIF, remote from its exchange)
+  const int pl = (step - 1) & 1;
+  const int64_t n_spk = min((int64_t)sh.spk_count[pl], sh.spk_cap);
+  const uint32_t* spk = sh.spk_ids + (int64_t)pl * sh.spk_cap;
+  // lane per spike, 4 spikes in flight per thread: their bin offsets, then their
+  // entries 8 at a time (32 loads in flight), then the shared-memory sums
+  constexpr int kS = 4, kE = 8;
+  for (int64_t i0 = (int64_t)threadIdx.x; i0 < n_spk; i0 += kS * (int64_t)blockDim.x) {
+    int64_t lo[kS];
+    int n[kS];
+#pragma unroll
+    for (int u = 0; u < kS; ++u) {
+      const int64_t i = i0 + (int64_t)u * blockDim.x;
+      lo[u] = 0;
+      n[u] = 0;
+      if (i < n_spk) {
+        const uint32_t pre = spk[i];
+        const uint16_t* bo = sh.pb_binoff + (int64_t)pre * (B + 1) + c;
+        const int b0 = bo[0], b1 = bo[1];
+        lo[u] = sh.pb_rowptr[pre] + b0;
+        n[u] = b1 - b0;
+      }
+    }
+    int left = max(max(n[0], n[1]), max(n[2], n[3]));
+    for (int k0 = 0; k0 < left; k0 += kE) {
+      uint32_t x[kS][kE];
+#pragma unroll
+      for (int u = 0; u < kS; ++u)
+#pragma unroll
+        for (int k = 0; k < kE; ++k) x[u][k] = (k0 + k < n[u]) ? __ldg(sh.pb_syn + lo[u] + k0 + k) : 0u;
+#pragma unroll
+      for (int u = 0; u < kS; ++u)
+#pragma unroll
+        for (int k = 0; k < kE; ++k)
+          if (k0 + k < n[u]) {
+            const int32_t q = (int32_t)((x[u][k] >> 26) & 31u) + 1;
+            atomicAdd(&sacc[x[u][k] & 0x03FFFFFFu], (x[u][k] >> 31) ? q * negg : q);
+          }
+    }
+  }
+  __syncthreads();
+  lif_phase<kBinWarps>(sh, p, step, c, B, S, sacc);
+}
 }  // namespace
 
 extern "C" int nc_build_push_csr(const nc_shard_t* sh, int32_t phase, int64_t* push_rowptr, int32_t* push_fill,
@@ -459,6 +564,41 @@ extern "C" int nc_build_push_csr(const nc_shard_t* sh, int32_t phase, int64_t* p
     return NC_E_ARG;
   }
   k_push_build<<<16 * num_sms(), 256, 0, (cudaStream_t)stream>>>(*sh, phase, push_rowptr, push_fill, push_syn);
+  NC_LAUNCH_CHECK();
+  return NC_OK;
+}
+
+extern "C" int nc_build_push_binned(const nc_shard_t* sh, int32_t phase, uint32_t* counts, const int64_t* pb_rowptr,
+                                    const uint16_t* pb_binoff, uint32_t* fill, uint32_t* pb_syn, void* stream) {
+  if (int e = check_shard(sh)) return e;
+  if ((phase != 0 && phase != 1) || sh->pb_bins < 1 || sh->pb_rows < 32 || (sh->pb_rows & 31) ||
+      (int64_t)sh->pb_bins * sh->pb_rows < sh->n_local || (phase == 0 && !counts) ||
+      (phase == 1 && (!pb_rowptr || !pb_binoff || !fill || !pb_syn))) {
+    nc_set_error("nc_build_push_binned: bad arguments");
+    return NC_E_ARG;
+  }
+  k_push_binned<<<16 * num_sms(), 256, 0, (cudaStream_t)stream>>>(*sh, phase, counts, pb_rowptr, pb_binoff, fill,
+                                                                  pb_syn);
+  NC_LAUNCH_CHECK();
+  return NC_OK;
+}
+
+extern "C" int nc_sim_step_binned(const nc_shard_t* sh, const nc_lif_params_t* p, void* stream) {
+  if (int e = check_shard(sh)) return e;
+  if (!p || !sh->pb_rowptr || !sh->pb_binoff || !sh->pb_syn || !sh->spk_ids || !sh->spk_count || sh->pb_bins < 1 ||
+      sh->pb_rows < 32 || (sh->pb_rows & 31) || (int64_t)sh->pb_bins * sh->pb_rows < sh->n_local ||
+      sh->pb_rows / 32 > kLifMaxTiles) {
+    nc_set_error("nc_sim_step_binned: shard has no binned push / spike lists, or bins too large");
+    return NC_E_ARG;
+  }
+  if (!g_prepared)
+    if (int e = nc_sim_prepare()) return e;
+  const size_t smem = (size_t)sh->pb_rows * 4;
+  if (smem > (size_t)g_max_dyn_smem) {
+    nc_set_error("nc_sim_step_binned: %d rows per bin need %zu B of shared memory", sh->pb_rows, smem);
+    return NC_E_ARG;
+  }
+  k_step_binned<<<sh->pb_bins, kBinThreads, smem, (cudaStream_t)stream>>>(*sh, *p);
   NC_LAUNCH_CHECK();
   return NC_OK;
 }

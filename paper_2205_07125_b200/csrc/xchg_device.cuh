@@ -35,14 +35,37 @@ __device__ __forceinline__ int owner_of(const nc_xchg_t& X, uint32_t id) {
   return -1;
 }
 
+// Warp-aggregated append of the lanes' ids (where `ok`) to the step's spike
+// list (binned delivery); the whole warp calls.
+__device__ __forceinline__ void spk_append(const nc_xchg_t& X, int step, bool ok, uint32_t id) {
+  if (!X.spk_ids) return;
+  const uint32_t m = __ballot_sync(kFull, ok);
+  if (!m) return;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(m) - 1;
+  int32_t base = 0;
+  if (lane == leader) base = atomicAdd(X.spk_count + (step & 1), __popc(m));
+  base = __shfl_sync(kFull, base, leader);
+  if (ok) {
+    const int64_t pos = (int64_t)base + __popc(m & ((1u << lane) - 1u));
+    if (pos < X.spk_cap) X.spk_ids[(int64_t)(step & 1) * X.spk_cap + pos] = id;
+    else atomicExch(X.status, 1);
+  }
+}
+
 // OR `cnt` ids into the bitmap, count deliveries, relay-bucket if asked.
 // Called by a whole block.
 static __device__ void scatter_ids(const nc_xchg_t& X, const uint32_t* ids, int64_t cnt, int src, bool phase2,
-                            uint32_t* cur, long long* deliv, int32_t* status) {
+                            uint32_t* cur, long long* deliv, int32_t* status, int step) {
   __shared__ unsigned int per_src[NC_MAX_SHARDS];
   if (threadIdx.x < NC_MAX_SHARDS) per_src[threadIdx.x] = 0;
   __syncthreads();
   const uint32_t fwd = phase2 ? 0u : (uint32_t)X.fwd_row[src];
+  if (X.spk_ids)   // binned delivery: the ids also go to the step's spike list
+    for (int64_t k0 = threadIdx.x & ~31; k0 < cnt; k0 += blockDim.x) {
+      const int64_t k = k0 + (threadIdx.x & 31);
+      spk_append(X, step, k < cnt, k < cnt ? ids[k] : 0u);
+    }
   for (int64_t k = threadIdx.x; k < cnt; k += blockDim.x) {
     const uint32_t id = ids[k];
     atomicOr(cur + (id >> 5), 1u << (id & 31));
@@ -135,7 +158,7 @@ __device__ __forceinline__ bool ll_wait(const uint64_t* w, uint32_t tag, uint64_
 // Receive chunk kb of the message in `slot` and OR its ids into the bitmap,
 // count deliveries, relay-bucket if asked (two-level phase 1).  Whole block.
 static __device__ void ll_recv_scatter(const nc_xchg_t& X, const uint64_t* slot, int kb, int B, uint32_t tag,
-                                       int src, bool phase2, uint32_t* cur, long long* deliv) {
+                                       int src, bool phase2, uint32_t* cur, long long* deliv, int step) {
   __shared__ long long s_cnt;
   __shared__ unsigned int per_src[NC_MAX_SHARDS];
   if (threadIdx.x < NC_MAX_SHARDS) per_src[threadIdx.x] = 0;
@@ -160,6 +183,7 @@ static __device__ void ll_recv_scatter(const nc_xchg_t& X, const uint64_t* slot,
     const bool good = k < hi && ll_wait(slot + 1 + k, tag, X.timeout_ns, X.status, &v);
     const uint32_t id = (uint32_t)v;
     if (good) atomicOr(cur + (id >> 5), 1u << (id & 31));
+    spk_append(X, step, good, id);
     if (plain) continue;
     const uint32_t dm = good ? (uint32_t)(uint16_t)X.dest_global[id] : 0u;
     if ((dm >> X.rank) & 1u) atomicAdd(&per_src[phase2 ? max(owner_of(X, id), 0) : src], 1u);
@@ -225,7 +249,7 @@ static __device__ void p2p_block(const nc_xchg_t& X, int ex, int B, int step) {
   // ---- phase 1 receive from peer b, chunk kb
   if (peer) {
     if (dbg) dbg[2] = globaltimer();
-    ll_recv_scatter(X, my_inbox + slot_off(X, 0, par, b), kb, B, tag, b, false, cur, deliv);
+    ll_recv_scatter(X, my_inbox + slot_off(X, 0, par, b), kb, B, tag, b, false, cur, deliv, step);
   }
   if (X.two_level) {
     // ---- grid barrier: every phase-1 inbox drained, forward buckets complete
@@ -257,7 +281,7 @@ static __device__ void p2p_block(const nc_xchg_t& X, int ex, int B, int step) {
     }
     // ---- phase 2 receive from relay b
     if (peer && ((X.recv2_mask >> b) & 1u))
-      ll_recv_scatter(X, my_inbox + slot_off(X, 1, par, b), kb, B, tag, b, true, cur, deliv);
+      ll_recv_scatter(X, my_inbox + slot_off(X, 1, par, b), kb, B, tag, b, true, cur, deliv, step);
   }
   // ---- latency record: last block out stamps (end - start of block 0)
   __syncthreads();

@@ -86,8 +86,8 @@ class DistSimulator:
         import torch.distributed as dist
         if transport not in ("p2p", "nccl"):
             raise ValueError(f"transport must be 'p2p' or 'nccl', got {transport!r}")
-        if delivery not in ("fused", "push", "pull", "persistent"):
-            raise ValueError(f"delivery must be 'fused', 'pull', 'push' or 'persistent', got {delivery!r}")
+        if delivery not in ("fused", "push", "pull", "persistent", "binned"):
+            raise ValueError(f"delivery must be 'fused', 'pull', 'push', 'binned' or 'persistent', got {delivery!r}")
         if delivery == "persistent" and transport != "p2p":
             raise ValueError("the persistent engine exchanges spikes with device-initiated P2P stores (transport='p2p')")
         self.rank = dist.get_rank()
@@ -124,7 +124,8 @@ class DistSimulator:
         self.cap = max(cap, 1)
         del probe
         self.state = _ShardState(net, self.rank, self.plan, record_steps=record_raster_steps,
-                                 push=(delivery in ("push", "persistent")), bucket_cap=None,
+                                 push=(delivery in ("push", "persistent")), binned=(delivery == "binned"),
+                                 bucket_cap=None,
                                  bucket_stride=self.cap)
         self.states = [self.state]
         self.record_steps = int(record_raster_steps)
@@ -167,6 +168,9 @@ class DistSimulator:
         X.send_hdr, X.send2_hdr = self.hdr[0].data_ptr(), self.hdr[1].data_ptr()
         X.recv_hdr, X.recv2_hdr = self.hdr[2].data_ptr(), self.hdr[3].data_ptr()
         X.recv_ids, X.recv2_ids = self.recv_ids.data_ptr(), self.recv2_ids.data_ptr()
+        if self.state.spk_ids is not None:   # binned delivery: remote spikes join the step's list
+            X.spk_ids, X.spk_count, X.spk_cap = (self.state.spk_ids.data_ptr(), self.state.spk_count.data_ptr(),
+                                                 self.state.spk_cap)
         self.dbg = None
         if os.environ.get("NC_XCHG_DBG"):   # diagnostics (tools/xchg_stamps.py)
             self.dbg = torch.zeros((64, n * self.blocks_per_peer, 4), dtype=torch.int64, device=dev)
@@ -297,7 +301,9 @@ class DistSimulator:
         L = self.lib
         s = self.state
         lif = C.byref(self.c_lif)
-        if self.delivery == "fused":
+        if self.delivery == "binned":
+            _native.check(L.nc_sim_step_binned(C.byref(s.c), lif, st), "step binned")
+        elif self.delivery == "fused":
             _native.check(L.nc_sim_step_fused(C.byref(s.c), lif, st), "step")
         else:
             if self.delivery == "push":
@@ -318,7 +324,7 @@ class DistSimulator:
     def launches_per_step(self) -> float:
         if self.delivery == "persistent":
             return 0.0  # one cooperative launch per advance() call
-        step = 2 if self.delivery == "fused" else 3
+        step = 2 if self.delivery in ("fused", "binned") else 3
         if self.transport == "p2p":
             return step + 1 + (1 if self.plan.two_level else 0)
         ex = 2 * (2 if self.plan.two_level else 1) + (1 if self.plan.two_level else 0)

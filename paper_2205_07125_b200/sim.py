@@ -504,7 +504,7 @@ class _ShardState:
     """Device buffers and the C descriptor of one shard."""
 
     def __init__(self, net: Network, h: int, plan: ExchangePlan, *, record_steps: int, push: bool,
-                 bucket_cap: int | None, bucket_stride: int | None = None):
+                 bucket_cap: int | None, bucket_stride: int | None = None, binned: bool = False):
         import torch
         lay = net.layout
         dev = net.device
@@ -547,6 +547,14 @@ class _ShardState:
         self.push_rowptr = self.push_syn = None
         if push:
             self.push_rowptr, self.push_syn = _push_csr(csr, lay, h, dev)
+        self.pb = None
+        self.spk_ids = self.spk_count = None
+        if binned:
+            self.pb = _push_binned(csr, lay, h, dev)
+            # spike lists by step parity; every internal id fires at most once per step
+            self.spk_cap = lay.n_words * 32
+            self.spk_ids = torch.zeros(2 * self.spk_cap, dtype=torch.int32, device=dev)
+            self.spk_count = torch.zeros(2, dtype=torch.int32, device=dev)
         self.c = _native.ShardC(
             shard=h, n_shards=n, n_local=n_local, local_base=int(lay.base[h]), n_words=lay.n_words,
             n_tiles=csr.n_tiles, tile_words=csr.tile_words, flags=1 if csr.partials_global else 0,
@@ -563,6 +571,62 @@ class _ShardState:
             record_steps=self.record_steps, local_words=self.local_words,
             spike_total=self.spike_total.data_ptr(), work=self.work.data_ptr(),
             row_perm=None if csr.row_perm is None else csr.row_perm.data_ptr(), cta_groups=csr.cta_groups)
+        if self.pb is not None:
+            self.c.pb_bins, self.c.pb_rows = self.pb["bins"], self.pb["rows"]
+            self.c.pb_rowptr = self.pb["rowptr"].data_ptr()
+            self.c.pb_binoff = self.pb["binoff"].data_ptr()
+            self.c.pb_syn = self.pb["syn"].data_ptr()
+            self.c.spk_ids, self.c.spk_count, self.c.spk_cap = (self.spk_ids.data_ptr(), self.spk_count.data_ptr(),
+                                                                self.spk_cap)
+
+
+def _push_binned(csr: ShardCSR, lay: ShardLayout, h: int, dev):
+    """Binned push synapses of one shard (include/neurocomm_b200.h, nc_shard_t pb_*):
+    rows = internal pre ids, entries grouped by the bin (CTA of k_step_binned) that
+    owns their post row; built on the device by nc_build_push_binned.  Cached on
+    the SellCSR."""
+    import torch
+    cached = getattr(csr, "_binned_cache", None)
+    if cached is not None:
+        return cached
+    L = _native.lib()
+    st = _native.stream_handle(dev)
+    n_local = lay.n_local(h)
+    bins = sell.device_sms(dev)
+    rows = max(32, ((n_local + 31) // 32 + bins - 1) // bins * 32)
+    n_pre = lay.n_words * 32
+    scratch = torch.zeros(8, dtype=torch.int32, device=dev)
+    c = _native.ShardC(shard=h, n_shards=lay.n_shards, n_local=n_local, local_base=int(lay.base[h]),
+                       n_words=lay.n_words, n_tiles=csr.n_tiles, tile_words=csr.tile_words, flags=0,
+                       slice_ptr=csr.slice_ptr.data_ptr(), row_meta=csr.row_meta.data_ptr(), syn=csr.syn.data_ptr(),
+                       bitmap0=scratch.data_ptr(), bitmap1=scratch.data_ptr(), status=scratch.data_ptr(),
+                       step=scratch.data_ptr(),
+                       row_perm=None if csr.row_perm is None else csr.row_perm.data_ptr(),
+                       cta_groups=csr.cta_groups, pb_bins=bins, pb_rows=rows)
+    counts = torch.zeros(n_pre * bins, dtype=torch.int32, device=dev)
+    _native.check(L.nc_build_push_binned(C.byref(c), 0, counts.data_ptr(), None, None, None, None, st),
+                  "binned push count")
+    per_bin = counts.view(n_pre, bins)
+    run = torch.cumsum(per_bin, 1, dtype=torch.int64)
+    row_len = run[:, -1]
+    if n_pre and int(row_len.max().item()) >= 1 << 16:
+        raise ValueError("binned push: a pre neuron has >= 65536 local synapses (16-bit bin offsets)")
+    binoff = torch.zeros((n_pre, bins + 1), dtype=torch.int32, device=dev)
+    binoff[:, 1:] = run.to(torch.int32)
+    binoff16 = binoff.to(torch.int16)   # values < 2^16 (two's complement view of uint16)
+    rowptr = torch.zeros(n_pre + 1, dtype=torch.int64, device=dev)
+    rowptr[1:] = torch.cumsum(row_len, 0)
+    total = int(rowptr[-1].item())
+    del run, binoff, per_bin
+    counts.zero_()
+    syn = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+    _native.check(L.nc_build_push_binned(C.byref(c), 1, None, rowptr.data_ptr(), binoff16.data_ptr(),
+                                         counts.data_ptr(), syn.data_ptr(), st), "binned push fill")
+    torch.cuda.synchronize(dev)
+    del counts, scratch
+    out = {"bins": bins, "rows": rows, "rowptr": rowptr, "binoff": binoff16, "syn": syn}
+    csr._binned_cache = out
+    return out
 
 
 def _push_csr(csr: ShardCSR, lay: ShardLayout, h: int, dev):
@@ -604,10 +668,10 @@ class Simulator:
                  *, delivery: str = "fused", record_raster_steps: int = 0, per_step_counts: bool = False,
                  bucket_cap: int | None = None, use_graph: bool = True, graph_chunk: int = 64):
         import torch
-        if delivery not in ("fused", "push", "pull", "persistent"):
-            raise ValueError(f"delivery must be 'fused', 'pull', 'push' or 'persistent', got {delivery!r}")
-        if delivery == "persistent" and net.layout.n_shards != 1:
-            raise ValueError("the persistent engine runs one shard per GPU; use distributed.DistSimulator")
+        if delivery not in ("fused", "push", "pull", "persistent", "binned"):
+            raise ValueError(f"delivery must be 'fused', 'pull', 'push', 'binned' or 'persistent', got {delivery!r}")
+        if delivery in ("persistent", "binned") and net.layout.n_shards != 1:
+            raise ValueError(f"the {delivery} engine runs one shard per GPU; use distributed.DistSimulator")
         if set(net.shards) != set(range(net.layout.n_shards)):
             raise ValueError("the single-process simulator needs every shard of the layout")
         self.net = net
@@ -624,7 +688,7 @@ class Simulator:
         self.record_steps = int(record_raster_steps)
         self.states = [
             _ShardState(net, h, self.plan, record_steps=self.record_steps, push=(delivery in ("push", "persistent")),
-                        bucket_cap=bucket_cap)
+                        bucket_cap=bucket_cap, binned=(delivery == "binned"))
             for h in range(self.n)
         ]
         dev = net.device
@@ -666,6 +730,9 @@ class Simulator:
         if self.delivery == "fused":
             for s in self.states:
                 self._check(L.nc_sim_step_fused(C.byref(s.c), lif, st), "step")
+        elif self.delivery == "binned":
+            for s in self.states:
+                self._check(L.nc_sim_step_binned(C.byref(s.c), lif, st), "step binned")
         else:
             for s in self.states:
                 if self.delivery == "push":
@@ -685,7 +752,7 @@ class Simulator:
     def launches_per_step(self) -> float:
         if self.delivery == "persistent":
             return 0.0  # one launch per advance() call, whatever the step count
-        per_shard = 2 if self.delivery == "fused" else 3
+        per_shard = 2 if self.delivery in ("fused", "binned") else 3
         ex = 0
         if self.n > 1:
             ex = 3 if self.plan.two_level else 1

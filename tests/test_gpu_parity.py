@@ -159,6 +159,33 @@ def test_persistent_engine_matches_oracle():
     assert_same(rep, ref)
 
 
+@pytest.mark.parametrize("tile_words", [None, 64])
+def test_binned_push_engine_matches_oracle(tile_words):
+    """Event-driven step with binned push: each CTA sums its bin of every spiking
+    pre's synapses in shared memory, then updates its rows (one kernel per step)."""
+    g = cfg1(1)
+    pm = nc.partition_greedy(g, 1)
+    lif = S.LifParams()
+    lay = S.ShardLayout.from_assignment(pm.assignment, 1)
+    net = S.Network.from_graph(g, lay, tile_words=tile_words)
+    for use_graph in (True, False):
+        rep = S.Simulator(net, lif, 1, None, delivery="binned", record_raster_steps=100, per_step_counts=True,
+                          use_graph=use_graph).run(100)
+        assert_same(rep, oracle_run(g, pm, None, lif, 1, 100))
+
+
+def test_binned_push_on_device_generated_network():
+    """Device generator + bank placement + binned push agree with the pull kernel."""
+    spec = S.GeneratorSpec(20_000, 2, 0.01, 0.002, seed=3)
+    lay = S.ShardLayout.blocks(spec.n_neurons, 1)
+    net = S.Network.generate(spec, lay, tile_words=160)
+    lif = S.LifParams()
+    a = S.Simulator(net, lif, 7, None, delivery="fused", record_raster_steps=80).run(80)
+    b = S.Simulator(net, lif, 7, None, delivery="binned", record_raster_steps=80).run(80)
+    np.testing.assert_array_equal(a.raster, b.raster)
+    np.testing.assert_array_equal(a.v.view(np.uint32), b.v.view(np.uint32))
+
+
 def test_partition_invariance_and_route_independence():
     """Rasters do not depend on how many GPUs or which routes carry the spikes."""
     g = cfg1(3)

@@ -53,7 +53,7 @@ def main() -> int:
             ref = c_oracle.simulate_csr(rp, col, q, pm.assignment, world, rt.next_hop_matrix(), lif.constants(1),
                                         steps, threads=8)
         runs = [(t, "fused") for t in os.environ.get("NC_TRANSPORTS", "p2p,nccl").split(",")]
-        runs.append(("p2p", "persistent"))
+        runs += [("p2p", "persistent"), ("p2p", "binned"), ("nccl", "binned")]
         for transport, delivery in runs:
             sim = DistSimulator(net, lif, 1, rt, transport=transport, delivery=delivery,
                                 record_raster_steps=steps, per_step_counts=True)
