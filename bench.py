@@ -492,7 +492,7 @@ def main() -> int:
     ap.add_argument("--no-bank-order", dest="bank_order", action="store_false",
                     help="skip the shared-memory bank placement of the synapse entries (tuning)")
     ap.add_argument("--chunk", type=int, default=100)
-    ap.add_argument("--cpu-steps", type=int, default=10)
+    ap.add_argument("--cpu-steps", type=int, default=200, help="CPU-baseline sample (~10 s of OpenMP oracle work at config 2)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-push", dest="with_push", action="store_false",
                     help="skip the event-driven (push) measurement reported beside the headline")
