@@ -166,7 +166,8 @@ k_step_fused(const nc_shard_t sh, const nc_lif_params_t p) {
         // CTA-local index k of the row placed here in tile t (rows stay inside the CTA's slices)
         const int k = pos < sh.n_local ? sh.row_perm[(int64_t)t * sh.n_local + pos] : -1;
         const int32_t sum = sell_row_sum<pglob ? kPfTiled : 0>(syn4 + b0, meta, bm, g_inh, lane, 0u);
-        if (k >= 0) {
+        // partials of sparse tiles are mostly 0 (no pre of the row fired): skip those
+        if (k >= 0 && sum != 0) {
           if (!pglob) atomicAdd(&spart[k], sum);
           else red_add(&sh.acc[((c + (k >> 5) * G) << 5) + (k & 31)], sum);
         }
