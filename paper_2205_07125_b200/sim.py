@@ -722,7 +722,8 @@ class Simulator:
         self.hop_ids = torch.zeros((rows, self.n, self.n), dtype=torch.int64, device=self.net.device)
         self.deliv_ids = torch.zeros((rows, self.n, self.n), dtype=torch.int64, device=self.net.device)
         self.fwd_count.zero_()
-        self._graph = None
+        if self.n > 1:   # the exchange launches capture the counter buffers reallocated above
+            self._graph = None
 
     def _one_step(self, st):
         L = self.lib
