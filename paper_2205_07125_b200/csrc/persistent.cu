@@ -84,8 +84,6 @@ __global__ void __launch_bounds__(kPThreads) k_persistent(const nc_shard_t sh, c
   if (bid == 0 && threadIdx.x == 0) *sh.step = step;
 }
 
-int g_grid = 0;
-
 }  // namespace
 
 static unsigned long long* g_phase_stamps = nullptr;
@@ -129,8 +127,6 @@ extern "C" int nc_run_persistent(const nc_shard_t* sh, const nc_lif_params_t* p,
     nc_set_error("nc_run_persistent: %d exchange blocks exceed the resident grid (%d)", nex, grid);
     return NC_E_ARG;
   }
-  g_grid = grid;
-  (void)g_grid;
   nc_xchg_t xz{};
   const nc_xchg_t& xr = X ? *X : xz;
   int has_x = X ? 1 : 0;

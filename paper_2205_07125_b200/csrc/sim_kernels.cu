@@ -287,8 +287,6 @@ int launch_step(const nc_shard_t& sh, const nc_lif_params_t& p, cudaStream_t st)
   // tiled: the row placement was built for cta_groups CTAs (sh.row_perm)
   const int grid = sh.n_tiles > 1 ? sh.cta_groups : num_sms();
   size_t smem = step_smem_bytes(sh, grid);
-  static const long smem_pad = getenv("NC_SMEM_PAD") ? atol(getenv("NC_SMEM_PAD")) : 0;   // tuning experiments
-  smem += (size_t)smem_pad;
   if (smem > (size_t)g_max_dyn_smem) {
     nc_set_error("step kernel needs %zu B of shared memory (tile_words=%d): re-tile the network", smem,
                  sh.tile_words);

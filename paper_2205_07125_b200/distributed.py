@@ -141,7 +141,6 @@ class DistSimulator:
         self.lat_stamps = torch.zeros((2, max(latency_steps, 1)), dtype=torch.int64, device=dev)
         # P2P: the exchange kernel records its own duration per step (no stamp kernels)
         self.lat_ns = torch.zeros(max(latency_steps, 1), **i32)
-        self.sync_words = torch.zeros(8, **i32)
         self._gbar = torch.zeros(1, **i32)
         self.hop_ids = None
         self.deliv_ids = None
