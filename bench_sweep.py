@@ -65,6 +65,8 @@ def main() -> int:
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--delivery", default="push", choices=["push", "fused"])
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--blocks-per-peer", type=int, default=None)
+    ap.add_argument("--rates", default=",".join(str(r) for r in RATES))
     ap.add_argument("--out", default=str(ROOT / "gpurun_out" / "sweep.json"))
     args = ap.parse_args()
 
@@ -85,11 +87,12 @@ def main() -> int:
     build_s = time.time() - t0
     topo = nc.build_topology(nc.TopologySpec(gpus_per_node=max(1, world // args.groups), nodes_per_switch=8), world)
     rows = []
-    for rate in RATES:
+    for rate in [float(r) for r in args.rates.split(",")]:
         lif = S.LifParams.for_rate(rate)
         for mode, rt in tables.items():
             sim = DistSimulator(net, lif, args.seed, rt, transport="p2p", delivery=args.delivery,
-                                latency_steps=args.warmup + args.steps, graph_chunk=50)
+                                latency_steps=args.warmup + args.steps, graph_chunk=50,
+                                blocks_per_peer=args.blocks_per_peer)
             sim.reset(1)
             sim.advance(args.warmup)
             torch.cuda.synchronize()
