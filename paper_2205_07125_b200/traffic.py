@@ -23,7 +23,7 @@ from .accum import limbs_to_float
 __all__ = [
     "GpuTrafficGraph", "TrafficReport", "report_from_vector", "aggregate", "per_gpu_send_traffic",
     "peak_reduction", "write_traffic_csv", "read_traffic_csv", "write_traffic_summary",
-    "exact_bin_sums",
+    "exact_bin_sums", "aggregate_sharded",
 ]
 
 INT_MAX = 2**31 - 1
@@ -78,13 +78,19 @@ def _n_digits(lsb: int, msb: int, n_terms: int) -> int:
     return (bits + 31) // 32 + 2
 
 
-def exact_bin_sums(values_dev, keys_dev, n_bins: int, *, pairs=None, stream=None):
+def exact_bin_sums(values_dev, keys_dev, n_bins: int, *, pairs=None, stream=None, group=None):
     """Correctly rounded per-bin sums on the device.
 
     ``pairs=None``: bin ``keys[k]`` receives ``values[k]`` (binned_sums).
     ``pairs=(ei, ej, ep)``: edge mode -- values are the neuron weights, keys
     the assignment, and cell ``min*N+max`` receives ``(ep*w[ei])*w[ej]``.
     Returns a float64 numpy array of ``n_bins`` (or ``n_bins**2``) cells.
+
+    ``group`` (a torch.distributed process group, or ``True`` for the default
+    one): every rank passes its own slice of the terms; the exponent range and
+    term count are all-reduced so all ranks accumulate on the same fixed-point
+    grid, the integer limbs are all-reduced (exact), and every rank rounds the
+    same total once -- the SURVEY 8(e) partition-time path.
     """
     import torch
     L = _native.lib()
@@ -93,26 +99,43 @@ def exact_bin_sums(values_dev, keys_dev, n_bins: int, *, pairs=None, stream=None
     mm = torch.tensor([INT_MAX, INT_MIN], dtype=torch.int32, device=dev)
     if pairs is None:
         n = int(values_dev.numel())
-        _native.check(L.nc_traffic_exponents(None, None, None, values_dev.data_ptr(), n, mm.data_ptr(), st),
-                      "weight exponents")
+        if n:
+            _native.check(L.nc_traffic_exponents(None, None, None, values_dev.data_ptr(), n, mm.data_ptr(), st),
+                          "weight exponents")
     else:
         ei, ej, ep = pairs
         n = int(ei.numel())
-        _native.check(L.nc_traffic_exponents(ei.data_ptr(), ej.data_ptr(), ep.data_ptr(), values_dev.data_ptr(),
-                                             n, mm.data_ptr(), st), "traffic exponents")
+        if n:
+            _native.check(L.nc_traffic_exponents(ei.data_ptr(), ej.data_ptr(), ep.data_ptr(),
+                                                 values_dev.data_ptr(), n, mm.data_ptr(), st), "traffic exponents")
+    n_local = n
     n_cells = n_bins * n_bins if pairs is not None else n_bins
+    if group is not None:
+        import torch.distributed as dist
+        grp = None if group is True else group
+        mn, mx = mm[0:1].clone(), mm[1:2].clone()
+        dist.all_reduce(mn, op=dist.ReduceOp.MIN, group=grp)
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=grp)
+        mm = torch.cat([mn, mx])
+        cnt = torch.tensor([n], dtype=torch.int64, device=dev)
+        dist.all_reduce(cnt, group=grp)
+        n = int(cnt.item())
     lo, hi = mm.cpu().tolist()
     if n == 0 or lo == INT_MAX:
         return np.zeros(n_cells, dtype=np.float64)
     nd = _n_digits(lo, hi, n)
     limbs = torch.zeros((n_cells, nd), dtype=torch.int64, device=dev)
-    if pairs is None:
-        rc = L.nc_weight_histogram(values_dev.data_ptr(), keys_dev.data_ptr(), n, n_bins, lo, nd,
-                                   limbs.data_ptr(), st)
-    else:
-        rc = L.nc_traffic_histogram(ei.data_ptr(), ej.data_ptr(), ep.data_ptr(), values_dev.data_ptr(),
-                                    keys_dev.data_ptr(), n, n_bins, lo, nd, limbs.data_ptr(), st)
-    _native.check(rc, "traffic histogram")
+    if n_local:
+        if pairs is None:
+            rc = L.nc_weight_histogram(values_dev.data_ptr(), keys_dev.data_ptr(), n_local, n_bins, lo, nd,
+                                       limbs.data_ptr(), st)
+        else:
+            rc = L.nc_traffic_histogram(ei.data_ptr(), ej.data_ptr(), ep.data_ptr(), values_dev.data_ptr(),
+                                        keys_dev.data_ptr(), n_local, n_bins, lo, nd, limbs.data_ptr(), st)
+        _native.check(rc, "traffic histogram")
+    if group is not None:   # exact: integer limbs (< 2^33 each after the kernel's carry flush)
+        import torch.distributed as dist
+        dist.all_reduce(limbs, group=None if group is True else group)
     host = limbs.cpu().numpy().view(np.uint64)
     out = np.zeros(n_cells, dtype=np.float64)
     for c in np.flatnonzero(host.any(axis=1)).tolist():
@@ -166,6 +189,29 @@ def aggregate(graph, pm) -> GpuTrafficGraph:
     cells = exact_bin_sums(w, asg, n, pairs=(ei, ej, ep)).reshape(n, n)
     upper = np.triu(cells)
     pg = upper + np.triu(cells, 1).T
+    wg = exact_bin_sums(w, asg, n)
+    return GpuTrafficGraph(n, pg, wg)
+
+
+def aggregate_sharded(edge_i, edge_j, edge_p, weights, assignment, n_gpus: int, group=True) -> GpuTrafficGraph:
+    """aggregate() over an edge list split across ranks: every rank
+    passes its own slice of (edge_i, edge_j, edge_p) and the full weights and
+    assignment; the K5 limbs are all-reduced over NCCL and rounded once, so every
+    rank returns pg / wg bit-identical to the single-GPU aggregate of the whole
+    graph (any split, any order: the sums are exact)."""
+    import torch
+    dev = _device()
+    def up(a, dt):
+        if isinstance(a, np.ndarray):
+            return torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev)
+        return a.to(device=dev)
+
+    ei, ej = up(edge_i, np.int64), up(edge_j, np.int64)
+    ep, w = up(edge_p, np.float64), up(weights, np.float64)
+    asg = up(assignment, np.int64)
+    n = int(n_gpus)
+    cells = exact_bin_sums(w, asg, n, pairs=(ei, ej, ep), group=group).reshape(n, n)
+    pg = np.triu(cells) + np.triu(cells, 1).T
     wg = exact_bin_sums(w, asg, n)
     return GpuTrafficGraph(n, pg, wg)
 

@@ -32,3 +32,15 @@ def test_multirank_parity(n):
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     print(out.stdout[-4000:], out.stderr[-4000:])
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_multirank_sharded_aggregate(n):
+    """K5 over an edge list split across ranks (limbs all-reduced) == single-GPU aggregate, bit for bit."""
+    if _gpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", "--master-port=29532", str(ROOT / "tests" / "workers" / "dist_aggregate.py")]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    print(out.stdout[-4000:], out.stderr[-4000:])
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
