@@ -292,3 +292,28 @@ def test_device_generator_matches_oracle_and_statistics():
         np.testing.assert_array_equal(rep.deliv_ids, ref["deliv"])
         np.testing.assert_array_equal(rep.v, ref["v"])
     del torch
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_config1_gpu_matches_committed_rasters(seed):
+    """BASELINE config 1 (4 partitions, the reference's two-level routes, 100 steps) on the
+    GPU against the committed golden rasters of tests/golden/oracle_rasters.json."""
+    import hashlib
+    import json
+    from pathlib import Path
+    gold = json.loads((Path(__file__).resolve().parent / "golden" / "oracle_rasters.json").read_text())
+    want = gold["seeds"][str(seed)]
+    fx = np.load(Path(__file__).resolve().parent / "golden" / "reference_fixtures.npz")
+    from paper_2205_07125_b200.routing import RoutingTable
+    g = cfg1(seed)
+    pm = nc.partition_greedy(g, 4)
+    key = f"cfg1_s{seed}/p0"
+    rt = RoutingTable(4, 2, fx[f"{key}/rt_src"], fx[f"{key}/rt_dst"], fx[f"{key}/rt_via"], {})
+    rep = nc.simulate(g, pm, rt, gold["steps"], S.LifParams(), seed=seed)
+    assert hashlib.sha256(np.ascontiguousarray(rep.raster, dtype=np.uint8).tobytes()).hexdigest() == \
+        want["raster_sha256"]
+    assert rep.raster.sum(axis=1).astype(int).tolist() == want["spikes_per_step"]
+    assert rep.deliv_ids.sum(axis=0).astype(int).tolist() == want["deliv_total"]
+    assert rep.hop_ids.sum(axis=0).astype(int).tolist() == want["hop_total"]
+    assert hashlib.sha256(np.ascontiguousarray(rep.v, dtype=np.float32).view(np.uint32).tobytes()).hexdigest() == \
+        want["v_sha256"]

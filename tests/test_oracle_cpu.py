@@ -86,3 +86,17 @@ def test_two_level_counts_route_independent():
     np.testing.assert_array_equal(d["deliv"], t["deliv"])
     # direct: every delivery is one hop
     np.testing.assert_array_equal(d["hop"], d["deliv"])
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_config1_oracle_matches_committed_rasters(seed):
+    """The oracle (+ the bit-identical planner feeding it) reproduces the committed
+    config-1 golden rasters (tests/golden/make_raster_golden.py)."""
+    import json
+    import sys
+    from pathlib import Path
+    here = Path(__file__).resolve().parent / "golden"
+    sys.path.insert(0, str(here))
+    import make_raster_golden as mk
+    gold = json.loads((here / "oracle_rasters.json").read_text())["seeds"][str(seed)]
+    assert mk.digest(mk.case(seed)[4]) == gold
