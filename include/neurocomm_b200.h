@@ -429,6 +429,15 @@ int nc_sell_bank_order(const int64_t* padded_ptr, const uint32_t* row_meta, int3
 int nc_sell_repack(const int64_t* padded_ptr, const int64_t* slice_ptr, const uint32_t* row_meta, int32_t n_tiles,
                    int32_t n_local, const uint32_t* src, uint32_t* dst, int32_t to_jagged, void* stream);
 
+/* GA balance repair (replaces _repair_balance, partition.py:167-184): while the
+ * heaviest GPU's load (correctly rounded exact sum of its weights, = math.fsum;
+ * lowest index on ties) exceeds `bound`, move its heaviest neuron (lowest index
+ * on ties) to the lightest GPU.  Loads are kept as exact fixed-point integers
+ * updated per move; identical decisions to the reference.  *n_moves (optional)
+ * receives the number of moves. */
+int nc_repair_balance(int64_t n_neurons, const double* weights, int64_t* assignment, int32_t n_gpus, double bound,
+                      int64_t* n_moves);
+
 /* ---------------------------------------------------------------- text I/O
  * Native readers / writers of the reference's text artefacts with its exact
  * acceptance rules and error texts (str.splitlines lines, float()/int()

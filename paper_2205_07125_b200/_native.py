@@ -115,6 +115,7 @@ _SIGS = {
     "nc_sell_fill_pads": (c_int32, [c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p]),
     "nc_dest_mask_from_csr": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_int32, c_void_p, c_int32,
                                         c_void_p, c_int32, c_int32, c_void_p, c_void_p]),
+    "nc_repair_balance": (c_int32, [c_int64, c_void_p, c_void_p, c_int32, c_double, c_void_p]),
     "nc_nng_scan": (c_int32, [C.c_char_p, c_void_p, c_void_p, c_void_p]),
     "nc_nng_read": (c_int32, [C.c_char_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "nc_nng_write": (c_int32, [C.c_char_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),

@@ -10,6 +10,7 @@ connection stats, level-2 traffic and the analytic netsim step.  The GPU
 from __future__ import annotations
 
 import hashlib
+import math
 import json
 from pathlib import Path
 
@@ -294,3 +295,37 @@ def test_writer_float_repr_fuzz(tmp_path):
     nc.save_graph(g, tmp_path / "f.nng")
     lines = (tmp_path / "f.nng").read_text().splitlines()[1:]
     assert lines == [repr(float(x)) for x in vals]
+
+
+def _repair_reference_loop(asg, w, n, bound):
+    """The reference's _repair_balance loop (partition.py:167-184), restated with fsum sums."""
+    from paper_2205_07125_b200.accum import binned_sums
+    while True:
+        wg = binned_sums(asg, w, n)
+        hi = int(np.argmax(wg))
+        if wg[hi] <= bound:
+            return
+        lo = int(np.argmin(wg))
+        members = np.flatnonzero(asg == hi)
+        asg[int(members[np.argmax(w[members])])] = lo
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_native_repair_balance_matches_fsum_loop(seed):
+    from paper_2205_07125_b200.partition import _rebalance
+    rng = np.random.default_rng(seed)
+    m, n = int(rng.integers(5, 400)), int(rng.integers(2, 9))
+    kind = seed % 3
+    if kind == 0:
+        w = rng.uniform(0.5, 2.0, m)
+    elif kind == 1:
+        w = 10.0 ** rng.uniform(-30, 30, m)                 # wide exponent range
+    else:
+        w = rng.choice([0.1, 0.2, 0.3, 1.0 / 3.0], m)       # many ties, inexact decimals
+    asg = rng.integers(0, n, m).astype(np.int64)
+    asg[: m // 2] = 0                                        # skewed start: many moves
+    bound = math.fsum(w) / n + float(w.max())
+    a, b = asg.copy(), asg.copy()
+    _repair_reference_loop(a, w, n, bound)
+    _rebalance(b, w, n, bound)
+    np.testing.assert_array_equal(a, b)
