@@ -2,8 +2,9 @@
 
 Default (N=1): BASELINE config 2 -- 1M LIF neurons x ~1k synapses (random, C=1,
 device-generated with the generate_synthetic distributions), single B200,
-update + delivery kernels, 1000 timed steps.  N>1 (torchrun): weak scaling,
-1M neurons per GPU, block partition, direct spike exchange.
+update + delivery kernels, 1000 timed steps.  N>1 (torchrun): strong scaling of the
+same network (block partition over the N GPUs, direct P2P spike exchange); `--scaling
+weak` grows the network to 1M neurons per GPU instead.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -93,14 +94,23 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def total_neurons(args, world: int) -> int:
+    return args.neurons * world if args.scaling == "weak" else args.neurons
+
+
 def workload_name(args, world: int) -> str:
+    n = total_neurons(args, world)
     if args.communities > 1:
-        return (f"regional (config 5 family): {args.neurons * world} neurons in {args.communities} regions, "
+        return (f"regional (config 5 family): {n} neurons in {args.communities} regions, "
                 f"{args.intra_frac:.0%} of ~{args.degree:.0f} synapses intra-region, {world} GPU(s), block partition")
-    if world == 1 and args.neurons == 1_000_000:
+    if world == 1 and n == 1_000_000:
         return "config 2: 1M LIF neurons x 1k synapses, single B200, update + delivery kernels"
-    return (f"weak scaling: {args.neurons} neurons/GPU x {args.degree:.0f} synapses, {world} GPU(s), "
-            f"block partition, direct exchange ({args.transport})")
+    if args.scaling == "weak":
+        return (f"weak scaling: {args.neurons} neurons/GPU x {args.degree:.0f} synapses, {world} GPU(s), "
+                f"block partition, direct exchange ({args.transport})")
+    return (f"strong scaling: {n} neurons x {args.degree:.0f} synapses"
+            f"{' (the config-2 network)' if n == 1_000_000 else ''} over {world} GPU(s), block partition, "
+            f"direct exchange ({args.transport})")
 
 
 def dist_env():
@@ -112,13 +122,14 @@ def dist_env():
 
 # --------------------------------------------------------------------------- ours
 
-def make_sim(net, lif, args, delivery, world):
+def make_sim(net, lif, args, delivery, world, record_raster_steps: int = 0):
     from paper_2205_07125_b200 import sim as S
     if world > 1:
         from paper_2205_07125_b200 import distributed as D
         cap = args.msg_cap if args.msg_cap is not None else (65536 if args.transport == "nccl" else None)
         return D.DistSimulator(net, lif, args.seed, None, transport=args.transport, delivery=delivery,
-                               msg_cap=cap, latency_steps=args.warmup + args.steps, graph_chunk=args.chunk)
+                               msg_cap=cap, latency_steps=args.warmup + args.steps, graph_chunk=args.chunk,
+                               record_raster_steps=record_raster_steps)
     return S.Simulator(net, lif, args.seed, None, delivery=delivery, graph_chunk=args.chunk)
 
 
@@ -247,7 +258,7 @@ def run_ours(args) -> dict | None:
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    n_neurons = args.neurons * world
+    n_neurons = total_neurons(args, world)
     if args.communities > 1:
         # regional model (config 5): `intra_frac` of each neuron's ~degree synapses inside its region
         c = args.communities
@@ -296,7 +307,7 @@ def run_ours(args) -> dict | None:
     prof = ROOT / "profiles" / "ncu_step_fused.json"
     if prof.is_file() and main_kernel == "fused" and world == 1:
         traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
-    e2e = e2e_measure(sim, net, args) if (world == 1 and rank == 0) else None
+    e2e = e2e_measure(sim, net, args, world, rank, lif)
     launches = max(1, int(round(args.steps * sim.launches_per_step())))
     if world > 1:
         sim.close()
@@ -330,7 +341,7 @@ def run_ours(args) -> dict | None:
         result = {
             "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 5), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "fp32 state / int32 synaptic sums",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "fp32 state / int32 synaptic sums",
             "data": "synthetic (device SBM generator, generate_synthetic distributions)",
             "config": {
                 "workload": workload_name(args, world),
@@ -404,18 +415,24 @@ def cpu_baseline(net, lay, lif, args) -> dict:
                       f"OpenMP {threads} threads), {dt:.1f} s excluding {setup:.1f} s setup"}
 
 
-def e2e_measure(sim, net, args) -> dict:
-    """Public API with host buffers: the network (pull slots, block starts, row_meta, tile
-    placement) uploaded from pinned host memory inside the timed region (amortised per
-    step), the step loop graph-replayed in chunks with every step's spike raster row
-    recorded on the device and read back to pinned host memory after each chunk."""
+def e2e_measure(sim, net, args, world: int, rank: int, lif) -> dict | None:
+    """Public API with host buffers: every rank's shard of the network (pull slots, block
+    starts, row_meta, tile placement) uploaded from pinned host memory inside the timed
+    region (amortised per step), the step loop graph-replayed in chunks with every step's
+    spike raster row recorded on the device and read back to pinned host memory after each
+    chunk.  N>1: DistSimulator (P2P exchange), barrier before, max over ranks."""
     import torch
     from paper_2205_07125_b200 import sim as S
-    csr = net.shards[0]
+    csr = net.shards[rank]
     steps = args.steps
-    esim = S.Simulator(net, sim.lif, args.seed, None, delivery="fused", record_raster_steps=steps,
-                       graph_chunk=args.chunk)
-    st = esim.states[0]
+    if world > 1:
+        import torch.distributed as dist
+        esim = make_sim(net, lif, args, "fused", world, record_raster_steps=steps)
+        st = esim.state
+    else:
+        esim = S.Simulator(net, lif, args.seed, None, delivery="fused", record_raster_steps=steps,
+                           graph_chunk=args.chunk)
+        st = esim.states[0]
     words = st.local_words
     parts = [csr.syn, csr.slice_ptr, csr.row_meta] + ([csr.row_perm] if csr.row_perm is not None else [])
     hosts = []
@@ -428,6 +445,9 @@ def e2e_measure(sim, net, args) -> dict:
     esim.advance(min(args.chunk, steps))          # warm: graph capture outside the timed region
     esim.reset(1)                                 # state re-initialised; the captured graph is kept
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+        torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -443,11 +463,23 @@ def e2e_measure(sim, net, args) -> dict:
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     h2d = sum(h.numel() * h.element_size() for h in hosts)
+    d2h = words * 4
+    if world > 1:
+        esim.check_status()
+        v = torch.tensor([ms, float(h2d), float(d2h)], dtype=torch.float64, device=csr.syn.device)
+        mx = v.clone()
+        dist.all_reduce(mx[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(v[1:], op=dist.ReduceOp.SUM)
+        ms, h2d, d2h = float(mx[0].item()), float(v[1].item()), float(v[2].item())
+        esim.close()
     del esim
+    if rank != 0:
+        return None
     return {"value": round(steps / (ms * 1e-3), 2), "unit": UNIT, "h2d_bytes_per_step": int(h2d // steps),
-            "d2h_bytes_per_step": int(words * 4),
+            "d2h_bytes_per_step": int(d2h),
             "note": "network H2D from pinned memory once per call (amortised), every step's spike raster "
-                    "row D2H (per graph chunk)"}
+                    "row D2H (per graph chunk)" + ("; bytes summed over ranks, time = max over ranks"
+                                                   if world > 1 else "")}
 
 
 # --------------------------------------------------------------------------- reference arm
@@ -465,11 +497,9 @@ def run_reference(args) -> dict | None:
     from oracle import c_oracle
     from paper_2205_07125_b200.sim import LifParams
     # bounded sample: at most ~2.5e9 synapses in host memory (the CPU cost of a step is
-    # linear in the synapse count, so k of the N shards' worth is timed and scaled by k/N)
-    k = world
-    while k > 1 and args.neurons * k * args.degree > 2.5e9:
-        k -= 1
-    n = args.neurons * k
+    # linear in the synapse count, so an n-neuron slice is timed and scaled by n / total)
+    total = total_neurons(args, world)
+    n = total if total * args.degree <= 2.5e9 else max(1, int(2.5e9 // args.degree))
     threads = os.cpu_count() or 1
     t = time.time()
     rowptr, col, q = c_oracle.generate_random_csr(n, args.degree, args.seed, threads=threads)
@@ -489,20 +519,20 @@ def run_reference(args) -> dict | None:
     t = time.time()
     run(steps)
     dt = max(time.time() - t - setup, 1e-9)
-    v = steps / dt * k / world
-    wl = ("config 2: 1M LIF neurons x 1k synapses, update + delivery" if world == 1 else
-          f"weak scaling: {args.neurons} neurons/GPU x {args.degree} synapses x {world} GPUs")
+    v = steps / dt * n / total
+    wl = workload_name(args, world)
     return {
         "metric": METRIC, "value": round(v, 4), "unit": UNIT, "n_gpus": world, "steps": steps,
         "warmup": warm, "ms_per_step": round(1e3 / v, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "fp32 state / int32 synaptic sums",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "fp32 state / int32 synaptic sums",
         "data": "synthetic (oracle CPU generator, same distributions)", "impl": "reference",
-        "config": {"workload": wl + " (CPU oracle port, all host threads)", "neurons": args.neurons * world,
+        "config": {"workload": wl + " (CPU oracle port, all host threads)", "neurons": total,
                    "mean_degree": args.degree, "synapses_simulated": int(rowptr[-1]),
                    "graph_build_s": round(t_build, 2)},
         "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{steps} full steps of a {n}-neuron network (= {k} of the {world} GPUs' "
-                                   f"neurons; steps/s scaled by {k}/{world}) (oracle/sim_oracle.c, OpenMP "
+                         "sample": f"{steps} full steps of a {n}-neuron network"
+                                   + (f" (a {n}/{total} slice; steps/s scaled by that fraction)" if n < total else "")
+                                   + f" (oracle/sim_oracle.c, OpenMP "
                                    f"{threads} threads; requested --steps {args.steps}, capped at ~60 s; "
                                    f"{setup:.1f} s one-time setup excluded)"},
         "e2e": {"value": round(v, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -515,7 +545,10 @@ def main() -> int:
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--neurons", type=int, default=1_000_000, help="neurons per GPU")
+    ap.add_argument("--neurons", type=int, default=1_000_000,
+                    help="network neurons (strong scaling) or neurons per GPU (--scaling weak)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="N>1: the same network over N GPUs (strong) or N x --neurons (weak)")
     ap.add_argument("--degree", type=float, default=1000.0)
     ap.add_argument("--communities", type=int, default=1, help=">1: regional SBM (config 5 family)")
     ap.add_argument("--intra-frac", type=float, default=0.9, help="regional: fraction of synapses inside a region")

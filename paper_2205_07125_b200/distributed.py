@@ -278,13 +278,17 @@ class DistSimulator:
         _native.check(self.lib.nc_sim_init(C.byref(s.c), C.byref(self.c_lif), st), "sim init")
         s.raster.zero_()
         rows = counter_steps if self.per_step_counts else 1
-        self.hop_ids = torch.zeros((rows, self.n, self.n), dtype=torch.int64, device=self.dev)
-        self.deliv_ids = torch.zeros((rows, self.n, self.n), dtype=torch.int64, device=self.dev)
-        self.X.hop_ids, self.X.deliv_ids = self.hop_ids.data_ptr(), self.deliv_ids.data_ptr()
+        if getattr(self, "hop_ids", None) is not None and self.hop_ids.shape[0] == rows:
+            self.hop_ids.zero_()        # same buffers: a captured step graph stays valid
+            self.deliv_ids.zero_()
+        else:
+            self.hop_ids = torch.zeros((rows, self.n, self.n), dtype=torch.int64, device=self.dev)
+            self.deliv_ids = torch.zeros((rows, self.n, self.n), dtype=torch.int64, device=self.dev)
+            self.X.hop_ids, self.X.deliv_ids = self.hop_ids.data_ptr(), self.deliv_ids.data_ptr()
+            self._graph = None
         self.lat_stamps.zero_()
         self.lat_ns.zero_()
         _native.check(self.lib.nc_xchg_reset(C.byref(self.X), st), "xchg reset")
-        self._graph = None
         torch.cuda.synchronize(self.dev)
         dist.barrier()
 

@@ -36,6 +36,8 @@ SMEM_RESERVE = 2048                # static shared memory (tile claim counters, 
 
 
 MAX_TILES = 256                    # csrc/sim_kernels.cu kMaxTiles
+BALANCE_UNITS = 6                  # tiled kernel: (slice, tile) units per warp at least ...
+BALANCE_MAX_TILES = 8              # ... up to this many tiles
 
 
 SMEM_TILED = 160 * 1024            # tiled step: shared memory left to L1 for the loads in flight
@@ -66,6 +68,12 @@ def plan_tiles(n_words: int, n_local: int, n_sms: int) -> tuple[int, int, bool]:
     budget = min(budget_all, SMEM_TILED) - (0 if global_part else part)
     tw_max = min(MAX_TILE_WORDS, max(32, budget // 8 // 32 * 32))
     T = (n_words + tw_max - 1) // tw_max
+    # small shards (strong scaling): warps claim (slice, tile) units dynamically, so with
+    # few slices per warp the last round leaves most warps idle; more (smaller) tiles
+    # give at least BALANCE_UNITS units per warp (measured at 4 GPUs on the config-2
+    # network, 1.65 slices per warp: 2 / 3 / 4 / 8 tiles at 0.80 / 0.82 / 0.84 / 0.82 of the
+    # copy peak)
+    T = max(T, min(BALANCE_MAX_TILES, -(-BALANCE_UNITS * n_sms * 32 // max(n_slices, 1))))
     if T > MAX_TILES:
         raise ValueError(f"spike bitmap of {n_words} words needs {T} tiles (max {MAX_TILES})")
     tw = ((n_words + T - 1) // T + 31) // 32 * 32   # multiple of 32: both buffers start in bank 0
