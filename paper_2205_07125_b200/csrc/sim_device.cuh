@@ -133,10 +133,13 @@ constexpr int kPfTiled = NC_PF_DIST;
 // (weight units).  Slots past the lane's own length are not loaded (`pad`, the
 // all-pad slot 0 -- id 0, q = 0 -- stands in: its lookups stay in the staged
 // tile and add nothing).
+// `part` of `nparts` (small shards split blocks so that every warp has several
+// units to claim): part k takes the k-th run of whole load groups of the
+// regular part; the last part also takes the ragged tail.
 template <int kPfDist>
 __device__ __forceinline__ int32_t sell_row_sum(const uint4* __restrict__ blk, uint32_t meta,
                                                 const uint32_t* __restrict__ bm, int32_t g_inh, int lane,
-                                                uint32_t pad) {
+                                                uint32_t pad, int part = 0, int nparts = 1) {
   const int emid = (int)(meta & 0xFFFFu);
   const int mine = (int)(meta >> 16);
   const int lo = __reduce_min_sync(kFull, (unsigned)mine);
@@ -145,20 +148,24 @@ __device__ __forceinline__ int32_t sell_row_sum(const uint4* __restrict__ blk, u
   int32_t acc = 0;
   const uint4* p = blk + lane;
   const uint4 padv = make_uint4(pad, pad, pad, pad);
+  const int per = nparts == 1 ? lo : ((lo + nparts - 1) / nparts + kUnroll - 1) / kUnroll * kUnroll;
+  const int ub = min(lo, part * per);
+  const int ue = min(lo, ub + per);
   // regular part: every lane has slots [0, lo)
-  for (int u0 = 0; u0 < lo; u0 += kUnroll) {
-    if (kPfDist > 0 && lane == 0 && u0 + kPfDist < lo) {
+  for (int u0 = ub; u0 < ue; u0 += kUnroll) {
+    if (kPfDist > 0 && lane == 0 && u0 + kPfDist < ue) {
       const int a = u0 + kPfDist;
-      prefetch_l2(blk + a * 32, (uint32_t)min(kUnroll, lo - a) * 512u);
+      prefetch_l2(blk + a * 32, (uint32_t)min(kUnroll, ue - a) * 512u);
     }
     uint4 e[kUnroll];
-    load_group(e, p + u0 * 32, lo - u0, padv, std::make_integer_sequence<int, kUnroll>{});
+    load_group(e, p + u0 * 32, ue - u0, padv, std::make_integer_sequence<int, kUnroll>{});
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      if (u0 + u >= lo) break;   // warp-uniform: no lookups for the pad of a partial group
+      if (u0 + u >= ue) break;   // warp-uniform: no lookups for the pad of a partial group
       acc += slot_term(e[u], bm) * (u0 + u < emid ? 1 : wi);
     }
   }
+  if (part != nparts - 1) return acc;
   // ragged tail (short: rows of a block have near-equal lengths)
   int off = lo * 32;
   for (int u0 = lo; u0 < hi; u0 += kTailUnroll) {

@@ -121,6 +121,10 @@ k_step_fused(const nc_shard_t sh, const nc_lif_params_t p) {
       else if (row < sh.n_local) sh.acc[row] = 0;
     }
     for (int k = threadIdx.x; k < T; k += blockDim.x) next_slice[k] = 0;
+    // flags bits 1-2: blocks split into 2^s parts claimed separately (small shards)
+    const int sp = (sh.flags >> 1) & 3;
+    const int nparts = 1 << sp;
+    const int units = cnt << sp;
     auto tile_bytes = [&](int t) {
       return (uint32_t)((min(TW, sh.n_words - t * TW) + 3) >> 2) * 16u;
     };
@@ -144,34 +148,37 @@ k_step_fused(const nc_shard_t sh, const nc_lif_params_t p) {
       // the next claim's block start and row_meta load (and its first slots are
       // prefetched into L2) while the current block streams
       auto claim = [&](int64_t& b0, uint32_t& m) {
-        int j = 0;
-        if (lane == 0) j = atomicAdd(&next_slice[t], 1);
-        j = __shfl_sync(kFull, j, 0);
-        if (j < cnt) {
+        int u = 0;
+        if (lane == 0) u = atomicAdd(&next_slice[t], 1);
+        u = __shfl_sync(kFull, u, 0);
+        if (u < units) {
+          const int j = u >> sp;
           const int pos = ((c + j * G) << 5) + lane;
           b0 = sh.slice_ptr[(int64_t)(c + j * G) * T + t];
           m = pos < sh.n_local ? sh.row_meta[(int64_t)t * sh.n_local + pos] : 0u;
           if (kPfTiled > 0 && pglob && lane == 0) prefetch_l2(syn4 + b0, kPfTiled * 512u);
         }
-        return j;
+        return u;
       };
       int64_t b0 = 0;
       uint32_t meta = 0u;
-      int j = claim(b0, meta);
-      while (j < cnt) {
+      int u = claim(b0, meta);
+      while (u < units) {
         int64_t b0n = 0;
         uint32_t metan = 0u;
-        const int jn = claim(b0n, metan);
+        const int un = claim(b0n, metan);
+        const int j = u >> sp;
         const int pos = ((c + j * G) << 5) + lane;
         // CTA-local index k of the row placed here in tile t (rows stay inside the CTA's slices)
         const int k = pos < sh.n_local ? sh.row_perm[(int64_t)t * sh.n_local + pos] : -1;
-        const int32_t sum = sell_row_sum<pglob ? kPfTiled : 0>(syn4 + b0, meta, bm, g_inh, lane, 0u);
+        const int32_t sum = sell_row_sum<pglob ? kPfTiled : 0>(syn4 + b0, meta, bm, g_inh, lane, 0u,
+                                                               u & (nparts - 1), nparts);
         // partials of sparse tiles are mostly 0 (no pre of the row fired): skip those
         if (k >= 0 && sum != 0) {
           if (!pglob) atomicAdd(&spart[k], sum);
           else red_add(&sh.acc[((c + (k >> 5) * G) << 5) + (k & 31)], sum);
         }
-        j = jn;
+        u = un;
         b0 = b0n;
         meta = metan;
       }

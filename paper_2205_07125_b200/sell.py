@@ -69,15 +69,24 @@ def plan_tiles(n_words: int, n_local: int, n_sms: int) -> tuple[int, int, bool]:
     tw_max = min(MAX_TILE_WORDS, max(32, budget // 8 // 32 * 32))
     T = (n_words + tw_max - 1) // tw_max
     # small shards (strong scaling): warps claim (slice, tile) units dynamically, so with
-    # few slices per warp the last round leaves most warps idle; more (smaller) tiles
-    # give at least BALANCE_UNITS units per warp (measured at 4 GPUs on the config-2
-    # network, 1.65 slices per warp: 2 / 3 / 4 / 8 tiles at 0.80 / 0.82 / 0.84 / 0.82 of the
-    # copy peak)
-    T = max(T, min(BALANCE_MAX_TILES, -(-BALANCE_UNITS * n_sms * 32 // max(n_slices, 1))))
+    # few units per warp the last round leaves many warps idle.  Below BALANCE_UNITS
+    # units per warp the blocks are split in two (block_split) and, if that is still
+    # short, the bitmap is cut into more tiles (measured on the config-2 network over
+    # 4 GPUs, 250 k rows/GPU: 2 tiles 0.79, split 0.84; 125 k rows/GPU: 2 tiles 0.61,
+    # 8 tiles 0.66, 2 tiles split 0.73, 4 tiles split 0.74 of the copy peak)
+    if n_slices * T < BALANCE_UNITS * n_sms * 32:
+        T = max(T, min(BALANCE_MAX_TILES, -(-BALANCE_UNITS * n_sms * 32 // (2 * max(n_slices, 1)))))
     if T > MAX_TILES:
         raise ValueError(f"spike bitmap of {n_words} words needs {T} tiles (max {MAX_TILES})")
     tw = ((n_words + T - 1) // T + 31) // 32 * 32   # multiple of 32: both buffers start in bank 0
     return T, tw, global_part
+
+
+def block_split(n_local: int, n_tiles: int, n_sms: int) -> int:
+    """log2 of the parts each (slice, tile) block is split into for the warps' claims
+    (nc_shard_t.flags bits 1-2; tiled kernel only): 1 below BALANCE_UNITS units per warp."""
+    n_slices = (n_local + 31) // 32
+    return 1 if n_tiles > 1 and n_slices * n_tiles < BALANCE_UNITS * n_sms * 32 else 0
 
 
 def device_sms(device=None) -> int:

@@ -14,6 +14,7 @@ import numpy as np
 import pytest
 
 import paper_2205_07125_b200 as nc
+from paper_2205_07125_b200 import sell
 from paper_2205_07125_b200 import sim as S
 from oracle import c_oracle
 
@@ -203,10 +204,15 @@ def test_partition_invariance_and_route_independence():
     np.testing.assert_array_equal(rep.raster, base.raster)
 
 
-@pytest.mark.parametrize("tile_words,glob", [(64, False), (100, False), (96, True)])
-def test_tiled_bitmap_matches_oracle(tile_words, glob):
+@pytest.mark.parametrize("tile_words,glob,split", [(64, False, None), (100, False, 0), (96, True, None),
+                                                   (96, True, 0), (64, False, 2)])
+def test_tiled_bitmap_matches_oracle(tile_words, glob, split, monkeypatch):
     """Force the shared-memory tiling of the spike bitmap (used above ~1.8 M neurons),
-    with the per-row partial sums in shared memory or (huge shards) in global memory."""
+    with the per-row partial sums in shared memory or (huge shards) in global memory, and
+    the blocks claimed whole (split 0), in halves (small shards: the default here) or in
+    quarters."""
+    if split is not None:
+        monkeypatch.setattr(sell, "block_split", lambda *a: split)
     g = cfg1(2)
     pm = nc.partition_greedy(g, 2)
     rt = routes(g, pm, "direct")

@@ -110,6 +110,17 @@ def test_plan_tiles():
     assert glob and T * tw >= 1_562_501 and 2 * tw * 4 <= sell.SMEM_BYTES - sell.SMEM_RESERVE
 
 
+def test_small_shard_balance():
+    # strong scaling of the config-2 network: 1 / 2 GPUs unchanged, 4 GPUs split blocks,
+    # 8 GPUs split blocks over 4 tiles (>= BALANCE_UNITS claim units per warp)
+    for n_local, want_T, want_split in ((1_000_000, 2, 0), (500_000, 2, 0), (250_000, 2, 1), (125_000, 4, 1)):
+        T, tw, glob = sell.plan_tiles(31_250, n_local, 148)
+        assert (T, sell.block_split(n_local, T, 148), glob) == (want_T, want_split, False)
+        units = (n_local + 31) // 32 * T << sell.block_split(n_local, T, 148)
+        assert units >= sell.BALANCE_UNITS * 148 * 32 or T == sell.BALANCE_MAX_TILES
+    assert sell.block_split(1000, 1, 148) == 0   # one-tile kernel: never split
+
+
 def test_layout_from_counts_torch_matches_numpy():
     rng = np.random.default_rng(1)
     counts = rng.integers(0, 50, (77 * 3 * 2,))
