@@ -205,6 +205,13 @@ typedef struct nc_shard {
   uint32_t* spk_ids;      /* [2][spk_cap] */
   int32_t* spk_count;     /* [2] */
   int64_t spk_cap;
+  /* optional (NULL = off): device %globaltimer of the fused step kernel, per
+   * step s (slot s mod kstamp_steps): [2s] = first CTA start (atomicMin; the host
+   * fills it with ~0), [2s+1] = last CTA end (atomicMax; host fills 0) -- the
+   * kernel's duration inside a timed loop without a profiler */
+  unsigned long long* kstamp;
+  int32_t kstamp_steps;
+  int32_t pad4;
 } nc_shard_t;
 
 /* Set kernel attributes (dynamic shared memory opt-in) once; call before any

@@ -53,6 +53,7 @@ class ShardC(C.Structure):
         ("row_perm", c_void_p), ("cta_groups", c_int32), ("pb_bins", c_int32),
         ("pb_rowptr", c_void_p), ("pb_binoff", c_void_p), ("pb_syn", c_void_p), ("pb_rows", c_int32),
         ("pad3", c_int32), ("spk_ids", c_void_p), ("spk_count", c_void_p), ("spk_cap", c_int64),
+        ("kstamp", c_void_p), ("kstamp_steps", c_int32), ("pad4", c_int32),
     ]
 
 

@@ -55,6 +55,12 @@ __device__ __forceinline__ uint4 ld_keep(const uint4* p) {
 // bit * q + acc is one IMAD (left to itself the compiler emits ISETP + SEL +
 // IADD).  Moving the bit and q extraction to the FMA pipe (mul.hi tricks)
 // balanced the pipes but measured 2-3 % slower, so this stays on the ALU pipe.
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t r;
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));

@@ -44,6 +44,7 @@ k_step_fused(const nc_shard_t sh, const nc_lif_params_t p) {
   uint32_t* cur = (step & 1) ? sh.bitmap1 : sh.bitmap0;
   uint32_t* sbm = reinterpret_cast<uint32_t*>(smem4);
   if (threadIdx.x == 0) block_count = 0;
+  if (sh.kstamp && threadIdx.x == 0) atomicMin(&sh.kstamp[2 * (step % sh.kstamp_steps)], globaltimer_ns());
   if (kLif) clear_remote(sh, cur, blockIdx.x, gridDim.x);
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -211,6 +212,10 @@ k_step_fused(const nc_shard_t sh, const nc_lif_params_t p) {
     }
   }
   if (kLif) add_spike_total(sh, my_spikes, &block_count);
+  if (sh.kstamp) {   // uniform
+    __syncthreads();
+    if (threadIdx.x == 0) atomicMax(&sh.kstamp[2 * (step % sh.kstamp_steps) + 1], globaltimer_ns());
+  }
 }
 
 // K1+K2 alone: consumes and zeroes acc.
