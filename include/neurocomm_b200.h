@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define NC_ABI_VERSION 1
+#define NC_ABI_VERSION 2
 
 enum {
   NC_OK = 0,

@@ -15,7 +15,7 @@ from pathlib import Path
 
 LIB_NAME = "libneurocomm_b200.so"
 LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 NC_OK, NC_E_ARG, NC_E_CUDA, NC_E_OVERFLOW, NC_E_TIMEOUT, NC_E_NCCL, NC_E_PARSE, NC_E_IO = range(8)
 MAX_SHARDS = 16
