@@ -91,7 +91,8 @@ int nc_weight_histogram(const double* weights, const int64_t* assignment, int64_
  *
  * Synapses: each undirected edge (i, j, p) of NeuronGraph is one synapse in
  * each direction.  A pull synapse is a 25-bit field
- *     (q << 19) | (pre_internal_id - first id of its bitmap tile),
+ *     (q << 19) | (id ^ 31),  id = pre_internal_id - first id of its bitmap tile
+ * (the low 5 bits hold 31 - the pre's bit in its bitmap word),
  * q = ceil(32 * p) in [1, 32]; q = 0 is the pad.  Tiles are at most 16384
  * words, so the tile-relative id fits 19 bits (with one tile it is the
  * internal id).  A 16-byte slot holds 5 fields, field i at bit 25 i of

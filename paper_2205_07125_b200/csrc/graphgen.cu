@@ -223,7 +223,7 @@ __global__ void k_sell_pack(const uint32_t* src, int64_t n_slots, uint4* dst) {
 #pragma unroll
     for (int i = 0; i < ncdev::kSlotEntries; ++i) {
       const uint32_t e = src[s * ncdev::kSlotEntries + i];
-      f[i] = ((e >> 26) << 19) | (e & ncdev::kFieldIdMask);
+      f[i] = ncdev::make_field(e >> 26, e & ncdev::kFieldIdMask);
     }
     dst[s] = ncdev::pack_slot(f);
   }
@@ -255,7 +255,7 @@ __global__ void k_dest_mask(const int64_t* slice_ptr, const uint32_t* row_meta, 
       for (int c = 0; c < ncdev::kSlotEntries; ++c) {
         const uint32_t f = x.f[c] & ncdev::kFieldMask;
         if ((f >> 19) == 0) continue;  // pad
-        const int64_t pre = (f & ncdev::kFieldIdMask) + tbase;
+        const int64_t pre = ncdev::field_id(f) + tbase;
         for (int h = 0; h < n_shards; ++h)
           if (pre >= shard_base[h] && pre < shard_base[h + 1]) m |= 1u << h;
       }

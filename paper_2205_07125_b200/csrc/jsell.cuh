@@ -6,13 +6,22 @@
 
 namespace ncdev {
 
-// A 16-byte slot holds 5 synapse fields of 25 bits: f = (q << 19) | id, id the
-// pre's bitmap index relative to its tile (< 2^19, so tiles are <= 16384
-// words), q in [1, 32] its weight units; the pad field is 0 (q = 0).  Field i
-// starts at bit 25 i of the slot (x | y << 32 | z << 64 | w << 96).
+// A 16-byte slot holds 5 synapse fields of 25 bits: f = (q << 19) | (id ^ 31),
+// id the pre's bitmap index relative to its tile (< 2^19, so tiles are <= 16384
+// words), q in [1, 32] its weight units; the pad field has q = 0.  The low 5
+// bits store 31 - (bit in word), so a left funnel shift of the word by f moves
+// the pre's bit to bit 31 (field_term).  Field i starts at bit 25 i of the slot
+// (x | y << 32 | z << 64 | w << 96).
 constexpr int kSlotEntries = 5;
 constexpr uint32_t kFieldMask = (1u << 25) - 1u;
 constexpr uint32_t kFieldIdMask = (1u << 19) - 1u;
+constexpr uint32_t kBitXor = 31u;
+
+// packed field <-> (q, tile-relative id)
+__host__ __device__ __forceinline__ uint32_t make_field(uint32_t q, uint32_t id) {
+  return (q << 19) | (id ^ kBitXor);
+}
+__host__ __device__ __forceinline__ uint32_t field_id(uint32_t f) { return (f & kFieldIdMask) ^ kBitXor; }
 
 struct Fields {
   uint32_t f[kSlotEntries];

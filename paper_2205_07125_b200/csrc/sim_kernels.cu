@@ -453,7 +453,7 @@ __global__ void k_push_build(const nc_shard_t sh, int phase, int64_t* rowptr, in
         const uint32_t f = x.f[c] & kFieldMask;
         const uint32_t q = f >> 19;
         if (q == 0) continue;
-        const uint32_t pre = (f & kFieldIdMask) + (uint32_t)t * (uint32_t)sh.tile_words * 32u;
+        const uint32_t pre = field_id(f) + (uint32_t)t * (uint32_t)sh.tile_words * 32u;
         if (phase == 0) {
           atomicAdd(reinterpret_cast<unsigned long long*>(rowptr + pre + 1), 1ull);
         } else {
@@ -496,7 +496,7 @@ __global__ void k_push_binned(const nc_shard_t sh, int phase, uint32_t* counts, 
         const uint32_t f = x.f[c] & kFieldMask;
         const uint32_t q = f >> 19;
         if (q == 0) continue;
-        const uint32_t pre = (f & kFieldIdMask) + (uint32_t)t * (uint32_t)sh.tile_words * 32u;
+        const uint32_t pre = field_id(f) + (uint32_t)t * (uint32_t)sh.tile_words * 32u;
         const int64_t key = (int64_t)pre * B + bin;
         if (phase == 0) {
           atomicAdd(counts + key, 1u);

@@ -29,6 +29,7 @@ ID_BITS = 26                       # unpacked builder entry: (q << 26) | tile-re
 ID_MASK = (1 << ID_BITS) - 1
 SLOT_ENTRIES = 5                   # packed slot: 5 fields of 25 bits, (q << 19) | tile-relative id
 FIELD_ID_BITS = 19
+BIT_XOR = 31                       # packed id stores 31 - (bit in word) in its low 5 bits
 FIELD_MASK = (1 << 25) - 1
 MAX_TILE_WORDS = 1 << (FIELD_ID_BITS - 5)   # 16384 words: tile-relative ids fit 19 bits
 SMEM_BYTES = 227 * 1024            # opt-in dynamic shared memory per CTA on sm_100
@@ -298,7 +299,8 @@ def host_build(row, pre_internal, q, inh, n_local: int, n_tiles: int, tile_words
 def pack_slots(unpacked: np.ndarray) -> np.ndarray:
     """numpy twin of nc_sell_pack: 5 unpacked entries (q << 26 | id) per slot -> 4 uint32 words."""
     e = np.asarray(unpacked, dtype=np.uint64).reshape(-1, SLOT_ENTRIES)
-    f = ((e >> np.uint64(ID_BITS)) << np.uint64(FIELD_ID_BITS)) | (e & np.uint64((1 << FIELD_ID_BITS) - 1))
+    f = ((e >> np.uint64(ID_BITS)) << np.uint64(FIELD_ID_BITS)) | \
+        ((e & np.uint64((1 << FIELD_ID_BITS) - 1)) ^ np.uint64(BIT_XOR))
     lo = f[:, 0] | (f[:, 1] << np.uint64(25)) | ((f[:, 2] & np.uint64((1 << 14) - 1)) << np.uint64(50))
     hi = (f[:, 2] >> np.uint64(14)) | (f[:, 3] << np.uint64(11)) | (f[:, 4] << np.uint64(36))
     out = np.empty((e.shape[0], 4), dtype=np.uint32)
@@ -307,6 +309,11 @@ def pack_slots(unpacked: np.ndarray) -> np.ndarray:
     out[:, 2] = (hi & np.uint64(0xFFFFFFFF)).astype(np.uint32)
     out[:, 3] = (hi >> np.uint64(32)).astype(np.uint32)
     return out.reshape(-1)
+
+
+def field_id(f):
+    """Tile-relative pre id of packed fields (the low 5 bits store 31 - bit; jsell.cuh)."""
+    return (f & ((1 << FIELD_ID_BITS) - 1)) ^ BIT_XOR
 
 
 def unpack_slots(words):
@@ -365,7 +372,7 @@ def decode(csr: SellCSR):
     keep = (q > 0) & valid_row[:, None]
     rows5 = row[:, None].expand(-1, SLOT_ENTRIES)[keep]
     inh5 = inh[:, None].expand(-1, SLOT_ENTRIES)[keep]
-    pre = (ent & ((1 << FIELD_ID_BITS) - 1)) + (t * (csr.tile_words * 32))[:, None]   # back to internal ids
+    pre = field_id(ent) + (t * (csr.tile_words * 32))[:, None]   # back to internal ids
     return rows5, pre[keep], q[keep], inh5
 
 

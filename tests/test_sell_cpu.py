@@ -58,7 +58,7 @@ def test_host_build_round_trip(n_local, n_tiles, tile_words):
             assert (np.diff(lens[own, t]) <= 0).all() or n_tiles == 1
     # fields of a tile block hold ids relative to the tile (they index the staged copy)
     f = sell.unpack_slots(torch.from_numpy(syn.astype(np.int64)).view(-1, 4))
-    assert (f & ((1 << sell.FIELD_ID_BITS) - 1) < tile_words * 32).all()
+    assert (sell.field_id(f) < tile_words * 32).all()
     assert int((f >> sell.FIELD_ID_BITS > 0).sum()) == m
 
 
@@ -72,9 +72,10 @@ def test_pack_slots_bit_layout():
     for s_ in range(50):
         v = sum(int(words[s_, i]) << (32 * i) for i in range(4))
         for i in range(5):
-            assert (v >> (25 * i)) & ((1 << 25) - 1) == (int(q[s_, i]) << 19) | int(ids[s_, i])
+            assert (v >> (25 * i)) & ((1 << 25) - 1) == (int(q[s_, i]) << 19) | (int(ids[s_, i]) ^ 31)
     f = sell.unpack_slots(torch.from_numpy(sell.pack_slots(unpacked.reshape(-1)).astype(np.int64)).view(-1, 4))
-    np.testing.assert_array_equal(f.numpy(), (q << 19) | ids)
+    np.testing.assert_array_equal(f.numpy(), (q << 19) | (ids ^ 31))
+    np.testing.assert_array_equal(sell.field_id(f).numpy(), ids)
 
 
 def test_jagged_positions_match_the_formula():
