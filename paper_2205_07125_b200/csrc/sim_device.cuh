@@ -68,7 +68,8 @@ __device__ __forceinline__ uint32_t field_term(uint32_t f, const uint32_t* __res
   // the pre's bit to bit 31 (the field stores 31 - bit), sign-spread to a mask that
   // keeps the field's q bits: 3 ALU ops, no multiply; slot_term shifts the sum down once
   // (measured against bit * q as one IMAD per field: 0.543 vs 0.565 ms in a sustained
-  // 1 000-step loop under sw_power_cap, 0.580 vs 0.601 ms at 8 tiles)
+  // 1 000-step loop under sw_power_cap, 0.580 vs 0.601 ms at 8 tiles; against the bit by
+  // mul.hi and the product by mad on the FMA pipe: 0.522 vs 0.528 ms)
   const int32_t fired = (int32_t)__funnelshift_l(word, word, f) >> 31;
   return acc + (f & (uint32_t)fired & (63u << 19));
 }
