@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define NC_ABI_VERSION 2
+#define NC_ABI_VERSION 3
 
 enum {
   NC_OK = 0,
@@ -213,6 +213,16 @@ typedef struct nc_shard {
   unsigned long long* kstamp;
   int32_t kstamp_steps;
   int32_t pad4;
+  /* optional fused P2P send (direct exchange, P2P transport; xsend_on = 0: off):
+   * the step kernel stores every spike bucketed for peer h straight into h's
+   * IPC-mapped inbox (xsend[h], the nc_xchg_t P2P layout, tagged 8-byte words)
+   * while other CTAs still compute, and its last CTA writes the tagged headers
+   * (count; 0 for peers outside xsend_mask = the heartbeat); nc_xchg_p2p then
+   * only receives (nc_xchg_t.fused_send = 1) */
+  unsigned long long* xsend[NC_MAX_SHARDS];
+  int64_t xsend_cap;      /* ids per message = nc_xchg_t.cap */
+  int32_t xsend_on;
+  int32_t xsend_mask;     /* peers with a phase-1 message (nc_xchg_t.send1_mask) */
 } nc_shard_t;
 
 /* Set kernel attributes (dynamic shared memory opt-in) once; call before any
@@ -331,6 +341,9 @@ typedef struct nc_xchg {
   unsigned long long* dbg;         /* diagnostics or NULL: [64 steps][n*B blocks][4]
                                       globaltimer at block start, message published,
                                       peer flag seen, inbound ids scattered      */
+  int32_t fused_send;              /* 1: the step kernel already sent phase 1
+                                      (nc_shard_t.xsend): receive only           */
+  int32_t pad2;
 } nc_xchg_t;
 
 /* Inbox words needed per rank for the P2P transport. */

@@ -15,7 +15,7 @@ from pathlib import Path
 
 LIB_NAME = "libneurocomm_b200.so"
 LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 NC_OK, NC_E_ARG, NC_E_CUDA, NC_E_OVERFLOW, NC_E_TIMEOUT, NC_E_NCCL, NC_E_PARSE, NC_E_IO = range(8)
 MAX_SHARDS = 16
@@ -54,6 +54,7 @@ class ShardC(C.Structure):
         ("pb_rowptr", c_void_p), ("pb_binoff", c_void_p), ("pb_syn", c_void_p), ("pb_rows", c_int32),
         ("pad3", c_int32), ("spk_ids", c_void_p), ("spk_count", c_void_p), ("spk_cap", c_int64),
         ("kstamp", c_void_p), ("kstamp_steps", c_int32), ("pad4", c_int32),
+        ("xsend", c_void_p * MAX_SHARDS), ("xsend_cap", c_int64), ("xsend_on", c_int32), ("xsend_mask", c_int32),
     ]
 
 
@@ -88,6 +89,7 @@ class XchgC(C.Structure):
         ("done", c_void_p), ("send_done", c_void_p), ("blocks_per_peer", c_int32), ("pad1", c_int32),
         ("barrier", c_void_p), ("lat_start", c_void_p), ("lat_ns", c_void_p),
         ("spk_ids", c_void_p), ("spk_count", c_void_p), ("spk_cap", c_int64), ("dbg", c_void_p),
+        ("fused_send", c_int32), ("pad2", c_int32),
     ]
 
 

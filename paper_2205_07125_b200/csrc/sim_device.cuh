@@ -222,9 +222,16 @@ __device__ __forceinline__ bool lif_step(float& v, float& isyn, uint8_t& ref, in
   return false;
 }
 
-// Warp-aggregated append of the ids of lanes in `m` (whole warp calls).
+__device__ __forceinline__ void st_relaxed_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Warp-aggregated append of the ids of lanes in `m` (whole warp calls); with
+// `remote` (fused P2P send) each id also goes, tagged, to the same position of
+// the peer's inbox message (xchg_device.cuh: word 1 + pos of the slot).
 __device__ __forceinline__ void warp_append(uint32_t* ids, int32_t* count, int64_t cap, uint32_t m,
-                                            uint32_t my_id, int lane, int32_t* status) {
+                                            uint32_t my_id, int lane, int32_t* status,
+                                            unsigned long long* remote = nullptr, uint32_t tag = 0u) {
   if (m == 0) return;
   const int leader = __ffs(m) - 1;
   int32_t base = 0;
@@ -232,8 +239,37 @@ __device__ __forceinline__ void warp_append(uint32_t* ids, int32_t* count, int64
   base = __shfl_sync(kFull, base, leader);
   if ((m >> lane) & 1u) {
     const int64_t pos = (int64_t)base + __popc(m & ((1u << lane) - 1u));
-    if (pos < cap) ids[pos] = my_id;
-    else atomicExch(status, 1);
+    if (pos < cap) {
+      ids[pos] = my_id;
+      if (remote) st_relaxed_sys_u64(remote + 1 + pos, ((unsigned long long)tag << 32) | my_id);
+    } else {
+      atomicExch(status, 1);
+    }
+  }
+}
+
+// Phase-1 message slot of this shard in peer h's inbox (xchg_device.cuh slot_off).
+__device__ __forceinline__ unsigned long long* xsend_slot(const nc_shard_t& sh, int h, int step) {
+  return sh.xsend[h] + ((int64_t)((step & 1) * sh.n_shards + sh.shard)) * (sh.xsend_cap + 1);
+}
+
+// Fused P2P send, end of the step kernel: the last CTA writes every peer's
+// tagged header (count; 0 = heartbeat) once all CTAs have bucketed their spikes.
+__device__ __forceinline__ void xsend_headers(const nc_shard_t& sh, int step) {
+  if (!sh.xsend_on) return;
+  __syncthreads();
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(sh.work + 2, 1u) + 1u == gridDim.x;
+    if (last) __threadfence();
+  }
+  __syncthreads();
+  const int h = threadIdx.x;
+  if (last && h < sh.n_shards && h != sh.shard) {
+    int64_t cnt = ((sh.xsend_mask >> h) & 1) ? *(volatile int32_t*)(sh.bucket_count + h) : 0;
+    cnt = cnt < sh.xsend_cap ? cnt : sh.xsend_cap;
+    st_relaxed_sys_u64(xsend_slot(sh, h, step), ((unsigned long long)(step + 1) << 32) | (uint32_t)cnt);
   }
 }
 
@@ -258,7 +294,8 @@ __device__ __forceinline__ uint32_t emit_spikes(const nc_shard_t& sh, uint32_t* 
       pending &= pending - 1;
       const uint32_t m = __ballot_sync(kFull, (hm >> h) & 1u);
       warp_append(sh.bucket_ids + (int64_t)h * sh.bucket_cap, sh.bucket_count + h, sh.bucket_cap, m,
-                  my_id, lane, sh.status);
+                  my_id, lane, sh.status, sh.xsend_on ? xsend_slot(sh, h, step) : nullptr,
+                  (uint32_t)step + 1u);
     }
   }
   return fmask;

@@ -212,6 +212,7 @@ k_step_fused(const nc_shard_t sh, const nc_lif_params_t p) {
     }
   }
   if (kLif) add_spike_total(sh, my_spikes, &block_count);
+  if (kLif) xsend_headers(sh, step);
   if (sh.kstamp) {   // uniform
     __syncthreads();
     if (threadIdx.x == 0) atomicMax(&sh.kstamp[2 * (step % sh.kstamp_steps) + 1], globaltimer_ns());

@@ -242,8 +242,9 @@ static __device__ void p2p_block(const nc_xchg_t& X, int ex, int B, int step) {
       }
       if (threadIdx.x == 0 && kb == 0 && cnt) add64(hop + X.rank * X.n + b, cnt);
     }
-    ll_send(reinterpret_cast<uint64_t*>(X.peer_inbox[b]) + slot_off(X, 0, par, X.rank),
-            X.bucket_ids + (int64_t)b * X.bucket_cap, cnt, kb, B, tag);
+    if (!X.fused_send)   // else the step kernel stored the ids and the header already
+      ll_send(reinterpret_cast<uint64_t*>(X.peer_inbox[b]) + slot_off(X, 0, par, X.rank),
+              X.bucket_ids + (int64_t)b * X.bucket_cap, cnt, kb, B, tag);
     if (dbg) dbg[1] = globaltimer();
   }
   // ---- phase 1 receive from peer b, chunk kb

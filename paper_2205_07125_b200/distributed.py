@@ -187,6 +187,17 @@ class DistSimulator:
             self._setup_nccl()
         else:
             self._setup_p2p()
+        # fused send (direct P2P exchange after the fused step): the step kernel stores its
+        # bucketed spikes straight into the peers' inboxes and writes the headers; the
+        # exchange kernel only receives.  NC_FUSED_SEND=0 keeps the send in the exchange kernel.
+        self.fused_send = (transport == "p2p" and delivery == "fused" and not self.plan.two_level
+                           and int(self.state.bucket_cap) <= cap and os.environ.get("NC_FUSED_SEND", "1") != "0")
+        if self.fused_send:
+            c = self.state.c
+            for h in range(n):
+                c.xsend[h] = X.peer_inbox[h] if h != self.rank else None
+            c.xsend_cap, c.xsend_on, c.xsend_mask = cap, 1, self.masks["send1"]
+            X.fused_send = 1
         self._graph = None
         self._graph_len = 0
         _native.check(self.lib.nc_sim_prepare(), "prepare")
