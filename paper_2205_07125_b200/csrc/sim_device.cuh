@@ -260,9 +260,11 @@ __device__ __forceinline__ void xsend_headers(const nc_shard_t& sh, int step) {
   __syncthreads();
   __shared__ bool last;
   if (threadIdx.x == 0) {
-    __threadfence();
-    last = atomicAdd(sh.work + 2, 1u) + 1u == gridDim.x;
-    if (last) __threadfence();
+    // release: this CTA's bucket counts (ordered by the barrier) before the arrival;
+    // acquire: the last arrival sees every CTA's counts
+    uint32_t prev;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(sh.work + 2) : "memory");
+    last = prev + 1u == gridDim.x;
   }
   __syncthreads();
   const int h = threadIdx.x;
