@@ -213,7 +213,7 @@ typedef struct nc_shard {
   unsigned long long* kstamp;
   int32_t kstamp_steps;
   int32_t pad4;
-  /* optional fused P2P send (direct exchange, P2P transport; xsend_on = 0: off):
+  /* optional fused P2P send (P2P transport, phase 1; xsend_on = 0: off):
    * the step kernel stores every spike bucketed for peer h straight into h's
    * IPC-mapped inbox (xsend[h], the nc_xchg_t P2P layout, tagged 8-byte words)
    * while other CTAs still compute, and its last CTA writes the tagged headers

@@ -187,10 +187,11 @@ class DistSimulator:
             self._setup_nccl()
         else:
             self._setup_p2p()
-        # fused send (direct P2P exchange after the fused step): the step kernel stores its
-        # bucketed spikes straight into the peers' inboxes and writes the headers; the
-        # exchange kernel only receives.  NC_FUSED_SEND=0 keeps the send in the exchange kernel.
-        self.fused_send = (transport == "p2p" and delivery == "fused" and not self.plan.two_level
+        # fused send (P2P exchange after the fused step): the step kernel stores its bucketed
+        # spikes straight into the first hops' inboxes and writes the headers; the exchange
+        # kernel only receives phase 1 (and runs the relay phase of two-level routing).
+        # NC_FUSED_SEND=0 keeps the phase-1 send in the exchange kernel.
+        self.fused_send = (transport == "p2p" and delivery == "fused"
                            and int(self.state.bucket_cap) <= cap and os.environ.get("NC_FUSED_SEND", "1") != "0")
         if self.fused_send:
             c = self.state.c
