@@ -74,6 +74,9 @@ def gather_dest(net: Network, rank: int, world: int, device):
     return _as_u16(g)
 
 
+
+FUSED_SEND_MIN_ROWS = 32768   # fused P2P send from the step kernel above this many local rows
+
 class DistSimulator:
     """Step loop of this rank's shard with a multi-GPU spike exchange."""
 
@@ -190,9 +193,14 @@ class DistSimulator:
         # fused send (P2P exchange after the fused step): the step kernel stores its bucketed
         # spikes straight into the first hops' inboxes and writes the headers; the exchange
         # kernel only receives phase 1 (and runs the relay phase of two-level routing).
-        # NC_FUSED_SEND=0 keeps the phase-1 send in the exchange kernel.
-        self.fused_send = (transport == "p2p" and delivery == "fused"
-                           and int(self.state.bucket_cap) <= cap and os.environ.get("NC_FUSED_SEND", "1") != "0")
+        # Only for shards big enough that the step kernel outlasts the transfer: on config 1
+        # (2 500 rows per GPU, a ~5 us step kernel) the last-CTA header pass cost more than
+        # the overlap gained (63.6 k vs 66.9 k steps/s, profiles/r01_cfg1_4gpu_fused_send.jsonl).
+        # NC_FUSED_SEND=0 / 1 forces it off / on.
+        env = os.environ.get("NC_FUSED_SEND")
+        big = lay.n_local(self.rank) >= FUSED_SEND_MIN_ROWS
+        self.fused_send = (transport == "p2p" and delivery == "fused" and int(self.state.bucket_cap) <= cap
+                           and (env == "1" or (env is None and big)))
         if self.fused_send:
             c = self.state.c
             for h in range(n):

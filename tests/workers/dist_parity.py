@@ -53,10 +53,15 @@ def main() -> int:
             ref = c_oracle.simulate_csr(rp, col, q, pm.assignment, world, rt.next_hop_matrix(), lif.constants(1),
                                         steps, threads=8)
         runs = [(t, "fused") for t in os.environ.get("NC_TRANSPORTS", "p2p,nccl").split(",")]
-        runs += [("p2p", "persistent"), ("p2p", "binned"), ("nccl", "binned")]
+        runs += [("p2p", "fused+send"), ("p2p", "persistent"), ("p2p", "binned"), ("nccl", "binned")]
         for transport, delivery in runs:
-            sim = DistSimulator(net, lif, 1, rt, transport=transport, delivery=delivery,
+            # fused+send: the step kernel's own P2P send, forced on (off by default at this size)
+            if delivery == "fused+send":
+                os.environ["NC_FUSED_SEND"] = "1"
+            sim = DistSimulator(net, lif, 1, rt, transport=transport, delivery=delivery.split("+")[0],
                                 record_raster_steps=steps, per_step_counts=True)
+            os.environ.pop("NC_FUSED_SEND", None)
+            assert sim.fused_send == (delivery == "fused+send")
             rep = sim.run(steps)
             sim.close()
             if rank == 0:
