@@ -610,9 +610,15 @@ def main() -> int:
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    # stdout carries exactly the one JSON line: anything a library writes to fd 1 while we
+    # run (NCCL's "NCCL version ..." banner on rank 0, for one) goes to stderr instead
+    sys.stdout.flush()
+    json_out = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     res = run_reference(args) if args.impl == "reference" else run_ours(args)
     if res is not None:
-        print(json.dumps(res), flush=True)
+        print(json.dumps(res), file=json_out, flush=True)
+    json_out.close()
     return 0
 
 
