@@ -255,8 +255,10 @@ __device__ __forceinline__ unsigned long long* xsend_slot(const nc_shard_t& sh, 
 
 // Fused P2P send, end of the step kernel: the last CTA writes every peer's
 // tagged header (count; 0 = heartbeat) once all CTAs have bucketed their spikes.
+// kSend = false compiles the send out (the launcher picks it from sh.xsend_on).
+template <bool kSend>
 __device__ __forceinline__ void xsend_headers(const nc_shard_t& sh, int step) {
-  if (!sh.xsend_on) return;
+  if (!kSend || !sh.xsend_on) return;
   __syncthreads();
   __shared__ bool last;
   if (threadIdx.x == 0) {
@@ -276,6 +278,7 @@ __device__ __forceinline__ void xsend_headers(const nc_shard_t& sh, int step) {
 }
 
 // K2: bitmap word, raster, fired list and next-hop buckets for one 32-neuron tile.
+template <bool kSend>
 __device__ __forceinline__ uint32_t emit_spikes(const nc_shard_t& sh, uint32_t* cur, int tile, int row,
                                                 bool fired, int lane, int step) {
   const uint32_t fmask = __ballot_sync(kFull, fired);
@@ -296,7 +299,7 @@ __device__ __forceinline__ uint32_t emit_spikes(const nc_shard_t& sh, uint32_t* 
       pending &= pending - 1;
       const uint32_t m = __ballot_sync(kFull, (hm >> h) & 1u);
       warp_append(sh.bucket_ids + (int64_t)h * sh.bucket_cap, sh.bucket_count + h, sh.bucket_cap, m,
-                  my_id, lane, sh.status, sh.xsend_on ? xsend_slot(sh, h, step) : nullptr,
+                  my_id, lane, sh.status, (kSend && sh.xsend_on) ? xsend_slot(sh, h, step) : nullptr,
                   (uint32_t)step + 1u);
     }
   }
@@ -321,6 +324,7 @@ __device__ __forceinline__ void add_spike_total(const nc_shard_t& sh, uint32_t l
 }
 
 // LIF + spike emission for the 32 rows of one slice (lane = row).
+template <bool kSend>
 __device__ __forceinline__ uint32_t update_slice(const nc_shard_t& sh, const nc_lif_params_t& p, uint32_t* cur,
                                                  int slice, int lane, int32_t acc, int step) {
   const int row = (slice << 5) + lane;
@@ -334,7 +338,7 @@ __device__ __forceinline__ uint32_t update_slice(const nc_shard_t& sh, const nc_
     sh.i_syn[row] = isyn;
     sh.refrac[row] = ref;
   }
-  return emit_spikes(sh, cur, slice, row, fired, lane, step);
+  return emit_spikes<kSend>(sh, cur, slice, row, fired, lane, step);
 }
 
 // K1+K2 alone (consumes and zeroes acc).  Every CTA owns a contiguous range of

@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(1024, 1) k_step_binned(const nc_shard_t sh, co
 // keeps the per-row partial sums in shared memory behind the tile.
 // kGlobalPart: tiled partial sums in `acc` (flags bit 0), with an L2 prefetch
 // of the synapse stream (measured: +7% there, -2% with shared partials).
-template <bool kTiled, bool kLif, bool kGlobalPart = false>
+template <bool kTiled, bool kLif, bool kGlobalPart = false, bool kSend = false>
 __global__ void __launch_bounds__(kThreads, 1)
 k_step_fused(const nc_shard_t sh, const nc_lif_params_t p) {
   extern __shared__ uint4 smem4[];
@@ -90,7 +90,7 @@ k_step_fused(const nc_shard_t sh, const nc_lif_params_t p) {
       const int row = (slice << 5) + lane;
       const int32_t acc = sell_row_sum<0>(syn4 + b0, meta, sbm, g_inh, lane, 0u);
       if (kLif) {
-        const uint32_t fm = update_slice(sh, p, cur, slice, lane, acc, step);
+        const uint32_t fm = update_slice<kSend>(sh, p, cur, slice, lane, acc, step);
         if (lane == 0) my_spikes += __popc(fm);
       } else if (row < sh.n_local) {
         sh.acc[row] = acc;
@@ -204,7 +204,7 @@ k_step_fused(const nc_shard_t sh, const nc_lif_params_t p) {
       const int row = (slice << 5) + lane;
       const int32_t acc = pglob ? (row < sh.n_local ? sh.acc[row] : 0) : spart[j * 32 + lane];
       if (kLif) {
-        const uint32_t fm = update_slice(sh, p, cur, slice, lane, acc, step);
+        const uint32_t fm = update_slice<kSend>(sh, p, cur, slice, lane, acc, step);
         if (lane == 0) my_spikes += __popc(fm);
       } else if (row < sh.n_local) {
         sh.acc[row] = acc;
@@ -212,7 +212,7 @@ k_step_fused(const nc_shard_t sh, const nc_lif_params_t p) {
     }
   }
   if (kLif) add_spike_total(sh, my_spikes, &block_count);
-  if (kLif) xsend_headers(sh, step);
+  if (kLif) xsend_headers<kSend>(sh, step);
   if (sh.kstamp) {   // uniform
     __syncthreads();
     if (threadIdx.x == 0) atomicMax(&sh.kstamp[2 * (step % sh.kstamp_steps) + 1], globaltimer_ns());
@@ -305,12 +305,17 @@ int launch_step(const nc_shard_t& sh, const nc_lif_params_t& p, cudaStream_t st)
                  sh.tile_words);
     return NC_E_ARG;
   }
+  // the fused P2P send is a separate instantiation so that the plain step carries none of it
+  const bool send = kLif && sh.xsend_on;
   if (sh.n_tiles <= 1)
-    k_step_fused<false, kLif><<<grid, kThreads, smem, st>>>(sh, p);
+    send ? k_step_fused<false, kLif, false, true><<<grid, kThreads, smem, st>>>(sh, p)
+         : k_step_fused<false, kLif><<<grid, kThreads, smem, st>>>(sh, p);
   else if (sh.flags & 1)
-    k_step_fused<true, kLif, true><<<grid, kThreads, smem, st>>>(sh, p);
+    send ? k_step_fused<true, kLif, true, true><<<grid, kThreads, smem, st>>>(sh, p)
+         : k_step_fused<true, kLif, true><<<grid, kThreads, smem, st>>>(sh, p);
   else
-    k_step_fused<true, kLif, false><<<grid, kThreads, smem, st>>>(sh, p);
+    send ? k_step_fused<true, kLif, false, true><<<grid, kThreads, smem, st>>>(sh, p)
+         : k_step_fused<true, kLif, false><<<grid, kThreads, smem, st>>>(sh, p);
   NC_LAUNCH_CHECK();
   return NC_OK;
 }
@@ -353,6 +358,9 @@ extern "C" int nc_sim_prepare(void) {
   if (int e = opt_in_smem(k_step_fused<true, false>, optin)) return e;
   if (int e = opt_in_smem(k_step_fused<true, true, true>, optin)) return e;
   if (int e = opt_in_smem(k_step_fused<true, false, true>, optin)) return e;
+  if (int e = opt_in_smem(k_step_fused<false, true, false, true>, optin)) return e;
+  if (int e = opt_in_smem(k_step_fused<true, true, true, true>, optin)) return e;
+  if (int e = opt_in_smem(k_step_fused<true, true, false, true>, optin)) return e;
   if (int e = opt_in_smem(k_step_binned, optin)) return e;
   g_prepared = true;
   return NC_OK;
