@@ -41,57 +41,89 @@ def load_peaks() -> dict:
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clock and throttle reasons sampled every few ms DURING the timed region
+    (NVML in a background thread; nvidia-smi polling if NVML is unavailable), so
+    even a 10-ms timed region carries a clock record."""
 
-    QUERY = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap", "hw_power_brake"]
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period_s: float = 0.002):
         self.index = index
-        self.proc = None
-        self.lines: list[str] = []
+        self.period = period_s
+        self.sm: list[float] = []
+        self.max_mhz = None
+        self.reasons: set[str] = set()
+        self.source = None
+        self._stop = threading.Event()
+        self._t = None
+        self._proc = None
+
+    def _handle(self, nv):
+        try:
+            import torch
+            pr = torch.cuda.get_device_properties(self.index)
+            bus = "%08x:%02x:%02x.0" % (pr.pci_domain_id, pr.pci_bus_id, pr.pci_device_id)
+            return nv.nvmlDeviceGetHandleByPciBusId(bus.encode())
+        except Exception:
+            return nv.nvmlDeviceGetHandleByIndex(self.index)
+
+    def _nvml_loop(self, nv, h):
+        bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap,
+                nv.nvmlClocksEventReasonHwPowerBrakeSlowdown]
+        while not self._stop.is_set():
+            try:
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                for name, b in zip(self.NAMES, bits):
+                    if r & b:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(self.period)
+
+    def _smi_loop(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        self._proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "20"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        for line in self._proc.stdout:
+            f = [x.strip() for x in line.split(",")]
+            try:
+                self.sm.append(float(f[0]))
+                self.max_mhz = float(f[1])
+            except (ValueError, IndexError):
+                continue
+            for name, val in zip(self.NAMES, f[2:6]):
+                if val.lower() == "active":
+                    self.reasons.add(name)
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._t = threading.Thread(target=self._read, daemon=True)
-            self._t.start()
-        except (OSError, FileNotFoundError):
-            self.proc = None
+            import pynvml as nv
+            nv.nvmlInit()
+            h = self._handle(nv)
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self.source = "nvml, %.0f ms period" % (self.period * 1e3)
+            self._t = threading.Thread(target=self._nvml_loop, args=(nv, h), daemon=True)
+        except Exception:
+            self.source = "nvidia-smi -lms 20"
+            self._t = threading.Thread(target=self._smi_loop, daemon=True)
+        self._t.start()
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self._stop.set()
+        if self._proc is not None:
+            self._proc.terminate()
+        if self._t is not None:
+            self._t.join(timeout=5)
+        return False
 
     def summary(self) -> dict:
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 7:
-                continue
-            try:
-                sm.append(float(f[1]))
-                mx.append(float(f[2]))
-            except ValueError:
-                continue
-            for name, val in zip(names, f[3:7]):
-                if val.lower() == "active":
-                    reasons.add(name)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.sm), "source": self.source}
 
 
 def total_neurons(args, world: int) -> int:
@@ -127,9 +159,10 @@ def make_sim(net, lif, args, delivery, world, record_raster_steps: int = 0):
     if world > 1:
         from paper_2205_07125_b200 import distributed as D
         cap = args.msg_cap if args.msg_cap is not None else (65536 if args.transport == "nccl" else None)
+        fs = {"auto": None, "on": True, "off": False}[args.fused_send]
         return D.DistSimulator(net, lif, args.seed, None, transport=args.transport, delivery=delivery,
                                msg_cap=cap, latency_steps=args.warmup + args.steps, graph_chunk=args.chunk,
-                               record_raster_steps=record_raster_steps)
+                               record_raster_steps=record_raster_steps, fused_send=fs)
     return S.Simulator(net, lif, args.seed, None, delivery=delivery, graph_chunk=args.chunk)
 
 
@@ -144,24 +177,29 @@ def enable_kernel_stamps(sim, n_steps: int) -> None:
         s.c.kstamp_steps = n_steps
 
 
-def live_kernel_ms(sim, first: int, n: int, world: int, dev) -> float | None:
-    """Mean in-loop duration of the fused step kernel over steps [first, first + n), max over ranks."""
+def live_kernel_ms(sim, first: int, n: int, world: int, dev):
+    """Mean in-loop duration of the fused step kernel over steps [first, first + n):
+    (max over ranks, [per rank]) -- the per-rank spread is the step skew every
+    exchange waits for."""
     import torch
     import torch.distributed as dist
     buf = getattr(sim.states[0], "kstamp_buf", None)
     if buf is None:
-        return None
+        return None, None
     st = buf.view(-1, 2)[first:first + n]
     d = (st[:, 1] - st[:, 0]).to(torch.float64)
     t = (d.mean() / 1e6).reshape(1).to(dev)
+    per = [float(t.item())]
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+        parts = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(parts, t)
+        per = [float(x.item()) for x in parts]
+    return max(per), per
 
 
 def time_steps(sim, args, world, dev, clocks=None):
     """W warm-up steps, then exactly K timed steps between barrier + synchronize;
-    CUDA events on the launching stream, max over ranks.  Returns (ms, spikes, lat, lat_max)."""
+    CUDA events on the launching stream, max over ranks.  Returns (ms, spikes, lat, lat_min)."""
     import torch
     import torch.distributed as dist
 
@@ -175,6 +213,9 @@ def time_steps(sim, args, world, dev, clocks=None):
         if getattr(s, "kstamp_buf", None) is not None:
             s.kstamp_buf.view(-1, 2)[:, 0] = -1     # start: atomicMin from ~0
             s.kstamp_buf.view(-1, 2)[:, 1] = 0      # end: atomicMax from 0
+    # every CUDA graph the warm-up and the timed loop replay is captured here, outside both
+    sim.prepare(args.warmup)
+    sim.prepare(args.steps)
     sim.advance(args.warmup)
     barrier()
     spikes0 = sum(int(s.spike_total.item()) for s in sim.states)
@@ -190,7 +231,7 @@ def time_steps(sim, args, world, dev, clocks=None):
     ms = e0.elapsed_time(e1)
     spikes = sum(int(s.spike_total.item()) for s in sim.states) - spikes0
     sim.check_status()
-    lat = lat_max = None
+    lat = lat_min = None
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -198,15 +239,15 @@ def time_steps(sim, args, world, dev, clocks=None):
         sp = torch.tensor([spikes], device=dev, dtype=torch.int64)
         dist.all_reduce(sp)
         spikes = int(sp.item())
-        lat, lat_max = sim.latencies_us(args.warmup + args.steps)
-        lat, lat_max = lat[args.warmup:], lat_max[args.warmup:]
+        lat, lat_min = sim.latencies_us(args.warmup + args.steps)     # per step: max, min over ranks
+        lat, lat_min = lat[args.warmup:], lat_min[args.warmup:]
         # ids this rank put on each channel, over warm-up + timed steps (hop counters of rank 0's row)
         row = sim.hop_ids.sum(0)[rank_of(sim)].to(torch.float64) / max(args.warmup + args.steps, 1)
         mx, tot = row.max().reshape(1), row.sum().reshape(1)
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         dist.all_reduce(tot)
         lat = (lat, float(mx.item()), float(tot.item()) / world)
-    return ms, spikes, lat, lat_max
+    return ms, spikes, lat, lat_min
 
 
 class _Null:
@@ -254,26 +295,46 @@ def rank_of(sim) -> int:
     return int(getattr(sim, "rank", 0))
 
 
-def lat_summary(lat, lat_max, transport):
+def lat_summary(lat, lat_min, transport):
+    """Exchange latency per SURVEY 8(d): device %globaltimer per rank and step from
+    buckets ready to the last inbound spike in the bitmap; p50/p99 over the timed
+    steps of the per-step MAX over ranks.  The per-step MIN over ranks (the rank whose
+    buckets were ready last: transfer + signalling alone) is reported beside it."""
     if lat is None:
         return None
     lat, max_channel_ids, ids_per_rank = lat
     wire = 8 if transport == "p2p" else 4     # P2P: tagged 8-byte words; NCCL: plain 4-byte ids
     p50 = float(np.percentile(lat, 50))
+    p50_min = float(np.percentile(lat_min, 50))
     bytes_rank = ids_per_rank * wire
     return {"p50": round(p50, 2), "p99": round(float(np.percentile(lat, 99)), 2),
+            "p50_transfer_only": round(p50_min, 2),
+            "p99_transfer_only": round(float(np.percentile(lat_min, 99)), 2),
             "bytes_per_step_per_rank": round(bytes_rank, 1),
             "max_channel_bytes_per_step": round(max_channel_ids * wire, 1),
-            "nvlink_gbs_at_p50": round(bytes_rank / (p50 * 1e-6) / 1e9, 2) if p50 > 0 else None,
+            "nvlink_gbs_at_transfer_p50": round(bytes_rank / (p50_min * 1e-6) / 1e9, 2) if p50_min > 0 else None,
             "nvlink_peak_gbs": 900.0,
-            "p50_incl_skew": round(float(np.percentile(lat_max, 50)), 2),
             "bytes_note": "ids each rank sends per step x bytes per id on the wire; GB/s = that over the p50 "
-                          "exchange time, against 900 GB/s per direction per GPU (latency bound)",
-            "p99_incl_skew": round(float(np.percentile(lat_max, 99)), 2), "transport": transport,
-            "what": "device %globaltimer per step and rank from buckets ready (p2p: the exchange kernel's "
-                    "first block starts after the step kernel) to the last inbound spike ORed into the bitmap; "
-                    "p50/p99 over steps of the min over ranks (the last-ready rank: transfer + signalling), "
-                    "*_incl_skew: max over ranks (adds waiting for slower peers)"}
+                          "transfer-only time, against 900 GB/s per direction per GPU (latency bound)",
+            "transport": transport,
+            "what": "device %globaltimer per step and rank from buckets ready (the exchange kernel's first block, "
+                    "which starts after the step kernel) to the last inbound spike ORed into the bitmap; p50/p99 over "
+                    "timed steps of the per-step max over ranks (SURVEY 8(d); includes waiting for the slowest "
+                    "rank's step kernel); *_transfer_only: of the per-step min over ranks"}
+
+
+def common_config(args, world: int) -> dict:
+    """The `config` both arms print (identical by construction)."""
+    return {"workload": workload_name(args, world), "neurons": total_neurons(args, world),
+            "mean_degree": args.degree, "communities": args.communities,
+            "intra_frac": args.intra_frac if args.communities > 1 else None,
+            "generator_seed": args.seed, "lif": "LifParams() defaults (DESIGN.md section 3)",
+            "partition": "blocks" if world > 1 else None,
+            "exchange": "direct" if world > 1 else "none",
+            "l2": ("inputs larger than L2 (the whole synapse array, ~%.1f GB, is streamed every step)"
+                   % (3.2 * args.degree * total_neurons(args, world) / 1e9 / world)
+                   if 3.2 * args.degree * total_neurons(args, world) / world > 126e6 else
+                   "synapse array fits in L2 (126 MB): no flush between steps")}
 
 
 def run_ours(args) -> dict | None:
@@ -289,15 +350,7 @@ def run_ours(args) -> dict | None:
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     n_neurons = total_neurons(args, world)
-    if args.communities > 1:
-        # regional model (config 5): `intra_frac` of each neuron's ~degree synapses inside its region
-        c = args.communities
-        size = n_neurons / c
-        p_in = args.intra_frac * args.degree / max(size - 1, 1)
-        p_out = (1 - args.intra_frac) * args.degree / max(n_neurons - size, 1)
-        spec = S.GeneratorSpec(n_neurons, c, min(p_in, 1.0), min(p_out, p_in), seed=args.seed)
-    else:
-        spec = S.GeneratorSpec.random(n_neurons, args.degree, seed=args.seed)
+    spec = generator_spec(args, n_neurons)
     lay = S.ShardLayout.blocks(n_neurons, world)
     t_build = time.time()
     net = S.Network.generate(spec, lay, device=dev, shards=[rank], tile_words=args.tile_words,
@@ -311,13 +364,14 @@ def run_ours(args) -> dict | None:
     if args.delivery == "fused":
         enable_kernel_stamps(sim, args.warmup + args.steps)
     clocks = ClockSampler(local)
-    ms, spikes, lat, lat_max = time_steps(sim, args, world, dev, clocks)
+    ms, spikes, lat, lat_min = time_steps(sim, args, world, dev, clocks)
     value = args.steps / (ms * 1e-3)
     main_kernel = {"fused": "fused", "push": "push"}.get(args.delivery, "step")
     # fused: the kernel's mean duration inside the timed loop (device stamps); the same
     # kernel timed alone afterwards (50 back-to-back launches, CUDA events) is reported beside
     # it.  binned / persistent engines: one kernel (or one launch) per step, timed as the step
-    kms_live = live_kernel_ms(sim, args.warmup, args.steps, world, dev) if args.delivery == "fused" else None
+    kms_live, kms_ranks = (live_kernel_ms(sim, args.warmup, args.steps, world, dev) if args.delivery == "fused"
+                           else (None, None))
     kms_alone = kernel_ms(sim, main_kernel) if main_kernel != "step" else ms / args.steps
     kms = kms_live if kms_live is not None else kms_alone
     n_local = lay.n_local(rank)
@@ -328,6 +382,9 @@ def run_ours(args) -> dict | None:
     syn_bytes = int(net.n_synapses) * 16 // 5
     neuron_bytes = n_local * (4 * csr.n_tiles + 8 + 8 + 2 + 4) + csr.slice_ptr.numel() * 8 + 2 * (lay.n_words * 4)
     alg_bytes = syn_bytes + neuron_bytes
+    # SURVEY 8(d)'s pull formula (8 B per synapse: 4 B pre id + 4 B weight, 8 B rowptr and 4 B input
+    # per neuron, the bitmap) for the same step -- what an unpacked CSR would have to move
+    pull_bytes = int(net.n_synapses) * 8 + (n_local + 1) * 8 + n_local * 4 + lay.n_neurons // 8
     peaks = load_peaks()
     if main_kernel != "fused":
         fired_syn = spikes / max(args.steps, 1) * args.degree / max(world, 1)
@@ -343,6 +400,7 @@ def run_ours(args) -> dict | None:
     prof = ROOT / "profiles" / "ncu_step_fused.json"
     if prof.is_file() and main_kernel == "fused" and world == 1:
         traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+    fused_send = getattr(sim, "fused_send", None)
     e2e = e2e_measure(sim, net, args, world, rank, lif)
     launches = max(1, int(round(args.steps * sim.launches_per_step())))
     if world > 1:
@@ -353,12 +411,12 @@ def run_ours(args) -> dict | None:
     event = None
     if args.with_push and args.delivery == "fused":
         psim = make_sim(net, lif, args, args.event, world)
-        pms, pspikes, plat, plat_max = time_steps(psim, args, world, dev)
+        pms, pspikes, plat, plat_min = time_steps(psim, args, world, dev)
         fired_syn = pspikes / max(args.steps, 1) * args.degree / max(world, 1)
         event = {"engine": args.event, "value": round(args.steps / (pms * 1e-3), 2),
                  "ms_per_step": round(pms / args.steps, 5),
                  "delivered_synapses_per_step": round(fired_syn, 1),
-                 "exchange_us": lat_summary(plat, plat_max, args.transport),
+                 "exchange_us": lat_summary(plat, plat_min, args.transport),
                  "gpu_launches": max(1, int(round(args.steps * psim.launches_per_step())))}
         if args.event in ("push", "persistent"):
             push_ms = kernel_ms(psim, "push")
@@ -372,35 +430,47 @@ def run_ours(args) -> dict | None:
         del psim
 
     result = None
+    parity = None
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu, parity = cpu_baseline_and_parity(net, lay, lif, args, spec)
     if rank == 0:
-        cpu = cpu_baseline(net, lay, lif, args) if (world == 1 and not args.no_cpu) else None
         result = {
             "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 5), "higher_is_better": True,
             "scaling": args.scaling, "vs_baseline": None, "dtype": "fp32 state / int32 synaptic sums",
             "data": "synthetic (device SBM generator, generate_synthetic distributions)",
-            "config": {
-                "workload": workload_name(args, world),
-                "neurons": n_neurons, "mean_degree": args.degree, "synapses": int(net.n_synapses) * world,
-                "delivery": args.delivery, "exchange": "none" if world == 1 else "direct",
+            "config": common_config(args, world),
+            "details": {
+                "synapses": int(net.n_synapses) * world, "delivery": args.delivery,
                 "firing_rate_hz": round(spikes / n_neurons / (args.steps * 1e-3), 3),
-                "l2": "inputs larger than L2 (synapse array %.2f GB streamed every step)" % (csr.n_entries * 4 / 1e9),
+                "synapse_array_gb": round(csr.n_entries * 4 / 1e9, 3),
                 "sell_padding": round(csr.n_entries * 4 / max(csr.n_real * 3.2, 1) - 1.0, 4),
-                "bitmap_tiles": csr.n_tiles,
-                "graph_build_s": round(t_build, 2),
+                "bitmap_tiles": csr.n_tiles, "graph_build_s": round(t_build, 2),
+                "fused_send": fused_send,
             },
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": traffic,
-                         "kernel": {"fused": "k_step_fused", "push": "k_deliver_push", "binned": "k_step_binned (whole step)"}.get(args.delivery, "k_persistent (whole step)"),
+                         "kernel": {"fused": "k_step_fused", "push": "k_deliver_push",
+                                    "binned": "k_step_binned (whole step)"}.get(args.delivery,
+                                                                                 "k_persistent (whole step)"),
                          "kernel_ms": round(kms, 5), "algorithmic_bytes": int(alg_bytes),
+                         "bytes_formula": "packed J-SELL: 3.2 B/synapse + 26 B/neuron + bitmaps (DESIGN.md section 5)",
+                         "pull_formula_bytes": int(pull_bytes),
+                         "pull_formula_note": "SURVEY 8(d) pull formula (8 B/synapse unpacked CSR) for the same step; "
+                                              "its GB/s over kernel_ms would read %.2fx the copy peak -- the packing, "
+                                              "not skipped work (ncu DRAM bytes = traffic)"
+                                              % (pull_bytes / (kms * 1e-3) / 1e9 / peaks["hbm_gbs"]),
                          "kernel_ms_source": ("device %globaltimer stamps of every timed step's kernel "
                                               "(first CTA start to last CTA end), mean, max over ranks")
                          if kms_live is not None else "CUDA events, the kernel launched alone",
+                         "kernel_ms_per_rank": [round(x, 5) for x in kms_ranks] if kms_ranks else None,
                          "kernel_ms_alone": round(kms_alone, 5),
                          "peak_source": peaks["source"], "spec_peak_gbs": 8000.0,
                          "frac_of_spec": round(achieved / 8000.0, 4)},
+            "parity": parity,
             "event_driven": event,
-            "exchange_us": lat_summary(lat, lat_max, args.transport),
+            "exchange_us": lat_summary(lat, lat_min, args.transport),
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
@@ -412,37 +482,65 @@ def run_ours(args) -> dict | None:
     return result
 
 
-def gid_csr(net, lay, rank=0):
-    """Gid-space CSR of a single-shard network for the CPU oracle (decoded on the GPU)."""
-    import torch
-    from paper_2205_07125_b200 import sell
-    lay = net.layout
-    row, pre, q, _ = sell.decode(net.shards[rank])
-    dev = row.device
-    gid_of_internal = torch.full((lay.n_words * 32,), -1, dtype=torch.int64, device=dev)
-    for h, m in enumerate(lay.members):
-        gid_of_internal[int(lay.base[h]): int(lay.base[h]) + m.size] = torch.from_numpy(m).to(dev)
-    post = torch.from_numpy(lay.members[rank]).to(dev)[row]
-    pre = gid_of_internal[pre]
-    order = torch.argsort(post, stable=True)
-    post, pre, q = post[order], pre[order], q[order]
-    n = lay.n_neurons
-    rowptr = torch.zeros(n + 1, dtype=torch.int64, device=dev)
-    rowptr[1:] = torch.cumsum(torch.bincount(post, minlength=n), 0)
-    out = rowptr.cpu().numpy(), pre.to(torch.int32).cpu().numpy(), q.to(torch.uint8).cpu().numpy()
-    del row, pre, q, order, post, gid_of_internal
-    torch.cuda.empty_cache()
-    return out
+def generator_spec(args, n_neurons: int):
+    from paper_2205_07125_b200 import sim as S
+    if args.communities > 1:
+        # regional model (config 5): `intra_frac` of each neuron's ~degree synapses inside its region
+        c = args.communities
+        size = n_neurons / c
+        p_in = args.intra_frac * args.degree / max(size - 1, 1)
+        p_out = (1 - args.intra_frac) * args.degree / max(n_neurons - size, 1)
+        return S.GeneratorSpec(n_neurons, c, min(p_in, 1.0), min(p_out, p_in), seed=args.seed)
+    return S.GeneratorSpec.random(n_neurons, args.degree, seed=args.seed)
 
 
-def cpu_baseline(net, lay, lif, args) -> dict:
-    """The CPU oracle (C, OpenMP on every host core) on a bounded sample of the same workload."""
+def oracle_csr(spec, threads: int):
+    """The oracle's own CPU restatement of the device generator (oracle/sim_oracle.c):
+    the symmetric gid-space CSR of the same network, built without the GPU."""
     from oracle import c_oracle
-    rowptr, col, q = gid_csr(net, lay)
+    return c_oracle.generate_sbm_csr(spec.n_neurons, spec.n_communities, spec.p_in, spec.p_out, spec.seed,
+                                     intra=spec.intra_p_range, inter=spec.inter_p_range, threads=threads)
+
+
+def cpu_baseline_and_parity(net, lay, lif, args, spec):
+    """(cpu_baseline, parity) on the benchmarked network, rank 0, N = 1.
+
+    The oracle builds the network itself (its CPU generator), then
+    * parity: runs `parity_steps` full steps with the raster on and compares every
+      step's raster, the per-step spike counts and the final V / I bit for bit with
+      a fresh GPU run of the same steps on the benchmarked device layout;
+    * cpu_baseline: times `cpu_steps` more full steps (OpenMP, every host core).
+    """
+    import hashlib
+    from oracle import c_oracle
+    from paper_2205_07125_b200 import sim as S
     threads = os.cpu_count() or 1
+    t = time.time()
+    rowptr, col, q = oracle_csr(spec, threads)
+    t_gen = time.time() - t
     owner = np.zeros(lay.n_neurons, dtype=np.int32)
+    k = args.parity_steps
+    parity = None
+    if k > 0:
+        gsim = S.Simulator(net, lif, args.seed, None, delivery="fused", record_raster_steps=k, graph_chunk=args.chunk)
+        rep = gsim.run(k)
+        del gsim
+        ref = c_oracle.simulate_csr(rowptr, col, q, owner, 1, [[-1]], lif.constants(args.seed), k, threads=threads,
+                                    raster=True, counts=False)
+        same_graph = int(rowptr[-1]) == int(net.n_synapses)
+        sha = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:16]  # noqa: E731
+        parity = {"steps": k, "network": "the benchmarked one: device-generated J-SELL layout (%d tiles, bank "
+                                         "order %s) vs the oracle's own CPU generator" % (
+                                             net.shards[0].n_tiles, "on" if args.bank_order else "off"),
+                  "synapses_equal": same_graph,
+                  "raster_equal": bool(np.array_equal(rep.raster, ref["raster"])),
+                  "spikes_per_step_equal": bool(np.array_equal(rep.raster.sum(1), ref["raster"].sum(1))),
+                  "v_equal": bool(np.array_equal(rep.v.view(np.uint32), ref["v"].view(np.uint32))),
+                  "i_equal": bool(np.array_equal(rep.i_syn.view(np.uint32), ref["i"].view(np.uint32))),
+                  "spikes": int(rep.raster.sum()), "raster_sha256_16": sha(ref["raster"]),
+                  "v_sha256_16": sha(ref["v"])}
     steps = args.cpu_steps
-    run = lambda k: c_oracle.simulate_csr(rowptr, col, q, owner, 1, [[-1]], lif.constants(args.seed), k,  # noqa
+    run = lambda n: c_oracle.simulate_csr(rowptr, col, q, owner, 1, [[-1]], lif.constants(args.seed), n,  # noqa
                                           threads=threads, raster=False, counts=False)
     t = time.time()
     run(0)                                   # setup only (initial state, destination sets)
@@ -450,9 +548,11 @@ def cpu_baseline(net, lay, lif, args) -> dict:
     t = time.time()
     run(steps)
     dt = max(time.time() - t - setup, 1e-9)
-    return {"value": round(steps / dt, 4), "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{steps} full steps of the same {lay.n_neurons}-neuron network (oracle/sim_oracle.c, "
-                      f"OpenMP {threads} threads), {dt:.1f} s excluding {setup:.1f} s setup"}
+    cpu = {"value": round(steps / dt, 4), "unit": UNIT, "cores": threads, "kind": "port",
+           "sample": f"{steps} full steps of the same {lay.n_neurons}-neuron network (oracle/sim_oracle.c, "
+                     f"OpenMP {threads} threads), {dt:.1f} s excluding {setup:.1f} s setup and the "
+                     f"{t_gen:.1f} s CPU network build"}
+    return cpu, parity
 
 
 def e2e_measure(sim, net, args, world: int, rank: int, lif) -> dict | None:
@@ -482,8 +582,8 @@ def e2e_measure(sim, net, args, world: int, rank: int, lif) -> dict | None:
         hosts.append(h)
     raster_host = torch.empty((steps, words), dtype=torch.int32, pin_memory=True)
     esim.reset(1)
-    esim.advance(min(args.chunk, steps))          # warm: graph capture outside the timed region
-    esim.reset(1)                                 # state re-initialised; the captured graph is kept
+    for k in set(min(args.chunk, steps - d) for d in range(0, steps, args.chunk)):
+        esim.prepare(k)                           # graph capture outside the timed region
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -527,9 +627,10 @@ def e2e_measure(sim, net, args, world: int, rank: int, lif) -> dict | None:
 def run_reference(args) -> dict | None:
     """CPU oracle port of the same workload on every host core (rank 0 only).
 
-    Each timed step is one full step of the whole network (all N shards' neurons,
-    same generator and parameters); the number of timed steps is capped so the
-    run stays within about a minute (the sample is stated in the output).
+    The oracle builds the same network with its CPU generator (oracle/sim_oracle.c,
+    the restatement of csrc/graphgen.cu), runs W warm-up steps and then times K
+    full steps of the whole network, K capped so the run stays within about a
+    minute (the sample is stated in the output).
     """
     rank, world, _ = dist_env()
     if rank != 0:
@@ -539,10 +640,19 @@ def run_reference(args) -> dict | None:
     # bounded sample: at most ~2.5e9 synapses in host memory (the CPU cost of a step is
     # linear in the synapse count, so an n-neuron slice is timed and scaled by n / total)
     total = total_neurons(args, world)
-    n = total if total * args.degree <= 2.5e9 else max(1, int(2.5e9 // args.degree))
     threads = os.cpu_count() or 1
+    spec = generator_spec(args, total)
+    sliced = total * args.degree > 2.5e9
+    if sliced:
+        n = max(1, int(2.5e9 // args.degree))
+        spec.n_neurons = n
+        if args.communities > 1:
+            spec.n_communities = max(1, args.communities * n // total)
+        else:
+            spec.p_in = args.degree / max(n - 1, 1)
+    n = spec.n_neurons
     t = time.time()
-    rowptr, col, q = c_oracle.generate_random_csr(n, args.degree, args.seed, threads=threads)
+    rowptr, col, q = oracle_csr(spec, threads)
     t_build = time.time() - t
     owner = np.zeros(n, dtype=np.int32)
     lif = LifParams().constants(args.seed)
@@ -551,30 +661,28 @@ def run_reference(args) -> dict | None:
     t = time.time()
     run(0)                                   # setup only (initial state, destination sets)
     setup = time.time() - t
-    warm = max(1, min(args.warmup, 3))
+    warm = args.warmup
     t = time.time()
     run(warm)
-    one = max(time.time() - t - setup, 1e-6) / warm
+    one = max(time.time() - t - setup, 1e-6) / max(warm, 1)
     steps = int(max(3, min(args.steps, 60.0 // one)))
     t = time.time()
-    run(steps)
-    dt = max(time.time() - t - setup, 1e-9)
+    run(warm + steps)                        # the oracle restarts from step 0: warm-up steps, then the timed ones
+    dt = max(time.time() - t - setup - one * warm, 1e-9)
     v = steps / dt * n / total
-    wl = workload_name(args, world)
     return {
         "metric": METRIC, "value": round(v, 4), "unit": UNIT, "n_gpus": world, "steps": steps,
         "warmup": warm, "ms_per_step": round(1e3 / v, 3), "higher_is_better": True,
         "scaling": args.scaling, "vs_baseline": None, "dtype": "fp32 state / int32 synaptic sums",
-        "data": "synthetic (oracle CPU generator, same distributions)", "impl": "reference",
-        "config": {"workload": wl + " (CPU oracle port, all host threads)", "neurons": total,
-                   "mean_degree": args.degree, "synapses_simulated": int(rowptr[-1]),
-                   "graph_build_s": round(t_build, 2)},
+        "data": "synthetic (oracle CPU generator: the same network as the device generator)", "impl": "reference",
+        "config": common_config(args, world),
+        "details": {"synapses_simulated": int(rowptr[-1]), "graph_build_s": round(t_build, 2),
+                    "engine": "oracle/sim_oracle.c (CPU port of the loop semantics; the reference has no loop)"},
         "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{steps} full steps of a {n}-neuron network"
-                                   + (f" (a {n}/{total} slice; steps/s scaled by that fraction)" if n < total else "")
-                                   + f" (oracle/sim_oracle.c, OpenMP "
-                                   f"{threads} threads; requested --steps {args.steps}, capped at ~60 s; "
-                                   f"{setup:.1f} s one-time setup excluded)"},
+                         "sample": f"{steps} full steps after {warm} warm-up steps of a {n}-neuron network"
+                                   + (f" (a {n}/{total} slice; steps/s scaled by that fraction)" if sliced else "")
+                                   + f" (oracle/sim_oracle.c, OpenMP {threads} threads; requested --steps "
+                                   f"{args.steps}, capped at ~60 s; {setup:.1f} s one-time setup excluded)"},
         "e2e": {"value": round(v, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -604,6 +712,10 @@ def main() -> int:
                     help="skip the shared-memory bank placement of the synapse entries (tuning)")
     ap.add_argument("--chunk", type=int, default=100)
     ap.add_argument("--cpu-steps", type=int, default=200, help="CPU-baseline sample (~10 s of OpenMP oracle work at config 2)")
+    ap.add_argument("--parity-steps", type=int, default=20,
+                    help="steps of the benchmarked network checked bit for bit against the oracle (N=1; 0 = off)")
+    ap.add_argument("--fused-send", default="auto", choices=["auto", "on", "off"],
+                    help="N>1, P2P: the step kernel stores its spikes into the peers' inboxes (auto: large shards)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-push", dest="with_push", action="store_false",
                     help="skip the event-driven (push) measurement reported beside the headline")

@@ -349,6 +349,9 @@ typedef struct nc_xchg {
 /* Inbox words needed per rank for the P2P transport. */
 #define NC_P2P_INBOX_WORDS(n, cap) ((size_t)8 * (size_t)(n) * ((size_t)(cap) + 1))
 
+/* Before a run: zero this rank's P2P inbox (tags restart with the step
+ * counter), flags, barrier and relay counts.  Every rank must finish its reset
+ * before any rank sends (synchronize + barrier). */
 int nc_xchg_reset(const nc_xchg_t* X, void* stream);
 /* NCCL path: seal (headers + hop counters), grouped send/recv, scatter. */
 int nc_xchg_seal(const nc_xchg_t* X, int32_t phase, void* stream);

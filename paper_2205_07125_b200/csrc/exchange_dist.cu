@@ -104,6 +104,12 @@ __global__ void k_reset(const nc_xchg_t X) {
 
 extern "C" int nc_xchg_reset(const nc_xchg_t* X, void* stream) {
   if (int e = check_x(X)) return e;
+  // P2P inboxes: tags are step + 1 and the step counter restarts at 0, so words left
+  // by a previous run would carry the tags of this run's messages -- clear them
+  // (callers order this before any peer's first send: synchronize + barrier)
+  if (X->my_inbox)
+    NC_CUDA_TRY(cudaMemsetAsync(X->my_inbox, 0, NC_P2P_INBOX_WORDS(X->n, X->cap) * sizeof(uint32_t),
+                                (cudaStream_t)stream));
   k_reset<<<1, 64, 0, (cudaStream_t)stream>>>(*X);
   NC_LAUNCH_CHECK();
   return NC_OK;

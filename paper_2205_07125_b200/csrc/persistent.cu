@@ -104,6 +104,10 @@ extern "C" int nc_run_persistent(const nc_shard_t* sh, const nc_lif_params_t* p,
     nc_set_error("nc_run_persistent: shard needs push CSR, acc, step and status buffers");
     return NC_E_ARG;
   }
+  if (X && X->fused_send) {   // this engine sends from its exchange blocks; nothing would write the inboxes
+    nc_set_error("nc_run_persistent: nc_xchg_t.fused_send must be 0 (the persistent engine does its own send)");
+    return NC_E_ARG;
+  }
   if (n_steps == 0) return NC_OK;
   const int B = blocks_per_peer > 0 ? blocks_per_peer : 1;
   int dev = 0, sms = 0, occ = 0;
@@ -117,10 +121,6 @@ extern "C" int nc_run_persistent(const nc_shard_t* sh, const nc_lif_params_t* p,
   // every resident slot: the push and LIF phases are latency bound and want
   // as many warps in flight as the SM holds
   int per_sm = occ < 8 ? occ : 8;
-  if (const char* e = getenv("NC_PERSIST_BLOCKS_PER_SM")) {   // tuning knob
-    const int v = atoi(e);
-    if (v >= 1 && v < per_sm) per_sm = v;
-  }
   int grid = sms * per_sm;
   const int nex = X ? X->n * B : 0;
   if (grid < nex) {

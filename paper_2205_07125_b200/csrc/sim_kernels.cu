@@ -330,6 +330,22 @@ int check_shard(const nc_shard_t* sh) {
     nc_set_error("invalid nc_shard_t");
     return NC_E_ARG;
   }
+  if (sh->xsend_on) {
+    // fused P2P send: every message slot holds xsend_cap + 1 words, so a bucket
+    // longer than that would run into the next source's slot (or past the peer's
+    // IPC allocation); headers use work[2..3]
+    if (!sh->work || sh->xsend_cap < sh->bucket_cap || sh->n_shards > kThreads) {
+      nc_set_error("invalid nc_shard_t: fused send needs work counters, xsend_cap >= bucket_cap "
+                   "(%lld < %lld) and n_shards <= %d", (long long)sh->xsend_cap, (long long)sh->bucket_cap,
+                   kThreads);
+      return NC_E_ARG;
+    }
+    for (int h = 0; h < sh->n_shards; ++h)
+      if (h != sh->shard && !sh->xsend[h]) {   // every peer gets a header (heartbeat)
+        nc_set_error("invalid nc_shard_t: fused send has no inbox for peer %d", h);
+        return NC_E_ARG;
+      }
+  }
   return NC_OK;
 }
 

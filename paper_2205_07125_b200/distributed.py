@@ -20,8 +20,6 @@ through it.
 
 from __future__ import annotations
 
-import os
-
 import ctypes as C
 
 import numpy as np
@@ -30,7 +28,40 @@ from . import _native
 from .routing import RoutingTable
 from .sim import ExchangePlan, LifParams, Network, SimReport, _ShardState, _as_u16
 
-__all__ = ["channel_masks", "gather_dest", "DistSimulator"]
+__all__ = ["channel_masks", "gather_dest", "DistSimulator", "TorchGroup"]
+
+
+class TorchGroup:
+    """The collectives the exchange needs for bootstrap and result gathering, over
+    torch.distributed (one process per GPU).  Nothing on the step path uses them.
+
+    ``same_process`` False: peers' P2P windows are opened with CUDA IPC handles.
+    A group whose ranks share one process (and device) sets it True, and the raw
+    device pointers are exchanged instead (tests/virtual_ranks.py)."""
+
+    same_process = False
+
+    def __init__(self):
+        import torch.distributed as dist
+        self._d = dist
+        self.rank = dist.get_rank()
+        self.world = dist.get_world_size()
+
+    def all_reduce(self, t, op: str = "sum"):
+        d = self._d
+        d.all_reduce(t, op={"sum": d.ReduceOp.SUM, "max": d.ReduceOp.MAX, "min": d.ReduceOp.MIN}[op])
+
+    def all_gather(self, parts, t):
+        self._d.all_gather(parts, t)
+
+    def all_gather_object(self, out, obj):
+        self._d.all_gather_object(out, obj)
+
+    def broadcast_object_list(self, objs, src: int = 0):
+        self._d.broadcast_object_list(objs, src=src)
+
+    def barrier(self):
+        self._d.barrier()
 
 
 def channel_masks(plan: ExchangePlan) -> list[dict]:
@@ -55,10 +86,10 @@ def channel_masks(plan: ExchangePlan) -> list[dict]:
     return [{"send1": send1[r], "recv1": recv1[r], "send2": send2[r], "recv2": recv2[r]} for r in range(n)]
 
 
-def gather_dest(net: Network, rank: int, world: int, device):
+def gather_dest(net: Network, rank: int, world: int, device, group=None):
     """Destination mask of every internal id on every rank (all_gather of the shard masks)."""
     import torch
-    import torch.distributed as dist
+    grp = group if group is not None else TorchGroup()
     lay = net.layout
     width = max(lay.n_local(h) for h in range(lay.n_shards))
     mine = torch.zeros(max(width, 1), dtype=torch.int32, device=device)
@@ -66,7 +97,7 @@ def gather_dest(net: Network, rank: int, world: int, device):
     if n_local:
         mine[:n_local] = net.shards[rank].dest
     parts = [torch.zeros_like(mine) for _ in range(world)]
-    dist.all_gather(parts, mine)
+    grp.all_gather(parts, mine)
     g = torch.zeros(lay.n_words * 32, dtype=torch.int32, device=device)
     for h in range(world):
         b = int(lay.base[h])
@@ -84,17 +115,21 @@ class DistSimulator:
                  *, transport: str = "p2p", delivery: str = "fused", msg_cap: int | None = None,
                  record_raster_steps: int = 0, per_step_counts: bool = False, latency_steps: int = 4096,
                  use_graph: bool = True, graph_chunk: int = 64, timeout_s: float = 10.0,
-                 blocks_per_peer: int | None = None):
+                 blocks_per_peer: int | None = None, fused_send: bool | None = None, group=None,
+                 debug_stamps: bool = False):
+        """``fused_send``: the fused step kernel stores phase-1 spikes straight into the
+        peers' inboxes (P2P transport); None = on for shards of >= FUSED_SEND_MIN_ROWS
+        rows.  ``group``: collectives for bootstrap (default: torch.distributed)."""
         import torch
-        import torch.distributed as dist
         if transport not in ("p2p", "nccl"):
             raise ValueError(f"transport must be 'p2p' or 'nccl', got {transport!r}")
         if delivery not in ("fused", "push", "pull", "persistent", "binned"):
             raise ValueError(f"delivery must be 'fused', 'pull', 'push', 'binned' or 'persistent', got {delivery!r}")
         if delivery == "persistent" and transport != "p2p":
             raise ValueError("the persistent engine exchanges spikes with device-initiated P2P stores (transport='p2p')")
-        self.rank = dist.get_rank()
-        self.world = dist.get_world_size()
+        self.g = group if group is not None else TorchGroup()
+        self.rank = self.g.rank
+        self.world = self.g.world
         lay = net.layout
         if lay.n_shards != self.world:
             raise ValueError(f"partition has {lay.n_shards} GPUs but {self.world} ranks are running")
@@ -125,7 +160,7 @@ class DistSimulator:
         # global message capacity: the exact per-rank bucket bound, maxed over ranks
         probe = _ShardState(net, self.rank, self.plan, record_steps=0, push=False, bucket_cap=None)
         cap_t = torch.tensor([probe.exact_cap], dtype=torch.int64, device=dev)
-        dist.all_reduce(cap_t, op=dist.ReduceOp.MAX)
+        self.g.all_reduce(cap_t, "max")
         cap = int(cap_t.item())
         if msg_cap is not None:
             cap = min(cap, int(msg_cap))
@@ -137,7 +172,7 @@ class DistSimulator:
                                  bucket_stride=self.cap)
         self.states = [self.state]
         self.record_steps = int(record_raster_steps)
-        self.dest_global = gather_dest(net, self.rank, self.world, dev)
+        self.dest_global = gather_dest(net, self.rank, self.world, dev, self.g)
 
         i32 = dict(dtype=torch.int32, device=dev)
         n, cap = self.n, self.cap
@@ -179,7 +214,7 @@ class DistSimulator:
             X.spk_ids, X.spk_count, X.spk_cap = (self.state.spk_ids.data_ptr(), self.state.spk_count.data_ptr(),
                                                  self.state.spk_cap)
         self.dbg = None
-        if os.environ.get("NC_XCHG_DBG"):   # diagnostics (tools/xchg_stamps.py)
+        if debug_stamps:   # per-block phase stamps of the first 64 steps (tools/xchg_stamps.py)
             self.dbg = torch.zeros((64, n * self.blocks_per_peer, 4), dtype=torch.int64, device=dev)
             X.dbg = self.dbg.data_ptr()
         self.X = X
@@ -196,29 +231,29 @@ class DistSimulator:
         # Only for shards big enough that the step kernel outlasts the transfer: on config 1
         # (2 500 rows per GPU, a ~5 us step kernel) the last-CTA header pass cost more than
         # the overlap gained (63.6 k vs 66.9 k steps/s, profiles/r01_cfg1_4gpu_fused_send.jsonl).
-        # NC_FUSED_SEND=0 / 1 forces it off / on.
-        env = os.environ.get("NC_FUSED_SEND")
+        # fused_send=True / False forces it on / off.
         big = lay.n_local(self.rank) >= FUSED_SEND_MIN_ROWS
         self.fused_send = (transport == "p2p" and delivery == "fused" and int(self.state.bucket_cap) <= cap
-                           and (env == "1" or (env is None and big)))
+                           and (bool(fused_send) if fused_send is not None else big))
         if self.fused_send:
             c = self.state.c
             for h in range(n):
                 c.xsend[h] = X.peer_inbox[h] if h != self.rank else None
             c.xsend_cap, c.xsend_on, c.xsend_mask = cap, 1, self.masks["send1"]
             X.fused_send = 1
-        self._graph = None
-        self._graph_len = 0
+        from .sim import StepGraphs
+        self._graphs = StepGraphs(dev, self._one_step, graph_chunk)
         _native.check(self.lib.nc_sim_prepare(), "prepare")
 
     # ------------------------------------------------------------ bootstrap
     def _setup_nccl(self):
-        import torch.distributed as dist
+        if self.g.same_process:
+            raise ValueError("the NCCL transport needs one process per GPU")
         uid = C.create_string_buffer(128)
         if self.rank == 0:
             _native.check(self.lib.nc_nccl_get_unique_id(uid), "nccl unique id")
         obj = [bytes(uid.raw) if self.rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
+        self.g.broadcast_object_list(obj, src=0)
         buf = C.create_string_buffer(obj[0], 128)
         comm = C.c_void_p()
         _native.check(self.lib.nc_nccl_comm_init(C.byref(comm), self.world, buf, self.rank), "nccl comm init")
@@ -233,7 +268,6 @@ class DistSimulator:
         self.hdr.zero_()
 
     def _setup_p2p(self):
-        import torch.distributed as dist
         n, cap = self.n, self.cap
         inbox_words = 4 * n * (cap + 1) * 2    # (phase, parity, src) slots of (cap + 1) tagged 8-byte words
         flag_words = 2 * _native.MAX_SHARDS + 16 + 2 * _native.MAX_SHARDS  # flags, done/barrier/lat, send_done
@@ -247,7 +281,8 @@ class DistSimulator:
             handles.append(bytes(h.raw))
             ptrs.append(p.value)
         allh = [None] * self.world
-        dist.all_gather_object(allh, handles)
+        # one process per GPU: IPC handles; ranks sharing a process: the pointers themselves
+        self.g.all_gather_object(allh, ptrs if self.g.same_process else handles)
         X = self.X
         X.my_inbox, X.my_flags = ptrs[0], ptrs[1]
         base = ptrs[1]
@@ -259,6 +294,9 @@ class DistSimulator:
         for peer in range(self.world):
             if peer == self.rank:
                 X.peer_inbox[peer], X.peer_flags[peer] = ptrs[0], ptrs[1]
+                continue
+            if self.g.same_process:
+                X.peer_inbox[peer], X.peer_flags[peer] = allh[peer]
                 continue
             opened = []
             for k in range(2):
@@ -272,16 +310,15 @@ class DistSimulator:
     def close(self):
         """Release the communicator and IPC windows (collective: call on every rank)."""
         import torch
-        import torch.distributed as dist
         torch.cuda.synchronize(self.dev)
         # captured graphs reference the communicator and the IPC windows
-        self._graph = None
+        self._graphs.clear()
         torch.cuda.synchronize(self.dev)
-        dist.barrier()
+        self.g.barrier()
         for p in self._ipc_peer:
             self.lib.nc_ipc_close(C.c_void_p(p))
         self._ipc_peer = []
-        dist.barrier()
+        self.g.barrier()
         for p in self._ipc_own:
             self.lib.nc_free(C.c_void_p(p))
         self._ipc_own = []
@@ -292,7 +329,6 @@ class DistSimulator:
     # ------------------------------------------------------------ stepping
     def reset(self, counter_steps: int):
         import torch
-        import torch.distributed as dist
         st = _native.stream_handle(self.dev)
         s = self.state
         _native.check(self.lib.nc_sim_init(C.byref(s.c), C.byref(self.c_lif), st), "sim init")
@@ -305,12 +341,12 @@ class DistSimulator:
             self.hop_ids = torch.zeros((rows, self.n, self.n), dtype=torch.int64, device=self.dev)
             self.deliv_ids = torch.zeros((rows, self.n, self.n), dtype=torch.int64, device=self.dev)
             self.X.hop_ids, self.X.deliv_ids = self.hop_ids.data_ptr(), self.deliv_ids.data_ptr()
-            self._graph = None
+            self._graphs.clear()
         self.lat_stamps.zero_()
         self.lat_ns.zero_()
         _native.check(self.lib.nc_xchg_reset(C.byref(self.X), st), "xchg reset")
         torch.cuda.synchronize(self.dev)
-        dist.barrier()
+        self.g.barrier()     # every inbox cleared before any rank's first send
 
     def _exchange(self, st):
         L, X = self.lib, C.byref(self.X)
@@ -326,6 +362,12 @@ class DistSimulator:
             _native.check(L.nc_xchg_scatter(X, 2, st), "scatter 2")
 
     def _one_step(self, st):
+        self.step_kernels(st)
+        self.exchange_kernels(st)
+        self.end_kernels(st)
+
+    def step_kernels(self, st):
+        """Delivery + LIF + bucketing of this rank's shard (and the fused send)."""
         L = self.lib
         s = self.state
         lif = C.byref(self.c_lif)
@@ -339,6 +381,10 @@ class DistSimulator:
             else:
                 _native.check(L.nc_sim_deliver_pull(C.byref(s.c), self.c_lif.g_inh, st), "pull")
             _native.check(L.nc_sim_lif_update(C.byref(s.c), lif, st), "lif")
+
+    def exchange_kernels(self, st):
+        L = self.lib
+        s = self.state
         if self.transport == "p2p":
             self._exchange(st)          # stamps its own start (buckets ready) and end
         else:
@@ -347,7 +393,9 @@ class DistSimulator:
             self._exchange(st)
             _native.check(L.nc_stamp(self.lat_stamps[1].data_ptr(), s.step.data_ptr(), self.latency_steps, st),
                           "stamp")
-        _native.check(L.nc_sim_end_step(C.byref(s.c), st), "end step")
+
+    def end_kernels(self, st):
+        _native.check(self.lib.nc_sim_end_step(C.byref(self.state.c), st), "end step")
 
     def launches_per_step(self) -> float:
         if self.delivery == "persistent":
@@ -364,7 +412,6 @@ class DistSimulator:
             self._one_step(st)
 
     def advance(self, steps: int):
-        import torch
         if self.delivery == "persistent":
             s = self.state
             st = _native.stream_handle(self.dev)
@@ -376,23 +423,12 @@ class DistSimulator:
         if not self.use_graph:
             self.advance_eager(steps)
             return
-        done = 0
-        while done < steps:
-            k = min(self.graph_chunk, steps - done)
-            if self._graph is None or self._graph_len != k:
-                g = torch.cuda.CUDAGraph()
-                side = torch.cuda.Stream(self.dev)
-                side.wait_stream(torch.cuda.current_stream(self.dev))
-                with torch.cuda.stream(side):
-                    g.capture_begin()
-                    cst = _native.stream_handle(self.dev)
-                    for _ in range(k):
-                        self._one_step(cst)
-                    g.capture_end()
-                torch.cuda.current_stream(self.dev).wait_stream(side)
-                self._graph, self._graph_len = g, k
-            self._graph.replay()
-            done += k
+        self._graphs.run(steps)
+
+    def prepare(self, steps: int):
+        """Capture every CUDA graph a following advance(steps) replays (no work is run)."""
+        if self.use_graph and self.delivery != "persistent":
+            self._graphs.prepare(steps)
 
     def check_status(self):
         flags = self.state.status.cpu().tolist()
@@ -403,29 +439,28 @@ class DistSimulator:
 
     def latencies_us(self, steps: int) -> tuple[np.ndarray, np.ndarray]:
         """Per-step exchange time (us) from this rank's buckets-ready stamp to its last inbound
-        spike: (min over ranks, max over ranks).  The minimum is the rank that became
-        ready last, i.e. the pure transfer + signalling latency; the maximum adds the
-        wait for slower peers (step-time skew)."""
+        spike: (max over ranks, min over ranks).  The maximum is SURVEY 8(d)'s exchange
+        latency (it includes waiting for the slowest peer's buckets); the minimum is the
+        rank that became ready last, i.e. transfer + signalling alone."""
         import torch
-        import torch.distributed as dist
         k = min(steps, self.latency_steps)
         if self.transport == "p2p" and self.delivery != "persistent":
             d = self.lat_ns[:k].to(torch.float64)
         else:
             d = (self.lat_stamps[1, :k] - self.lat_stamps[0, :k]).to(torch.float64)
         lo, hi = d.clone(), d.clone()
-        dist.all_reduce(lo, op=dist.ReduceOp.MIN)
-        dist.all_reduce(hi, op=dist.ReduceOp.MAX)
-        return lo.cpu().numpy() / 1e3, hi.cpu().numpy() / 1e3
+        self.g.all_reduce(lo, "min")
+        self.g.all_reduce(hi, "max")
+        return hi.cpu().numpy() / 1e3, lo.cpu().numpy() / 1e3
 
     def run(self, steps: int) -> SimReport:
         """Run `steps` steps; every rank gets the full report (rasters gathered)."""
         import torch
-        import torch.distributed as dist
         self.reset(steps if self.per_step_counts else 1)
         if self.record_steps and self.record_steps < steps:
             raise ValueError("record_raster_steps is smaller than the number of steps")
-        dist.barrier()
+        self.prepare(steps)
+        self.g.barrier()
         torch.cuda.synchronize(self.dev)
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
@@ -434,19 +469,18 @@ class DistSimulator:
         t1.record()
         torch.cuda.synchronize(self.dev)
         ms = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device=self.dev)
-        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        self.g.all_reduce(ms, "max")
         self.check_status()
         return self._report(steps, float(ms.item()))
 
     def _report(self, steps: int, ms: float) -> SimReport:
         import torch
-        import torch.distributed as dist
         lay = self.net.layout
         s = self.state
         hop = self.hop_ids.clone()
         deliv = self.deliv_ids.clone()
-        dist.all_reduce(hop)
-        dist.all_reduce(deliv)
+        self.g.all_reduce(hop)
+        self.g.all_reduce(deliv)
         width = max((lay.n_local(h) + 31) // 32 for h in range(lay.n_shards))
         nmax = max(lay.n_local(h) for h in range(lay.n_shards))
         raster = None
@@ -454,7 +488,7 @@ class DistSimulator:
             mine = torch.zeros((steps, max(width, 1)), dtype=torch.int32, device=self.dev)
             mine[:, : s.local_words] = s.raster[:steps, : s.local_words]
             parts = [torch.zeros_like(mine) for _ in range(self.world)]
-            dist.all_gather(parts, mine)
+            self.g.all_gather(parts, mine)
             raster = np.zeros((steps, lay.n_neurons), dtype=bool)
             for h in range(self.world):
                 nl = lay.n_local(h)
@@ -467,7 +501,7 @@ class DistSimulator:
         vt[0, : s.n_local] = s.v[: s.n_local]
         vt[1, : s.n_local] = s.i_syn[: s.n_local]
         parts = [torch.zeros_like(vt) for _ in range(self.world)]
-        dist.all_gather(parts, vt)
+        self.g.all_gather(parts, vt)
         v = np.zeros(lay.n_neurons, dtype=np.float32)
         i = np.zeros(lay.n_neurons, dtype=np.float32)
         for h in range(self.world):
@@ -476,12 +510,12 @@ class DistSimulator:
             v[lay.members[h]] = p[0, :nl]
             i[lay.members[h]] = p[1, :nl]
         sp = s.spike_total.clone()
-        dist.all_reduce(sp)
-        lat, lat_max = self.latencies_us(steps)
+        self.g.all_reduce(sp)
+        lat, lat_min = self.latencies_us(steps)
         mode = "two-level" if self.plan.two_level else "direct"
         return SimReport(steps=steps, n_gpus=self.world, raster=raster, deliv_ids=deliv.cpu().numpy(),
                          hop_ids=hop.cpu().numpy(), spikes=int(sp.item()), v=v, i_syn=i, elapsed_ms=ms,
                          exchange=mode, delivery=self.delivery,
-                         extra={"transport": self.transport, "exchange_us": lat, "exchange_wait_us": lat_max,
+                         extra={"transport": self.transport, "exchange_us": lat, "exchange_transfer_us": lat_min,
                                 "exchange_p50_us": float(np.percentile(lat, 50)) if lat.size else None,
                                 "exchange_p99_us": float(np.percentile(lat, 99)) if lat.size else None})

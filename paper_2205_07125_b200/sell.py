@@ -85,12 +85,7 @@ def plan_tiles(n_words: int, n_local: int, n_sms: int) -> tuple[int, int, bool]:
 
 def block_split(n_local: int, n_tiles: int, n_sms: int) -> int:
     """log2 of the parts each (slice, tile) block is split into for the warps' claims
-    (nc_shard_t.flags bits 1-2; tiled kernel only): 1 below BALANCE_UNITS units per warp.
-    NC_BLOCK_SPLIT=s forces it (tuning, tools/split_ab*.sh)."""
-    import os
-    forced = os.environ.get("NC_BLOCK_SPLIT")
-    if forced is not None and n_tiles > 1:
-        return int(forced) & 3
+    (nc_shard_t.flags bits 1-2; tiled kernel only): 1 below BALANCE_UNITS units per warp."""
     n_slices = (n_local + 31) // 32
     return 1 if n_tiles > 1 and n_slices * n_tiles < BALANCE_UNITS * n_sms * 32 else 0
 

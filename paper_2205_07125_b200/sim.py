@@ -35,7 +35,7 @@ from .routing import RoutingTable
 
 __all__ = [
     "LifParams", "ShardLayout", "ExchangePlan", "Network", "Simulator", "SimReport", "simulate",
-    "q_from_p", "inhibitory_mask", "ID_BITS",
+    "q_from_p", "inhibitory_mask", "ID_BITS", "StepGraphs",
 ]
 
 ID_BITS = sell.ID_BITS  # unpacked builder entry: (q << 26) | tile-relative pre id
@@ -662,6 +662,54 @@ def _push_csr(csr: ShardCSR, lay: ShardLayout, h: int, dev):
     return rowptr, ent
 
 
+class StepGraphs:
+    """CUDA graphs of k consecutive steps, one per chunk length k, captured once.
+
+    Capturing does not run anything, so :meth:`prepare` can capture every chunk
+    length a loop of `steps` will replay before a timed region starts."""
+
+    def __init__(self, device, one_step, chunk: int):
+        self.device = device
+        self.one_step = one_step          # one_step(stream_handle) enqueues one step
+        self.chunk = max(1, int(chunk))
+        self.graphs: dict = {}
+
+    def clear(self):
+        self.graphs.clear()
+
+    def _chunks(self, steps: int):
+        done = 0
+        while done < steps:
+            k = min(self.chunk, steps - done)
+            yield k
+            done += k
+
+    def get(self, k: int):
+        import torch
+        g = self.graphs.get(k)
+        if g is None:
+            g = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream(self.device)
+            side.wait_stream(torch.cuda.current_stream(self.device))
+            with torch.cuda.stream(side):
+                g.capture_begin()
+                cst = _native.stream_handle(self.device)
+                for _ in range(k):
+                    self.one_step(cst)
+                g.capture_end()
+            torch.cuda.current_stream(self.device).wait_stream(side)
+            self.graphs[k] = g
+        return g
+
+    def prepare(self, steps: int):
+        for k in set(self._chunks(steps)):
+            self.get(k)
+
+    def run(self, steps: int):
+        for k in self._chunks(steps):
+            self.get(k).replay()
+
+
 class Simulator:
     """Runs the step loop for the shards this process owns (all of them, on one device)."""
 
@@ -704,8 +752,7 @@ class Simulator:
         self._gbar = torch.zeros(1, dtype=torch.int32, device=dev)
         self.hop_ids = None
         self.deliv_ids = None
-        self._graph = None
-        self._graph_len = 0
+        self._graphs = StepGraphs(dev, self._one_step, graph_chunk)
         self._check(self.lib.nc_sim_prepare(), "prepare")
 
     def _check(self, rc, what):
@@ -724,7 +771,7 @@ class Simulator:
         self.deliv_ids = torch.zeros((rows, self.n, self.n), dtype=torch.int64, device=self.net.device)
         self.fwd_count.zero_()
         if self.n > 1:   # the exchange launches capture the counter buffers reallocated above
-            self._graph = None
+            self._graphs.clear()
 
     def _one_step(self, st):
         L = self.lib
@@ -768,7 +815,6 @@ class Simulator:
 
     def advance(self, steps: int):
         """Enqueue `steps` steps on the current stream (graph-replayed in chunks)."""
-        import torch
         if self.delivery == "persistent":
             s = self.states[0]
             st = _native.stream_handle(self.net.device)
@@ -778,23 +824,12 @@ class Simulator:
         if not self.use_graph:
             self.advance_eager(steps)
             return
-        done = 0
-        while done < steps:
-            k = min(self.graph_chunk, steps - done)
-            if self._graph is None or self._graph_len != k:
-                g = torch.cuda.CUDAGraph()
-                side = torch.cuda.Stream(self.net.device)
-                side.wait_stream(torch.cuda.current_stream(self.net.device))
-                with torch.cuda.stream(side):
-                    g.capture_begin()
-                    cst = _native.stream_handle(self.net.device)
-                    for _ in range(k):
-                        self._one_step(cst)
-                    g.capture_end()
-                torch.cuda.current_stream(self.net.device).wait_stream(side)
-                self._graph, self._graph_len = g, k
-            self._graph.replay()
-            done += k
+        self._graphs.run(steps)
+
+    def prepare(self, steps: int):
+        """Capture every CUDA graph a following advance(steps) replays (no work is run)."""
+        if self.use_graph and self.delivery != "persistent":
+            self._graphs.prepare(steps)
 
     def check_status(self):
         for s in self.states:
@@ -804,13 +839,14 @@ class Simulator:
             if flags[1]:
                 raise RuntimeError(f"exchange watchdog expired on shard {s.h}")
 
-    def run(self, steps: int, *, warmup_graph: bool = True) -> SimReport:
+    def run(self, steps: int) -> SimReport:
         import torch
         if steps < 0:
             raise ValueError("steps must be >= 0")
         self.reset(steps if self.per_step_counts else 1)
         if self.record_steps and self.record_steps < steps:
             raise ValueError("record_raster_steps is smaller than the number of steps")
+        self.prepare(steps)
         torch.cuda.synchronize(self.net.device)
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)

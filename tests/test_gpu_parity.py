@@ -323,3 +323,58 @@ def test_config1_gpu_matches_committed_rasters(seed):
     assert rep.hop_ids.sum(axis=0).astype(int).tolist() == want["hop_total"]
     assert hashlib.sha256(np.ascontiguousarray(rep.v, dtype=np.float32).view(np.uint32).tobytes()).hexdigest() == \
         want["v_sha256"]
+
+
+# ------------------------------------------------------------------ the benchmarked network
+
+def _row_hash(rows, cols, q, n):
+    """Order-independent per-row digest of (col, q) pairs (int64 wrap-around sums)."""
+    import torch
+    h = (cols.to(torch.int64) * 0x9E3779B1 + q.to(torch.int64) * 0x85EBCA77 + 0x27D4EB2F) & 0xFFFFFFFF
+    h = h * h + cols.to(torch.int64)
+    out = torch.zeros(n, dtype=torch.int64, device=cols.device)
+    out.index_add_(0, rows, h)
+    return out
+
+
+def test_config2_network_matches_oracle():
+    """BASELINE config 2 itself -- 1M neurons x ~1k synapses, the device generator, the
+    2-tile bank-ordered packed J-SELL layout bench.py times -- against the oracle's own CPU
+    generator and loop: same synapse multiset per row, then 20 steps of rasters, V and I
+    bit for bit."""
+    import os
+    import torch
+    spec = S.GeneratorSpec.random(1_000_000, 1000.0, seed=1)
+    lay = S.ShardLayout.blocks(spec.n_neurons, 1)
+    net = S.Network.generate(spec, lay)
+    csr = net.shards[0]
+    assert csr.n_tiles == 2 and csr.row_perm is not None
+    threads = os.cpu_count() or 1
+    rowptr, col, q = c_oracle.generate_random_csr(spec.n_neurons, 1000.0, spec.seed, threads=threads)
+    assert int(rowptr[-1]) == net.n_synapses
+    dev = csr.syn.device
+    # graph: per-row digests of the decoded device layout vs the oracle's CSR
+    row, pre, qq, _ = sell.decode(csr)
+    gid_of_internal = torch.full((lay.n_words * 32,), -1, dtype=torch.int64, device=dev)
+    gid_of_internal[: lay.n_local(0)] = torch.from_numpy(lay.members[0]).to(dev)
+    post = torch.from_numpy(net.layout.members[0]).to(dev)[row]
+    hd = _row_hash(post, gid_of_internal[pre], qq, spec.n_neurons)
+    del row, pre, qq, post, gid_of_internal
+    rp = torch.from_numpy(rowptr).to(dev)
+    rows = torch.repeat_interleave(torch.arange(spec.n_neurons, device=dev), rp[1:] - rp[:-1])
+    ho = _row_hash(rows, torch.from_numpy(col).to(dev), torch.from_numpy(q).to(dev), spec.n_neurons)
+    del rows, rp
+    assert torch.equal(hd, ho), f"{int((hd != ho).sum())} rows differ between the device and oracle generators"
+    del hd, ho
+    torch.cuda.empty_cache()
+    # dynamics
+    steps = 20
+    lif = S.LifParams()
+    rep = S.Simulator(net, lif, 1, None, record_raster_steps=steps).run(steps)
+    ref = c_oracle.simulate_csr(rowptr, col, q, np.zeros(spec.n_neurons, dtype=np.int32), 1, [[-1]],
+                                lif.constants(1), steps, threads=threads, counts=False)
+    assert rep.spikes > 1000
+    np.testing.assert_array_equal(rep.raster.sum(1), ref["raster"].sum(1))
+    np.testing.assert_array_equal(rep.raster, ref["raster"])
+    np.testing.assert_array_equal(rep.v.view(np.uint32), ref["v"].view(np.uint32))
+    np.testing.assert_array_equal(rep.i_syn.view(np.uint32), ref["i"].view(np.uint32))

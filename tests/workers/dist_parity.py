@@ -56,13 +56,13 @@ def main() -> int:
         runs += [("p2p", "fused+send"), ("p2p", "persistent"), ("p2p", "binned"), ("nccl", "binned")]
         for transport, delivery in runs:
             # fused+send: the step kernel's own P2P send, forced on (off by default at this size)
-            if delivery == "fused+send":
-                os.environ["NC_FUSED_SEND"] = "1"
             sim = DistSimulator(net, lif, 1, rt, transport=transport, delivery=delivery.split("+")[0],
-                                record_raster_steps=steps, per_step_counts=True)
-            os.environ.pop("NC_FUSED_SEND", None)
+                                record_raster_steps=steps, per_step_counts=True,
+                                fused_send=(delivery == "fused+send"))
             assert sim.fused_send == (delivery == "fused+send")
             rep = sim.run(steps)
+            # a second run on the same simulator (reset() must clear the P2P inboxes: tags restart)
+            rep2 = sim.run(steps) if transport == "p2p" else rep
             sim.close()
             if rank == 0:
                 checks = {
@@ -70,6 +70,8 @@ def main() -> int:
                     "deliv": np.array_equal(rep.deliv_ids, ref["deliv"]),
                     "hop": np.array_equal(rep.hop_ids, ref["hop"]),
                     "v": np.array_equal(rep.v.view(np.uint32), ref["v"].view(np.uint32)),
+                    "rerun": (np.array_equal(rep2.raster, ref["raster"]) and np.array_equal(rep2.hop_ids, ref["hop"])
+                              and np.array_equal(rep2.v.view(np.uint32), ref["v"].view(np.uint32))),
                 }
                 good = all(checks.values())
                 ok &= good

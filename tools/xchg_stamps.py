@@ -1,6 +1,6 @@
 """Per-phase timing of the P2P spike exchange (run under torchrun, one rank per GPU):
 
-    NC_XCHG_DBG=1 torchrun --nproc-per-node N tools/xchg_stamps.py [--delivery fused|persistent]
+    torchrun --nproc-per-node N tools/xchg_stamps.py [--delivery fused|persistent]
 
 Prints, per rank, medians over steps 20..63 of the exchange blocks' globaltimer
 stamps: start -> message published -> peer flag seen -> inbound ids scattered.
@@ -22,7 +22,6 @@ def main():
     ap.add_argument("--neurons", type=int, default=1_000_000)
     ap.add_argument("--delivery", default="fused")
     args = ap.parse_args()
-    os.environ.setdefault("NC_XCHG_DBG", "1")
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
@@ -31,7 +30,8 @@ def main():
     n = args.neurons * world
     spec = S.GeneratorSpec.random(n, 1000.0, seed=1)
     net = S.Network.generate(spec, S.ShardLayout.blocks(n, world), device=dev, shards=[rank])
-    sim = D.DistSimulator(net, S.LifParams(), 1, None, transport="p2p", delivery=args.delivery, latency_steps=80)
+    sim = D.DistSimulator(net, S.LifParams(), 1, None, transport="p2p", delivery=args.delivery, latency_steps=80,
+                          debug_stamps=True)
     sim.reset(1)
     sim.advance(80)
     torch.cuda.synchronize()
