@@ -1,0 +1,222 @@
+"""BASELINE configs 3, 4 and 5 at their real sizes (one process per GPU, torchrun).
+
+    torchrun --nproc-per-node N bench_configs.py --config 3|4|5 [--engines fused,persistent]
+
+* config 3: 10 M neurons x ~1 000 synapses (random, C = 1), direct exchange;
+  run at N = 1, 2, 4 (strong scaling of the same network).
+* config 4: the config-3 network over N GPUs in 2 groups, direct vs two-level
+  routing (the reference's group_gpus -> select_bridges -> build_routing_table
+  on the measured traffic matrix) at realised rates 1 / 2 / 5 / 10 / 20 / 50 Hz,
+  ids and bytes per hop from the int64 channel counters.
+* config 5: 50 M neurons in 64 regions, ~90 % of ~1 000 synapses intra-region,
+  two-level routing where N >= 4; memory per GPU reported.
+
+Every engine in --engines that fits the GPU runs on the same network: "fused"
+(the pull kernel K3+K1+K2 on the J-SELL layout, 3.2 B/synapse + an 8 B/synapse
+transient while building) and "persistent" (the event-driven whole-step
+kernel on the push CSR, 4 B/synapse).  Results are bit-identical between
+engines (tests/test_gpu_parity.py), so the faster one is the config's number.
+Exchange latency is SURVEY 8(d)'s: p50/p99 over steps of the per-step max over
+ranks (device %globaltimer), transfer-only (min over ranks) beside it.
+
+Prints one JSON line per (engine, route, rate) point on rank 0 and appends it
+to --out.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import bench as B  # noqa: E402  (timing, clocks, latency helpers)
+
+CONFIGS = {
+    3: dict(neurons=10_000_000, degree=1000.0, communities=1, intra_frac=None, rates=(None,)),
+    4: dict(neurons=10_000_000, degree=1000.0, communities=1, intra_frac=None, rates=(1, 2, 5, 10, 20, 50)),
+    5: dict(neurons=50_000_000, degree=1000.0, communities=64, intra_frac=0.9, rates=(None,)),
+}
+GB = 1e9
+
+
+def spec_for(cfg: dict, seed: int):
+    from paper_2205_07125_b200 import sim as S
+    n, c = cfg["neurons"], cfg["communities"]
+    if c == 1:
+        return S.GeneratorSpec.random(n, cfg["degree"], seed=seed)
+    size = n / c
+    p_in = cfg["intra_frac"] * cfg["degree"] / (size - 1)
+    p_out = (1 - cfg["intra_frac"]) * cfg["degree"] / (n - size)
+    return S.GeneratorSpec(n, c, min(p_in, 1.0), min(p_out, p_in), seed=seed)
+
+
+def traffic_from_push(net, rank: int, world: int, dev):
+    """pg[a][b] = sum over synapses a -> b of q / 32 from the push CSR (exact integer sums of
+    q, all-reduced), wg = neurons per shard: the planner's view of the generated network."""
+    import torch
+    import torch.distributed as dist
+    lay = net.layout
+    rowptr, ent = net.shards[rank]._push_cache
+    m = torch.zeros((world, world), dtype=torch.int64, device=dev)
+    chunk = 1 << 28
+    for a in range(world):
+        lo, hi = int(rowptr[int(lay.base[a])].item()), int(rowptr[int(lay.base[a + 1])].item())
+        tot = torch.zeros((), dtype=torch.int64, device=dev)
+        for s in range(lo, hi, chunk):
+            e = ent[s:min(hi, s + chunk)]
+            tot += (((e >> 26) & 31) + 1).sum(dtype=torch.int64)
+        m[a, rank] = tot
+    if world > 1:
+        dist.all_reduce(m)
+    return m.cpu().numpy().astype(np.float64) / 32.0
+
+
+def main() -> int:
+    import torch
+    import torch.distributed as dist
+
+    import paper_2205_07125_b200 as nc
+    from paper_2205_07125_b200 import sim as S
+    from paper_2205_07125_b200.distributed import DistSimulator
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, required=True, choices=sorted(CONFIGS))
+    ap.add_argument("--engines", default="fused,persistent")
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--groups", type=int, default=2)
+    ap.add_argument("--rates", default=None, help="comma list of target rates (Hz); default per config")
+    ap.add_argument("--routes", default=None, help="direct,two-level (default: per config)")
+    ap.add_argument("--neurons", type=int, default=None, help="override the config's neuron count (tests)")
+    ap.add_argument("--chunk", type=int, default=100)
+    ap.add_argument("--out", default=None)
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config])
+    if args.neurons:
+        cfg["neurons"] = args.neurons
+
+    rank, world, local = B.dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    engines = args.engines.split(",")
+    spec = spec_for(cfg, args.seed)
+    syn_per_gpu = cfg["neurons"] * cfg["degree"] / world
+    free = torch.cuda.mem_get_info(dev)[0]
+    want_pull = "fused" in engines and syn_per_gpu * 8.0 + 4 * GB < free
+    want_push = any(e in ("persistent", "push") for e in engines) or args.config == 4
+    skipped = {}
+    if "fused" in engines and not want_pull:
+        skipped["fused"] = ("pull layout build needs ~8 B/synapse transient (%.0f GB) on a GPU with %.0f GB free"
+                            % (syn_per_gpu * 8 / GB, free / GB))
+    lay = S.ShardLayout.blocks(cfg["neurons"], world)
+    torch.cuda.reset_peak_memory_stats(dev)
+    t0 = time.time()
+    net = S.Network.generate(spec, lay, device=dev, shards=[rank], pull=want_pull, push=want_push)
+    torch.cuda.synchronize()
+    build_s = time.time() - t0
+    csr = net.shards[rank]
+    mem = {"after_build_gb": round(torch.cuda.memory_allocated(dev) / GB, 2),
+           "build_peak_gb": round(torch.cuda.max_memory_allocated(dev) / GB, 2),
+           "pull_layout_gb": round(csr.n_entries * 4 / GB, 2) if want_pull else None,
+           "push_csr_gb": round(csr._push_cache[1].numel() * 4 / GB, 2) if want_push else None,
+           "gpu_total_gb": round(torch.cuda.get_device_properties(dev).total_memory / GB, 1)}
+    nsyn = torch.tensor([net.n_synapses], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(nsyn)
+
+    # routes from the reference planner on the generated network's traffic
+    tables = {"direct": None}
+    planner = None
+    routes = args.routes.split(",") if args.routes else (["direct", "two-level"] if args.config == 4 or (
+        args.config == 5 and world >= 4) else ["direct"])
+    if "two-level" in routes and world >= 3:
+        if not want_push:
+            raise SystemExit("two-level routes need the traffic matrix from the push CSR")
+        pg = traffic_from_push(net, rank, world, dev)
+        gt = nc.GpuTrafficGraph(world, pg, np.array([lay.n_local(h) for h in range(world)], dtype=np.float64))
+        groups = nc.group_gpus(gt, args.groups)
+        tables["two-level"] = nc.build_routing_table(gt, groups, nc.select_bridges(gt, groups))
+        tables["direct"] = nc.route_p2p(gt)
+        planner = {"groups": groups.membership.tolist(),
+                   "bridges": [[a, b, v] for (a, b), v in sorted(tables["two-level"].bridges.items())]}
+    tables = {k: v for k, v in tables.items() if k in routes}
+
+    rates = [float(r) for r in args.rates.split(",")] if args.rates else list(cfg["rates"])
+    out_path = Path(args.out) if args.out else None
+
+    class A:   # the timing helpers' argument bundle
+        steps, warmup, chunk, transport, msg_cap, seed, fused_send = (args.steps, args.warmup, args.chunk, "p2p",
+                                                                      None, args.seed, "auto")
+
+    for rate in rates:
+        lif = S.LifParams() if rate is None else S.LifParams.for_rate(rate)
+        for mode, rt in tables.items():
+            for eng in engines:
+                if eng in skipped or (eng == "fused" and not want_pull) or (eng != "fused" and not want_push):
+                    continue
+                t_case = time.time()
+                if world > 1:
+                    sim = DistSimulator(net, lif, args.seed, rt, transport="p2p", delivery=eng,
+                                        latency_steps=args.warmup + args.steps, graph_chunk=args.chunk)
+                else:
+                    sim = S.Simulator(net, lif, args.seed, rt, delivery=eng, graph_chunk=args.chunk)
+                if eng == "fused":
+                    B.enable_kernel_stamps(sim, args.warmup + args.steps)
+                clocks = B.ClockSampler(local)
+                ms, spikes, lat, lat_min = B.time_steps(sim, A, world, dev, clocks)
+                kms, kms_ranks = (B.live_kernel_ms(sim, args.warmup, args.steps, world, dev) if eng == "fused"
+                                  else (None, None))
+                hop = sim.hop_ids.sum(0).clone()
+                if world > 1:
+                    dist.all_reduce(hop)
+                fused_send = getattr(sim, "fused_send", None)
+                if world > 1:
+                    sim.close()
+                del sim
+                if rank != 0:
+                    continue
+                n = cfg["neurons"]
+                h = hop.cpu().numpy().astype(np.float64) / (args.warmup + args.steps)
+                row = {
+                    "config": args.config, "n_gpus": world, "engine": eng, "route": mode,
+                    "rate_target_hz": rate, "rate_hz": round(spikes / n / (args.steps * 1e-3), 3),
+                    "steps_per_s": round(args.steps / (ms * 1e-3), 2), "ms_per_step": round(ms / args.steps, 4),
+                    "steps": args.steps, "warmup": args.warmup,
+                    "exchange_us": B.lat_summary(lat, lat_min, "p2p"),
+                    "kernel_ms": round(kms, 4) if kms else None,
+                    "kernel_ms_per_rank": [round(x, 4) for x in kms_ranks] if kms_ranks else None,
+                    "ids_per_step": round(float(h.sum()), 1),
+                    "wire_bytes_per_step": round(float(h.sum()) * 8 + 8 * int((h > 0).sum()), 1),
+                    "channel_ids_per_step": np.round(h, 1).tolist(),
+                    "neurons": n, "synapses": int(nsyn.item()), "communities": cfg["communities"],
+                    "partition": "blocks", "bitmap_tiles": csr.n_tiles if want_pull else None,
+                    "fused_send": fused_send, "memory_per_gpu": mem, "build_s": round(build_s, 1),
+                    "planner": planner, "clocks": clocks.summary(), "case_s": round(time.time() - t_case, 1),
+                    "skipped_engines": skipped or None,
+                }
+                if eng == "fused" and kms:
+                    alg = net.n_synapses * 16 / 5 + lay.n_local(rank) * (4 * csr.n_tiles + 22)
+                    row["roofline_frac_rank0"] = round(alg / (kms_ranks[0] * 1e-3) / B.load_peaks()["hbm_gbs"] / GB, 3)
+                print(json.dumps(row), flush=True)
+                if out_path:
+                    with out_path.open("a") as f:
+                        f.write(json.dumps(row) + "\n")
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    raise SystemExit(main())

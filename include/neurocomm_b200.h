@@ -78,6 +78,12 @@ int nc_traffic_histogram(const int64_t* edge_i, const int64_t* edge_j, const dou
                          const double* weights, const int64_t* assignment, int64_t n_edges,
                          int32_t n_gpus, int32_t lsb_exponent, int32_t n_digits,
                          unsigned long long* pg_limbs, void* stream);
+/* Same with int32 neuron ids and assignment (16 B per edge streamed instead of
+ * 24; what traffic.aggregate uses below 2^31 neurons). */
+int nc_traffic_histogram32(const int32_t* edge_i, const int32_t* edge_j, const double* edge_p,
+                           const double* weights, const int32_t* assignment, int64_t n_edges,
+                           int32_t n_gpus, int32_t lsb_exponent, int32_t n_digits,
+                           unsigned long long* pg_limbs, void* stream);
 int nc_weight_histogram(const double* weights, const int64_t* assignment, int64_t n_neurons,
                         int32_t n_gpus, int32_t lsb_exponent, int32_t n_digits,
                         unsigned long long* wg_limbs, void* stream);
@@ -424,6 +430,14 @@ int nc_graphgen_count(const nc_graphgen_t* g, int32_t n_tiles, int32_t tile_word
 int nc_graphgen_fill(const nc_graphgen_t* g, int32_t n_tiles, int32_t tile_words, const int64_t* slice_ptr,
                      const uint32_t* row_meta, const int32_t* pos_of, int32_t* lower_fill, uint32_t* syn,
                      void* stream);
+/* Push synapses (nc_shard_t push_rowptr / push_syn format) straight from the
+ * generator, without a pull layout.  Phase 0: push_rowptr[pre + 1] += entries
+ * of pre (int64 [n_words*32 + 1], zeroed) and dest_mask[r] |= shards hosting a
+ * target of local row r, this shard excluded (zeroed, 4-byte aligned,
+ * n_local + 2 entries); the caller prefix-sums push_rowptr.  Phase 1 fills
+ * push_syn (push_fill int32 [n_words*32] zeroed: slot claims). */
+int nc_graphgen_push(const nc_graphgen_t* g, int32_t phase, int64_t* push_rowptr, int32_t* push_fill,
+                     uint32_t* push_syn, uint16_t* dest_mask, void* stream);
 /* Pad pre-fill of an unpacked padded SELL-32 array: every entry = 0 (q = 0).
  * n_tiles / tile_words are accepted for ABI stability. */
 int nc_sell_fill_pads(const int64_t* slice_ptr, int64_t n_blocks, int32_t n_tiles, int32_t tile_words,

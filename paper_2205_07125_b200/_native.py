@@ -100,6 +100,8 @@ _SIGS = {
     "nc_traffic_exponents": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
     "nc_traffic_histogram": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int32,
                                        c_int32, c_int32, c_void_p, c_void_p]),
+    "nc_traffic_histogram32": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int32,
+                                       c_int32, c_int32, c_void_p, c_void_p]),
     "nc_weight_histogram": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_int32, c_int32, c_void_p, c_void_p]),
     "nc_sim_init": (c_int32, [C.POINTER(ShardC), C.POINTER(LifParamsC), c_void_p]),
     "nc_sim_step_fused": (c_int32, [C.POINTER(ShardC), C.POINTER(LifParamsC), c_void_p]),
@@ -115,6 +117,7 @@ _SIGS = {
     "nc_graphgen_fill": (c_int32, [C.POINTER(GraphGenC), c_int32, c_int32, c_void_p, c_void_p, c_void_p, c_void_p,
                                    c_void_p, c_void_p]),
     "nc_graphgen_degrees": (c_int32, [C.POINTER(GraphGenC), c_void_p, c_void_p]),
+    "nc_graphgen_push": (c_int32, [C.POINTER(GraphGenC), c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "nc_sell_fill_pads": (c_int32, [c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p]),
     "nc_dest_mask_from_csr": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_int32, c_void_p, c_int32,
                                         c_void_p, c_int32, c_int32, c_void_p, c_void_p]),

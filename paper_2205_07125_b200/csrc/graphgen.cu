@@ -206,6 +206,54 @@ __global__ void k_fill(const nc_graphgen_t g, int32_t T, int32_t TW, const int64
   }
 }
 
+// Push synapses straight from the generator, for the event-driven engines (no
+// pull layout needed: config 5 over 2 GPUs holds 2.5e10 synapses per GPU, which
+// fit as 4-byte push entries but not as pull layout + transpose).  Rows are
+// internal pre ids (every neuron), entries this shard's post rows,
+// (inh(pre) << 31) | ((q - 1) << 26) | post_local -- the nc_build_push_csr
+// format.  Phase 0 counts entries per pre row into cnt[pre + 1] and ORs the
+// shards hosting each local row's targets into its 16-bit destination mask;
+// the host scans cnt into rowptr; phase 1 places the entries (slot claims with
+// atomics: the order inside a row is free, delivery sums integers).
+__device__ __forceinline__ void or_dest(uint16_t* dest, int64_t r, uint32_t m) {
+  unsigned int* w = reinterpret_cast<unsigned int*>(dest + (r & ~1ll));
+  atomicOr(w, m << (16 * (r & 1)));
+}
+
+__global__ void k_push_gen(const nc_graphgen_t g, int phase, unsigned long long* cnt, const int64_t* rowptr,
+                           int32_t* fill, uint32_t* out, uint16_t* dest) {
+  const Comm cm = make_comm(g);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n_neurons;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t oi = g.owner[i];
+    const uint32_t iid = (uint32_t)g.internal_id[i];
+    const uint32_t inh_i = is_inh(g, i);
+    for_each_upper(g, cm, i, [&](int64_t j, bool intra) {
+      const int32_t oj = g.owner[j];
+      if (oi != g.shard && oj != g.shard) return;
+      const uint32_t jid = (uint32_t)g.internal_id[j];
+      if (phase == 0) {
+        if (oj == g.shard) atomicAdd(cnt + iid + 1, 1ull);
+        if (oi == g.shard) atomicAdd(cnt + jid + 1, 1ull);
+        if (oi != oj) {
+          if (oi == g.shard) or_dest(dest, (int64_t)iid - g.local_base, 1u << oj);
+          else or_dest(dest, (int64_t)jid - g.local_base, 1u << oi);
+        }
+        return;
+      }
+      const uint32_t q = edge_q(g, i, j, intra);
+      if (oj == g.shard) {
+        const int32_t k = atomicAdd(fill + iid, 1);
+        out[rowptr[iid] + k] = (inh_i << 31) | ((q - 1u) << 26) | (uint32_t)((int64_t)jid - g.local_base);
+      }
+      if (oi == g.shard) {
+        const int32_t k = atomicAdd(fill + jid, 1);
+        out[rowptr[jid] + k] = (is_inh(g, j) << 31) | ((q - 1u) << 26) | (uint32_t)((int64_t)iid - g.local_base);
+      }
+    });
+  }
+}
+
 // Pad pre-fill of the unpacked padded layout: the pad entry (q = 0) is 0.
 __global__ void k_fill_pads(const int64_t* slice_ptr, int64_t n_blocks, uint32_t* syn) {
   for (int64_t b = blockIdx.x; b < n_blocks; b += gridDim.x)
@@ -390,6 +438,20 @@ extern "C" int nc_graphgen_fill(const nc_graphgen_t* g, int32_t n_tiles, int32_t
   }
   k_fill<<<grid_for(g->n_neurons, 128), 128, 0, (cudaStream_t)stream>>>(*g, n_tiles, tile_words, slice_ptr,
                                                                           row_meta, pos_of, lower_fill, syn);
+  NC_LAUNCH_CHECK();
+  return NC_OK;
+}
+
+extern "C" int nc_graphgen_push(const nc_graphgen_t* g, int32_t phase, int64_t* push_rowptr, int32_t* push_fill,
+                                uint32_t* push_syn, uint16_t* dest_mask, void* stream) {
+  if (!g || g->n_neurons < 1 || g->n_communities < 1 || g->n_communities > g->n_neurons || !g->owner ||
+      !g->internal_id || !push_rowptr || (phase == 0 && !dest_mask) ||
+      (phase == 1 && (!push_fill || !push_syn)) || (phase != 0 && phase != 1)) {
+    nc_set_error("nc_graphgen_push: bad arguments");
+    return NC_E_ARG;
+  }
+  k_push_gen<<<grid_for(g->n_neurons, 128), 128, 0, (cudaStream_t)stream>>>(
+      *g, phase, reinterpret_cast<unsigned long long*>(push_rowptr), push_rowptr, push_fill, push_syn, dest_mask);
   NC_LAUNCH_CHECK();
   return NC_OK;
 }

@@ -89,76 +89,121 @@ __global__ void k_exponents(const int64_t* __restrict__ ei, const int64_t* __res
   }
 }
 
-// Carry-normalise a block's limbs for one cell and add into global.
-__device__ void flush_cell(unsigned long long* g, const unsigned long long* s, int n_digits) {
-  unsigned long long carry = 0;
-  for (int k = 0; k < n_digits; ++k) {
-    const unsigned long long v = s[k] + carry;  // s[k] < 2^63, carry < 2^32: no wrap
-    const unsigned long long digit = (k + 1 < n_digits) ? (v & 0xffffffffull) : v;
-    carry = (k + 1 < n_digits) ? (v >> 32) : 0;
-    if (digit) atomicAdd(g + k, digit);
+// Shared-memory accumulator of one block: kCopies copies (lane & (kCopies-1)) of
+// [cell][digit] pairs of 32-bit words {sum, carries}.  A digit add is one NATIVE
+// 32-bit shared atomic (64-bit shared atomics compile to CAS spin loops on
+// sm_100a: ATOMS.CAST.SPIN.64, the round-1 bottleneck) plus, when the returned old
+// value shows a wrap, a second one on the carry word: the pair is exactly the
+// 64-bit limb sum + carries * 2^32.  Copies spread same-cell lanes over
+// different addresses.
+constexpr int kCopies = 4;
+
+__device__ __forceinline__ void add32c(unsigned int* p, unsigned int d) {
+  if (!d) return;
+  const unsigned int old = atomicAdd(p, d);
+  if (old + d < old) atomicAdd(p + 1, 1u);
+}
+
+template <typename Idx>
+__device__ __forceinline__ void edge_term(const Idx* __restrict__ ei, const Idx* __restrict__ ej,
+                                          const double* __restrict__ ep, const double* __restrict__ w,
+                                          const Idx* __restrict__ asg, int64_t k, int n_gpus, double* x,
+                                          int* cell) {
+  if (ei) {
+    const int64_t i = (int64_t)ei[k], j = (int64_t)ej[k];
+    *x = contrib(ep[k], __ldg(w + i), __ldg(w + j));
+    *cell = cell_index((int64_t)__ldg(asg + i), (int64_t)__ldg(asg + j), n_gpus);
+  } else {  // per-GPU weight totals (binned_sums over assignment)
+    *x = w[k];
+    *cell = (int)asg[k];
   }
 }
 
-template <bool kSmem>
+template <typename Idx>
 __global__ void __launch_bounds__(kThreads)
-k_histogram(const int64_t* __restrict__ ei, const int64_t* __restrict__ ej,
-            const double* __restrict__ ep, const double* __restrict__ w,
-            const int64_t* __restrict__ asg, int64_t n, int n_gpus, int lsb0, int n_digits,
-            unsigned long long* __restrict__ out) {
-  extern __shared__ unsigned long long sl[];
+k_histogram_smem(const Idx* __restrict__ ei, const Idx* __restrict__ ej, const double* __restrict__ ep,
+                 const double* __restrict__ w, const Idx* __restrict__ asg, int64_t n, int n_gpus, int lsb0,
+                 int n_digits, unsigned long long* __restrict__ out) {
+  extern __shared__ unsigned int sw[];
   const int n_cells = ei ? n_gpus * n_gpus : n_gpus;
-  if (kSmem) {
-    for (int k = threadIdx.x; k < n_cells * n_digits; k += blockDim.x) sl[k] = 0ull;
-    __syncthreads();
-  }
-  unsigned long long* acc = kSmem ? sl : out;
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
-       k += (int64_t)gridDim.x * blockDim.x) {
+  const int per_copy = n_cells * n_digits * 2;
+  for (int k = threadIdx.x; k < kCopies * per_copy; k += blockDim.x) sw[k] = 0u;
+  __syncthreads();
+  unsigned int* mine = sw + (threadIdx.x & (kCopies - 1)) * per_copy;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
     double x;
     int cell;
-    if (ei) {
-      const int64_t i = ei[k], j = ej[k];
-      x = contrib(ep[k], w[i], w[j]);
-      cell = cell_index(asg[i], asg[j], n_gpus);
-    } else {  // per-GPU weight totals (binned_sums over assignment)
-      x = w[k];
-      cell = (int)asg[k];
-    }
-    add_fixed(acc + (int64_t)cell * n_digits, n_digits, decompose(x), lsb0);
+    edge_term(ei, ej, ep, w, asg, k, n_gpus, &x, &cell);
+    const Decomposed d = decompose(x);
+    if (d.mant == 0) continue;
+    const int s = d.lsb - lsb0;  // >= 0 by construction of lsb0; digits k..k+2 < n_digits
+    const int kd = s >> 5, o = s & 31;
+    const unsigned long long lo = d.mant << o;
+    const unsigned long long hi = o ? (d.mant >> (64 - o)) : 0ull;
+    unsigned int* c = mine + (cell * n_digits + kd) * 2;
+    if (kd < n_digits) add32c(c, (unsigned int)lo);             // digits past the window are dropped,
+    if (kd + 1 < n_digits) add32c(c + 2, (unsigned int)(lo >> 32));   // as in add_fixed (callers size it)
+    if (kd + 2 < n_digits) add32c(c + 4, (unsigned int)hi);
   }
-  if (kSmem) {
-    __syncthreads();
-    for (int c = threadIdx.x; c < n_cells; c += blockDim.x)
-      flush_cell(out + (int64_t)c * n_digits, sl + (int64_t)c * n_digits, n_digits);
+  __syncthreads();
+  // one thread per cell: sum the copies into 64-bit digits, normalise, add to global
+  for (int cell = threadIdx.x; cell < n_cells; cell += blockDim.x) {
+    unsigned long long carry = 0;
+    for (int k = 0; k < n_digits; ++k) {
+      unsigned long long x = carry;   // < 2^32 + kCopies * 2^63 / 2^32: no wrap
+      for (int c = 0; c < kCopies; ++c) {
+        const unsigned int* e = sw + c * per_copy + (cell * n_digits + k) * 2;
+        x += (unsigned long long)e[0] + ((unsigned long long)e[1] << 32);
+      }
+      const unsigned long long digit = (k + 1 < n_digits) ? (x & 0xffffffffull) : x;
+      carry = (k + 1 < n_digits) ? (x >> 32) : 0;
+      if (digit) atomicAdd(out + (int64_t)cell * n_digits + k, digit);
+    }
   }
 }
 
-int launch_hist(const int64_t* ei, const int64_t* ej, const double* ep, const double* w,
-                const int64_t* asg, int64_t n, int n_gpus, int lsb0, int n_digits,
-                unsigned long long* out, cudaStream_t st) {
+// Fallback when the cells do not fit in shared memory: straight into the global
+// limbs (native 64-bit global reductions; each add < 2^32).
+template <typename Idx>
+__global__ void __launch_bounds__(kThreads)
+k_histogram_global(const Idx* __restrict__ ei, const Idx* __restrict__ ej, const double* __restrict__ ep,
+                   const double* __restrict__ w, const Idx* __restrict__ asg, int64_t n, int n_gpus, int lsb0,
+                   int n_digits, unsigned long long* __restrict__ out) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    double x;
+    int cell;
+    edge_term(ei, ej, ep, w, asg, k, n_gpus, &x, &cell);
+    add_fixed(out + (int64_t)cell * n_digits, n_digits, decompose(x), lsb0);
+  }
+}
+
+template <typename Idx>
+int launch_hist(const Idx* ei, const Idx* ej, const double* ep, const double* w, const Idx* asg, int64_t n,
+                int n_gpus, int lsb0, int n_digits, unsigned long long* out, cudaStream_t st) {
   if (n <= 0) return NC_OK;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const size_t n_cells = ei ? (size_t)n_gpus * n_gpus : (size_t)n_gpus;
-  const size_t smem = n_cells * n_digits * sizeof(unsigned long long);
+  const size_t smem = (size_t)kCopies * n_cells * n_digits * 2 * sizeof(unsigned int);
   int64_t blocks = (n + kThreads - 1) / kThreads;
-  // each block handles >= 16 items per thread before flushing; cap the grid
-  const int64_t max_blocks = (int64_t)sms * 8;
+  // a few resident blocks per SM, each streaming many items before its flush
+  const int64_t max_blocks = (int64_t)sms * 6;
   if (blocks > max_blocks) blocks = max_blocks;
   if (smem <= kSmemLimit) {
     static bool attr = false;
     if (!attr) {
-      NC_CUDA_TRY(cudaFuncSetAttribute(k_histogram<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      NC_CUDA_TRY(cudaFuncSetAttribute(k_histogram_smem<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)kSmemLimit));
+      NC_CUDA_TRY(cudaFuncSetAttribute(k_histogram_smem<int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)kSmemLimit));
       attr = true;
     }
-    k_histogram<true><<<(unsigned)blocks, kThreads, smem, st>>>(ei, ej, ep, w, asg, n, n_gpus, lsb0,
-                                                                 n_digits, out);
+    k_histogram_smem<Idx><<<(unsigned)blocks, kThreads, smem, st>>>(ei, ej, ep, w, asg, n, n_gpus, lsb0, n_digits,
+                                                                       out);
   } else {
-    k_histogram<false><<<(unsigned)blocks, kThreads, 0, st>>>(ei, ej, ep, w, asg, n, n_gpus, lsb0,
-                                                               n_digits, out);
+    k_histogram_global<Idx><<<(unsigned)blocks, kThreads, 0, st>>>(ei, ej, ep, w, asg, n, n_gpus, lsb0, n_digits,
+                                                                     out);
   }
   NC_LAUNCH_CHECK();
   return NC_OK;
@@ -194,6 +239,18 @@ extern "C" int nc_traffic_histogram(const int64_t* edge_i, const int64_t* edge_j
                      n_digits, pg_limbs, (cudaStream_t)stream);
 }
 
+extern "C" int nc_traffic_histogram32(const int32_t* edge_i, const int32_t* edge_j, const double* edge_p,
+                                      const double* weights, const int32_t* assignment, int64_t n_edges,
+                                      int32_t n_gpus, int32_t lsb_exponent, int32_t n_digits,
+                                      unsigned long long* pg_limbs, void* stream) {
+  if (n_gpus < 1 || n_digits < 3 || !edge_i || !edge_j) {
+    nc_set_error("nc_traffic_histogram32: bad arguments (n_gpus=%d n_digits=%d)", n_gpus, n_digits);
+    return NC_E_ARG;
+  }
+  return launch_hist(edge_i, edge_j, edge_p, weights, assignment, n_edges, n_gpus, lsb_exponent, n_digits,
+                     pg_limbs, (cudaStream_t)stream);
+}
+
 extern "C" int nc_weight_histogram(const double* weights, const int64_t* assignment, int64_t n_neurons,
                                    int32_t n_gpus, int32_t lsb_exponent, int32_t n_digits,
                                    unsigned long long* wg_limbs, void* stream) {
@@ -202,6 +259,6 @@ extern "C" int nc_weight_histogram(const double* weights, const int64_t* assignm
     return NC_E_ARG;
   }
   // same kernel with one cell per GPU (cell = assignment[k]), binned_sums semantics
-  return launch_hist(nullptr, nullptr, nullptr, weights, assignment, n_neurons, n_gpus, lsb_exponent,
-                     n_digits, wg_limbs, (cudaStream_t)stream);
+  return launch_hist<int64_t>(nullptr, nullptr, nullptr, weights, assignment, n_neurons, n_gpus, lsb_exponent,
+                              n_digits, wg_limbs, (cudaStream_t)stream);
 }

@@ -130,6 +130,8 @@ class DistSimulator:
         self.g = group if group is not None else TorchGroup()
         self.rank = self.g.rank
         self.world = self.g.world
+        from .sim import _check_layouts
+        _check_layouts(net, delivery)
         lay = net.layout
         if lay.n_shards != self.world:
             raise ValueError(f"partition has {lay.n_shards} GPUs but {self.world} ranks are running")

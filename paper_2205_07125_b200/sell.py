@@ -111,6 +111,7 @@ class SellCSR:
     row_perm: object = None  # torch int32 [n_tiles*n_local]: CTA-local index of the row at position p of
                              # tile t (None = identity; see include/neurocomm_b200.h)
     cta_groups: int = 1      # CTAs the tiled placement was built for
+    has_pull: bool = True    # False: placeholders only (push-only network, event-driven engines)
 
     @property
     def n_entries(self) -> int:

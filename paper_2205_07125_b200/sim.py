@@ -277,9 +277,17 @@ class Network:
 
     @classmethod
     def generate(cls, spec: GeneratorSpec, layout: ShardLayout, *, device=None, inh_every: int = 5,
-                 shards=None, tile_words: int | None = None, bank_order: bool = True) -> "Network":
-        """Counter-based device generator (csrc/graphgen.cu); every shard regenerates the same graph."""
+                 shards=None, tile_words: int | None = None, bank_order: bool = True, pull: bool = True,
+                 push: bool = False) -> "Network":
+        """Counter-based device generator (csrc/graphgen.cu); every shard regenerates the same graph.
+
+        ``pull``: the J-SELL pull layout (fused / pull / binned delivery).  ``push``:
+        the push CSR of the event-driven engines, generated directly (without the
+        pull layout when ``pull`` is False: 4 B per synapse instead of 3.2 + 4 + the
+        build's transient 8)."""
         import torch
+        if not (pull or push):
+            raise ValueError("generate at least one of the pull and push layouts")
         if layout.n_neurons != spec.n_neurons:
             raise ValueError("layout and generator disagree on the neuron count")
         if not 1 <= spec.n_communities <= spec.n_neurons:
@@ -307,6 +315,19 @@ class Network:
         sms = sell.device_sms(dev)
         for h in own:
             n_local = layout.n_local(h)
+            if not pull:
+                csr = _push_only_csr(layout, h, dev)
+                g = _native.GraphGenC(
+                    n_neurons=spec.n_neurons, n_communities=spec.n_communities, shard=h, p_in=spec.p_in,
+                    p_out=spec.p_out, intra_lo=spec.intra_p_range[0], intra_hi=spec.intra_p_range[1],
+                    inter_lo=spec.inter_p_range[0], inter_hi=spec.inter_p_range[1],
+                    seed=int(spec.seed) & (2**64 - 1), owner=owner_d.data_ptr(), internal_id=internal_d.data_ptr(),
+                    local_base=int(layout.base[h]), inh_every=inh_every, n_local=n_local)
+                csr.dest = _generate_push(g, csr, layout, h, dev)
+                csr.n_real = int(csr._push_cache[0][-1].item())
+                out[h] = csr
+                nsyn += csr.n_real
+                continue
             T, TW, pglob = _tiles(layout, n_local, sms, tile_words)
             g = _native.GraphGenC(
                 n_neurons=spec.n_neurons, n_communities=spec.n_communities, shard=h, p_in=spec.p_in,
@@ -357,6 +378,8 @@ class Network:
                            row_perm=None if perm is None else sell.local_index(perm, sms).reshape(-1).contiguous(),
                            cta_groups=sms)
             csr.dest = _dest_masks(csr, layout, h, dev)
+            if push:
+                _generate_push(g, csr, layout, h, dev)
             out[h] = csr
             nsyn += n_real
         return cls(layout, out, dev, inh_every, n_synapses=nsyn, source="device generator")
@@ -381,6 +404,40 @@ class Network:
         if (inhibitory_mask(pre, self.inh_every) != inh).any():
             raise AssertionError("E/I slot split disagrees with the pre neuron types")
         return self.layout.members[shard][row], pre, q.astype(np.uint8)
+
+
+def _push_only_csr(layout: ShardLayout, h: int, dev) -> ShardCSR:
+    """A shard without the pull layout (event-driven engines only): one-tile
+    placeholders keep the descriptor valid; has_pull is False."""
+    import torch
+    csr = ShardCSR(torch.zeros(2, dtype=torch.int64, device=dev), torch.zeros(1, dtype=torch.int32, device=dev),
+                   torch.zeros(4, dtype=torch.int32, device=dev), 1, layout.n_words, layout.n_local(h), 0)
+    csr.has_pull = False
+    return csr
+
+
+def _generate_push(g, csr: ShardCSR, layout: ShardLayout, h: int, dev):
+    """Push CSR of shard h straight from the generator (nc_graphgen_push), cached on the
+    SellCSR like _push_csr's transpose; returns the destination masks (int32 [n_local])."""
+    import torch
+    L = _native.lib()
+    st = _native.stream_handle(dev)
+    n_pre = layout.n_words * 32
+    n_local = layout.n_local(h)
+    rowptr = torch.zeros(n_pre + 1, dtype=torch.int64, device=dev)
+    dest16 = torch.zeros(n_local + 2, dtype=torch.int16, device=dev)
+    _native.check(L.nc_graphgen_push(C.byref(g), 0, rowptr.data_ptr(), None, None, dest16.data_ptr(), st),
+                  "graphgen push count")
+    torch.cumsum(rowptr, 0, out=rowptr)
+    total = int(rowptr[-1].item())
+    ent = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+    fill = torch.zeros(n_pre, dtype=torch.int32, device=dev)
+    _native.check(L.nc_graphgen_push(C.byref(g), 1, rowptr.data_ptr(), fill.data_ptr(), ent.data_ptr(), None, st),
+                  "graphgen push fill")
+    torch.cuda.synchronize(dev)
+    del fill
+    csr._push_cache = (rowptr, ent)
+    return dest16[:n_local].to(torch.int32) & 0xFFFF
 
 
 def _tiles(layout: ShardLayout, n_local: int, sms: int, tile_words: int | None, partials_global: bool = False):
@@ -662,6 +719,12 @@ def _push_csr(csr: ShardCSR, lay: ShardLayout, h: int, dev):
     return rowptr, ent
 
 
+def _check_layouts(net: Network, delivery: str):
+    if delivery in ("fused", "pull", "binned") and not all(getattr(c, "has_pull", True)
+                                                           for c in net.shards.values()):
+        raise ValueError(f"delivery {delivery!r} needs the pull layout: Network.generate(..., pull=True)")
+
+
 class StepGraphs:
     """CUDA graphs of k consecutive steps, one per chunk length k, captured once.
 
@@ -723,6 +786,7 @@ class Simulator:
             raise ValueError(f"the {delivery} engine runs one shard per GPU; use distributed.DistSimulator")
         if set(net.shards) != set(range(net.layout.n_shards)):
             raise ValueError("the single-process simulator needs every shard of the layout")
+        _check_layouts(net, delivery)
         self.net = net
         self.lif = lif
         self.seed = seed

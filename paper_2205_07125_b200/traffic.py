@@ -78,6 +78,53 @@ def _n_digits(lsb: int, msb: int, n_terms: int) -> int:
     return (bits + 31) // 32 + 2
 
 
+def _exp_range(x):
+    """(floor(log2 min|x|), floor(log2 max|x|)) over the nonzero entries of a device
+    float64 tensor, or None if all are zero."""
+    import torch
+    a = x.abs()
+    lo, hi = torch.aminmax(a)
+    if float(hi) == 0.0:
+        return None
+    if float(lo) == 0.0:
+        lo = torch.where(a > 0, a, torch.full_like(a, float("inf"))).min()
+    return math.frexp(float(lo))[1] - 1, math.frexp(float(hi))[1] - 1
+
+
+_WINDOWS: dict = {}
+
+
+def contribution_window(ep, w):
+    """[lowest mantissa bit, highest bit] exponents bounding every contribution
+    (ep * w[i]) * w[j] (device int32[2], the layout nc_traffic_exponents writes).
+
+    From the columns' exponent ranges instead of a pass over the edges: with
+    e(x) = floor(log2 |x|), a product of two doubles rounded to nearest has
+    e in [e(a) + e(b), e(a) + e(b) + 2], so every nonzero term has its leading
+    bit at or below e_max(p) + 2 e_max(w) + 4 and its lowest mantissa bit at or
+    above max(-1074, e_min(p) + 2 e_min(w) - 52).  The window only has to
+    contain the terms (the sum is exact and rounded once), so a few spare bits
+    cost nothing but shared memory.  Cached per (ep, w) tensor pair."""
+    import torch
+    key = (ep.data_ptr(), ep.numel(), w.data_ptr(), w.numel())
+    hit = _WINDOWS.get(key)
+    if hit is None or hit[0]() is not ep or hit[1]() is not w:
+        rp, rw = _exp_range(ep), _exp_range(w)
+        if rp is None or rw is None:
+            win = (INT_MAX, INT_MIN)
+        else:
+            win = (max(-1074, rp[0] + 2 * rw[0] - 52), rp[1] + 2 * rw[1] + 4)
+        import weakref
+        try:
+            hit = (weakref.ref(ep), weakref.ref(w), win)
+            if len(_WINDOWS) > 64:
+                _WINDOWS.clear()
+            _WINDOWS[key] = hit
+        except TypeError:
+            hit = (lambda: ep, lambda: w, win)
+    return torch.tensor(hit[2], dtype=torch.int32, device=ep.device)
+
+
 def exact_bin_sums(values_dev, keys_dev, n_bins: int, *, pairs=None, stream=None, group=None):
     """Correctly rounded per-bin sums on the device.
 
@@ -106,8 +153,7 @@ def exact_bin_sums(values_dev, keys_dev, n_bins: int, *, pairs=None, stream=None
         ei, ej, ep = pairs
         n = int(ei.numel())
         if n:
-            _native.check(L.nc_traffic_exponents(ei.data_ptr(), ej.data_ptr(), ep.data_ptr(),
-                                                 values_dev.data_ptr(), n, mm.data_ptr(), st), "traffic exponents")
+            mm = contribution_window(ep, values_dev)
     n_local = n
     n_cells = n_bins * n_bins if pairs is not None else n_bins
     if group is not None:
@@ -129,9 +175,14 @@ def exact_bin_sums(values_dev, keys_dev, n_bins: int, *, pairs=None, stream=None
         if pairs is None:
             rc = L.nc_weight_histogram(values_dev.data_ptr(), keys_dev.data_ptr(), n_local, n_bins, lo, nd,
                                        limbs.data_ptr(), st)
+        elif ei.dtype == torch.int32:
+            asg32 = keys_dev.to(torch.int32)
+            rc = L.nc_traffic_histogram32(ei.data_ptr(), ej.data_ptr(), ep.data_ptr(), values_dev.data_ptr(),
+                                          asg32.data_ptr(), n_local, n_bins, lo, nd, limbs.data_ptr(), st)
         else:
             rc = L.nc_traffic_histogram(ei.data_ptr(), ej.data_ptr(), ep.data_ptr(), values_dev.data_ptr(),
-                                        keys_dev.data_ptr(), n_local, n_bins, lo, nd, limbs.data_ptr(), st)
+                                        keys_dev.to(torch.int64).data_ptr(), n_local, n_bins, lo, nd,
+                                        limbs.data_ptr(), st)
         _native.check(rc, "traffic histogram")
     if group is not None:   # exact: integer limbs (< 2^33 each after the kernel's carry flush)
         import torch.distributed as dist
@@ -163,7 +214,9 @@ def _device_graph(graph, dev):
     if hit is not None and hit[0]() is graph and hit[1] == key:
         return hit[2]
     up = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev)  # noqa: E731
-    val = (up(graph.weights, np.float64), up(graph.edge_i, np.int64), up(graph.edge_j, np.int64),
+    # int32 ids below 2^31 neurons: K5 streams 16 B per edge instead of 24
+    idx = np.int32 if graph.n_neurons < 2**31 else np.int64
+    val = (up(graph.weights, np.float64), up(graph.edge_i, idx), up(graph.edge_j, idx),
            up(graph.edge_p, np.float64))
     try:
         ref = weakref.ref(graph)

@@ -355,9 +355,10 @@ def test_config2_network_matches_oracle():
     dev = csr.syn.device
     # graph: per-row digests of the decoded device layout vs the oracle's CSR
     row, pre, qq, _ = sell.decode(csr)
+    lay = net.layout           # generate() reorders each shard's rows by degree
     gid_of_internal = torch.full((lay.n_words * 32,), -1, dtype=torch.int64, device=dev)
     gid_of_internal[: lay.n_local(0)] = torch.from_numpy(lay.members[0]).to(dev)
-    post = torch.from_numpy(net.layout.members[0]).to(dev)[row]
+    post = torch.from_numpy(lay.members[0]).to(dev)[row]
     hd = _row_hash(post, gid_of_internal[pre], qq, spec.n_neurons)
     del row, pre, qq, post, gid_of_internal
     rp = torch.from_numpy(rowptr).to(dev)
@@ -378,3 +379,33 @@ def test_config2_network_matches_oracle():
     np.testing.assert_array_equal(rep.raster, ref["raster"])
     np.testing.assert_array_equal(rep.v.view(np.uint32), ref["v"].view(np.uint32))
     np.testing.assert_array_equal(rep.i_syn.view(np.uint32), ref["i"].view(np.uint32))
+
+
+def test_push_only_generator_matches_oracle():
+    """Network.generate(pull=False, push=True): the push CSR and destination masks straight
+    from the generator (nc_graphgen_push) drive the event-driven engines to the oracle's
+    rasters -- 2 shards with the local exchange (push delivery) and 1 shard (persistent)."""
+    spec = S.GeneratorSpec(12_000, 4, 0.02, 0.002, seed=7)
+    lif = S.LifParams()
+    for n_shards, delivery in ((2, "push"), (1, "persistent"), (1, "push")):
+        lay = S.ShardLayout.blocks(spec.n_neurons, n_shards)
+        full = S.Network.generate(spec, lay)                         # pull layout (oracle CSR source)
+        lean = S.Network.generate(spec, lay, pull=False, push=True)
+        assert lean.n_synapses == full.n_synapses
+        with pytest.raises(ValueError, match="pull layout"):
+            S.Simulator(lean, lif, 4, None, delivery="fused")
+        posts, pres, qs = [], [], []
+        for h in range(n_shards):
+            post, pre, q = full.host_csr(h)
+            posts.append(post), pres.append(pre), qs.append(q)
+        post, pre, q = np.concatenate(posts), np.concatenate(pres), np.concatenate(qs)
+        sel = pre > post
+        rp, col, qc = c_oracle.symmetric_csr(spec.n_neurons, post[sel], pre[sel], q[sel])
+        nh = S.ExchangePlan(n_shards, None).next_hop
+        ref = c_oracle.simulate_csr(rp, col, qc, lay.owner, n_shards, nh, lif.constants(4), 40, threads=8)
+        rep = S.Simulator(lean, lif, 4, None, delivery=delivery, record_raster_steps=40,
+                          per_step_counts=True).run(40)
+        assert rep.spikes > 0
+        np.testing.assert_array_equal(rep.raster, ref["raster"])
+        np.testing.assert_array_equal(rep.deliv_ids, ref["deliv"])
+        np.testing.assert_array_equal(rep.v.view(np.uint32), ref["v"].view(np.uint32))
