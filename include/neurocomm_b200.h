@@ -430,6 +430,18 @@ int nc_graphgen_count(const nc_graphgen_t* g, int32_t n_tiles, int32_t tile_word
 int nc_graphgen_fill(const nc_graphgen_t* g, int32_t n_tiles, int32_t tile_words, const int64_t* slice_ptr,
                      const uint32_t* row_meta, const int32_t* pos_of, int32_t* lower_fill, uint32_t* syn,
                      void* stream);
+/* The pull-layout passes over an explicit edge list instead of the generator
+ * (simulate() on a host NeuronGraph, model.py:53-92): edge k = (edge_i[k],
+ * edge_j[k]) with weight units q[k] (= ceil(32 p), 1..32), one synapse each
+ * way.  g supplies owner / internal_id / shard / local_base / n_local /
+ * inh_every (n_neurons bounds the ids; the SBM fields are ignored).
+ * nc_edges_count: seg_len[(row*n_tiles + tile)*2 + inh] += 1 (zeroed);
+ * nc_edges_fill: as nc_graphgen_fill. */
+int nc_edges_count(const nc_graphgen_t* g, const int32_t* edge_i, const int32_t* edge_j, int64_t n_edges,
+                   int32_t n_tiles, int32_t tile_words, int32_t* seg_len, void* stream);
+int nc_edges_fill(const nc_graphgen_t* g, const int32_t* edge_i, const int32_t* edge_j, const uint8_t* q,
+                  int64_t n_edges, int32_t n_tiles, int32_t tile_words, const int64_t* slice_ptr,
+                  const uint32_t* row_meta, const int32_t* pos_of, int32_t* fill, uint32_t* syn, void* stream);
 /* Push synapses (nc_shard_t push_rowptr / push_syn format) straight from the
  * generator, without a pull layout.  Phase 0: push_rowptr[pre + 1] += entries
  * of pre (int64 [n_words*32 + 1], zeroed) and dest_mask[r] |= shards hosting a

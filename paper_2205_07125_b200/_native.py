@@ -118,6 +118,10 @@ _SIGS = {
                                    c_void_p, c_void_p]),
     "nc_graphgen_degrees": (c_int32, [C.POINTER(GraphGenC), c_void_p, c_void_p]),
     "nc_graphgen_push": (c_int32, [C.POINTER(GraphGenC), c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "nc_edges_count": (c_int32, [C.POINTER(GraphGenC), c_void_p, c_void_p, c_int64, c_int32, c_int32, c_void_p,
+                                 c_void_p]),
+    "nc_edges_fill": (c_int32, [C.POINTER(GraphGenC), c_void_p, c_void_p, c_void_p, c_int64, c_int32, c_int32,
+                                c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "nc_sell_fill_pads": (c_int32, [c_void_p, c_int64, c_int32, c_int32, c_void_p, c_void_p]),
     "nc_dest_mask_from_csr": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_int32, c_void_p, c_int32,
                                         c_void_p, c_int32, c_int32, c_void_p, c_void_p]),

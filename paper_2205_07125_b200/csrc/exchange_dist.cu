@@ -192,6 +192,18 @@ __global__ void k_stamp(unsigned long long* dst, const int32_t* step, int32_t ma
 }
 }  // namespace
 
+int ncx_load_exchange_kernels(void) {
+  cudaFuncAttributes fa;
+  NC_CUDA_TRY(cudaFuncGetAttributes(&fa, k_seal));
+  NC_CUDA_TRY(cudaFuncGetAttributes(&fa, k_scatter));
+  NC_CUDA_TRY(cudaFuncGetAttributes(&fa, k_reset_fwd));
+  NC_CUDA_TRY(cudaFuncGetAttributes(&fa, k_p2p));
+  NC_CUDA_TRY(cudaFuncGetAttributes(&fa, k_p2p_tail));
+  NC_CUDA_TRY(cudaFuncGetAttributes(&fa, k_reset));
+  NC_CUDA_TRY(cudaFuncGetAttributes(&fa, k_stamp));
+  return NC_OK;
+}
+
 extern "C" int nc_stamp(unsigned long long* dst, const int32_t* step, int32_t max_steps, void* stream) {
   k_stamp<<<1, 1, 0, (cudaStream_t)stream>>>(dst, step, max_steps);
   NC_LAUNCH_CHECK();

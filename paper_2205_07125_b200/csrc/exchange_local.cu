@@ -139,6 +139,14 @@ __global__ void k_reset_fwd(int32_t* fwd_count, int n2) {
 
 }  // namespace
 
+int ncx_load_local_kernels(void) {
+  cudaFuncAttributes fa;
+  NC_CUDA_TRY(cudaFuncGetAttributes(&fa, k_phase1));
+  NC_CUDA_TRY(cudaFuncGetAttributes(&fa, k_phase2));
+  NC_CUDA_TRY(cudaFuncGetAttributes(&fa, k_reset_fwd));
+  return NC_OK;
+}
+
 extern "C" int nc_exchange_local(const nc_shard_t* shards, int32_t n_shards, const uint16_t* dest_mask,
                                  const uint16_t* fwd_table, uint32_t* fwd_ids, int32_t* fwd_count,
                                  int64_t fwd_cap, long long* hop_ids, long long* deliv_ids,

@@ -206,6 +206,49 @@ __global__ void k_fill(const nc_graphgen_t g, int32_t T, int32_t TW, const int64
   }
 }
 
+// The same two passes over an explicit edge list (a host NeuronGraph uploaded
+// as int32 (i, j) + uint8 q columns, simulate()'s path): every edge (i, j) is
+// one synapse each way, so post row j gets pre i and row i gets pre j.  Counts
+// go to one array with atomics (any order: delivery sums integers).
+__global__ void k_edges_count(const nc_graphgen_t g, const int32_t* __restrict__ ei, const int32_t* __restrict__ ej,
+                              int64_t n_edges, int32_t T, int32_t TW, int32_t* seg_len) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n_edges;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = ei[k], j = ej[k];
+    const bool im = g.owner[i] == g.shard, jm = g.owner[j] == g.shard;
+    if (!im && !jm) continue;
+    const uint32_t iid = (uint32_t)g.internal_id[i], jid = (uint32_t)g.internal_id[j];
+    if (im) atomicAdd(seg_len + seg_index((int64_t)iid - g.local_base, T, TW, jid, is_inh(g, j)), 1);
+    if (jm) atomicAdd(seg_len + seg_index((int64_t)jid - g.local_base, T, TW, iid, is_inh(g, i)), 1);
+  }
+}
+
+__global__ void k_edges_fill(const nc_graphgen_t g, const int32_t* __restrict__ ei, const int32_t* __restrict__ ej,
+                             const uint8_t* __restrict__ qe, int64_t n_edges, int32_t T, int32_t TW,
+                             const int64_t* slice_ptr, const uint32_t* row_meta, const int32_t* pos_of, int32_t* fill,
+                             uint32_t* syn) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n_edges;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = ei[k], j = ej[k];
+    const bool im = g.owner[i] == g.shard, jm = g.owner[j] == g.shard;
+    if (!im && !jm) continue;
+    const uint32_t q = qe[k];
+    const uint32_t iid = (uint32_t)g.internal_id[i], jid = (uint32_t)g.internal_id[j];
+    if (im) {
+      const int64_t ri = (int64_t)iid - g.local_base;
+      const int64_t seg = seg_index(ri, T, TW, jid, is_inh(g, j));
+      const int32_t c = atomicAdd(fill + seg, 1);
+      syn[sell_pos(slice_ptr, row_meta, pos_of, T, g.n_local, ri, seg, c)] = pack(jid - tile_base(jid, TW), q);
+    }
+    if (jm) {
+      const int64_t rj = (int64_t)jid - g.local_base;
+      const int64_t seg = seg_index(rj, T, TW, iid, is_inh(g, i));
+      const int32_t c = atomicAdd(fill + seg, 1);
+      syn[sell_pos(slice_ptr, row_meta, pos_of, T, g.n_local, rj, seg, c)] = pack(iid - tile_base(iid, TW), q);
+    }
+  }
+}
+
 // Push synapses straight from the generator, for the event-driven engines (no
 // pull layout needed: config 5 over 2 GPUs holds 2.5e10 synapses per GPU, which
 // fit as 4-byte push entries but not as pull layout + transpose).  Rows are
@@ -452,6 +495,37 @@ extern "C" int nc_graphgen_push(const nc_graphgen_t* g, int32_t phase, int64_t* 
   }
   k_push_gen<<<grid_for(g->n_neurons, 128), 128, 0, (cudaStream_t)stream>>>(
       *g, phase, reinterpret_cast<unsigned long long*>(push_rowptr), push_rowptr, push_fill, push_syn, dest_mask);
+  NC_LAUNCH_CHECK();
+  return NC_OK;
+}
+
+extern "C" int nc_edges_count(const nc_graphgen_t* g, const int32_t* edge_i, const int32_t* edge_j, int64_t n_edges,
+                              int32_t n_tiles, int32_t tile_words, int32_t* seg_len, void* stream) {
+  if (!g || !g->owner || !g->internal_id || n_edges < 0 || (n_edges && (!edge_i || !edge_j)) || n_tiles < 1 ||
+      tile_words < 1 || !seg_len) {
+    nc_set_error("nc_edges_count: bad arguments");
+    return NC_E_ARG;
+  }
+  if (n_edges == 0) return NC_OK;
+  k_edges_count<<<grid_for(n_edges, 256), 256, 0, (cudaStream_t)stream>>>(*g, edge_i, edge_j, n_edges, n_tiles,
+                                                                           tile_words, seg_len);
+  NC_LAUNCH_CHECK();
+  return NC_OK;
+}
+
+extern "C" int nc_edges_fill(const nc_graphgen_t* g, const int32_t* edge_i, const int32_t* edge_j, const uint8_t* q,
+                             int64_t n_edges, int32_t n_tiles, int32_t tile_words, const int64_t* slice_ptr,
+                             const uint32_t* row_meta, const int32_t* pos_of, int32_t* fill, uint32_t* syn,
+                             void* stream) {
+  if (!g || !g->owner || !g->internal_id || n_edges < 0 || (n_edges && (!edge_i || !edge_j || !q)) ||
+      n_tiles < 1 || tile_words < 1 || !slice_ptr || !row_meta || !fill || !syn) {
+    nc_set_error("nc_edges_fill: bad arguments");
+    return NC_E_ARG;
+  }
+  if (n_edges == 0) return NC_OK;
+  k_edges_fill<<<grid_for(n_edges, 256), 256, 0, (cudaStream_t)stream>>>(*g, edge_i, edge_j, q, n_edges, n_tiles,
+                                                                          tile_words, slice_ptr, row_meta, pos_of,
+                                                                          fill, syn);
   NC_LAUNCH_CHECK();
   return NC_OK;
 }

@@ -19,3 +19,9 @@ void nc_set_error(const char* fmt, ...);
   } while (0)
 #define NC_LAUNCH_CHECK() NC_CUDA_TRY(cudaGetLastError())
 #endif
+
+/* Force-load a module's kernels (cudaFuncGetAttributes) -- called by nc_sim_prepare,
+ * see there.  One per translation unit on the step path. */
+int ncx_load_exchange_kernels(void);
+int ncx_load_local_kernels(void);
+int ncx_load_persistent_kernels(void);

@@ -90,6 +90,12 @@ static unsigned long long* g_phase_stamps = nullptr;
 
 // Diagnostics: record (start, after push, after LIF, after exchange) globaltimer
 // stamps of the first 64 steps of the next persistent launches into dst[64][4].
+int ncx_load_persistent_kernels(void) {
+  cudaFuncAttributes fa;
+  NC_CUDA_TRY(cudaFuncGetAttributes(&fa, k_persistent));
+  return NC_OK;
+}
+
 extern "C" int nc_persistent_phase_stamps(unsigned long long* dst) {
   g_phase_stamps = dst;
   return NC_OK;

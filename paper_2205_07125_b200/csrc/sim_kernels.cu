@@ -378,6 +378,18 @@ extern "C" int nc_sim_prepare(void) {
   if (int e = opt_in_smem(k_step_fused<true, true, true, true>, optin)) return e;
   if (int e = opt_in_smem(k_step_fused<true, true, false, true>, optin)) return e;
   if (int e = opt_in_smem(k_step_binned, optin)) return e;
+  // Load every kernel of the step path now.  With CUDA's lazy module loading the
+  // first launch of a kernel loads it, and that load waits for the device: a
+  // first launch queued behind a spinning exchange kernel (k_p2p waits for its
+  // peers) would stall the host thread until the watchdog ends the spin.
+  cudaFuncAttributes fa;
+  NC_CUDA_TRY(cudaFuncGetAttributes(&fa, k_lif_update));
+  NC_CUDA_TRY(cudaFuncGetAttributes(&fa, k_deliver_push));
+  NC_CUDA_TRY(cudaFuncGetAttributes(&fa, k_end_step));
+  NC_CUDA_TRY(cudaFuncGetAttributes(&fa, k_init));
+  if (int e = ncx_load_exchange_kernels()) return e;
+  if (int e = ncx_load_local_kernels()) return e;
+  if (int e = ncx_load_persistent_kernels()) return e;
   g_prepared = true;
   return NC_OK;
 }

@@ -130,20 +130,59 @@ k_histogram_smem(const Idx* __restrict__ ei, const Idx* __restrict__ ej, const d
   for (int k = threadIdx.x; k < kCopies * per_copy; k += blockDim.x) sw[k] = 0u;
   __syncthreads();
   unsigned int* mine = sw + (threadIdx.x & (kCopies - 1)) * per_copy;
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
-    double x;
-    int cell;
-    edge_term(ei, ej, ep, w, asg, k, n_gpus, &x, &cell);
-    const Decomposed d = decompose(x);
-    if (d.mant == 0) continue;
-    const int s = d.lsb - lsb0;  // >= 0 by construction of lsb0; digits k..k+2 < n_digits
-    const int kd = s >> 5, o = s & 31;
-    const unsigned long long lo = d.mant << o;
-    const unsigned long long hi = o ? (d.mant >> (64 - o)) : 0ull;
-    unsigned int* c = mine + (cell * n_digits + kd) * 2;
-    if (kd < n_digits) add32c(c, (unsigned int)lo);             // digits past the window are dropped,
-    if (kd + 1 < n_digits) add32c(c + 2, (unsigned int)(lo >> 32));   // as in add_fixed (callers size it)
-    if (kd + 2 < n_digits) add32c(c + 4, (unsigned int)hi);
+  // kUnroll edges per thread and iteration, every load issued before the first use:
+  // the gathers of w / assignment (L2-resident) then overlap instead of serialising
+  constexpr int kUnroll = 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k0 < n; k0 += stride * kUnroll) {
+    double x[kUnroll];
+    int cell[kUnroll];
+    if (ei) {
+      int64_t i[kUnroll], j[kUnroll];
+      double pe[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int64_t k = k0 + u * stride;
+        const bool ok = k < n;
+        i[u] = ok ? (int64_t)__ldcs(ei + k) : 0;
+        j[u] = ok ? (int64_t)__ldcs(ej + k) : 0;
+        pe[u] = ok ? __ldcs(ep + k) : 0.0;
+      }
+      double wi[kUnroll], wj[kUnroll];
+      int64_t ai[kUnroll], aj[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        wi[u] = __ldg(w + i[u]);
+        wj[u] = __ldg(w + j[u]);
+        ai[u] = (int64_t)__ldg(asg + i[u]);
+        aj[u] = (int64_t)__ldg(asg + j[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        x[u] = contrib(pe[u], wi[u], wj[u]);   // p = 0 for the tail: nothing added
+        cell[u] = cell_index(ai[u], aj[u], n_gpus);
+      }
+    } else {  // per-GPU weight totals (binned_sums over assignment)
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int64_t k = k0 + u * stride;
+        x[u] = k < n ? w[k] : 0.0;
+        cell[u] = k < n ? (int)asg[k] : 0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const Decomposed d = decompose(x[u]);
+      if (d.mant == 0) continue;
+      const int s = d.lsb - lsb0;  // >= 0 by construction of lsb0
+      const int kd = s >> 5, o = s & 31;
+      const unsigned long long lo = d.mant << o;
+      const unsigned long long hi = o ? (d.mant >> (64 - o)) : 0ull;
+      unsigned int* c = mine + (cell[u] * n_digits + kd) * 2;
+      if (kd < n_digits) add32c(c, (unsigned int)lo);             // digits past the window are dropped,
+      if (kd + 1 < n_digits) add32c(c + 2, (unsigned int)(lo >> 32));   // as in add_fixed (callers size it)
+      if (kd + 2 < n_digits) add32c(c + 4, (unsigned int)hi);
+    }
   }
   __syncthreads();
   // one thread per cell: sum the copies into 64-bit digits, normalise, add to global

@@ -250,9 +250,20 @@ class Network:
     # ------------------------------------------------------------ builders
     @classmethod
     def from_graph(cls, graph: NeuronGraph, layout: ShardLayout, *, device=None, inh_every: int = 5,
-                   shards=None, tile_words: int | None = None, partials_global: bool = False) -> "Network":
+                   shards=None, tile_words: int | None = None, partials_global: bool = False,
+                   bank_order: bool = True, builder: str = "device") -> "Network":
+        """Pull layouts of a host NeuronGraph (model.py:53-92).  ``builder="device"``:
+        the edge columns are uploaded once (int32 ids + uint8 weight units) and the
+        J-SELL layout is built on the GPU by the generator's passes (nc_edges_count /
+        nc_edges_fill): 1e9 synapses in seconds.  ``"host"``: numpy (sell.host_build),
+        kept as an independent builder for the tests."""
         import torch
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        if builder == "device":
+            return cls._from_graph_device(graph, layout, dev, inh_every, shards, tile_words, partials_global,
+                                          bank_order)
+        if builder != "host":
+            raise ValueError(f"builder must be 'device' or 'host', got {builder!r}")
         deg = np.bincount(graph.edge_i, minlength=graph.n_neurons) + np.bincount(graph.edge_j,
                                                                                minlength=graph.n_neurons)
         layout = layout.reordered(deg)
@@ -274,6 +285,41 @@ class Network:
             out[h] = csr
             nsyn += n_real
         return cls(layout, out, dev, inh_every, n_synapses=nsyn, source="host graph")
+
+    @classmethod
+    def _from_graph_device(cls, graph, layout, dev, inh_every, shards, tile_words, partials_global, bank_order):
+        import torch
+        if layout.n_neurons != graph.n_neurons:
+            raise ValueError("layout and graph disagree on the neuron count")
+        L = _native.lib()
+        st = _native.stream_handle(dev)
+        ei, ej, qd = upload_edges(graph, dev)
+        n = int(ei.numel())
+        deg = torch.bincount(ei, minlength=graph.n_neurons) + torch.bincount(ej, minlength=graph.n_neurons)
+        layout = layout.reordered(deg.cpu().numpy())
+        del deg
+        owner_d = torch.from_numpy(layout.owner).to(dev)
+        internal_d = torch.from_numpy(layout.internal_id).to(dev)
+        own = range(layout.n_shards) if shards is None else shards
+        sms = sell.device_sms(dev)
+        out = {}
+        nsyn = 0
+        for h in own:
+            n_local = layout.n_local(h)
+            g = _native.GraphGenC(n_neurons=graph.n_neurons, n_communities=1, shard=h, owner=owner_d.data_ptr(),
+                                  internal_id=internal_d.data_ptr(), local_base=int(layout.base[h]),
+                                  inh_every=inh_every, n_local=n_local)
+            count = lambda T, TW, lo, up, g=g: L.nc_edges_count(C.byref(g), ei.data_ptr(), ej.data_ptr(),  # noqa
+                                                               n, T, TW, lo.data_ptr(), st)
+            fill = lambda T, TW, ptr, meta, pos, fl, syn, g=g: L.nc_edges_fill(  # noqa: E731
+                C.byref(g), ei.data_ptr(), ej.data_ptr(), qd.data_ptr(), n, T, TW, ptr.data_ptr(), meta.data_ptr(),
+                None if pos is None else pos.data_ptr(), fl.data_ptr(), syn.data_ptr(), st)
+            csr, n_real = _build_pull_shard(layout, h, dev, sms, tile_words, partials_global, bank_order, count,
+                                            fill)
+            csr.dest = _dest_masks(csr, layout, h, dev)
+            out[h] = csr
+            nsyn += n_real
+        return cls(layout, out, dev, inh_every, n_synapses=nsyn, source="host graph (device build)")
 
     @classmethod
     def generate(cls, spec: GeneratorSpec, layout: ShardLayout, *, device=None, inh_every: int = 5,
@@ -328,55 +374,18 @@ class Network:
                 out[h] = csr
                 nsyn += csr.n_real
                 continue
-            T, TW, pglob = _tiles(layout, n_local, sms, tile_words)
             g = _native.GraphGenC(
                 n_neurons=spec.n_neurons, n_communities=spec.n_communities, shard=h, p_in=spec.p_in,
                 p_out=spec.p_out, intra_lo=spec.intra_p_range[0], intra_hi=spec.intra_p_range[1],
                 inter_lo=spec.inter_p_range[0], inter_hi=spec.inter_p_range[1],
                 seed=int(spec.seed) & (2**64 - 1), owner=owner_d.data_ptr(), internal_id=internal_d.data_ptr(),
                 local_base=int(layout.base[h]), inh_every=inh_every, n_local=n_local)
-            n_seg = max(n_local * T * 2, 1)
-            lower = torch.zeros(n_seg, dtype=torch.int32, device=dev)
-            upper = torch.zeros(n_seg, dtype=torch.int32, device=dev)
-            _native.check(L.nc_graphgen_count(C.byref(g), T, TW, lower.data_ptr(), upper.data_ptr(), st),
-                          "graphgen count")
-            counts = (lower + upper)[: n_local * T * 2].to(torch.int64)
-            perm, pos_of = sell.tile_placement(sell.row_slots(counts, n_local, T), n_local, T, sms)
-            ptr, meta = sell.layout_from_counts(counts, n_local, T, perm)
-            total = int(ptr[-1].item())
-            syn = torch.zeros(max(total * sell.SLOT_ENTRIES, 4), dtype=torch.int32, device=dev)   # unpacked
-            _native.check(L.nc_sell_fill_pads(ptr.data_ptr(), ptr.numel() - 1, T, TW, syn.data_ptr(), st),
-                          "sell pads")
-            lower.zero_()
-            pos_of = None if pos_of is None else pos_of.contiguous()
-            _native.check(L.nc_graphgen_fill(C.byref(g), T, TW, ptr.data_ptr(), meta.data_ptr(),
-                                             None if pos_of is None else pos_of.data_ptr(),
-                                             lower.data_ptr(), syn.data_ptr(), st), "graphgen fill")
-            n_real = int(counts.sum().item())
-            del upper, counts, lower
-            if bank_order:   # spread each lookup instruction's 32 lanes over the 32 banks (config 2,
-                # packed slots: shared wavefronts 110 M -> 60 M, kernel 1.3 % faster)
-                src = syn.clone()
-                _native.check(L.nc_sell_bank_order(ptr.data_ptr(), meta.data_ptr(), T, n_local, src.data_ptr(),
-                                                   syn.data_ptr(), st), "bank order")
-                torch.cuda.synchronize(dev)
-                del src
-            # 5 entries per slot -> 16-byte slots of 25-bit fields
-            packed = torch.empty(max(total * 4, 4), dtype=torch.int32, device=dev)
-            _native.check(L.nc_sell_pack(syn.data_ptr(), total, packed.data_ptr(), st), "sell pack")
-            torch.cuda.synchronize(dev)
-            del syn
-            syn = packed
-            # padded SELL-32 -> J-SELL-32 (drops the padding of every block to its longest row)
-            jptr = sell.jagged_ptr(meta, n_local, T)
-            jsyn = torch.empty(max(int(jptr[-1].item()) * 4, 4), dtype=torch.int32, device=dev)
-            _native.check(L.nc_sell_repack(ptr.data_ptr(), jptr.data_ptr(), meta.data_ptr(), T, n_local,
-                                           syn.data_ptr(), jsyn.data_ptr(), 1, st), "sell repack")
-            torch.cuda.synchronize(dev)
-            del syn, ptr, pos_of
-            csr = ShardCSR(jptr, meta, jsyn, T, TW, n_local, n_real, partials_global=pglob,
-                           row_perm=None if perm is None else sell.local_index(perm, sms).reshape(-1).contiguous(),
-                           cta_groups=sms)
+            count = lambda T, TW, lo, up, g=g: L.nc_graphgen_count(C.byref(g), T, TW, lo.data_ptr(),  # noqa: E731
+                                                                  up.data_ptr(), st)
+            fill = lambda T, TW, ptr, meta, pos, fl, syn, g=g: L.nc_graphgen_fill(  # noqa: E731
+                C.byref(g), T, TW, ptr.data_ptr(), meta.data_ptr(), None if pos is None else pos.data_ptr(),
+                fl.data_ptr(), syn.data_ptr(), st)
+            csr, n_real = _build_pull_shard(layout, h, dev, sms, tile_words, False, bank_order, count, fill)
             csr.dest = _dest_masks(csr, layout, h, dev)
             if push:
                 _generate_push(g, csr, layout, h, dev)
@@ -404,6 +413,82 @@ class Network:
         if (inhibitory_mask(pre, self.inh_every) != inh).any():
             raise AssertionError("E/I slot split disagrees with the pre neuron types")
         return self.layout.members[shard][row], pre, q.astype(np.uint8)
+
+
+def upload_edges(graph: NeuronGraph, dev, chunk: int = 1 << 26):
+    """Edge columns of a NeuronGraph on the device as int32 ids and uint8 weight units
+    q = ceil(32 p) (q_from_p), converted chunk by chunk on the device."""
+    import torch
+    m = int(graph.n_neurons)
+    if m >= 2**31:
+        raise ValueError("at most 2^31 - 1 neurons")
+    n = int(graph.edge_i.size)
+    ei = torch.empty(n, dtype=torch.int32, device=dev)
+    ej = torch.empty(n, dtype=torch.int32, device=dev)
+    qd = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+    for a in range(0, n, chunk):
+        b = min(n, a + chunk)
+        ci = torch.from_numpy(np.ascontiguousarray(graph.edge_i[a:b])).to(dev)
+        cj = torch.from_numpy(np.ascontiguousarray(graph.edge_j[a:b])).to(dev)
+        if ci.numel() and (int(torch.minimum(ci.min(), cj.min())) < 0 or int(torch.maximum(ci.max(), cj.max())) >= m):
+            raise ValueError(f"edge endpoints outside [0, {m})")
+        ei[a:b] = ci
+        ej[a:b] = cj
+        p = torch.from_numpy(np.ascontiguousarray(graph.edge_p[a:b], dtype=np.float64)).to(dev)
+        qd[a:b] = torch.ceil(p * Q_LEVELS).clamp_(1, Q_LEVELS).to(torch.uint8)
+    return ei, ej, qd[:n]
+
+
+def _build_pull_shard(layout: ShardLayout, h: int, dev, sms: int, tile_words, partials_global: bool,
+                      bank_order: bool, count, fill):
+    """J-SELL-32 pull layout of shard h on the device from an edge source (the
+    generator or an uploaded edge list): count entries per (row, tile, sign)
+    segment -> tile placement and block starts -> fill the unpacked padded SELL
+    -> bank order -> pack 5 fields per 16-byte slot -> drop the padding (J-SELL)."""
+    import torch
+    L = _native.lib()
+    st = _native.stream_handle(dev)
+    n_local = layout.n_local(h)
+    T, TW, pglob = _tiles(layout, n_local, sms, tile_words, partials_global)
+    n_seg = max(n_local * T * 2, 1)
+    lower = torch.zeros(n_seg, dtype=torch.int32, device=dev)
+    upper = torch.zeros(n_seg, dtype=torch.int32, device=dev)
+    _native.check(count(T, TW, lower, upper), "pull layout count")
+    counts = (lower + upper)[: n_local * T * 2].to(torch.int64)
+    perm, pos_of = sell.tile_placement(sell.row_slots(counts, n_local, T), n_local, T, sms)
+    ptr, meta = sell.layout_from_counts(counts, n_local, T, perm)
+    total = int(ptr[-1].item())
+    syn = torch.zeros(max(total * sell.SLOT_ENTRIES, 4), dtype=torch.int32, device=dev)   # unpacked
+    _native.check(L.nc_sell_fill_pads(ptr.data_ptr(), ptr.numel() - 1, T, TW, syn.data_ptr(), st), "sell pads")
+    lower.zero_()
+    pos_of = None if pos_of is None else pos_of.contiguous()
+    _native.check(fill(T, TW, ptr, meta, pos_of, lower, syn), "pull layout fill")
+    n_real = int(counts.sum().item())
+    del upper, counts, lower
+    if bank_order:   # spread each lookup instruction's 32 lanes over the 32 banks (config 2,
+        # packed slots: shared wavefronts 110 M -> 60 M, kernel 1.3 % faster)
+        src = syn.clone()
+        _native.check(L.nc_sell_bank_order(ptr.data_ptr(), meta.data_ptr(), T, n_local, src.data_ptr(),
+                                           syn.data_ptr(), st), "bank order")
+        torch.cuda.synchronize(dev)
+        del src
+    # 5 entries per slot -> 16-byte slots of 25-bit fields
+    packed = torch.empty(max(total * 4, 4), dtype=torch.int32, device=dev)
+    _native.check(L.nc_sell_pack(syn.data_ptr(), total, packed.data_ptr(), st), "sell pack")
+    torch.cuda.synchronize(dev)
+    del syn
+    syn = packed
+    # padded SELL-32 -> J-SELL-32 (drops the padding of every block to its longest row)
+    jptr = sell.jagged_ptr(meta, n_local, T)
+    jsyn = torch.empty(max(int(jptr[-1].item()) * 4, 4), dtype=torch.int32, device=dev)
+    _native.check(L.nc_sell_repack(ptr.data_ptr(), jptr.data_ptr(), meta.data_ptr(), T, n_local,
+                                   syn.data_ptr(), jsyn.data_ptr(), 1, st), "sell repack")
+    torch.cuda.synchronize(dev)
+    del syn, ptr, pos_of
+    csr = ShardCSR(jptr, meta, jsyn, T, TW, n_local, n_real, partials_global=pglob,
+                   row_perm=None if perm is None else sell.local_index(perm, sms).reshape(-1).contiguous(),
+                   cta_groups=sms)
+    return csr, n_real
 
 
 def _push_only_csr(layout: ShardLayout, h: int, dev) -> ShardCSR:

@@ -409,3 +409,57 @@ def test_push_only_generator_matches_oracle():
         np.testing.assert_array_equal(rep.raster, ref["raster"])
         np.testing.assert_array_equal(rep.deliv_ids, ref["deliv"])
         np.testing.assert_array_equal(rep.v.view(np.uint32), ref["v"].view(np.uint32))
+
+
+@pytest.mark.parametrize("tile_words", [None, 64])
+def test_device_edge_builder_equals_host_builder(tile_words):
+    """Network.from_graph builds the J-SELL layout on the GPU from the uploaded edge list
+    (nc_edges_count / nc_edges_fill); the numpy builder (sell.host_build) is the
+    independent check: same synapses per shard, same rasters and counters."""
+    g = cfg1(2)
+    pm = nc.partition_greedy(g, 3)
+    lay = S.ShardLayout.from_assignment(pm.assignment, 3)
+    dev_net = S.Network.from_graph(g, lay, tile_words=tile_words)
+    host_net = S.Network.from_graph(g, lay, tile_words=tile_words, builder="host")
+    assert dev_net.source.endswith("(device build)")
+    for h in range(3):
+        a = np.stack(dev_net.host_csr(h)).T
+        b = np.stack(host_net.host_csr(h)).T
+        np.testing.assert_array_equal(a[np.lexsort(a.T[::-1])], b[np.lexsort(b.T[::-1])])
+    lif = S.LifParams()
+    ra = S.Simulator(dev_net, lif, 2, None, record_raster_steps=30, per_step_counts=True).run(30)
+    rb = S.Simulator(host_net, lif, 2, None, record_raster_steps=30, per_step_counts=True).run(30)
+    np.testing.assert_array_equal(ra.raster, rb.raster)
+    np.testing.assert_array_equal(ra.hop_ids, rb.hop_ids)
+    np.testing.assert_array_equal(ra.v.view(np.uint32), rb.v.view(np.uint32))
+
+
+def graph_from_csr(rowptr, col, q):
+    """NeuronGraph of a symmetric CSR (upper triangle), p = q / 32 (so q_from_p(p) == q)."""
+    m = rowptr.size - 1
+    rows = np.repeat(np.arange(m, dtype=np.int32), np.diff(rowptr))
+    up = col > rows
+    ei = rows[up].astype(np.int64)
+    del rows
+    ej = col[up].astype(np.int64)
+    ep = q[up].astype(np.float64) / 32.0
+    return nc.NeuronGraph(m, np.ones(m), ei, ej, ep)
+
+
+def test_simulate_api_at_config2_scale():
+    """simulate(graph, pm, rt, steps) -- the drop-in API -- on a 1e9-synapse host
+    NeuronGraph (BASELINE config 2's network, from the oracle's CPU generator):
+    device edge upload + layout build + 10 steps, bit-equal to the oracle."""
+    import os
+    threads = os.cpu_count() or 1
+    rowptr, col, q = c_oracle.generate_random_csr(1_000_000, 1000.0, 1, threads=threads)
+    g = graph_from_csr(rowptr, col, q)
+    assert 2 * g.n_edges == int(rowptr[-1]) > 9.9e8
+    pm = nc.PartitionMap(1, np.zeros(g.n_neurons, dtype=np.int64))
+    lif = S.LifParams()
+    rep = nc.simulate(g, pm, None, 10, lif, seed=1)
+    ref = c_oracle.simulate_csr(rowptr, col, q, np.zeros(g.n_neurons, dtype=np.int32), 1, [[-1]],
+                                lif.constants(1), 10, threads=threads, counts=False)
+    assert rep.spikes > 100
+    np.testing.assert_array_equal(rep.raster, ref["raster"])
+    np.testing.assert_array_equal(rep.v.view(np.uint32), ref["v"].view(np.uint32))
