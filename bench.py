@@ -432,8 +432,9 @@ def run_ours(args) -> dict | None:
     result = None
     parity = None
     cpu = None
+    e2e_api = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu, parity = cpu_baseline_and_parity(net, lay, lif, args, spec)
+        cpu, parity, e2e_api = cpu_baseline_and_parity(net, lay, lif, args, spec)
     if rank == 0:
         result = {
             "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -473,6 +474,7 @@ def run_ours(args) -> dict | None:
             "exchange_us": lat_summary(lat, lat_min, args.transport),
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "e2e_api": e2e_api,
             "gpu_launches": launches,
             "clocks": clocks.summary(),
         }
@@ -539,6 +541,7 @@ def cpu_baseline_and_parity(net, lay, lif, args, spec):
                   "i_equal": bool(np.array_equal(rep.i_syn.view(np.uint32), ref["i"].view(np.uint32))),
                   "spikes": int(rep.raster.sum()), "raster_sha256_16": sha(ref["raster"]),
                   "v_sha256_16": sha(ref["v"])}
+    e2e_api = simulate_api_e2e(rowptr, col, q, lif, args) if args.e2e_api else None
     steps = args.cpu_steps
     run = lambda n: c_oracle.simulate_csr(rowptr, col, q, owner, 1, [[-1]], lif.constants(args.seed), n,  # noqa
                                           threads=threads, raster=False, counts=False)
@@ -552,7 +555,37 @@ def cpu_baseline_and_parity(net, lay, lif, args, spec):
            "sample": f"{steps} full steps of the same {lay.n_neurons}-neuron network (oracle/sim_oracle.c, "
                      f"OpenMP {threads} threads), {dt:.1f} s excluding {setup:.1f} s setup and the "
                      f"{t_gen:.1f} s CPU network build"}
-    return cpu, parity
+    return cpu, parity, e2e_api
+
+
+def simulate_api_e2e(rowptr, col, q, lif, args) -> dict:
+    """The drop-in API end to end: simulate(graph, pm, rt, steps) on the benchmarked network
+    as a host NeuronGraph (model.py:53-92; built from the oracle's CSR outside the timed
+    region, p = q / 32 so the weight units are the same), timed on the host clock around
+    the call: edge upload, the device layout build, `steps` steps, raster / V / I read-back."""
+    import torch
+    import paper_2205_07125_b200 as nc
+    m = rowptr.size - 1
+    rows = np.repeat(np.arange(m, dtype=np.int32), np.diff(rowptr))
+    up = col > rows
+    g = nc.NeuronGraph(m, np.ones(m), rows[up].astype(np.int64), col[up].astype(np.int64),
+                       q[up].astype(np.float64) / 32.0)
+    del rows, up
+    pm = nc.PartitionMap(1, np.zeros(m, dtype=np.int64))
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    rep = nc.simulate(g, pm, None, args.steps, lif, seed=args.seed)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t
+    h2d = g.edge_i.size * (8 + 8 + 8)          # int64 ids + fp64 p uploaded (converted on the device)
+    return {"value": round(args.steps / dt, 2), "unit": UNIT, "wall_s": round(dt, 3),
+            "steps": args.steps, "loop_ms": round(rep.elapsed_ms, 3), "spikes": int(rep.spikes),
+            "h2d_bytes_per_step": int(h2d // max(args.steps, 1)),
+            "d2h_bytes_per_step": int(rep.raster[0].size + 8 * m // max(args.steps, 1)) if rep.raster is not None
+            else None,
+            "note": "simulate(NeuronGraph, PartitionMap, None, steps): host edge columns -> device (int32 ids, "
+                    "q from p), J-SELL build on the GPU, the step loop, rasters + final V/I to the host; one "
+                    "call, host wall clock"}
 
 
 def e2e_measure(sim, net, args, world: int, rank: int, lif) -> dict | None:
@@ -714,6 +747,8 @@ def main() -> int:
     ap.add_argument("--cpu-steps", type=int, default=200, help="CPU-baseline sample (~10 s of OpenMP oracle work at config 2)")
     ap.add_argument("--parity-steps", type=int, default=20,
                     help="steps of the benchmarked network checked bit for bit against the oracle (N=1; 0 = off)")
+    ap.add_argument("--no-e2e-api", dest="e2e_api", action="store_false",
+                    help="skip the simulate() end-to-end measurement (N=1)")
     ap.add_argument("--fused-send", default="auto", choices=["auto", "on", "off"],
                     help="N>1, P2P: the step kernel stores its spikes into the peers' inboxes (auto: large shards)")
     ap.add_argument("--no-cpu", action="store_true")

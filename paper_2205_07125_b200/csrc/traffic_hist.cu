@@ -23,7 +23,8 @@
 namespace {
 
 constexpr int kThreads = 256;
-constexpr size_t kSmemLimit = 96 * 1024;
+constexpr size_t kSmemLimit = 96 * 1024;    // fall back to global limbs above this
+constexpr size_t kSmemBudget = 48 * 1024;   // lane copies are halved down to this
 
 struct Decomposed {
   unsigned long long mant;  // integer mantissa (0 => nothing to add)
@@ -89,47 +90,39 @@ __global__ void k_exponents(const int64_t* __restrict__ ei, const int64_t* __res
   }
 }
 
-// Shared-memory accumulator of one block: kCopies copies (lane & (kCopies-1)) of
-// [cell][digit] pairs of 32-bit words {sum, carries}.  A digit add is one NATIVE
-// 32-bit shared atomic (64-bit shared atomics compile to CAS spin loops on
-// sm_100a: ATOMS.CAST.SPIN.64, the round-1 bottleneck) plus, when the returned old
-// value shows a wrap, a second one on the carry word: the pair is exactly the
-// 64-bit limb sum + carries * 2^32.  Copies spread same-cell lanes over
-// different addresses.
-constexpr int kCopies = 4;
-
+// Shared-memory accumulator of one block: `copies` copies (lane & (copies-1)) of
+// [cell][digit] pairs of 32-bit words {sum, carries}, upper cells only
+// (compact index, see ucell).  A digit add is one NATIVE 32-bit shared atomic
+// (64-bit shared atomics compile to CAS spin loops on sm_100a,
+// ATOMS.CAST.SPIN.64: the round-1 bottleneck) plus, when the returned old value
+// shows a wrap, a second one on the carry word: the pair is exactly the 64-bit
+// limb sum + carries * 2^32.  Lanes get their own copy (up to 32, as shared
+// memory allows) so lanes hitting the same cell hit different addresses, and the
+// copy stride is odd so those addresses fall in different banks (with 4 copies
+// 64 words apart, 95 % of the shared wavefronts were bank conflicts).
 __device__ __forceinline__ void add32c(unsigned int* p, unsigned int d) {
   if (!d) return;
   const unsigned int old = atomicAdd(p, d);
   if (old + d < old) atomicAdd(p + 1, 1u);
 }
 
-template <typename Idx>
-__device__ __forceinline__ void edge_term(const Idx* __restrict__ ei, const Idx* __restrict__ ej,
-                                          const double* __restrict__ ep, const double* __restrict__ w,
-                                          const Idx* __restrict__ asg, int64_t k, int n_gpus, double* x,
-                                          int* cell) {
-  if (ei) {
-    const int64_t i = (int64_t)ei[k], j = (int64_t)ej[k];
-    *x = contrib(ep[k], __ldg(w + i), __ldg(w + j));
-    *cell = cell_index((int64_t)__ldg(asg + i), (int64_t)__ldg(asg + j), n_gpus);
-  } else {  // per-GPU weight totals (binned_sums over assignment)
-    *x = w[k];
-    *cell = (int)asg[k];
-  }
-}
+// compact index of upper cell (lo, hi), lo <= hi < n: row lo starts at lo*(2n-lo+1)/2
+__device__ __forceinline__ int ucell(int lo, int hi, int n) { return lo * (2 * n - lo + 1) / 2 + (hi - lo); }
+
+int smem_cells(bool edges, int n_gpus) { return edges ? n_gpus * (n_gpus + 1) / 2 : n_gpus; }
+int copy_stride(int cells, int n_digits) { return (cells * n_digits * 2) | 1; }   // odd: banks shift per copy
 
 template <typename Idx>
 __global__ void __launch_bounds__(kThreads)
 k_histogram_smem(const Idx* __restrict__ ei, const Idx* __restrict__ ej, const double* __restrict__ ep,
                  const double* __restrict__ w, const Idx* __restrict__ asg, int64_t n, int n_gpus, int lsb0,
-                 int n_digits, unsigned long long* __restrict__ out) {
+                 int n_digits, int copies, unsigned long long* __restrict__ out) {
   extern __shared__ unsigned int sw[];
-  const int n_cells = ei ? n_gpus * n_gpus : n_gpus;
-  const int per_copy = n_cells * n_digits * 2;
-  for (int k = threadIdx.x; k < kCopies * per_copy; k += blockDim.x) sw[k] = 0u;
+  const int n_cells = ei ? n_gpus * (n_gpus + 1) / 2 : n_gpus;
+  const int cstride = (n_cells * n_digits * 2) | 1;
+  for (int k = threadIdx.x; k < copies * cstride; k += blockDim.x) sw[k] = 0u;
   __syncthreads();
-  unsigned int* mine = sw + (threadIdx.x & (kCopies - 1)) * per_copy;
+  unsigned int* mine = sw + (threadIdx.x & (copies - 1)) * cstride;
   // kUnroll edges per thread and iteration, every load issued before the first use:
   // the gathers of w / assignment (L2-resident) then overlap instead of serialising
   constexpr int kUnroll = 4;
@@ -149,18 +142,18 @@ k_histogram_smem(const Idx* __restrict__ ei, const Idx* __restrict__ ej, const d
         pe[u] = ok ? __ldcs(ep + k) : 0.0;
       }
       double wi[kUnroll], wj[kUnroll];
-      int64_t ai[kUnroll], aj[kUnroll];
+      int ai[kUnroll], aj[kUnroll];
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
         wi[u] = __ldg(w + i[u]);
         wj[u] = __ldg(w + j[u]);
-        ai[u] = (int64_t)__ldg(asg + i[u]);
-        aj[u] = (int64_t)__ldg(asg + j[u]);
+        ai[u] = (int)__ldg(asg + i[u]);
+        aj[u] = (int)__ldg(asg + j[u]);
       }
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
         x[u] = contrib(pe[u], wi[u], wj[u]);   // p = 0 for the tail: nothing added
-        cell[u] = cell_index(ai[u], aj[u], n_gpus);
+        cell[u] = ucell(min(ai[u], aj[u]), max(ai[u], aj[u]), n_gpus);
       }
     } else {  // per-GPU weight totals (binned_sums over assignment)
 #pragma unroll
@@ -187,17 +180,38 @@ k_histogram_smem(const Idx* __restrict__ ei, const Idx* __restrict__ ej, const d
   __syncthreads();
   // one thread per cell: sum the copies into 64-bit digits, normalise, add to global
   for (int cell = threadIdx.x; cell < n_cells; cell += blockDim.x) {
+    int gcell = cell;
+    if (ei) {   // compact upper index -> lo * n + hi of the output
+      int lo = 0, rem = cell;
+      while (rem >= n_gpus - lo) rem -= n_gpus - lo++;
+      gcell = lo * n_gpus + lo + rem;
+    }
     unsigned long long carry = 0;
     for (int k = 0; k < n_digits; ++k) {
-      unsigned long long x = carry;   // < 2^32 + kCopies * 2^63 / 2^32: no wrap
-      for (int c = 0; c < kCopies; ++c) {
-        const unsigned int* e = sw + c * per_copy + (cell * n_digits + k) * 2;
+      unsigned long long x = carry;   // copies * (2^32 + carries * 2^32) + 2^32: no wrap below 2^31 adds
+      for (int c = 0; c < copies; ++c) {
+        const unsigned int* e = sw + c * cstride + (cell * n_digits + k) * 2;
         x += (unsigned long long)e[0] + ((unsigned long long)e[1] << 32);
       }
       const unsigned long long digit = (k + 1 < n_digits) ? (x & 0xffffffffull) : x;
       carry = (k + 1 < n_digits) ? (x >> 32) : 0;
-      if (digit) atomicAdd(out + (int64_t)cell * n_digits + k, digit);
+      if (digit) atomicAdd(out + (int64_t)gcell * n_digits + k, digit);
     }
+  }
+}
+
+template <typename Idx>
+__device__ __forceinline__ void edge_term(const Idx* __restrict__ ei, const Idx* __restrict__ ej,
+                                          const double* __restrict__ ep, const double* __restrict__ w,
+                                          const Idx* __restrict__ asg, int64_t k, int n_gpus, double* x,
+                                          int* cell) {
+  if (ei) {
+    const int64_t i = (int64_t)ei[k], j = (int64_t)ej[k];
+    *x = contrib(ep[k], __ldg(w + i), __ldg(w + j));
+    *cell = cell_index((int64_t)__ldg(asg + i), (int64_t)__ldg(asg + j), n_gpus);
+  } else {  // per-GPU weight totals (binned_sums over assignment)
+    *x = w[k];
+    *cell = (int)asg[k];
   }
 }
 
@@ -223,12 +237,11 @@ int launch_hist(const Idx* ei, const Idx* ej, const double* ep, const double* w,
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const size_t n_cells = ei ? (size_t)n_gpus * n_gpus : (size_t)n_gpus;
-  const size_t smem = (size_t)kCopies * n_cells * n_digits * 2 * sizeof(unsigned int);
-  int64_t blocks = (n + kThreads - 1) / kThreads;
-  // a few resident blocks per SM, each streaming many items before its flush
-  const int64_t max_blocks = (int64_t)sms * 6;
-  if (blocks > max_blocks) blocks = max_blocks;
+  // lane-private copies (up to 32) within a 48 KB budget: several blocks per SM
+  const int cstride = copy_stride(smem_cells(ei != nullptr, n_gpus), n_digits);
+  int copies = 32;
+  while (copies > 1 && (size_t)copies * cstride * sizeof(unsigned int) > kSmemBudget) copies >>= 1;
+  const size_t smem = (size_t)copies * cstride * sizeof(unsigned int);
   if (smem <= kSmemLimit) {
     static bool attr = false;
     if (!attr) {
@@ -238,9 +251,16 @@ int launch_hist(const Idx* ei, const Idx* ej, const double* ep, const double* w,
                                        (int)kSmemLimit));
       attr = true;
     }
+    int occ = 1;
+    NC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_histogram_smem<Idx>, kThreads, smem));
+    int64_t blocks = (n + kThreads - 1) / kThreads;
+    const int64_t max_blocks = (int64_t)sms * (occ > 0 ? occ : 1);   // one resident wave, grid-stride
+    if (blocks > max_blocks) blocks = max_blocks;
     k_histogram_smem<Idx><<<(unsigned)blocks, kThreads, smem, st>>>(ei, ej, ep, w, asg, n, n_gpus, lsb0, n_digits,
-                                                                       out);
+                                                                       copies, out);
   } else {
+    int64_t blocks = (n + kThreads - 1) / kThreads;
+    if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
     k_histogram_global<Idx><<<(unsigned)blocks, kThreads, 0, st>>>(ei, ej, ep, w, asg, n, n_gpus, lsb0, n_digits,
                                                                      out);
   }
