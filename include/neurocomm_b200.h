@@ -84,6 +84,12 @@ int nc_traffic_histogram32(const int32_t* edge_i, const int32_t* edge_j, const d
                            const double* weights, const int32_t* assignment, int64_t n_edges,
                            int32_t n_gpus, int32_t lsb_exponent, int32_t n_digits,
                            unsigned long long* pg_limbs, void* stream);
+/* Same with the per-neuron gathers packed: neuron_records[k] = 16 bytes
+ * {double weight; int32 gpu; int32 unused} (one gather per endpoint). */
+int nc_traffic_histogram_packed(const int32_t* edge_i, const int32_t* edge_j, const double* edge_p,
+                                const void* neuron_records, int64_t n_edges, int32_t n_gpus,
+                                int32_t lsb_exponent, int32_t n_digits, unsigned long long* pg_limbs,
+                                void* stream);
 int nc_weight_histogram(const double* weights, const int64_t* assignment, int64_t n_neurons,
                         int32_t n_gpus, int32_t lsb_exponent, int32_t n_digits,
                         unsigned long long* wg_limbs, void* stream);
@@ -442,6 +448,21 @@ int nc_edges_count(const nc_graphgen_t* g, const int32_t* edge_i, const int32_t*
 int nc_edges_fill(const nc_graphgen_t* g, const int32_t* edge_i, const int32_t* edge_j, const uint8_t* q,
                   int64_t n_edges, int32_t n_tiles, int32_t tile_words, const int64_t* slice_ptr,
                   const uint32_t* row_meta, const int32_t* pos_of, int32_t* fill, uint32_t* syn, void* stream);
+/* K6 straight off the generator's network (config-3 scale, where the
+ * NeuronGraph and its CSR do not fit in host memory; replaces
+ * partition_greedy's adjacency_from_edges + greedy_fill, partition.py:95-114,
+ * greedy.py:32-117): the same fill over adjacency_from_edges' row order and
+ * values, rows regenerated on demand on the host (upper part) or read from a
+ * 4 B/edge transpose (lower part), p recomputed per edge.  spec: the generator
+ * fields of nc_graphgen_t (owner/internal_id unused); weights NULL = all 1;
+ * threads 0 = all cores (the transpose build; the fill is sequential). */
+int nc_greedy_fill_generated(const nc_graphgen_t* spec, const double* weights, int32_t n_buckets,
+                             double capacity, int64_t* assignment, int32_t threads);
+/* The generated network as NeuronGraph columns (ascending (i, j), fp64 p),
+ * host restatement of the device generator.  NULL arrays: returns the edge
+ * count; < 0 on error. */
+int64_t nc_hostgen_edges(const nc_graphgen_t* spec, int64_t* edge_i, int64_t* edge_j, double* edge_p,
+                         int32_t threads);
 /* Push synapses (nc_shard_t push_rowptr / push_syn format) straight from the
  * generator, without a pull layout.  Phase 0: push_rowptr[pre + 1] += entries
  * of pre (int64 [n_words*32 + 1], zeroed) and dest_mask[r] |= shards hosting a

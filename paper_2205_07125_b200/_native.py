@@ -97,9 +97,13 @@ _SIGS = {
     "nc_abi_version": (c_int32, []),
     "nc_last_error": (C.c_char_p, []),
     "nc_greedy_fill": (c_int32, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_double, c_void_p]),
+    "nc_greedy_fill_generated": (c_int32, [C.POINTER(GraphGenC), c_void_p, c_int32, c_double, c_void_p, c_int32]),
+    "nc_hostgen_edges": (c_int64, [C.POINTER(GraphGenC), c_void_p, c_void_p, c_void_p, c_int32]),
     "nc_traffic_exponents": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
     "nc_traffic_histogram": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int32,
                                        c_int32, c_int32, c_void_p, c_void_p]),
+    "nc_traffic_histogram_packed": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int32, c_int32,
+                                              c_int32, c_void_p, c_void_p]),
     "nc_traffic_histogram32": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int32,
                                        c_int32, c_int32, c_void_p, c_void_p]),
     "nc_weight_histogram": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_int32, c_int32, c_void_p, c_void_p]),

@@ -24,7 +24,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr size_t kSmemLimit = 96 * 1024;    // fall back to global limbs above this
-constexpr size_t kSmemBudget = 48 * 1024;   // lane copies are halved down to this
+constexpr size_t kSmemBudget = 32 * 1024;   // lane copies are halved down to this
 
 struct Decomposed {
   unsigned long long mant;  // integer mantissa (0 => nothing to add)
@@ -112,7 +112,9 @@ __device__ __forceinline__ int ucell(int lo, int hi, int n) { return lo * (2 * n
 int smem_cells(bool edges, int n_gpus) { return edges ? n_gpus * (n_gpus + 1) / 2 : n_gpus; }
 int copy_stride(int cells, int n_digits) { return (cells * n_digits * 2) | 1; }   // odd: banks shift per copy
 
-template <typename Idx>
+// kPacked: w points at one 16-byte record per neuron {double w; int32 gpu; pad}
+// (nc_traffic_histogram_packed): one gather per endpoint instead of two.
+template <typename Idx, bool kPacked = false>
 __global__ void __launch_bounds__(kThreads)
 k_histogram_smem(const Idx* __restrict__ ei, const Idx* __restrict__ ej, const double* __restrict__ ep,
                  const double* __restrict__ w, const Idx* __restrict__ asg, int64_t n, int n_gpus, int lsb0,
@@ -143,12 +145,24 @@ k_histogram_smem(const Idx* __restrict__ ei, const Idx* __restrict__ ej, const d
       }
       double wi[kUnroll], wj[kUnroll];
       int ai[kUnroll], aj[kUnroll];
+      if (kPacked) {
+        const int4* rec = reinterpret_cast<const int4*>(w);
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        wi[u] = __ldg(w + i[u]);
-        wj[u] = __ldg(w + j[u]);
-        ai[u] = (int)__ldg(asg + i[u]);
-        aj[u] = (int)__ldg(asg + j[u]);
+        for (int u = 0; u < kUnroll; ++u) {
+          const int4 a = __ldg(rec + i[u]), b = __ldg(rec + j[u]);
+          wi[u] = __hiloint2double(a.y, a.x);
+          wj[u] = __hiloint2double(b.y, b.x);
+          ai[u] = a.z;
+          aj[u] = b.z;
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          wi[u] = __ldg(w + i[u]);
+          wj[u] = __ldg(w + j[u]);
+          ai[u] = (int)__ldg(asg + i[u]);
+          aj[u] = (int)__ldg(asg + j[u]);
+        }
       }
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
@@ -230,7 +244,7 @@ k_histogram_global(const Idx* __restrict__ ei, const Idx* __restrict__ ej, const
   }
 }
 
-template <typename Idx>
+template <typename Idx, bool kPacked = false>
 int launch_hist(const Idx* ei, const Idx* ej, const double* ep, const double* w, const Idx* asg, int64_t n,
                 int n_gpus, int lsb0, int n_digits, unsigned long long* out, cudaStream_t st) {
   if (n <= 0) return NC_OK;
@@ -245,19 +259,21 @@ int launch_hist(const Idx* ei, const Idx* ej, const double* ep, const double* w,
   if (smem <= kSmemLimit) {
     static bool attr = false;
     if (!attr) {
-      NC_CUDA_TRY(cudaFuncSetAttribute(k_histogram_smem<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)kSmemLimit));
-      NC_CUDA_TRY(cudaFuncSetAttribute(k_histogram_smem<int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      NC_CUDA_TRY(cudaFuncSetAttribute(k_histogram_smem<Idx, kPacked>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)kSmemLimit));
       attr = true;
     }
     int occ = 1;
-    NC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_histogram_smem<Idx>, kThreads, smem));
+    NC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_histogram_smem<Idx, kPacked>, kThreads, smem));
     int64_t blocks = (n + kThreads - 1) / kThreads;
     const int64_t max_blocks = (int64_t)sms * (occ > 0 ? occ : 1);   // one resident wave, grid-stride
     if (blocks > max_blocks) blocks = max_blocks;
-    k_histogram_smem<Idx><<<(unsigned)blocks, kThreads, smem, st>>>(ei, ej, ep, w, asg, n, n_gpus, lsb0, n_digits,
+    k_histogram_smem<Idx, kPacked><<<(unsigned)blocks, kThreads, smem, st>>>(ei, ej, ep, w, asg, n, n_gpus, lsb0, n_digits,
                                                                        copies, out);
+  } else if (kPacked) {
+    nc_set_error("traffic histogram: %d GPUs x %d digits do not fit in shared memory (packed path)", n_gpus,
+                 n_digits);
+    return NC_E_ARG;
   } else {
     int64_t blocks = (n + kThreads - 1) / kThreads;
     if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
@@ -308,6 +324,19 @@ extern "C" int nc_traffic_histogram32(const int32_t* edge_i, const int32_t* edge
   }
   return launch_hist(edge_i, edge_j, edge_p, weights, assignment, n_edges, n_gpus, lsb_exponent, n_digits,
                      pg_limbs, (cudaStream_t)stream);
+}
+
+extern "C" int nc_traffic_histogram_packed(const int32_t* edge_i, const int32_t* edge_j, const double* edge_p,
+                                           const void* neuron_records, int64_t n_edges, int32_t n_gpus,
+                                           int32_t lsb_exponent, int32_t n_digits, unsigned long long* pg_limbs,
+                                           void* stream) {
+  if (n_gpus < 1 || n_digits < 3 || !edge_i || !edge_j || !neuron_records) {
+    nc_set_error("nc_traffic_histogram_packed: bad arguments (n_gpus=%d n_digits=%d)", n_gpus, n_digits);
+    return NC_E_ARG;
+  }
+  return launch_hist<int32_t, true>(edge_i, edge_j, edge_p, reinterpret_cast<const double*>(neuron_records),
+                                    nullptr, n_edges, n_gpus, lsb_exponent, n_digits, pg_limbs,
+                                    (cudaStream_t)stream);
 }
 
 extern "C" int nc_weight_histogram(const double* weights, const int64_t* assignment, int64_t n_neurons,

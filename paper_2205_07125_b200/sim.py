@@ -231,6 +231,28 @@ class GeneratorSpec:
         """C = 1 random network with mean degree `degree` (synapses per neuron)."""
         return cls(n_neurons, 1, degree / max(n_neurons - 1, 1), 0.0, seed)
 
+    def to_c(self) -> "_native.GraphGenC":
+        return _native.GraphGenC(
+            n_neurons=self.n_neurons, n_communities=self.n_communities, p_in=self.p_in, p_out=self.p_out,
+            intra_lo=self.intra_p_range[0], intra_hi=self.intra_p_range[1], inter_lo=self.inter_p_range[0],
+            inter_hi=self.inter_p_range[1], seed=int(self.seed) & (2**64 - 1))
+
+    def host_graph(self, threads: int = 0) -> NeuronGraph:
+        """The generated network as a host NeuronGraph (model.py:53-92): edges ascending
+        (i, j), their fp64 p, unit weights -- what the reference's planner consumes.
+        Host restatement of the device generator (csrc/graphgen_host.cpp)."""
+        L = _native.lib()
+        g = self.to_c()
+        n = int(L.nc_hostgen_edges(C.byref(g), None, None, None, int(threads)))
+        if n < 0:
+            _native.check(-1, "host generator")
+        ei = np.empty(n, dtype=np.int64)
+        ej = np.empty(n, dtype=np.int64)
+        ep = np.empty(n, dtype=np.float64)
+        if L.nc_hostgen_edges(C.byref(g), ei.ctypes.data, ej.ctypes.data, ep.ctypes.data, int(threads)) != n:
+            raise RuntimeError("host generator: edge count changed between passes")
+        return NeuronGraph(self.n_neurons, np.ones(self.n_neurons), ei, ej, ep)
+
 
 ShardCSR = sell.SellCSR
 

@@ -176,9 +176,16 @@ def exact_bin_sums(values_dev, keys_dev, n_bins: int, *, pairs=None, stream=None
             rc = L.nc_weight_histogram(values_dev.data_ptr(), keys_dev.data_ptr(), n_local, n_bins, lo, nd,
                                        limbs.data_ptr(), st)
         elif ei.dtype == torch.int32:
-            asg32 = keys_dev.to(torch.int32)
-            rc = L.nc_traffic_histogram32(ei.data_ptr(), ej.data_ptr(), ep.data_ptr(), values_dev.data_ptr(),
-                                          asg32.data_ptr(), n_local, n_bins, lo, nd, limbs.data_ptr(), st)
+            # one 16-byte record per neuron {weight, gpu}: a single gather per endpoint
+            rec = torch.zeros((values_dev.numel(), 4), dtype=torch.int32, device=dev)
+            rec[:, :2] = values_dev.to(torch.float64).contiguous().view(torch.int32).view(-1, 2)
+            rec[:, 2] = keys_dev.to(torch.int32)
+            rc = L.nc_traffic_histogram_packed(ei.data_ptr(), ej.data_ptr(), ep.data_ptr(), rec.data_ptr(), n_local,
+                                               n_bins, lo, nd, limbs.data_ptr(), st)
+            if rc != 0:   # cells x digits too large for shared memory: the global-limb path
+                asg32 = keys_dev.to(torch.int32)
+                rc = L.nc_traffic_histogram32(ei.data_ptr(), ej.data_ptr(), ep.data_ptr(), values_dev.data_ptr(),
+                                              asg32.data_ptr(), n_local, n_bins, lo, nd, limbs.data_ptr(), st)
         else:
             rc = L.nc_traffic_histogram(ei.data_ptr(), ej.data_ptr(), ep.data_ptr(), values_dev.data_ptr(),
                                         keys_dev.to(torch.int64).data_ptr(), n_local, n_bins, lo, nd,

@@ -463,3 +463,17 @@ def test_simulate_api_at_config2_scale():
     assert rep.spikes > 100
     np.testing.assert_array_equal(rep.raster, ref["raster"])
     np.testing.assert_array_equal(rep.v.view(np.uint32), ref["v"].view(np.uint32))
+
+
+def test_host_generator_equals_device_generator():
+    """GeneratorSpec.host_graph (csrc/graphgen_host.cpp: the planner's view, what
+    partition_greedy_generated partitions) and Network.generate (csrc/graphgen.cu: what
+    the GPU simulates) produce the same synapses: (post, pre, q = ceil(32 p))."""
+    spec = S.GeneratorSpec(40_000, 5, 0.01, 0.001, seed=11)
+    g = spec.host_graph()
+    q = S.q_from_p(g.edge_p)
+    want = np.concatenate([np.stack([g.edge_j, g.edge_i, q]), np.stack([g.edge_i, g.edge_j, q])], axis=1).T
+    net = S.Network.generate(spec, S.ShardLayout.blocks(spec.n_neurons, 2))
+    got = np.concatenate([np.stack(net.host_csr(h)).T for h in range(2)]).astype(np.int64)
+    want = want.astype(np.int64)
+    np.testing.assert_array_equal(got[np.lexsort(got.T[::-1])], want[np.lexsort(want.T[::-1])])

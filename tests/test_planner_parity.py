@@ -329,3 +329,44 @@ def test_native_repair_balance_matches_fsum_loop(seed):
     _repair_reference_loop(a, w, n, bound)
     _rebalance(b, w, n, bound)
     np.testing.assert_array_equal(a, b)
+
+
+# ------------------------------------------------------------------ K6 off the generator (config-3 scale)
+
+@pytest.mark.parametrize("spec_args,n_gpus,slack", [
+    ((5000, 1, 60 / 4999, 0.0, 3), 4, 0.0),
+    ((6000, 4, 0.02, 0.002, 7), 4, 0.0),
+    ((3001, 3, 0.05, 0.01, 1), 3, 0.05),
+    ((20000, 8, 0.01, 0.0005, 2), 8, 0.0),
+])
+def test_streamed_k6_equals_materialised(spec_args, n_gpus, slack):
+    """partition_greedy_generated (rows regenerated on demand, the transpose as int32) ==
+    partition_greedy on the same network materialised as a NeuronGraph (adjacency_from_edges
+    + greedy_fill, the reference's path), bit for bit."""
+    from paper_2205_07125_b200 import partition as P
+    from paper_2205_07125_b200 import sim as S
+    n, c, p_in, p_out, seed = spec_args
+    spec = S.GeneratorSpec(n, c, p_in, p_out, seed=seed)
+    g = spec.host_graph()
+    nc.model.validate(g) if hasattr(nc.model, "validate") else None
+    cfg = nc.PartitionConfig(balance_slack=slack)
+    want = nc.partition_greedy(g, n_gpus, cfg)
+    got = P.partition_greedy_generated(spec, n_gpus, cfg, threads=3)
+    np.testing.assert_array_equal(got.assignment, want.assignment)
+
+
+def test_host_graph_matches_generator_statistics():
+    """host_graph: edges ascending, i < j, p inside the ModelSpec ranges, count near the SBM mean."""
+    from paper_2205_07125_b200 import sim as S
+    spec = S.GeneratorSpec(12_000, 4, 0.02, 0.002, seed=7)
+    g = spec.host_graph(threads=2)
+    assert (g.edge_i < g.edge_j).all()
+    key = g.edge_i * g.n_neurons + g.edge_j
+    assert (np.diff(key) > 0).all()
+    sizes = nc.model.community_sizes(spec.n_neurons, spec.n_communities)
+    same = (g.edge_i // sizes[0]) == (g.edge_j // sizes[0])
+    assert ((g.edge_p[same] >= 0.5) & (g.edge_p[same] < 1.0)).all()
+    assert ((g.edge_p[~same] >= 0.05) & (g.edge_p[~same] < 0.5)).all()
+    mean = sum(s * (s - 1) // 2 for s in sizes.tolist()) * spec.p_in + \
+        (spec.n_neurons ** 2 - (sizes ** 2).sum()) / 2 * spec.p_out
+    assert abs(g.n_edges - mean) < 4 * np.sqrt(mean)
