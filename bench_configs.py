@@ -98,6 +98,10 @@ def main() -> int:
     ap.add_argument("--routes", default=None, help="direct,two-level (default: per config)")
     ap.add_argument("--neurons", type=int, default=None, help="override the config's neuron count (tests)")
     ap.add_argument("--chunk", type=int, default=100)
+    ap.add_argument("--partition", default="blocks",
+                    help="blocks | greedy[:file.npz]: the reference's partition_greedy of the generated network "
+                         "(partition_greedy_generated; loaded from the .npz tools/k6_config3.py writes when given, "
+                         "else computed here on the host)")
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
@@ -119,7 +123,29 @@ def main() -> int:
     if "fused" in engines and not want_pull:
         skipped["fused"] = ("pull layout build needs ~8 B/synapse transient (%.0f GB) on a GPU with %.0f GB free"
                             % (syn_per_gpu * 8 / GB, free / GB))
-    lay = S.ShardLayout.blocks(cfg["neurons"], world)
+    part_s = None
+    if args.partition == "blocks":
+        lay = S.ShardLayout.blocks(cfg["neurons"], world)
+    elif args.partition.startswith("greedy"):
+        path = args.partition.split(":", 1)[1] if ":" in args.partition else None
+        t0 = time.time()
+        if path:
+            z = np.load(path)
+            meta = json.loads(str(z["meta"]))
+            want = {"n_neurons": spec.n_neurons, "n_communities": spec.n_communities, "p_in": spec.p_in,
+                    "p_out": spec.p_out, "seed": spec.seed}
+            if meta["spec"] != want or meta["n_gpus"] != world:
+                raise SystemExit(f"{path}: partition of {meta['spec']} over {meta['n_gpus']} GPUs, need {want} "
+                                 f"over {world}")
+            asg = z["assignment"].astype(np.int64)
+            part_s = meta["seconds"]
+        else:
+            from paper_2205_07125_b200.partition import partition_greedy_generated
+            asg = partition_greedy_generated(spec, world).assignment
+            part_s = round(time.time() - t0, 1)
+        lay = S.ShardLayout.from_assignment(asg, world)
+    else:
+        raise SystemExit(f"unknown --partition {args.partition!r}")
     torch.cuda.reset_peak_memory_stats(dev)
     t0 = time.time()
     net = S.Network.generate(spec, lay, device=dev, shards=[rank], pull=want_pull, push=want_push)
@@ -200,7 +226,7 @@ def main() -> int:
                     "wire_bytes_per_step": round(float(h.sum()) * 8 + 8 * int((h > 0).sum()), 1),
                     "channel_ids_per_step": np.round(h, 1).tolist(),
                     "neurons": n, "synapses": int(nsyn.item()), "communities": cfg["communities"],
-                    "partition": "blocks", "bitmap_tiles": csr.n_tiles if want_pull else None,
+                    "partition": args.partition.split(":")[0], "partition_s": part_s, "bitmap_tiles": csr.n_tiles if want_pull else None,
                     "fused_send": fused_send, "memory_per_gpu": mem, "build_s": round(build_s, 1),
                     "planner": planner, "clocks": clocks.summary(), "case_s": round(time.time() - t_case, 1),
                     "skipped_engines": skipped or None,

@@ -28,7 +28,7 @@ from . import _native
 from .routing import RoutingTable
 from .sim import ExchangePlan, LifParams, Network, SimReport, _ShardState, _as_u16
 
-__all__ = ["channel_masks", "gather_dest", "DistSimulator", "TorchGroup"]
+__all__ = ["channel_masks", "gather_dest", "DistSimulator", "TorchGroup", "choose_delivery"]
 
 
 class TorchGroup:
@@ -104,6 +104,32 @@ def gather_dest(net: Network, rank: int, world: int, device, group=None):
         g[b:b + lay.n_local(h)] = parts[h][: lay.n_local(h)]
     return _as_u16(g)
 
+
+
+def choose_delivery(net: Network, lif: LifParams, seed: int, rt: RoutingTable | None = None, *, candidates=None,
+                    steps: int = 20, warmup: int = 5, group=None, **kw):
+    """sim.choose_delivery for one process per GPU: every engine that fits on EVERY rank
+    is timed (max over ranks) and all ranks return the same fastest one."""
+    import torch
+    from .sim import _timed_steps, delivery_candidates
+    grp = group if group is not None else TorchGroup()
+    names = ["fused", "persistent"]
+    if candidates is None:
+        mine = delivery_candidates(net)
+        ok = torch.tensor([int(n in mine or (n == "persistent" and "push" in mine)) for n in names],
+                          dtype=torch.int32, device=net.device)
+        grp.all_reduce(ok, "min")
+        candidates = [n for n, f in zip(names, ok.tolist()) if f]
+    if not candidates:
+        raise ValueError("no delivery engine fits this network on every rank")
+    times = {}
+    for d in candidates:
+        sim = DistSimulator(net, lif, seed, rt, delivery=d, transport="p2p", group=grp, **kw)
+        t = torch.tensor([_timed_steps(sim, warmup, steps)], dtype=torch.float64, device=net.device)
+        grp.all_reduce(t, "max")
+        times[d] = float(t.item())
+        sim.close()
+    return min(times, key=times.get), times
 
 
 FUSED_SEND_MIN_ROWS = 32768   # fused P2P send from the step kernel above this many local rows

@@ -35,7 +35,7 @@ from .routing import RoutingTable
 
 __all__ = [
     "LifParams", "ShardLayout", "ExchangePlan", "Network", "Simulator", "SimReport", "simulate",
-    "q_from_p", "inhibitory_mask", "ID_BITS", "StepGraphs",
+    "q_from_p", "inhibitory_mask", "ID_BITS", "StepGraphs", "choose_delivery",
 ]
 
 ID_BITS = sell.ID_BITS  # unpacked builder entry: (q << 26) | tile-relative pre id
@@ -1057,6 +1057,57 @@ class Simulator:
                          v=v, i_syn=i, elapsed_ms=elapsed_ms, exchange=mode, delivery=self.delivery)
 
 
+# ---------------------------------------------------------------- engine choice
+
+def _timed_steps(sim, warm: int, steps: int) -> float:
+    """ms per step of `steps` steps after `warm` (CUDA events on the current stream)."""
+    import torch
+    sim.reset(1)
+    sim.prepare(warm)
+    sim.prepare(steps)
+    sim.advance(warm)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    sim.advance(steps)
+    e1.record()
+    torch.cuda.synchronize()
+    sim.check_status()
+    return e0.elapsed_time(e1) / max(steps, 1)
+
+
+def delivery_candidates(net: Network) -> list:
+    """Engines that can run `net` here: the pull kernel if the layout has it, the
+    event-driven engines if the push CSR fits next to it (4 B per synapse)."""
+    import torch
+    out = []
+    if all(getattr(c, "has_pull", True) for c in net.shards.values()):
+        out.append("fused")
+    cached = all(getattr(c, "_push_cache", None) is not None for c in net.shards.values())
+    free = torch.cuda.mem_get_info(net.device)[0]
+    if cached or 4.4 * net.n_synapses + 2e9 < free:
+        out.append("persistent" if net.layout.n_shards == 1 else "push")
+    return out
+
+
+def choose_delivery(net: Network, lif: LifParams, seed: int, rt: RoutingTable | None = None, *,
+                    candidates=None, steps: int = 20, warmup: int = 5):
+    """The fastest delivery engine for this network and drive, measured (every engine gives
+    bit-identical results, tests/test_gpu_parity.py): (name, {name: ms per step}).  The pull
+    kernel streams every synapse each step; the event-driven engines do work proportional
+    to spikes x degree, so which one wins depends on rate, size and bitmap tiling."""
+    cands = list(candidates) if candidates else delivery_candidates(net)
+    if not cands:
+        raise ValueError("no delivery engine fits this network on this device")
+    times = {}
+    for d in cands:
+        sim = Simulator(net, lif, seed, rt, delivery=d)
+        times[d] = _timed_steps(sim, warmup, steps)
+        del sim
+    best = min(times, key=times.get)
+    return best, times
+
+
 # ---------------------------------------------------------------- public API
 
 def simulate(graph: NeuronGraph, pm, rt: RoutingTable | None, steps: int, lif: LifParams = LifParams(),
@@ -1068,7 +1119,8 @@ def simulate(graph: NeuronGraph, pm, rt: RoutingTable | None, steps: int, lif: L
     (generate_synthetic -> partition_greedy -> build_routing_table or route_p2p).
     ``rt=None`` means direct routing.  All partitions run on the current CUDA
     device with the local exchange transport; use :mod:`.distributed` for one
-    process per GPU.
+    process per GPU.  ``delivery="auto"`` times the engines that fit
+    (:func:`choose_delivery`) and runs the fastest.
     """
     if steps < 0:
         raise ValueError(f"steps must be >= 0, got {steps}")
@@ -1076,6 +1128,8 @@ def simulate(graph: NeuronGraph, pm, rt: RoutingTable | None, steps: int, lif: L
         raise ValueError(f"partition map covers {pm.assignment.size} neurons, graph has {graph.n_neurons}")
     layout = ShardLayout.from_assignment(pm.assignment, pm.n_gpus)
     net = Network.from_graph(graph, layout, device=device, inh_every=lif.inh_every)
+    if delivery == "auto":   # measure the engines that fit, keep the fastest (identical results)
+        delivery, _ = choose_delivery(net, lif, seed, rt)
     sim = Simulator(net, lif, seed, rt, delivery=delivery,
                     record_raster_steps=steps if "raster" in record else 0,
                     per_step_counts="counts" in record, use_graph=use_graph)

@@ -477,3 +477,21 @@ def test_host_generator_equals_device_generator():
     got = np.concatenate([np.stack(net.host_csr(h)).T for h in range(2)]).astype(np.int64)
     want = want.astype(np.int64)
     np.testing.assert_array_equal(got[np.lexsort(got.T[::-1])], want[np.lexsort(want.T[::-1])])
+
+
+def test_auto_delivery_picks_a_measured_engine_and_matches_oracle():
+    """simulate(delivery="auto"): the engines that fit are timed, the fastest runs; the
+    result is the oracle's whichever wins."""
+    g = cfg1(3)
+    pm = nc.partition_greedy(g, 2)
+    lay = S.ShardLayout.from_assignment(pm.assignment, 2)
+    net = S.Network.from_graph(g, lay)
+    best, times = S.choose_delivery(net, S.LifParams(), 3)
+    assert set(times) == {"fused", "push"} and best in times and all(t > 0 for t in times.values())
+    rep = nc.simulate(g, pm, None, 40, S.LifParams(), seed=3, delivery="auto")
+    assert rep.delivery in ("fused", "push")
+    rp, col, q = c_oracle.symmetric_csr(g.n_neurons, g.edge_i, g.edge_j, S.q_from_p(g.edge_p))
+    ref = c_oracle.simulate_csr(rp, col, q, pm.assignment, 2, S.ExchangePlan(2, None).next_hop,
+                                S.LifParams().constants(3), 40, threads=8)
+    np.testing.assert_array_equal(rep.raster, ref["raster"])
+    np.testing.assert_array_equal(rep.hop_ids, ref["hop"])
