@@ -8,8 +8,8 @@ timed CPU baseline; the product package never imports it.
   Parity UNPINNED against the reference (which has no spike loop); pinned by
   Philox known-answer vectors, the independent numpy restatement
   (sim_numpy.py) and committed golden rasters (tests/golden/).
-* planner.py -- pure-Python restatements of the reference planner functions
-  (greedy_fill, aggregate/fsum, routing) for small cases on boxes where the
-  reference itself is absent; pinned against fixtures generated by running
-  the reference (tests/golden/make_golden.py).
+* The planner stages are checked against outputs of the reference itself, not a
+  restatement: tests/golden/make_golden.py runs the reference (in the build container) and
+  commits its results (reference_fixtures.*, reference_io.json); the reference's own test
+  suite runs against the drop-in through conformance/.
 """

@@ -45,3 +45,28 @@ def test_error_path_host_entry_point():
                             1.0, out.ctypes.data)
     assert rc == _native.NC_E_ARG
     assert b"n_buckets" in lib.nc_last_error()
+
+
+def test_struct_field_offsets_match_header(tmp_path):
+    """Every ctypes mirror field sits at the offset the C compiler gives it in the header
+    (offsetof over a generated translation unit, compiled with gcc here)."""
+    structs = {"nc_lif_params_t": _native.LifParamsC, "nc_shard_t": _native.ShardC,
+               "nc_graphgen_t": _native.GraphGenC, "nc_xchg_t": _native.XchgC}
+    lines = ["#include <stdio.h>", "#include <stddef.h>", '#include "neurocomm_b200.h"', "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
+        for f in py._fields_:
+            lines.append(f'printf("{cname} {f[0]} %zu\\n", offsetof({cname}, {f[0]}));')
+    lines += ["return 0; }"]
+    src = tmp_path / "offsets.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "offsets"
+    subprocess.run(["gcc", "-std=c11", "-I", str(ROOT / "include"), str(src), "-o", str(exe)], check=True)
+    got = {}
+    for ln in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.splitlines():
+        cname, field, off = ln.split()
+        got[(cname, field)] = int(off)
+    for cname, py in structs.items():
+        assert got[(cname, "size")] == ctypes.sizeof(py), cname
+        for f in py._fields_:
+            assert got[(cname, f[0])] == getattr(py, f[0]).offset, (cname, f[0])
