@@ -22,7 +22,13 @@
 
 namespace {
 
-constexpr int kThreads = 256;
+#ifndef NC_K5_THREADS
+#define NC_K5_THREADS 256
+#endif
+#ifndef NC_K5_UNROLL
+#define NC_K5_UNROLL 4
+#endif
+constexpr int kThreads = NC_K5_THREADS;
 constexpr size_t kSmemLimit = 96 * 1024;    // fall back to global limbs above this
 constexpr size_t kSmemBudget = 32 * 1024;   // lane copies are halved down to this
 
@@ -127,7 +133,7 @@ k_histogram_smem(const Idx* __restrict__ ei, const Idx* __restrict__ ej, const d
   unsigned int* mine = sw + (threadIdx.x & (copies - 1)) * cstride;
   // kUnroll edges per thread and iteration, every load issued before the first use:
   // the gathers of w / assignment (L2-resident) then overlap instead of serialising
-  constexpr int kUnroll = 4;
+  constexpr int kUnroll = NC_K5_UNROLL;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t k0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k0 < n; k0 += stride * kUnroll) {
     double x[kUnroll];
