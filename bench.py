@@ -159,7 +159,7 @@ def make_sim(net, lif, args, delivery, world, record_raster_steps: int = 0):
     if world > 1:
         from paper_2205_07125_b200 import distributed as D
         cap = args.msg_cap if args.msg_cap is not None else (65536 if args.transport == "nccl" else None)
-        fs = {"auto": None, "on": True, "off": False}[args.fused_send]
+        fs = args.fused_send == "on"
         return D.DistSimulator(net, lif, args.seed, None, transport=args.transport, delivery=delivery,
                                msg_cap=cap, latency_steps=args.warmup + args.steps, graph_chunk=args.chunk,
                                record_raster_steps=record_raster_steps, fused_send=fs)
@@ -749,8 +749,9 @@ def main() -> int:
                     help="steps of the benchmarked network checked bit for bit against the oracle (N=1; 0 = off)")
     ap.add_argument("--no-e2e-api", dest="e2e_api", action="store_false",
                     help="skip the simulate() end-to-end measurement (N=1)")
-    ap.add_argument("--fused-send", default="auto", choices=["auto", "on", "off"],
-                    help="N>1, P2P: the step kernel stores its spikes into the peers' inboxes (auto: large shards)")
+    ap.add_argument("--fused-send", default="off", choices=["on", "off"],
+                    help="N>1, P2P: the step kernel stores its spikes into the peers' inboxes (A/B: "
+                         "profiles/r02_fused_send_ab/)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-push", dest="with_push", action="store_false",
                     help="skip the event-driven (push) measurement reported beside the headline")

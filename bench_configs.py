@@ -183,7 +183,7 @@ def main() -> int:
 
     class A:   # the timing helpers' argument bundle
         steps, warmup, chunk, transport, msg_cap, seed, fused_send = (args.steps, args.warmup, args.chunk, "p2p",
-                                                                      None, args.seed, "auto")
+                                                                      None, args.seed, "off")
 
     for rate in rates:
         lif = S.LifParams() if rate is None else S.LifParams.for_rate(rate)

@@ -132,8 +132,6 @@ def choose_delivery(net: Network, lif: LifParams, seed: int, rt: RoutingTable | 
     return min(times, key=times.get), times
 
 
-FUSED_SEND_MIN_ROWS = 32768   # fused P2P send from the step kernel above this many local rows
-
 class DistSimulator:
     """Step loop of this rank's shard with a multi-GPU spike exchange."""
 
@@ -144,8 +142,8 @@ class DistSimulator:
                  blocks_per_peer: int | None = None, fused_send: bool | None = None, group=None,
                  debug_stamps: bool = False):
         """``fused_send``: the fused step kernel stores phase-1 spikes straight into the
-        peers' inboxes (P2P transport); None = on for shards of >= FUSED_SEND_MIN_ROWS
-        rows.  ``group``: collectives for bootstrap (default: torch.distributed)."""
+        peers' inboxes (P2P transport); off by default (see below).  ``group``: collectives
+        for bootstrap (default: torch.distributed)."""
         import torch
         if transport not in ("p2p", "nccl"):
             raise ValueError(f"transport must be 'p2p' or 'nccl', got {transport!r}")
@@ -255,14 +253,14 @@ class DistSimulator:
             self._setup_p2p()
         # fused send (P2P exchange after the fused step): the step kernel stores its bucketed
         # spikes straight into the first hops' inboxes and writes the headers; the exchange
-        # kernel only receives phase 1 (and runs the relay phase of two-level routing).
-        # Only for shards big enough that the step kernel outlasts the transfer: on config 1
-        # (2 500 rows per GPU, a ~5 us step kernel) the last-CTA header pass cost more than
-        # the overlap gained (63.6 k vs 66.9 k steps/s, profiles/r01_cfg1_4gpu_fused_send.jsonl).
-        # fused_send=True / False forces it on / off.
-        big = lay.n_local(self.rank) >= FUSED_SEND_MIN_ROWS
+        # kernel only receives phase 1 (and runs the relay phase of two-level routing).  It
+        # lowers the exposed exchange time (p50, max over ranks, 8.2 -> 7.0 us at 2 GPUs,
+        # 9.6 -> 8.8 us at 4) but the extra stores lengthen the step kernel more than that:
+        # steps/s 3 548 -> 3 495 and 6 602 -> 6 531 (same box, 1 000 steps,
+        # profiles/r02_fused_send_ab/), and on config 1 the last-CTA header pass alone cost
+        # 63.6 k vs 66.9 k steps/s.  So it is off unless asked for (fused_send=True).
         self.fused_send = (transport == "p2p" and delivery == "fused" and int(self.state.bucket_cap) <= cap
-                           and (bool(fused_send) if fused_send is not None else big))
+                           and bool(fused_send))
         if self.fused_send:
             c = self.state.c
             for h in range(n):
