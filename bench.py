@@ -295,18 +295,25 @@ def rank_of(sim) -> int:
     return int(getattr(sim, "rank", 0))
 
 
-def lat_summary(lat, lat_min, transport):
+def lat_summary(lat, lat_min, transport, nccl_msg_bytes=None):
     """Exchange latency per SURVEY 8(d): device %globaltimer per rank and step from
     buckets ready to the last inbound spike in the bitmap; p50/p99 over the timed
     steps of the per-step MAX over ranks.  The per-step MIN over ranks (the rank whose
-    buckets were ready last: transfer + signalling alone) is reported beside it."""
+    buckets were ready last: transfer + signalling alone) is reported beside it.
+    Wire bytes: P2P moves 8 bytes per id (tag + id) + an 8-byte header per message;
+    NCCL moves every message at its full capacity, (cap + 1) x 4 bytes, whatever the
+    spike count (`nccl_msg_bytes` per rank and step)."""
     if lat is None:
         return None
     lat, max_channel_ids, ids_per_rank = lat
-    wire = 8 if transport == "p2p" else 4     # P2P: tagged 8-byte words; NCCL: plain 4-byte ids
     p50 = float(np.percentile(lat, 50))
     p50_min = float(np.percentile(lat_min, 50))
-    bytes_rank = ids_per_rank * wire
+    if transport == "p2p":
+        bytes_rank = ids_per_rank * 8
+        wire = 8
+    else:
+        bytes_rank = float(nccl_msg_bytes) if nccl_msg_bytes is not None else ids_per_rank * 4
+        wire = 4
     return {"p50": round(p50, 2), "p99": round(float(np.percentile(lat, 99)), 2),
             "p50_transfer_only": round(p50_min, 2),
             "p99_transfer_only": round(float(np.percentile(lat_min, 99)), 2),
@@ -314,8 +321,9 @@ def lat_summary(lat, lat_min, transport):
             "max_channel_bytes_per_step": round(max_channel_ids * wire, 1),
             "nvlink_gbs_at_transfer_p50": round(bytes_rank / (p50_min * 1e-6) / 1e9, 2) if p50_min > 0 else None,
             "nvlink_peak_gbs": 900.0,
-            "bytes_note": "ids each rank sends per step x bytes per id on the wire; GB/s = that over the p50 "
-                          "transfer-only time, against 900 GB/s per direction per GPU (latency bound)",
+            "bytes_note": "bytes each rank puts on the wire per step (P2P: 8 B per id; NCCL: every message at "
+                          "its full capacity); GB/s = that over the p50 transfer-only time, against 900 GB/s "
+                          "per direction per GPU (latency bound)",
             "transport": transport,
             "what": "device %globaltimer per step and rank from buckets ready (the exchange kernel's first block, "
                     "which starts after the step kernel) to the last inbound spike ORed into the bitmap; p50/p99 over "
@@ -401,6 +409,9 @@ def run_ours(args) -> dict | None:
     if prof.is_file() and main_kernel == "fused" and world == 1:
         traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
     fused_send = getattr(sim, "fused_send", None)
+    nccl_bytes = None
+    if world > 1 and args.transport == "nccl":   # fixed-capacity messages to every phase-1 peer
+        nccl_bytes = bin(sim.masks["send1"]).count("1") * (sim.cap + 1) * 4
     e2e = e2e_measure(sim, net, args, world, rank, lif)
     launches = max(1, int(round(args.steps * sim.launches_per_step())))
     if world > 1:
@@ -471,7 +482,7 @@ def run_ours(args) -> dict | None:
                          "frac_of_spec": round(achieved / 8000.0, 4)},
             "parity": parity,
             "event_driven": event,
-            "exchange_us": lat_summary(lat, lat_min, args.transport),
+            "exchange_us": lat_summary(lat, lat_min, args.transport, nccl_bytes),
             "cpu_baseline": cpu,
             "e2e": e2e,
             "e2e_api": e2e_api,

@@ -64,7 +64,8 @@ def traffic_from_push(net, rank: int, world: int, dev):
     import torch
     import torch.distributed as dist
     lay = net.layout
-    rowptr, ent = net.shards[rank]._push_cache
+    arr = next(iter(net.shards[rank]._push_arrays.values()))   # any windows: rows are pre ids
+    rowptr, ent = arr["rowptr"], arr["syn"]
     m = torch.zeros((world, world), dtype=torch.int64, device=dev)
     chunk = 1 << 28
     for a in range(world):
@@ -155,7 +156,9 @@ def main() -> int:
     mem = {"after_build_gb": round(torch.cuda.memory_allocated(dev) / GB, 2),
            "build_peak_gb": round(torch.cuda.max_memory_allocated(dev) / GB, 2),
            "pull_layout_gb": round(csr.n_entries * 4 / GB, 2) if want_pull else None,
-           "push_csr_gb": round(csr._push_cache[1].numel() * 4 / GB, 2) if want_push else None,
+           "push_csr_gb": round(next(iter(csr._push_arrays.values()))["syn"].numel() * 4 / GB, 2)
+           if want_push else None,
+           "push_windows": next(iter(csr._push_arrays.values()))["windows"] if want_push else None,
            "gpu_total_gb": round(torch.cuda.get_device_properties(dev).total_memory / GB, 1)}
     nsyn = torch.tensor([net.n_synapses], dtype=torch.int64, device=dev)
     if world > 1:

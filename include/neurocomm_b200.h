@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define NC_ABI_VERSION 3
+#define NC_ABI_VERSION 4
 
 enum {
   NC_OK = 0,
@@ -235,6 +235,16 @@ typedef struct nc_shard {
   int64_t xsend_cap;      /* ids per message = nc_xchg_t.cap */
   int32_t xsend_on;
   int32_t xsend_mask;     /* peers with a phase-1 message (nc_xchg_t.send1_mask) */
+  /* push windows (push_windows > 1): the local post rows are cut into windows of
+   * push_window_rows (multiple of 32); every push row is grouped by window and an
+   * entry holds the post row relative to its window start.  Window w of pre i =
+   * push_syn[push_rowptr[i] + push_winoff[i*(W+1) + w] ... + push_winoff[i*(W+1) + w + 1]).
+   * The persistent engine delivers one window at a time with a grid barrier in
+   * between, so the atomic reductions of a window stay in L2 (config 5 over 2 GPUs:
+   * 25 M post rows = 100 MB of accumulators).  push_windows <= 1: plain rows. */
+  const uint16_t* push_winoff;
+  int32_t push_windows;
+  int32_t push_window_rows;
 } nc_shard_t;
 
 /* Set kernel attributes (dynamic shared memory opt-in) once; call before any
@@ -463,6 +473,14 @@ int nc_greedy_fill_generated(const nc_graphgen_t* spec, const double* weights, i
  * count; < 0 on error. */
 int64_t nc_hostgen_edges(const nc_graphgen_t* spec, int64_t* edge_i, int64_t* edge_j, double* edge_p,
                          int32_t threads);
+/* Windowed push synapses (nc_shard_t push_windows > 1) straight from the
+ * generator.  Phase 0: counts[pre*W + w] += entries of pre in window w (uint32,
+ * zeroed) and the destination masks as nc_graphgen_push; the caller builds
+ * push_rowptr (row totals, scanned) and push_winoff (per-row prefix, < 65536);
+ * phase 1 fills push_syn (fill uint32 [n_pre*W] zeroed). */
+int nc_graphgen_push_windowed(const nc_graphgen_t* g, int32_t phase, int32_t windows, int32_t window_rows,
+                              uint32_t* counts, const int64_t* push_rowptr, const uint16_t* push_winoff,
+                              uint32_t* fill, uint32_t* push_syn, uint16_t* dest_mask, void* stream);
 /* Push synapses (nc_shard_t push_rowptr / push_syn format) straight from the
  * generator, without a pull layout.  Phase 0: push_rowptr[pre + 1] += entries
  * of pre (int64 [n_words*32 + 1], zeroed) and dest_mask[r] |= shards hosting a

@@ -15,7 +15,7 @@ from pathlib import Path
 
 LIB_NAME = "libneurocomm_b200.so"
 LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 NC_OK, NC_E_ARG, NC_E_CUDA, NC_E_OVERFLOW, NC_E_TIMEOUT, NC_E_NCCL, NC_E_PARSE, NC_E_IO = range(8)
 MAX_SHARDS = 16
@@ -55,6 +55,7 @@ class ShardC(C.Structure):
         ("pad3", c_int32), ("spk_ids", c_void_p), ("spk_count", c_void_p), ("spk_cap", c_int64),
         ("kstamp", c_void_p), ("kstamp_steps", c_int32), ("pad4", c_int32),
         ("xsend", c_void_p * MAX_SHARDS), ("xsend_cap", c_int64), ("xsend_on", c_int32), ("xsend_mask", c_int32),
+        ("push_winoff", c_void_p), ("push_windows", c_int32), ("push_window_rows", c_int32),
     ]
 
 
@@ -122,6 +123,8 @@ _SIGS = {
                                    c_void_p, c_void_p]),
     "nc_graphgen_degrees": (c_int32, [C.POINTER(GraphGenC), c_void_p, c_void_p]),
     "nc_graphgen_push": (c_int32, [C.POINTER(GraphGenC), c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "nc_graphgen_push_windowed": (c_int32, [C.POINTER(GraphGenC), c_int32, c_int32, c_int32, c_void_p, c_void_p,
+                                            c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "nc_edges_count": (c_int32, [C.POINTER(GraphGenC), c_void_p, c_void_p, c_int64, c_int32, c_int32, c_void_p,
                                  c_void_p]),
     "nc_edges_fill": (c_int32, [C.POINTER(GraphGenC), c_void_p, c_void_p, c_void_p, c_int64, c_int32, c_int32,

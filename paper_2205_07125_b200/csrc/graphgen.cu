@@ -297,6 +297,49 @@ __global__ void k_push_gen(const nc_graphgen_t g, int phase, unsigned long long*
   }
 }
 
+// Windowed push (nc_shard_t push_windows): the same enumeration, entries grouped
+// by the window of their post row and stored relative to the window start.
+__global__ void k_push_gen_win(const nc_graphgen_t g, int phase, int W, int wrows, uint32_t* cnt,
+                               const int64_t* rowptr, const uint16_t* winoff, uint32_t* fill, uint32_t* out,
+                               uint16_t* dest) {
+  const Comm cm = make_comm(g);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.n_neurons;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t oi = g.owner[i];
+    const uint32_t iid = (uint32_t)g.internal_id[i];
+    const uint32_t inh_i = is_inh(g, i);
+    for_each_upper(g, cm, i, [&](int64_t j, bool intra) {
+      const int32_t oj = g.owner[j];
+      if (oi != g.shard && oj != g.shard) return;
+      const uint32_t jid = (uint32_t)g.internal_id[j];
+      // (pre, local post) pairs of this edge on this shard
+      const int64_t rj = (int64_t)jid - g.local_base, ri = (int64_t)iid - g.local_base;
+      if (phase == 0) {
+        if (oj == g.shard) atomicAdd(cnt + (int64_t)iid * W + rj / wrows, 1u);
+        if (oi == g.shard) atomicAdd(cnt + (int64_t)jid * W + ri / wrows, 1u);
+        if (oi != oj) {
+          if (oi == g.shard) or_dest(dest, ri, 1u << oj);
+          else or_dest(dest, rj, 1u << oi);
+        }
+        return;
+      }
+      const uint32_t q = edge_q(g, i, j, intra);
+      if (oj == g.shard) {
+        const int64_t w = rj / wrows, key = (int64_t)iid * W + w;
+        const uint32_t k = atomicAdd(fill + key, 1u);
+        out[rowptr[iid] + winoff[(int64_t)iid * (W + 1) + w] + k] =
+            (inh_i << 31) | ((q - 1u) << 26) | (uint32_t)(rj - w * wrows);
+      }
+      if (oi == g.shard) {
+        const int64_t w = ri / wrows, key = (int64_t)jid * W + w;
+        const uint32_t k = atomicAdd(fill + key, 1u);
+        out[rowptr[jid] + winoff[(int64_t)jid * (W + 1) + w] + k] =
+            (is_inh(g, j) << 31) | ((q - 1u) << 26) | (uint32_t)(ri - w * wrows);
+      }
+    });
+  }
+}
+
 // Pad pre-fill of the unpacked padded layout: the pad entry (q = 0) is 0.
 __global__ void k_fill_pads(const int64_t* slice_ptr, int64_t n_blocks, uint32_t* syn) {
   for (int64_t b = blockIdx.x; b < n_blocks; b += gridDim.x)
@@ -495,6 +538,23 @@ extern "C" int nc_graphgen_push(const nc_graphgen_t* g, int32_t phase, int64_t* 
   }
   k_push_gen<<<grid_for(g->n_neurons, 128), 128, 0, (cudaStream_t)stream>>>(
       *g, phase, reinterpret_cast<unsigned long long*>(push_rowptr), push_rowptr, push_fill, push_syn, dest_mask);
+  NC_LAUNCH_CHECK();
+  return NC_OK;
+}
+
+extern "C" int nc_graphgen_push_windowed(const nc_graphgen_t* g, int32_t phase, int32_t windows, int32_t window_rows,
+                                         uint32_t* counts, const int64_t* push_rowptr, const uint16_t* push_winoff,
+                                         uint32_t* fill, uint32_t* push_syn, uint16_t* dest_mask, void* stream) {
+  if (!g || g->n_neurons < 1 || g->n_communities < 1 || g->n_communities > g->n_neurons || !g->owner ||
+      !g->internal_id || windows < 1 || window_rows < 32 || (window_rows & 31) ||
+      (int64_t)windows * window_rows < g->n_local ||
+      (phase == 0 && (!counts || !dest_mask)) || (phase == 1 && (!push_rowptr || !push_winoff || !fill || !push_syn)) ||
+      (phase != 0 && phase != 1)) {
+    nc_set_error("nc_graphgen_push_windowed: bad arguments");
+    return NC_E_ARG;
+  }
+  k_push_gen_win<<<grid_for(g->n_neurons, 128), 128, 0, (cudaStream_t)stream>>>(
+      *g, phase, windows, window_rows, counts, push_rowptr, push_winoff, fill, push_syn, dest_mask);
   NC_LAUNCH_CHECK();
   return NC_OK;
 }

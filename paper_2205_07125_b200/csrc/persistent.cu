@@ -62,7 +62,14 @@ __global__ void __launch_bounds__(kPThreads) k_persistent(const nc_shard_t sh, c
   const bool ph = phase_st && bid == 0 && threadIdx.x == 0;
   for (int s = 0; s < n_steps; ++s, ++step) {
     if (ph && s < 64) phase_st[s * 4 + 0] = gtimer();
-    ncdev::push_phase(sh, negg, step, P);
+    if (sh.push_windows > 1) {   // one window of post rows at a time: its reductions stay in L2
+      for (int w = 0; w < sh.push_windows; ++w) {
+        ncdev::push_phase(sh, negg, step, P, w);
+        if (w + 1 < sh.push_windows) grid_sync(gbar, ++k * nblk, sh.status);
+      }
+    } else {
+      ncdev::push_phase(sh, negg, step, P);
+    }
     grid_sync(gbar, ++k * nblk, sh.status);
     if (ph && s < 64) phase_st[s * 4 + 1] = gtimer();
     ncdev::lif_phase(sh, p, step, bid, nblk, S);
@@ -76,6 +83,7 @@ __global__ void __launch_bounds__(kPThreads) k_persistent(const nc_shard_t sh, c
       if (threadIdx.x == 0 && st_done && step < stamp_cap) st_done[step] = gtimer();
       if ((int)threadIdx.x < sh.n_shards) sh.bucket_count[threadIdx.x] = 0;
       if (threadIdx.x == 0) sh.work[0] = 0u;   // push chunk claims of the next step
+      if ((int)threadIdx.x < sh.push_windows) sh.work[4 + threadIdx.x] = 0u;   // windowed claims
       if (has_x && (int)threadIdx.x < X.n) X.fwd_count[threadIdx.x] = 0;
       if (threadIdx.x == 0 && sh.fired_count) *sh.fired_count = 0;
     }
@@ -108,6 +116,12 @@ extern "C" int nc_run_persistent(const nc_shard_t* sh, const nc_lif_params_t* p,
   if (!sh || !p || !gbar || n_steps < 0 || !sh->push_rowptr || !sh->push_syn || !sh->acc || !sh->step ||
       !sh->status || !sh->work) {
     nc_set_error("nc_run_persistent: shard needs push CSR, acc, step and status buffers");
+    return NC_E_ARG;
+  }
+  if (sh->push_windows > 1 && (!sh->push_winoff || sh->push_windows > 32 || sh->push_window_rows < 32 ||
+                                (int64_t)sh->push_windows * sh->push_window_rows < sh->n_local)) {
+    nc_set_error("nc_run_persistent: bad push windows (%d x %d rows, winoff %p)", sh->push_windows,
+                 sh->push_window_rows, (const void*)sh->push_winoff);
     return NC_E_ARG;
   }
   if (X && X->fused_send) {   // this engine sends from its exchange blocks; nothing would write the inboxes

@@ -484,14 +484,40 @@ struct PushSmem {
   uint32_t ids[kPushIds];
 };
 
-static __device__ void push_phase(const nc_shard_t& sh, int32_t negg, int step, PushSmem& P) {
+// Entries [beg, end) of one push row (or window of it) into acc: 8 loads in flight per
+// lane, integer reductions; `base` = first post row of the window.
+__device__ __forceinline__ void push_segment(const nc_shard_t& sh, int32_t negg, int64_t beg, int64_t end,
+                                             int base, int lane) {
+  for (int64_t e0 = beg + lane; e0 < end; e0 += 256) {
+    uint32_t x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = (e0 + 32 * u < end) ? __ldg(sh.push_syn + e0 + 32 * u) : 0u;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (e0 + 32 * u < end) {
+        const int32_t q = (int32_t)((x[u] >> 26) & 31u) + 1;
+        red_add(sh.acc + base + (x[u] & 0x03FFFFFFu), (x[u] >> 31) ? q * negg : q);
+      }
+    }
+  }
+}
+
+// Event-driven delivery of the previous step's spikes.  Blocks claim 32-word
+// chunks of the spike bitmap, warp 0 compacts the chunk's spikes, the warps walk
+// their push rows.  Windowed push (sh.push_windows > 1): window `window` only
+// (its own claim counter work[4 + window]; the persistent engine runs the windows
+// one after the other with a grid barrier in between), or every window of each
+// row (window < 0, k_deliver_push).
+static __device__ void push_phase(const nc_shard_t& sh, int32_t negg, int step, PushSmem& P, int window = -1) {
   const uint32_t* prev = ((step - 1) & 1) ? sh.bitmap1 : sh.bitmap0;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
   const int n_chunks = (sh.n_words + 31) >> 5;
+  const int W = sh.push_windows > 1 ? sh.push_windows : 1;
+  uint32_t* claim = (W > 1 && window >= 0) ? sh.work + 4 + window : sh.work;
   for (;;) {
-    if (threadIdx.x == 0) P.chunk = (int)atomicAdd(sh.work, 1u);
+    if (threadIdx.x == 0) P.chunk = (int)atomicAdd(claim, 1u);
     __syncthreads();
     const int c = P.chunk;
     if (c >= n_chunks) break;
@@ -516,19 +542,15 @@ static __device__ void push_phase(const nc_shard_t& sh, int32_t negg, int step, 
     __syncthreads();
     for (int i = warp; i < P.n; i += nwarps) {
       const uint32_t pre = P.ids[i];
-      const int64_t beg = sh.push_rowptr[pre], end = sh.push_rowptr[pre + 1];
-      for (int64_t e0 = beg + lane; e0 < end; e0 += 256) {
-        uint32_t x[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) x[u] = (e0 + 32 * u < end) ? __ldg(sh.push_syn + e0 + 32 * u) : 0u;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          if (e0 + 32 * u < end) {
-            const int32_t q = (int32_t)((x[u] >> 26) & 31u) + 1;
-            red_add(sh.acc + (x[u] & 0x03FFFFFFu), (x[u] >> 31) ? q * negg : q);
-          }
-        }
+      const int64_t r0 = sh.push_rowptr[pre];
+      if (W == 1) {
+        push_segment(sh, negg, r0, sh.push_rowptr[pre + 1], 0, lane);
+        continue;
       }
+      const uint16_t* wo = sh.push_winoff + (int64_t)pre * (W + 1);
+      const int w0 = window >= 0 ? window : 0, w1 = window >= 0 ? window + 1 : W;
+      for (int w = w0; w < w1; ++w)
+        push_segment(sh, negg, r0 + wo[w], r0 + wo[w + 1], w * sh.push_window_rows, lane);
     }
     __syncthreads();
   }

@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(256) k_deliver_push(const nc_shard_t sh, int32
 __global__ void k_end_step(const nc_shard_t sh) {
   const int t = threadIdx.x;
   if (t < sh.n_shards) sh.bucket_count[t] = 0;
-  if (t < 4 && sh.work) sh.work[t] = 0u;
+  if (t < 4 + (sh.push_windows > 1 ? sh.push_windows : 0) && sh.work) sh.work[t] = 0u;
   if (t == 0) {
     if (sh.fired_count) *sh.fired_count = 0;
     if (sh.spk_count) sh.spk_count[(*sh.step + 1) & 1] = 0;   // the list step + 1 appends to
@@ -258,7 +258,7 @@ __global__ void k_init(const nc_shard_t sh, const nc_lif_params_t p) {
     sh.bitmap1[w] = 0u;
   }
   if (t0 < sh.n_shards) sh.bucket_count[t0] = 0;
-  if (t0 < 4 && sh.work) sh.work[t0] = 0u;
+  if (t0 < 4 + (sh.push_windows > 1 ? sh.push_windows : 0) && sh.work) sh.work[t0] = 0u;
   if (t0 < 2 && sh.spk_count) sh.spk_count[t0] = 0;
   if (t0 == 0) {
     *sh.step = 0;
@@ -423,7 +423,8 @@ extern "C" int nc_sim_deliver_pull(const nc_shard_t* sh, int32_t g_inh, void* st
 
 extern "C" int nc_sim_deliver_push(const nc_shard_t* sh, int32_t g_inh, void* stream) {
   if (int e = check_shard(sh)) return e;
-  if (!sh->push_rowptr || !sh->push_syn || !sh->acc || !sh->work) {
+  if (!sh->push_rowptr || !sh->push_syn || !sh->acc || !sh->work ||
+      (sh->push_windows > 1 && (!sh->push_winoff || sh->push_windows > 32))) {
     nc_set_error("nc_sim_deliver_push: shard has no push CSR / acc / work counters");
     return NC_E_ARG;
   }
@@ -454,7 +455,7 @@ extern "C" int nc_sim_lif_update(const nc_shard_t* sh, const nc_lif_params_t* p,
 
 extern "C" int nc_sim_end_step(const nc_shard_t* sh, void* stream) {
   if (int e = check_shard(sh)) return e;
-  k_end_step<<<1, 32, 0, (cudaStream_t)stream>>>(*sh);
+  k_end_step<<<1, 64, 0, (cudaStream_t)stream>>>(*sh);
   NC_LAUNCH_CHECK();
   return NC_OK;
 }

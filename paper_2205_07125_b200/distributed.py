@@ -140,7 +140,7 @@ class DistSimulator:
                  record_raster_steps: int = 0, per_step_counts: bool = False, latency_steps: int = 4096,
                  use_graph: bool = True, graph_chunk: int = 64, timeout_s: float = 10.0,
                  blocks_per_peer: int | None = None, fused_send: bool | None = None, group=None,
-                 debug_stamps: bool = False):
+                 debug_stamps: bool = False, push_windows: int | None = None):
         """``fused_send``: the fused step kernel stores phase-1 spikes straight into the
         peers' inboxes (P2P transport); off by default (see below).  ``group``: collectives
         for bootstrap (default: torch.distributed)."""
@@ -192,10 +192,12 @@ class DistSimulator:
             cap = min(cap, int(msg_cap))
         self.cap = max(cap, 1)
         del probe
+        from .sim import push_windows_for
+        if push_windows is None:
+            push_windows = push_windows_for(lay.n_local(self.rank)) if delivery == "persistent" else 1
         self.state = _ShardState(net, self.rank, self.plan, record_steps=record_raster_steps,
                                  push=(delivery in ("push", "persistent")), binned=(delivery == "binned"),
-                                 bucket_cap=None,
-                                 bucket_stride=self.cap)
+                                 bucket_cap=None, bucket_stride=self.cap, push_windows=push_windows)
         self.states = [self.state]
         self.record_steps = int(record_raster_steps)
         self.dest_global = gather_dest(net, self.rank, self.world, dev, self.g)

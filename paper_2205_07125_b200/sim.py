@@ -346,13 +346,14 @@ class Network:
     @classmethod
     def generate(cls, spec: GeneratorSpec, layout: ShardLayout, *, device=None, inh_every: int = 5,
                  shards=None, tile_words: int | None = None, bank_order: bool = True, pull: bool = True,
-                 push: bool = False) -> "Network":
+                 push: bool = False, push_windows: int | None = None) -> "Network":
         """Counter-based device generator (csrc/graphgen.cu); every shard regenerates the same graph.
 
         ``pull``: the J-SELL pull layout (fused / pull / binned delivery).  ``push``:
         the push CSR of the event-driven engines, generated directly (without the
         pull layout when ``pull`` is False: 4 B per synapse instead of 3.2 + 4 + the
-        build's transient 8)."""
+        build's transient 8), grouped into ``push_windows`` post-row windows (None:
+        push_windows_for(rows of the shard), what the persistent engine wants)."""
         import torch
         if not (pull or push):
             raise ValueError("generate at least one of the pull and push layouts")
@@ -391,8 +392,9 @@ class Network:
                     inter_lo=spec.inter_p_range[0], inter_hi=spec.inter_p_range[1],
                     seed=int(spec.seed) & (2**64 - 1), owner=owner_d.data_ptr(), internal_id=internal_d.data_ptr(),
                     local_base=int(layout.base[h]), inh_every=inh_every, n_local=n_local)
-                csr.dest = _generate_push(g, csr, layout, h, dev)
-                csr.n_real = int(csr._push_cache[0][-1].item())
+                win = push_windows if push_windows is not None else push_windows_for(n_local)
+                csr.dest = _generate_push(g, csr, layout, h, dev, win)
+                csr.n_real = int(csr._push_total)
                 out[h] = csr
                 nsyn += csr.n_real
                 continue
@@ -410,7 +412,8 @@ class Network:
             csr, n_real = _build_pull_shard(layout, h, dev, sms, tile_words, False, bank_order, count, fill)
             csr.dest = _dest_masks(csr, layout, h, dev)
             if push:
-                _generate_push(g, csr, layout, h, dev)
+                _generate_push(g, csr, layout, h, dev,
+                               push_windows if push_windows is not None else push_windows_for(n_local))
             out[h] = csr
             nsyn += n_real
         return cls(layout, out, dev, inh_every, n_synapses=nsyn, source="device generator")
@@ -523,14 +526,43 @@ def _push_only_csr(layout: ShardLayout, h: int, dev) -> ShardCSR:
     return csr
 
 
-def _generate_push(g, csr: ShardCSR, layout: ShardLayout, h: int, dev):
-    """Push CSR of shard h straight from the generator (nc_graphgen_push), cached on the
-    SellCSR like _push_csr's transpose; returns the destination masks (int32 [n_local])."""
+def _generate_push(g, csr: ShardCSR, layout: ShardLayout, h: int, dev, windows: int = 1):
+    """Push CSR of shard h straight from the generator (nc_graphgen_push, or
+    nc_graphgen_push_windowed for windows > 1), cached on the SellCSR like the
+    transposes (push_arrays); returns the destination masks (int32 [n_local])."""
     import torch
     L = _native.lib()
     st = _native.stream_handle(dev)
     n_pre = layout.n_words * 32
     n_local = layout.n_local(h)
+    if windows > 1:
+        rows = max(32, ((n_local + 31) // 32 + windows - 1) // windows * 32)
+        dest16 = torch.zeros(n_local + 2, dtype=torch.int16, device=dev)
+        counts = torch.zeros(n_pre * windows, dtype=torch.int32, device=dev)
+        _native.check(L.nc_graphgen_push_windowed(C.byref(g), 0, windows, rows, counts.data_ptr(), None, None, None,
+                                                  None, dest16.data_ptr(), st), "graphgen windowed push count")
+        run = torch.cumsum(counts.view(n_pre, windows), 1, dtype=torch.int64)
+        row_len = run[:, -1]
+        if n_pre and int(row_len.max().item()) >= 1 << 16:
+            raise ValueError("windowed push: a pre neuron has >= 65536 local synapses (16-bit offsets)")
+        winoff = torch.zeros((n_pre, windows + 1), dtype=torch.int32, device=dev)
+        winoff[:, 1:] = run.to(torch.int32)
+        winoff16 = winoff.to(torch.int16)
+        rowptr = torch.zeros(n_pre + 1, dtype=torch.int64, device=dev)
+        rowptr[1:] = torch.cumsum(row_len, 0)
+        del run, winoff, row_len
+        total = int(rowptr[-1].item())
+        ent = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+        counts.zero_()
+        _native.check(L.nc_graphgen_push_windowed(C.byref(g), 1, windows, rows, None, rowptr.data_ptr(),
+                                                  winoff16.data_ptr(), counts.data_ptr(), ent.data_ptr(), None, st),
+                      "graphgen windowed push fill")
+        torch.cuda.synchronize(dev)
+        del counts
+        csr.__dict__.setdefault("_push_arrays", {})[windows] = {
+            "rowptr": rowptr, "syn": ent, "winoff": winoff16, "windows": windows, "rows": rows}
+        csr._push_total = total
+        return dest16[:n_local].to(torch.int32) & 0xFFFF
     rowptr = torch.zeros(n_pre + 1, dtype=torch.int64, device=dev)
     dest16 = torch.zeros(n_local + 2, dtype=torch.int16, device=dev)
     _native.check(L.nc_graphgen_push(C.byref(g), 0, rowptr.data_ptr(), None, None, dest16.data_ptr(), st),
@@ -544,6 +576,9 @@ def _generate_push(g, csr: ShardCSR, layout: ShardLayout, h: int, dev):
     torch.cuda.synchronize(dev)
     del fill
     csr._push_cache = (rowptr, ent)
+    csr.__dict__.setdefault("_push_arrays", {})[1] = {"rowptr": rowptr, "syn": ent, "winoff": None, "windows": 1,
+                                                      "rows": 0}
+    csr._push_total = total
     return dest16[:n_local].to(torch.int32) & 0xFFFF
 
 
@@ -668,7 +703,8 @@ class _ShardState:
     """Device buffers and the C descriptor of one shard."""
 
     def __init__(self, net: Network, h: int, plan: ExchangePlan, *, record_steps: int, push: bool,
-                 bucket_cap: int | None, bucket_stride: int | None = None, binned: bool = False):
+                 bucket_cap: int | None, bucket_stride: int | None = None, binned: bool = False,
+                 push_windows: int = 1):
         import torch
         lay = net.layout
         dev = net.device
@@ -707,10 +743,12 @@ class _ShardState:
         self.raster = torch.zeros((max(self.record_steps, 1), max(self.local_words, 1)), dtype=torch.int32,
                                   device=dev)
         self.spike_total = torch.zeros(1, dtype=torch.int64, device=dev)
-        self.work = torch.zeros(4, dtype=torch.int32, device=dev)
+        self.work = torch.zeros(4 + 32, dtype=torch.int32, device=dev)   # + per-window push claims
         self.push_rowptr = self.push_syn = None
+        self.push = None
         if push:
-            self.push_rowptr, self.push_syn = _push_csr(csr, lay, h, dev)
+            self.push = push_arrays(csr, lay, h, dev, push_windows)
+            self.push_rowptr, self.push_syn = self.push["rowptr"], self.push["syn"]
         self.pb = None
         self.spk_ids = self.spk_count = None
         if binned:
@@ -736,6 +774,9 @@ class _ShardState:
             record_steps=self.record_steps, local_words=self.local_words,
             spike_total=self.spike_total.data_ptr(), work=self.work.data_ptr(),
             row_perm=None if csr.row_perm is None else csr.row_perm.data_ptr(), cta_groups=csr.cta_groups)
+        if self.push is not None and self.push["windows"] > 1:
+            self.c.push_winoff = self.push["winoff"].data_ptr()
+            self.c.push_windows, self.c.push_window_rows = self.push["windows"], self.push["rows"]
         if self.pb is not None:
             self.c.pb_bins, self.c.pb_rows = self.pb["bins"], self.pb["rows"]
             self.c.pb_rowptr = self.pb["rowptr"].data_ptr()
@@ -745,19 +786,20 @@ class _ShardState:
                                                                 self.spk_cap)
 
 
-def _push_binned(csr: ShardCSR, lay: ShardLayout, h: int, dev):
+def _push_binned(csr: ShardCSR, lay: ShardLayout, h: int, dev, bins: int | None = None):
     """Binned push synapses of one shard (include/neurocomm_b200.h, nc_shard_t pb_*):
-    rows = internal pre ids, entries grouped by the bin (CTA of k_step_binned) that
-    owns their post row; built on the device by nc_build_push_binned.  Cached on
-    the SellCSR."""
+    rows = internal pre ids, entries grouped by the bin that owns their post row;
+    built on the device by nc_build_push_binned.  bins = the SM count for
+    k_step_binned (a CTA per bin), or a few L2-sized windows for the persistent
+    engine (nc_shard_t push_windows: the same format).  Cached on the SellCSR."""
     import torch
-    cached = getattr(csr, "_binned_cache", None)
-    if cached is not None:
-        return cached
     L = _native.lib()
     st = _native.stream_handle(dev)
     n_local = lay.n_local(h)
-    bins = sell.device_sms(dev)
+    bins = sell.device_sms(dev) if bins is None else int(bins)
+    cache = csr.__dict__.setdefault("_binned_cache", {})
+    if bins in cache:
+        return cache[bins]
     rows = max(32, ((n_local + 31) // 32 + bins - 1) // bins * 32)
     n_pre = lay.n_words * 32
     scratch = torch.zeros(8, dtype=torch.int32, device=dev)
@@ -790,7 +832,41 @@ def _push_binned(csr: ShardCSR, lay: ShardLayout, h: int, dev):
     torch.cuda.synchronize(dev)
     del counts, scratch
     out = {"bins": bins, "rows": rows, "rowptr": rowptr, "binoff": binoff16, "syn": syn}
-    csr._binned_cache = out
+    cache[bins] = out
+    return out
+
+
+PUSH_WINDOW_BYTES = 32 << 20   # int32 accumulators per push window: one window's reductions stay in L2
+
+
+def push_windows_for(n_local: int) -> int:
+    """Windows of the persistent engine's push delivery for a shard (nc_shard_t
+    push_windows): 1 while the shard's accumulators (4 B per post row) fit in
+    PUSH_WINDOW_BYTES, else enough windows of at most that size (config 5 over 2
+    GPUs: 25 M rows -> 3 windows)."""
+    return int(min(32, max(1, -(-int(n_local) * 4 // PUSH_WINDOW_BYTES))))
+
+
+def push_arrays(csr: ShardCSR, lay: ShardLayout, h: int, dev, windows: int = 1) -> dict:
+    """Push synapses of one shard for the event-driven engines: {"rowptr", "syn",
+    "winoff", "windows", "rows"}; windows > 1 groups every row by post-row window
+    (entries relative to the window start).  Generated directly by Network.generate
+    (push=True) or transposed from the pull layout here; cached on the SellCSR."""
+    cache = csr.__dict__.setdefault("_push_arrays", {})
+    if windows in cache:
+        return cache[windows]
+    if not getattr(csr, "has_pull", True):
+        if not cache:
+            raise ValueError("this shard has neither a pull layout nor push synapses")
+        return next(iter(cache.values()))   # push-only network: the windows it was generated with
+    if windows <= 1:
+        rowptr, ent = _push_csr(csr, lay, h, dev)
+        out = {"rowptr": rowptr, "syn": ent, "winoff": None, "windows": 1, "rows": 0}
+    else:
+        pb = _push_binned(csr, lay, h, dev, bins=windows)
+        out = {"rowptr": pb["rowptr"], "syn": pb["syn"], "winoff": pb["binoff"], "windows": windows,
+               "rows": pb["rows"]}
+    cache[windows] = out
     return out
 
 
@@ -885,7 +961,8 @@ class Simulator:
 
     def __init__(self, net: Network, lif: LifParams = LifParams(), seed: int = 0, rt: RoutingTable | None = None,
                  *, delivery: str = "fused", record_raster_steps: int = 0, per_step_counts: bool = False,
-                 bucket_cap: int | None = None, use_graph: bool = True, graph_chunk: int = 64):
+                 bucket_cap: int | None = None, use_graph: bool = True, graph_chunk: int = 64,
+                 push_windows: int | None = None):
         import torch
         if delivery not in ("fused", "push", "pull", "persistent", "binned"):
             raise ValueError(f"delivery must be 'fused', 'pull', 'push', 'binned' or 'persistent', got {delivery!r}")
@@ -908,7 +985,9 @@ class Simulator:
         self.record_steps = int(record_raster_steps)
         self.states = [
             _ShardState(net, h, self.plan, record_steps=self.record_steps, push=(delivery in ("push", "persistent")),
-                        bucket_cap=bucket_cap, binned=(delivery == "binned"))
+                        bucket_cap=bucket_cap, binned=(delivery == "binned"),
+                        push_windows=(push_windows if push_windows is not None else
+                                      push_windows_for(net.layout.n_local(h)) if delivery == "persistent" else 1))
             for h in range(self.n)
         ]
         dev = net.device
@@ -1083,7 +1162,7 @@ def delivery_candidates(net: Network) -> list:
     out = []
     if all(getattr(c, "has_pull", True) for c in net.shards.values()):
         out.append("fused")
-    cached = all(getattr(c, "_push_cache", None) is not None for c in net.shards.values())
+    cached = all(getattr(c, "_push_arrays", None) for c in net.shards.values())
     free = torch.cuda.mem_get_info(net.device)[0]
     if cached or 4.4 * net.n_synapses + 2e9 < free:
         out.append("persistent" if net.layout.n_shards == 1 else "push")
