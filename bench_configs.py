@@ -99,6 +99,8 @@ def main() -> int:
     ap.add_argument("--routes", default=None, help="direct,two-level (default: per config)")
     ap.add_argument("--neurons", type=int, default=None, help="override the config's neuron count (tests)")
     ap.add_argument("--chunk", type=int, default=100)
+    ap.add_argument("--push-windows", type=int, default=None,
+                    help="post-row windows of the push CSR (default: sim.push_windows_for per shard)")
     ap.add_argument("--partition", default="blocks",
                     help="blocks | greedy[:file.npz]: the reference's partition_greedy of the generated network "
                          "(partition_greedy_generated; loaded from the .npz tools/k6_config3.py writes when given, "
@@ -149,7 +151,8 @@ def main() -> int:
         raise SystemExit(f"unknown --partition {args.partition!r}")
     torch.cuda.reset_peak_memory_stats(dev)
     t0 = time.time()
-    net = S.Network.generate(spec, lay, device=dev, shards=[rank], pull=want_pull, push=want_push)
+    net = S.Network.generate(spec, lay, device=dev, shards=[rank], pull=want_pull, push=want_push,
+                             push_windows=args.push_windows)
     torch.cuda.synchronize()
     build_s = time.time() - t0
     csr = net.shards[rank]
@@ -195,11 +198,13 @@ def main() -> int:
                 if eng in skipped or (eng == "fused" and not want_pull) or (eng != "fused" and not want_push):
                     continue
                 t_case = time.time()
+                pw = args.push_windows if eng == "persistent" else None
                 if world > 1:
                     sim = DistSimulator(net, lif, args.seed, rt, transport="p2p", delivery=eng,
-                                        latency_steps=args.warmup + args.steps, graph_chunk=args.chunk)
+                                        latency_steps=args.warmup + args.steps, graph_chunk=args.chunk,
+                                        push_windows=pw)
                 else:
-                    sim = S.Simulator(net, lif, args.seed, rt, delivery=eng, graph_chunk=args.chunk)
+                    sim = S.Simulator(net, lif, args.seed, rt, delivery=eng, graph_chunk=args.chunk, push_windows=pw)
                 if eng == "fused":
                     B.enable_kernel_stamps(sim, args.warmup + args.steps)
                 clocks = B.ClockSampler(local)
@@ -210,6 +215,7 @@ def main() -> int:
                 if world > 1:
                     dist.all_reduce(hop)
                 fused_send = getattr(sim, "fused_send", None)
+                sim_windows = sim.states[0].c.push_windows if eng != "fused" else None
                 if world > 1:
                     sim.close()
                 del sim
@@ -230,7 +236,8 @@ def main() -> int:
                     "channel_ids_per_step": np.round(h, 1).tolist(),
                     "neurons": n, "synapses": int(nsyn.item()), "communities": cfg["communities"],
                     "partition": args.partition.split(":")[0], "partition_s": part_s, "bitmap_tiles": csr.n_tiles if want_pull else None,
-                    "fused_send": fused_send, "memory_per_gpu": mem, "build_s": round(build_s, 1),
+                    "fused_send": fused_send, "memory_per_gpu": mem,
+                    "push_windows": sim_windows, "build_s": round(build_s, 1),
                     "planner": planner, "clocks": clocks.summary(), "case_s": round(time.time() - t_case, 1),
                     "skipped_engines": skipped or None,
                 }

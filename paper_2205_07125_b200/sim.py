@@ -836,14 +836,14 @@ def _push_binned(csr: ShardCSR, lay: ShardLayout, h: int, dev, bins: int | None 
     return out
 
 
-PUSH_WINDOW_BYTES = 32 << 20   # int32 accumulators per push window: one window's reductions stay in L2
+PUSH_WINDOW_BYTES = 64 << 20   # int32 accumulators per push window (config 3 on 1 GPU, 40 MB: 1 window is fastest)
 
 
 def push_windows_for(n_local: int) -> int:
     """Windows of the persistent engine's push delivery for a shard (nc_shard_t
     push_windows): 1 while the shard's accumulators (4 B per post row) fit in
     PUSH_WINDOW_BYTES, else enough windows of at most that size (config 5 over 2
-    GPUs: 25 M rows -> 3 windows)."""
+    GPUs: 25 M rows -> 2 windows)."""
     return int(min(32, max(1, -(-int(n_local) * 4 // PUSH_WINDOW_BYTES))))
 
 
