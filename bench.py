@@ -393,6 +393,9 @@ def run_ours(args) -> dict | None:
     # SURVEY 8(d)'s pull formula (8 B per synapse: 4 B pre id + 4 B weight, 8 B rowptr and 4 B input
     # per neuron, the bitmap) for the same step -- what an unpacked CSR would have to move
     pull_bytes = int(net.n_synapses) * 8 + (n_local + 1) * 8 + n_local * 4 + lay.n_neurons // 8
+    layout_bytes = (csr.n_entries * 4 + csr.row_meta.numel() * 4 + csr.slice_ptr.numel() * 8
+                    + (csr.row_perm.numel() * 4 if csr.row_perm is not None else 0) + n_local * 22
+                    + 2 * lay.n_words * 4)
     peaks = load_peaks()
     if main_kernel != "fused":
         fired_syn = spikes / max(args.steps, 1) * args.degree / max(world, 1)
@@ -469,6 +472,9 @@ def run_ours(args) -> dict | None:
                          "kernel_ms": round(kms, 5), "algorithmic_bytes": int(alg_bytes),
                          "bytes_formula": "packed J-SELL: 3.2 B/synapse + 26 B/neuron + bitmaps (DESIGN.md section 5)",
                          "pull_formula_bytes": int(pull_bytes),
+                         "layout_bytes": int(layout_bytes),
+                         "layout_note": "bytes the layout actually streams per step (J-SELL array incl. its per-"
+                                        "(row, tile) segment padding, row_meta, row_perm, block starts, neuron state)",
                          "pull_formula_note": "SURVEY 8(d) pull formula (8 B/synapse unpacked CSR) for the same step; "
                                               "its GB/s over kernel_ms would read %.2fx the copy peak -- the packing, "
                                               "not skipped work (ncu DRAM bytes = traffic)"

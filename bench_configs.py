@@ -243,7 +243,15 @@ def main() -> int:
                 }
                 if eng == "fused" and kms:
                     alg = net.n_synapses * 16 / 5 + lay.n_local(rank) * (4 * csr.n_tiles + 22)
-                    row["roofline_frac_rank0"] = round(alg / (kms_ranks[0] * 1e-3) / B.load_peaks()["hbm_gbs"] / GB, 3)
+                    peak = B.load_peaks()["hbm_gbs"] * GB
+                    row["roofline_frac_rank0"] = round(alg / (kms_ranks[0] * 1e-3) / peak, 3)
+                    # the bytes the layout actually streams: the J-SELL array with its per-(row, tile)
+                    # segment padding, row_meta and row_perm per (row, tile), block starts, state
+                    lay_bytes = (csr.n_entries * 4 + csr.row_meta.numel() * 4 + csr.slice_ptr.numel() * 8
+                                 + (csr.row_perm.numel() * 4 if csr.row_perm is not None else 0)
+                                 + lay.n_local(rank) * 22)
+                    row["layout_bytes_rank0"] = int(lay_bytes)
+                    row["layout_frac_rank0"] = round(lay_bytes / (kms_ranks[0] * 1e-3) / peak, 3)
                 print(json.dumps(row), flush=True)
                 if out_path:
                     with out_path.open("a") as f:
