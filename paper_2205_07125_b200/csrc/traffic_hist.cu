@@ -30,7 +30,13 @@ namespace {
 #endif
 constexpr int kThreads = NC_K5_THREADS;
 constexpr size_t kSmemLimit = 96 * 1024;    // fall back to global limbs above this
-constexpr size_t kSmemBudget = 32 * 1024;   // lane copies are halved down to this
+#ifndef NC_K5_SMEM_KB
+#define NC_K5_SMEM_KB 16
+#endif
+#ifndef NC_K5_MIN_BLOCKS
+#define NC_K5_MIN_BLOCKS 1
+#endif
+constexpr size_t kSmemBudget = NC_K5_SMEM_KB * 1024;   // lane copies are halved down to this
 
 struct Decomposed {
   unsigned long long mant;  // integer mantissa (0 => nothing to add)
@@ -121,7 +127,7 @@ int copy_stride(int cells, int n_digits) { return (cells * n_digits * 2) | 1; } 
 // kPacked: w points at one 16-byte record per neuron {double w; int32 gpu; pad}
 // (nc_traffic_histogram_packed): one gather per endpoint instead of two.
 template <typename Idx, bool kPacked = false>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, NC_K5_MIN_BLOCKS)
 k_histogram_smem(const Idx* __restrict__ ei, const Idx* __restrict__ ej, const double* __restrict__ ep,
                  const double* __restrict__ w, const Idx* __restrict__ asg, int64_t n, int n_gpus, int lsb0,
                  int n_digits, int copies, unsigned long long* __restrict__ out) {
