@@ -186,6 +186,7 @@ def main() -> int:
 
     rates = [float(r) for r in args.rates.split(",")] if args.rates else list(cfg["rates"])
     out_path = Path(args.out) if args.out else None
+    model_rows = []   # config 4: (route table, nu, measured exchange p50) for the netsim calibration
 
     class A:   # the timing helpers' argument bundle
         steps, warmup, chunk, transport, msg_cap, seed, fused_send = (args.steps, args.warmup, args.chunk, "p2p",
@@ -241,6 +242,17 @@ def main() -> int:
                     "planner": planner, "clocks": clocks.summary(), "case_s": round(time.time() - t_case, 1),
                     "skipped_engines": skipped or None,
                 }
+                if planner is not None and rt is not None:
+                    # the reference's analytic per-step model (netsim.py:177-246) for the same table,
+                    # activity nu = realised rate x 1 ms, in its own units (calibrated below)
+                    nu = min(1.0, row["rate_hz"] * 1e-3)
+                    topo = nc.build_topology(nc.TopologySpec(gpus_per_node=max(1, world // args.groups),
+                                                             nodes_per_switch=8), world)
+                    row["netsim_step_time_model_units"] = nc.step_latency(
+                        nc.map_flows(rt, gt, topo, nu), rt, topo, noise=nu).step_time
+                    row["connections_out_degree"] = nc.connection_stats(rt).out_degree.tolist()
+                    if eng == "persistent" and row["exchange_us"]:
+                        model_rows.append((rt, nu, row["exchange_us"]["p50"], row))
                 if eng == "fused" and kms:
                     alg = net.n_synapses * 16 / 5 + lay.n_local(rank) * (4 * csr.n_tiles + 22)
                     peak = B.load_peaks()["hbm_gbs"] * GB
@@ -256,6 +268,18 @@ def main() -> int:
                 if out_path:
                     with out_path.open("a") as f:
                         f.write(json.dumps(row) + "\n")
+    if rank == 0 and len(model_rows) >= 4:
+        # calibrate the reference's TopologySpec on the measured exchange latency
+        spec_fit, fit = nc.netsim.calibrate_topology([(rt, nu, t) for rt, nu, t, _ in model_rows], gt, world)
+        calib = {k: getattr(spec_fit, k) for k in ("per_hop_latency", "intra_node_bandwidth",
+                                                  "inter_node_bandwidth", "connection_setup_cost")}
+        summary = {"calibration": calib, "model_vs_measured_us": [
+            {"route": r["route"], "rate_hz": r["rate_hz"], "measured_p50": t, "model": round(m, 2)}
+            for (_, _, t, r), (_, _, _, m) in zip(model_rows, fit)]}
+        print(json.dumps(summary), flush=True)
+        if out_path:
+            with out_path.open("a") as f:
+                f.write(json.dumps(summary) + "\n")
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
