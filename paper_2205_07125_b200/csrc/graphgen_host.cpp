@@ -239,7 +239,7 @@ extern "C" int nc_greedy_fill_generated(const nc_graphgen_t* spec, const double*
   std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return wp[a] > wp[b]; });
   for (int64_t k = 0; k < m; ++k) assignment[k] = -1;
   ncgreedy::IndexedHeap heap(m, score.data(), wp);
-  std::vector<int64_t> touched, row_items;
+  std::vector<int64_t> touched, row_items, nbr;
   std::vector<double> row_new;
   int64_t cursor = 0, left = m;
   for (int32_t b = 0; b + 1 < n_buckets; ++b) {
@@ -265,16 +265,31 @@ extern "C" int nc_greedy_fill_generated(const nc_graphgen_t* spec, const double*
       load += w;
       row_items.clear();
       row_new.clear();
+      // the row first (upper part regenerated, then the stored lower part), with the
+      // per-item state of every neighbour prefetched: at 1e7 items those are cache misses
+      // and the row's ~1 000 of them can be in flight together
+      nbr.clear();
+      for_each_upper(g, pick, [&](int64_t j, bool intra) { nbr.push_back(intra ? j : ~j); });
+      const size_t n_up = nbr.size();
+      for (int64_t e = lptr[pick]; e < lptr[pick + 1]; ++e) nbr.push_back(lower[(size_t)e]);
+      for (int64_t x : nbr) {
+        const int64_t u = x < 0 ? ~x : x;
+        __builtin_prefetch(&free_[u]);
+        __builtin_prefetch(&score[u]);
+        __builtin_prefetch(&heap.pos[u]);
+      }
       // pairs (pick, j > pick): value (p * W_pick) * W_j
-      for_each_upper(g, pick, [&](int64_t j, bool intra) {
-        if (!free_[j]) return;
+      for (size_t k = 0; k < n_up; ++k) {
+        const bool intra = nbr[k] >= 0;
+        const int64_t j = intra ? nbr[k] : ~nbr[k];
+        if (!free_[j]) continue;
         row_items.push_back(j);
         row_new.push_back(score[j] + (edge_p(g, pick, j, intra) * W(pick)) * W(j));
-      });
+      }
       // pairs (i < pick, pick): value (p * W_i) * W_pick
       const int64_t ci = g.of(pick);
-      for (int64_t e = lptr[pick]; e < lptr[pick + 1]; ++e) {
-        const int64_t i = lower[(size_t)e];
+      for (size_t k = n_up; k < nbr.size(); ++k) {
+        const int64_t i = nbr[k];
         if (!free_[i]) continue;
         row_items.push_back(i);
         row_new.push_back(score[i] + (edge_p(g, i, pick, g.of(i) == ci) * W(i)) * W(pick));
