@@ -240,6 +240,7 @@ extern "C" int nc_greedy_fill_generated(const nc_graphgen_t* spec, const double*
   for (int64_t k = 0; k < m; ++k) assignment[k] = -1;
   ncgreedy::IndexedHeap heap(m, score.data(), wp);
   std::vector<int64_t> touched, row_items, nbr;
+  std::vector<int32_t> touched_in(m, -1);   // bucket that last wrote the item's score
   std::vector<double> row_new;
   int64_t cursor = 0, left = m;
   for (int32_t b = 0; b + 1 < n_buckets; ++b) {
@@ -296,7 +297,10 @@ extern "C" int nc_greedy_fill_generated(const nc_graphgen_t* spec, const double*
       }
       for (size_t k = 0; k < row_items.size(); ++k) {
         score[row_items[k]] = row_new[k];
-        touched.push_back(row_items[k]);
+        if (touched_in[row_items[k]] != b) {   // once per item and bucket: the list stays O(M)
+          touched_in[row_items[k]] = b;
+          touched.push_back(row_items[k]);
+        }
         heap.touch(row_items[k]);
       }
     }

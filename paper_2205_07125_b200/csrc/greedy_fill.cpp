@@ -49,7 +49,8 @@ extern "C" int nc_greedy_fill(int64_t m, const double* weights, const int64_t* i
   for (int64_t k = 0; k < m; ++k) assignment[k] = -1;
 
   IndexedHeap heap(m, score.data(), weights);
-  std::vector<int64_t> touched;       // items whose score was written this bucket
+  std::vector<int64_t> touched;       // items whose score was written this bucket (each once)
+  std::vector<int32_t> touched_in(m, -1);   // bucket that last wrote the item's score
   std::vector<int64_t> row_items;
   std::vector<double> row_new;
   int64_t cursor = 0;
@@ -91,7 +92,10 @@ extern "C" int nc_greedy_fill(int64_t m, const double* weights, const int64_t* i
       // invariant only survives one changed key at a time)
       for (size_t k = 0; k < row_items.size(); ++k) {
         score[row_items[k]] = row_new[k];
-        touched.push_back(row_items[k]);
+        if (touched_in[row_items[k]] != b) {   // once per item and bucket: the list stays O(M)
+          touched_in[row_items[k]] = b;
+          touched.push_back(row_items[k]);
+        }
         heap.touch(row_items[k]);
       }
     }
