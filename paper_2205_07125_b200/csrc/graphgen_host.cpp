@@ -19,6 +19,7 @@
 // against the materialised path).  The device generator uses CUDA's log1p, this
 // file glibc's; bench.py's parity leg checks the two build the same network.
 
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <thread>
@@ -190,36 +191,49 @@ extern "C" int nc_greedy_fill_generated(const nc_graphgen_t* spec, const double*
   }
   const int T = n_threads(threads);
   const std::vector<int64_t> cut = balanced_ranges(g, T);
-  // ---- lower part: ids i < r with r in upper(i), ascending i, int32.  Thread t
-  // owns rows [a_t, b_t) as sources; per-thread counts per target row give every
-  // thread its own run inside each target row, so the runs are in source order.
-  std::vector<std::vector<int32_t>> cnt(T);
-  parallel_rows(cut, [&](int t, int64_t a, int64_t b) {
-    cnt[t].assign(m, 0);
-    for (int64_t i = a; i < b; ++i) for_each_upper(g, i, [&](int64_t j, bool) { ++cnt[t][j]; });
+  // ---- lower part: ids i < r with r in upper(i), ascending i, int32.  The sources
+  // are cut into C contiguous chunks of equal generator work (C = 8 x threads, taken
+  // dynamically by the threads: early chunks scatter over every target row and run
+  // slower); per-chunk counts per target row give every chunk its own run inside
+  // each target row, so the runs are in source order.
+  const std::vector<int64_t> ccut = balanced_ranges(g, 8 * T);
+  const int Cn = (int)ccut.size() - 1;
+  std::vector<std::vector<int32_t>> cnt(Cn);
+  auto each_chunk = [&](auto&& f) {   // f(chunk, row_begin, row_end) over the chunks, dynamically
+    std::atomic<int> next{0};
+    std::vector<std::thread> ts;
+    for (int t = 0; t < T; ++t)
+      ts.emplace_back([&] {
+        for (int c = next++; c < Cn; c = next++) f(c, ccut[c], ccut[c + 1]);
+      });
+    for (auto& th : ts) th.join();
+  };
+  each_chunk([&](int c, int64_t a, int64_t b) {
+    std::vector<int32_t>& k = cnt[c];
+    k.assign(m, 0);
+    for (int64_t i = a; i < b; ++i) for_each_upper(g, i, [&](int64_t j, bool) { ++k[j]; });
   });
   std::vector<int64_t> lptr(m + 1, 0);
-  for (int64_t j = 0; j < m; ++j) {
-    int64_t s = 0;
-    for (int t = 0; t < T; ++t) s += cnt[t][j];
-    lptr[j + 1] = lptr[j] + s;
-  }
-  // cnt[t][j] -> start of thread t's run in row j (relative)
+  // cnt[c][j] -> start of chunk c's run in row j (relative); lptr[j + 1] = row length
   parallel_rows(even_ranges(m, T), [&](int, int64_t a, int64_t b) {
     for (int64_t j = a; j < b; ++j) {
       int32_t run = 0;
-      for (int t = 0; t < T; ++t) {
-        const int32_t c = cnt[t][j];
-        cnt[t][j] = run;
-        run += c;
+      for (int c = 0; c < Cn; ++c) {
+        const int32_t n = cnt[c][j];
+        cnt[c][j] = run;
+        run += n;
       }
+      lptr[j + 1] = run;
     }
   });
+  std::partial_sum(lptr.begin(), lptr.end(), lptr.begin());
   std::vector<int32_t> lower((size_t)lptr[m]);
-  parallel_rows(cut, [&](int t, int64_t a, int64_t b) {
-    std::vector<int32_t>& off = cnt[t];
+  each_chunk([&](int c, int64_t a, int64_t b) {
+    std::vector<int32_t>& off = cnt[c];
     for (int64_t i = a; i < b; ++i)
       for_each_upper(g, i, [&](int64_t j, bool) { lower[(size_t)(lptr[j] + off[j]++)] = (int32_t)i; });
+    off.clear();
+    off.shrink_to_fit();
   });
   cnt.clear();
   cnt.shrink_to_fit();
