@@ -351,7 +351,8 @@ typedef struct nc_xchg {
   uint32_t* peer_inbox[NC_MAX_SHARDS];
   uint32_t* peer_flags[NC_MAX_SHARDS];
   uint32_t* done;                  /* monotonically counting block exits        */
-  uint32_t* send_done;             /* [2][NC_MAX_SHARDS] chunk-publish counters */
+  uint32_t* send_done;             /* [2][NC_MAX_SHARDS]: [0][d] = relay arrivals for
+                                      destination d (two-level, monotonic per run) */
   int32_t blocks_per_peer;         /* P2P kernel blocks per peer (chunks)       */
   int32_t pad1;
   uint32_t* barrier;               /* in-kernel grid barrier counter            */

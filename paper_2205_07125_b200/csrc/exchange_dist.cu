@@ -18,10 +18,12 @@
 //    Phase-1 messages go to every peer every step (possibly empty: a
 //    heartbeat that bounds the step lag between any two ranks to one), so
 //    inbox slots double-buffered by step parity are never overwritten before
-//    they are read.  Two-level routes add an in-kernel grid barrier (every
-//    phase-1 inbox drained) and a phase-2 push from relays.  Every spin is
-//    bounded by a %globaltimer watchdog that sets status[1] and returns
-//    instead of hanging the GPU.
+//    they are read.  Two-level routes: a relay forwards every id it receives
+//    for another group straight into the destination's phase-2 inbox as it
+//    arrives (positions claimed with one atomic per warp and destination), and
+//    the last of the contributing blocks writes that message's header -- no
+//    grid barrier, no second pass.  Every spin is bounded by a %globaltimer
+//    watchdog that sets status[1] and returns instead of hanging the GPU.
 //
 // Counters: hop_ids[u*n+v] (ids this rank sent on u->v, u = this rank) and
 // deliv_ids[s*n+d] (d = this rank); per-step rows when per_step is set.

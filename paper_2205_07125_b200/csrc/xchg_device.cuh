@@ -155,10 +155,42 @@ __device__ __forceinline__ bool ll_wait(const uint64_t* w, uint32_t tag, uint64_
   }
 }
 
+// Relay, two-level phase 1: once every block that forwards to destination d has
+// claimed its positions, the last one to arrive writes d's phase-2 header (tag |
+// count).  The data words were stored straight into d's inbox as they arrived
+// (pipelined: no grid barrier, no local re-bucketing); they carry their own tags,
+// so the header may land before them.  send_done[d] counts arrivals monotonically:
+// step s is complete at (s + 1) x the number of contributing blocks.
+__device__ __forceinline__ void relay_arrive(const nc_xchg_t& X, uint32_t fwd, int B, int step, uint32_t tag,
+                                             long long* hop) {
+  __threadfence();   // this block's position claims and stores before its arrival
+  while (fwd) {
+    const int d = __ffs(fwd) - 1;
+    fwd &= fwd - 1;
+    uint32_t contrib = 0;
+    for (int s = 0; s < X.n; ++s) contrib += (X.fwd_row[s] >> d) & 1u;
+    contrib *= (uint32_t)B;
+    const uint32_t arrived = atomicAdd(X.send_done + d, 1u) + 1u;
+    if (arrived != (uint32_t)(step + 1) * contrib) continue;
+    __threadfence();
+    int64_t cnt = *(volatile int32_t*)(X.fwd_count + d);
+    if (cnt > X.cap) {
+      atomicExch(X.status, 1);
+      cnt = X.cap;
+    }
+    uint64_t* slot = reinterpret_cast<uint64_t*>(X.peer_inbox[d]) + slot_off(X, 1, step & 1, X.rank);
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(slot), "l"(((uint64_t)tag << 32) | (uint32_t)cnt)
+                 : "memory");
+    if (cnt) add64(hop + X.rank * X.n + d, cnt);
+  }
+}
+
 // Receive chunk kb of the message in `slot` and OR its ids into the bitmap,
-// count deliveries, relay-bucket if asked (two-level phase 1).  Whole block.
+// count deliveries; as a two-level relay (phase 1, fwd_row[src] != 0) forward each
+// id straight into its destinations' phase-2 inboxes (relay_arrive).  Whole block.
 static __device__ void ll_recv_scatter(const nc_xchg_t& X, const uint64_t* slot, int kb, int B, uint32_t tag,
-                                       int src, bool phase2, uint32_t* cur, long long* deliv, int step) {
+                                       int src, bool phase2, uint32_t* cur, long long* deliv, int step,
+                                       long long* hop = nullptr) {
   __shared__ long long s_cnt;
   __shared__ unsigned int per_src[NC_MAX_SHARDS];
   if (threadIdx.x < NC_MAX_SHARDS) per_src[threadIdx.x] = 0;
@@ -199,12 +231,18 @@ static __device__ void ll_recv_scatter(const nc_xchg_t& X, const uint64_t* slot,
       base = __shfl_sync(kFull, base, leader);
       if ((f >> d) & 1u) {
         const int32_t pos = base + __popc(m & ((1u << lane) - 1u));
-        if (pos < X.cap) X.fwd_ids[(int64_t)d * X.cap + pos] = id;
-        else atomicExch(X.status, 1);
+        if (pos < X.cap) {
+          uint64_t* dst = reinterpret_cast<uint64_t*>(X.peer_inbox[d]) + slot_off(X, 1, step & 1, X.rank);
+          asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(dst + 1 + pos),
+                       "l"(((uint64_t)tag << 32) | id) : "memory");
+        } else {
+          atomicExch(X.status, 1);
+        }
       }
     }
   }
   __syncthreads();
+  if (!phase2 && fwd && threadIdx.x == 0) relay_arrive(X, fwd, B, step, tag, hop);
   if (plain) {
     if (threadIdx.x == 0 && hi > lo) add64(deliv + (int64_t)src * X.n + X.rank, (long long)(hi - lo));
   } else if (threadIdx.x < X.n && per_src[threadIdx.x]) {
@@ -247,43 +285,14 @@ static __device__ void p2p_block(const nc_xchg_t& X, int ex, int B, int step) {
               X.bucket_ids + (int64_t)b * X.bucket_cap, cnt, kb, B, tag);
     if (dbg) dbg[1] = globaltimer();
   }
-  // ---- phase 1 receive from peer b, chunk kb
+  // ---- phase 1 receive from peer b, chunk kb; as a relay for b, forward as the ids arrive
   if (peer) {
     if (dbg) dbg[2] = globaltimer();
-    ll_recv_scatter(X, my_inbox + slot_off(X, 0, par, b), kb, B, tag, b, false, cur, deliv, step);
+    ll_recv_scatter(X, my_inbox + slot_off(X, 0, par, b), kb, B, tag, b, false, cur, deliv, step, hop);
   }
-  if (X.two_level) {
-    // ---- grid barrier: every phase-1 inbox drained, forward buckets complete
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      atomicAdd(X.barrier, 1u);
-      const uint32_t target = (uint32_t)(step + 1) * (uint32_t)nex;
-      const uint64_t t0 = globaltimer();
-      while ((int32_t)(*(volatile uint32_t*)X.barrier - target) < 0) {
-        if (globaltimer() - t0 > X.timeout_ns) {
-          atomicExch(X.status + 1, 1);
-          break;
-        }
-      }
-      __threadfence();
-    }
-    __syncthreads();
-    // ---- phase 2 push: relayed ids for destination b
-    if (peer && ((X.send2_mask >> b) & 1u)) {
-      int64_t cnt = X.fwd_count[b];
-      if (cnt > X.cap) {
-        if (threadIdx.x == 0 && kb == 0) atomicExch(X.status, 1);
-        cnt = X.cap;
-      }
-      if (threadIdx.x == 0 && kb == 0 && cnt) add64(hop + X.rank * X.n + b, cnt);
-      ll_send(reinterpret_cast<uint64_t*>(X.peer_inbox[b]) + slot_off(X, 1, par, X.rank),
-              X.fwd_ids + (int64_t)b * X.cap, cnt, kb, B, tag);
-    }
-    // ---- phase 2 receive from relay b
-    if (peer && ((X.recv2_mask >> b) & 1u))
-      ll_recv_scatter(X, my_inbox + slot_off(X, 1, par, b), kb, B, tag, b, true, cur, deliv, step);
-  }
+  // ---- phase 2 receive from relay b (two-level): its pipelined forwards of our group's spikes
+  if (X.two_level && peer && ((X.recv2_mask >> b) & 1u))
+    ll_recv_scatter(X, my_inbox + slot_off(X, 1, par, b), kb, B, tag, b, true, cur, deliv, step);
   // ---- latency record: last block out stamps (end - start of block 0)
   __syncthreads();
   if (dbg) dbg[3] = globaltimer();
