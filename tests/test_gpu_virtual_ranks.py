@@ -52,12 +52,17 @@ def _setup(world: int, mode: str):
 
 @pytest.mark.parametrize("world,mode,fused", [(2, "direct", False), (2, "direct", True), (4, "direct", False),
                                               (4, "direct", True), (4, "two-level", False),
-                                              (4, "two-level", True)])
+                                              (4, "two-level", True), (8, "direct", False),
+                                              (8, "two-level", False), (8, "two-level", True)])
 def test_virtual_ranks_p2p_matches_oracle(world, mode, fused):
+    """8 ranks = config 4's real shape: 8 GPUs in 2 groups of 4 (gpurun offers 4 GPUs)."""
     from virtual_ranks import VirtualCluster
     nets, rt, ref = _setup(world, mode)
+    if world == 8 and mode == "two-level":
+        assert sorted(np.bincount(np.asarray(nc.group_gpus(nc.aggregate(_cache["g"], nc.partition_greedy(
+            _cache["g"], 8)), 2).membership))) == [4, 4]
     vc = VirtualCluster(nets, S.LifParams(), 1, rt, transport="p2p", delivery="fused", record_raster_steps=60,
-                        per_step_counts=True, fused_send=fused)
+                        per_step_counts=True, fused_send=fused, blocks_per_peer=2 if world <= 4 else 1)
     try:
         assert all(s.fused_send == fused for s in vc.sims)
         for attempt in range(2):     # the second run reuses the inboxes (reset must clear them)
