@@ -79,6 +79,15 @@ def main() -> int:
                       f"{rep.steps_per_s:.0f} steps/s exchange p50={rep.extra['exchange_p50_us']:.1f}us "
                       f"p99={rep.extra['exchange_p99_us']:.1f}us {'OK' if good else 'MISMATCH ' + str(checks)}",
                       flush=True)
+    # engine choice by measurement: every rank must get the same answer
+    from paper_2205_07125_b200.distributed import choose_delivery
+    best, times = choose_delivery(net, lif, 1, rt, steps=10, warmup=3)
+    names = [None] * world
+    dist.all_gather_object(names, best)
+    good = best in times and len(set(names)) == 1 and set(times) <= {"fused", "persistent"}
+    ok &= good
+    if rank == 0:
+        print(f"[{world} ranks] choose_delivery -> {best} {times} {'OK' if good else 'MISMATCH'}", flush=True)
     flag = torch.tensor([1 if ok else 0], device=dev)
     dist.broadcast(flag, 0)
     dist.destroy_process_group()
