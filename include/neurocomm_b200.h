@@ -355,7 +355,8 @@ typedef struct nc_xchg {
                                       destination d (two-level, monotonic per run) */
   int32_t blocks_per_peer;         /* P2P kernel blocks per peer (chunks)       */
   int32_t pad1;
-  uint32_t* barrier;               /* in-kernel grid barrier counter            */
+  uint32_t* barrier;               /* unused since relays forward as ids arrive (kept
+                                      for layout stability; zeroed by the reset)  */
   unsigned long long* lat_start;
   uint32_t* lat_ns;                /* per-step exchange latency (ns) or NULL    */
   uint32_t* spk_ids;               /* binned delivery: append received ids to the  */
