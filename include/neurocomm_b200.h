@@ -475,6 +475,14 @@ int nc_greedy_fill_generated(const nc_graphgen_t* spec, const double* weights, i
  * count; < 0 on error. */
 int64_t nc_hostgen_edges(const nc_graphgen_t* spec, int64_t* edge_i, int64_t* edge_j, double* edge_p,
                          int32_t threads);
+/* K5 over a generated network (traffic.aggregate_generated): the rows
+ * [row_begin, row_end) of the generator's network are enumerated on the fly and
+ * every edge's (p * W_i) * W_j added exactly into pg_limbs (layout as
+ * nc_traffic_histogram; weights NULL = all 1; assignment int32 [n_neurons]).
+ * Split the rows over ranks and all-reduce the limbs for the multi-GPU path. */
+int nc_traffic_histogram_generated(const nc_graphgen_t* g, const double* weights, const int32_t* assignment,
+                                   int64_t row_begin, int64_t row_end, int32_t n_gpus, int32_t lsb_exponent,
+                                   int32_t n_digits, unsigned long long* pg_limbs, void* stream);
 /* Windowed push synapses (nc_shard_t push_windows > 1) straight from the
  * generator.  Phase 0: counts[pre*W + w] += entries of pre in window w (uint32,
  * zeroed) and the destination masks as nc_graphgen_push; the caller builds

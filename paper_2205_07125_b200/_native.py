@@ -123,6 +123,8 @@ _SIGS = {
                                    c_void_p, c_void_p]),
     "nc_graphgen_degrees": (c_int32, [C.POINTER(GraphGenC), c_void_p, c_void_p]),
     "nc_graphgen_push": (c_int32, [C.POINTER(GraphGenC), c_int32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "nc_traffic_histogram_generated": (c_int32, [C.POINTER(GraphGenC), c_void_p, c_void_p, c_int64, c_int64,
+                                                 c_int32, c_int32, c_int32, c_void_p, c_void_p]),
     "nc_graphgen_push_windowed": (c_int32, [C.POINTER(GraphGenC), c_int32, c_int32, c_int32, c_void_p, c_void_p,
                                             c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "nc_edges_count": (c_int32, [C.POINTER(GraphGenC), c_void_p, c_void_p, c_int64, c_int32, c_int32, c_void_p,

@@ -19,6 +19,7 @@
 #include <stdint.h>
 #include <climits>
 #include "nc_common.h"
+#include "sbm_gen.cuh"
 
 namespace {
 
@@ -121,6 +122,45 @@ __device__ __forceinline__ void add32c(unsigned int* p, unsigned int d) {
 // compact index of upper cell (lo, hi), lo <= hi < n: row lo starts at lo*(2n-lo+1)/2
 __device__ __forceinline__ int ucell(int lo, int hi, int n) { return lo * (2 * n - lo + 1) / 2 + (hi - lo); }
 
+// One term into the block's copy `mine` of the cell accumulators (see above).
+__device__ __forceinline__ void acc_term(unsigned int* mine, int cell, int n_digits, double x, int lsb0) {
+  const Decomposed d = decompose(x);
+  if (d.mant == 0) return;
+  const int s = d.lsb - lsb0;  // >= 0 by construction of lsb0
+  const int kd = s >> 5, o = s & 31;
+  const unsigned long long lo = d.mant << o;
+  const unsigned long long hi = o ? (d.mant >> (64 - o)) : 0ull;
+  unsigned int* c = mine + (cell * n_digits + kd) * 2;
+  if (kd < n_digits) add32c(c, (unsigned int)lo);             // digits past the window are dropped,
+  if (kd + 1 < n_digits) add32c(c + 2, (unsigned int)(lo >> 32));   // as in add_fixed (callers size it)
+  if (kd + 2 < n_digits) add32c(c + 4, (unsigned int)hi);
+}
+
+// End of a block: sum the copies of every cell into 64-bit digits, carry-normalise,
+// add to the global limbs (upper cells: compact index -> lo * n + hi).
+__device__ void flush_cells(const unsigned int* sw, int copies, int cstride, int n_cells, int n_digits, int n_gpus,
+                            bool upper, unsigned long long* out) {
+  for (int cell = threadIdx.x; cell < n_cells; cell += blockDim.x) {
+    int gcell = cell;
+    if (upper) {
+      int lo = 0, rem = cell;
+      while (rem >= n_gpus - lo) rem -= n_gpus - lo++;
+      gcell = lo * n_gpus + lo + rem;
+    }
+    unsigned long long carry = 0;
+    for (int k = 0; k < n_digits; ++k) {
+      unsigned long long x = carry;   // copies * (2^32 + carries * 2^32) + 2^32: no wrap below 2^31 adds
+      for (int c = 0; c < copies; ++c) {
+        const unsigned int* e = sw + c * cstride + (cell * n_digits + k) * 2;
+        x += (unsigned long long)e[0] + ((unsigned long long)e[1] << 32);
+      }
+      const unsigned long long digit = (k + 1 < n_digits) ? (x & 0xffffffffull) : x;
+      carry = (k + 1 < n_digits) ? (x >> 32) : 0;
+      if (digit) atomicAdd(out + (int64_t)gcell * n_digits + k, digit);
+    }
+  }
+}
+
 int smem_cells(bool edges, int n_gpus) { return edges ? n_gpus * (n_gpus + 1) / 2 : n_gpus; }
 int copy_stride(int cells, int n_digits) { return (cells * n_digits * 2) | 1; }   // odd: banks shift per copy
 
@@ -190,40 +230,40 @@ k_histogram_smem(const Idx* __restrict__ ei, const Idx* __restrict__ ej, const d
       }
     }
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const Decomposed d = decompose(x[u]);
-      if (d.mant == 0) continue;
-      const int s = d.lsb - lsb0;  // >= 0 by construction of lsb0
-      const int kd = s >> 5, o = s & 31;
-      const unsigned long long lo = d.mant << o;
-      const unsigned long long hi = o ? (d.mant >> (64 - o)) : 0ull;
-      unsigned int* c = mine + (cell[u] * n_digits + kd) * 2;
-      if (kd < n_digits) add32c(c, (unsigned int)lo);             // digits past the window are dropped,
-      if (kd + 1 < n_digits) add32c(c + 2, (unsigned int)(lo >> 32));   // as in add_fixed (callers size it)
-      if (kd + 2 < n_digits) add32c(c + 4, (unsigned int)hi);
-    }
+    for (int u = 0; u < kUnroll; ++u) acc_term(mine, cell[u], n_digits, x[u], lsb0);
   }
   __syncthreads();
-  // one thread per cell: sum the copies into 64-bit digits, normalise, add to global
-  for (int cell = threadIdx.x; cell < n_cells; cell += blockDim.x) {
-    int gcell = cell;
-    if (ei) {   // compact upper index -> lo * n + hi of the output
-      int lo = 0, rem = cell;
-      while (rem >= n_gpus - lo) rem -= n_gpus - lo++;
-      gcell = lo * n_gpus + lo + rem;
-    }
-    unsigned long long carry = 0;
-    for (int k = 0; k < n_digits; ++k) {
-      unsigned long long x = carry;   // copies * (2^32 + carries * 2^32) + 2^32: no wrap below 2^31 adds
-      for (int c = 0; c < copies; ++c) {
-        const unsigned int* e = sw + c * cstride + (cell * n_digits + k) * 2;
-        x += (unsigned long long)e[0] + ((unsigned long long)e[1] << 32);
-      }
-      const unsigned long long digit = (k + 1 < n_digits) ? (x & 0xffffffffull) : x;
-      carry = (k + 1 < n_digits) ? (x >> 32) : 0;
-      if (digit) atomicAdd(out + (int64_t)gcell * n_digits + k, digit);
-    }
+  flush_cells(sw, copies, cstride, n_cells, n_digits, n_gpus, ei != nullptr, out);
+}
+
+// K5 over a generated network (sim.GeneratorSpec, csrc/graphgen.cu): the edges of
+// rows [row_begin, row_end) are enumerated on the fly by the generator's own gap
+// sampler and their fp64 p by its per-edge counter (sbm_gen.cuh), so the
+// reference's aggregate() of a 1e10-synapse network (config 3/5) needs neither the
+// edge list nor a host NeuronGraph.  weights NULL = all 1.
+__global__ void __launch_bounds__(kThreads)
+k_histogram_generated(const nc_graphgen_t g, const double* __restrict__ w, const int32_t* __restrict__ asg,
+                      int64_t row_begin, int64_t row_end, int n_gpus, int lsb0, int n_digits, int copies,
+                      unsigned long long* __restrict__ out) {
+  extern __shared__ unsigned int sw[];
+  const int n_cells = n_gpus * (n_gpus + 1) / 2;
+  const int cstride = (n_cells * n_digits * 2) | 1;
+  for (int k = threadIdx.x; k < copies * cstride; k += blockDim.x) sw[k] = 0u;
+  __syncthreads();
+  unsigned int* mine = sw + (threadIdx.x & (copies - 1)) * cstride;
+  const ncgen::Comm cm = ncgen::make_comm(g);
+  for (int64_t i = row_begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < row_end;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int ai = __ldg(asg + i);
+    const double wi = w ? __ldg(w + i) : 1.0;
+    ncgen::for_each_upper(g, cm, i, [&](int64_t j, bool intra) {
+      const int aj = __ldg(asg + j);
+      const double x = contrib(ncgen::edge_p(g, i, j, intra), wi, w ? __ldg(w + j) : 1.0);
+      acc_term(mine, ucell(min(ai, aj), max(ai, aj), n_gpus), n_digits, x, lsb0);
+    });
   }
+  __syncthreads();
+  flush_cells(sw, copies, cstride, n_cells, n_digits, n_gpus, true, out);
 }
 
 template <typename Idx>
@@ -349,6 +389,42 @@ extern "C" int nc_traffic_histogram_packed(const int32_t* edge_i, const int32_t*
   return launch_hist<int32_t, true>(edge_i, edge_j, edge_p, reinterpret_cast<const double*>(neuron_records),
                                     nullptr, n_edges, n_gpus, lsb_exponent, n_digits, pg_limbs,
                                     (cudaStream_t)stream);
+}
+
+extern "C" int nc_traffic_histogram_generated(const nc_graphgen_t* g, const double* weights, const int32_t* assignment,
+                                              int64_t row_begin, int64_t row_end, int32_t n_gpus,
+                                              int32_t lsb_exponent, int32_t n_digits, unsigned long long* pg_limbs,
+                                              void* stream) {
+  if (!g || g->n_neurons < 1 || g->n_communities < 1 || g->n_communities > g->n_neurons || !assignment ||
+      n_gpus < 1 || n_digits < 3 || row_begin < 0 || row_end > g->n_neurons || !pg_limbs) {
+    nc_set_error("nc_traffic_histogram_generated: bad arguments");
+    return NC_E_ARG;
+  }
+  if (row_end <= row_begin) return NC_OK;
+  const int cstride = copy_stride(smem_cells(true, n_gpus), n_digits);
+  int copies = 32;
+  while (copies > 1 && (size_t)copies * cstride * sizeof(unsigned int) > kSmemBudget) copies >>= 1;
+  const size_t smem = (size_t)copies * cstride * sizeof(unsigned int);
+  if (smem > kSmemLimit) {
+    nc_set_error("nc_traffic_histogram_generated: %d GPUs x %d digits do not fit in shared memory", n_gpus,
+                 n_digits);
+    return NC_E_ARG;
+  }
+  int dev = 0, sms = 148, occ = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  NC_CUDA_TRY(cudaFuncSetAttribute(k_histogram_generated, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)kSmemLimit));
+  NC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_histogram_generated, kThreads, smem));
+  // rows carry very different numbers of edges (the first rows of a community enumerate
+  // the most): many small blocks, grid-stride over rows
+  int64_t blocks = (row_end - row_begin + kThreads - 1) / kThreads;
+  const int64_t cap = (int64_t)sms * (occ > 0 ? occ : 1) * 4;
+  if (blocks > cap) blocks = cap;
+  k_histogram_generated<<<(unsigned)blocks, kThreads, smem, (cudaStream_t)stream>>>(
+      *g, weights, assignment, row_begin, row_end, n_gpus, lsb_exponent, n_digits, copies, pg_limbs);
+  NC_LAUNCH_CHECK();
+  return NC_OK;
 }
 
 extern "C" int nc_weight_histogram(const double* weights, const int64_t* assignment, int64_t n_neurons,

@@ -11,6 +11,7 @@ stay on the host; they touch at most a few hundred numbers.
 from __future__ import annotations
 
 import csv
+import ctypes as C
 import json
 import math
 from dataclasses import dataclass
@@ -23,7 +24,7 @@ from .accum import limbs_to_float
 __all__ = [
     "GpuTrafficGraph", "TrafficReport", "report_from_vector", "aggregate", "per_gpu_send_traffic",
     "peak_reduction", "write_traffic_csv", "read_traffic_csv", "write_traffic_summary",
-    "exact_bin_sums", "aggregate_sharded",
+    "exact_bin_sums", "aggregate_sharded", "aggregate_generated",
 ]
 
 INT_MAX = 2**31 - 1
@@ -273,6 +274,68 @@ def aggregate_sharded(edge_i, edge_j, edge_p, weights, assignment, n_gpus: int, 
     cells = exact_bin_sums(w, asg, n, pairs=(ei, ej, ep), group=group).reshape(n, n)
     pg = np.triu(cells) + np.triu(cells, 1).T
     wg = exact_bin_sums(w, asg, n)
+    return GpuTrafficGraph(n, pg, wg)
+
+
+def aggregate_generated(spec, pm, *, weights=None, group=None) -> GpuTrafficGraph:
+    """aggregate() (traffic.py:66-84) of a generated network (sim.GeneratorSpec) without
+    materialising it: K5 consumes the generator's edges and fp64 p on the fly
+    (nc_traffic_histogram_generated), so the reference's traffic matrix of a 1e10-synapse
+    network (configs 3-5) costs one pass of the generator.  Bit-identical to
+    ``aggregate(spec.host_graph(), pm)`` (weights: None = all 1, else float64 [M]).
+    ``group`` (torch.distributed, True = default group): every rank enumerates its slice
+    of the rows and the integer limbs are all-reduced before the one rounding."""
+    import torch
+    m = int(spec.n_neurons)
+    if pm.assignment.size != m:
+        raise ValueError(f"partition map covers {pm.assignment.size} neurons, graph has {m}")
+    n = int(pm.n_gpus)
+    dev = _device()
+    L = _native.lib()
+    st = _native.stream_handle()
+    asg32 = torch.from_numpy(np.ascontiguousarray(pm.assignment, dtype=np.int32)).to(dev)
+    w_dev = None if weights is None else torch.from_numpy(np.ascontiguousarray(weights, dtype=np.float64)).to(dev)
+    # window: every term is p (times two weights) with p in [lo, hi) of the ranges in use
+    ranges = []
+    if spec.p_in > 0:
+        ranges.append(spec.intra_p_range)
+    if spec.p_out > 0 and spec.n_communities > 1:
+        ranges.append(spec.inter_p_range)
+    lo_p = min(r[0] for r in ranges) if ranges else 1.0
+    hi_p = max(r[1] for r in ranges) if ranges else 1.0
+    if w_dev is None:
+        ew = (0, 0)
+    else:
+        ew = _exp_range(w_dev)
+        if ew is None:
+            raise ValueError("weights are all zero")
+    ep_lo, ep_hi = math.frexp(lo_p)[1] - 1, math.frexp(hi_p)[1] - 1
+    lsb = max(-1074, ep_lo + 2 * ew[0] - 52)
+    msb = ep_hi + 2 * ew[1] + 4
+    n_terms = m * (m - 1) // 2                     # an upper bound on the edge count
+    nd = _n_digits(lsb, msb, n_terms)
+    limbs = torch.zeros((n * n, nd), dtype=torch.int64, device=dev)
+    rank, world = 0, 1
+    if group is not None:
+        import torch.distributed as dist
+        grp = None if group is True else group
+        rank, world = dist.get_rank(grp), dist.get_world_size(grp)
+    r0, r1 = m * rank // world, m * (rank + 1) // world
+    g = spec.to_c()
+    _native.check(L.nc_traffic_histogram_generated(C.byref(g), None if w_dev is None else w_dev.data_ptr(),
+                                                   asg32.data_ptr(), r0, r1, n, lsb, nd, limbs.data_ptr(), st),
+                  "traffic histogram (generated)")
+    if group is not None:
+        import torch.distributed as dist
+        dist.all_reduce(limbs, group=None if group is True else group)
+    host = limbs.cpu().numpy().view(np.uint64)
+    cells = np.zeros(n * n, dtype=np.float64)
+    for c in np.flatnonzero(host.any(axis=1)).tolist():
+        cells[c] = limbs_to_float(host[c].tolist(), lsb)
+    cells = cells.reshape(n, n)
+    pg = np.triu(cells) + np.triu(cells, 1).T
+    wsrc = torch.ones(m, dtype=torch.float64, device=dev) if w_dev is None else w_dev
+    wg = exact_bin_sums(wsrc, torch.from_numpy(np.ascontiguousarray(pm.assignment, dtype=np.int64)).to(dev), n)
     return GpuTrafficGraph(n, pg, wg)
 
 

@@ -529,3 +529,22 @@ def test_windowed_push_matches_oracle(source):
             np.testing.assert_array_equal(rep.raster, ref["raster"], err_msg=f"{delivery} run {attempt}")
             np.testing.assert_array_equal(rep.v.view(np.uint32), ref["v"].view(np.uint32))
             np.testing.assert_array_equal(rep.deliv_ids, ref["deliv"])
+
+
+@pytest.mark.parametrize("spec_args,n_gpus", [((30_000, 1, 60 / 29_999, 0.0, 3), 4),
+                                              ((24_000, 6, 0.01, 0.0008, 5), 8)])
+def test_aggregate_of_generated_network(spec_args, n_gpus):
+    """traffic.aggregate_generated (K5 fed by the generator, no edge list) equals the
+    reference-path aggregate of the same network materialised as a NeuronGraph, bit for
+    bit -- also with weights and with the reference partition of that network."""
+    from paper_2205_07125_b200 import partition as P
+    n, c, p_in, p_out, seed = spec_args
+    spec = S.GeneratorSpec(n, c, p_in, p_out, seed=seed)
+    g = spec.host_graph()
+    pm = P.partition_greedy_generated(spec, n_gpus)
+    for w in (None, np.random.default_rng(1).uniform(0.5, 2.0, n)):
+        gw = g if w is None else nc.NeuronGraph(n, w, g.edge_i, g.edge_j, g.edge_p)
+        want = nc.aggregate(gw, pm)
+        got = nc.traffic.aggregate_generated(spec, pm, weights=w)
+        np.testing.assert_array_equal(got.pg.view(np.uint64), want.pg.view(np.uint64))
+        np.testing.assert_array_equal(got.wg.view(np.uint64), want.wg.view(np.uint64))
