@@ -58,28 +58,6 @@ def spec_for(cfg: dict, seed: int):
     return S.GeneratorSpec(n, c, min(p_in, 1.0), min(p_out, p_in), seed=seed)
 
 
-def traffic_from_push(net, rank: int, world: int, dev):
-    """pg[a][b] = sum over synapses a -> b of q / 32 from the push CSR (exact integer sums of
-    q, all-reduced), wg = neurons per shard: the planner's view of the generated network."""
-    import torch
-    import torch.distributed as dist
-    lay = net.layout
-    arr = next(iter(net.shards[rank]._push_arrays.values()))   # any windows: rows are pre ids
-    rowptr, ent = arr["rowptr"], arr["syn"]
-    m = torch.zeros((world, world), dtype=torch.int64, device=dev)
-    chunk = 1 << 28
-    for a in range(world):
-        lo, hi = int(rowptr[int(lay.base[a])].item()), int(rowptr[int(lay.base[a + 1])].item())
-        tot = torch.zeros((), dtype=torch.int64, device=dev)
-        for s in range(lo, hi, chunk):
-            e = ent[s:min(hi, s + chunk)]
-            tot += (((e >> 26) & 31) + 1).sum(dtype=torch.int64)
-        m[a, rank] = tot
-    if world > 1:
-        dist.all_reduce(m)
-    return m.cpu().numpy().astype(np.float64) / 32.0
-
-
 def main() -> int:
     import torch
     import torch.distributed as dist
@@ -121,7 +99,7 @@ def main() -> int:
     syn_per_gpu = cfg["neurons"] * cfg["degree"] / world
     free = torch.cuda.mem_get_info(dev)[0]
     want_pull = "fused" in engines and syn_per_gpu * 8.0 + 4 * GB < free
-    want_push = any(e in ("persistent", "push") for e in engines) or args.config == 4
+    want_push = any(e in ("persistent", "push") for e in engines)
     skipped = {}
     if "fused" in engines and not want_pull:
         skipped["fused"] = ("pull layout build needs ~8 B/synapse transient (%.0f GB) on a GPU with %.0f GB free"
@@ -173,15 +151,20 @@ def main() -> int:
     routes = args.routes.split(",") if args.routes else (["direct", "two-level"] if args.config == 4 or (
         args.config == 5 and world >= 4) else ["direct"])
     if "two-level" in routes and world >= 3:
-        if not want_push:
-            raise SystemExit("two-level routes need the traffic matrix from the push CSR")
-        pg = traffic_from_push(net, rank, world, dev)
-        gt = nc.GpuTrafficGraph(world, pg, np.array([lay.n_local(h) for h in range(world)], dtype=np.float64))
+        # the reference's traffic matrix of this network and partition (aggregate, traffic.py:66-84),
+        # K5 fed by the generator with the rows split over the ranks (limbs all-reduced)
+        t_agg = time.time()
+        gt = nc.traffic.aggregate_generated(spec, nc.PartitionMap(world, lay.owner.astype(np.int64)),
+                                            group=True if world > 1 else None)
+        agg_s = time.time() - t_agg
         groups = nc.group_gpus(gt, args.groups)
         tables["two-level"] = nc.build_routing_table(gt, groups, nc.select_bridges(gt, groups))
         tables["direct"] = nc.route_p2p(gt)
         planner = {"groups": groups.membership.tolist(),
-                   "bridges": [[a, b, v] for (a, b), v in sorted(tables["two-level"].bridges.items())]}
+                   "bridges": [[a, b, v] for (a, b), v in sorted(tables["two-level"].bridges.items())],
+                   "pg": gt.pg.tolist(), "aggregate_s": round(agg_s, 2),
+                   "aggregate": "traffic.aggregate_generated (exact fsum of p per GPU pair, the reference's "
+                                "aggregate of the generated network)"}
     tables = {k: v for k, v in tables.items() if k in routes}
 
     rates = [float(r) for r in args.rates.split(",")] if args.rates else list(cfg["rates"])
