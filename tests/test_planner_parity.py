@@ -370,3 +370,13 @@ def test_host_graph_matches_generator_statistics():
     mean = sum(s * (s - 1) // 2 for s in sizes.tolist()) * spec.p_in + \
         (spec.n_neurons ** 2 - (sizes ** 2).sum()) / 2 * spec.p_out
     assert abs(g.n_edges - mean) < 4 * np.sqrt(mean)
+
+
+def test_streamed_k6_equals_materialised_at_1e6():
+    """The same at 1e6 neurons x ~100 synapses (5e7 edges): SURVEY 8(a)'s a3 scale check."""
+    from paper_2205_07125_b200 import partition as P
+    from paper_2205_07125_b200 import sim as S
+    spec = S.GeneratorSpec.random(1_000_000, 100.0, seed=4)
+    want = nc.partition_greedy(spec.host_graph(), 8)
+    got = P.partition_greedy_generated(spec, 8)
+    np.testing.assert_array_equal(got.assignment, want.assignment)
