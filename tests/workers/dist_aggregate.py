@@ -40,6 +40,17 @@ def main() -> int:
         if rank == 0:
             print(f"[{world} ranks] M={g.n_neurons} E={g.n_edges} N={n_gpus}: {'OK' if same else 'MISMATCH'}",
                   flush=True)
+    # K5 fed by the generator, rows split over the ranks (traffic.aggregate_generated(group=True))
+    from paper_2205_07125_b200 import sim as S
+    gspec = S.GeneratorSpec(40_000, 5, 0.01, 0.001, seed=3)
+    gpm = nc.PartitionMap(6, (np.arange(gspec.n_neurons) * 5 % 6).astype(np.int64))
+    one = nc.traffic.aggregate_generated(gspec, gpm)
+    split = nc.traffic.aggregate_generated(gspec, gpm, group=True)
+    same = (np.array_equal(one.pg.view(np.uint64), split.pg.view(np.uint64))
+            and np.array_equal(one.wg.view(np.uint64), split.wg.view(np.uint64)))
+    ok &= same
+    if rank == 0:
+        print(f"[{world} ranks] aggregate_generated rows split over ranks: {'OK' if same else 'MISMATCH'}", flush=True)
     flag = torch.tensor([1 if ok else 0], device="cuda")
     dist.all_reduce(flag, op=dist.ReduceOp.MIN)
     dist.destroy_process_group()
