@@ -236,6 +236,14 @@ def _device_graph(graph, dev):
     return val
 
 
+def _check_assignment(pm) -> None:
+    """The kernels index per-GPU cells by the assignment: refuse values outside [0, n_gpus)
+    (where the reference's numpy indexing would raise)."""
+    a = np.asarray(pm.assignment)
+    if a.size and (int(a.min()) < 0 or int(a.max()) >= int(pm.n_gpus)):
+        raise ValueError(f"assignment has GPU indices outside [0, {int(pm.n_gpus)})")
+
+
 def aggregate(graph, pm) -> GpuTrafficGraph:
     """Collapse neuron traffic onto GPUs (traffic.py:66-84) with the K5 kernel."""
     import torch
@@ -243,6 +251,7 @@ def aggregate(graph, pm) -> GpuTrafficGraph:
         raise ValueError(
             f"partition map covers {pm.assignment.size} neurons, graph has {graph.n_neurons}"
         )
+    _check_assignment(pm)
     n = int(pm.n_gpus)
     dev = _device()
     w, ei, ej, ep = _device_graph(graph, dev)
@@ -289,6 +298,7 @@ def aggregate_generated(spec, pm, *, weights=None, group=None) -> GpuTrafficGrap
     m = int(spec.n_neurons)
     if pm.assignment.size != m:
         raise ValueError(f"partition map covers {pm.assignment.size} neurons, graph has {m}")
+    _check_assignment(pm)
     n = int(pm.n_gpus)
     dev = _device()
     L = _native.lib()
