@@ -260,28 +260,30 @@ class _Null:
 
 def kernel_ms(sim, which: str, reps: int = 50) -> float:
     """Average duration of one kernel, timed alone with CUDA events on its stream."""
-    import ctypes as C
     import torch
     from paper_2205_07125_b200 import _native
     st = sim.states[0]
-    L = _native.lib()
     stream = torch.cuda.current_stream()
     k0 = torch.cuda.Event(enable_timing=True)
     k1 = torch.cuda.Event(enable_timing=True)
+    O = _native.ops()
+    lif = _native.as_bytes(sim.c_lif)
+
     def run(kind):
         torch.cuda.synchronize()
         k0.record(stream)
+        s = stream.cuda_stream
         for _ in range(reps):
             if kind == "fused":
-                L.nc_sim_step_fused(C.byref(st.c), C.byref(sim.c_lif), stream.cuda_stream)
+                O.sim_step_fused(st.c_t, lif, s)
             elif kind == "push":  # + the claim-counter reset a real step does
-                L.nc_sim_deliver_push(C.byref(st.c), sim.c_lif.g_inh, stream.cuda_stream)
-                L.nc_sim_end_step(C.byref(st.c), stream.cuda_stream)
+                O.sim_deliver_push(st.c_t, sim.c_lif.g_inh, s)
+                O.sim_end_step(st.c_t, s)
             elif kind == "lif":  # with the bucket reset a real step does after the exchange
-                L.nc_sim_lif_update(C.byref(st.c), C.byref(sim.c_lif), stream.cuda_stream)
-                L.nc_sim_end_step(C.byref(st.c), stream.cuda_stream)
+                O.sim_lif_update(st.c_t, lif, s)
+                O.sim_end_step(st.c_t, s)
             else:
-                L.nc_sim_end_step(C.byref(st.c), stream.cuda_stream)
+                O.sim_end_step(st.c_t, s)
         k1.record(stream)
         torch.cuda.synchronize()
         return k0.elapsed_time(k1) / reps

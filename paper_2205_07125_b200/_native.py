@@ -193,6 +193,36 @@ def lib():
     return _lib
 
 
+OPS_PATH = Path(__file__).resolve().parent / "libneurocomm_b200_torch.so"
+_ops = None
+
+
+def ops():
+    """torch.ops.neurocomm_b200: the thin PyTorch extension (csrc/torch_ops.cpp) through
+    which the simulators launch every per-step kernel.  Loaded once; raises loudly if
+    it is absent (no fallback)."""
+    global _ops
+    if _ops is not None:
+        return _ops
+    import torch
+    lib()   # the engine it links against, loaded and ABI-checked first
+    if not OPS_PATH.is_file():
+        raise RuntimeError(f"{OPS_PATH} not found: build it with `make -C paper_2205_07125_b200/csrc` "
+                           "(or __graft_entry__.build())")
+    torch.ops.load_library(str(OPS_PATH))
+    o = torch.ops.neurocomm_b200
+    if int(o.abi_version()) != ABI_VERSION:
+        raise RuntimeError(f"{OPS_PATH} was built against ABI {int(o.abi_version())}, expected {ABI_VERSION}")
+    _ops = o
+    return _ops
+
+
+def as_bytes(obj):
+    """A uint8 CPU tensor viewing a ctypes struct / array (no copy: later field writes show)."""
+    import torch
+    return torch.frombuffer(obj, dtype=torch.uint8)
+
+
 def exported_symbols() -> list[str]:
     return sorted(_SIGS)
 

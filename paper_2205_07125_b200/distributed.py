@@ -271,6 +271,9 @@ class DistSimulator:
             X.fused_send = 1
         from .sim import StepGraphs
         self._graphs = StepGraphs(dev, self._one_step, graph_chunk)
+        self.ops = _native.ops()
+        self.c_lif_t = _native.as_bytes(self.c_lif)
+        self.X_t = _native.as_bytes(self.X)
         _native.check(self.lib.nc_sim_prepare(), "prepare")
 
     # ------------------------------------------------------------ bootstrap
@@ -377,53 +380,52 @@ class DistSimulator:
         self.g.barrier()     # every inbox cleared before any rank's first send
 
     def _exchange(self, st):
-        L, X = self.lib, C.byref(self.X)
+        O, X = self.ops, self.X_t
         if self.transport == "p2p":
-            _native.check(L.nc_xchg_p2p(X, st), "p2p exchange")
+            O.xchg_p2p(X, st)
             return
-        _native.check(L.nc_xchg_seal(X, 1, st), "seal")
-        _native.check(L.nc_nccl_exchange(self._comm, X, 1, st), "nccl exchange")
-        _native.check(L.nc_xchg_scatter(X, 1, st), "scatter")
+        comm = int(self._comm.value)
+        O.xchg_seal(X, 1, st)
+        O.nccl_exchange(comm, X, 1, st)
+        O.xchg_scatter(X, 1, st)
         if self.plan.two_level:
-            _native.check(L.nc_xchg_seal(X, 2, st), "seal 2")
-            _native.check(L.nc_nccl_exchange(self._comm, X, 2, st), "nccl exchange 2")
-            _native.check(L.nc_xchg_scatter(X, 2, st), "scatter 2")
+            O.xchg_seal(X, 2, st)
+            O.nccl_exchange(comm, X, 2, st)
+            O.xchg_scatter(X, 2, st)
 
     def _one_step(self, st):
         self.step_kernels(st)
         self.exchange_kernels(st)
         self.end_kernels(st)
 
+    # the per-step launches go through the thin PyTorch extension (torch.ops.neurocomm_b200)
     def step_kernels(self, st):
         """Delivery + LIF + bucketing of this rank's shard (and the fused send)."""
-        L = self.lib
+        O = self.ops
         s = self.state
-        lif = C.byref(self.c_lif)
+        lif = self.c_lif_t
         if self.delivery == "binned":
-            _native.check(L.nc_sim_step_binned(C.byref(s.c), lif, st), "step binned")
+            O.sim_step_binned(s.c_t, lif, st)
         elif self.delivery == "fused":
-            _native.check(L.nc_sim_step_fused(C.byref(s.c), lif, st), "step")
+            O.sim_step_fused(s.c_t, lif, st)
         else:
             if self.delivery == "push":
-                _native.check(L.nc_sim_deliver_push(C.byref(s.c), self.c_lif.g_inh, st), "push")
+                O.sim_deliver_push(s.c_t, self.c_lif.g_inh, st)
             else:
-                _native.check(L.nc_sim_deliver_pull(C.byref(s.c), self.c_lif.g_inh, st), "pull")
-            _native.check(L.nc_sim_lif_update(C.byref(s.c), lif, st), "lif")
+                O.sim_deliver_pull(s.c_t, self.c_lif.g_inh, st)
+            O.sim_lif_update(s.c_t, lif, st)
 
     def exchange_kernels(self, st):
-        L = self.lib
         s = self.state
         if self.transport == "p2p":
             self._exchange(st)          # stamps its own start (buckets ready) and end
         else:
-            _native.check(L.nc_stamp(self.lat_stamps[0].data_ptr(), s.step.data_ptr(), self.latency_steps, st),
-                          "stamp")
+            self.ops.stamp(self.lat_stamps[0], s.step, self.latency_steps, st)
             self._exchange(st)
-            _native.check(L.nc_stamp(self.lat_stamps[1].data_ptr(), s.step.data_ptr(), self.latency_steps, st),
-                          "stamp")
+            self.ops.stamp(self.lat_stamps[1], s.step, self.latency_steps, st)
 
     def end_kernels(self, st):
-        _native.check(self.lib.nc_sim_end_step(C.byref(self.state.c), st), "end step")
+        self.ops.sim_end_step(self.state.c_t, st)
 
     def launches_per_step(self) -> float:
         if self.delivery == "persistent":
@@ -443,10 +445,8 @@ class DistSimulator:
         if self.delivery == "persistent":
             s = self.state
             st = _native.stream_handle(self.dev)
-            _native.check(self.lib.nc_run_persistent(C.byref(s.c), C.byref(self.c_lif), C.byref(self.X), int(steps),
-                                                     self.blocks_per_peer, self._gbar.data_ptr(),
-                                                     self.lat_stamps[0].data_ptr(), self.lat_stamps[1].data_ptr(),
-                                                     self.latency_steps, st), "persistent engine")
+            self.ops.run_persistent(s.c_t, self.c_lif_t, self.X_t, int(steps), self.blocks_per_peer, self._gbar,
+                                    self.lat_stamps[0], self.lat_stamps[1], self.latency_steps, st)
             return
         if not self.use_graph:
             self.advance_eager(steps)

@@ -774,6 +774,7 @@ class _ShardState:
             record_steps=self.record_steps, local_words=self.local_words,
             spike_total=self.spike_total.data_ptr(), work=self.work.data_ptr(),
             row_perm=None if csr.row_perm is None else csr.row_perm.data_ptr(), cta_groups=csr.cta_groups)
+        self.c_t = _native.as_bytes(self.c)   # the descriptor as the torch ops take it (a view)
         if self.push is not None and self.push["windows"] > 1:
             self.c.push_winoff = self.push["winoff"].data_ptr()
             self.c.push_windows, self.c.push_window_rows = self.push["windows"], self.push["rows"]
@@ -998,6 +999,10 @@ class Simulator:
                                    device=dev)
         self.fwd_count = torch.zeros(self.n * self.n, dtype=torch.int32, device=dev)
         self.shard_array = (_native.ShardC * self.n)(*[s.c for s in self.states])
+        self.ops = _native.ops()
+        self.c_lif_t = _native.as_bytes(self.c_lif)
+        self.shard_array_t = _native.as_bytes(self.shard_array)
+        self.fwd_table_t = torch.from_numpy(self.fwd_table)
         self._counter_steps = 0
         self._gbar = torch.zeros(1, dtype=torch.int32, device=dev)
         self.hop_ids = None
@@ -1024,29 +1029,28 @@ class Simulator:
             self._graphs.clear()
 
     def _one_step(self, st):
-        L = self.lib
-        lif = C.byref(self.c_lif)
+        """One step's launches, through the thin PyTorch extension (torch.ops.neurocomm_b200)."""
+        O = self.ops
+        lif = self.c_lif_t
         if self.delivery == "fused":
             for s in self.states:
-                self._check(L.nc_sim_step_fused(C.byref(s.c), lif, st), "step")
+                O.sim_step_fused(s.c_t, lif, st)
         elif self.delivery == "binned":
             for s in self.states:
-                self._check(L.nc_sim_step_binned(C.byref(s.c), lif, st), "step binned")
+                O.sim_step_binned(s.c_t, lif, st)
         else:
             for s in self.states:
                 if self.delivery == "push":
-                    self._check(L.nc_sim_deliver_push(C.byref(s.c), self.c_lif.g_inh, st), "deliver push")
+                    O.sim_deliver_push(s.c_t, self.c_lif.g_inh, st)
                 else:
-                    self._check(L.nc_sim_deliver_pull(C.byref(s.c), self.c_lif.g_inh, st), "deliver pull")
-                self._check(L.nc_sim_lif_update(C.byref(s.c), lif, st), "lif update")
+                    O.sim_deliver_pull(s.c_t, self.c_lif.g_inh, st)
+                O.sim_lif_update(s.c_t, lif, st)
         if self.n > 1:
-            self._check(L.nc_exchange_local(self.shard_array, self.n, self.dest_global.data_ptr(),
-                                            self.fwd_table.ctypes.data, self.fwd_ids.data_ptr(),
-                                            self.fwd_count.data_ptr(), self.fwd_cap, self.hop_ids.data_ptr(),
-                                            self.deliv_ids.data_ptr(), 1 if self.per_step_counts else 0, st),
-                        "exchange")
+            O.exchange_local(self.shard_array_t, self.n, self.dest_global, self.fwd_table_t, self.fwd_ids,
+                             self.fwd_count, self.fwd_cap, self.hop_ids, self.deliv_ids,
+                             1 if self.per_step_counts else 0, st)
         for s in self.states:
-            self._check(L.nc_sim_end_step(C.byref(s.c), st), "end step")
+            O.sim_end_step(s.c_t, st)
 
     def launches_per_step(self) -> float:
         if self.delivery == "persistent":
@@ -1068,8 +1072,7 @@ class Simulator:
         if self.delivery == "persistent":
             s = self.states[0]
             st = _native.stream_handle(self.net.device)
-            _native.check(self.lib.nc_run_persistent(C.byref(s.c), C.byref(self.c_lif), None, int(steps), 1,
-                                                     self._gbar.data_ptr(), None, None, 0, st), "persistent engine")
+            self.ops.run_persistent(s.c_t, self.c_lif_t, None, int(steps), 1, self._gbar, None, None, 0, st)
             return
         if not self.use_graph:
             self.advance_eager(steps)

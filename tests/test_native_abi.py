@@ -70,3 +70,25 @@ def test_struct_field_offsets_match_header(tmp_path):
         assert got[(cname, "size")] == ctypes.sizeof(py), cname
         for f in py._fields_:
             assert got[(cname, f[0])] == getattr(py, f[0]).offset, (cname, f[0])
+
+
+OPS = ["abi_version", "sim_init", "sim_step_fused", "sim_step_binned", "sim_deliver_push", "sim_deliver_pull",
+       "sim_lif_update", "sim_end_step", "exchange_local", "xchg_p2p", "xchg_seal", "xchg_scatter",
+       "nccl_exchange", "stamp", "run_persistent"]
+
+
+def test_torch_extension_registers_the_step_ops():
+    """The thin PyTorch extension (csrc/torch_ops.cpp) loads and registers every step-loop
+    op; a bad descriptor is refused before anything reaches the GPU (ValueError, as the
+    C-ABI path raises for NC_E_ARG)."""
+    import pytest
+    import torch
+    o = _native.ops()
+    for name in OPS:
+        assert hasattr(o, name), name
+    assert int(o.abi_version()) == _native.ABI_VERSION
+    shard = _native.as_bytes(_native.ShardC())          # all zero: no step / status buffers
+    with pytest.raises(ValueError, match="invalid nc_shard_t"):
+        o.sim_end_step(shard, 0)
+    with pytest.raises(RuntimeError, match="bytes"):
+        o.sim_end_step(torch.zeros(3, dtype=torch.uint8), 0)
