@@ -77,6 +77,8 @@ def main() -> int:
     ap.add_argument("--routes", default=None, help="direct,two-level (default: per config)")
     ap.add_argument("--neurons", type=int, default=None, help="override the config's neuron count (tests)")
     ap.add_argument("--chunk", type=int, default=100)
+    ap.add_argument("--no-ei-group", dest="ei_group", action="store_false",
+                    help="layout A/B: do not put each shard's inhibitory ids after its excitatory ones")
     ap.add_argument("--push-windows", type=int, default=None,
                     help="post-row windows of the push CSR (default: sim.push_windows_for per shard)")
     ap.add_argument("--partition", default="blocks",
@@ -130,7 +132,7 @@ def main() -> int:
     torch.cuda.reset_peak_memory_stats(dev)
     t0 = time.time()
     net = S.Network.generate(spec, lay, device=dev, shards=[rank], pull=want_pull, push=want_push,
-                             push_windows=args.push_windows)
+                             push_windows=args.push_windows, group_inhibitory=args.ei_group)
     torch.cuda.synchronize()
     build_s = time.time() - t0
     csr = net.shards[rank]
@@ -221,7 +223,9 @@ def main() -> int:
                     "neurons": n, "synapses": int(nsyn.item()), "communities": cfg["communities"],
                     "partition": args.partition.split(":")[0], "partition_s": part_s, "bitmap_tiles": csr.n_tiles if want_pull else None,
                     "fused_send": fused_send, "memory_per_gpu": mem,
-                    "push_windows": sim_windows, "build_s": round(build_s, 1),
+                    "push_windows": sim_windows, "ei_group": args.ei_group,
+                    "pull_layout_bytes_per_synapse": round(csr.n_entries * 4 / max(net.n_synapses, 1), 4)
+                    if want_pull else None, "build_s": round(build_s, 1),
                     "planner": planner, "clocks": clocks.summary(), "case_s": round(time.time() - t_case, 1),
                     "skipped_engines": skipped or None,
                 }

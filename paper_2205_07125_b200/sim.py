@@ -149,11 +149,15 @@ class ShardLayout:
     n_words: int               # bitmap words incl. a guard word, multiple of 4
 
     @classmethod
-    def from_assignment(cls, assignment, n_shards: int, order_key=None) -> "ShardLayout":
+    def from_assignment(cls, assignment, n_shards: int, order_key=None, group_key=None) -> "ShardLayout":
         """Shards from a PartitionMap assignment.  Inside a shard, neurons are in
         ascending gid, or by descending `order_key` (ties: gid) when given --
         the engine passes the degree so the 32 rows of a SELL slice have
-        similar lengths (less padding)."""
+        similar lengths (less padding) -- within ascending `group_key` groups
+        when given (the engine passes the inhibitory flag: excitatory ids first,
+        then inhibitory ones, so most bitmap tiles hold pres of one sign and a
+        row's synapses in such a tile need one E/I segment instead of two --
+        half the per-(row, tile) segment padding)."""
         owner = np.ascontiguousarray(assignment, dtype=np.int64)
         if owner.size and (owner.min() < 0 or owner.max() >= n_shards):
             raise ValueError("assignment has GPU indices outside [0, n_gpus)")
@@ -162,7 +166,11 @@ class ShardLayout:
         members = [np.flatnonzero(owner == h) for h in range(n_shards)]
         if order_key is not None:
             key = np.asarray(order_key)
-            members = [m[np.lexsort((m, -key[m]))] for m in members]
+            if group_key is not None:
+                grp = np.asarray(group_key)
+                members = [m[np.lexsort((m, -key[m], grp[m]))] for m in members]
+            else:
+                members = [m[np.lexsort((m, -key[m]))] for m in members]
         counts = np.array([m.size for m in members], dtype=np.int64)
         padded = (counts + 31) // 32 * 32
         base = np.zeros(n_shards + 1, dtype=np.int64)
@@ -182,9 +190,11 @@ class ShardLayout:
         sizes = community_sizes(n_neurons, n_shards)
         return cls.from_assignment(np.repeat(np.arange(n_shards), sizes), n_shards)
 
-    def reordered(self, order_key) -> "ShardLayout":
-        """Same shards, rows ordered by descending `order_key` inside each shard."""
-        return ShardLayout.from_assignment(self.owner, self.n_shards, order_key)
+    def reordered(self, order_key, inh_every: int = 0) -> "ShardLayout":
+        """Same shards, rows ordered by descending `order_key` inside each shard, the
+        excitatory neurons before the inhibitory ones when `inh_every` > 0."""
+        grp = inhibitory_mask(np.arange(self.n_neurons), inh_every).astype(np.int8) if inh_every > 0 else None
+        return ShardLayout.from_assignment(self.owner, self.n_shards, order_key, grp)
 
     @property
     def guard_id(self) -> int:
@@ -288,7 +298,7 @@ class Network:
             raise ValueError(f"builder must be 'device' or 'host', got {builder!r}")
         deg = np.bincount(graph.edge_i, minlength=graph.n_neurons) + np.bincount(graph.edge_j,
                                                                                minlength=graph.n_neurons)
-        layout = layout.reordered(deg)
+        layout = layout.reordered(deg, inh_every)
         own = range(layout.n_shards) if shards is None else shards
         out = {}
         nsyn = 0
@@ -318,7 +328,7 @@ class Network:
         ei, ej, qd = upload_edges(graph, dev)
         n = int(ei.numel())
         deg = torch.bincount(ei, minlength=graph.n_neurons) + torch.bincount(ej, minlength=graph.n_neurons)
-        layout = layout.reordered(deg.cpu().numpy())
+        layout = layout.reordered(deg.cpu().numpy(), inh_every)
         del deg
         owner_d = torch.from_numpy(layout.owner).to(dev)
         internal_d = torch.from_numpy(layout.internal_id).to(dev)
@@ -346,14 +356,16 @@ class Network:
     @classmethod
     def generate(cls, spec: GeneratorSpec, layout: ShardLayout, *, device=None, inh_every: int = 5,
                  shards=None, tile_words: int | None = None, bank_order: bool = True, pull: bool = True,
-                 push: bool = False, push_windows: int | None = None) -> "Network":
+                 push: bool = False, push_windows: int | None = None, group_inhibitory: bool = True) -> "Network":
         """Counter-based device generator (csrc/graphgen.cu); every shard regenerates the same graph.
 
         ``pull``: the J-SELL pull layout (fused / pull / binned delivery).  ``push``:
         the push CSR of the event-driven engines, generated directly (without the
         pull layout when ``pull`` is False: 4 B per synapse instead of 3.2 + 4 + the
         build's transient 8), grouped into ``push_windows`` post-row windows (None:
-        push_windows_for(rows of the shard), what the persistent engine wants)."""
+        push_windows_for(rows of the shard), what the persistent engine wants).
+        ``group_inhibitory``: excitatory internal ids before inhibitory ones in each
+        shard (ShardLayout.from_assignment); results are identical either way."""
         import torch
         if not (pull or push):
             raise ValueError("generate at least one of the pull and push layouts")
@@ -374,7 +386,7 @@ class Network:
             local_base=0, inh_every=inh_every)
         deg = torch.zeros(spec.n_neurons, dtype=torch.int32, device=dev)
         _native.check(L.nc_graphgen_degrees(C.byref(g0), deg.data_ptr(), st), "graphgen degrees")
-        layout = layout.reordered(deg.cpu().numpy())
+        layout = layout.reordered(deg.cpu().numpy(), inh_every if group_inhibitory else 0)
         del deg
         owner_d = torch.from_numpy(layout.owner).to(dev)
         internal_d = torch.from_numpy(layout.internal_id).to(dev)
