@@ -90,6 +90,20 @@ int nc_traffic_histogram_packed(const int32_t* edge_i, const int32_t* edge_j, co
                                 const void* neuron_records, int64_t n_edges, int32_t n_gpus,
                                 int32_t lsb_exponent, int32_t n_digits, unsigned long long* pg_limbs,
                                 void* stream);
+/* Same when every neuron weight equals `weight` (generate_synthetic's default
+ * weight_low == weight_high; contributions (p * weight) * weight, the same two
+ * roundings) and the assignment is uint8 (n_gpus <= 256): one byte gathered per
+ * endpoint. */
+int nc_traffic_histogram_uniform(const int32_t* edge_i, const int32_t* edge_j, const double* edge_p,
+                                 double weight, const uint8_t* assignment, int64_t n_edges, int32_t n_gpus,
+                                 int32_t lsb_exponent, int32_t n_digits, unsigned long long* pg_limbs,
+                                 void* stream);
+/* PartitionMap.assignment (int64) -> uint8 gpu ids for nc_traffic_histogram_uniform,
+ * counts[g] += neurons on GPU g (uint64 [n_gpus], zeroed by the caller), *bad |= 1
+ * if a value lies outside [0, n_gpus) (written as 0; the caller raises, as the
+ * reference's indexing would). */
+int nc_assignment_u8(const int64_t* assignment, int64_t n_neurons, int32_t n_gpus, uint8_t* out,
+                     unsigned long long* counts, unsigned long long* bad, void* stream);
 int nc_weight_histogram(const double* weights, const int64_t* assignment, int64_t n_neurons,
                         int32_t n_gpus, int32_t lsb_exponent, int32_t n_digits,
                         unsigned long long* wg_limbs, void* stream);

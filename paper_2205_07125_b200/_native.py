@@ -105,6 +105,9 @@ _SIGS = {
                                        c_int32, c_int32, c_void_p, c_void_p]),
     "nc_traffic_histogram_packed": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int32, c_int32,
                                               c_int32, c_void_p, c_void_p]),
+    "nc_traffic_histogram_uniform": (c_int32, [c_void_p, c_void_p, c_void_p, c_double, c_void_p, c_int64, c_int32,
+                                               c_int32, c_int32, c_void_p, c_void_p]),
+    "nc_assignment_u8": (c_int32, [c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
     "nc_traffic_histogram32": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int32,
                                        c_int32, c_int32, c_void_p, c_void_p]),
     "nc_weight_histogram": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_int32, c_int32, c_void_p, c_void_p]),

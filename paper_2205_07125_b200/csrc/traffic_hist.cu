@@ -31,6 +31,9 @@ namespace {
 #endif
 constexpr int kThreads = NC_K5_THREADS;
 constexpr size_t kSmemLimit = 96 * 1024;    // fall back to global limbs above this
+#ifndef NC_K5_UNIFORM_UNROLL
+#define NC_K5_UNIFORM_UNROLL 8   // 1-byte gathers: more edges in flight per thread
+#endif
 #ifndef NC_K5_SMEM_KB
 #define NC_K5_SMEM_KB 16
 #endif
@@ -164,13 +167,23 @@ __device__ void flush_cells(const unsigned int* sw, int copies, int cstride, int
 int smem_cells(bool edges, int n_gpus) { return edges ? n_gpus * (n_gpus + 1) / 2 : n_gpus; }
 int copy_stride(int cells, int n_digits) { return (cells * n_digits * 2) | 1; }   // odd: banks shift per copy
 
-// kPacked: w points at one 16-byte record per neuron {double w; int32 gpu; pad}
-// (nc_traffic_histogram_packed): one gather per endpoint instead of two.
-template <typename Idx, bool kPacked = false>
+// How a neuron's {weight, gpu} is gathered per edge endpoint:
+//   kSplit   w[i] and asg[i] (two gathers);
+//   kPacked  one 16-byte record per neuron {double w; int32 gpu; pad}
+//            (nc_traffic_histogram_packed): one gather;
+//   kUniform every weight equals w0 (generate_synthetic's default weight_low ==
+//            weight_high): only the uint8 gpu id is gathered, 1 byte per endpoint
+//            instead of 16 (the L1 data path and register writeback of the
+//            gathers were the bound, 80 % / 70 % busy with the 16-byte records);
+//            (p * w0) * w0 is the same two roundings as (p * w_i) * w_j.
+enum { kSplit = 0, kPacked = 1, kUniform = 2 };
+
+template <typename Idx, int kRec = kSplit, int kUnroll = NC_K5_UNROLL>
 __global__ void __launch_bounds__(kThreads, NC_K5_MIN_BLOCKS)
 k_histogram_smem(const Idx* __restrict__ ei, const Idx* __restrict__ ej, const double* __restrict__ ep,
                  const double* __restrict__ w, const Idx* __restrict__ asg, int64_t n, int n_gpus, int lsb0,
-                 int n_digits, int copies, unsigned long long* __restrict__ out) {
+                 int n_digits, int copies, unsigned long long* __restrict__ out, double w0 = 1.0,
+                 const uint8_t* __restrict__ asg8 = nullptr) {
   extern __shared__ unsigned int sw[];
   const int n_cells = ei ? n_gpus * (n_gpus + 1) / 2 : n_gpus;
   const int cstride = (n_cells * n_digits * 2) | 1;
@@ -179,7 +192,6 @@ k_histogram_smem(const Idx* __restrict__ ei, const Idx* __restrict__ ej, const d
   unsigned int* mine = sw + (threadIdx.x & (copies - 1)) * cstride;
   // kUnroll edges per thread and iteration, every load issued before the first use:
   // the gathers of w / assignment (L2-resident) then overlap instead of serialising
-  constexpr int kUnroll = NC_K5_UNROLL;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t k0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k0 < n; k0 += stride * kUnroll) {
     double x[kUnroll];
@@ -197,7 +209,15 @@ k_histogram_smem(const Idx* __restrict__ ei, const Idx* __restrict__ ej, const d
       }
       double wi[kUnroll], wj[kUnroll];
       int ai[kUnroll], aj[kUnroll];
-      if (kPacked) {
+      if (kRec == kUniform) {
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          wi[u] = w0;
+          wj[u] = w0;
+          ai[u] = __ldg(asg8 + i[u]);
+          aj[u] = __ldg(asg8 + j[u]);
+        }
+      } else if (kRec == kPacked) {
         const int4* rec = reinterpret_cast<const int4*>(w);
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
@@ -296,9 +316,11 @@ k_histogram_global(const Idx* __restrict__ ei, const Idx* __restrict__ ej, const
   }
 }
 
-template <typename Idx, bool kPacked = false>
+template <typename Idx, int kRec = kSplit, int kUnroll = NC_K5_UNROLL>
 int launch_hist(const Idx* ei, const Idx* ej, const double* ep, const double* w, const Idx* asg, int64_t n,
-                int n_gpus, int lsb0, int n_digits, unsigned long long* out, cudaStream_t st) {
+                int n_gpus, int lsb0, int n_digits, unsigned long long* out, cudaStream_t st, double w0 = 1.0,
+                const uint8_t* asg8 = nullptr) {
+  constexpr auto kernel = k_histogram_smem<Idx, kRec, kUnroll>;
   if (n <= 0) return NC_OK;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -311,20 +333,19 @@ int launch_hist(const Idx* ei, const Idx* ej, const double* ep, const double* w,
   if (smem <= kSmemLimit) {
     static bool attr = false;
     if (!attr) {
-      NC_CUDA_TRY(cudaFuncSetAttribute(k_histogram_smem<Idx, kPacked>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)kSmemLimit));
+      NC_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemLimit));
       attr = true;
     }
     int occ = 1;
-    NC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_histogram_smem<Idx, kPacked>, kThreads, smem));
+    NC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, smem));
     int64_t blocks = (n + kThreads - 1) / kThreads;
     const int64_t max_blocks = (int64_t)sms * (occ > 0 ? occ : 1);   // one resident wave, grid-stride
     if (blocks > max_blocks) blocks = max_blocks;
-    k_histogram_smem<Idx, kPacked><<<(unsigned)blocks, kThreads, smem, st>>>(ei, ej, ep, w, asg, n, n_gpus, lsb0, n_digits,
-                                                                       copies, out);
-  } else if (kPacked) {
-    nc_set_error("traffic histogram: %d GPUs x %d digits do not fit in shared memory (packed path)", n_gpus,
-                 n_digits);
+    kernel<<<(unsigned)blocks, kThreads, smem, st>>>(ei, ej, ep, w, asg, n, n_gpus, lsb0, n_digits, copies, out, w0,
+                                                   asg8);
+  } else if (kRec != kSplit) {
+    nc_set_error("traffic histogram: %d GPUs x %d digits do not fit in shared memory (packed / uniform path)",
+                 n_gpus, n_digits);
     return NC_E_ARG;
   } else {
     int64_t blocks = (n + kThreads - 1) / kThreads;
@@ -334,6 +355,29 @@ int launch_hist(const Idx* ei, const Idx* ej, const double* ep, const double* w,
   }
   NC_LAUNCH_CHECK();
   return NC_OK;
+}
+
+// PartitionMap.assignment (any integer width, widened to int64 on the way in) -> uint8
+// gpu ids for the uniform-weight K5, per-GPU neuron counts, and a flag for values outside
+// [0, n_gpus) (stored as 0 so the histogram's cell index stays in range; the caller
+// raises after the one read-back).
+__global__ void k_assignment_u8(const int64_t* __restrict__ a, int64_t n, int n_gpus, uint8_t* __restrict__ out,
+                                unsigned long long* __restrict__ counts, unsigned long long* __restrict__ bad) {
+  __shared__ unsigned int hist[256];
+  for (int k = threadIdx.x; k < n_gpus; k += blockDim.x) hist[k] = 0u;
+  __syncthreads();
+  bool oob = false;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = __ldcs(a + k);
+    const bool ok = v >= 0 && v < n_gpus;
+    oob |= !ok;
+    out[k] = ok ? (uint8_t)v : (uint8_t)0;
+    if (ok) atomicAdd(&hist[v], 1u);
+  }
+  if (__any_sync(0xffffffffu, oob) && (threadIdx.x & 31) == 0) atomicOr(bad, 1ull);
+  __syncthreads();
+  for (int k = threadIdx.x; k < n_gpus; k += blockDim.x)
+    if (hist[k]) atomicAdd(counts + k, (unsigned long long)hist[k]);
 }
 
 }  // namespace
@@ -386,9 +430,36 @@ extern "C" int nc_traffic_histogram_packed(const int32_t* edge_i, const int32_t*
     nc_set_error("nc_traffic_histogram_packed: bad arguments (n_gpus=%d n_digits=%d)", n_gpus, n_digits);
     return NC_E_ARG;
   }
-  return launch_hist<int32_t, true>(edge_i, edge_j, edge_p, reinterpret_cast<const double*>(neuron_records),
+  return launch_hist<int32_t, kPacked>(edge_i, edge_j, edge_p, reinterpret_cast<const double*>(neuron_records),
                                     nullptr, n_edges, n_gpus, lsb_exponent, n_digits, pg_limbs,
                                     (cudaStream_t)stream);
+}
+
+extern "C" int nc_traffic_histogram_uniform(const int32_t* edge_i, const int32_t* edge_j, const double* edge_p,
+                                            double weight, const uint8_t* assignment, int64_t n_edges, int32_t n_gpus,
+                                            int32_t lsb_exponent, int32_t n_digits, unsigned long long* pg_limbs,
+                                            void* stream) {
+  if (n_gpus < 1 || n_gpus > 256 || n_digits < 3 || !edge_i || !edge_j || !assignment) {
+    nc_set_error("nc_traffic_histogram_uniform: bad arguments (n_gpus=%d n_digits=%d)", n_gpus, n_digits);
+    return NC_E_ARG;
+  }
+  return launch_hist<int32_t, kUniform, NC_K5_UNIFORM_UNROLL>(edge_i, edge_j, edge_p, nullptr, nullptr, n_edges, n_gpus,
+                                                          lsb_exponent, n_digits, pg_limbs, (cudaStream_t)stream,
+                                                          weight, assignment);
+}
+
+extern "C" int nc_assignment_u8(const int64_t* assignment, int64_t n_neurons, int32_t n_gpus, uint8_t* out,
+                                unsigned long long* counts, unsigned long long* bad, void* stream) {
+  if (n_gpus < 1 || n_gpus > 256 || n_neurons < 0 || (n_neurons && (!assignment || !out)) || !counts || !bad) {
+    nc_set_error("nc_assignment_u8: bad arguments (n_gpus=%d)", n_gpus);
+    return NC_E_ARG;
+  }
+  if (n_neurons == 0) return NC_OK;
+  int64_t blocks = (n_neurons + 1023) / 1024;
+  if (blocks > 148 * 4) blocks = 148 * 4;
+  k_assignment_u8<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(assignment, n_neurons, n_gpus, out, counts, bad);
+  NC_LAUNCH_CHECK();
+  return NC_OK;
 }
 
 extern "C" int nc_traffic_histogram_generated(const nc_graphgen_t* g, const double* weights, const int32_t* assignment,

@@ -452,9 +452,16 @@ class Network:
         return self.layout.members[shard][row], pre, q.astype(np.uint8)
 
 
-def upload_edges(graph: NeuronGraph, dev, chunk: int = 1 << 26):
+def upload_edges(graph: NeuronGraph, dev, chunk: int = 1 << 22, depth: int = 3):
     """Edge columns of a NeuronGraph on the device as int32 ids and uint8 weight units
-    q = ceil(32 p) (q_from_p), converted chunk by chunk on the device."""
+    q = ceil(32 p) (q_from_p).
+
+    Pipelined through `depth` pinned staging buffers of `chunk` edges: the host copies
+    chunk k into a pinned buffer (torch's multi-threaded CPU copy, any integer / float
+    dtype widened to int64 / float64) while the copy engine moves chunk k-1 and a side
+    stream narrows it on the device; endpoint range checks are reduced on the device and
+    read once at the end.  (A pageable .to(device) goes through the driver's single
+    staging thread.)"""
     import torch
     m = int(graph.n_neurons)
     if m >= 2**31:
@@ -463,16 +470,45 @@ def upload_edges(graph: NeuronGraph, dev, chunk: int = 1 << 26):
     ei = torch.empty(n, dtype=torch.int32, device=dev)
     ej = torch.empty(n, dtype=torch.int32, device=dev)
     qd = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
-    for a in range(0, n, chunk):
-        b = min(n, a + chunk)
-        ci = torch.from_numpy(np.ascontiguousarray(graph.edge_i[a:b])).to(dev)
-        cj = torch.from_numpy(np.ascontiguousarray(graph.edge_j[a:b])).to(dev)
-        if ci.numel() and (int(torch.minimum(ci.min(), cj.min())) < 0 or int(torch.maximum(ci.max(), cj.max())) >= m):
-            raise ValueError(f"edge endpoints outside [0, {m})")
-        ei[a:b] = ci
-        ej[a:b] = cj
-        p = torch.from_numpy(np.ascontiguousarray(graph.edge_p[a:b], dtype=np.float64)).to(dev)
-        qd[a:b] = torch.ceil(p * Q_LEVELS).clamp_(1, Q_LEVELS).to(torch.uint8)
+    if n == 0:
+        return ei, ej, qd[:0]
+    src = [torch.from_numpy(np.ascontiguousarray(a)) for a in (graph.edge_i, graph.edge_j)]
+    src_p = torch.from_numpy(np.ascontiguousarray(graph.edge_p, dtype=np.float64))
+    c = min(chunk, n)
+    k_buf = min(depth, (n + c - 1) // c)
+    host = [torch.empty((3, c), dtype=torch.int64, pin_memory=True) for _ in range(k_buf)]
+    devb = [torch.empty((3, c), dtype=torch.int64, device=dev) for _ in range(k_buf)]
+    done = [None] * k_buf
+    lo = torch.full((1,), 0, dtype=torch.int64, device=dev)
+    hi = torch.full((1,), 0, dtype=torch.int64, device=dev)
+    side = torch.cuda.Stream(dev)
+    side.wait_stream(torch.cuda.current_stream(dev))
+    for idx, a in enumerate(range(0, n, c)):
+        b = min(n, a + c)
+        k, w = idx % k_buf, b - a
+        if done[k] is not None:
+            done[k].synchronize()          # the copy engine has drained this staging buffer
+        h = host[k]
+        h[0, :w].copy_(src[0][a:b])
+        h[1, :w].copy_(src[1][a:b])
+        h[2, :w].view(torch.float64).copy_(src_p[a:b])
+        with torch.cuda.stream(side):
+            d = devb[k]
+            d[:, :w].copy_(h[:, :w], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(side)
+            done[k] = ev
+            ids = d[:2, :w]
+            torch.minimum(lo, ids.min().view(1), out=lo)
+            torch.maximum(hi, ids.max().view(1), out=hi)
+            ei[a:b].copy_(d[0, :w])
+            ej[a:b].copy_(d[1, :w])
+            qd[a:b] = torch.ceil(d[2, :w].view(torch.float64) * Q_LEVELS).clamp_(1, Q_LEVELS).to(torch.uint8)
+    torch.cuda.current_stream(dev).wait_stream(side)
+    for t in (ei, ej, qd, lo, hi):
+        t.record_stream(side)
+    if int(lo.item()) < 0 or int(hi.item()) >= m:
+        raise ValueError(f"edge endpoints outside [0, {m})")
     return ei, ej, qd[:n]
 
 
@@ -1126,14 +1162,7 @@ class Simulator:
         lay = self.net.layout
         raster = None
         if self.record_steps:
-            raster = np.zeros((steps, lay.n_neurons), dtype=bool)
-            for s in self.states:
-                if not s.n_local:
-                    continue
-                words = s.raster[:steps, : s.local_words].cpu().numpy().view(np.uint32)
-                bits = (words[:, :, None] >> np.arange(32, dtype=np.uint32)) & np.uint32(1)
-                bits = bits.reshape(steps, -1)[:, : s.n_local]
-                raster[:, lay.members[s.h]] = bits.astype(bool)
+            raster = _raster_to_host(self.states, lay, steps, self.net.device)
         v = np.zeros(lay.n_neurons, dtype=np.float32)
         i = np.zeros(lay.n_neurons, dtype=np.float32)
         spikes = 0
@@ -1149,6 +1178,29 @@ class Simulator:
         mode = "none" if self.n == 1 else ("two-level" if self.plan.two_level else "direct")
         return SimReport(steps=steps, n_gpus=self.n, raster=raster, deliv_ids=deliv, hop_ids=hop, spikes=spikes,
                          v=v, i_syn=i, elapsed_ms=elapsed_ms, exchange=mode, delivery=self.delivery)
+
+
+def _raster_to_host(states, lay, steps: int, dev, chunk_bytes: int = 256 << 20) -> np.ndarray:
+    """bool [steps, M] in gid order from the shards' recorded bitmap rows: bits unpacked
+    and scattered to gid order on the device (a step chunk at a time), one copy back."""
+    import torch
+    raster = np.zeros((steps, lay.n_neurons), dtype=bool)
+    if steps == 0 or lay.n_neurons == 0:
+        return raster
+    shifts = torch.arange(32, dtype=torch.int32, device=dev)
+    members = {s.h: torch.from_numpy(np.asarray(lay.members[s.h], dtype=np.int64)).to(dev) for s in states if s.n_local}
+    rows = max(1, chunk_bytes // lay.n_neurons)
+    for a in range(0, steps, rows):
+        b = min(steps, a + rows)
+        out = torch.zeros((b - a, lay.n_neurons), dtype=torch.bool, device=dev)
+        for s in states:
+            if not s.n_local:
+                continue
+            words = s.raster[a:b, : s.local_words]
+            bits = ((words.unsqueeze(-1) >> shifts) & 1).reshape(b - a, -1)[:, : s.n_local]
+            out[:, members[s.h]] = bits.bool()
+        raster[a:b] = out.cpu().numpy()
+    return raster
 
 
 # ---------------------------------------------------------------- engine choice

@@ -58,6 +58,49 @@ def test_aggregate_bit_identical_to_reference(ref_fixtures):
         assert nc.cross_traffic(g, pm).hex() == case["cross_traffic"]
 
 
+def test_aggregate_uniform_weights_path():
+    """Every weight equal (generate_synthetic's default): K5 gathers only a 1-byte gpu id
+    per endpoint and wg = count * w0; pg / wg must still be math.fsum per cell, also for
+    a GPU without neurons and for one GPU."""
+    import math
+    rng = np.random.default_rng(11)
+    m, e = 3000, 40000
+    i = rng.integers(0, m - 1, e)
+    j = np.minimum(i + 1 + rng.integers(0, 400, e), m - 1)
+    keep = i < j
+    key = np.unique(i[keep] * m + j[keep])
+    ei, ej = key // m, key % m
+    p = rng.uniform(1e-9, 1.0, ei.size)
+    for w0, n in ((1.0, 8), (0.3, 5), (3.7e10, 1), (1e-20, 3)):
+        w = np.full(m, w0)
+        g = nc.NeuronGraph(m, w, ei, ej, p)
+        asg = rng.integers(0, n, m)
+        if n > 2:
+            asg[asg == n - 1] = 0          # one GPU without neurons
+        pm = nc.PartitionMap(n, asg)
+        gt = nc.aggregate(g, pm)
+        a, b = asg[ei], asg[ej]
+        c = p * w0 * w0
+        for x in range(n):
+            assert gt.wg[x] == math.fsum(w[asg == x]), (w0, n, x)
+            for y in range(x, n):
+                sel = (np.minimum(a, b) == x) & (np.maximum(a, b) == y)
+                assert gt.pg[x, y] == math.fsum(c[sel]), (w0, n, x, y)
+                assert gt.pg[y, x] == gt.pg[x, y]
+    # assignment values outside [0, n) raise on both paths (range-checked on the device
+    # on the uniform one), and a valid call afterwards is unaffected
+    gw = nc.NeuronGraph(m, rng.uniform(0.5, 2.0, m), ei, ej, p)
+    for gr in (g, gw):
+        for bad in (-1, 3, 300):
+            asg = rng.integers(0, 3, m)
+            asg[m // 2] = bad
+            with pytest.raises(ValueError, match="outside"):
+                nc.aggregate(gr, nc.PartitionMap(3, asg))
+    pm = nc.PartitionMap(3, rng.integers(0, 3, m))
+    assert nc.aggregate(g, pm).pg[0, 0] == math.fsum(p[(pm.assignment[ei] == 0) & (pm.assignment[ej] == 0)]
+                                                      * w0 * w0)
+
+
 def test_genetic_partition_matches_reference(ref_fixtures):
     """GA baseline: same numpy stream, fitness through the exact GPU aggregate."""
     idx, arr = ref_fixtures
@@ -432,6 +475,32 @@ def test_device_edge_builder_equals_host_builder(tile_words):
     np.testing.assert_array_equal(ra.raster, rb.raster)
     np.testing.assert_array_equal(ra.hop_ids, rb.hop_ids)
     np.testing.assert_array_equal(ra.v.view(np.uint32), rb.v.view(np.uint32))
+
+
+@pytest.mark.parametrize("idtype", [np.int64, np.int32])
+def test_upload_edges_pipeline(idtype):
+    """sim.upload_edges (pinned staging buffers, copy engine + side-stream narrowing) gives
+    the plain conversion for any chunking, including a ragged last chunk; an endpoint
+    outside [0, M) raises after the upload."""
+    import torch
+    rng = np.random.default_rng(4)
+    m, e = 5000, 12345
+    ei = rng.integers(0, m, e).astype(idtype)
+    ej = rng.integers(0, m, e).astype(idtype)
+    p = rng.uniform(1e-9, 1.0, e)
+    g = nc.NeuronGraph(m, np.ones(m), ei, ej, p)
+    dev = torch.device("cuda", 0)
+    want_q = np.clip(np.ceil(p * 32), 1, 32).astype(np.uint8)
+    for chunk, depth in ((1 << 22, 3), (1000, 2), (777, 3), (e, 1)):
+        a, b, q = S.upload_edges(g, dev, chunk=chunk, depth=depth)
+        np.testing.assert_array_equal(a.cpu().numpy(), ei.astype(np.int32))
+        np.testing.assert_array_equal(b.cpu().numpy(), ej.astype(np.int32))
+        np.testing.assert_array_equal(q.cpu().numpy(), want_q)
+    for bad in (-1, m):
+        ej2 = ej.copy()
+        ej2[e - 3] = bad
+        with pytest.raises(ValueError, match="outside"):
+            S.upload_edges(nc.NeuronGraph(m, np.ones(m), ei, ej2, p), dev, chunk=1000, depth=2)
 
 
 def graph_from_csr(rowptr, col, q):

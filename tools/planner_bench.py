@@ -30,6 +30,7 @@ def main():
     import paper_2205_07125_b200 as nc
     ap = argparse.ArgumentParser()
     ap.add_argument("--sizes", default="10000,100000,1000000")
+    ap.add_argument("--reps", type=int, default=20)
     args = ap.parse_args()
     for m in [int(x) for x in args.sizes.split(",")]:
         c, n = (1, 4) if m <= 10_000 else ((1, 8) if m <= 100_000 else (8, 8))
@@ -47,11 +48,27 @@ def main():
         gt = nc.aggregate(g, pm)
         torch.cuda.synchronize()
         t_agg = time.time() - t
+        # median over repeated calls (the GA's use), uniform weights (the default spec) and
+        # with per-neuron weights (the general 16-byte record path)
+        def med(gr):
+            ts = []
+            for _ in range(args.reps):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                nc.aggregate(gr, pm)
+                ts.append(time.perf_counter() - t0)
+            return float(np.median(ts))
+        t_med = med(g)
+        gw = nc.NeuronGraph(g.n_neurons, np.random.default_rng(2).uniform(0.5, 2.0, g.n_neurons), g.edge_i,
+                            g.edge_j, g.edge_p)
+        nc.aggregate(gw, pm)
+        t_med_w = med(gw)
         ref = REFERENCE_S.get(m)
         print(json.dumps({
             "neurons": m, "communities": c, "gpus": n, "edges": int(g.n_edges),
             "ours_s": {"generate_synthetic": round(t_gen, 3), "partition_greedy": round(t_part, 3),
-                       "aggregate": round(t_agg, 4)},
+                       "aggregate": round(t_agg, 4), "aggregate_median": round(t_med, 5),
+                       "aggregate_weighted_median": round(t_med_w, 5)},
             "reference_s": None if ref is None else dict(zip(("generate_synthetic", "partition_greedy", "aggregate"),
                                                             ref)),
             "cross_traffic": float(np.triu(gt.pg, 1).sum()),
