@@ -76,6 +76,9 @@ def main() -> int:
     ap.add_argument("--rates", default=None, help="comma list of target rates (Hz); default per config")
     ap.add_argument("--routes", default=None, help="direct,two-level (default: per config)")
     ap.add_argument("--neurons", type=int, default=None, help="override the config's neuron count (tests)")
+    ap.add_argument("--communities", type=int, default=None,
+                    help="regional variant (SURVEY 8(d) config 3 'C = 8 (regional)'): C contiguous communities, "
+                         "90 %% of each neuron's synapses inside its own")
     ap.add_argument("--chunk", type=int, default=100)
     ap.add_argument("--no-ei-group", dest="ei_group", action="store_false",
                     help="layout A/B: do not put each shard's inhibitory ids after its excitatory ones")
@@ -90,6 +93,9 @@ def main() -> int:
     cfg = dict(CONFIGS[args.config])
     if args.neurons:
         cfg["neurons"] = args.neurons
+    if args.communities and args.communities > 1:
+        cfg["communities"] = args.communities
+        cfg["intra_frac"] = cfg["intra_frac"] or 0.9
 
     rank, world, local = B.dist_env()
     torch.cuda.set_device(local)
@@ -221,7 +227,7 @@ def main() -> int:
                     "wire_bytes_per_step": round(float(h.sum()) * 8 + 8 * int((h > 0).sum()), 1),
                     "channel_ids_per_step": np.round(h, 1).tolist(),
                     "neurons": n, "synapses": int(nsyn.item()), "communities": cfg["communities"],
-                    "partition": args.partition.split(":")[0], "partition_s": part_s, "bitmap_tiles": csr.n_tiles if want_pull else None,
+                    "intra_frac": cfg["intra_frac"], "partition": args.partition.split(":")[0], "partition_s": part_s, "bitmap_tiles": csr.n_tiles if want_pull else None,
                     "fused_send": fused_send, "memory_per_gpu": mem,
                     "push_windows": sim_windows, "ei_group": args.ei_group,
                     "pull_layout_bytes_per_synapse": round(csr.n_entries * 4 / max(net.n_synapses, 1), 4)
