@@ -452,7 +452,7 @@ class Network:
         return self.layout.members[shard][row], pre, q.astype(np.uint8)
 
 
-def upload_edges(graph: NeuronGraph, dev, chunk: int = 1 << 22, depth: int = 3):
+def upload_edges(graph: NeuronGraph, dev, chunk: int = 1 << 21, depth: int = 3):
     """Edge columns of a NeuronGraph on the device as int32 ids and uint8 weight units
     q = ceil(32 p) (q_from_p).
 

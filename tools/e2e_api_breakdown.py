@@ -40,7 +40,15 @@ def main():
         return r, round(time.perf_counter() - t0, 4)
 
     # the first simulate() call is what the bench's e2e_api measures (after the bench's own run)
+    import cProfile
+    import io
+    import pstats
+    pr = cProfile.Profile()
+    pr.enable()
     rep, out["simulate_first_s"] = timed(lambda: nc.simulate(g, pm, None, args.steps, seed=1))
+    pr.disable()
+    prof = io.StringIO()
+    pstats.Stats(pr, stream=prof).sort_stats("tottime").print_stats(25)
     out["loop_ms"] = round(rep.elapsed_ms, 3)
     for name, chunk in (("upload_s", 1 << 22), ("upload_chunk_1M_s", 1 << 20), ("upload_chunk_16M_s", 1 << 24)):
         r, out[name] = timed(lambda: S.upload_edges(g, dev, chunk=chunk))
@@ -59,6 +67,7 @@ def main():
     _, out["simulate_again_s"] = timed(lambda: nc.simulate(g, pm, None, args.steps, seed=1))
     out["threads"] = torch.get_num_threads()
     print(json.dumps(out), flush=True)
+    print(prof.getvalue(), file=sys.stderr)
 
 
 if __name__ == "__main__":
