@@ -209,13 +209,17 @@ def ops():
         return _ops
     import torch
     lib()   # the engine it links against, loaded and ABI-checked first
-    if not OPS_PATH.is_file():
-        raise RuntimeError(f"{OPS_PATH} not found: build it with `make -C paper_2205_07125_b200/csrc` "
+    # next to the engine (its rpath is $ORIGIN): an engine build elsewhere
+    # (NEUROCOMM_B200_LIB, kernel A/Bs) comes with its own extension build
+    path = Path(os.environ["NEUROCOMM_B200_LIB"]).with_name(OPS_PATH.name) if "NEUROCOMM_B200_LIB" in os.environ \
+        else OPS_PATH
+    if not path.is_file():
+        raise RuntimeError(f"{path} not found: build it with `make -C paper_2205_07125_b200/csrc` "
                            "(or __graft_entry__.build())")
-    torch.ops.load_library(str(OPS_PATH))
+    torch.ops.load_library(str(path))
     o = torch.ops.neurocomm_b200
     if int(o.abi_version()) != ABI_VERSION:
-        raise RuntimeError(f"{OPS_PATH} was built against ABI {int(o.abi_version())}, expected {ABI_VERSION}")
+        raise RuntimeError(f"{path} was built against ABI {int(o.abi_version())}, expected {ABI_VERSION}")
     _ops = o
     return _ops
 

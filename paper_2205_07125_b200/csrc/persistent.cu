@@ -47,7 +47,11 @@ __device__ __forceinline__ void grid_sync(unsigned int*, unsigned int, int32_t*)
   cooperative_groups::this_grid().sync();
 }
 
-__global__ void __launch_bounds__(kPThreads) k_persistent(const nc_shard_t sh, const nc_lif_params_t p,
+#ifndef NC_PERSIST_MIN_BLOCKS
+#define NC_PERSIST_MIN_BLOCKS 1
+#endif
+
+__global__ void __launch_bounds__(kPThreads, NC_PERSIST_MIN_BLOCKS) k_persistent(const nc_shard_t sh, const nc_lif_params_t p,
                                                           const nc_xchg_t X, int has_x, int n_steps, int B,
                                                           unsigned int* gbar, unsigned long long* st_ready,
                                                           unsigned long long* st_done, int stamp_cap,

@@ -442,10 +442,10 @@ extern "C" int nc_sim_lif_update(const nc_shard_t* sh, const nc_lif_params_t* p,
     nc_set_error("nc_sim_lif_update: shard has no acc buffer");
     return NC_E_ARG;
   }
-  // contiguous tile ranges, ~2 CTAs per SM (more if a range would exceed the
+  // contiguous tile ranges, ~4 CTAs per SM (more if a range would exceed the
   // shared spike-mask storage): one global atomic per bucket per CTA
   const int tiles = (sh->n_local + 31) / 32;
-  int grid = 2 * num_sms();
+  int grid = 4 * num_sms();
   if ((tiles + grid - 1) / grid > kLifMaxTiles) grid = (tiles + kLifMaxTiles - 1) / kLifMaxTiles;
   if (grid > tiles) grid = tiles > 0 ? tiles : 1;
   k_lif_update<<<grid, kLifThreads, 0, (cudaStream_t)stream>>>(*sh, *p);

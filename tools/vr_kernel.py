@@ -29,14 +29,19 @@ def main():
     ap.add_argument("--degree", type=float, default=1000.0)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--tile-words", type=int, default=None, help="force the bitmap tile size (A/B)")
+    ap.add_argument("--split", type=int, default=None, help="force log2 of the block split (A/B, 0-3)")
     args = ap.parse_args()
+    if args.split is not None:
+        from paper_2205_07125_b200 import sell
+        sell.block_split = lambda n_local, n_tiles, n_sms: args.split if n_tiles > 1 else 0
     peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] if (ROOT / "MEASURED_PEAKS.json").exists() \
         else 6544.0
     spec = S.GeneratorSpec.random(args.neurons, args.degree, seed=1)
     t1 = None
     for world in [int(x) for x in args.worlds.split(",")]:
         lay = S.ShardLayout.blocks(args.neurons, world)
-        nets = [S.Network.generate(spec, lay, shards=[r]) for r in range(world)]
+        nets = [S.Network.generate(spec, lay, shards=[r], tile_words=args.tile_words) for r in range(world)]
         n = args.warmup + args.steps
         vc = VirtualCluster(nets, S.LifParams(), 1, None, transport="p2p", delivery="fused")
         bufs = []
@@ -70,7 +75,7 @@ def main():
         out = {"world": world, "neurons": args.neurons, "kernel_ms_per_rank": [round(x, 5) for x in per],
                "kernel_ms_max": round(max(per), 5), "ideal_ms": round(t1 / world, 5) if t1 else None,
                "kernel_efficiency": round(t1 / world / max(per), 3) if t1 else None,
-               "tiles": nets[0].shards[0].n_tiles, "rows_per_rank": nets[0].shards[0].n_local,
+               "tiles": nets[0].shards[0].n_tiles, "split": args.split, "tile_words": nets[0].shards[0].tile_words, "rows_per_rank": nets[0].shards[0].n_local,
                "frac_slowest": round(alg[worst] / (per[worst] * 1e-3) / 1e9 / peak, 3)}
         print(json.dumps(out), flush=True)
         vc.close()
