@@ -48,7 +48,7 @@ __device__ __forceinline__ void grid_sync(unsigned int*, unsigned int, int32_t*)
 }
 
 #ifndef NC_PERSIST_MIN_BLOCKS
-#define NC_PERSIST_MIN_BLOCKS 1
+#define NC_PERSIST_MIN_BLOCKS 3   // <= 85 registers: 3 CTAs (24 warps) per SM for the latency-bound phases
 #endif
 
 __global__ void __launch_bounds__(kPThreads, NC_PERSIST_MIN_BLOCKS) k_persistent(const nc_shard_t sh, const nc_lif_params_t p,
@@ -149,6 +149,13 @@ extern "C" int nc_run_persistent(const nc_shard_t* sh, const nc_lif_params_t* p,
   const int nex = X ? X->n * B : 0;
   if (grid < nex) {
     nc_set_error("nc_run_persistent: %d exchange blocks exceed the resident grid (%d)", nex, grid);
+    return NC_E_ARG;
+  }
+  // the LIF phase keeps a spike mask per 32-row tile of the CTA's range in shared memory
+  const int64_t tiles = ((int64_t)sh->n_local + 31) / 32;
+  if ((tiles + grid - 1) / grid > ncdev::kLifMaxTiles) {
+    nc_set_error("nc_run_persistent: %lld rows need more than %d tiles per CTA on a %d-CTA grid",
+                 (long long)sh->n_local, ncdev::kLifMaxTiles, grid);
     return NC_E_ARG;
   }
   nc_xchg_t xz{};

@@ -466,14 +466,24 @@ static __device__ void lif_phase(const nc_shard_t& sh, const nc_lif_params_t& p,
     cta_base[h] = total ? atomicAdd(cnt, total) : 0;
   }
   __syncthreads();
-  // ---- pass B: write ids
+  // ---- pass B: write ids (hop masks of kLifUnroll tiles loaded together; none with
+  // one shard, where only the fired list is written)
   if (nb) {
-    for (int tile = t0 + warp; tile < t1; tile += kWarps) {
-      const uint32_t fmask = fmask_s[tile - t0];
-      if (!fmask) continue;
+    for (int tile0 = t0 + warp; tile0 < t1; tile0 += kWarps * kLifUnroll) {
+      uint32_t fm[kLifUnroll], hmu[kLifUnroll];
+#pragma unroll
+      for (int u = 0; u < kLifUnroll; ++u) {
+        const int tile = tile0 + u * kWarps;
+        fm[u] = tile < t1 ? fmask_s[tile - t0] : 0u;
+        hmu[u] = (nq && ((fm[u] >> lane) & 1u)) ? (uint32_t)sh.hop_mask[(tile << 5) + lane] : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < kLifUnroll; ++u) {
+      const int tile = tile0 + u * kWarps;
+      const uint32_t fmask = fm[u];
+      if (!fmask) continue;   // warp-uniform
       const int row = (tile << 5) + lane;
-      const bool fired = (fmask >> lane) & 1u;
-      const uint32_t hm = fired ? (uint32_t)sh.hop_mask[row] : 0u;
+      const uint32_t hm = hmu[u];
       const uint32_t my_id = (uint32_t)(sh.local_base + row);
       for (int h = 0; h < nb; ++h) {
         const uint32_t m = (h < nq) ? __ballot_sync(kFull, (hm >> h) & 1u) : fmask;
@@ -487,6 +497,7 @@ static __device__ void lif_phase(const nc_shard_t& sh, const nc_lif_params_t& p,
         if (lane == 0) warp_cnt[warp][h] += __popc(m);
         __syncwarp();
       }
+      }
     }
   }
   add_spike_total(sh, my_spikes, &block_count);
@@ -497,7 +508,6 @@ static __device__ void lif_phase(const nc_shard_t& sh, const nc_lif_params_t& p,
 // compacts the chunk's spikes into a shared list, then the warps take spikes
 // round-robin and walk each pre neuron's push row with 8 loads in flight per
 // lane, adding integer weights with red.global.add (exact, so order free).
-constexpr int kPushIds = 1024;
 
 // Fire-and-forget add.  Written out because inside the persistent kernel nvcc
 // otherwise emits ATOMG (returns a value) for the same atomicAdd.
@@ -505,8 +515,10 @@ __device__ __forceinline__ void red_add(int32_t* p, int32_t v) {
   asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+constexpr int kPushIds = 1024;
+
 struct PushSmem {
-  int chunk;
+  int next;
   int n;
   uint32_t ids[kPushIds];
 };
@@ -530,11 +542,20 @@ __device__ __forceinline__ void push_segment(const nc_shard_t& sh, int32_t negg,
 }
 
 // Event-driven delivery of the previous step's spikes.  Blocks claim 32-word
-// chunks of the spike bitmap, warp 0 compacts the chunk's spikes, the warps walk
-// their push rows.  Windowed push (sh.push_windows > 1): window `window` only
-// (its own claim counter work[4 + window]; the persistent engine runs the windows
-// one after the other with a grid barrier in between), or every window of each
-// row (window < 0, k_deliver_push).
+// chunks of the spike bitmap from a per-step counter (dynamic: the number of spikes
+// per chunk varies); warp 0 compacts the chunk's spikes into a shared list, then the
+// warps take spikes round-robin and walk each pre neuron's push row.  Warp 0 issues
+// the NEXT chunk's claim and bitmap load right after compacting the current one, so
+// both round trips overlap the rows instead of sitting between the two barriers of
+// every chunk (at config 3 over 4 GPUs a chunk's ~11 spikes x 250 synapses are about
+// one load round trip of work: the chunk overhead was ~80 of ~240 us per step).
+// (Measured and dropped: warps claiming chunks on their own -- no barriers, but a
+// chunk's spikes then run one after another in one warp, 2x slower at config 2 -- and
+// a spike list filled by the LIF phase and the exchange: the same at 4 GPUs, 8 %
+// slower on one.)  Windowed push (sh.push_windows > 1): window `window` only (its own
+// claim counter work[4 + window]; the persistent engine runs the windows one after the
+// other with a grid barrier in between), or every window of each row (window < 0,
+// k_deliver_push).
 static __device__ void push_phase(const nc_shard_t& sh, int32_t negg, int step, PushSmem& P, int window = -1) {
   const uint32_t* prev = ((step - 1) & 1) ? sh.bitmap1 : sh.bitmap0;
   const int lane = threadIdx.x & 31;
@@ -543,14 +564,18 @@ static __device__ void push_phase(const nc_shard_t& sh, int32_t negg, int step, 
   const int n_chunks = (sh.n_words + 31) >> 5;
   const int W = sh.push_windows > 1 ? sh.push_windows : 1;
   uint32_t* claim = (W > 1 && window >= 0) ? sh.work + 4 + window : sh.work;
+  // warp 0 holds the claimed chunk index and its bitmap words (one per lane)
+  int c = 0;
+  uint32_t bits = 0u;
+  if (warp == 0) {
+    if (lane == 0) c = (int)atomicAdd(claim, 1u);
+    c = __shfl_sync(kFull, c, 0);
+    const int w = (c << 5) + lane;
+    bits = (c < n_chunks && w < sh.n_words) ? prev[w] : 0u;
+  }
   for (;;) {
-    if (threadIdx.x == 0) P.chunk = (int)atomicAdd(claim, 1u);
-    __syncthreads();
-    const int c = P.chunk;
-    if (c >= n_chunks) break;
     if (warp == 0) {
       const int w = (c << 5) + lane;
-      uint32_t bits = w < sh.n_words ? prev[w] : 0u;
       const int cnt = __popc(bits);
       int incl = cnt;
 #pragma unroll
@@ -559,15 +584,26 @@ static __device__ void push_phase(const nc_shard_t& sh, int32_t negg, int step, 
         if (lane >= o) incl += y;
       }
       int pos = incl - cnt;
-      if (lane == 31) P.n = incl;
-      while (bits) {
-        const int b = __ffs(bits) - 1;
-        bits &= bits - 1;
-        P.ids[pos++] = ((uint32_t)w << 5) + (uint32_t)b;
+      if (lane == 31) P.n = c < n_chunks ? incl : -1;
+      uint32_t b = bits;
+      while (b) {
+        const int bit = __ffs(b) - 1;
+        b &= b - 1;
+        P.ids[pos++] = ((uint32_t)w << 5) + (uint32_t)bit;
+      }
+      // the next chunk's claim and bitmap words load while the rows below stream
+      if (c < n_chunks) {
+        int cn = 0;
+        if (lane == 0) cn = (int)atomicAdd(claim, 1u);
+        c = __shfl_sync(kFull, cn, 0);
+        const int wn = (c << 5) + lane;
+        bits = (c < n_chunks && wn < sh.n_words) ? prev[wn] : 0u;
       }
     }
     __syncthreads();
-    for (int i = warp; i < P.n; i += nwarps) {
+    const int n = P.n;
+    if (n < 0) break;   // uniform: warp 0 found the chunks exhausted
+    for (int i = warp; i < n; i += nwarps) {
       const uint32_t pre = P.ids[i];
       const int64_t r0 = sh.push_rowptr[pre];
       if (W == 1) {
@@ -576,8 +612,8 @@ static __device__ void push_phase(const nc_shard_t& sh, int32_t negg, int step, 
       }
       const uint16_t* wo = sh.push_winoff + (int64_t)pre * (W + 1);
       const int w0 = window >= 0 ? window : 0, w1 = window >= 0 ? window + 1 : W;
-      for (int w = w0; w < w1; ++w)
-        push_segment(sh, negg, r0 + wo[w], r0 + wo[w + 1], w * sh.push_window_rows, lane);
+      for (int x = w0; x < w1; ++x)
+        push_segment(sh, negg, r0 + wo[x], r0 + wo[x + 1], x * sh.push_window_rows, lane);
     }
     __syncthreads();
   }

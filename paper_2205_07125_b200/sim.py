@@ -801,7 +801,9 @@ class _ShardState:
         self.spk_ids = self.spk_count = None
         if binned:
             self.pb = _push_binned(csr, lay, h, dev)
-            # spike lists by step parity; every internal id fires at most once per step
+        if binned:
+            # spike lists by step parity (local fired ids from the LIF phase, remote ones
+            # appended by the exchange); every internal id fires at most once per step
             self.spk_cap = lay.n_words * 32
             self.spk_ids = torch.zeros(2 * self.spk_cap, dtype=torch.int32, device=dev)
             self.spk_count = torch.zeros(2, dtype=torch.int32, device=dev)
@@ -831,6 +833,7 @@ class _ShardState:
             self.c.pb_rowptr = self.pb["rowptr"].data_ptr()
             self.c.pb_binoff = self.pb["binoff"].data_ptr()
             self.c.pb_syn = self.pb["syn"].data_ptr()
+        if self.spk_ids is not None:
             self.c.spk_ids, self.c.spk_count, self.c.spk_cap = (self.spk_ids.data_ptr(), self.spk_count.data_ptr(),
                                                                 self.spk_cap)
 

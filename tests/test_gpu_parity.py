@@ -203,6 +203,28 @@ def test_persistent_engine_matches_oracle():
     assert_same(rep, ref)
 
 
+def test_persistent_engine_across_launches():
+    """The persistent engine's per-step counters (chunk claims, buckets) are reset at the
+    end of every step inside the kernel, so a run split over several launches
+    (advance(7), advance(13), advance(20)) gives the one-launch result."""
+    import torch
+    g = cfg1(2)
+    pm = nc.partition_greedy(g, 1)
+    lif = S.LifParams()
+    net = S.Network.from_graph(g, S.ShardLayout.from_assignment(pm.assignment, 1))
+    sim = S.Simulator(net, lif, 3, None, delivery="persistent", record_raster_steps=40, per_step_counts=True)
+    whole = sim.run(40)
+    assert_same(whole, oracle_run(g, pm, None, lif, 3, 40))
+    sim.reset(40)
+    for k in (7, 13, 20):
+        sim.advance(k)
+    torch.cuda.synchronize()
+    sim.check_status()
+    split = sim.report(40, 0.0)
+    np.testing.assert_array_equal(split.raster, whole.raster)
+    np.testing.assert_array_equal(split.v.view(np.uint32), whole.v.view(np.uint32))
+
+
 @pytest.mark.parametrize("tile_words", [None, 64])
 def test_binned_push_engine_matches_oracle(tile_words):
     """Event-driven step with binned push: each CTA sums its bin of every spiking

@@ -15,7 +15,7 @@ def main():
     for mode in ("push", "persistent"):
         sim = S.Simulator(net, S.LifParams(), 1, None, delivery=mode)
         st = torch.zeros((64, 4), dtype=torch.int64, device="cuda")
-        _native.lib().nc_persistent_phase_stamps(st.data_ptr() if mode == "persistent" else None)
+        _native.lib().nc_persistent_phase_stamps(st.data_ptr() if mode.startswith("persistent") else None)
         sim.reset(1)
         sim.advance(20)
         torch.cuda.synchronize()
@@ -25,10 +25,10 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         out[mode] = 200 / (e0.elapsed_time(e1) * 1e-3)
-        if mode == "persistent":
+        if mode.startswith("persistent"):
             a = st.cpu().numpy().astype(np.float64)
             d = np.diff(a, axis=1) / 1e3
-            print("persistent phases (us, median over 64 steps): push %.1f  lif %.1f  exchange %.1f  step %.1f" % (
+            print(mode, "phases (us, median over 64 steps): push %.1f  lif %.1f  exchange %.1f  step %.1f" % (
                 np.median(d[:, 0]), np.median(d[:, 1]), np.median(d[:, 2]),
                 np.median(np.diff(a[:, 0])) / 1e3))
     print({k: round(v, 1) for k, v in out.items()})
