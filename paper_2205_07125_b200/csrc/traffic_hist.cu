@@ -32,13 +32,17 @@ namespace {
 constexpr int kThreads = NC_K5_THREADS;
 constexpr size_t kSmemLimit = 96 * 1024;    // fall back to global limbs above this
 #ifndef NC_K5_UNIFORM_UNROLL
-#define NC_K5_UNIFORM_UNROLL 8   // 1-byte gathers: more edges in flight per thread
+#define NC_K5_UNIFORM_UNROLL 6   // 1-byte gathers: more edges in flight per thread
 #endif
+// A/B on B200 (tools/k5_kernel_ab.py, 4.9e7 edges, 8 GPUs; profiles/r02_k5_kernel_ab.log):
+// 8 KB of lane copies, >= 4 CTAs per SM (<= 64 registers) and 6 edges in flight per
+// thread on the uniform path: 0.216 ms (3.67 TB/s) against 0.246 with 16 KB / no
+// register cap / 8 in flight; 5 CTAs per SM or 12 in flight are slower.
 #ifndef NC_K5_SMEM_KB
-#define NC_K5_SMEM_KB 16
+#define NC_K5_SMEM_KB 8
 #endif
 #ifndef NC_K5_MIN_BLOCKS
-#define NC_K5_MIN_BLOCKS 1
+#define NC_K5_MIN_BLOCKS 4
 #endif
 constexpr size_t kSmemBudget = NC_K5_SMEM_KB * 1024;   // lane copies are halved down to this
 
