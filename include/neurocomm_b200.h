@@ -177,7 +177,7 @@ typedef struct nc_shard {
   int32_t n_words;        /* bitmap words over all internal ids incl. guard   */
   int32_t n_tiles;        /* bitmap tiles (1 = whole bitmap in shared memory)  */
   int32_t tile_words;     /* words per bitmap tile (multiple of 4)             */
-  int32_t flags;          /* bit 0: tiled partial sums in `acc` (huge shards); bits 1-2: s, the tiled kernel's warps claim each (slice, tile) block in 2^s parts (small shards) */
+  int32_t flags;          /* bit 0: tiled partial sums in `acc` (huge shards); bits 1-2: s, the tiled kernel's warps claim each (slice, tile) block in 2^s parts (small shards); bit 3: three tile buffers instead of two */
   /* neuron state, n_local each */
   float* v;
   float* i_syn;

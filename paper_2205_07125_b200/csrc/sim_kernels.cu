@@ -100,11 +100,11 @@ k_step_fused(const nc_shard_t sh, const nc_lif_params_t p) {
       meta = metan;
     }
   } else {
-    // Tiled: two tile buffers in shared memory, filled by TMA bulk copies that
-    // complete on mbarriers.  Warps claim (slice, tile) blocks dynamically and
+    // Tiled: two (or three) tile buffers in shared memory, filled by TMA bulk copies
+    // that complete on mbarriers.  Warps claim (slice, tile) blocks dynamically and
     // move on to the next tile as soon as they run out of work -- no CTA-wide
     // barrier between tiles: the last warp to leave tile t refills t's buffer
-    // with tile t + 2.  Warps span at most two consecutive tiles, so partial
+    // with tile t + NB.  Warps span at most NB consecutive tiles, so partial
     // sums are combined with shared (or, flags bit 0, global) integer atomics.
     const int T = sh.n_tiles, TW = sh.tile_words;
     // CTA c owns slices c, c+G, c+2G, ...: rows are ordered by degree inside the
@@ -112,9 +112,12 @@ k_step_fused(const nc_shard_t sh, const nc_lif_params_t p) {
     const int G = gridDim.x, c = blockIdx.x;
     const int cnt = c < n_slices ? (n_slices - c + G - 1) / G : 0;
     constexpr bool pglob = kGlobalPart;
-    int32_t* spart = reinterpret_cast<int32_t*>(sbm + 2 * TW);   // shared partials (!pglob)
-    __shared__ uint64_t full[2];
-    __shared__ int done[2];
+    // flags bit 3: three tile buffers (small tiles of small shards: a warp that runs out of
+    // tile t + 1 finds t + 2 already loaded instead of waiting for the last warp of t)
+    const int NB = (sh.flags & 8) ? 3 : 2;
+    int32_t* spart = reinterpret_cast<int32_t*>(sbm + NB * TW);   // shared partials (!pglob)
+    __shared__ uint64_t full[3];
+    __shared__ int done[3];
     __shared__ int next_slice[kMaxTiles];
     for (int k = threadIdx.x; k < cnt * 32; k += blockDim.x) {
       const int row = ((c + (k >> 5) * G) << 5) + (k & 31);
@@ -130,20 +133,21 @@ k_step_fused(const nc_shard_t sh, const nc_lif_params_t p) {
       return (uint32_t)((min(TW, sh.n_words - t * TW) + 3) >> 2) * 16u;
     };
     if (threadIdx.x == 0) {
-      done[0] = done[1] = 0;
-      mbar_init(&full[0], 1);
-      mbar_init(&full[1], 1);
+      for (int k = 0; k < NB; ++k) {
+        done[k] = 0;
+        mbar_init(&full[k], 1);
+      }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      for (int t = 0; t < 2 && t < T; ++t) {
+      for (int t = 0; t < NB && t < T; ++t) {
         mbar_arrive_expect_tx(&full[t], tile_bytes(t));
         bulk_g2s(sbm + t * TW, prev + t * TW, tile_bytes(t), &full[t]);
       }
     }
     __syncthreads();
     for (int t = 0; t < T; ++t) {
-      const int b = t & 1;
+      const int b = t % NB;
       const int w0 = t * TW;
-      mbar_wait(&full[b], (uint32_t)(t >> 1) & 1u);
+      mbar_wait(&full[b], (uint32_t)(t / NB) & 1u);
       // entries hold tile-relative pre ids: look them up in the staged copy directly
       const uint32_t* bm = sbm + b * TW;
       // the next claim's block start and row_meta load (and its first slots are
@@ -183,16 +187,16 @@ k_step_fused(const nc_shard_t sh, const nc_lif_params_t p) {
         b0 = b0n;
         meta = metan;
       }
-      // leave tile t; the last warp out refills its buffer with tile t + 2
+      // leave tile t; the last warp out refills its buffer with tile t + NB
       __syncwarp();
       if (lane == 0) {
         __threadfence_block();
         if (atomicAdd(&done[b], 1) == wpb - 1) {
           done[b] = 0;
-          if (t + 2 < T) {
+          if (t + NB < T) {
             fence_proxy_async_smem();
-            mbar_arrive_expect_tx(&full[b], tile_bytes(t + 2));
-            bulk_g2s(sbm + b * TW, prev + (t + 2) * TW, tile_bytes(t + 2), &full[b]);
+            mbar_arrive_expect_tx(&full[b], tile_bytes(t + NB));
+            bulk_g2s(sbm + b * TW, prev + (t + NB) * TW, tile_bytes(t + NB), &full[b]);
           }
         }
       }
@@ -288,11 +292,12 @@ int g_max_dyn_smem = 0;   // opt-in limit minus the kernels' static shared memor
 // the per-row partial sums of the CTA's slice range
 size_t step_smem_bytes(const nc_shard_t& sh, int grid) {
   if (sh.n_tiles <= 1) return (size_t)((sh.n_words + 3) >> 2) * 16;
-  // two tile buffers (+ the CTA's partial sums unless they live in acc)
-  if (sh.flags & 1) return (size_t)sh.tile_words * 8;
+  // two (flags bit 3: three) tile buffers (+ the CTA's partial sums unless they live in acc)
+  const size_t bufs = (size_t)sh.tile_words * 4 * ((sh.flags & 8) ? 3 : 2);
+  if (sh.flags & 1) return bufs;
   const int n_slices = (sh.n_local + 31) >> 5;
   const int per = (n_slices + grid - 1) / grid;
-  return (size_t)sh.tile_words * 8 + (size_t)per * 32 * 4;
+  return bufs + (size_t)per * 32 * 4;
 }
 
 template <bool kLif>

@@ -83,6 +83,17 @@ def plan_tiles(n_words: int, n_local: int, n_sms: int) -> tuple[int, int, bool]:
     return T, tw, global_part
 
 
+def triple_buffer(n_local: int, n_tiles: int, tile_words: int, n_sms: int, partials_global: bool) -> bool:
+    """Three tile buffers (nc_shard_t.flags bit 3) when a shard has 3+ tiles and they fit
+    next to the partial sums under SMEM_TILED: the small tiles of small strong-scaling
+    shards, where warps otherwise wait for the last warp of tile t before t + 2 loads."""
+    if n_tiles < 3:
+        return False
+    per = ((n_local + 31) // 32 + n_sms - 1) // n_sms
+    part = 0 if partials_global else per * 32 * 4
+    return 3 * tile_words * 4 + part <= SMEM_TILED
+
+
 def block_split(n_local: int, n_tiles: int, n_sms: int) -> int:
     """log2 of the parts each (slice, tile) block is split into for the warps' claims
     (nc_shard_t.flags bits 1-2; tiled kernel only): 1 below BALANCE_UNITS units per warp."""

@@ -810,7 +810,9 @@ class _ShardState:
         self.c = _native.ShardC(
             shard=h, n_shards=n, n_local=n_local, local_base=int(lay.base[h]), n_words=lay.n_words,
             n_tiles=csr.n_tiles, tile_words=csr.tile_words,
-            flags=(1 if csr.partials_global else 0) | (sell.block_split(n_local, csr.n_tiles, csr.cta_groups) << 1),
+            flags=(1 if csr.partials_global else 0) | (sell.block_split(n_local, csr.n_tiles, csr.cta_groups) << 1)
+            | (8 if sell.triple_buffer(n_local, csr.n_tiles, csr.tile_words, csr.cta_groups, csr.partials_global)
+               else 0),
             v=self.v.data_ptr(), i_syn=self.i_syn.data_ptr(), refrac=self.refrac.data_ptr(),
             acc=self.acc.data_ptr(), gid=self.gid.data_ptr(), hop_mask=self.hop_mask.data_ptr(),
             slice_ptr=csr.slice_ptr.data_ptr(), row_meta=csr.row_meta.data_ptr(), syn=csr.syn.data_ptr(),

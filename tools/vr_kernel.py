@@ -31,7 +31,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--tile-words", type=int, default=None, help="force the bitmap tile size (A/B)")
     ap.add_argument("--split", type=int, default=None, help="force log2 of the block split (A/B, 0-3)")
+    ap.add_argument("--buffers", type=int, default=None, choices=(2, 3), help="force the tile buffer count (A/B)")
     args = ap.parse_args()
+    if args.buffers is not None:
+        from paper_2205_07125_b200 import sell
+        sell.triple_buffer = lambda *a: args.buffers == 3
     if args.split is not None:
         from paper_2205_07125_b200 import sell
         sell.block_split = lambda n_local, n_tiles, n_sms: args.split if n_tiles > 1 else 0
@@ -75,7 +79,7 @@ def main():
         out = {"world": world, "neurons": args.neurons, "kernel_ms_per_rank": [round(x, 5) for x in per],
                "kernel_ms_max": round(max(per), 5), "ideal_ms": round(t1 / world, 5) if t1 else None,
                "kernel_efficiency": round(t1 / world / max(per), 3) if t1 else None,
-               "tiles": nets[0].shards[0].n_tiles, "split": args.split, "tile_words": nets[0].shards[0].tile_words, "rows_per_rank": nets[0].shards[0].n_local,
+               "tiles": nets[0].shards[0].n_tiles, "split": args.split, "buffers": args.buffers, "tile_words": nets[0].shards[0].tile_words, "rows_per_rank": nets[0].shards[0].n_local,
                "frac_slowest": round(alg[worst] / (per[worst] * 1e-3) / 1e9 / peak, 3)}
         print(json.dumps(out), flush=True)
         vc.close()
