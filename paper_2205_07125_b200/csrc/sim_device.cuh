@@ -17,10 +17,30 @@ constexpr int kUnroll = 8;        // 16-byte slots in flight per lane
 constexpr int kTailUnroll = NC_TAIL_UNROLL;   // ... in the ragged tail of a J-SELL block
 constexpr uint32_t kFull = 0xffffffffu;
 
+#ifndef NC_STREAM_EVICT_FIRST
+#define NC_STREAM_EVICT_FIRST 0
+#endif
+// Synapse stream loads: read once per step, so with NC_STREAM_EVICT_FIRST they are
+// marked L2 evict-first (an L2 cache-policy operand; the constant policy folds into the
+// load's uniform descriptor, no instruction) and leave L2 to what is reused: the
+// bitmap tiles and, for huge shards, the partial sums in `acc`.
+__device__ __forceinline__ uint64_t stream_policy() {
+  uint64_t pol = 0;
+#if NC_STREAM_EVICT_FIRST
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+#endif
+  return pol;
+}
+
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
   uint4 r;
+#if NC_STREAM_EVICT_FIRST
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(stream_policy()));
+#else
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+#endif
   return r;
 }
 
@@ -29,9 +49,15 @@ __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
 template <int kOff>
 __device__ __forceinline__ uint4 ld_stream_at(const uint4* p) {
   uint4 r;
+#if NC_STREAM_EVICT_FIRST
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4+%5], %6;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "n"(kOff), "l"(stream_policy()));
+#else
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4+%5];"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "l"(p), "n"(kOff));
+#endif
   return r;
 }
 
