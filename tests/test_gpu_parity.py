@@ -269,15 +269,19 @@ def test_partition_invariance_and_route_independence():
     np.testing.assert_array_equal(rep.raster, base.raster)
 
 
-@pytest.mark.parametrize("tile_words,glob,split", [(64, False, None), (100, False, 0), (96, True, None),
-                                                   (96, True, 0), (64, False, 2)])
-def test_tiled_bitmap_matches_oracle(tile_words, glob, split, monkeypatch):
+@pytest.mark.parametrize("tile_words,glob,split,buffers", [(64, False, None, None), (100, False, 0, None),
+                                                           (96, True, None, None), (96, True, 0, None),
+                                                           (64, False, 2, None), (64, False, None, 2),
+                                                           (96, True, None, 3)])
+def test_tiled_bitmap_matches_oracle(tile_words, glob, split, buffers, monkeypatch):
     """Force the shared-memory tiling of the spike bitmap (used above ~1.8 M neurons),
-    with the per-row partial sums in shared memory or (huge shards) in global memory, and
-    the blocks claimed whole (split 0), in halves (small shards: the default here) or in
-    quarters."""
+    with the per-row partial sums in shared memory or (huge shards) in global memory, the
+    blocks claimed whole (split 0), in halves (small shards: the default here) or in
+    quarters, and two or three tile buffers (the default for these small tiles: three)."""
     if split is not None:
         monkeypatch.setattr(sell, "block_split", lambda *a: split)
+    if buffers is not None:
+        monkeypatch.setattr(sell, "triple_buffer", lambda *a: buffers == 3)
     g = cfg1(2)
     pm = nc.partition_greedy(g, 2)
     rt = routes(g, pm, "direct")

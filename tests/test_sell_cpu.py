@@ -111,6 +111,16 @@ def test_plan_tiles():
     assert glob and T * tw >= 1_562_501 and 2 * tw * 4 <= sell.SMEM_BYTES - sell.SMEM_RESERVE
 
 
+def test_triple_buffer_choice():
+    # 3 buffers only for 3+ tiles that fit next to the partial sums under SMEM_TILED:
+    # config 2 over 8 GPUs (4 tiles of 7 840 words) yes; 1 GPU (2 tiles) and config 3 on
+    # one GPU (20 tiles of 15 648 words, 188 KB for three) no
+    assert sell.triple_buffer(125_000, 4, 7_840, 148, False)
+    assert not sell.triple_buffer(1_000_000, 2, 15_648, 148, False)
+    assert not sell.triple_buffer(10_000_000, 20, 15_648, 148, True)
+    assert sell.triple_buffer(5_000, 5, 64, 148, False)
+
+
 def test_small_shard_balance():
     # strong scaling of the config-2 network: 1 / 2 GPUs unchanged, 4 GPUs split blocks,
     # 8 GPUs split blocks over 4 tiles (>= BALANCE_UNITS claim units per warp)
