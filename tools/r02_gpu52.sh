@@ -1,0 +1,13 @@
+#!/bin/bash
+mkdir -p gpurun_out
+o=gpurun_out/r02_prefetch_ab.jsonl; : > $o
+for rep in 1 2; do
+  for l in default variants/nopf; do
+    if [ $l = default ]; then E=""; else E="NEUROCOMM_B200_LIB=$l/libneurocomm_b200.so"; fi
+    env $E timeout 900 python tools/vr_kernel.py --worlds 1,4,8 --steps 200 2>/dev/null | python -c "
+import json,sys
+for l in sys.stdin:
+    d=json.loads(l); d['lib']='$l'; print(json.dumps(d))" | tee -a $o
+  done
+done
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -p no:cacheprovider -x -k "tiled or config2 or fused" > gpurun_out/r02_pf_tests.log 2>&1; tail -1 gpurun_out/r02_pf_tests.log
