@@ -26,6 +26,7 @@ to --out.
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import sys
@@ -178,6 +179,7 @@ def main() -> int:
     rates = [float(r) for r in args.rates.split(",")] if args.rates else list(cfg["rates"])
     out_path = Path(args.out) if args.out else None
     model_rows = []   # config 4: (route table, nu, measured exchange p50) for the netsim calibration
+    digests = {}      # rate -> {engine/route: state digest}
 
     class A:   # the timing helpers' argument bundle
         steps, warmup, chunk, transport, msg_cap, seed, fused_send = (args.steps, args.warmup, args.chunk, "p2p",
@@ -206,6 +208,19 @@ def main() -> int:
                 hop = sim.hop_ids.sum(0).clone()
                 if world > 1:
                     dist.all_reduce(hop)
+                # the state after warm-up + timed steps: every engine and route of one rate runs
+                # the same dynamics from the same seed, so the digests must agree (bit-exact
+                # cross-engine check at real size, where the CPU oracle cannot follow)
+                digest = hashlib.sha256()
+                for st_ in sim.states:
+                    digest.update(st_.v[: st_.n_local].cpu().numpy().tobytes())
+                    digest.update(st_.i_syn[: st_.n_local].cpu().numpy().tobytes())
+                digest = digest.hexdigest()
+                if world > 1:
+                    parts = [None] * world
+                    dist.all_gather_object(parts, digest)
+                    digest = hashlib.sha256("".join(parts).encode()).hexdigest()
+                state_sha = digest[:16]
                 fused_send = getattr(sim, "fused_send", None)
                 sim_windows = sim.states[0].c.push_windows if eng != "fused" else None
                 if world > 1:
@@ -234,6 +249,7 @@ def main() -> int:
                     if want_pull else None, "build_s": round(build_s, 1),
                     "planner": planner, "clocks": clocks.summary(), "case_s": round(time.time() - t_case, 1),
                     "skipped_engines": skipped or None,
+                    "state_sha256_16": state_sha,
                 }
                 if planner is not None and rt is not None:
                     # the reference's analytic per-step model (netsim.py:177-246) for the same table,
@@ -257,10 +273,20 @@ def main() -> int:
                                  + lay.n_local(rank) * 22)
                     row["layout_bytes_rank0"] = int(lay_bytes)
                     row["layout_frac_rank0"] = round(lay_bytes / (kms_ranks[0] * 1e-3) / peak, 3)
+                digests.setdefault(str(rate), {})[f"{eng}/{mode}"] = state_sha
                 print(json.dumps(row), flush=True)
                 if out_path:
                     with out_path.open("a") as f:
                         f.write(json.dumps(row) + "\n")
+    if rank == 0 and any(len(d) > 1 for d in digests.values()):
+        agree = {"cross_engine_state_agreement": {r: len(set(d.values())) == 1 for r, d in digests.items()},
+                 "state_sha256_16": digests,
+                 "what": "V and I of every neuron after warm-up + timed steps, per rate: every engine (pull / "
+                         "event-driven) and route (direct / two-level) must reach the same bits"}
+        print(json.dumps(agree), flush=True)
+        if out_path:
+            with out_path.open("a") as f:
+                f.write(json.dumps(agree) + "\n")
     if rank == 0 and len(model_rows) >= 4:
         # calibrate the reference's TopologySpec on the measured exchange latency
         spec_fit, fit = nc.netsim.calibrate_topology([(rt, nu, t) for rt, nu, t, _ in model_rows], gt, world)
