@@ -166,6 +166,17 @@ constexpr int kPfTiled = NC_PF_DIST;
 // `part` of `nparts` (small shards split blocks so that every warp has several
 // units to claim): part k takes the k-th run of whole load groups of the
 // regular part; the last part also takes the ragged tail.
+#ifndef NC_ROWSUM_LEAN
+#define NC_ROWSUM_LEAN 1
+#endif
+
+// All kUnroll slots of a group (no padding: no predicates, no zeroed registers).
+template <int... U>
+__device__ __forceinline__ void load_group_full(uint4 (&e)[sizeof...(U)], const uint4* q,
+                                                std::integer_sequence<int, U...>) {
+  ((e[U] = ld_stream_at<U * 512>(q)), ...);
+}
+
 template <int kPfDist>
 __device__ __forceinline__ int32_t sell_row_sum(const uint4* __restrict__ blk, uint32_t meta,
                                                 const uint32_t* __restrict__ bm, int32_t g_inh, int lane,
@@ -181,6 +192,41 @@ __device__ __forceinline__ int32_t sell_row_sum(const uint4* __restrict__ blk, u
   const int per = nparts == 1 ? lo : ((lo + nparts - 1) / nparts + kUnroll - 1) / kUnroll * kUnroll;
   const int ub = min(lo, part * per);
   const int ue = min(lo, ub + per);
+#if NC_ROWSUM_LEAN
+  // Slots below the warp's smallest emid are excitatory in every lane and slots at or above
+  // its largest are inhibitory in every lane (warp-uniform tests): those add into accE /
+  // accI and only the few slots in between pick a per-lane weight.  Whole groups load
+  // without predicates.
+  const int elo = (int)__reduce_min_sync(kFull, (unsigned)emid);
+  const int ehi = (int)__reduce_max_sync(kFull, (unsigned)emid);
+  int32_t accE = 0, accI = 0;
+  auto add_slot = [&](const uint4& x, int slot) {
+    const int32_t t = slot_term(x, bm);
+    if (slot < elo) accE += t;
+    else if (slot >= ehi) accI += t;
+    else acc += t * (slot < emid ? 1 : wi);
+  };
+  for (int u0 = ub; u0 < ue; u0 += kUnroll) {
+    if (kPfDist > 0 && lane == 0 && u0 + kPfDist < ue) {
+      const int a = u0 + kPfDist;
+      prefetch_l2(blk + a * 32, (uint32_t)min(kUnroll, ue - a) * 512u);
+    }
+    uint4 e[kUnroll];
+    if (ue - u0 >= kUnroll) {   // warp-uniform
+      load_group_full(e, p + u0 * 32, std::make_integer_sequence<int, kUnroll>{});
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) add_slot(e[u], u0 + u);
+    } else {
+      load_group(e, p + u0 * 32, ue - u0, padv, std::make_integer_sequence<int, kUnroll>{});
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        if (u0 + u >= ue) break;   // warp-uniform: no lookups for the pad of a partial group
+        add_slot(e[u], u0 + u);
+      }
+    }
+  }
+  acc += accE + accI * wi;
+#else
   // regular part: every lane has slots [0, lo)
   for (int u0 = ub; u0 < ue; u0 += kUnroll) {
     if (kPfDist > 0 && lane == 0 && u0 + kPfDist < ue) {
@@ -195,6 +241,7 @@ __device__ __forceinline__ int32_t sell_row_sum(const uint4* __restrict__ blk, u
       acc += slot_term(e[u], bm) * (u0 + u < emid ? 1 : wi);
     }
   }
+#endif
   if (part != nparts - 1) return acc;
   // ragged tail (short: rows of a block have near-equal lengths)
   int off = lo * 32;
