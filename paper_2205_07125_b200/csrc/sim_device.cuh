@@ -100,13 +100,19 @@ __device__ __forceinline__ uint32_t field_term(uint32_t f, const uint32_t* __res
   return acc + (f & (uint32_t)fired & (63u << 19));
 }
 
+// Weight units of the fired pres of one 16-byte slot (5 synapses), still scaled by 2^19
+// and added to acc (a whole group of slots can be summed before one shift: <= 8 x 160
+// units x 2^19 < 2^31).
+__device__ __forceinline__ uint32_t slot_term_raw(uint4 e, const uint32_t* __restrict__ bm, uint32_t acc) {
+  const Fields x = unpack_slot(e);
+#pragma unroll
+  for (int i = 0; i < kSlotEntries; ++i) acc = field_term(x.f[i], bm, acc);
+  return acc;
+}
+
 // Weight units of the fired pres of one 16-byte slot (5 synapses).
 __device__ __forceinline__ int32_t slot_term(uint4 e, const uint32_t* __restrict__ bm) {
-  const Fields x = unpack_slot(e);
-  uint32_t s = field_term(x.f[0], bm, 0u);
-#pragma unroll
-  for (int i = 1; i < kSlotEntries; ++i) s = field_term(x.f[i], bm, s);
-  return (int32_t)(s >> 19);   // <= 5 x 32 weight units
+  return (int32_t)(slot_term_raw(e, bm, 0u) >> 19);   // <= 5 x 32 weight units
 }
 
 // ---- 1-D TMA bulk copies into shared memory, completed on an mbarrier
@@ -214,8 +220,16 @@ __device__ __forceinline__ int32_t sell_row_sum(const uint4* __restrict__ blk, u
     uint4 e[kUnroll];
     if (ue - u0 >= kUnroll) {   // warp-uniform
       load_group_full(e, p + u0 * 32, std::make_integer_sequence<int, kUnroll>{});
+      if (u0 + kUnroll <= elo || u0 >= ehi) {   // warp-uniform: one sign for the whole group
+        uint32_t g = 0u;
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) add_slot(e[u], u0 + u);
+        for (int u = 0; u < kUnroll; ++u) g = slot_term_raw(e[u], bm, g);
+        if (u0 >= ehi) accI += (int32_t)(g >> 19);
+        else accE += (int32_t)(g >> 19);
+      } else {
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) add_slot(e[u], u0 + u);
+      }
     } else {
       load_group(e, p + u0 * 32, ue - u0, padv, std::make_integer_sequence<int, kUnroll>{});
 #pragma unroll
