@@ -81,6 +81,10 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   return t;
 }
 
+#ifndef NC_OFFSET_FMA
+#define NC_OFFSET_FMA 0
+#endif
+
 // Weight units of one synapse field ((q << 19) | (id ^ 31), id relative to the
 // staged tile) if its pre fired, still scaled by 2^19, added to acc.  The left
 // funnel shift by the field's low 5 bits (31 - bit) moves the pre's spike bit to
@@ -89,8 +93,15 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 __device__ __forceinline__ uint32_t field_term(uint32_t f, const uint32_t* __restrict__ bm, uint32_t acc) {
   // byte offset of the bitmap word, added to the (warp-uniform) buffer base by
   // the load itself: LDS [R + UR], 2 ALU ops per lookup
+#if NC_OFFSET_FMA
+  // f >> 3 as a high multiply: on the FMA pipe, next to the ALU-pipe-bound rest
+  uint32_t f3;
+  asm("mul.hi.u32 %0, %1, 536870912;" : "=r"(f3) : "r"(f));
+#else
+  const uint32_t f3 = f >> 3;
+#endif
   const uint32_t word = *reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(bm) +
-                                                           ((f >> 3) & ((kFieldIdMask >> 5) << 2)));
+                                                           (f3 & ((kFieldIdMask >> 5) << 2)));
   // the pre's bit to bit 31 (the field stores 31 - bit), sign-spread to a mask that
   // keeps the field's q bits: 3 ALU ops, no multiply; slot_term shifts the sum down once
   // (measured against bit * q as one IMAD per field: 0.543 vs 0.565 ms in a sustained
