@@ -10,7 +10,10 @@
 
 namespace ncdev {
 
-constexpr int kUnroll = 8;        // 16-byte slots in flight per lane
+#ifndef NC_UNROLL
+#define NC_UNROLL 8
+#endif
+constexpr int kUnroll = NC_UNROLL;   // 16-byte slots in flight per lane
 #ifndef NC_TAIL_UNROLL
 #define NC_TAIL_UNROLL 4
 #endif
