@@ -471,7 +471,7 @@ using LifSmem = LifSmemT<kLifWarps>;
 // synaptic input comes from acc (consumed and zeroed) or, when sacc is given,
 // from shared memory indexed by the row's offset in the block's range.  The
 // fired list is sh.fired_ids, or the step's spike list when sh.spk_ids is set.
-template <int kWarps>
+template <int kWarps, int kU = kLifUnroll>
 static __device__ void lif_phase(const nc_shard_t& sh, const nc_lif_params_t& p, int step, int bid, int nblk,
                                  LifSmemT<kWarps>& S, const int32_t* sacc = nullptr) {
   unsigned int& block_count = S.block_count;
@@ -495,18 +495,18 @@ static __device__ void lif_phase(const nc_shard_t& sh, const nc_lif_params_t& p,
   const int per = (ntiles + nblk - 1) / nblk;
   const int t0 = bid * per, t1 = min(ntiles, t0 + per);
   uint32_t my_spikes = 0;
-  // ---- pass A: update, spike masks, per-warp bucket counts.  kLifUnroll tiles per
+  // ---- pass A: update, spike masks, per-warp bucket counts.  kU tiles per
   // warp and iteration with every state load issued before the first use: one
-  // memory round trip per kLifUnroll tiles instead of two per tile (loads after
+  // memory round trip per kU tiles instead of two per tile (loads after
   // the acc store and the hop-mask load behind the update serialised; at config 3,
   // 10 M rows on one GPU, the LIF phase took 444 us of a 992 us step).
-  for (int tile0 = t0 + warp; tile0 < t1; tile0 += kWarps * kLifUnroll) {
-    float v[kLifUnroll], isyn[kLifUnroll];
-    uint8_t ref[kLifUnroll];
-    int32_t a[kLifUnroll];
-    uint32_t gid[kLifUnroll], hm[kLifUnroll];
+  for (int tile0 = t0 + warp; tile0 < t1; tile0 += kWarps * kU) {
+    float v[kU], isyn[kU];
+    uint8_t ref[kU];
+    int32_t a[kU];
+    uint32_t gid[kU], hm[kU];
 #pragma unroll
-    for (int u = 0; u < kLifUnroll; ++u) {
+    for (int u = 0; u < kU; ++u) {
       const int tile = tile0 + u * kWarps;
       const int row = (tile << 5) + lane;
       const bool ok = tile < t1 && row < sh.n_local;
@@ -519,13 +519,13 @@ static __device__ void lif_phase(const nc_shard_t& sh, const nc_lif_params_t& p,
     }
     if (!sacc) {
 #pragma unroll
-      for (int u = 0; u < kLifUnroll; ++u) {
+      for (int u = 0; u < kU; ++u) {
         const int row = ((tile0 + u * kWarps) << 5) + lane;
         if (tile0 + u * kWarps < t1 && row < sh.n_local) sh.acc[row] = 0;
       }
     }
 #pragma unroll
-    for (int u = 0; u < kLifUnroll; ++u) {
+    for (int u = 0; u < kU; ++u) {
       const int tile = tile0 + u * kWarps;
       if (tile >= t1) break;   // warp-uniform
       const int row = (tile << 5) + lane;
@@ -567,19 +567,19 @@ static __device__ void lif_phase(const nc_shard_t& sh, const nc_lif_params_t& p,
     cta_base[h] = total ? atomicAdd(cnt, total) : 0;
   }
   __syncthreads();
-  // ---- pass B: write ids (hop masks of kLifUnroll tiles loaded together; none with
+  // ---- pass B: write ids (hop masks of kU tiles loaded together; none with
   // one shard, where only the fired list is written)
   if (nb) {
-    for (int tile0 = t0 + warp; tile0 < t1; tile0 += kWarps * kLifUnroll) {
-      uint32_t fm[kLifUnroll], hmu[kLifUnroll];
+    for (int tile0 = t0 + warp; tile0 < t1; tile0 += kWarps * kU) {
+      uint32_t fm[kU], hmu[kU];
 #pragma unroll
-      for (int u = 0; u < kLifUnroll; ++u) {
+      for (int u = 0; u < kU; ++u) {
         const int tile = tile0 + u * kWarps;
         fm[u] = tile < t1 ? fmask_s[tile - t0] : 0u;
         hmu[u] = (nq && ((fm[u] >> lane) & 1u)) ? (uint32_t)sh.hop_mask[(tile << 5) + lane] : 0u;
       }
 #pragma unroll
-      for (int u = 0; u < kLifUnroll; ++u) {
+      for (int u = 0; u < kU; ++u) {
       const int tile = tile0 + u * kWarps;
       const uint32_t fmask = fm[u];
       if (!fmask) continue;   // warp-uniform

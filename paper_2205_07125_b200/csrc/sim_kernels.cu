@@ -224,9 +224,16 @@ k_step_fused(const nc_shard_t sh, const nc_lif_params_t p) {
 }
 
 // K1+K2 alone: consumes and zeroes acc.
+#ifndef NC_LIF_UNROLL_ALONE
+#define NC_LIF_UNROLL_ALONE 8
+#endif
+// K1+K2 as its own kernel (per-kernel event-driven engine): 8 tiles per warp in flight
+// (128 registers, 2 CTAs per SM; config 3, 10 M rows: 1 / 3 / 4 / 8 in flight = 453 /
+// 320 / 242 / 103 us), while inside the persistent engine, capped at 80 registers, 4 is
+// best (88 us).
 __global__ void __launch_bounds__(kLifThreads) k_lif_update(const nc_shard_t sh, const nc_lif_params_t p) {
   __shared__ LifSmem S;
-  lif_phase(sh, p, *sh.step, blockIdx.x, gridDim.x, S);
+  lif_phase<kLifWarps, NC_LIF_UNROLL_ALONE>(sh, p, *sh.step, blockIdx.x, gridDim.x, S);
 }
 
 __global__ void __launch_bounds__(256) k_deliver_push(const nc_shard_t sh, int32_t negg) {
@@ -447,10 +454,15 @@ extern "C" int nc_sim_lif_update(const nc_shard_t* sh, const nc_lif_params_t* p,
     nc_set_error("nc_sim_lif_update: shard has no acc buffer");
     return NC_E_ARG;
   }
-  // contiguous tile ranges, ~4 CTAs per SM (more if a range would exceed the
-  // shared spike-mask storage): one global atomic per bucket per CTA
+  // contiguous tile ranges, one wave of resident CTAs (more if a range would exceed
+  // the shared spike-mask storage): one global atomic per bucket per CTA
   const int tiles = (sh->n_local + 31) / 32;
-  int grid = 4 * num_sms();
+  static int occ = 0;
+  if (occ == 0) {
+    NC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lif_update, kLifThreads, 0));
+    if (occ < 1) occ = 1;
+  }
+  int grid = occ * num_sms();
   if ((tiles + grid - 1) / grid > kLifMaxTiles) grid = (tiles + kLifMaxTiles - 1) / kLifMaxTiles;
   if (grid > tiles) grid = tiles > 0 ? tiles : 1;
   k_lif_update<<<grid, kLifThreads, 0, (cudaStream_t)stream>>>(*sh, *p);
