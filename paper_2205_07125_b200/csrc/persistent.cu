@@ -4,12 +4,14 @@
 // so a step costs no kernel launches and no host involvement at all.
 //
 // Per step (same arithmetic as the per-kernel path, hence bit-identical):
-//   1. push_phase   acc += weights of the previous step's spikes (all blocks)
+//   1. push_phase   acc += weights of the previous step's spikes (all blocks; with
+//                   push windows, one L2-sized post-row window at a time, a grid
+//                   barrier between windows)
 //   2. grid barrier
 //   3. lif_phase    LIF update, spike bitmap, CTA-aggregated bucket appends
 //   4. grid barrier; stamp "buckets ready"
-//   5. p2p_block    blocks [0, n*B): NVLink stores into the peers' inboxes,
-//                   release/acquire flags, scatter (+ relay phase if two-level)
+//   5. p2p_block    blocks [0, n*B): NVLink stores of tagged 8-byte words into the
+//                   peers' inboxes, poll + scatter (relays forward as ids arrive)
 //   6. grid barrier; stamp "all inbound spikes in the bitmap"; reset counters
 // The grid is sized from the occupancy calculator and launched cooperatively,
 // so every block is resident and the barriers cannot deadlock; the flag waits
