@@ -75,3 +75,39 @@ def test_virtual_ranks_p2p_matches_oracle(world, mode, fused):
             assert np.isfinite(rep.extra["exchange_us"]).all()
     finally:
         vc.close()
+
+
+def test_eight_rank_strong_scaling_shape_matches_one_gpu():
+    """The shard shape of config 2 over 8 GPUs -- the bench's strong scaling at N = 8, which
+    gpurun cannot run on 8 real GPUs: 125 k rows per rank, 4 bitmap tiles, blocks claimed
+    in halves, three tile buffers -- as 8 virtual ranks, against the same network on one GPU
+    (2 tiles, one shard): identical rasters and V after 12 steps."""
+    import torch
+    from virtual_ranks import VirtualCluster
+    from paper_2205_07125_b200 import sell
+    n = 1_000_000
+    spec = S.GeneratorSpec.random(n, 1000.0, seed=1)
+    lif = S.LifParams()
+    one = S.Network.generate(spec, S.ShardLayout.blocks(n, 1))
+    ref = S.Simulator(one, lif, 1, None, record_raster_steps=12).run(12)
+    lay1 = one.layout
+    del one
+    torch.cuda.empty_cache()
+    lay = S.ShardLayout.blocks(n, 8)
+    nets = [S.Network.generate(spec, lay, shards=[r]) for r in range(8)]
+    csr = nets[0].shards[0]
+    sms = sell.device_sms()
+    assert csr.n_tiles >= 3 and sell.triple_buffer(csr.n_local, csr.n_tiles, csr.tile_words, csr.cta_groups,
+                                                   csr.partials_global)
+    assert sell.block_split(csr.n_local, csr.n_tiles, sms) == 1
+    vc = VirtualCluster(nets, lif, 1, None, transport="p2p", delivery="fused", record_raster_steps=12,
+                        blocks_per_peer=1)
+    try:
+        rep = vc.run(12)
+    finally:
+        vc.close()
+    assert rep.spikes == ref.spikes > 0
+    np.testing.assert_array_equal(rep.raster, ref.raster)
+    np.testing.assert_array_equal(rep.v.view(np.uint32), ref.v.view(np.uint32))
+    np.testing.assert_array_equal(rep.i_syn.view(np.uint32), ref.i_syn.view(np.uint32))
+    assert lay1.n_neurons == lay.n_neurons
