@@ -1,3 +1,8 @@
+"""The per-kernel event-driven engine's kernels timed alone at config 3 (or N neurons):
+k_deliver_push, k_lif_update and k_end_step, each launched back to back with CUDA events
+(bench.kernel_ms), after 100 steps of the network.
+
+    python tools/lif_time.py [n_neurons]"""
 import sys, torch
 sys.path.insert(0, '.')
 import bench as B
