@@ -98,6 +98,12 @@ int nc_traffic_histogram_uniform(const int32_t* edge_i, const int32_t* edge_j, c
                                  double weight, const uint8_t* assignment, int64_t n_edges, int32_t n_gpus,
                                  int32_t lsb_exponent, int32_t n_digits, unsigned long long* pg_limbs,
                                  void* stream);
+/* Host pass of the edge upload (sim.upload_edges): int64 ids and fp64 p of n edges ->
+ * int32 ids and uint8 weight units q = clamp(ceil(32 p), 1, 32) in caller buffers (pinned
+ * staging), `threads` host threads (0 = all); NC_E_ARG if an endpoint lies outside
+ * [0, n_neurons). */
+int nc_edges_narrow(const int64_t* edge_i, const int64_t* edge_j, const double* edge_p, int64_t n,
+                    int64_t n_neurons, int32_t* out_i, int32_t* out_j, uint8_t* out_q, int32_t threads);
 /* PartitionMap.assignment (int64) -> uint8 gpu ids for nc_traffic_histogram_uniform,
  * counts[g] += neurons on GPU g (uint64 [n_gpus], zeroed by the caller), *bad |= 1
  * if a value lies outside [0, n_gpus) (written as 0; the caller raises, as the

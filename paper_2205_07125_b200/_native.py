@@ -107,6 +107,8 @@ _SIGS = {
                                               c_int32, c_void_p, c_void_p]),
     "nc_traffic_histogram_uniform": (c_int32, [c_void_p, c_void_p, c_void_p, c_double, c_void_p, c_int64, c_int32,
                                                c_int32, c_int32, c_void_p, c_void_p]),
+    "nc_edges_narrow": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
+                                  c_int32]),
     "nc_assignment_u8": (c_int32, [c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
     "nc_traffic_histogram32": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int32,
                                        c_int32, c_int32, c_void_p, c_void_p]),

@@ -323,3 +323,42 @@ extern "C" int nc_greedy_fill_generated(const nc_graphgen_t* spec, const double*
     if (free_[k]) assignment[k] = n_buckets - 1;
   return NC_OK;
 }
+
+// Host side of the edge upload (sim.upload_edges): NeuronGraph columns (int64 ids, fp64 p)
+// narrowed into pinned staging buffers as the device takes them -- int32 ids and uint8
+// weight units q = clamp(ceil(32 p), 1, 32) (sim.q_from_p) -- in one multi-threaded pass, so
+// the copy engine moves 9 instead of 24 bytes per edge.  Endpoints outside [0, n_neurons)
+// are an NC_E_ARG error (nothing is uploaded for the chunk).
+extern "C" int nc_edges_narrow(const int64_t* edge_i, const int64_t* edge_j, const double* edge_p, int64_t n,
+                               int64_t n_neurons, int32_t* out_i, int32_t* out_j, uint8_t* out_q,
+                               int32_t threads) {
+  if (n < 0 || (n && (!edge_i || !edge_j || !edge_p || !out_i || !out_j || !out_q)) || n_neurons < 1 ||
+      n_neurons >= (int64_t(1) << 31)) {
+    nc_set_error("nc_edges_narrow: bad arguments");
+    return NC_E_ARG;
+  }
+  if (n == 0) return NC_OK;
+  int T = n_threads(threads);
+  if ((int64_t)T * 65536 > n) T = (int)std::max<int64_t>(1, n / 65536);
+  const std::vector<int64_t> cut = even_ranges(n, T);
+  std::vector<int> bad(T, 0);
+  parallel_rows(cut, [&](int t, int64_t b, int64_t e) {
+    int oob = 0;
+    for (int64_t k = b; k < e; ++k) {
+      const int64_t a = edge_i[k], c = edge_j[k];
+      oob |= (a < 0) | (a >= n_neurons) | (c < 0) | (c >= n_neurons);
+      out_i[k] = (int32_t)a;
+      out_j[k] = (int32_t)c;
+      double q = std::ceil(edge_p[k] * 32.0);
+      q = q < 1.0 ? 1.0 : (q > 32.0 ? 32.0 : q);
+      out_q[k] = (uint8_t)q;
+    }
+    bad[t] = oob;
+  });
+  for (int t = 0; t < T; ++t)
+    if (bad[t]) {
+      nc_set_error("edge endpoints outside [0, %lld)", (long long)n_neurons);
+      return NC_E_ARG;
+    }
+  return NC_OK;
+}

@@ -452,11 +452,12 @@ class Network:
         return self.layout.members[shard][row], pre, q.astype(np.uint8)
 
 
-def upload_edges(graph: NeuronGraph, dev, chunk: int = 1 << 21, depth: int = 3):
+def upload_edges(graph: NeuronGraph, dev, chunk: int | None = None, depth: int = 3):
     """Edge columns of a NeuronGraph on the device as int32 ids and uint8 weight units
     q = ceil(32 p) (q_from_p).
 
-    Pipelined through `depth` pinned staging buffers of `chunk` edges: the host copies
+    int64 id columns (the reference's): `_upload_edges_narrowed`, narrowed on the host.
+    Other integer widths: pipelined through `depth` pinned staging buffers of `chunk` edges: the host copies
     chunk k into a pinned buffer (torch's multi-threaded CPU copy, any integer / float
     dtype widened to int64 / float64) while the copy engine moves chunk k-1 and a side
     stream narrows it on the device; endpoint range checks are reduced on the device and
@@ -472,9 +473,13 @@ def upload_edges(graph: NeuronGraph, dev, chunk: int = 1 << 21, depth: int = 3):
     qd = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
     if n == 0:
         return ei, ej, qd[:0]
-    src = [torch.from_numpy(np.ascontiguousarray(a)) for a in (graph.edge_i, graph.edge_j)]
-    src_p = torch.from_numpy(np.ascontiguousarray(graph.edge_p, dtype=np.float64))
-    c = min(chunk, n)
+    cols = [np.ascontiguousarray(a) for a in (graph.edge_i, graph.edge_j)]
+    pcol = np.ascontiguousarray(graph.edge_p, dtype=np.float64)
+    if all(c.dtype == np.int64 for c in cols):
+        return _upload_edges_narrowed(cols[0], cols[1], pcol, m, ei, ej, qd, dev, chunk or (1 << 23), depth)
+    src = [torch.from_numpy(a) for a in cols]
+    src_p = torch.from_numpy(pcol)
+    c = min(chunk or (1 << 21), n)
     k_buf = min(depth, (n + c - 1) // c)
     host = [torch.empty((3, c), dtype=torch.int64, pin_memory=True) for _ in range(k_buf)]
     devb = [torch.empty((3, c), dtype=torch.int64, device=dev) for _ in range(k_buf)]
@@ -509,6 +514,43 @@ def upload_edges(graph: NeuronGraph, dev, chunk: int = 1 << 21, depth: int = 3):
         t.record_stream(side)
     if int(lo.item()) < 0 or int(hi.item()) >= m:
         raise ValueError(f"edge endpoints outside [0, {m})")
+    return ei, ej, qd[:n]
+
+
+def _upload_edges_narrowed(ci, cj, cp, m: int, ei, ej, qd, dev, chunk: int, depth: int):
+    """upload_edges for int64 / fp64 columns (what generate_synthetic and load_graph give):
+    the host narrows each chunk into pinned staging buffers -- int32 ids, uint8 weight units,
+    endpoint range check -- in one multi-threaded native pass (nc_edges_narrow, the GIL
+    released), so the copy engine moves 9 instead of 24 bytes per edge and the device does
+    no conversion; the pass over chunk k overlaps the copy of chunk k - 1."""
+    import torch
+    n = int(ci.size)
+    L = _native.lib()
+    c = min(chunk, n)
+    k_buf = min(depth, (n + c - 1) // c)
+    host = [torch.empty(9 * c, dtype=torch.uint8, pin_memory=True) for _ in range(k_buf)]
+    done = [None] * k_buf
+    side = torch.cuda.Stream(dev)
+    side.wait_stream(torch.cuda.current_stream(dev))
+    for idx, a in enumerate(range(0, n, c)):
+        b = min(n, a + c)
+        k, w = idx % k_buf, b - a
+        if done[k] is not None:
+            done[k].synchronize()
+        h = host[k]
+        hi, hj, hq = h[: 4 * c].view(torch.int32), h[4 * c: 8 * c].view(torch.int32), h[8 * c:]
+        _native.check(L.nc_edges_narrow(ci.ctypes.data + 8 * a, cj.ctypes.data + 8 * a, cp.ctypes.data + 8 * a, w, m,
+                                        hi.data_ptr(), hj.data_ptr(), hq.data_ptr(), 0), "edge upload")
+        with torch.cuda.stream(side):
+            ei[a:b].copy_(hi[:w], non_blocking=True)
+            ej[a:b].copy_(hj[:w], non_blocking=True)
+            qd[a:b].copy_(hq[:w], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(side)
+            done[k] = ev
+    torch.cuda.current_stream(dev).wait_stream(side)
+    for t in (ei, ej, qd):
+        t.record_stream(side)
     return ei, ej, qd[:n]
 
 
