@@ -415,6 +415,8 @@ int nc_stamp(unsigned long long* dst, const int32_t* step, int32_t max_steps, vo
  * CSR and acc on the shard; X may be NULL for a single GPU.  gbar: one uint32
  * of scratch (zeroed by the call).  stamp_ready/stamp_done (nullable) receive
  * %globaltimer per step (index = step < stamp_cap) around the exchange. */
+/* Largest shard (rows) nc_run_persistent accepts on the current device (0 on error). */
+int64_t nc_persistent_max_rows(void);
 int nc_run_persistent(const nc_shard_t* sh, const nc_lif_params_t* p, const nc_xchg_t* X, int32_t n_steps,
                       int32_t blocks_per_peer, unsigned int* gbar, unsigned long long* stamp_ready,
                       unsigned long long* stamp_done, int32_t stamp_cap, void* stream);

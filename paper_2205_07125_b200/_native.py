@@ -109,6 +109,7 @@ _SIGS = {
                                                c_int32, c_int32, c_void_p, c_void_p]),
     "nc_edges_narrow": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
                                   c_int32]),
+    "nc_persistent_max_rows": (c_int64, []),
     "nc_assignment_u8": (c_int32, [c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_void_p, c_void_p]),
     "nc_traffic_histogram32": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int32,
                                        c_int32, c_int32, c_void_p, c_void_p]),

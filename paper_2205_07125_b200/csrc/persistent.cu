@@ -115,6 +115,17 @@ extern "C" int nc_persistent_phase_stamps(unsigned long long* dst) {
   return NC_OK;
 }
 
+// Largest shard (rows) the persistent engine takes on this device: its LIF phase keeps a
+// spike mask per 32-row tile of each CTA's range in shared memory.
+extern "C" int64_t nc_persistent_max_rows(void) {
+  int dev = 0, sms = 0, occ = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_persistent, kPThreads, 0) != cudaSuccess || occ < 1)
+    return 0;
+  const int64_t grid = (int64_t)sms * (occ < 8 ? occ : 8);
+  return grid * ncdev::kLifMaxTiles * 32;
+}
+
 extern "C" int nc_run_persistent(const nc_shard_t* sh, const nc_lif_params_t* p, const nc_xchg_t* X,
                                  int32_t n_steps, int32_t blocks_per_peer, unsigned int* gbar,
                                  unsigned long long* stamp_ready, unsigned long long* stamp_done, int32_t stamp_cap,

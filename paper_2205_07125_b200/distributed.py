@@ -116,7 +116,9 @@ def choose_delivery(net: Network, lif: LifParams, seed: int, rt: RoutingTable | 
     names = ["fused", "persistent"]
     if candidates is None:
         mine = delivery_candidates(net)
-        ok = torch.tensor([int(n in mine or (n == "persistent" and "push" in mine)) for n in names],
+        rows = max(net.layout.n_local(h) for h in net.shards)
+        fits = rows <= int(_native.lib().nc_persistent_max_rows())   # the persistent engine's LIF masks
+        ok = torch.tensor([int(n in mine or (n == "persistent" and "push" in mine and fits)) for n in names],
                           dtype=torch.int32, device=net.device)
         grp.all_reduce(ok, "min")
         candidates = [n for n, f in zip(names, ok.tolist()) if f]

@@ -1279,7 +1279,9 @@ def delivery_candidates(net: Network) -> list:
     cached = all(getattr(c, "_push_arrays", None) for c in net.shards.values())
     free = torch.cuda.mem_get_info(net.device)[0]
     if cached or 4.4 * net.n_synapses + 2e9 < free:
-        out.append("persistent" if net.layout.n_shards == 1 else "push")
+        rows = max(net.layout.n_local(h) for h in net.shards)
+        one = net.layout.n_shards == 1
+        out.append("persistent" if one and rows <= int(_native.lib().nc_persistent_max_rows()) else "push")
     return out
 
 
