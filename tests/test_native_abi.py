@@ -92,3 +92,32 @@ def test_torch_extension_registers_the_step_ops():
         o.sim_end_step(shard, 0)
     with pytest.raises(RuntimeError, match="bytes"):
         o.sim_end_step(torch.zeros(3, dtype=torch.uint8), 0)
+
+
+def test_edges_narrow_host_pass():
+    """nc_edges_narrow (the host half of sim.upload_edges, CPU only): int64 ids -> int32,
+    fp64 p -> q_from_p's uint8 weight units, every thread split; out-of-range ids -> NC_E_ARG."""
+    import numpy as np
+    from paper_2205_07125_b200 import _native, sim as S
+    L = _native.lib()
+    rng = np.random.default_rng(5)
+    for n, threads in ((1, 0), (70_001, 3), (300_000, 0)):
+        m = 9_000
+        ei = rng.integers(0, m, n).astype(np.int64)
+        ej = rng.integers(0, m, n).astype(np.int64)
+        p = rng.uniform(0.0, 1.0, n)
+        p[: min(n, 6)] = [1e-300, 1 / 32, 0.5, 1.0, 31 / 32, 1 - 1e-16][: min(n, 6)]
+        oi, oj, oq = np.empty(n, np.int32), np.empty(n, np.int32), np.empty(n, np.uint8)
+        rc = L.nc_edges_narrow(ei.ctypes.data, ej.ctypes.data, p.ctypes.data, n, m, oi.ctypes.data, oj.ctypes.data,
+                               oq.ctypes.data, threads)
+        assert rc == 0
+        np.testing.assert_array_equal(oi, ei)
+        np.testing.assert_array_equal(oj, ej)
+        np.testing.assert_array_equal(oq, S.q_from_p(p))
+        ej[n // 2] = m
+        assert L.nc_edges_narrow(ei.ctypes.data, ej.ctypes.data, p.ctypes.data, n, m, oi.ctypes.data,
+                                 oj.ctypes.data, oq.ctypes.data, threads) != 0
+        ej[n // 2] = 0
+        ei[n - 1] = -1
+        assert L.nc_edges_narrow(ei.ctypes.data, ej.ctypes.data, p.ctypes.data, n, m, oi.ctypes.data,
+                                 oj.ctypes.data, oq.ctypes.data, threads) != 0
