@@ -52,6 +52,7 @@ def main():
             hop0 = sim.hop_ids.clone()
             dist.barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            dist.all_reduce(torch.zeros(1, device=dev))   # device-aligned start (bench.align_start)
             e0.record()
             sim.advance(args.steps)
             e1.record()
