@@ -235,8 +235,8 @@ def time_steps(sim, args, world, dev, clocks=None):
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     ctx = clocks if clocks is not None else _Null()
-    align_start(world, dev)
-    with ctx:
+    with ctx:   # the sampler starts (nvmlInit: ms, varying per host) before the aligned start
+        align_start(world, dev)
         e0.record()
         sim.advance(args.steps)
         e1.record()
